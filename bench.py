@@ -1,0 +1,330 @@
+#!/usr/bin/env python
+"""bench.py -- the Feasible Triplet hot path on B200 (BASELINE.json config 4 by default).
+
+A "step" is one whole run of the workload through the C-ABI: lcsb_reset (W_0 = 0) +
+lcsb_sweep(S) + lcsb_bound.  metric = logical state-updates per second (sigma^(d l) x S per step).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--workload config4] [--impl ours|reference]
+
+Prints ONE JSON line on rank 0.  Under torchrun (N > 1) every rank runs its own replica of the
+workload (the sharded l = 18 path is not built yet), timed as the max over
+ranks.  `--impl reference` times the CPU oracle (oracle/, the reference arm of this tier) on a
+bounded sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+WORKLOADS = {
+    # name: (sigma, d, ell, dtype, form, sweeps, bound resource)
+    "config1": dict(sigma=2, d=2, ell=8, dtype="f64", form="two_array", sweeps=500),
+    "config2": dict(sigma=3, d=3, ell=4, dtype="f64", form="ks", sweeps=300),
+    "config3": dict(sigma=4, d=2, ell=8, dtype="f32", form="ks", sweeps=100),
+    "config4": dict(sigma=2, d=2, ell=17, dtype="f32", form="two_array", sweeps=50),
+}
+METRIC = "state-updates/sec per sweep (1/2/4/8 B200) and % of HBM roofline"
+SAMPLE_SEED = 0x240710925
+
+
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled every 200 ms during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "200", "-i", str(self.index)],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.thread.join(timeout=2)
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in self.lines:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[2:6]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def _dist():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def algorithmic_bytes_per_sweep(w: dict, stored: int) -> int:
+    """Compulsory bytes of one sweep: every input generation read once and the
+    new table written once.  two-array: 2 tables; KS: (d + 1) tables."""
+    esize = 4 if w["dtype"] == "f32" else 8
+    tables = 2 if w["form"] == "two_array" else w["d"] + 1
+    return tables * stored * esize
+
+
+def run_ours(args, w, ws, rank, local):
+    import torch
+    from paper_2407_10925_b200 import Lcsb
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    stream = torch.cuda.current_stream(dev)
+    h = Lcsb(w["sigma"], w["d"], w["ell"], dtype=w["dtype"], form=w["form"])
+    S = w["sweeps"]
+    n_logical = h.num_states
+    stored = h.stored_states
+    kernel_name = h.kernel_in_use
+
+    def step(ev=None):
+        h.reset()
+        if ev is not None:
+            ev[0].record(stream)
+        h.sweep(S)
+        if ev is not None:
+            ev[1].record(stream)
+        return h.bound()
+
+    for _ in range(args.warmup):
+        b = step()
+    if ws > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    sweep_evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+                 for _ in range(args.steps)]
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    clocks = ClockSampler(local)
+    clocks.start()
+    launches0 = h.launch_count
+    t0.record(stream)
+    for i in range(args.steps):
+        b = step(sweep_evs[i])
+    t1.record(stream)
+    torch.cuda.synchronize()
+    launches = h.launch_count - launches0
+    clk = clocks.stop()
+    if ws > 1:
+        torch.distributed.barrier()
+    ms_total = t0.elapsed_time(t1)
+    sweep_ms = [s.elapsed_time(e) for s, e in sweep_evs]
+    if ws > 1:
+        t = torch.tensor([ms_total], device=dev, dtype=torch.float64)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        ms_total = float(t.item())
+    ms_per_step = ms_total / args.steps
+    value = ws * n_logical * S / (ms_per_step / 1e3)
+    # dominant kernel: the sweep; one launch per sweep on `stream`
+    launch_ms = statistics.mean(sweep_ms) / S
+    alg_bytes = algorithmic_bytes_per_sweep(w, stored)
+    peak, peak_kind = _peaks()
+    achieved = alg_bytes / (launch_ms / 1e3) / 1e9
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", f"traffic_{args.workload}.json")
+    if os.path.exists(tpath):
+        try:
+            with open(tpath) as f:
+                traffic = json.load(f).get("dram_bytes_per_launch")
+        except Exception:
+            traffic = None
+
+    # ---- end-to-end through the public API with host buffers (create .. gather to host)
+    import numpy as np
+    from seeded_inputs import splitmix64_indices  # the seeded index generator (no method math)
+    idx = splitmix64_indices(SAMPLE_SEED, 1 << 20, n_logical)
+    idx_pinned = torch.from_numpy(idx.view(np.int64)).pin_memory()
+    out_pinned = torch.empty(1 << 20, dtype=torch.float64).pin_memory()
+    h.destroy()
+    torch.cuda.synchronize()
+    e2e_times = []
+    for rep in range(2):
+        torch.cuda.synchronize()
+        te = time.perf_counter()
+        h2 = Lcsb(w["sigma"], w["d"], w["ell"], dtype=w["dtype"], form=w["form"])
+        h2.sweep(S)
+        be = h2.bound()
+        h2.table_gather(idx_pinned.numpy().view(np.uint64), out=out_pinned.numpy())
+        h2.destroy()
+        torch.cuda.synchronize()
+        e2e_times.append(time.perf_counter() - te)
+    e2e_s = min(e2e_times[1:] or e2e_times)
+    e2e_value = ws * n_logical * S / e2e_s
+
+    res = {
+        "metric": METRIC,
+        "value": value,
+        "unit": "state-updates/s",
+        "n_gpus": ws,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": ms_per_step,
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "f64" if w["dtype"] == "f64" else "f32-storage/f64-arith",
+        "data": "synthetic (the method's only input is (sigma, d, l) and W_0 = 0)",
+        "config": {
+            "workload": f"{args.workload}: sigma={w['sigma']}, d={w['d']}, l={w['ell']}, "
+                        f"{w['form']} form, {w['dtype']} storage, {S} sweeps + 1 bound per step",
+            "states": n_logical, "stored_states": stored, "sweeps_per_step": S,
+            "kernel": kernel_name,
+            "parallelism": "replicas" if ws > 1 else "single-gpu",
+            "l2_flush": "inputs larger than L2 (each table %.1f GiB vs 126 MB L2)"
+                        % (stored * (4 if w["dtype"] == "f32" else 8) / 2**30)
+            if stored * 4 > 2**27 else "working set L2-resident (latency-bound config)",
+            "sweep_ms_per_launch": launch_ms,
+            "bound": b.bound, "bound_at_Rmin": b.bound_at_Rmin,
+            "sweeps_per_s": S / (ms_per_step / 1e3),
+            "sweep_only_state_updates_per_s": ws * n_logical / (launch_ms / 1e3),
+        },
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": traffic,
+                     "peak_kind": peak_kind,
+                     "algorithmic_bytes_per_launch": alg_bytes,
+                     "kernel": kernel_name + " sweep kernel"},
+        "e2e": {"value": e2e_value, "unit": "state-updates/s",
+                "h2d_bytes_per_step": int(idx.nbytes),
+                "d2h_bytes_per_step": int(out_pinned.numel() * 8 + 32),
+                "what": "lcsb_create + lcsb_sweep(S) + lcsb_bound + lcsb_table_gather of 2^20 "
+                        "seeded states to pinned host memory, wall clock",
+                "bound": be.bound},
+        "gpu_launches": int(launches),
+        "clocks": clk,
+    }
+    return res
+
+
+def cpu_baseline(w, budget_s=15.0):
+    """The oracle as it stands, timed on this host, on a bounded sample of the same workload:
+    one sweep of F (oracle/ft_oracle.c fo_apply_F_at, all OpenMP threads) over a contiguous
+    slice of the workload's logical states (the paper's thread-slice unit),
+    reading a full-size logical input table (np.zeros: W_0, sweep 1 of the run)."""
+    import numpy as np
+    from oracle import ft_oracle as fo
+    n = fo.n_states(w["sigma"], w["d"], w["ell"])
+    try:
+        src = np.zeros(n, dtype=np.float64)
+        table_note = "full-size fp64 logical input table"
+    except MemoryError:
+        return None
+    d = w["d"]
+    count = 1 << 16
+    cores = fo.num_threads()
+    x0 = n // 3
+    spent, done = 0.0, 0
+    # calibrate, then run ~budget_s of work
+    while spent < budget_s:
+        idx = np.arange(x0 + done, x0 + done + count, dtype=np.uint64) % np.uint64(n)
+        t = time.perf_counter()
+        _parallel_apply_at(fo, w, [src] * d, idx, cores)
+        dt = time.perf_counter() - t
+        spent += dt
+        done += count
+        if dt < budget_s / 20:
+            count *= 2
+    return {"value": done / spent, "unit": "state-updates/s", "cores": cores, "kind": "oracle",
+            "sample": f"{done} consecutive logical states of one sweep of {w['sigma']},{w['d']},"
+                      f"{w['ell']} ({table_note}), {spent:.1f} s"}
+
+
+def _parallel_apply_at(fo, w, src, idx, cores):
+    from concurrent.futures import ThreadPoolExecutor
+    parts = [idx[i::cores] for i in range(cores)]
+    with ThreadPoolExecutor(cores) as ex:  # ctypes releases the GIL during the C call
+        list(ex.map(lambda p: fo.apply_F_at(w["sigma"], w["d"], w["ell"], src, p), parts))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--workload", default="config4", choices=sorted(WORKLOADS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3  # timing rule: at least 3 warm-up steps
+    ws, rank, local = _dist()
+    w = WORKLOADS[args.workload]
+
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        base = cpu_baseline(w, budget_s=max(5.0, 3.0 * args.steps))
+        res = {"impl": "reference", "metric": METRIC, "value": base["value"],
+               "unit": "state-updates/s", "n_gpus": ws, "steps": args.steps,
+               "warmup": args.warmup, "higher_is_better": True, "scaling": "weak",
+               "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+               "config": {"workload": args.workload},
+               "cpu_baseline": base,
+               "e2e": {"value": base["value"], "unit": "state-updates/s",
+                       "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+        print(json.dumps(res), flush=True)
+        return
+
+    import torch
+    if ws > 1:
+        torch.distributed.init_process_group("nccl", device_id=torch.device("cuda", local))
+    res = run_ours(args, w, ws, rank, local)
+    if rank == 0:
+        if not args.no_cpu_baseline and ws == 1:
+            res["cpu_baseline"] = cpu_baseline(w)
+        print(json.dumps(res), flush=True)
+    if ws > 1:
+        torch.distributed.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

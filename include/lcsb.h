@@ -1,0 +1,156 @@
+/*
+ * lcsb.h -- C-ABI of the B200 Feasible Triplet library (liblcsb.so).
+ *
+ * The library computes the value-iteration sweep of the Feasible Triplet recurrence of
+ * arXiv 2407.10925 (Kiwi-Soto's F; Alg. 1; Alg. 2
+ * PAPER.md:696-717; binary Alg. 5 PAPER.md:728-750 with F_0/F_1 of PAPER.md:752-779) and the
+ * bound reduction that turns the swept table into a certified lower bound on the
+ * Chvatal-Sankoff constant gamma_{sigma,d} (Lemma 1).
+ *
+ * A "state" is a d-tuple of length-l strings over {0..sigma-1}; a table holds one real per
+ * state, sigma^(d l) of them.  Logical state order (reading R14):
+ *     idx = sum_{k<l} sum_{j<d} A_j[k] * sigma^(d(l-1-k) + (d-1-j))
+ * i.e. the heads are the most significant digit group and string 0 is the most significant
+ * digit of each group.  For sigma = d = 2 this is the paper's interleaved pair
+ * (a = 1011, b = 0010 -> 142).
+ *
+ * Every pointer argument is a HOST pointer unless stated otherwise; the library owns all of
+ * its device memory.  Functions return LCSB_OK (0) or an error code and never abort; the
+ * message of the last failure is available from lcsb_last_error().  A handle is not
+ * thread-safe; distinct handles are independent.
+ */
+#ifndef LCSB_H
+#define LCSB_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct lcsb lcsb_t; /* opaque; owns every device table and scratch buffer */
+
+/* STORAGE dtype of the tables.  Arithmetic is always fp64 (BASELINE.json: "fp32 storage with
+ * fp64 accumulation"); LCSB_F32 rounds every stored value to nearest-even fp32. */
+enum { LCSB_F64 = 0, LCSB_F32 = 1 };
+
+/* Recurrence form.
+ *   KS:        Alg. 2 / Alg. 5 -- an option that advances k strings reads the table k sweeps
+ *              back (reading R1); d+1 tables live.
+ *   TWO_ARRAY: Lueker's two-array form for sigma = d = 2 ("storing only two arrays",
+ *              PAPER.md:400): every option reads the previous sweep; 2 tables live; the bound
+ *              is 2 rho / (1 + rho) with rho = R - E (reading R10).
+ *   AUTO:      TWO_ARRAY for sigma = d = 2, KS otherwise. */
+enum { LCSB_FORM_AUTO = 0, LCSB_FORM_KS = 1, LCSB_FORM_TWO_ARRAY = 2 };
+
+/* Which R the headline bound uses (reading R5).  Both are always computed:
+ *   R_MAX = max(v_new - v_prev) (Alg. 2 line 5), R_MIN = min(...). */
+enum { LCSB_R_MAX = 0, LCSB_R_MIN = 1 };
+
+/* Kernel selection: AUTO picks the specialised kernel for the shape; GENERIC forces the
+ * full-table one-thread-per-state kernel (used as a cross-check). */
+enum { LCSB_KERNEL_AUTO = 0, LCSB_KERNEL_GENERIC = 1 };
+
+/* Status codes. */
+enum {
+  LCSB_OK = 0,
+  LCSB_EINVAL = 1,    /* bad argument or unsupported combination */
+  LCSB_ECAPACITY = 2, /* not enough device memory; lcsb_last_error() states the bytes needed */
+  LCSB_ESTATE = 3,    /* call not valid in the handle's state (e.g. bound before any sweep) */
+  LCSB_ECUDA = 4,     /* a CUDA runtime call failed */
+  LCSB_ENCCL = 5      /* reserved for the sharded path */
+};
+
+/* Device allocation hooks (optional).  alloc returns a device pointer of >= bytes, 256-B
+ * aligned, usable on `stream`, or NULL; free_ releases it.  NULL hooks -> cudaMallocAsync /
+ * cudaFreeAsync on the handle's stream.  The Python binding passes the PyTorch caching
+ * allocator here. */
+typedef void* (*lcsb_alloc_fn)(size_t bytes, void* stream, void* ctx);
+typedef void (*lcsb_free_fn)(void* ptr, size_t bytes, void* stream, void* ctx);
+
+typedef struct {
+  int32_t sigma;    /* alphabet size, >= 2 */
+  int32_t d;        /* number of strings, 2..16 */
+  int32_t ell;      /* string-length parameter l >= 1; sigma^(d l) must be < 2^62 */
+  int32_t dtype;    /* LCSB_F64 / LCSB_F32 */
+  int32_t form;     /* LCSB_FORM_* */
+  int32_t rmode;    /* LCSB_R_* : which R gives lcsb_bound_t.bound / best_bound */
+  int32_t symmetry; /* -1 auto; 0 full logical table; 1 complement-folded half table
+                       (two-array binary only, l >= 2).  AUTO = 1 when
+                       allowed, else 0. */
+  int32_t kernel;   /* LCSB_KERNEL_* */
+  void* stream;     /* cudaStream_t every kernel and copy is enqueued on; NULL = legacy default */
+  lcsb_alloc_fn alloc;
+  lcsb_free_fn free_;
+  void* alloc_ctx;
+} lcsb_config;
+
+/* Fill *cfg with defaults: sigma=2,d=2,ell=1, F32, AUTO form, R_MAX, symmetry auto, AUTO
+ * kernel, NULL stream and hooks. */
+void lcsb_config_init(lcsb_config* cfg);
+
+/* Device bytes a handle with this config would own (tables + scratch).  0 on bad config. */
+uint64_t lcsb_required_bytes(const lcsb_config* cfg);
+
+/* Create a handle and zero every live table: W_0 = 0, the (d+1) x sigma^(d l) zero matrix of
+ * Alg. 2 line 2 / v_0 = v_1 = 0 of Alg. 5.
+ * Errors: EINVAL (bad parameters), ECAPACITY (device memory), ECUDA. */
+int lcsb_create(int32_t sigma, int32_t d, int32_t ell, int32_t dtype, lcsb_t** out);
+int lcsb_create_ex(const lcsb_config* cfg, lcsb_t** out);
+
+/* Restart the run without reallocating: zero every live table again (W_0 = 0), reset the sweep
+ * count and the best-so-far triplet.  Asynchronous.  Errors: ECUDA. */
+int lcsb_reset(lcsb_t* h);
+
+/* Enqueue n >= 0 sweeps on the handle's stream and return (asynchronous).  One sweep computes
+ * v_new = F(v_{n-1}, ..., v_{n-d}) at every state (Eq. ineq3) and rotates the
+ * generations (Alg. 2 line 11).  Errors: EINVAL (n < 0), ECUDA (launch failure). */
+int lcsb_sweep(lcsb_t* h, int64_t n);
+
+typedef struct {
+  double R_max, R_min;         /* max / min over states of v_new - v_prev */
+  double E_at_Rmax, E_at_Rmin; /* E = max(0, max W) for each R (Alg. 2 lines 6-7) */
+  double bound_at_Rmax, bound_at_Rmin; /* KS: d (R - E); two-array: 2 rho/(1+rho), rho = R-E */
+  double bound;                /* bound_at_R<rmode> */
+  double best_bound;           /* best over every lcsb_bound call so far for rmode, starting
+                                  from the triplet (v_0, 0, 0) (Alg. 2 lines 2, 8-10) */
+  int64_t sweeps_done;         /* sweeps performed by this handle */
+  int64_t best_sweep;          /* sweeps_done at the best evaluation (0 = initial triplet) */
+} lcsb_bound_t;
+
+/* Evaluate the bound at the current iterate (Alg. 2 lines 5-10) for both R readings.
+ * Synchronises the handle's stream; the only host round-trip of the path.
+ * Errors: ESTATE (no sweep yet), ECUDA. */
+int lcsb_bound(lcsb_t* h, lcsb_bound_t* out);
+
+/* Copy count table entries, logical indices [first, first+count), of generation `which`
+ * (0 = newest, 1 = one sweep back, ... up to d-1 for KS / 1 for two-array) into host_dst,
+ * unfolded (complement symmetry applied) and widened to fp64.  Synchronous.
+ * Errors: EINVAL (range / which), ECUDA. */
+int lcsb_table(lcsb_t* h, int32_t which, uint64_t first, uint64_t count, double* host_dst);
+
+/* Same for n arbitrary logical indices host_idx[0..n) -> host_dst[0..n).  Synchronous. */
+int lcsb_table_gather(lcsb_t* h, int32_t which, const uint64_t* host_idx, uint64_t n,
+                      double* host_dst);
+
+int64_t lcsb_sweeps_done(const lcsb_t* h);
+uint64_t lcsb_num_states(const lcsb_t* h);   /* logical states sigma^(d l) */
+uint64_t lcsb_stored_states(const lcsb_t* h);/* entries per stored table */
+uint64_t lcsb_device_bytes(const lcsb_t* h); /* device bytes owned */
+int32_t lcsb_kernel_in_use(const lcsb_t* h); /* 1 generic, 2 binary half-table paired */
+
+/* Launches of the library's own kernels enqueued by this handle so far (for bench accounting). */
+int64_t lcsb_launch_count(const lcsb_t* h);
+
+/* Message of the last failure on this handle (h != NULL) or of the last failed create on
+ * this thread (h == NULL).  Never NULL. */
+const char* lcsb_last_error(const lcsb_t* h);
+
+/* Free every device buffer (through free_ when hooks were given).  Safe on NULL. */
+void lcsb_destroy(lcsb_t* h);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* LCSB_H */

@@ -1,0 +1,132 @@
+// kern_reduce.cu -- bound reductions and table read-out.
+//
+//  rdiff:  R_max = max_j (v_new - v_prev)[j], R_min = min_j (...)   (Alg. 2 line 5, Alg. 5 line 7;
+//          PAPER.md:705, 738; R_min per PAPER.md:694).  Over stored entries: with the
+//          complement-folded table every logical entry equals a stored one, so the max/min are
+//          the logical ones.  Differences are exact in fp64 for fp32 storage.
+//          Grid-stride, 16-byte vector loads, warp shuffle + block reduction, one atomic per
+//          block on order-preserving integer encodings (max/min are exact and order-free, so the
+//          result is independent of the launch geometry).
+//  expand: logical-order read-out, unfolding the complement symmetry and
+//          widening to fp64.
+#include <math.h>
+
+#include "lcsb_internal.cuh"
+
+namespace lcsbk {
+namespace {
+
+__global__ void red_init_kernel(unsigned long long* red) {
+  int i = threadIdx.x;
+  if (i < kRedSlots) {
+    // slot 1 is a min (R_min): start at +inf; the others are maxima: start at -inf
+    red[i] = (i == 1) ? ord_enc(INFINITY) : ord_enc(-INFINITY);
+  }
+}
+
+__device__ __forceinline__ void acc(double dd, double& mx, double& mn) {
+  mx = fmax(mx, dd);
+  mn = fmin(mn, dd);
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256) rdiff_kernel(const T* __restrict__ a, const T* __restrict__ b,
+                                                    uint64_t n, unsigned long long* red) {
+  double mx = -INFINITY, mn = INFINITY;
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  const uint64_t t0 = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (sizeof(T) == 4) {
+    const uint64_t nv = n / 4;
+    const float4* a4 = reinterpret_cast<const float4*>(a);
+    const float4* b4 = reinterpret_cast<const float4*>(b);
+    for (uint64_t i = t0; i < nv; i += stride) {
+      float4 x = __ldcs(a4 + i), y = __ldcs(b4 + i);
+      acc((double)x.x - (double)y.x, mx, mn);
+      acc((double)x.y - (double)y.y, mx, mn);
+      acc((double)x.z - (double)y.z, mx, mn);
+      acc((double)x.w - (double)y.w, mx, mn);
+    }
+    for (uint64_t i = nv * 4 + t0; i < n; i += stride) acc((double)a[i] - (double)b[i], mx, mn);
+  } else {
+    const uint64_t nv = n / 2;
+    const double2* a2 = reinterpret_cast<const double2*>(a);
+    const double2* b2 = reinterpret_cast<const double2*>(b);
+    for (uint64_t i = t0; i < nv; i += stride) {
+      double2 x = __ldcs(a2 + i), y = __ldcs(b2 + i);
+      acc((double)x.x - (double)y.x, mx, mn);
+      acc((double)x.y - (double)y.y, mx, mn);
+    }
+    for (uint64_t i = nv * 2 + t0; i < n; i += stride) acc((double)a[i] - (double)b[i], mx, mn);
+  }
+  __shared__ double smx[8], smn[8];
+  for (int o = 16; o > 0; o >>= 1) {
+    mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    mn = fmin(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+  }
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  if (lane == 0) {
+    smx[wid] = mx;
+    smn[wid] = mn;
+  }
+  __syncthreads();
+  if (wid == 0) {
+    const int nw = blockDim.x >> 5;
+    mx = lane < nw ? smx[lane] : -INFINITY;
+    mn = lane < nw ? smn[lane] : INFINITY;
+    for (int o = 16; o > 0; o >>= 1) {
+      mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+      mn = fmin(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+    }
+    if (lane == 0) {
+      atomicMax(red + 0, ord_enc(mx));
+      atomicMin(red + 1, ord_enc(mn));
+    }
+  }
+}
+
+template <typename T>
+__global__ void expand_kernel(const T* __restrict__ tab, int symmetric, int ell, uint64_t first,
+                              uint64_t count, const uint64_t* __restrict__ idx, double* out) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  const uint64_t half = symmetric ? (1ull << (2 * ell - 1)) : 0;
+  const uint64_t top = symmetric ? ((1ull << (2 * ell)) - 1) : 0;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count; i += stride) {
+    uint64_t y = idx ? idx[i] : first + i;
+    if (symmetric && y >= half) y = top - y;  // Eq. (comp_eq)
+    out[i] = (double)tab[y];
+  }
+}
+
+}  // namespace
+
+cudaError_t launch_red_init(unsigned long long* red, cudaStream_t s) {
+  red_init_kernel<<<1, 32, 0, s>>>(red);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_rdiff(const void* newest, const void* prev, uint64_t n, int dtype,
+                         unsigned long long* red, cudaStream_t s, int sms) {
+  uint64_t per = (dtype == LCSB_F32) ? 4 : 2;
+  uint64_t blocks = (n / per + 255) / 256;
+  if (blocks > (uint64_t)sms * 8) blocks = (uint64_t)sms * 8;
+  if (blocks < 1) blocks = 1;
+  if (dtype == LCSB_F32)
+    rdiff_kernel<float><<<(unsigned)blocks, 256, 0, s>>>((const float*)newest, (const float*)prev, n, red);
+  else
+    rdiff_kernel<double><<<(unsigned)blocks, 256, 0, s>>>((const double*)newest, (const double*)prev, n, red);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_expand(const void* tab, int dtype, int symmetric, int ell, uint64_t first,
+                          uint64_t count, const uint64_t* idx, double* out, cudaStream_t s) {
+  uint64_t blocks = (count + 255) / 256;
+  if (blocks > 4096) blocks = 4096;
+  if (blocks < 1) blocks = 1;
+  if (dtype == LCSB_F32)
+    expand_kernel<float><<<(unsigned)blocks, 256, 0, s>>>((const float*)tab, symmetric, ell, first, count, idx, out);
+  else
+    expand_kernel<double><<<(unsigned)blocks, 256, 0, s>>>((const double*)tab, symmetric, ell, first, count, idx, out);
+  return cudaGetLastError();
+}
+
+}  // namespace lcsbk

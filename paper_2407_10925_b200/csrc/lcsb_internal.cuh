@@ -1,0 +1,68 @@
+// lcsb_internal.cuh -- shared declarations of the B200 Feasible Triplet library.
+// Product code: never includes or links anything under oracle/.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <string.h>
+
+#include "lcsb.h"
+
+namespace lcsbk {
+
+constexpr int kMaxD = 16;
+constexpr int kMaxGen = kMaxD + 1;
+
+// ordered encoding of doubles into uint64 so that unsigned integer max/min == fp max/min
+__host__ __device__ inline unsigned long long ord_enc(double x) {
+#ifdef __CUDA_ARCH__
+  long long b = __double_as_longlong(x);
+#else
+  long long b;
+  memcpy(&b, &x, sizeof b);
+#endif
+  return b < 0 ? ~(unsigned long long)b : ((unsigned long long)b | 0x8000000000000000ull);
+}
+
+inline double ord_dec(unsigned long long u) {
+  unsigned long long b = (u & 0x8000000000000000ull) ? (u & 0x7fffffffffffffffull) : ~u;
+  double x;
+  memcpy(&x, &b, sizeof x);
+  return x;
+}
+
+// Reduction slots (device, unsigned long long each):
+//   0: R_max  1: R_min  2: max W at R_max  3: max W at R_min
+constexpr int kRedSlots = 4;
+
+struct GenericArgs {
+  int sigma, d, ell;
+  uint64_t n;                       // logical states
+  const void* src[kMaxD];           // src[k-1]: table read when |N| = k
+  void* dst;                        // output table (sweep mode)
+  const void* center;               // W mode: the table v in W = (v + dR) - F(...)
+  int form;                         // LCSB_FORM_KS / LCSB_FORM_TWO_ARRAY
+  const unsigned long long* red_in; // W mode: encoded R_max, R_min
+  unsigned long long* red_out;      // W mode: encoded max W slots
+};
+
+struct Bin2Args {
+  const void* src;  // stored half table (2^(2l-1) entries)
+  void* dst;        // output half table (sweep mode)
+  int ell;
+  int m;            // tile = 4^m Q1 outputs
+  const unsigned long long* red_in;
+  unsigned long long* red_out;
+};
+
+// launchers (return cudaError_t of the launch)
+cudaError_t launch_generic_sweep(const GenericArgs& a, int dtype, cudaStream_t s, int sms);
+cudaError_t launch_generic_wpass(const GenericArgs& a, int dtype, cudaStream_t s, int sms);
+cudaError_t launch_bin2_sweep(const Bin2Args& a, int dtype, cudaStream_t s, int sms);
+cudaError_t launch_bin2_wpass(const Bin2Args& a, int dtype, cudaStream_t s, int sms);
+cudaError_t launch_red_init(unsigned long long* red, cudaStream_t s);
+cudaError_t launch_rdiff(const void* newest, const void* prev, uint64_t n, int dtype,
+                         unsigned long long* red, cudaStream_t s, int sms);
+cudaError_t launch_expand(const void* tab, int dtype, int symmetric, int ell, uint64_t first,
+                          uint64_t count, const uint64_t* idx, double* out, cudaStream_t s);
+
+}  // namespace lcsbk

@@ -1,0 +1,293 @@
+"""Thin ctypes binding of liblcsb.so (include/lcsb.h).  Argument marshalling only: every step of
+the sweep and the bound runs in the library's CUDA kernels.  PyTorch provides the device, the
+stream and (through the allocation hooks) the caching allocator.
+
+There is no fallback: if liblcsb.so is missing or no CUDA device is present, every call raises.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass
+
+import numpy as np
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+SO_PATH = os.path.join(_PKG, "liblcsb.so")
+
+LCSB_F64, LCSB_F32 = 0, 1
+LCSB_FORM_AUTO, LCSB_FORM_KS, LCSB_FORM_TWO_ARRAY = 0, 1, 2
+LCSB_R_MAX, LCSB_R_MIN = 0, 1
+LCSB_KERNEL_AUTO, LCSB_KERNEL_GENERIC = 0, 1
+STATUS = {0: "LCSB_OK", 1: "LCSB_EINVAL", 2: "LCSB_ECAPACITY", 3: "LCSB_ESTATE", 4: "LCSB_ECUDA",
+          5: "LCSB_ENCCL"}
+
+_ALLOC_FN = ctypes.CFUNCTYPE(ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p, ctypes.c_void_p)
+_FREE_FN = ctypes.CFUNCTYPE(None, ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p,
+                            ctypes.c_void_p)
+
+
+class LcsbConfig(ctypes.Structure):
+    _fields_ = [("sigma", ctypes.c_int32), ("d", ctypes.c_int32), ("ell", ctypes.c_int32),
+                ("dtype", ctypes.c_int32), ("form", ctypes.c_int32), ("rmode", ctypes.c_int32),
+                ("symmetry", ctypes.c_int32), ("kernel", ctypes.c_int32),
+                ("stream", ctypes.c_void_p), ("alloc", _ALLOC_FN), ("free_", _FREE_FN),
+                ("alloc_ctx", ctypes.c_void_p)]
+
+
+class LcsbBound(ctypes.Structure):
+    _fields_ = [("R_max", ctypes.c_double), ("R_min", ctypes.c_double),
+                ("E_at_Rmax", ctypes.c_double), ("E_at_Rmin", ctypes.c_double),
+                ("bound_at_Rmax", ctypes.c_double), ("bound_at_Rmin", ctypes.c_double),
+                ("bound", ctypes.c_double), ("best_bound", ctypes.c_double),
+                ("sweeps_done", ctypes.c_int64), ("best_sweep", ctypes.c_int64)]
+
+
+# every symbol include/lcsb.h declares (checked by tests/test_abi.py)
+EXPORTS = ["lcsb_config_init", "lcsb_required_bytes", "lcsb_create", "lcsb_create_ex",
+           "lcsb_reset", "lcsb_sweep", "lcsb_bound", "lcsb_table", "lcsb_table_gather", "lcsb_sweeps_done",
+           "lcsb_num_states", "lcsb_stored_states", "lcsb_device_bytes", "lcsb_kernel_in_use",
+           "lcsb_launch_count", "lcsb_last_error", "lcsb_destroy"]
+
+_LIB = None
+
+
+class LcsbError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"{STATUS.get(code, code)}: {msg}")
+        self.code = code
+
+
+def load_library():
+    """Load liblcsb.so (raises if it was not built: run __graft_entry__.build())."""
+    global _LIB
+    if _LIB is not None:
+        return _LIB
+    if not os.path.exists(SO_PATH):
+        raise ImportError(f"{SO_PATH} is missing; build it with `python -c 'import __graft_entry__ "
+                          "as g; g.build()'` (there is no CPU fallback)")
+    lib = ctypes.CDLL(SO_PATH)
+    P = ctypes.c_void_p
+    lib.lcsb_config_init.argtypes = [ctypes.POINTER(LcsbConfig)]
+    lib.lcsb_config_init.restype = None
+    lib.lcsb_required_bytes.argtypes = [ctypes.POINTER(LcsbConfig)]
+    lib.lcsb_required_bytes.restype = ctypes.c_uint64
+    lib.lcsb_create.argtypes = [ctypes.c_int32] * 4 + [ctypes.POINTER(P)]
+    lib.lcsb_create.restype = ctypes.c_int
+    lib.lcsb_create_ex.argtypes = [ctypes.POINTER(LcsbConfig), ctypes.POINTER(P)]
+    lib.lcsb_create_ex.restype = ctypes.c_int
+    lib.lcsb_reset.argtypes = [P]
+    lib.lcsb_reset.restype = ctypes.c_int
+    lib.lcsb_sweep.argtypes = [P, ctypes.c_int64]
+    lib.lcsb_sweep.restype = ctypes.c_int
+    lib.lcsb_bound.argtypes = [P, ctypes.POINTER(LcsbBound)]
+    lib.lcsb_bound.restype = ctypes.c_int
+    lib.lcsb_table.argtypes = [P, ctypes.c_int32, ctypes.c_uint64, ctypes.c_uint64, P]
+    lib.lcsb_table.restype = ctypes.c_int
+    lib.lcsb_table_gather.argtypes = [P, ctypes.c_int32, P, ctypes.c_uint64, P]
+    lib.lcsb_table_gather.restype = ctypes.c_int
+    for name, rt in [("lcsb_sweeps_done", ctypes.c_int64), ("lcsb_num_states", ctypes.c_uint64),
+                     ("lcsb_stored_states", ctypes.c_uint64),
+                     ("lcsb_device_bytes", ctypes.c_uint64),
+                     ("lcsb_kernel_in_use", ctypes.c_int32),
+                     ("lcsb_launch_count", ctypes.c_int64)]:
+        getattr(lib, name).argtypes = [P]
+        getattr(lib, name).restype = rt
+    lib.lcsb_last_error.argtypes = [P]
+    lib.lcsb_last_error.restype = ctypes.c_char_p
+    lib.lcsb_destroy.argtypes = [P]
+    lib.lcsb_destroy.restype = None
+    _LIB = lib
+    return lib
+
+
+def _check(rc: int, h=None):
+    if rc != 0:
+        msg = load_library().lcsb_last_error(h).decode(errors="replace")
+        raise LcsbError(rc, msg)
+
+
+def _dtype_code(dtype) -> int:
+    return {"f32": LCSB_F32, "f64": LCSB_F64, LCSB_F32: LCSB_F32, LCSB_F64: LCSB_F64}[dtype]
+
+
+def _form_code(form) -> int:
+    return {"auto": 0, "ks": 1, "two_array": 2, 0: 0, 1: 1, 2: 2}[form]
+
+
+class _TorchAllocator:
+    """Routes the library's device allocations through torch's caching allocator."""
+
+    def __init__(self, device: int):
+        import torch
+        self.torch = torch
+        self.device = device
+        self.alloc_cb = _ALLOC_FN(self._alloc)
+        self.free_cb = _FREE_FN(self._free)
+
+    def _alloc(self, nbytes, stream, ctx):
+        try:
+            return self.torch.cuda.caching_allocator_alloc(int(nbytes), self.device,
+                                                           int(stream or 0))
+        except Exception:  # out of memory -> NULL -> LCSB_ECAPACITY
+            return None
+
+    def _free(self, ptr, nbytes, stream, ctx):
+        self.torch.cuda.caching_allocator_delete(int(ptr))
+
+
+def make_config(sigma, d, ell, dtype="f32", form="auto", rmode="max", symmetry=-1,
+                kernel="auto") -> LcsbConfig:
+    cfg = LcsbConfig()
+    load_library().lcsb_config_init(ctypes.byref(cfg))
+    cfg.sigma, cfg.d, cfg.ell = sigma, d, ell
+    cfg.dtype = _dtype_code(dtype)
+    cfg.form = _form_code(form)
+    cfg.rmode = {"max": LCSB_R_MAX, "min": LCSB_R_MIN}[rmode]
+    cfg.symmetry = symmetry
+    cfg.kernel = {"auto": LCSB_KERNEL_AUTO, "generic": LCSB_KERNEL_GENERIC}[kernel]
+    return cfg
+
+
+def lcsb_required_bytes(sigma, d, ell, dtype="f32", form="auto", symmetry=-1,
+                        kernel="auto") -> int:
+    cfg = make_config(sigma, d, ell, dtype, form, "max", symmetry, kernel)
+    return int(load_library().lcsb_required_bytes(ctypes.byref(cfg)))
+
+
+@dataclass
+class BoundResult:
+    R_max: float
+    R_min: float
+    E_at_Rmax: float
+    E_at_Rmin: float
+    bound_at_Rmax: float
+    bound_at_Rmin: float
+    bound: float
+    best_bound: float
+    sweeps_done: int
+    best_sweep: int
+
+
+class Lcsb:
+    """One handle: the device tables of one (sigma, d, l) run."""
+
+    def __init__(self, sigma, d, ell, dtype="f32", form="auto", rmode="max", symmetry=-1,
+                 kernel="auto", stream=None, torch_allocator=True):
+        import torch
+        if not torch.cuda.is_available():
+            raise LcsbError(4, "no CUDA device (the library has no CPU path)")
+        lib = load_library()
+        self._lib = lib
+        self.device = torch.cuda.current_device()
+        self.stream = stream if stream is not None else torch.cuda.current_stream()
+        cfg = make_config(sigma, d, ell, dtype, form, rmode, symmetry, kernel)
+        cfg.stream = ctypes.c_void_p(self.stream.cuda_stream)
+        self._alloc = _TorchAllocator(self.device) if torch_allocator else None
+        if self._alloc is not None:
+            cfg.alloc = self._alloc.alloc_cb
+            cfg.free_ = self._alloc.free_cb
+        self._cfg = cfg
+        h = ctypes.c_void_p()
+        _check(lib.lcsb_create_ex(ctypes.byref(cfg), ctypes.byref(h)))
+        self._h = h
+        self.sigma, self.d, self.ell = sigma, d, ell
+
+    # --- the C-ABI calls -------------------------------------------------------------------
+    def reset(self):
+        _check(self._lib.lcsb_reset(self._h), self._h)
+
+    def sweep(self, n: int = 1):
+        _check(self._lib.lcsb_sweep(self._h, int(n)), self._h)
+
+    def bound(self) -> BoundResult:
+        out = LcsbBound()
+        _check(self._lib.lcsb_bound(self._h, ctypes.byref(out)), self._h)
+        return BoundResult(**{f: getattr(out, f) for f, _ in LcsbBound._fields_})
+
+    def table(self, which: int = 0, first: int = 0, count: int | None = None) -> np.ndarray:
+        if count is None:
+            count = self.num_states - first
+        out = np.empty(int(count), dtype=np.float64)
+        _check(self._lib.lcsb_table(self._h, int(which), int(first), int(count),
+                                    out.ctypes.data_as(ctypes.c_void_p)), self._h)
+        return out
+
+    def table_gather(self, idx, which: int = 0, out=None) -> np.ndarray:
+        idx = np.ascontiguousarray(idx, dtype=np.uint64)
+        if out is None:
+            out = np.empty(idx.shape[0], dtype=np.float64)
+        _check(self._lib.lcsb_table_gather(self._h, int(which),
+                                           idx.ctypes.data_as(ctypes.c_void_p), idx.shape[0],
+                                           out.ctypes.data_as(ctypes.c_void_p)), self._h)
+        return out
+
+    @property
+    def sweeps_done(self) -> int:
+        return int(self._lib.lcsb_sweeps_done(self._h))
+
+    @property
+    def num_states(self) -> int:
+        return int(self._lib.lcsb_num_states(self._h))
+
+    @property
+    def stored_states(self) -> int:
+        return int(self._lib.lcsb_stored_states(self._h))
+
+    @property
+    def device_bytes(self) -> int:
+        return int(self._lib.lcsb_device_bytes(self._h))
+
+    @property
+    def kernel_in_use(self) -> str:
+        return {1: "generic", 2: "bin2"}.get(int(self._lib.lcsb_kernel_in_use(self._h)), "?")
+
+    @property
+    def launch_count(self) -> int:
+        return int(self._lib.lcsb_launch_count(self._h))
+
+    def destroy(self):
+        if getattr(self, "_h", None) is not None and self._h.value:
+            self._lib.lcsb_destroy(self._h)
+            self._h = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.destroy()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.destroy()
+
+
+# module-level names mirroring the C-ABI
+def lcsb_create(sigma, d, ell, dtype="f32", **kw) -> Lcsb:
+    return Lcsb(sigma, d, ell, dtype, **kw)
+
+
+def lcsb_reset(h: Lcsb):
+    h.reset()
+
+
+def lcsb_sweep(h: Lcsb, n: int = 1):
+    h.sweep(n)
+
+
+def lcsb_bound(h: Lcsb) -> BoundResult:
+    return h.bound()
+
+
+def lcsb_table(h: Lcsb, which=0, first=0, count=None) -> np.ndarray:
+    return h.table(which, first, count)
+
+
+def lcsb_table_gather(h: Lcsb, idx, which=0) -> np.ndarray:
+    return h.table_gather(idx, which)
+
+
+def lcsb_destroy(h: Lcsb):
+    h.destroy()

@@ -1,0 +1,65 @@
+"""CPU checks of the C-ABI boundary: the library loads, exports every symbol include/lcsb.h
+declares, and validates configurations on the host (no compute without a GPU)."""
+import ctypes
+import os
+import re
+
+import pytest
+
+from tests.conftest import ROOT, has_cuda
+
+import paper_2407_10925_b200 as pkg
+from paper_2407_10925_b200 import lcsb as L
+
+
+def _header_functions():
+    src = open(os.path.join(ROOT, "include", "lcsb.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(lcsb_[a-z_]+)\s*\(", src)))
+
+
+def test_library_exports_every_header_symbol():
+    lib = pkg.load_library()
+    declared = _header_functions()
+    assert "lcsb_create" in declared and "lcsb_sweep" in declared
+    for name in declared:
+        assert hasattr(lib, name), name
+    assert sorted(L.EXPORTS) == declared
+
+
+def test_library_is_sm100a():
+    # the product .so carries sm_100a SASS (built by __graft_entry__.build())
+    import subprocess
+    out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "--list-elf", pkg.SO_PATH],
+                         capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+
+
+def test_required_bytes_and_validation():
+    lib = pkg.load_library()
+    # config 4: two-array half table, 2 x 2^33 fp32 entries = 64 GiB (+ scratch)
+    assert L.lcsb_required_bytes(2, 2, 17, "f32") == 2 * (1 << 33) * 4 + 256
+    # full table when symmetry is off
+    assert L.lcsb_required_bytes(2, 2, 17, "f32", symmetry=0) == 2 * (1 << 34) * 4 + 256
+    # config 3: KS ring of d+1 = 3 tables of 4^16 fp32
+    assert L.lcsb_required_bytes(4, 2, 8, "f32") == 3 * (1 << 32) * 4 + 256
+    # config 2: 4 tables of 3^12 fp64
+    assert L.lcsb_required_bytes(3, 3, 4, "f64") == 4 * 3 ** 12 * 8 + 256
+    # invalid: two-array for sigma != 2, d > 16, sigma^(d l) too large, symmetry without binary
+    assert L.lcsb_required_bytes(3, 2, 2, "f32", form="two_array") == 0
+    assert L.lcsb_required_bytes(2, 17, 1, "f32") == 0
+    assert L.lcsb_required_bytes(2, 2, 40, "f32") == 0
+    assert L.lcsb_required_bytes(3, 2, 2, "f32", symmetry=1) == 0
+    assert L.lcsb_required_bytes(2, 2, 1, "f32", symmetry=1) == 0
+
+
+@pytest.mark.skipif(has_cuda(), reason="checks the no-GPU failure path")
+def test_create_fails_loudly_without_gpu():
+    lib = pkg.load_library()
+    cfg = L.make_config(2, 2, 4, "f32")
+    h = ctypes.c_void_p()
+    rc = lib.lcsb_create_ex(ctypes.byref(cfg), ctypes.byref(h))
+    assert rc == 4  # LCSB_ECUDA: there is no CPU fallback
+    assert b"CUDA" in lib.lcsb_last_error(None)
+    with pytest.raises(pkg.LcsbError):
+        pkg.Lcsb(2, 2, 4)

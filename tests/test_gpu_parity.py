@@ -1,0 +1,257 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the CPU oracle, element by element.
+
+Tolerances (north_star / DESIGN.md "Parity bar"):
+  * fp32 storage: the oracle emulates the storage rounding; sums of <= 27 same-scale fp32 values
+    are exact in fp64, so tables and bounds must be BIT-identical;
+  * fp64 storage: 1e-12 relative per table entry and on the bound (the complement-folded table
+    and the string swap reorder a few fp64 additions relative to the full-table oracle).
+"""
+import numpy as np
+import pytest
+
+from tests.conftest import has_cuda
+
+pytestmark = [pytest.mark.gpu,
+              pytest.mark.skipif(not has_cuda(), reason="needs a CUDA device")]
+
+from oracle import ft_oracle as fo  # noqa: E402
+
+SEED = 0x240710925
+
+
+def _lcsb():
+    from paper_2407_10925_b200 import Lcsb
+    return Lcsb
+
+
+def _cmp_tables(gpu, ref, dtype):
+    if dtype == "f32":
+        assert np.array_equal(gpu, ref), np.max(np.abs(gpu - ref))
+    else:
+        np.testing.assert_allclose(gpu, ref, rtol=1e-12, atol=1e-300)
+
+
+def _cmp_bound(gb, rb, dtype):
+    for key in ("R_max", "R_min", "E_at_Rmax", "E_at_Rmin", "bound_at_Rmax", "bound_at_Rmin"):
+        g, r = getattr(gb, key), rb[key]
+        if dtype == "f32":
+            assert g == r, (key, g, r)
+        else:
+            assert abs(g - r) <= 1e-12 * max(1.0, abs(r)), (key, g, r)
+
+
+# ------------------------------------------------------------------ binary two-array (bin2)
+
+@pytest.mark.parametrize("dtype", ["f32", "f64"])
+@pytest.mark.parametrize("ell", [2, 3, 4, 5, 6, 7, 8])
+def test_bin2_half_table_matches_oracle(ell, dtype):
+    Lcsb = _lcsb()
+    sweeps = 40
+    h = Lcsb(2, 2, ell, dtype=dtype)
+    assert h.kernel_in_use == "bin2" and h.stored_states == 1 << (2 * ell - 1)
+    run = fo.Run(2, 2, ell, "two_array", dtype)
+    for s in range(1, sweeps + 1):
+        h.sweep(1)
+        run.sweep(1)
+        if s in (1, 2, 3, 7, sweeps):
+            _cmp_tables(h.table(0), run.newest, dtype)
+            _cmp_tables(h.table(1), run.prev, dtype)
+    _cmp_bound(h.bound(), run.bound(), dtype)
+    h.destroy()
+
+
+@pytest.mark.parametrize("dtype", ["f32", "f64"])
+def test_bin2_matches_generic_full_table_two_array(dtype):
+    Lcsb = _lcsb()
+    a = Lcsb(2, 2, 9, dtype=dtype)
+    b = Lcsb(2, 2, 9, dtype=dtype, symmetry=0, kernel="generic")
+    assert a.kernel_in_use == "bin2" and b.kernel_in_use == "generic"
+    a.sweep(60)
+    b.sweep(60)
+    _cmp_tables(a.table(), b.table(), dtype)
+    ba, bb = a.bound(), b.bound()
+    assert abs(ba.bound_at_Rmax - bb.bound_at_Rmax) <= 1e-12
+    a.destroy()
+    b.destroy()
+
+
+def test_config1_binary_l8_f64_500_sweeps():
+    """BASELINE config 1: 2^16 states, fp64, 500 sweeps, bound 0.776860."""
+    Lcsb = _lcsb()
+    h = Lcsb(2, 2, 8, dtype="f64")
+    h.sweep(500)
+    gb = h.bound()
+    ref = fo.feasible_triplet(2, 2, 8, 500, form="two_array", dtype="f64")
+    _cmp_bound(gb, ref, "f64")
+    _cmp_tables(h.table(), ref["table"], "f64")
+    assert fo.floor6(gb.bound) == 0.776860
+    h.destroy()
+
+
+# ------------------------------------------------------------------ general KS form (generic)
+
+@pytest.mark.parametrize("sigma,d,ell,dtype,sweeps", [
+    (2, 2, 1, "f64", 30), (2, 2, 4, "f64", 40), (2, 2, 6, "f32", 40),
+    (3, 2, 2, "f64", 40), (3, 2, 3, "f32", 30), (4, 2, 2, "f64", 30), (4, 2, 3, "f32", 25),
+    (2, 3, 2, "f64", 40), (3, 3, 1, "f64", 40), (3, 3, 2, "f32", 20), (2, 4, 2, "f64", 30),
+    (5, 2, 2, "f64", 20), (2, 5, 1, "f64", 40), (10, 2, 1, "f64", 30), (3, 4, 1, "f32", 30),
+])
+def test_generic_ks_matches_oracle(sigma, d, ell, dtype, sweeps):
+    Lcsb = _lcsb()
+    h = Lcsb(sigma, d, ell, dtype=dtype, form="ks")
+    run = fo.Run(sigma, d, ell, "ks", dtype)
+    for s in range(1, sweeps + 1):
+        h.sweep(1)
+        run.sweep(1)
+        if s in (1, 2, 5, sweeps):
+            for k in range(d):
+                _cmp_tables(h.table(k), run.gens[k], dtype)
+    _cmp_bound(h.bound(), run.bound(), dtype)
+    h.destroy()
+
+
+def test_generic_two_array_l1():
+    # l = 1 cannot use the half-table kernel; AUTO falls back to the full-table generic kernel
+    Lcsb = _lcsb()
+    h = Lcsb(2, 2, 1, dtype="f64")
+    assert h.kernel_in_use == "generic"
+    h.sweep(20)
+    gb = h.bound()
+    assert gb.bound == pytest.approx(2.0 / 3.0, abs=1e-15)
+    assert list(h.table()) == [10.5, 9.5, 9.5, 10.5]  # (k+1)/2, (k-1)/2 at k = 20
+    h.destroy()
+
+
+def test_config2_sigma3_d3_l4_f64_300_sweeps():
+    """BASELINE config 2: 3^12 states, fp64, KS, 300 sweeps (paper 0.556649)."""
+    Lcsb = _lcsb()
+    h = Lcsb(3, 3, 4, dtype="f64")
+    h.sweep(300)
+    gb = h.bound()
+    ref = fo.feasible_triplet(3, 3, 4, 300, form="ks", dtype="f64")
+    _cmp_bound(gb, ref, "f64")
+    _cmp_tables(h.table(), ref["table"], "f64")
+    assert 0.556649 - 5e-7 <= gb.bound < 0.556649 + 1e-6
+    h.destroy()
+
+
+# ------------------------------------------------------------------ full-size configs, sampled
+
+def _splitmix(seed, n, hi):
+    from seeded_inputs import splitmix64_indices
+    return splitmix64_indices(seed, n, hi)
+
+
+def test_config3_sigma4_l8_sampled_after_3_sweeps():
+    """BASELINE config 3 (4^16 states, fp32 storage, KS): 2^20 seeded states after 3 sweeps."""
+    Lcsb = _lcsb()
+    h = Lcsb(4, 2, 8, dtype="f32")
+    idx = _splitmix(SEED, 1 << 20, 4 ** 16)
+    h.sweep(3)
+    g = h.table_gather(idx)
+    ref = fo.sample_values(4, 2, 8, 3, idx, form="ks", dtype="f32")
+    assert np.array_equal(g, ref)
+    h.destroy()
+
+
+def test_config4_binary_l17_sampled_after_3_sweeps():
+    """BASELINE config 4 (2^34 states, fp32 half table): 2^20 seeded states after 3 sweeps."""
+    Lcsb = _lcsb()
+    h = Lcsb(2, 2, 17, dtype="f32")
+    assert h.kernel_in_use == "bin2"
+    idx = _splitmix(SEED, 1 << 20, 1 << 34)
+    h.sweep(3)
+    g = h.table_gather(idx)
+    ref = fo.sample_values(2, 2, 17, 3, idx, form="two_array", dtype="f32")
+    assert np.array_equal(g, ref)
+    # also the previous sweep
+    g2 = h.table_gather(idx, which=1)
+    ref2 = fo.sample_values(2, 2, 17, 2, idx, form="two_array", dtype="f32")
+    assert np.array_equal(g2, ref2)
+    h.destroy()
+
+
+def test_config4_properties_at_full_size():
+    """Properties that hold at any size, on the full 2^34-state run: every entry of the new
+    table dominates the old (monotone in n), the bound is certified below Lueker's upper bound
+    0.82628, and the complement/swap symmetries hold on sampled states."""
+    Lcsb = _lcsb()
+    h = Lcsb(2, 2, 17, dtype="f32")
+    h.sweep(50)
+    b = h.bound()
+    assert b.R_min >= 0.0
+    assert 0.0 <= b.bound < 0.82628
+    idx = _splitmix(SEED + 1, 1 << 18, 1 << 34)
+    ell = 17
+    comp = ((1 << 34) - 1) - idx
+    a_bits = idx & np.uint64(0xAAAAAAAAAAAAAAAA)
+    b_bits = idx & np.uint64(0x5555555555555555)
+    swap = (a_bits >> np.uint64(1)) | (b_bits << np.uint64(1))
+    v = h.table_gather(idx)
+    assert np.array_equal(v, h.table_gather(comp))
+    assert np.array_equal(v, h.table_gather(swap))
+    del ell
+    h.destroy()
+
+
+# ------------------------------------------------------------------ edge cases and errors
+
+def test_errors_and_edge_cases():
+    from paper_2407_10925_b200 import LcsbError
+    Lcsb = _lcsb()
+    h = Lcsb(2, 2, 3, dtype="f32")
+    with pytest.raises(LcsbError) as e:
+        h.bound()                      # no sweep yet
+    assert e.value.code == 3
+    h.sweep(0)
+    assert h.sweeps_done == 0
+    with pytest.raises(LcsbError):
+        h.sweep(-1)
+    h.sweep(1)
+    with pytest.raises(LcsbError):
+        h.table(0, 60, 10)            # past the 64 states
+    with pytest.raises(LcsbError):
+        h.table(2)                     # two-array keeps 2 generations
+    with pytest.raises(LcsbError):
+        h.table_gather(np.array([64], dtype=np.uint64))
+    assert h.table(0, 0, 0).shape == (0,)
+    h.destroy()
+    with pytest.raises(LcsbError) as e:
+        Lcsb(2, 2, 20, dtype="f64", symmetry=0)   # 2 x 8 TiB
+    assert e.value.code == 2
+    with pytest.raises(LcsbError) as e:
+        Lcsb(3, 2, 2, form="two_array")
+    assert e.value.code == 1
+
+
+def test_determinism_bitwise():
+    Lcsb = _lcsb()
+    out = []
+    for _ in range(2):
+        h = Lcsb(2, 2, 10, dtype="f64")
+        h.sweep(25)
+        out.append((h.table(), h.bound().bound))
+        h.destroy()
+    assert np.array_equal(out[0][0], out[1][0]) and out[0][1] == out[1][1]
+
+
+def test_rmode_min_and_best_bookkeeping():
+    Lcsb = _lcsb()
+    h = Lcsb(2, 2, 6, dtype="f64", rmode="min")
+    run = fo.Run(2, 2, 6, "two_array", "f64")
+    for _ in range(6):
+        h.sweep(5)
+        run.sweep(5)
+        gb = h.bound()
+        rb = run.bound()
+        assert gb.bound == pytest.approx(rb["bound_at_Rmin"], abs=1e-12)
+        assert gb.best_bound == pytest.approx(rb["best_at_Rmin"], abs=1e-12)
+    h.destroy()
+
+
+@pytest.fixture(autouse=True)
+def _release_cached_memory():
+    yield
+    import torch
+    torch.cuda.synchronize()
+    torch.cuda.empty_cache()
