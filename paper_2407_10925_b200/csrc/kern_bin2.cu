@@ -209,22 +209,29 @@ __global__ void __launch_bounds__(kTPB) bin2_kernel(Bin2Args a) {
   }
 }
 
-template <typename T, bool WMODE>
-cudaError_t launch_m(const Bin2Args& a, cudaStream_t s, int sms) {
+template <typename T, int M, bool WMODE>
+cudaError_t launch_one(const Bin2Args& a, cudaStream_t s, int sms) {
   const int L = 2 * a.ell;
-  const uint64_t ntiles = 1ull << (L - 2 - 2 * a.m);
-  uint64_t blocks = (uint64_t)sms * 8;
+  const uint64_t ntiles = 1ull << (L - 2 - 2 * M);
+  static uint64_t cap = 0;
+  if (cap == 0) cap = resident_blocks(bin2_kernel<T, M, WMODE>, kTPB, sms);
+  uint64_t blocks = cap;
   if (blocks > ntiles) blocks = ntiles;
   if (blocks < 1) blocks = 1;
+  bin2_kernel<T, M, WMODE><<<(unsigned)blocks, kTPB, 0, s>>>(a);
+  return cudaGetLastError();
+}
+
+template <typename T, bool WMODE>
+cudaError_t launch_m(const Bin2Args& a, cudaStream_t s, int sms) {
   switch (a.m) {
-    case 1: bin2_kernel<T, 1, WMODE><<<(unsigned)blocks, kTPB, 0, s>>>(a); break;
-    case 2: bin2_kernel<T, 2, WMODE><<<(unsigned)blocks, kTPB, 0, s>>>(a); break;
-    case 3: bin2_kernel<T, 3, WMODE><<<(unsigned)blocks, kTPB, 0, s>>>(a); break;
-    case 4: bin2_kernel<T, 4, WMODE><<<(unsigned)blocks, kTPB, 0, s>>>(a); break;
-    case 5: bin2_kernel<T, 5, WMODE><<<(unsigned)blocks, kTPB, 0, s>>>(a); break;
+    case 1: return launch_one<T, 1, WMODE>(a, s, sms);
+    case 2: return launch_one<T, 2, WMODE>(a, s, sms);
+    case 3: return launch_one<T, 3, WMODE>(a, s, sms);
+    case 4: return launch_one<T, 4, WMODE>(a, s, sms);
+    case 5: return launch_one<T, 5, WMODE>(a, s, sms);
     default: return cudaErrorInvalidValue;
   }
-  return cudaGetLastError();
 }
 
 }  // namespace

@@ -217,7 +217,14 @@ __global__ void __launch_bounds__(256) generic_wpass_kernel(GenericArgs a) {
 template <int S_, int D_>
 cudaError_t launch_pair(const GenericArgs& a, int dtype, cudaStream_t s, int sms, bool wpass) {
   uint64_t blocks = (a.n + 255) / 256;
-  uint64_t cap = (uint64_t)sms * 8;
+  static uint64_t caps[2][2] = {{0, 0}, {0, 0}};
+  uint64_t& cap = caps[dtype == LCSB_F32][wpass];
+  if (!cap)
+    cap = dtype == LCSB_F32
+              ? (wpass ? resident_blocks(generic_wpass_kernel<float, S_, D_>, 256, sms)
+                       : resident_blocks(generic_sweep_kernel<float, S_, D_>, 256, sms))
+              : (wpass ? resident_blocks(generic_wpass_kernel<double, S_, D_>, 256, sms)
+                       : resident_blocks(generic_sweep_kernel<double, S_, D_>, 256, sms));
   if (blocks > cap) blocks = cap;
   if (blocks < 1) blocks = 1;
   if (dtype == LCSB_F32) {

@@ -108,7 +108,11 @@ cudaError_t launch_rdiff(const void* newest, const void* prev, uint64_t n, int d
                          unsigned long long* red, cudaStream_t s, int sms) {
   uint64_t per = (dtype == LCSB_F32) ? 4 : 2;
   uint64_t blocks = (n / per + 255) / 256;
-  if (blocks > (uint64_t)sms * 8) blocks = (uint64_t)sms * 8;
+  static uint64_t cap_f = 0, cap_d = 0;
+  if (!cap_f) cap_f = resident_blocks(rdiff_kernel<float>, 256, sms);
+  if (!cap_d) cap_d = resident_blocks(rdiff_kernel<double>, 256, sms);
+  const uint64_t cap = (dtype == LCSB_F32) ? cap_f : cap_d;
+  if (blocks > cap) blocks = cap;
   if (blocks < 1) blocks = 1;
   if (dtype == LCSB_F32)
     rdiff_kernel<float><<<(unsigned)blocks, 256, 0, s>>>((const float*)newest, (const float*)prev, n, red);

@@ -30,6 +30,19 @@ inline double ord_dec(unsigned long long u) {
   return x;
 }
 
+// Persistent grids: the number of CTAs that are co-resident (SMs x occupancy), so a static
+// grid-stride partition has no partial second wave.  Cached per kernel by the caller.
+template <typename K>
+inline uint64_t resident_blocks(K kernel, int tpb, int sms) {
+  int per_sm = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, tpb, 0) != cudaSuccess ||
+      per_sm < 1) {
+    cudaGetLastError();
+    per_sm = 1;
+  }
+  return (uint64_t)per_sm * (uint64_t)sms;
+}
+
 // Reduction slots (device, unsigned long long each):
 //   0: R_max  1: R_min  2: max W at R_max  3: max W at R_min
 constexpr int kRedSlots = 4;
