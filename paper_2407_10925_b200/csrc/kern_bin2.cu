@@ -215,7 +215,7 @@ cudaError_t launch_one(const Bin2Args& a, cudaStream_t s, int sms) {
   const uint64_t ntiles = 1ull << (L - 2 - 2 * M);
   static uint64_t cap = 0;
   if (cap == 0) cap = resident_blocks(bin2_kernel<T, M, WMODE>, kTPB, sms);
-  uint64_t blocks = cap;
+  uint64_t blocks = a.grid_mult > 0 ? (uint64_t)a.grid_mult * sms : cap;
   if (blocks > ntiles) blocks = ntiles;
   if (blocks < 1) blocks = 1;
   bin2_kernel<T, M, WMODE><<<(unsigned)blocks, kTPB, 0, s>>>(a);

@@ -1,0 +1,305 @@
+// kern_bin2_tma.cu -- the binary two-array half-table sweep (same arithmetic and tile pairing as
+// kern_bin2.cu) with every byte moved by the Tensor Memory Accelerator:
+//
+//   * a persistent CTA walks its share of tile pairs {t, psi(t)} (kern_bin2.cu explains the
+//     pairing); for each pair it bulk-copies (cp.async.bulk, 1-D TMA) the two contiguous adv_b
+//     windows (2 x 2T entries) into an S-stage shared-memory ring completed by mbarrier
+//     transaction counts, so S pairs of loads are in flight per CTA while it computes;
+//   * the pair's outputs are assembled in shared memory as six contiguous runs -- Q1 tile t,
+//     Q1 tile psi(t) (permuted in smem so the run is contiguous in HBM), and for each window its
+//     Q0 rows and their mirrors (reversed in smem) -- and written back with bulk stores
+//     (cp.async.bulk.global.shared::cta), double-buffered.
+// HBM therefore sees one streaming read of every stored entry and full-line writes of every
+// output; the SM only does the fp64 means/max in between.
+#include <math.h>
+
+#include "lcsb_internal.cuh"
+
+namespace lcsbk {
+namespace {
+
+template <typename T>
+struct Vec;
+template <>
+struct Vec<float> {
+  using v2 = float2;
+  using v4 = float4;
+};
+template <>
+struct Vec<double> {
+  using v2 = double2;
+  using v4 = double4;
+};
+
+__device__ __forceinline__ uint64_t pairswap(uint64_t v) {
+  return ((v & 0xAAAAAAAAAAAAAAAAull) >> 1) | ((v & 0x5555555555555555ull) << 1);
+}
+__device__ __forceinline__ uint32_t pairswap32(uint32_t v) {
+  return ((v & 0xAAAAAAAAu) >> 1) | ((v & 0x55555555u) << 1);
+}
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t done = 0;
+  do {
+    asm volatile(
+        "{\n"
+        " .reg .pred p;\n"
+        " mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+        " selp.u32 %0, 1, 0, p;\n"
+        "}\n"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+  } while (!done);
+}
+__device__ __forceinline__ void tma_load_1d(void* dst_smem, const void* src, uint32_t bytes,
+                                            uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst_smem)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void tma_store_1d(void* dst, const void* src_smem, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst),
+               "r"(smem_u32(src_smem)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
+template <int N>
+__device__ __forceinline__ void bulk_wait() {
+  asm volatile("cp.async.bulk.wait_group %0;" ::"n"(N) : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void fence_mbar_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+
+__device__ __forceinline__ double q0_val(double v0, double v1, double v2, double v3) {
+  double r = ((v0 + v1) + v2) + v3;
+  double cand = 0.25 * r;
+  double best = 0.0;
+  if (cand > best) best = cand;
+  return 1.0 + best;
+}
+
+constexpr int kThreads = 256;
+
+template <typename T, int M, int S>
+struct TmaCfg {
+  static constexpr uint32_t TT = 1u << (2 * M);   // Q1 outputs per tile
+  static constexpr uint32_t WIN = 2 * TT;         // entries per adv_b window
+  static constexpr uint32_t WIN_BYTES = WIN * sizeof(T);
+  static constexpr uint32_t OUTN = 4 * TT;        // outputs per tile pair
+  static constexpr size_t SMEM = (size_t)S * 2 * WIN * sizeof(T) + 2 * (size_t)OUTN * sizeof(T) +
+                                 (size_t)S * sizeof(uint64_t);
+};
+
+struct Geo {
+  uint64_t q1, lmask, amask, bmask, ntiles;
+};
+
+__device__ __forceinline__ void tile_info(const Geo& g, uint64_t tau, uint32_t tt_log2,
+                                          uint64_t& x0, uint64_t& p0, uint64_t& taup) {
+  const uint64_t TT = 1ull << tt_log2;
+  x0 = g.q1 + tau * TT;
+  p0 = pairswap(~x0 & g.lmask) & ~(TT - 1);
+  taup = (p0 - g.q1) >> tt_log2;
+}
+
+__device__ __forceinline__ uint64_t win_base(const Geo& g, uint64_t x) {
+  return (x & g.amask) | ((x & g.bmask & ~g.q1) << 2);
+}
+
+// next tile >= c (stepping by G) that is the smaller member of its pair
+__device__ __forceinline__ uint64_t next_item(const Geo& g, uint64_t c, uint64_t G,
+                                              uint32_t tt_log2) {
+  while (c < g.ntiles) {
+    uint64_t x0, p0, taup;
+    tile_info(g, c, tt_log2, x0, p0, taup);
+    if (taup >= c) return c;
+    c += G;
+  }
+  return c;
+}
+
+template <typename T, int M, int S>
+__global__ void __launch_bounds__(kThreads) bin2_tma_kernel(Bin2Args a) {
+  using C = TmaCfg<T, M, S>;
+  using V2 = typename Vec<T>::v2;
+  constexpr uint32_t TT = C::TT, WIN = C::WIN, OUTN = C::OUTN;
+  constexpr uint32_t LOG = 2 * M;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  T* in = reinterpret_cast<T*>(smem_raw);                 // [S][2][WIN]
+  T* out = in + (size_t)S * 2 * WIN;                      // [2][OUTN]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(out + 2 * OUTN);
+
+  const int L = 2 * a.ell;
+  Geo g;
+  g.lmask = (1ull << L) - 1;
+  g.q1 = 1ull << (L - 2);
+  g.amask = 0xAAAAAAAAAAAAAAAAull & g.lmask;
+  g.bmask = 0x5555555555555555ull & g.lmask;
+  g.ntiles = 1ull << (L - 2 - LOG);
+  const T* src = reinterpret_cast<const T*>(a.src);
+  T* dst = reinterpret_cast<T*>(a.dst);
+  const int tid = threadIdx.x;
+  const uint64_t G = gridDim.x;
+
+  uint64_t pc = 0;  // producer cursor (thread 0 only)
+  if (tid == 0) {
+    for (int s = 0; s < S; ++s) mbar_init(&bars[s], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  if (tid == 0) {
+    pc = next_item(g, blockIdx.x, G, LOG);
+    for (int s = 0; s < S && pc < g.ntiles; ++s) {
+      uint64_t x0, p0, taup;
+      tile_info(g, pc, LOG, x0, p0, taup);
+      T* buf = in + (size_t)s * 2 * WIN;
+      mbar_expect_tx(&bars[s], 2 * C::WIN_BYTES);
+      tma_load_1d(buf, src + win_base(g, x0), C::WIN_BYTES, &bars[s]);
+      tma_load_1d(buf + WIN, src + win_base(g, p0), C::WIN_BYTES, &bars[s]);
+      pc = next_item(g, pc + G, G, LOG);
+    }
+  }
+
+  uint32_t i = 0;
+  for (uint64_t cc = next_item(g, blockIdx.x, G, LOG); cc < g.ntiles;
+       cc = next_item(g, cc + G, G, LOG), ++i) {
+    const uint32_t s = i % S;
+    const uint32_t parity = (i / S) & 1u;
+    T* buf = in + (size_t)s * 2 * WIN;
+    T* ob = out + (size_t)(i & 1u) * OUTN;
+    if (tid == 0) bulk_wait_read<1>();  // the stores issued from ob two items ago have read it
+    mbar_wait(&bars[s], parity);
+    __syncthreads();
+
+    const V2* W2 = reinterpret_cast<const V2*>(buf);
+    const V2* P2 = reinterpret_cast<const V2*>(buf + WIN);
+#pragma unroll
+    for (uint32_t o = tid; o < TT; o += kThreads) {
+      const V2 w = W2[pairswap32(o)];
+      const V2 q = P2[TT - 1 - o];
+      const double bx = 0.5 * ((double)w.x + (double)w.y);  // adv_b(x)
+      const double bp = 0.5 * ((double)q.x + (double)q.y);  // adv_b(psi x) = adv_a(x)
+      double v = bx;
+      if (bp > v) v = bp;
+      ob[o] = (T)v;
+      ob[TT + pairswap32(~o & (TT - 1))] = (T)v;
+    }
+#pragma unroll
+    for (uint32_t j = tid; j < TT; j += kThreads) {
+      const uint32_t half = j / (TT / 2);        // 0: rows of window t, 1: of window psi(t)
+      const uint32_t r = j % (TT / 2);
+      const T* row = buf + half * WIN + 4 * r;
+      const V2 lo = reinterpret_cast<const V2*>(row)[0];
+      const V2 hi = reinterpret_cast<const V2*>(row)[1];
+      const double fwd = q0_val(lo.x, lo.y, hi.x, hi.y);
+      const double mir = q0_val(hi.y, hi.x, lo.y, lo.x);
+      T* q0 = ob + 2 * TT + half * TT;
+      q0[r] = (T)fwd;
+      q0[TT / 2 + (TT / 2 - 1 - r)] = (T)mir;
+    }
+    fence_proxy_async_smem();
+    __syncthreads();
+
+    if (tid == 0) {
+      uint64_t x0, p0, taup;
+      tile_info(g, cc, LOG, x0, p0, taup);
+      const bool self = (taup == cc);
+      const uint64_t wb = win_base(g, x0), wp = win_base(g, p0);
+      constexpr uint32_t QB = TT * sizeof(T), HB = TT / 2 * sizeof(T);
+      tma_store_1d(dst + x0, ob, QB);
+      tma_store_1d(dst + (wb >> 2), ob + 2 * TT, HB);
+      tma_store_1d(dst + (g.q1 - (wb >> 2) - TT / 2), ob + 2 * TT + TT / 2, HB);
+      if (!self) {
+        tma_store_1d(dst + p0, ob + TT, QB);
+        tma_store_1d(dst + (wp >> 2), ob + 3 * TT, HB);
+        tma_store_1d(dst + (g.q1 - (wp >> 2) - TT / 2), ob + 3 * TT + TT / 2, HB);
+      }
+      bulk_commit();
+      if (pc < g.ntiles) {  // refill the stage this item just vacated
+        uint64_t px0, pp0, ptaup;
+        tile_info(g, pc, LOG, px0, pp0, ptaup);
+        mbar_expect_tx(&bars[s], 2 * C::WIN_BYTES);
+        tma_load_1d(buf, src + win_base(g, px0), C::WIN_BYTES, &bars[s]);
+        tma_load_1d(buf + WIN, src + win_base(g, pp0), C::WIN_BYTES, &bars[s]);
+        pc = next_item(g, pc + G, G, LOG);
+      }
+    }
+  }
+  if (tid == 0) bulk_wait<0>();
+}
+
+template <typename T, int M, int S>
+cudaError_t launch_tma(const Bin2Args& a, cudaStream_t s, int sms) {
+  using C = TmaCfg<T, M, S>;
+  static uint64_t cap = 0;
+  if (cap == 0) {
+    cudaError_t e = cudaFuncSetAttribute(bin2_tma_kernel<T, M, S>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
+    if (e != cudaSuccess) return e;
+    int per_sm = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, bin2_tma_kernel<T, M, S>, kThreads,
+                                                      C::SMEM) != cudaSuccess ||
+        per_sm < 1) {
+      cudaGetLastError();
+      per_sm = 1;
+    }
+    cap = (uint64_t)per_sm * sms;
+  }
+  const uint64_t ntiles = 1ull << (2 * a.ell - 2 - 2 * M);
+  uint64_t blocks = cap < ntiles ? cap : ntiles;
+  bin2_tma_kernel<T, M, S><<<(unsigned)blocks, kThreads, C::SMEM, s>>>(a);
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+// variant: 1 = (M=5, S=4), 2 = (M=4, S=8), 3 = (M=5, S=2), 4 = (M=4, S=4)
+cudaError_t launch_bin2_tma_sweep(const Bin2Args& a, int dtype, int variant, cudaStream_t s,
+                                  int sms) {
+  if (dtype == LCSB_F32) {
+    switch (variant) {
+      case 1: return launch_tma<float, 5, 4>(a, s, sms);
+      case 2: return launch_tma<float, 4, 8>(a, s, sms);
+      case 3: return launch_tma<float, 5, 2>(a, s, sms);
+      case 4: return launch_tma<float, 4, 4>(a, s, sms);
+      default: return cudaErrorInvalidValue;
+    }
+  }
+  switch (variant) {
+    case 1: return launch_tma<double, 4, 4>(a, s, sms);
+    case 2: return launch_tma<double, 4, 8>(a, s, sms);
+    case 3: return launch_tma<double, 4, 2>(a, s, sms);
+    case 4: return launch_tma<double, 3, 8>(a, s, sms);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+int bin2_tma_min_ell(int dtype, int variant) {
+  // the tile (4^M Q1 outputs) must fit: l - 1 >= M
+  if (dtype == LCSB_F32) return (variant == 2 || variant == 4) ? 5 : 6;
+  return variant == 4 ? 4 : 5;
+}
+
+}  // namespace lcsbk

@@ -25,6 +25,7 @@ struct lcsb {
   int form;       // resolved LCSB_FORM_KS / LCSB_FORM_TWO_ARRAY
   int symmetric;  // complement-folded half table
   int kernel;     // 1 generic, 2 bin2
+  int bin2_variant;  // 0 register kernel, 5 register kernel 8 CTAs/SM, 1..4 TMA pipelines
   uint64_t n_logical;
   uint64_t n_stored;
   size_t esize;
@@ -254,6 +255,8 @@ extern "C" int lcsb_create_ex(const lcsb_config* cfg, lcsb_t** out) {
     }
   }
   h->cur = 0;
+  h->bin2_variant = 1;
+  if (const char* v = getenv("LCSB_BIN2_VARIANT")) h->bin2_variant = atoi(v);
   *out = h;
   return LCSB_OK;
 }
@@ -308,7 +311,13 @@ extern "C" int lcsb_sweep(lcsb_t* h, int64_t n) {
       a.dst = h->tab[out];
       a.ell = h->cfg.ell;
       a.m = bin2_tile_m(h->cfg.ell);
-      e = launch_bin2_sweep(a, h->cfg.dtype, s, h->sms);
+      const int v = h->bin2_variant;
+      if (v >= 1 && v <= 4 && h->cfg.ell >= bin2_tma_min_ell(h->cfg.dtype, v)) {
+        e = launch_bin2_tma_sweep(a, h->cfg.dtype, v, s, h->sms);
+      } else {
+        a.grid_mult = (v == 5) ? 8 : 0;
+        e = launch_bin2_sweep(a, h->cfg.dtype, s, h->sms);
+      }
     } else {
       GenericArgs a;
       fill_generic(h, &a);

@@ -63,6 +63,7 @@ struct Bin2Args {
   void* dst;        // output half table (sweep mode)
   int ell;
   int m;            // tile = 4^m Q1 outputs
+  int grid_mult;    // register kernel: 0 = co-resident grid, k > 0 = k CTAs per SM
   const unsigned long long* red_in;
   unsigned long long* red_out;
 };
@@ -72,6 +73,9 @@ cudaError_t launch_generic_sweep(const GenericArgs& a, int dtype, cudaStream_t s
 cudaError_t launch_generic_wpass(const GenericArgs& a, int dtype, cudaStream_t s, int sms);
 cudaError_t launch_bin2_sweep(const Bin2Args& a, int dtype, cudaStream_t s, int sms);
 cudaError_t launch_bin2_wpass(const Bin2Args& a, int dtype, cudaStream_t s, int sms);
+cudaError_t launch_bin2_tma_sweep(const Bin2Args& a, int dtype, int variant, cudaStream_t s,
+                                  int sms);
+int bin2_tma_min_ell(int dtype, int variant);
 cudaError_t launch_red_init(unsigned long long* red, cudaStream_t s);
 cudaError_t launch_rdiff(const void* newest, const void* prev, uint64_t n, int dtype,
                          unsigned long long* red, cudaStream_t s, int sms);
