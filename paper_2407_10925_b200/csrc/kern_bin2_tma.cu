@@ -102,13 +102,13 @@ __device__ __forceinline__ double q0_val(double v0, double v1, double v2, double
 
 constexpr int kThreads = 256;
 
-template <typename T, int M, int S>
+template <typename T, int M, int S, int OB>
 struct TmaCfg {
   static constexpr uint32_t TT = 1u << (2 * M);   // Q1 outputs per tile
   static constexpr uint32_t WIN = 2 * TT;         // entries per adv_b window
   static constexpr uint32_t WIN_BYTES = WIN * sizeof(T);
   static constexpr uint32_t OUTN = 4 * TT;        // outputs per tile pair
-  static constexpr size_t SMEM = (size_t)S * 2 * WIN * sizeof(T) + 2 * (size_t)OUTN * sizeof(T) +
+  static constexpr size_t SMEM = (size_t)S * 2 * WIN * sizeof(T) + OB * (size_t)OUTN * sizeof(T) +
                                  (size_t)S * sizeof(uint64_t);
 };
 
@@ -140,16 +140,16 @@ __device__ __forceinline__ uint64_t next_item(const Geo& g, uint64_t c, uint64_t
   return c;
 }
 
-template <typename T, int M, int S>
+template <typename T, int M, int S, int OB>
 __global__ void __launch_bounds__(kThreads) bin2_tma_kernel(Bin2Args a) {
-  using C = TmaCfg<T, M, S>;
+  using C = TmaCfg<T, M, S, OB>;
   using V2 = typename Vec<T>::v2;
   constexpr uint32_t TT = C::TT, WIN = C::WIN, OUTN = C::OUTN;
   constexpr uint32_t LOG = 2 * M;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   T* in = reinterpret_cast<T*>(smem_raw);                 // [S][2][WIN]
-  T* out = in + (size_t)S * 2 * WIN;                      // [2][OUTN]
-  uint64_t* bars = reinterpret_cast<uint64_t*>(out + 2 * OUTN);
+  T* out = in + (size_t)S * 2 * WIN;                      // [OB][OUTN]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(out + OB * OUTN);
 
   const int L = 2 * a.ell;
   Geo g;
@@ -188,8 +188,8 @@ __global__ void __launch_bounds__(kThreads) bin2_tma_kernel(Bin2Args a) {
     const uint32_t s = i % S;
     const uint32_t parity = (i / S) & 1u;
     T* buf = in + (size_t)s * 2 * WIN;
-    T* ob = out + (size_t)(i & 1u) * OUTN;
-    if (tid == 0) bulk_wait_read<1>();  // the stores issued from ob two items ago have read it
+    T* ob = out + (size_t)(i % OB) * OUTN;
+    if (tid == 0) bulk_wait_read<OB - 1>();  // the stores issued from ob OB items ago have read it
     mbar_wait(&bars[s], parity);
     __syncthreads();
 
@@ -250,17 +250,17 @@ __global__ void __launch_bounds__(kThreads) bin2_tma_kernel(Bin2Args a) {
   if (tid == 0) bulk_wait<0>();
 }
 
-template <typename T, int M, int S>
+template <typename T, int M, int S, int OB>
 cudaError_t launch_tma(const Bin2Args& a, cudaStream_t s, int sms) {
-  using C = TmaCfg<T, M, S>;
+  using C = TmaCfg<T, M, S, OB>;
   static uint64_t cap = 0;
   if (cap == 0) {
-    cudaError_t e = cudaFuncSetAttribute(bin2_tma_kernel<T, M, S>,
+    cudaError_t e = cudaFuncSetAttribute(bin2_tma_kernel<T, M, S, OB>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
     if (e != cudaSuccess) return e;
     int per_sm = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, bin2_tma_kernel<T, M, S>, kThreads,
-                                                      C::SMEM) != cudaSuccess ||
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, bin2_tma_kernel<T, M, S, OB>,
+                                                      kThreads, C::SMEM) != cudaSuccess ||
         per_sm < 1) {
       cudaGetLastError();
       per_sm = 1;
@@ -269,37 +269,47 @@ cudaError_t launch_tma(const Bin2Args& a, cudaStream_t s, int sms) {
   }
   const uint64_t ntiles = 1ull << (2 * a.ell - 2 - 2 * M);
   uint64_t blocks = cap < ntiles ? cap : ntiles;
-  bin2_tma_kernel<T, M, S><<<(unsigned)blocks, kThreads, C::SMEM, s>>>(a);
+  bin2_tma_kernel<T, M, S, OB><<<(unsigned)blocks, kThreads, C::SMEM, s>>>(a);
   return cudaGetLastError();
 }
 
+struct VariantDesc {
+  int m, s, ob;
+};
+// (M, S, OB) per variant id, fp32 and fp64 storage
+constexpr VariantDesc kF32[] = {{0, 0, 0}, {5, 4, 2}, {4, 8, 2}, {5, 2, 2}, {4, 4, 2}, {0, 0, 0},
+                                {5, 1, 2}, {5, 3, 2}, {4, 2, 2}, {5, 2, 1}, {5, 1, 1}, {6, 1, 1}};
+constexpr VariantDesc kF64[] = {{0, 0, 0}, {4, 4, 2}, {4, 8, 2}, {4, 2, 2}, {3, 8, 2}, {0, 0, 0},
+                                {4, 1, 2}, {4, 3, 2}, {5, 1, 1}, {4, 2, 1}, {4, 1, 1}, {3, 4, 2}};
+constexpr int kNumVariants = 12;
+
 }  // namespace
 
-// variant: 1 = (M=5, S=4), 2 = (M=4, S=8), 3 = (M=5, S=2), 4 = (M=4, S=4)
 cudaError_t launch_bin2_tma_sweep(const Bin2Args& a, int dtype, int variant, cudaStream_t s,
                                   int sms) {
+#define LCSB_V(T, M, S, OB) \
+  if (d.m == M && d.s == S && d.ob == OB) return launch_tma<T, M, S, OB>(a, s, sms);
+  if (variant <= 0 || variant >= kNumVariants) return cudaErrorInvalidValue;
   if (dtype == LCSB_F32) {
-    switch (variant) {
-      case 1: return launch_tma<float, 5, 4>(a, s, sms);
-      case 2: return launch_tma<float, 4, 8>(a, s, sms);
-      case 3: return launch_tma<float, 5, 2>(a, s, sms);
-      case 4: return launch_tma<float, 4, 4>(a, s, sms);
-      default: return cudaErrorInvalidValue;
-    }
+    const VariantDesc d = kF32[variant];
+    LCSB_V(float, 5, 4, 2) LCSB_V(float, 4, 8, 2) LCSB_V(float, 5, 2, 2) LCSB_V(float, 4, 4, 2)
+    LCSB_V(float, 5, 1, 2) LCSB_V(float, 5, 3, 2) LCSB_V(float, 4, 2, 2) LCSB_V(float, 5, 2, 1)
+    LCSB_V(float, 5, 1, 1) LCSB_V(float, 6, 1, 1)
+  } else {
+    const VariantDesc d = kF64[variant];
+    LCSB_V(double, 4, 4, 2) LCSB_V(double, 4, 8, 2) LCSB_V(double, 4, 2, 2) LCSB_V(double, 3, 8, 2)
+    LCSB_V(double, 4, 1, 2) LCSB_V(double, 4, 3, 2) LCSB_V(double, 5, 1, 1) LCSB_V(double, 4, 2, 1)
+    LCSB_V(double, 4, 1, 1) LCSB_V(double, 3, 4, 2)
   }
-  switch (variant) {
-    case 1: return launch_tma<double, 4, 4>(a, s, sms);
-    case 2: return launch_tma<double, 4, 8>(a, s, sms);
-    case 3: return launch_tma<double, 4, 2>(a, s, sms);
-    case 4: return launch_tma<double, 3, 8>(a, s, sms);
-    default: return cudaErrorInvalidValue;
-  }
+#undef LCSB_V
+  return cudaErrorInvalidValue;
 }
 
+// smallest l whose Q1 has at least one tile of 4^M outputs (l - 1 >= M); 0 = not a TMA variant
 int bin2_tma_min_ell(int dtype, int variant) {
-  // the tile (4^M Q1 outputs) must fit: l - 1 >= M
-  if (dtype == LCSB_F32) return (variant == 2 || variant == 4) ? 5 : 6;
-  return variant == 4 ? 4 : 5;
+  if (variant <= 0 || variant >= kNumVariants) return 0;
+  const VariantDesc d = (dtype == LCSB_F32) ? kF32[variant] : kF64[variant];
+  return d.m ? d.m + 1 : 0;
 }
 
 }  // namespace lcsbk

@@ -255,7 +255,7 @@ extern "C" int lcsb_create_ex(const lcsb_config* cfg, lcsb_t** out) {
     }
   }
   h->cur = 0;
-  h->bin2_variant = 1;
+  h->bin2_variant = 3;
   if (const char* v = getenv("LCSB_BIN2_VARIANT")) h->bin2_variant = atoi(v);
   *out = h;
   return LCSB_OK;
@@ -312,7 +312,8 @@ extern "C" int lcsb_sweep(lcsb_t* h, int64_t n) {
       a.ell = h->cfg.ell;
       a.m = bin2_tile_m(h->cfg.ell);
       const int v = h->bin2_variant;
-      if (v >= 1 && v <= 4 && h->cfg.ell >= bin2_tma_min_ell(h->cfg.dtype, v)) {
+      const int min_ell = bin2_tma_min_ell(h->cfg.dtype, v);
+      if (min_ell > 0 && h->cfg.ell >= min_ell) {
         e = launch_bin2_tma_sweep(a, h->cfg.dtype, v, s, h->sms);
       } else {
         a.grid_mult = (v == 5) ? 8 : 0;

@@ -3,7 +3,7 @@
 # command, then one --set full capture of the sweep kernel.  Run under gpurun from the repo root.
 set -u
 WL=${1:-config4}
-KREGEX=${2:-bin2_kernelIfLi5ELb0}
+KREGEX=${2:-bin2_tma_kernel}
 OUT=gpurun_out
 mkdir -p $OUT
 BENCH="python bench.py --workload $WL --steps 1 --warmup 3 --no-cpu-baseline"
