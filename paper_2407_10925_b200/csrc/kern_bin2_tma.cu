@@ -108,6 +108,7 @@ struct TmaCfg {
   static constexpr uint32_t WIN = 2 * TT;         // entries per adv_b window
   static constexpr uint32_t WIN_BYTES = WIN * sizeof(T);
   static constexpr uint32_t OUTN = 4 * TT;        // outputs per tile pair
+  // OB = 0: outputs are stored straight from registers (sector-complete runs), no smem staging
   static constexpr size_t SMEM = (size_t)S * 2 * WIN * sizeof(T) + OB * (size_t)OUTN * sizeof(T) +
                                  (size_t)S * sizeof(uint64_t);
 };
@@ -148,7 +149,7 @@ __global__ void __launch_bounds__(kThreads) bin2_tma_kernel(Bin2Args a) {
   constexpr uint32_t LOG = 2 * M;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   T* in = reinterpret_cast<T*>(smem_raw);                 // [S][2][WIN]
-  T* out = in + (size_t)S * 2 * WIN;                      // [OB][OUTN]
+  T* out = in + (size_t)S * 2 * WIN;                      // [OB][OUTN] (OB may be 0)
   uint64_t* bars = reinterpret_cast<uint64_t*>(out + OB * OUTN);
 
   const int L = 2 * a.ell;
@@ -188,10 +189,14 @@ __global__ void __launch_bounds__(kThreads) bin2_tma_kernel(Bin2Args a) {
     const uint32_t s = i % S;
     const uint32_t parity = (i / S) & 1u;
     T* buf = in + (size_t)s * 2 * WIN;
-    T* ob = out + (size_t)(i % OB) * OUTN;
-    if (tid == 0) bulk_wait_read<OB - 1>();  // the stores issued from ob OB items ago have read it
+    T* ob = OB ? out + (size_t)(i % (OB ? OB : 1)) * OUTN : nullptr;
+    if (OB && tid == 0) bulk_wait_read<(OB ? OB - 1 : 0)>();  // stores from ob OB items ago have read it
     mbar_wait(&bars[s], parity);
     __syncthreads();
+    uint64_t x0, p0, taup;
+    tile_info(g, cc, LOG, x0, p0, taup);
+    const bool self = (taup == cc);
+    const uint64_t wb = win_base(g, x0), wp = win_base(g, p0);
 
     const V2* W2 = reinterpret_cast<const V2*>(buf);
     const V2* P2 = reinterpret_cast<const V2*>(buf + WIN);
@@ -203,8 +208,13 @@ __global__ void __launch_bounds__(kThreads) bin2_tma_kernel(Bin2Args a) {
       const double bp = 0.5 * ((double)q.x + (double)q.y);  // adv_b(psi x) = adv_a(x)
       double v = bx;
       if (bp > v) v = bp;
-      ob[o] = (T)v;
-      ob[TT + pairswap32(~o & (TT - 1))] = (T)v;
+      if (OB) {
+        ob[o] = (T)v;
+        ob[TT + pairswap32(~o & (TT - 1))] = (T)v;
+      } else {
+        dst[x0 + o] = (T)v;
+        if (!self) dst[p0 + pairswap32(~o & (TT - 1))] = (T)v;
+      }
     }
 #pragma unroll
     for (uint32_t j = tid; j < TT; j += kThreads) {
@@ -215,28 +225,32 @@ __global__ void __launch_bounds__(kThreads) bin2_tma_kernel(Bin2Args a) {
       const V2 hi = reinterpret_cast<const V2*>(row)[1];
       const double fwd = q0_val(lo.x, lo.y, hi.x, hi.y);
       const double mir = q0_val(hi.y, hi.x, lo.y, lo.x);
-      T* q0 = ob + 2 * TT + half * TT;
-      q0[r] = (T)fwd;
-      q0[TT / 2 + (TT / 2 - 1 - r)] = (T)mir;
+      if (OB) {
+        T* q0 = ob + 2 * TT + half * TT;
+        q0[r] = (T)fwd;
+        q0[TT / 2 + (TT / 2 - 1 - r)] = (T)mir;
+      } else if (half == 0 || !self) {
+        const uint64_t rb = (half ? wp : wb) >> 2;
+        dst[rb + r] = (T)fwd;
+        dst[(g.q1 - 1) - (rb + r)] = (T)mir;
+      }
     }
-    fence_proxy_async_smem();
+    if (OB) fence_proxy_async_smem();
     __syncthreads();
 
     if (tid == 0) {
-      uint64_t x0, p0, taup;
-      tile_info(g, cc, LOG, x0, p0, taup);
-      const bool self = (taup == cc);
-      const uint64_t wb = win_base(g, x0), wp = win_base(g, p0);
-      constexpr uint32_t QB = TT * sizeof(T), HB = TT / 2 * sizeof(T);
-      tma_store_1d(dst + x0, ob, QB);
-      tma_store_1d(dst + (wb >> 2), ob + 2 * TT, HB);
-      tma_store_1d(dst + (g.q1 - (wb >> 2) - TT / 2), ob + 2 * TT + TT / 2, HB);
-      if (!self) {
-        tma_store_1d(dst + p0, ob + TT, QB);
-        tma_store_1d(dst + (wp >> 2), ob + 3 * TT, HB);
-        tma_store_1d(dst + (g.q1 - (wp >> 2) - TT / 2), ob + 3 * TT + TT / 2, HB);
+      if (OB) {
+        constexpr uint32_t QB = TT * sizeof(T), HB = TT / 2 * sizeof(T);
+        tma_store_1d(dst + x0, ob, QB);
+        tma_store_1d(dst + (wb >> 2), ob + 2 * TT, HB);
+        tma_store_1d(dst + (g.q1 - (wb >> 2) - TT / 2), ob + 2 * TT + TT / 2, HB);
+        if (!self) {
+          tma_store_1d(dst + p0, ob + TT, QB);
+          tma_store_1d(dst + (wp >> 2), ob + 3 * TT, HB);
+          tma_store_1d(dst + (g.q1 - (wp >> 2) - TT / 2), ob + 3 * TT + TT / 2, HB);
+        }
+        bulk_commit();
       }
-      bulk_commit();
       if (pc < g.ntiles) {  // refill the stage this item just vacated
         uint64_t px0, pp0, ptaup;
         tile_info(g, pc, LOG, px0, pp0, ptaup);
@@ -247,7 +261,7 @@ __global__ void __launch_bounds__(kThreads) bin2_tma_kernel(Bin2Args a) {
       }
     }
   }
-  if (tid == 0) bulk_wait<0>();
+  if (OB && tid == 0) bulk_wait<0>();
 }
 
 template <typename T, int M, int S, int OB>
@@ -278,10 +292,12 @@ struct VariantDesc {
 };
 // (M, S, OB) per variant id, fp32 and fp64 storage
 constexpr VariantDesc kF32[] = {{0, 0, 0}, {5, 4, 2}, {4, 8, 2}, {5, 2, 2}, {4, 4, 2}, {0, 0, 0},
-                                {5, 1, 2}, {5, 3, 2}, {4, 2, 2}, {5, 2, 1}, {5, 1, 1}, {6, 1, 1}};
+                                {5, 1, 2}, {5, 3, 2}, {4, 2, 2}, {5, 2, 1}, {5, 1, 1}, {6, 1, 1},
+                                {6, 1, 0}, {6, 2, 0}, {5, 2, 0}, {5, 4, 0}, {6, 3, 0}};
 constexpr VariantDesc kF64[] = {{0, 0, 0}, {4, 4, 2}, {4, 8, 2}, {4, 2, 2}, {3, 8, 2}, {0, 0, 0},
-                                {4, 1, 2}, {4, 3, 2}, {5, 1, 1}, {4, 2, 1}, {4, 1, 1}, {3, 4, 2}};
-constexpr int kNumVariants = 12;
+                                {4, 1, 2}, {4, 3, 2}, {5, 1, 1}, {4, 2, 1}, {4, 1, 1}, {3, 4, 2},
+                                {5, 1, 0}, {5, 2, 0}, {4, 2, 0}, {4, 4, 0}, {5, 3, 0}};
+constexpr int kNumVariants = 17;
 
 }  // namespace
 
@@ -294,12 +310,14 @@ cudaError_t launch_bin2_tma_sweep(const Bin2Args& a, int dtype, int variant, cud
     const VariantDesc d = kF32[variant];
     LCSB_V(float, 5, 4, 2) LCSB_V(float, 4, 8, 2) LCSB_V(float, 5, 2, 2) LCSB_V(float, 4, 4, 2)
     LCSB_V(float, 5, 1, 2) LCSB_V(float, 5, 3, 2) LCSB_V(float, 4, 2, 2) LCSB_V(float, 5, 2, 1)
-    LCSB_V(float, 5, 1, 1) LCSB_V(float, 6, 1, 1)
+    LCSB_V(float, 5, 1, 1) LCSB_V(float, 6, 1, 1) LCSB_V(float, 6, 1, 0) LCSB_V(float, 6, 2, 0)
+    LCSB_V(float, 5, 2, 0) LCSB_V(float, 5, 4, 0) LCSB_V(float, 6, 3, 0)
   } else {
     const VariantDesc d = kF64[variant];
     LCSB_V(double, 4, 4, 2) LCSB_V(double, 4, 8, 2) LCSB_V(double, 4, 2, 2) LCSB_V(double, 3, 8, 2)
     LCSB_V(double, 4, 1, 2) LCSB_V(double, 4, 3, 2) LCSB_V(double, 5, 1, 1) LCSB_V(double, 4, 2, 1)
-    LCSB_V(double, 4, 1, 1) LCSB_V(double, 3, 4, 2)
+    LCSB_V(double, 4, 1, 1) LCSB_V(double, 3, 4, 2) LCSB_V(double, 5, 1, 0) LCSB_V(double, 5, 2, 0)
+    LCSB_V(double, 4, 2, 0) LCSB_V(double, 4, 4, 0) LCSB_V(double, 5, 3, 0)
   }
 #undef LCSB_V
   return cudaErrorInvalidValue;
