@@ -60,6 +60,23 @@ def test_bin2_half_table_matches_oracle(ell, dtype):
     h.destroy()
 
 
+@pytest.mark.parametrize("variant", list(range(0, 17)))
+@pytest.mark.parametrize("dtype", ["f32", "f64"])
+def test_bin2_every_variant_matches_oracle(variant, dtype, monkeypatch):
+    """Every sweep variant (register kernel, TMA pipelines of each tile size / stage count /
+    store mode) gives the oracle's tables at l = 8 (and l = 7, the smallest l of the 4^6 tile)."""
+    monkeypatch.setenv("LCSB_BIN2_VARIANT", str(variant))
+    Lcsb = _lcsb()
+    for ell in (7, 8):
+        h = Lcsb(2, 2, ell, dtype=dtype)
+        run = fo.Run(2, 2, ell, "two_array", dtype)
+        h.sweep(12)
+        run.sweep(12)
+        _cmp_tables(h.table(0), run.newest, dtype)
+        _cmp_bound(h.bound(), run.bound(), dtype)
+        h.destroy()
+
+
 @pytest.mark.parametrize("dtype", ["f32", "f64"])
 def test_bin2_matches_generic_full_table_two_array(dtype):
     Lcsb = _lcsb()
