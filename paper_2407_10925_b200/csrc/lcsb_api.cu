@@ -144,6 +144,9 @@ static int plan_config(const lcsb_config* c, Plan* p, char* why, size_t whylen) 
   p->form = form;
   p->symmetric = sym;
   p->kernel = sym ? 2 : 1;
+  if (!sym && c->sigma == 4 && c->d == 2 && form == LCSB_FORM_KS && c->ell >= 3 &&
+      c->kernel == LCSB_KERNEL_AUTO)
+    p->kernel = 3;  // sigma = 4, d = 2 swap-paired TMA kernel (kern_q4.cu)
   p->ntab = (form == LCSB_FORM_KS) ? c->d + 1 : 2;  // Alg. 2: d+1 rows; two-array: 2
   p->n_logical = n;
   p->n_stored = sym ? n / 2 : n;
@@ -332,6 +335,14 @@ extern "C" int lcsb_sweep(lcsb_t* h, int64_t n) {
         a.grid_mult = (v == 5) ? 8 : 0;
         e = launch_bin2_sweep(a, h->cfg.dtype, s, h->sms);
       }
+    } else if (h->kernel == 3) {
+      Q4Args a;
+      memset(&a, 0, sizeof a);
+      a.g1 = h->tab[slot_back(h, 0)];
+      a.g2 = h->tab[slot_back(h, 1)];
+      a.dst = h->tab[out];
+      a.ell = h->cfg.ell;
+      e = launch_q4_sweep(a, h->cfg.dtype, s, h->sms);
     } else {
       GenericArgs a;
       fill_generic(h, &a);
@@ -372,6 +383,15 @@ extern "C" int lcsb_bound(lcsb_t* h, lcsb_bound_t* out) {
     a.red_in = h->red;
     a.red_out = h->red + 2;
     CU(h, launch_bin2_wpass(a, h->cfg.dtype, s, h->sms));
+  } else if (h->kernel == 3) {
+    Q4Args a;
+    memset(&a, 0, sizeof a);
+    a.g1 = newest;
+    a.g2 = newest;
+    a.ell = h->cfg.ell;
+    a.red_in = h->red;
+    a.red_out = h->red + 2;
+    CU(h, launch_q4_wpass(a, h->cfg.dtype, s, h->sms));
   } else {
     GenericArgs a;
     fill_generic(h, &a);

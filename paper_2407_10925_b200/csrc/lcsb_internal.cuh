@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <string.h>
+#include <math.h>
 
 #include "lcsb.h"
 
@@ -68,6 +69,50 @@ struct Bin2Args {
   unsigned long long* red_out;
 };
 
+struct Q4Args {
+  const void* g1;   // table one sweep back (W pass: the newest table)
+  const void* g2;   // table two sweeps back (W pass: the newest table)
+  void* dst;        // output (sweep mode)
+  int ell;
+  const unsigned long long* red_in;
+  unsigned long long* red_out;
+};
+
+#ifdef __CUDACC__
+__device__ __forceinline__ double dec_ord(unsigned long long u) {
+  unsigned long long b = (u & 0x8000000000000000ull) ? (u & 0x7fffffffffffffffull) : ~u;
+  return __longlong_as_double((long long)b);
+}
+
+// block-wide max of two doubles, one atomicMax per block into out[0], out[1] (blockDim % 32 == 0)
+__device__ __forceinline__ void block_max2_to(double w0, double w1, unsigned long long* out) {
+  __shared__ double s0[32], s1[32];
+  for (int o = 16; o > 0; o >>= 1) {
+    w0 = fmax(w0, __shfl_xor_sync(0xffffffffu, w0, o));
+    w1 = fmax(w1, __shfl_xor_sync(0xffffffffu, w1, o));
+  }
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  if (lane == 0) {
+    s0[wid] = w0;
+    s1[wid] = w1;
+  }
+  __syncthreads();
+  if (wid == 0) {
+    const int nw = (blockDim.x + 31) >> 5;
+    w0 = lane < nw ? s0[lane] : -INFINITY;
+    w1 = lane < nw ? s1[lane] : -INFINITY;
+    for (int o = 16; o > 0; o >>= 1) {
+      w0 = fmax(w0, __shfl_xor_sync(0xffffffffu, w0, o));
+      w1 = fmax(w1, __shfl_xor_sync(0xffffffffu, w1, o));
+    }
+    if (lane == 0) {
+      atomicMax(out + 0, ord_enc(w0));
+      atomicMax(out + 1, ord_enc(w1));
+    }
+  }
+}
+#endif
+
 // launchers (return cudaError_t of the launch)
 cudaError_t launch_generic_sweep(const GenericArgs& a, int dtype, cudaStream_t s, int sms);
 cudaError_t launch_generic_wpass(const GenericArgs& a, int dtype, cudaStream_t s, int sms);
@@ -76,6 +121,9 @@ cudaError_t launch_bin2_wpass(const Bin2Args& a, int dtype, cudaStream_t s, int 
 cudaError_t launch_bin2_tma_sweep(const Bin2Args& a, int dtype, int variant, cudaStream_t s,
                                   int sms);
 int bin2_tma_min_ell(int dtype, int variant);
+cudaError_t launch_q4_sweep(const Q4Args& a, int dtype, cudaStream_t s, int sms);
+cudaError_t launch_q4_wpass(const Q4Args& a, int dtype, cudaStream_t s, int sms);
+int q4_min_ell();
 cudaError_t launch_red_init(unsigned long long* red, cudaStream_t s);
 cudaError_t launch_rdiff(const void* newest, const void* prev, uint64_t n, int dtype,
                          unsigned long long* red, cudaStream_t s, int sms);

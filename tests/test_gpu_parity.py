@@ -127,6 +127,40 @@ def test_generic_ks_matches_oracle(sigma, d, ell, dtype, sweeps):
     h.destroy()
 
 
+@pytest.mark.parametrize("ell,dtype", [(3, "f32"), (3, "f64"), (4, "f32"), (4, "f64")])
+def test_q4_kernel_matches_oracle(ell, dtype):
+    """sigma = 4, d = 2, KS form: the swap-paired TMA kernel against the oracle, every table of
+    the ring after several sweeps, and the bound (both R readings)."""
+    Lcsb = _lcsb()
+    h = Lcsb(4, 2, ell, dtype=dtype, form="ks")
+    assert h.kernel_in_use == "q4"
+    run = fo.Run(4, 2, ell, "ks", dtype)
+    for s in range(1, 16):
+        h.sweep(1)
+        run.sweep(1)
+        if s in (1, 2, 3, 15):
+            _cmp_tables(h.table(0), run.gens[0], dtype)
+            _cmp_tables(h.table(1), run.gens[1], dtype)
+    _cmp_bound(h.bound(), run.bound(), dtype)
+    h.destroy()
+
+
+@pytest.mark.parametrize("dtype", ["f32", "f64"])
+def test_q4_matches_generic_kernel_l5(dtype):
+    Lcsb = _lcsb()
+    a = Lcsb(4, 2, 5, dtype=dtype)
+    b = Lcsb(4, 2, 5, dtype=dtype, kernel="generic")
+    assert a.kernel_in_use == "q4" and b.kernel_in_use == "generic"
+    a.sweep(30)
+    b.sweep(30)
+    _cmp_tables(a.table(), b.table(), dtype)
+    ba, bb = a.bound(), b.bound()
+    _cmp_bound(ba, {k: getattr(bb, k) for k in ("R_max", "R_min", "E_at_Rmax", "E_at_Rmin",
+                                                  "bound_at_Rmax", "bound_at_Rmin")}, dtype)
+    a.destroy()
+    b.destroy()
+
+
 def test_generic_two_array_l1():
     # l = 1 cannot use the half-table kernel; AUTO falls back to the full-table generic kernel
     Lcsb = _lcsb()
