@@ -59,7 +59,7 @@ enum {
   LCSB_ECAPACITY = 2, /* not enough device memory; lcsb_last_error() states the bytes needed */
   LCSB_ESTATE = 3,    /* call not valid in the handle's state (e.g. bound before any sweep) */
   LCSB_ECUDA = 4,     /* a CUDA runtime call failed */
-  LCSB_ENCCL = 5      /* reserved for the sharded path */
+  LCSB_ENCCL = 5      /* an NCCL call of the sharded process mode failed */
 };
 
 /* Device allocation hooks (optional).  alloc returns a device pointer of >= bytes, 256-B
@@ -84,10 +84,26 @@ typedef struct {
   lcsb_alloc_fn alloc;
   lcsb_free_fn free_;
   void* alloc_ctx;
+  /* ---- sharding of the complement-folded binary half table (two-array form) ----
+   * The stored table is split over `shards` = P in {1, 2, 4, 8} shards by a key on the first
+   * characters of both strings; every sweep reads only the shard's own table and writes its
+   * outputs into the owners' tables (peer stores over NVLink).  Two modes:
+   *   virtual_shards = 1: this handle holds all P shards on its own GPU (one-GPU mode, used to
+   *                       test the sharded kernels; no communication library involved);
+   *   virtual_shards = 0, P > 1: one process per GPU, this process owns shard `shard`; all P
+   *                       processes pass the same 128-byte ncclUniqueId in nccl_id (from
+   *                       lcsb_nccl_unique_id on one rank).  The library builds its own NCCL
+   *                       communicator, exchanges CUDA IPC handles of the tables through it, and
+   *                       uses NCCL all-reduces for the per-sweep barrier and the bound.  Every
+   *                       process must call create / reset / sweep / bound / destroy collectively. */
+  int32_t shards;
+  int32_t shard;
+  int32_t virtual_shards;
+  const void* nccl_id;
 } lcsb_config;
 
 /* Fill *cfg with defaults: sigma=2,d=2,ell=1, F32, AUTO form, R_MAX, symmetry auto, AUTO
- * kernel, NULL stream and hooks. */
+ * kernel, NULL stream and hooks, 1 shard. */
 void lcsb_config_init(lcsb_config* cfg);
 
 /* Device bytes a handle with this config would own (tables + scratch).  0 on bad config. */
@@ -134,7 +150,19 @@ int lcsb_table(lcsb_t* h, int32_t which, uint64_t first, uint64_t count, double*
 int lcsb_table_gather(lcsb_t* h, int32_t which, const uint64_t* host_idx, uint64_t n,
                       double* host_dst);
 
+/* Write a fresh ncclUniqueId (NCCL_UNIQUE_ID_BYTES = 128) into out[0..len); for sharded
+ * process mode, called on one rank and broadcast to the others by the caller.  Errors: EINVAL
+ * (len < 128), ENCCL. */
+int lcsb_nccl_unique_id(void* out, size_t len);
+
+/* Host-only sharding plan (no GPU needed): the shard and shard-local index holding logical
+ * state `logical` of the binary (sigma = d = 2) complement-folded table of length-ell strings
+ * split over `shards` shards.  Errors: EINVAL. */
+int lcsb_shard_locate(int32_t ell, int32_t shards, uint64_t logical, int32_t* shard,
+                      uint64_t* local);
+
 int64_t lcsb_sweeps_done(const lcsb_t* h);
+int32_t lcsb_num_shards(const lcsb_t* h);   /* P (1 when unsharded) */
 uint64_t lcsb_num_states(const lcsb_t* h);   /* logical states sigma^(d l) */
 uint64_t lcsb_stored_states(const lcsb_t* h);/* entries per stored table */
 uint64_t lcsb_device_bytes(const lcsb_t* h); /* device bytes owned */

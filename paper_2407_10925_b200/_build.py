@@ -39,7 +39,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
         return SO
     tmp = SO + f".tmp{os.getpid()}"
     cmd = [nvcc(), *NVCC_FLAGS, "-I", os.path.join(ROOT, "include"), "-I", CSRC,
-           *[os.path.join(CSRC, s) for s in SOURCES], "-o", tmp, "-lcudart"]
+           *[os.path.join(CSRC, s) for s in SOURCES], "-o", tmp, "-lcudart", "-lnccl"]
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
         sys.stderr.write(res.stdout + res.stderr)

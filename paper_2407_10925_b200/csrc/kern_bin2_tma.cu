@@ -61,7 +61,11 @@ struct TmaCfg {
 };
 
 struct Geo {
-  uint64_t q1, lmask, amask, bmask, ntiles;
+  int L, p;
+  uint32_t shard;
+  uint64_t q1, lmask, amask, bmask;
+  uint32_t h;       // tile-index pairs: the tile of 4^M outputs is fixed by h = l-1-M pairs
+  uint64_t nloc;    // tiles owned by this shard: 4^h / 2^p
 };
 
 __device__ __forceinline__ void tile_info(const Geo& g, uint64_t tau, uint32_t tt_log2,
@@ -76,19 +80,46 @@ __device__ __forceinline__ uint64_t win_base(const Geo& g, uint64_t x) {
   return (x & g.amask) | ((x & g.bmask & ~g.q1) << 2);
 }
 
-// next tile >= c (stepping by G) that is the smaller member of its pair
+// j-th tile owned by this shard.  Tile index bits: pair i (i = 1..h, top first) = (a_i, b_i) of
+// the tile's fixed characters.  Shard key kappa_i = a_i ^ b_i ^ 1 for i <= p, so
+// the owned tiles have b_i = a_i ^ kappa_i ^ 1: j's top p bits are a_1..a_p, the rest free.
+__device__ __forceinline__ uint64_t owned_tile(const Geo& g, uint64_t j) {
+  if (g.p == 0) return j;
+  const uint32_t rest = 2 * (g.h - g.p);
+  uint64_t tau = j & ((1ull << rest) - 1);
+  for (int i = 1; i <= g.p; ++i) {
+    const uint64_t ai = (j >> (rest + g.p - i)) & 1ull;
+    const uint64_t ki = (g.shard >> (g.p - i)) & 1u;
+    const uint64_t bi = ai ^ ki ^ 1ull;
+    tau |= ((ai << 1) | bi) << (2 * (g.h - i));
+  }
+  return tau;
+}
+
+// next owned item >= c (step G) whose tile is the smaller member of its psi pair; returns the
+// enumeration index and the tile
 __device__ __forceinline__ uint64_t next_item(const Geo& g, uint64_t c, uint64_t G,
-                                              uint32_t tt_log2) {
-  while (c < g.ntiles) {
+                                              uint32_t tt_log2, uint64_t& tau_out) {
+  while (c < g.nloc) {
+    const uint64_t tau = owned_tile(g, c);
     uint64_t x0, p0, taup;
-    tile_info(g, c, tt_log2, x0, p0, taup);
-    if (taup >= c) return c;
+    tile_info(g, tau, tt_log2, x0, p0, taup);
+    if (taup >= tau) {
+      tau_out = tau;
+      return c;
+    }
     c += G;
   }
   return c;
 }
 
-template <typename T, int M, int S, int OB>
+template <typename T>
+__device__ __forceinline__ T* out_ptr(const Geo& g, void* const* tabs, uint64_t global) {
+  const uint32_t sh = shard_of_stored(global, g.L, g.p);
+  return reinterpret_cast<T*>(tabs[sh]) + local_of_stored(global, g.L, g.p);
+}
+
+template <typename T, int M, int S, int OB, bool WMODE>
 __global__ void __launch_bounds__(kThreads) bin2_tma_kernel(Bin2Args a) {
   using C = TmaCfg<T, M, S, OB>;
   using V2 = typename Vec<T>::v2;
@@ -99,40 +130,50 @@ __global__ void __launch_bounds__(kThreads) bin2_tma_kernel(Bin2Args a) {
   T* out = in + (size_t)S * 2 * WIN;                      // [OB][OUTN] (OB may be 0)
   uint64_t* bars = reinterpret_cast<uint64_t*>(out + OB * OUTN);
 
-  const int L = 2 * a.ell;
   Geo g;
-  g.lmask = (1ull << L) - 1;
-  g.q1 = 1ull << (L - 2);
+  g.L = 2 * a.ell;
+  g.p = a.shard_bits;
+  g.shard = (uint32_t)a.shard;
+  g.lmask = (1ull << g.L) - 1;
+  g.q1 = 1ull << (g.L - 2);
   g.amask = 0xAAAAAAAAAAAAAAAAull & g.lmask;
   g.bmask = 0x5555555555555555ull & g.lmask;
-  g.ntiles = 1ull << (L - 2 - LOG);
-  const T* src = reinterpret_cast<const T*>(a.src);
-  T* dst = reinterpret_cast<T*>(a.dst);
+  g.h = (uint32_t)(a.ell - 1 - M);
+  g.nloc = (1ull << (2 * g.h)) >> g.p;
+  const T* src = reinterpret_cast<const T*>(a.src);  // this shard's input table
   const int tid = threadIdx.x;
   const uint64_t G = gridDim.x;
 
-  uint64_t pc = 0;  // producer cursor (thread 0 only)
+  double R0 = 0.0, R1 = 0.0, wm0 = -INFINITY, wm1 = -INFINITY;
+  if (WMODE) {
+    R0 = dec_ord(a.red_in[0]);
+    R1 = dec_ord(a.red_in[1]);
+  }
+
+  uint64_t pc = 0, ptau = 0;  // producer cursor (thread 0 only)
   if (tid == 0) {
     for (int s = 0; s < S; ++s) mbar_init(&bars[s], 1);
     fence_mbar_init();
   }
   __syncthreads();
   if (tid == 0) {
-    pc = next_item(g, blockIdx.x, G, LOG);
-    for (int s = 0; s < S && pc < g.ntiles; ++s) {
+    pc = next_item(g, blockIdx.x, G, LOG, ptau);
+    for (int s = 0; s < S && pc < g.nloc; ++s) {
       uint64_t x0, p0, taup;
-      tile_info(g, pc, LOG, x0, p0, taup);
+      tile_info(g, ptau, LOG, x0, p0, taup);
       T* buf = in + (size_t)s * 2 * WIN;
       mbar_expect_tx(&bars[s], 2 * C::WIN_BYTES);
-      tma_load_1d(buf, src + win_base(g, x0), C::WIN_BYTES, &bars[s]);
-      tma_load_1d(buf + WIN, src + win_base(g, p0), C::WIN_BYTES, &bars[s]);
-      pc = next_item(g, pc + G, G, LOG);
+      tma_load_1d(buf, src + local_of_stored(win_base(g, x0), g.L, g.p), C::WIN_BYTES, &bars[s]);
+      tma_load_1d(buf + WIN, src + local_of_stored(win_base(g, p0), g.L, g.p), C::WIN_BYTES,
+                  &bars[s]);
+      pc = next_item(g, pc + G, G, LOG, ptau);
     }
   }
 
   uint32_t i = 0;
-  for (uint64_t cc = next_item(g, blockIdx.x, G, LOG); cc < g.ntiles;
-       cc = next_item(g, cc + G, G, LOG), ++i) {
+  uint64_t ctau = 0;
+  for (uint64_t cc = next_item(g, blockIdx.x, G, LOG, ctau); cc < g.nloc;
+       cc = next_item(g, cc + G, G, LOG, ctau), ++i) {
     const uint32_t s = i % S;
     const uint32_t parity = (i / S) & 1u;
     T* buf = in + (size_t)s * 2 * WIN;
@@ -141,9 +182,17 @@ __global__ void __launch_bounds__(kThreads) bin2_tma_kernel(Bin2Args a) {
     mbar_wait(&bars[s], parity);
     __syncthreads();
     uint64_t x0, p0, taup;
-    tile_info(g, cc, LOG, x0, p0, taup);
-    const bool self = (taup == cc);
+    tile_info(g, ctau, LOG, x0, p0, taup);
+    const bool self = (taup == ctau);
     const uint64_t wb = win_base(g, x0), wp = win_base(g, p0);
+    // the six output runs (each lies in one shard)
+    void* const* tabs = WMODE ? const_cast<void* const*>(a.src_shards) : a.dst_shards;
+    T* runQ1 = out_ptr<T>(g, tabs, x0);
+    T* runQ1p = out_ptr<T>(g, tabs, p0);
+    T* runF = out_ptr<T>(g, tabs, wb >> 2);
+    T* runM = out_ptr<T>(g, tabs, g.q1 - (wb >> 2) - TT / 2);
+    T* runFp = out_ptr<T>(g, tabs, wp >> 2);
+    T* runMp = out_ptr<T>(g, tabs, g.q1 - (wp >> 2) - TT / 2);
 
     const V2* W2 = reinterpret_cast<const V2*>(buf);
     const V2* P2 = reinterpret_cast<const V2*>(buf + WIN);
@@ -155,12 +204,17 @@ __global__ void __launch_bounds__(kThreads) bin2_tma_kernel(Bin2Args a) {
       const double bp = 0.5 * ((double)q.x + (double)q.y);  // adv_b(psi x) = adv_a(x)
       double v = bx;
       if (bp > v) v = bp;
-      if (OB) {
+      if (WMODE) {
+        // W = (u + R) - F'(u); W(psi x) = W(x) exactly (both entries hold the same value)
+        const double ux = (double)runQ1[o];
+        wm0 = fmax(wm0, (ux + R0) - v);
+        wm1 = fmax(wm1, (ux + R1) - v);
+      } else if (OB) {
         ob[o] = (T)v;
         ob[TT + pairswap32(~o & (TT - 1))] = (T)v;
       } else {
-        dst[x0 + o] = (T)v;
-        if (!self) dst[p0 + pairswap32(~o & (TT - 1))] = (T)v;
+        runQ1[o] = (T)v;
+        if (!self) runQ1p[pairswap32(~o & (TT - 1))] = (T)v;
       }
     }
 #pragma unroll
@@ -172,55 +226,67 @@ __global__ void __launch_bounds__(kThreads) bin2_tma_kernel(Bin2Args a) {
       const V2 hi = reinterpret_cast<const V2*>(row)[1];
       const double fwd = q0_val(lo.x, lo.y, hi.x, hi.y);
       const double mir = q0_val(hi.y, hi.x, lo.y, lo.x);
-      if (OB) {
+      if (half == 1 && self) continue;
+      T* rf = half ? runFp : runF;
+      T* rm = half ? runMp : runM;
+      if (WMODE) {
+        const double uf = (double)rf[r], um = (double)rm[TT / 2 - 1 - r];
+        wm0 = fmax(wm0, (uf + R0) - fwd);
+        wm1 = fmax(wm1, (uf + R1) - fwd);
+        wm0 = fmax(wm0, (um + R0) - mir);
+        wm1 = fmax(wm1, (um + R1) - mir);
+      } else if (OB) {
         T* q0 = ob + 2 * TT + half * TT;
         q0[r] = (T)fwd;
         q0[TT / 2 + (TT / 2 - 1 - r)] = (T)mir;
-      } else if (half == 0 || !self) {
-        const uint64_t rb = (half ? wp : wb) >> 2;
-        dst[rb + r] = (T)fwd;
-        dst[(g.q1 - 1) - (rb + r)] = (T)mir;
+      } else {
+        rf[r] = (T)fwd;
+        rm[TT / 2 - 1 - r] = (T)mir;
       }
     }
-    if (OB) fence_proxy_async_smem();
+    if (OB && !WMODE) fence_proxy_async_smem();
     __syncthreads();
 
     if (tid == 0) {
-      if (OB) {
+      if (OB && !WMODE) {  // OB > 0 only when unsharded (launcher enforces)
         constexpr uint32_t QB = TT * sizeof(T), HB = TT / 2 * sizeof(T);
-        tma_store_1d(dst + x0, ob, QB);
-        tma_store_1d(dst + (wb >> 2), ob + 2 * TT, HB);
-        tma_store_1d(dst + (g.q1 - (wb >> 2) - TT / 2), ob + 2 * TT + TT / 2, HB);
+        tma_store_1d(runQ1, ob, QB);
+        tma_store_1d(runF, ob + 2 * TT, HB);
+        tma_store_1d(runM, ob + 2 * TT + TT / 2, HB);
         if (!self) {
-          tma_store_1d(dst + p0, ob + TT, QB);
-          tma_store_1d(dst + (wp >> 2), ob + 3 * TT, HB);
-          tma_store_1d(dst + (g.q1 - (wp >> 2) - TT / 2), ob + 3 * TT + TT / 2, HB);
+          tma_store_1d(runQ1p, ob + TT, QB);
+          tma_store_1d(runFp, ob + 3 * TT, HB);
+          tma_store_1d(runMp, ob + 3 * TT + TT / 2, HB);
         }
         bulk_commit();
       }
-      if (pc < g.ntiles) {  // refill the stage this item just vacated
+      if (pc < g.nloc) {  // refill the stage this item just vacated
         uint64_t px0, pp0, ptaup;
-        tile_info(g, pc, LOG, px0, pp0, ptaup);
+        tile_info(g, ptau, LOG, px0, pp0, ptaup);
         mbar_expect_tx(&bars[s], 2 * C::WIN_BYTES);
-        tma_load_1d(buf, src + win_base(g, px0), C::WIN_BYTES, &bars[s]);
-        tma_load_1d(buf + WIN, src + win_base(g, pp0), C::WIN_BYTES, &bars[s]);
-        pc = next_item(g, pc + G, G, LOG);
+        tma_load_1d(buf, src + local_of_stored(win_base(g, px0), g.L, g.p), C::WIN_BYTES,
+                    &bars[s]);
+        tma_load_1d(buf + WIN, src + local_of_stored(win_base(g, pp0), g.L, g.p), C::WIN_BYTES,
+                    &bars[s]);
+        pc = next_item(g, pc + G, G, LOG, ptau);
       }
     }
   }
-  if (OB && tid == 0) bulk_wait<0>();
+  if (OB && !WMODE && tid == 0) bulk_wait<0>();
+  if (!WMODE && g.p > 0) __threadfence_system();  // peer stores visible before the barrier
+  if (WMODE) block_max2_to(wm0, wm1, a.red_out);
 }
 
-template <typename T, int M, int S, int OB>
+template <typename T, int M, int S, int OB, bool WMODE>
 cudaError_t launch_tma(const Bin2Args& a, cudaStream_t s, int sms) {
   using C = TmaCfg<T, M, S, OB>;
   static uint64_t cap = 0;
   if (cap == 0) {
-    cudaError_t e = cudaFuncSetAttribute(bin2_tma_kernel<T, M, S, OB>,
+    cudaError_t e = cudaFuncSetAttribute(bin2_tma_kernel<T, M, S, OB, WMODE>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
     if (e != cudaSuccess) return e;
     int per_sm = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, bin2_tma_kernel<T, M, S, OB>,
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, bin2_tma_kernel<T, M, S, OB, WMODE>,
                                                       kThreads, C::SMEM) != cudaSuccess ||
         per_sm < 1) {
       cudaGetLastError();
@@ -228,9 +294,11 @@ cudaError_t launch_tma(const Bin2Args& a, cudaStream_t s, int sms) {
     }
     cap = (uint64_t)per_sm * sms;
   }
-  const uint64_t ntiles = 1ull << (2 * a.ell - 2 - 2 * M);
-  uint64_t blocks = cap < ntiles ? cap : ntiles;
-  bin2_tma_kernel<T, M, S, OB><<<(unsigned)blocks, kThreads, C::SMEM, s>>>(a);
+  if (!WMODE && OB > 0 && a.shard_bits > 0) return cudaErrorInvalidValue;
+  const uint64_t nloc = (1ull << (2 * (a.ell - 1 - M))) >> a.shard_bits;
+  uint64_t blocks = cap < nloc ? cap : nloc;
+  if (blocks < 1) blocks = 1;
+  bin2_tma_kernel<T, M, S, OB, WMODE><<<(unsigned)blocks, kThreads, C::SMEM, s>>>(a);
   return cudaGetLastError();
 }
 
@@ -240,37 +308,70 @@ struct VariantDesc {
 // (M, S, OB) per variant id, fp32 and fp64 storage
 constexpr VariantDesc kF32[] = {{0, 0, 0}, {5, 4, 2}, {4, 8, 2}, {5, 2, 2}, {4, 4, 2}, {0, 0, 0},
                                 {5, 1, 2}, {5, 3, 2}, {4, 2, 2}, {5, 2, 1}, {5, 1, 1}, {6, 1, 1},
-                                {6, 1, 0}, {6, 2, 0}, {5, 2, 0}, {5, 4, 0}, {6, 3, 0}};
+                                {6, 1, 0}, {6, 2, 0}, {5, 2, 0}, {5, 4, 0}, {6, 3, 0}, {4, 2, 0}};
 constexpr VariantDesc kF64[] = {{0, 0, 0}, {4, 4, 2}, {4, 8, 2}, {4, 2, 2}, {3, 8, 2}, {0, 0, 0},
                                 {4, 1, 2}, {4, 3, 2}, {5, 1, 1}, {4, 2, 1}, {4, 1, 1}, {3, 4, 2},
-                                {5, 1, 0}, {5, 2, 0}, {4, 2, 0}, {4, 4, 0}, {5, 3, 0}};
-constexpr int kNumVariants = 17;
+                                {5, 1, 0}, {5, 2, 0}, {4, 2, 0}, {4, 4, 0}, {5, 3, 0}, {3, 2, 0}};
+constexpr int kNumVariants = 18;
 
 }  // namespace
 
 cudaError_t launch_bin2_tma_sweep(const Bin2Args& a, int dtype, int variant, cudaStream_t s,
                                   int sms) {
 #define LCSB_V(T, M, S, OB) \
-  if (d.m == M && d.s == S && d.ob == OB) return launch_tma<T, M, S, OB>(a, s, sms);
+  if (d.m == M && d.s == S && d.ob == OB) return launch_tma<T, M, S, OB, false>(a, s, sms);
   if (variant <= 0 || variant >= kNumVariants) return cudaErrorInvalidValue;
   if (dtype == LCSB_F32) {
     const VariantDesc d = kF32[variant];
     LCSB_V(float, 5, 4, 2) LCSB_V(float, 4, 8, 2) LCSB_V(float, 5, 2, 2) LCSB_V(float, 4, 4, 2)
     LCSB_V(float, 5, 1, 2) LCSB_V(float, 5, 3, 2) LCSB_V(float, 4, 2, 2) LCSB_V(float, 5, 2, 1)
     LCSB_V(float, 5, 1, 1) LCSB_V(float, 6, 1, 1) LCSB_V(float, 6, 1, 0) LCSB_V(float, 6, 2, 0)
-    LCSB_V(float, 5, 2, 0) LCSB_V(float, 5, 4, 0) LCSB_V(float, 6, 3, 0)
+    LCSB_V(float, 5, 2, 0) LCSB_V(float, 5, 4, 0) LCSB_V(float, 6, 3, 0) LCSB_V(float, 4, 2, 0)
   } else {
     const VariantDesc d = kF64[variant];
     LCSB_V(double, 4, 4, 2) LCSB_V(double, 4, 8, 2) LCSB_V(double, 4, 2, 2) LCSB_V(double, 3, 8, 2)
     LCSB_V(double, 4, 1, 2) LCSB_V(double, 4, 3, 2) LCSB_V(double, 5, 1, 1) LCSB_V(double, 4, 2, 1)
     LCSB_V(double, 4, 1, 1) LCSB_V(double, 3, 4, 2) LCSB_V(double, 5, 1, 0) LCSB_V(double, 5, 2, 0)
-    LCSB_V(double, 4, 2, 0) LCSB_V(double, 4, 4, 0) LCSB_V(double, 5, 3, 0)
+    LCSB_V(double, 4, 2, 0) LCSB_V(double, 4, 4, 0) LCSB_V(double, 5, 3, 0) LCSB_V(double, 3, 2, 0)
   }
 #undef LCSB_V
   return cudaErrorInvalidValue;
 }
 
+// W pass on the same pipeline (two stages, no output staging); M = tile exponent
+cudaError_t launch_bin2_tma_wpass(const Bin2Args& a, int dtype, int M, cudaStream_t s, int sms) {
+  if (dtype == LCSB_F32) {
+    if (M == 5) return launch_tma<float, 5, 2, 0, true>(a, s, sms);
+    if (M == 4) return launch_tma<float, 4, 2, 0, true>(a, s, sms);
+    if (M == 3) return launch_tma<float, 3, 2, 0, true>(a, s, sms);
+  } else {
+    if (M == 4) return launch_tma<double, 4, 2, 0, true>(a, s, sms);
+    if (M == 3) return launch_tma<double, 3, 2, 0, true>(a, s, sms);
+  }
+  return cudaErrorInvalidValue;
+}
+// largest W-pass tile exponent usable at this l and shard count (0 = none)
+int bin2_tma_wpass_m(int dtype, int ell, int p) {
+  const int ms32[] = {5, 4, 3}, ms64[] = {4, 3, 0};
+  const int* ms = (dtype == LCSB_F32) ? ms32 : ms64;
+  for (int i = 0; i < 3; ++i)
+    if (ms[i] && ell >= ms[i] + 1 && p < ell - 1 - ms[i]) return ms[i];
+  return 0;
+}
+
 // smallest l whose Q1 has at least one tile of 4^M outputs (l - 1 >= M); 0 = not a TMA variant
+// tile exponent M of a variant (0 = not a TMA variant)
+int bin2_tma_m(int dtype, int variant) {
+  if (variant <= 0 || variant >= kNumVariants) return 0;
+  return (dtype == LCSB_F32) ? kF32[variant].m : kF64[variant].m;
+}
+// does the variant store straight from registers (required when sharded)
+int bin2_tma_direct(int dtype, int variant) {
+  if (variant <= 0 || variant >= kNumVariants) return 0;
+  const VariantDesc d = (dtype == LCSB_F32) ? kF32[variant] : kF64[variant];
+  return d.m > 0 && d.ob == 0;
+}
+
 int bin2_tma_min_ell(int dtype, int variant) {
   if (variant <= 0 || variant >= kNumVariants) return 0;
   const VariantDesc d = (dtype == LCSB_F32) ? kF32[variant] : kF64[variant];

@@ -84,8 +84,12 @@ __global__ void __launch_bounds__(256) rdiff_kernel(const T* __restrict__ a, con
   }
 }
 
+struct ExpandTabs {
+  const void* t[kMaxShards];
+};
+
 template <typename T>
-__global__ void expand_kernel(const T* __restrict__ tab, int symmetric, int ell, uint64_t first,
+__global__ void expand_kernel(ExpandTabs tabs, int p, int symmetric, int ell, uint64_t first,
                               uint64_t count, const uint64_t* __restrict__ idx, double* out) {
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   const uint64_t half = symmetric ? (1ull << (2 * ell - 1)) : 0;
@@ -93,7 +97,8 @@ __global__ void expand_kernel(const T* __restrict__ tab, int symmetric, int ell,
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count; i += stride) {
     uint64_t y = idx ? idx[i] : first + i;
     if (symmetric && y >= half) y = top - y;  // Eq. (comp_eq)
-    out[i] = (double)tab[y];
+    const uint32_t sh = shard_of_stored(y, 2 * ell, p);
+    out[i] = (double)reinterpret_cast<const T*>(tabs.t[sh])[local_of_stored(y, 2 * ell, p)];
   }
 }
 
@@ -121,15 +126,18 @@ cudaError_t launch_rdiff(const void* newest, const void* prev, uint64_t n, int d
   return cudaGetLastError();
 }
 
-cudaError_t launch_expand(const void* tab, int dtype, int symmetric, int ell, uint64_t first,
-                          uint64_t count, const uint64_t* idx, double* out, cudaStream_t s) {
+cudaError_t launch_expand(const void* const* tabs, int p, int dtype, int symmetric, int ell,
+                          uint64_t first, uint64_t count, const uint64_t* idx, double* out,
+                          cudaStream_t s) {
   uint64_t blocks = (count + 255) / 256;
   if (blocks > 4096) blocks = 4096;
   if (blocks < 1) blocks = 1;
+  ExpandTabs t;
+  for (int k = 0; k < kMaxShards; ++k) t.t[k] = (k < (1 << p)) ? tabs[k] : nullptr;
   if (dtype == LCSB_F32)
-    expand_kernel<float><<<(unsigned)blocks, 256, 0, s>>>((const float*)tab, symmetric, ell, first, count, idx, out);
+    expand_kernel<float><<<(unsigned)blocks, 256, 0, s>>>(t, p, symmetric, ell, first, count, idx, out);
   else
-    expand_kernel<double><<<(unsigned)blocks, 256, 0, s>>>((const double*)tab, symmetric, ell, first, count, idx, out);
+    expand_kernel<double><<<(unsigned)blocks, 256, 0, s>>>(t, p, symmetric, ell, first, count, idx, out);
   return cudaGetLastError();
 }
 

@@ -1,8 +1,9 @@
-// lcsb_api.cu -- the C-ABI of include/lcsb.h: handle, table ring, kernel dispatch, bound
-// bookkeeping.  Host code only enqueues work; the whole sweep / bound path runs in the kernels
-// of kern_*.cu.  No CPU fallback exists: every entry point fails with LCSB_ECUDA when the
+// lcsb_api.cu -- the C-ABI of include/lcsb.h: handle, table ring, shards, kernel dispatch and the
+// bound bookkeeping.  Host code only enqueues work; the whole sweep / bound path runs in the
+// kernels of kern_*.cu.  No CPU fallback exists: every entry point fails with LCSB_ECUDA when the
 // device work cannot be enqueued.
 #include <math.h>
+#include <nccl.h>
 #include <stdarg.h>
 #include <stdio.h>
 #include <stdlib.h>
@@ -18,23 +19,31 @@ int bin2_tile_m(int ell);
 
 using namespace lcsbk;
 
+enum { MODE_SINGLE = 0, MODE_VIRTUAL = 1, MODE_PROCESS = 2 };
+
 struct lcsb {
   lcsb_config cfg;
   int device;
   int sms;
   int form;       // resolved LCSB_FORM_KS / LCSB_FORM_TWO_ARRAY
   int symmetric;  // complement-folded half table
-  int kernel;     // 1 generic, 2 bin2
-  int bin2_variant;  // 0 register kernel, 5 register kernel 8 CTAs/SM, 1..4 TMA pipelines
+  int kernel;     // 1 generic, 2 bin2, 3 q4
+  int bin2_variant;  // 0 auto; see pick_bin2_variant
   uint64_t n_logical;
-  uint64_t n_stored;
+  uint64_t n_stored;  // entries of the whole stored table
+  uint64_t n_local;   // entries per shard
   size_t esize;
-  int ntab;                 // tables in the ring
-  void* tab[kMaxGen];
-  size_t tab_bytes;
-  int cur;                  // ring slot of the newest table
-  unsigned long long* red;  // device reduction slots
+  int ntab;           // tables in the ring
+  int p, P;           // shards: P = 2^p
+  int mode;           // MODE_*
+  int first, nown;    // owned shards [first, first + nown)
+  void* tabs[kMaxShards][kMaxGen];
+  size_t tab_bytes;   // bytes per shard table
+  int cur;            // ring slot of the newest table
+  unsigned long long* red;       // device reduction slots
   unsigned long long* red_host;  // pinned
+  ncclComm_t comm;
+  int* barrier_buf;
   int64_t sweeps_done;
   int64_t launches;
   double best_rho[2];
@@ -50,8 +59,7 @@ static int set_err(lcsb_t* h, int code, const char* fmt, ...) {
   va_start(ap, fmt);
   vsnprintf(buf, 512, fmt, ap);
   va_end(ap);
-  if (!h) return code;
-  snprintf(g_err, sizeof g_err, "%s", h->err);
+  if (h) snprintf(g_err, sizeof g_err, "%s", h->err);
   return code;
 }
 
@@ -60,6 +68,13 @@ static int set_err(lcsb_t* h, int code, const char* fmt, ...) {
     cudaError_t e_ = (call);                                                          \
     if (e_ != cudaSuccess)                                                            \
       return set_err((h), LCSB_ECUDA, "%s failed: %s", #call, cudaGetErrorString(e_)); \
+  } while (0)
+
+#define NC(h, call)                                                                     \
+  do {                                                                                  \
+    ncclResult_t r_ = (call);                                                           \
+    if (r_ != ncclSuccess)                                                              \
+      return set_err((h), LCSB_ENCCL, "%s failed: %s", #call, ncclGetErrorString(r_)); \
   } while (0)
 
 static bool mul_ok(uint64_t a, uint64_t b, uint64_t* out) {
@@ -79,14 +94,41 @@ extern "C" void lcsb_config_init(lcsb_config* c) {
   c->rmode = LCSB_R_MAX;
   c->symmetry = -1;
   c->kernel = LCSB_KERNEL_AUTO;
+  c->shards = 1;
 }
 
+// ---------------------------------------------------------------- bin2 variant choice
+// Auto choice of the bin2 sweep variant, from the A/B measurements on B200 (DESIGN.md §7):
+// fp32 -> (M=6, 2 stages, direct stores), 97% of the measured copy bandwidth at l=17;
+// fp64 -> (M=5, 1 stage, smem-staged bulk stores), 97% at l=16; smaller tiles for small l;
+// the register kernel below that.  Sharded runs need direct stores (outputs go to peers) and
+// a tile small enough that the shard key bits sit above it (p < l - 1 - M).
+static int pick_bin2_variant(int dtype, int ell, int p) {
+  static const int f32_chain[] = {13, 6, 8};
+  static const int f64_chain[] = {8, 3, 4};
+  static const int direct_chain[] = {13, 14, 17};
+  const int* chain = p > 0 ? direct_chain : (dtype == LCSB_F32 ? f32_chain : f64_chain);
+  for (int i = 0; i < 3; ++i) {
+    const int v = chain[i];
+    const int M = bin2_tma_m(dtype, v);
+    if (M > 0 && ell >= M + 1 && p < ell - 1 - M) return v;
+  }
+  return p > 0 ? 0 : 5;  // 5 = register kernel (unsharded only); 0 = none
+}
+
+// ---------------------------------------------------------------- planning
 struct Plan {
-  int form, symmetric, kernel, ntab;
-  uint64_t n_logical, n_stored;
+  int form, symmetric, kernel, ntab, p, P, mode;
+  uint64_t n_logical, n_stored, n_local;
   size_t esize;
-  uint64_t bytes;
+  uint64_t bytes;  // device bytes this handle allocates
 };
+
+static int log2_exact(int v) {
+  int p = 0;
+  while ((1 << p) < v) ++p;
+  return (1 << p) == v ? p : -1;
+}
 
 static int plan_config(const lcsb_config* c, Plan* p, char* why, size_t whylen) {
   if (!c) {
@@ -141,6 +183,33 @@ static int plan_config(const lcsb_config* c, Plan* p, char* why, size_t whylen) 
     snprintf(why, whylen, "symmetry must be -1, 0 or 1");
     return LCSB_EINVAL;
   }
+  const int P = c->shards < 1 ? 1 : c->shards;
+  const int lp = log2_exact(P);
+  if (lp < 0 || P > kMaxShards) {
+    snprintf(why, whylen, "shards must be 1, 2, 4 or 8");
+    return LCSB_EINVAL;
+  }
+  if (P > 1) {
+    if (!sym) {
+      snprintf(why, whylen, "sharding needs the complement-folded binary two-array table");
+      return LCSB_EINVAL;
+    }
+    if (pick_bin2_variant(c->dtype, c->ell, lp) == 0 ||
+        bin2_tma_wpass_m(c->dtype, c->ell, lp) == 0) {
+      snprintf(why, whylen, "ell = %d is too small for %d shards", c->ell, P);
+      return LCSB_EINVAL;
+    }
+    if (!c->virtual_shards) {
+      if (c->shard < 0 || c->shard >= P) {
+        snprintf(why, whylen, "shard must be in [0, %d)", P);
+        return LCSB_EINVAL;
+      }
+      if (!c->nccl_id) {
+        snprintf(why, whylen, "process-sharded mode needs nccl_id");
+        return LCSB_EINVAL;
+      }
+    }
+  }
   p->form = form;
   p->symmetric = sym;
   p->kernel = sym ? 2 : 1;
@@ -148,11 +217,17 @@ static int plan_config(const lcsb_config* c, Plan* p, char* why, size_t whylen) 
       c->kernel == LCSB_KERNEL_AUTO)
     p->kernel = 3;  // sigma = 4, d = 2 swap-paired TMA kernel (kern_q4.cu)
   p->ntab = (form == LCSB_FORM_KS) ? c->d + 1 : 2;  // Alg. 2: d+1 rows; two-array: 2
+  p->P = P;
+  p->p = lp;
+  p->mode = P == 1 ? MODE_SINGLE : (c->virtual_shards ? MODE_VIRTUAL : MODE_PROCESS);
   p->n_logical = n;
   p->n_stored = sym ? n / 2 : n;
+  p->n_local = p->n_stored / (uint64_t)P;
   p->esize = (c->dtype == LCSB_F32) ? 4 : 8;
-  uint64_t tb;
-  if (!mul_ok(p->n_stored, p->esize, &tb) || !mul_ok(tb, (uint64_t)p->ntab, &p->bytes)) {
+  const uint64_t owned = (p->mode == MODE_PROCESS) ? 1 : (uint64_t)P;
+  uint64_t tb, all;
+  if (!mul_ok(p->n_local, p->esize, &tb) || !mul_ok(tb, (uint64_t)p->ntab, &all) ||
+      !mul_ok(all, owned, &p->bytes)) {
     snprintf(why, whylen, "table size overflows");
     return LCSB_EINVAL;
   }
@@ -167,9 +242,40 @@ extern "C" uint64_t lcsb_required_bytes(const lcsb_config* c) {
   return p.bytes;
 }
 
+extern "C" int lcsb_shard_locate(int32_t ell, int32_t shards, uint64_t logical, int32_t* shard,
+                                 uint64_t* local) {
+  const int p = log2_exact(shards);
+  if (ell < 2 || ell > 31 || p < 0 || shards > kMaxShards || !shard || !local)
+    return set_err(nullptr, LCSB_EINVAL, "bad arguments to lcsb_shard_locate");
+  const int L = 2 * ell;
+  if (logical >= (1ull << L)) return set_err(nullptr, LCSB_EINVAL, "logical index out of range");
+  uint64_t s = logical;
+  if (s >= (1ull << (L - 1))) s = ((1ull << L) - 1) - s;  // Eq. (comp_eq)
+  *shard = (int32_t)shard_of_stored(s, L, p);
+  *local = local_of_stored(s, L, p);
+  return LCSB_OK;
+}
+
+extern "C" int lcsb_nccl_unique_id(void* out, size_t len) {
+  if (!out || len < sizeof(ncclUniqueId))
+    return set_err(nullptr, LCSB_EINVAL, "need a %zu-byte buffer", sizeof(ncclUniqueId));
+  ncclUniqueId id;
+  NC(nullptr, ncclGetUniqueId(&id));
+  memcpy(out, &id, sizeof id);
+  return LCSB_OK;
+}
+
+// ---------------------------------------------------------------- memory
 static void* dev_alloc(lcsb_t* h, size_t bytes) {
-  if (h->cfg.alloc) return h->cfg.alloc(bytes, h->cfg.stream, h->cfg.alloc_ctx);
   void* p = nullptr;
+  if (h->mode == MODE_PROCESS) {  // IPC-exportable allocations
+    if (cudaMalloc(&p, bytes) != cudaSuccess) {
+      cudaGetLastError();
+      return nullptr;
+    }
+    return p;
+  }
+  if (h->cfg.alloc) return h->cfg.alloc(bytes, h->cfg.stream, h->cfg.alloc_ctx);
   if (cudaMallocAsync(&p, bytes, (cudaStream_t)h->cfg.stream) != cudaSuccess) {
     cudaGetLastError();
     return nullptr;
@@ -179,21 +285,83 @@ static void* dev_alloc(lcsb_t* h, size_t bytes) {
 
 static void dev_free(lcsb_t* h, void* p, size_t bytes) {
   if (!p) return;
-  if (h->cfg.free_)
+  if (h->mode == MODE_PROCESS)
+    cudaFree(p);
+  else if (h->cfg.free_)
     h->cfg.free_(p, bytes, h->cfg.stream, h->cfg.alloc_ctx);
   else
     cudaFreeAsync(p, (cudaStream_t)h->cfg.stream);
 }
 
+static bool owns(const lcsb_t* h, int k) { return k >= h->first && k < h->first + h->nown; }
+
+static int barrier(lcsb_t* h) {  // process mode: every rank's preceding work is complete
+  if (h->mode != MODE_PROCESS) return LCSB_OK;
+  NC(h, ncclAllReduce(h->barrier_buf, h->barrier_buf, 1, ncclInt32, ncclSum, h->comm,
+                      (cudaStream_t)h->cfg.stream));
+  return LCSB_OK;
+}
+
 extern "C" void lcsb_destroy(lcsb_t* h) {
   if (!h) return;
   cudaSetDevice(h->device);
-  cudaStreamSynchronize((cudaStream_t)h->cfg.stream);
-  for (int i = 0; i < h->ntab; ++i) dev_free(h, h->tab[i], h->tab_bytes);
+  cudaStream_t s = (cudaStream_t)h->cfg.stream;
+  cudaStreamSynchronize(s);
+  if (h->mode == MODE_PROCESS && h->comm) {
+    barrier(h);  // no peer may still be writing into our tables
+    cudaStreamSynchronize(s);
+    for (int k = 0; k < h->P; ++k)
+      if (!owns(h, k))
+        for (int i = 0; i < h->ntab; ++i)
+          if (h->tabs[k][i]) cudaIpcCloseMemHandle(h->tabs[k][i]);
+  }
+  for (int k = 0; k < h->P; ++k)
+    if (owns(h, k))
+      for (int i = 0; i < h->ntab; ++i) dev_free(h, h->tabs[k][i], h->tab_bytes);
   dev_free(h, h->red, 256);
+  if (h->barrier_buf) cudaFree(h->barrier_buf);
+  if (h->comm) ncclCommDestroy(h->comm);
   if (h->red_host) cudaFreeHost(h->red_host);
-  if (!h->cfg.free_) cudaStreamSynchronize((cudaStream_t)h->cfg.stream);
+  cudaStreamSynchronize(s);
   delete h;
+}
+
+static int exchange_ipc(lcsb_t* h) {
+  cudaStream_t s = (cudaStream_t)h->cfg.stream;
+  const size_t hb = sizeof(cudaIpcMemHandle_t);
+  const size_t mine = hb * (size_t)h->ntab;
+  char host_mine[sizeof(cudaIpcMemHandle_t) * kMaxGen];
+  for (int i = 0; i < h->ntab; ++i)
+    CU(h, cudaIpcGetMemHandle(reinterpret_cast<cudaIpcMemHandle_t*>(host_mine + i * hb),
+                              h->tabs[h->first][i]));
+  char* dbuf = nullptr;
+  CU(h, cudaMalloc(&dbuf, mine * (size_t)(h->P + 1)));
+  char* host_all = (char*)malloc(mine * (size_t)h->P);
+  int rc = LCSB_OK;
+  cudaError_t e = cudaMemcpyAsync(dbuf + mine * h->P, host_mine, mine, cudaMemcpyHostToDevice, s);
+  ncclResult_t r = ncclSuccess;
+  if (e == cudaSuccess)
+    r = ncclAllGather(dbuf + mine * h->P, dbuf, mine, ncclUint8, h->comm, s);
+  if (e == cudaSuccess && r == ncclSuccess)
+    e = cudaMemcpyAsync(host_all, dbuf, mine * h->P, cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  if (r != ncclSuccess)
+    rc = set_err(h, LCSB_ENCCL, "IPC handle all-gather: %s", ncclGetErrorString(r));
+  else if (e != cudaSuccess)
+    rc = set_err(h, LCSB_ECUDA, "IPC handle exchange: %s", cudaGetErrorString(e));
+  for (int k = 0; rc == LCSB_OK && k < h->P; ++k) {
+    if (owns(h, k)) continue;
+    for (int i = 0; i < h->ntab && rc == LCSB_OK; ++i) {
+      cudaIpcMemHandle_t mh;
+      memcpy(&mh, host_all + (size_t)k * mine + i * hb, hb);
+      e = cudaIpcOpenMemHandle(&h->tabs[k][i], mh, cudaIpcMemLazyEnablePeerAccess);
+      if (e != cudaSuccess)
+        rc = set_err(h, LCSB_ECUDA, "cudaIpcOpenMemHandle(shard %d): %s", k, cudaGetErrorString(e));
+    }
+  }
+  free(host_all);
+  cudaFree(dbuf);
+  return rc;
 }
 
 extern "C" int lcsb_create_ex(const lcsb_config* cfg, lcsb_t** out) {
@@ -215,7 +383,7 @@ extern "C" int lcsb_create_ex(const lcsb_config* cfg, lcsb_t** out) {
   if (!cfg->alloc && p.bytes > free_b)
     return set_err(nullptr, LCSB_ECAPACITY,
                    "needs %llu bytes of device memory for %d tables of %llu entries, %llu free",
-                   (unsigned long long)p.bytes, p.ntab, (unsigned long long)p.n_stored,
+                   (unsigned long long)p.bytes, p.ntab, (unsigned long long)p.n_local,
                    (unsigned long long)free_b);
 
   lcsb_t* h = new (std::nothrow) lcsb();
@@ -229,19 +397,44 @@ extern "C" int lcsb_create_ex(const lcsb_config* cfg, lcsb_t** out) {
   h->kernel = p.kernel;
   h->n_logical = p.n_logical;
   h->n_stored = p.n_stored;
+  h->n_local = p.n_local;
   h->esize = p.esize;
   h->ntab = p.ntab;
-  h->tab_bytes = (size_t)(p.n_stored * p.esize);
+  h->p = p.p;
+  h->P = p.P;
+  h->mode = p.mode;
+  h->first = (p.mode == MODE_PROCESS) ? cfg->shard : 0;
+  h->nown = (p.mode == MODE_PROCESS) ? 1 : p.P;
+  h->tab_bytes = (size_t)(p.n_local * p.esize);
+  h->bin2_variant = 0;  // auto (pick_bin2_variant)
+  if (const char* v = getenv("LCSB_BIN2_VARIANT")) h->bin2_variant = atoi(v);
   cudaStream_t s = (cudaStream_t)cfg->stream;
 
-  for (int i = 0; i < h->ntab; ++i) {
-    h->tab[i] = dev_alloc(h, h->tab_bytes);
-    if (!h->tab[i]) {
-      int code = set_err(nullptr, LCSB_ECAPACITY,
-                         "device allocation of table %d (%llu bytes) failed; %llu bytes needed",
-                         i, (unsigned long long)h->tab_bytes, (unsigned long long)p.bytes);
+  if (h->mode == MODE_PROCESS) {
+    ncclUniqueId id;
+    memcpy(&id, cfg->nccl_id, sizeof id);
+    ncclResult_t r = ncclCommInitRank(&h->comm, h->P, id, cfg->shard);
+    if (r != ncclSuccess) {
+      h->comm = nullptr;
       lcsb_destroy(h);
-      return code;
+      return set_err(nullptr, LCSB_ENCCL, "ncclCommInitRank failed: %s", ncclGetErrorString(r));
+    }
+    if (cudaMalloc(&h->barrier_buf, 256) != cudaSuccess) {
+      lcsb_destroy(h);
+      return set_err(nullptr, LCSB_ECAPACITY, "barrier buffer allocation failed");
+    }
+    cudaMemsetAsync(h->barrier_buf, 0, 256, s);
+  }
+  for (int k = h->first; k < h->first + h->nown; ++k) {
+    for (int i = 0; i < h->ntab; ++i) {
+      h->tabs[k][i] = dev_alloc(h, h->tab_bytes);
+      if (!h->tabs[k][i]) {
+        int code = set_err(nullptr, LCSB_ECAPACITY,
+                           "device allocation of table %d (%llu bytes) failed; %llu bytes needed",
+                           i, (unsigned long long)h->tab_bytes, (unsigned long long)p.bytes);
+        lcsb_destroy(h);
+        return code;
+      }
     }
   }
   h->red = (unsigned long long*)dev_alloc(h, 256);
@@ -250,16 +443,25 @@ extern "C" int lcsb_create_ex(const lcsb_config* cfg, lcsb_t** out) {
     return set_err(nullptr, LCSB_ECAPACITY, "scratch allocation failed");
   }
   // W_0 = 0: every live generation starts at zero
-  for (int i = 0; i < h->ntab; ++i) {
-    e = cudaMemsetAsync(h->tab[i], 0, h->tab_bytes, s);
-    if (e != cudaSuccess) {
+  for (int k = h->first; k < h->first + h->nown; ++k)
+    for (int i = 0; i < h->ntab; ++i) {
+      e = cudaMemsetAsync(h->tabs[k][i], 0, h->tab_bytes, s);
+      if (e != cudaSuccess) {
+        lcsb_destroy(h);
+        return set_err(nullptr, LCSB_ECUDA, "cudaMemsetAsync failed: %s", cudaGetErrorString(e));
+      }
+    }
+  if (h->mode == MODE_PROCESS) {
+    rc = exchange_ipc(h);
+    if (rc == LCSB_OK) rc = barrier(h);
+    if (rc != LCSB_OK) {
+      char msg[512];
+      snprintf(msg, sizeof msg, "%s", h->err);
       lcsb_destroy(h);
-      return set_err(nullptr, LCSB_ECUDA, "cudaMemsetAsync failed: %s", cudaGetErrorString(e));
+      return set_err(nullptr, rc, "%s", msg);
     }
   }
   h->cur = 0;
-  h->bin2_variant = 0;  // auto: the measured-best TMA variant that fits ell (pick_bin2_variant)
-  if (const char* v = getenv("LCSB_BIN2_VARIANT")) h->bin2_variant = atoi(v);
   *out = h;
   return LCSB_OK;
 }
@@ -277,26 +479,18 @@ extern "C" int lcsb_create(int32_t sigma, int32_t d, int32_t ell, int32_t dtype,
 extern "C" int lcsb_reset(lcsb_t* h) {
   if (!h) return set_err(nullptr, LCSB_EINVAL, "handle is NULL");
   CU(h, cudaSetDevice(h->device));
-  for (int i = 0; i < h->ntab; ++i)
-    CU(h, cudaMemsetAsync(h->tab[i], 0, h->tab_bytes, (cudaStream_t)h->cfg.stream));
+  int rc = barrier(h);  // nobody is still sweeping into our tables
+  if (rc != LCSB_OK) return rc;
+  for (int k = h->first; k < h->first + h->nown; ++k)
+    for (int i = 0; i < h->ntab; ++i)
+      CU(h, cudaMemsetAsync(h->tabs[k][i], 0, h->tab_bytes, (cudaStream_t)h->cfg.stream));
+  rc = barrier(h);  // everyone's tables are zero before anyone sweeps into them
+  if (rc != LCSB_OK) return rc;
   h->cur = 0;
   h->sweeps_done = 0;
   h->best_rho[0] = h->best_rho[1] = 0.0;
   h->best_sweep[0] = h->best_sweep[1] = 0;
   return LCSB_OK;
-}
-
-// Auto choice of the bin2 sweep variant, from the A/B measurements on B200 (DESIGN.md):
-// fp32 -> (M=6, 2 stages, direct stores) 97% of the measured copy bandwidth at l=17;
-// fp64 -> (M=5, 1 stage, smem-staged bulk stores) 97% at l=16; smaller tiles for small l,
-// and the register kernel below l=4.
-static int pick_bin2_variant(int dtype, int ell) {
-  static const int f32_chain[] = {13, 6, 8};
-  static const int f64_chain[] = {8, 3, 4};
-  const int* chain = (dtype == LCSB_F32) ? f32_chain : f64_chain;
-  for (int i = 0; i < 3; ++i)
-    if (ell >= bin2_tma_min_ell(dtype, chain[i])) return chain[i];
-  return 5;  // register kernel
 }
 
 static inline int slot_back(const lcsb_t* h, int k) {  // table k sweeps back from the newest
@@ -312,6 +506,20 @@ static void fill_generic(const lcsb_t* h, GenericArgs* a) {
   a->form = h->form;
 }
 
+static void fill_bin2(const lcsb_t* h, Bin2Args* a, int shard, int in_slot, int out_slot) {
+  memset(a, 0, sizeof *a);
+  a->src = h->tabs[shard][in_slot];
+  a->dst = out_slot >= 0 ? h->tabs[shard][out_slot] : nullptr;
+  a->ell = h->cfg.ell;
+  a->m = bin2_tile_m(h->cfg.ell);
+  a->shard_bits = h->p;
+  a->shard = shard;
+  for (int k = 0; k < h->P; ++k) {
+    a->src_shards[k] = h->tabs[k][in_slot];
+    a->dst_shards[k] = out_slot >= 0 ? h->tabs[k][out_slot] : nullptr;
+  }
+}
+
 extern "C" int lcsb_sweep(lcsb_t* h, int64_t n) {
   if (!h) return set_err(nullptr, LCSB_EINVAL, "handle is NULL");
   if (n < 0) return set_err(h, LCSB_EINVAL, "n must be >= 0");
@@ -319,41 +527,50 @@ extern "C" int lcsb_sweep(lcsb_t* h, int64_t n) {
   cudaStream_t s = (cudaStream_t)h->cfg.stream;
   for (int64_t it = 0; it < n; ++it) {
     const int out = (h->cur + 1) % h->ntab;  // the slot of the oldest table
-    cudaError_t e;
+    cudaError_t e = cudaSuccess;
     if (h->kernel == 2) {
-      Bin2Args a;
-      memset(&a, 0, sizeof a);
-      a.src = h->tab[h->cur];
-      a.dst = h->tab[out];
-      a.ell = h->cfg.ell;
-      a.m = bin2_tile_m(h->cfg.ell);
-      const int v = h->bin2_variant ? h->bin2_variant : pick_bin2_variant(h->cfg.dtype, h->cfg.ell);
-      const int min_ell = bin2_tma_min_ell(h->cfg.dtype, v);
-      if (min_ell > 0 && h->cfg.ell >= min_ell) {
-        e = launch_bin2_tma_sweep(a, h->cfg.dtype, v, s, h->sms);
-      } else {
-        a.grid_mult = (v == 5) ? 8 : 0;
-        e = launch_bin2_sweep(a, h->cfg.dtype, s, h->sms);
+      const int v = h->bin2_variant ? h->bin2_variant
+                                    : pick_bin2_variant(h->cfg.dtype, h->cfg.ell, h->p);
+      const int M = bin2_tma_m(h->cfg.dtype, v);
+      const bool tma_ok = M > 0 && h->cfg.ell >= M + 1 && h->p < h->cfg.ell - 1 - M &&
+                          (h->p == 0 || bin2_tma_direct(h->cfg.dtype, v));
+      if (!tma_ok && h->p > 0)
+        return set_err(h, LCSB_EINVAL, "variant %d cannot run sharded at ell = %d", v,
+                       h->cfg.ell);
+      for (int k = h->first; k < h->first + h->nown && e == cudaSuccess; ++k) {
+        Bin2Args a;
+        fill_bin2(h, &a, k, h->cur, out);
+        if (tma_ok) {
+          e = launch_bin2_tma_sweep(a, h->cfg.dtype, v, s, h->sms);
+        } else {
+          a.grid_mult = (v == 5) ? 8 : 0;
+          e = launch_bin2_sweep(a, h->cfg.dtype, s, h->sms);
+        }
+        h->launches += 1;
       }
     } else if (h->kernel == 3) {
       Q4Args a;
       memset(&a, 0, sizeof a);
-      a.g1 = h->tab[slot_back(h, 0)];
-      a.g2 = h->tab[slot_back(h, 1)];
-      a.dst = h->tab[out];
+      a.g1 = h->tabs[0][slot_back(h, 0)];
+      a.g2 = h->tabs[0][slot_back(h, 1)];
+      a.dst = h->tabs[0][out];
       a.ell = h->cfg.ell;
       e = launch_q4_sweep(a, h->cfg.dtype, s, h->sms);
+      h->launches += 1;
     } else {
       GenericArgs a;
       fill_generic(h, &a);
       for (int k = 1; k <= h->cfg.d; ++k)
-        a.src[k - 1] = (h->form == LCSB_FORM_KS) ? h->tab[slot_back(h, k - 1)] : h->tab[h->cur];
-      a.dst = h->tab[out];
+        a.src[k - 1] = (h->form == LCSB_FORM_KS) ? h->tabs[0][slot_back(h, k - 1)]
+                                                 : h->tabs[0][h->cur];
+      a.dst = h->tabs[0][out];
       e = launch_generic_sweep(a, h->cfg.dtype, s, h->sms);
+      h->launches += 1;
     }
     if (e != cudaSuccess)
       return set_err(h, LCSB_ECUDA, "sweep launch failed: %s", cudaGetErrorString(e));
-    h->launches += 1;
+    int rc = barrier(h);  // every shard's outputs are in place before the next sweep reads them
+    if (rc != LCSB_OK) return rc;
     h->cur = out;
     h->sweeps_done += 1;
   }
@@ -370,38 +587,53 @@ extern "C" int lcsb_bound(lcsb_t* h, lcsb_bound_t* out) {
   if (h->sweeps_done < 1) return set_err(h, LCSB_ESTATE, "lcsb_bound needs at least one sweep");
   CU(h, cudaSetDevice(h->device));
   cudaStream_t s = (cudaStream_t)h->cfg.stream;
-  const void* newest = h->tab[h->cur];
-  const void* prev = h->tab[slot_back(h, 1)];
+  const int prev = slot_back(h, 1);
   CU(h, launch_red_init(h->red, s));
-  CU(h, launch_rdiff(newest, prev, h->n_stored, h->cfg.dtype, h->red, s, h->sms));
+  h->launches += 1;
+  for (int k = h->first; k < h->first + h->nown; ++k) {
+    CU(h, launch_rdiff(h->tabs[k][h->cur], h->tabs[k][prev], h->n_local, h->cfg.dtype, h->red, s,
+                       h->sms));
+    h->launches += 1;
+  }
+  if (h->mode == MODE_PROCESS) {
+    NC(h, ncclAllReduce(h->red + 0, h->red + 0, 1, ncclUint64, ncclMax, h->comm, s));
+    NC(h, ncclAllReduce(h->red + 1, h->red + 1, 1, ncclUint64, ncclMin, h->comm, s));
+  }
   if (h->kernel == 2) {
-    Bin2Args a;
-    memset(&a, 0, sizeof a);
-    a.src = newest;
-    a.ell = h->cfg.ell;
-    a.m = bin2_tile_m(h->cfg.ell);
-    a.red_in = h->red;
-    a.red_out = h->red + 2;
-    CU(h, launch_bin2_wpass(a, h->cfg.dtype, s, h->sms));
+    const int M = bin2_tma_wpass_m(h->cfg.dtype, h->cfg.ell, h->p);
+    for (int k = h->first; k < h->first + h->nown; ++k) {
+      Bin2Args a;
+      fill_bin2(h, &a, k, h->cur, -1);
+      a.red_in = h->red;
+      a.red_out = h->red + 2;
+      if (M > 0)
+        CU(h, launch_bin2_tma_wpass(a, h->cfg.dtype, M, s, h->sms));
+      else
+        CU(h, launch_bin2_wpass(a, h->cfg.dtype, s, h->sms));
+      h->launches += 1;
+    }
   } else if (h->kernel == 3) {
     Q4Args a;
     memset(&a, 0, sizeof a);
-    a.g1 = newest;
-    a.g2 = newest;
+    a.g1 = h->tabs[0][h->cur];
+    a.g2 = h->tabs[0][h->cur];
     a.ell = h->cfg.ell;
     a.red_in = h->red;
     a.red_out = h->red + 2;
     CU(h, launch_q4_wpass(a, h->cfg.dtype, s, h->sms));
+    h->launches += 1;
   } else {
     GenericArgs a;
     fill_generic(h, &a);
-    for (int k = 1; k <= h->cfg.d; ++k) a.src[k - 1] = newest;
-    a.center = newest;
+    for (int k = 1; k <= h->cfg.d; ++k) a.src[k - 1] = h->tabs[0][h->cur];
+    a.center = h->tabs[0][h->cur];
     a.red_in = h->red;
     a.red_out = h->red + 2;
     CU(h, launch_generic_wpass(a, h->cfg.dtype, s, h->sms));
+    h->launches += 1;
   }
-  h->launches += 3;
+  if (h->mode == MODE_PROCESS)
+    NC(h, ncclAllReduce(h->red + 2, h->red + 2, 2, ncclUint64, ncclMax, h->comm, s));
   CU(h, cudaMemcpyAsync(h->red_host, h->red, kRedSlots * sizeof(unsigned long long),
                         cudaMemcpyDeviceToHost, s));
   CU(h, cudaStreamSynchronize(s));
@@ -448,7 +680,9 @@ static int readout(lcsb_t* h, int which, uint64_t first, uint64_t count, const u
   if (count == 0) return LCSB_OK;
   CU(h, cudaSetDevice(h->device));
   cudaStream_t s = (cudaStream_t)h->cfg.stream;
-  const void* tab = h->tab[slot_back(h, which)];
+  const int slot = slot_back(h, which);
+  const void* tabs[kMaxShards];
+  for (int k = 0; k < h->P; ++k) tabs[k] = h->tabs[k][slot];
   const uint64_t chunk = 1ull << 22;
   const uint64_t c0 = count < chunk ? count : chunk;
   double* dbuf = (double*)dev_alloc(h, c0 * sizeof(double));
@@ -465,14 +699,15 @@ static int readout(lcsb_t* h, int which, uint64_t first, uint64_t count, const u
     if (host_idx)
       e = cudaMemcpyAsync(ibuf, host_idx + off, c * sizeof(uint64_t), cudaMemcpyHostToDevice, s);
     if (e == cudaSuccess)
-      e = launch_expand(tab, h->cfg.dtype, h->symmetric, h->cfg.ell, first + off, c,
+      e = launch_expand(tabs, h->p, h->cfg.dtype, h->symmetric, h->cfg.ell, first + off, c,
                         host_idx ? ibuf : nullptr, dbuf, s);
     if (e == cudaSuccess) {
       h->launches += 1;
       e = cudaMemcpyAsync(host_dst + off, dbuf, c * sizeof(double), cudaMemcpyDeviceToHost, s);
     }
     if (e == cudaSuccess) e = cudaStreamSynchronize(s);
-    if (e != cudaSuccess) rc = set_err(h, LCSB_ECUDA, "table read-out failed: %s", cudaGetErrorString(e));
+    if (e != cudaSuccess)
+      rc = set_err(h, LCSB_ECUDA, "table read-out failed: %s", cudaGetErrorString(e));
   }
   dev_free(h, dbuf, c0 * sizeof(double));
   dev_free(h, ibuf, c0 * sizeof(uint64_t));
@@ -491,10 +726,11 @@ extern "C" int lcsb_table_gather(lcsb_t* h, int32_t which, const uint64_t* host_
 }
 
 extern "C" int64_t lcsb_sweeps_done(const lcsb_t* h) { return h ? h->sweeps_done : -1; }
+extern "C" int32_t lcsb_num_shards(const lcsb_t* h) { return h ? h->P : 0; }
 extern "C" uint64_t lcsb_num_states(const lcsb_t* h) { return h ? h->n_logical : 0; }
 extern "C" uint64_t lcsb_stored_states(const lcsb_t* h) { return h ? h->n_stored : 0; }
 extern "C" uint64_t lcsb_device_bytes(const lcsb_t* h) {
-  return h ? (uint64_t)h->tab_bytes * (uint64_t)h->ntab + 256 : 0;
+  return h ? (uint64_t)h->tab_bytes * (uint64_t)h->ntab * (uint64_t)h->nown + 256 : 0;
 }
 extern "C" int32_t lcsb_kernel_in_use(const lcsb_t* h) { return h ? h->kernel : 0; }
 extern "C" int64_t lcsb_launch_count(const lcsb_t* h) { return h ? h->launches : 0; }

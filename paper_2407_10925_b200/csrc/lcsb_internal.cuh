@@ -59,15 +59,56 @@ struct GenericArgs {
   unsigned long long* red_out;      // W mode: encoded max W slots
 };
 
+constexpr int kMaxShards = 8;
+
 struct Bin2Args {
-  const void* src;  // stored half table (2^(2l-1) entries)
-  void* dst;        // output half table (sweep mode)
+  const void* src;  // this shard's input half table (unsharded: the whole stored table)
+  void* dst;        // output half table (register kernel, unsharded)
   int ell;
-  int m;            // tile = 4^m Q1 outputs
+  int m;            // register kernel: tile = 4^m Q1 outputs
   int grid_mult;    // register kernel: 0 = co-resident grid, k > 0 = k CTAs per SM
+  int shard_bits;   // TMA kernel: 2^shard_bits shards (0 = unsharded)
+  int shard;        // TMA kernel: this shard
+  void* dst_shards[kMaxShards];        // output table of every shard (unsharded: [0] = dst)
+  const void* src_shards[kMaxShards];  // input table of every shard (W pass reads u there)
   const unsigned long long* red_in;
   unsigned long long* red_out;
 };
+
+// Sharding of the binary complement-folded half table over 2^p shards.
+// Stored index s (a_0 = 0): a_i at bit L-1-2i, b_i at bit L-2-2i.  Shard key
+// kappa_i = a_i ^ b_{i-1} ^ 1 (i = 1..p), kappa_1 most significant.  Local index = s with the
+// bits a_0..a_p removed (b_0..b_{p-1} become the top p bits).  Every adv_b window and every
+// output run of the bin2 kernels lies in one shard, contiguously, when p < l - 1 - M.
+__host__ __device__ inline uint32_t shard_of_stored(uint64_t s, int L, int p) {
+  uint32_t k = 0;
+  for (int i = 1; i <= p; ++i) {
+    const uint32_t ai = (uint32_t)(s >> (L - 1 - 2 * i)) & 1u;
+    const uint32_t bi1 = (uint32_t)(s >> (L - 2 * i)) & 1u;
+    k = (k << 1) | (ai ^ bi1 ^ 1u);
+  }
+  return k;
+}
+__host__ __device__ inline uint64_t local_of_stored(uint64_t s, int L, int p) {
+  if (p == 0) return s;
+  const int lowbits = L - 1 - 2 * p;
+  uint64_t top = 0;
+  for (int i = 0; i < p; ++i) top = (top << 1) | ((s >> (L - 2 - 2 * i)) & 1ull);
+  return (top << lowbits) | (s & ((1ull << lowbits) - 1));
+}
+__host__ __device__ inline uint64_t global_of_local(uint32_t shard, uint64_t loc, int L, int p) {
+  if (p == 0) return loc;
+  const int lowbits = L - 1 - 2 * p;
+  uint64_t s = loc & ((1ull << lowbits) - 1);
+  const uint64_t top = loc >> lowbits;
+  for (int i = 0; i < p; ++i) {
+    const uint64_t bi = (top >> (p - 1 - i)) & 1ull;
+    const uint64_t k = (shard >> (p - 1 - i)) & 1u;
+    s |= bi << (L - 2 - 2 * i);
+    s |= (k ^ bi ^ 1ull) << (L - 3 - 2 * i);  // a_{i+1}
+  }
+  return s;
+}
 
 struct Q4Args {
   const void* g1;   // table one sweep back (W pass: the newest table)
@@ -121,13 +162,19 @@ cudaError_t launch_bin2_wpass(const Bin2Args& a, int dtype, cudaStream_t s, int 
 cudaError_t launch_bin2_tma_sweep(const Bin2Args& a, int dtype, int variant, cudaStream_t s,
                                   int sms);
 int bin2_tma_min_ell(int dtype, int variant);
+int bin2_tma_m(int dtype, int variant);
+int bin2_tma_direct(int dtype, int variant);
+cudaError_t launch_bin2_tma_wpass(const Bin2Args& a, int dtype, int M, cudaStream_t s, int sms);
+int bin2_tma_wpass_m(int dtype, int ell, int p);
 cudaError_t launch_q4_sweep(const Q4Args& a, int dtype, cudaStream_t s, int sms);
 cudaError_t launch_q4_wpass(const Q4Args& a, int dtype, cudaStream_t s, int sms);
 int q4_min_ell();
 cudaError_t launch_red_init(unsigned long long* red, cudaStream_t s);
 cudaError_t launch_rdiff(const void* newest, const void* prev, uint64_t n, int dtype,
                          unsigned long long* red, cudaStream_t s, int sms);
-cudaError_t launch_expand(const void* tab, int dtype, int symmetric, int ell, uint64_t first,
-                          uint64_t count, const uint64_t* idx, double* out, cudaStream_t s);
+// tabs[k]: the table of shard k (unsharded: tabs[0]); p = log2(shards)
+cudaError_t launch_expand(const void* const* tabs, int p, int dtype, int symmetric, int ell,
+                          uint64_t first, uint64_t count, const uint64_t* idx, double* out,
+                          cudaStream_t s);
 
 }  // namespace lcsbk

@@ -32,7 +32,9 @@ class LcsbConfig(ctypes.Structure):
                 ("dtype", ctypes.c_int32), ("form", ctypes.c_int32), ("rmode", ctypes.c_int32),
                 ("symmetry", ctypes.c_int32), ("kernel", ctypes.c_int32),
                 ("stream", ctypes.c_void_p), ("alloc", _ALLOC_FN), ("free_", _FREE_FN),
-                ("alloc_ctx", ctypes.c_void_p)]
+                ("alloc_ctx", ctypes.c_void_p), ("shards", ctypes.c_int32),
+                ("shard", ctypes.c_int32), ("virtual_shards", ctypes.c_int32),
+                ("nccl_id", ctypes.c_void_p)]
 
 
 class LcsbBound(ctypes.Structure):
@@ -45,9 +47,11 @@ class LcsbBound(ctypes.Structure):
 
 # every symbol include/lcsb.h declares (checked by tests/test_abi.py)
 EXPORTS = ["lcsb_config_init", "lcsb_required_bytes", "lcsb_create", "lcsb_create_ex",
-           "lcsb_reset", "lcsb_sweep", "lcsb_bound", "lcsb_table", "lcsb_table_gather", "lcsb_sweeps_done",
+           "lcsb_reset", "lcsb_sweep", "lcsb_bound", "lcsb_table", "lcsb_table_gather",
+           "lcsb_nccl_unique_id", "lcsb_shard_locate", "lcsb_sweeps_done", "lcsb_num_shards",
            "lcsb_num_states", "lcsb_stored_states", "lcsb_device_bytes", "lcsb_kernel_in_use",
            "lcsb_launch_count", "lcsb_last_error", "lcsb_destroy"]
+NCCL_ID_BYTES = 128
 
 _LIB = None
 
@@ -86,7 +90,14 @@ def load_library():
     lib.lcsb_table.restype = ctypes.c_int
     lib.lcsb_table_gather.argtypes = [P, ctypes.c_int32, P, ctypes.c_uint64, P]
     lib.lcsb_table_gather.restype = ctypes.c_int
+    lib.lcsb_nccl_unique_id.argtypes = [P, ctypes.c_size_t]
+    lib.lcsb_nccl_unique_id.restype = ctypes.c_int
+    lib.lcsb_shard_locate.argtypes = [ctypes.c_int32, ctypes.c_int32, ctypes.c_uint64,
+                                      ctypes.POINTER(ctypes.c_int32),
+                                      ctypes.POINTER(ctypes.c_uint64)]
+    lib.lcsb_shard_locate.restype = ctypes.c_int
     for name, rt in [("lcsb_sweeps_done", ctypes.c_int64), ("lcsb_num_states", ctypes.c_uint64),
+                     ("lcsb_num_shards", ctypes.c_int32),
                      ("lcsb_stored_states", ctypes.c_uint64),
                      ("lcsb_device_bytes", ctypes.c_uint64),
                      ("lcsb_kernel_in_use", ctypes.c_int32),
@@ -137,7 +148,7 @@ class _TorchAllocator:
 
 
 def make_config(sigma, d, ell, dtype="f32", form="auto", rmode="max", symmetry=-1,
-                kernel="auto") -> LcsbConfig:
+                kernel="auto", shards=1, shard=0, virtual_shards=False) -> LcsbConfig:
     cfg = LcsbConfig()
     load_library().lcsb_config_init(ctypes.byref(cfg))
     cfg.sigma, cfg.d, cfg.ell = sigma, d, ell
@@ -146,12 +157,16 @@ def make_config(sigma, d, ell, dtype="f32", form="auto", rmode="max", symmetry=-
     cfg.rmode = {"max": LCSB_R_MAX, "min": LCSB_R_MIN}[rmode]
     cfg.symmetry = symmetry
     cfg.kernel = {"auto": LCSB_KERNEL_AUTO, "generic": LCSB_KERNEL_GENERIC}[kernel]
+    cfg.shards = int(shards)
+    cfg.shard = int(shard)
+    cfg.virtual_shards = 1 if virtual_shards else 0
     return cfg
 
 
 def lcsb_required_bytes(sigma, d, ell, dtype="f32", form="auto", symmetry=-1,
-                        kernel="auto") -> int:
-    cfg = make_config(sigma, d, ell, dtype, form, "max", symmetry, kernel)
+                        kernel="auto", shards=1, virtual_shards=True) -> int:
+    cfg = make_config(sigma, d, ell, dtype, form, "max", symmetry, kernel, shards, 0,
+                      virtual_shards)
     return int(load_library().lcsb_required_bytes(ctypes.byref(cfg)))
 
 
@@ -173,7 +188,8 @@ class Lcsb:
     """One handle: the device tables of one (sigma, d, l) run."""
 
     def __init__(self, sigma, d, ell, dtype="f32", form="auto", rmode="max", symmetry=-1,
-                 kernel="auto", stream=None, torch_allocator=True):
+                 kernel="auto", stream=None, torch_allocator=True, shards=1, shard=0,
+                 virtual_shards=False, nccl_id: bytes | None = None):
         import torch
         if not torch.cuda.is_available():
             raise LcsbError(4, "no CUDA device (the library has no CPU path)")
@@ -181,8 +197,15 @@ class Lcsb:
         self._lib = lib
         self.device = torch.cuda.current_device()
         self.stream = stream if stream is not None else torch.cuda.current_stream()
-        cfg = make_config(sigma, d, ell, dtype, form, rmode, symmetry, kernel)
+        cfg = make_config(sigma, d, ell, dtype, form, rmode, symmetry, kernel, shards, shard,
+                          virtual_shards)
         cfg.stream = ctypes.c_void_p(self.stream.cuda_stream)
+        self._nccl_id = None
+        if nccl_id is not None:
+            if len(nccl_id) != NCCL_ID_BYTES:
+                raise ValueError("nccl_id must be 128 bytes")
+            self._nccl_id = ctypes.create_string_buffer(bytes(nccl_id), NCCL_ID_BYTES)
+            cfg.nccl_id = ctypes.cast(self._nccl_id, ctypes.c_void_p)
         self._alloc = _TorchAllocator(self.device) if torch_allocator else None
         if self._alloc is not None:
             cfg.alloc = self._alloc.alloc_cb
@@ -227,6 +250,10 @@ class Lcsb:
         return int(self._lib.lcsb_sweeps_done(self._h))
 
     @property
+    def num_shards(self) -> int:
+        return int(self._lib.lcsb_num_shards(self._h))
+
+    @property
     def num_states(self) -> int:
         return int(self._lib.lcsb_num_states(self._h))
 
@@ -262,6 +289,21 @@ class Lcsb:
 
     def __exit__(self, *exc):
         self.destroy()
+
+
+def lcsb_nccl_unique_id() -> bytes:
+    buf = ctypes.create_string_buffer(NCCL_ID_BYTES)
+    _check(load_library().lcsb_nccl_unique_id(ctypes.cast(buf, ctypes.c_void_p), NCCL_ID_BYTES))
+    return buf.raw
+
+
+def lcsb_shard_locate(ell: int, shards: int, logical: int):
+    """(shard, local index) holding logical binary state `logical` (host-only plan)."""
+    sh = ctypes.c_int32()
+    loc = ctypes.c_uint64()
+    _check(load_library().lcsb_shard_locate(int(ell), int(shards), int(logical), ctypes.byref(sh),
+                                            ctypes.byref(loc)))
+    return int(sh.value), int(loc.value)
 
 
 # module-level names mirroring the C-ABI

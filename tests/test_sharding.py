@@ -1,0 +1,178 @@
+"""The sharded binary half table (config 5): host-side plan checks on CPU, a
+world-size-2 gloo test of the multi-process plumbing, and (GPU) virtual shards on one device
+bitwise equal to the unsharded run.
+
+The item / window / run geometry is re-derived here in plain Python from the paper's index
+arithmetic (Alg. 3/4; comp_eq PAPER.md:404-411), independently of the CUDA
+code, and checked against the library's host-side shard map (lcsb_shard_locate)."""
+import os
+import socket
+
+import numpy as np
+import pytest
+
+from tests.conftest import has_cuda
+
+from paper_2407_10925_b200 import lcsb as L
+
+
+def _pairswap(v):
+    return ((v & 0xAAAAAAAAAAAAAAAA) >> 1) | ((v & 0x5555555555555555) << 1)
+
+
+def _items(ell, M):
+    """Every tile pair {t, psi(t)} of the bin2 sweep: (tile, partner, windows, output runs)."""
+    Lb = 2 * ell
+    lmask = (1 << Lb) - 1
+    q1 = 1 << (Lb - 2)
+    A = 0xAAAAAAAAAAAAAAAA & lmask
+    B = 0x5555555555555555 & lmask
+    T = 1 << (2 * M)
+    out = []
+    for tau in range(1 << (Lb - 2 - 2 * M)):
+        x0 = q1 + tau * T
+        p0 = _pairswap(~x0 & lmask) & ~(T - 1)
+        taup = (p0 - q1) // T
+        if taup < tau:
+            continue
+        wb = (x0 & A) | ((x0 & B & ~q1) << 2)
+        wp = (p0 & A) | ((p0 & B & ~q1) << 2)
+        windows = [(wb, 2 * T), (wp, 2 * T)]
+        runs = [(x0, T), (wb >> 2, T // 2), (q1 - (wb >> 2) - T // 2, T // 2)]
+        if taup != tau:
+            runs += [(p0, T), (wp >> 2, T // 2), (q1 - (wp >> 2) - T // 2, T // 2)]
+        out.append((tau, taup, windows, runs))
+    return out
+
+
+@pytest.mark.parametrize("ell,shards", [(6, 2), (6, 4), (7, 8), (8, 2), (8, 8)])
+def test_shard_map_is_a_balanced_bijection(ell, shards):
+    H = 1 << (2 * ell - 1)
+    seen = np.zeros((shards, H // shards), dtype=np.int8)
+    for s in range(H):
+        k, loc = L.lcsb_shard_locate(ell, shards, s)
+        assert 0 <= k < shards and 0 <= loc < H // shards
+        seen[k, loc] += 1
+        # the complemented logical state lives in the same place
+        assert L.lcsb_shard_locate(ell, shards, (1 << (2 * ell)) - 1 - s) == (k, loc)
+    assert np.all(seen == 1)
+
+
+@pytest.mark.parametrize("ell,M,shards", [(8, 4, 2), (8, 4, 4), (9, 4, 8), (10, 5, 8)])
+def test_items_read_one_shard_and_write_contiguous_runs(ell, M, shards):
+    """Both windows of an item lie in ONE shard (so the sweep reads only local memory), the
+    item's owner is the key of its tile's leading characters, items partition the stored
+    table, and every output run is contiguous inside one shard."""
+    p = shards.bit_length() - 1
+    assert p < ell - 1 - M
+    H = 1 << (2 * ell - 1)
+    covered = np.zeros(H, dtype=np.int8)
+    written = np.zeros(H, dtype=np.int8)
+    per_shard = [0] * shards
+    h = ell - 1 - M
+    for tau, taup, windows, runs in _items(ell, M):
+        owners = set()
+        for base, n in windows:
+            locs = [L.lcsb_shard_locate(ell, shards, base + i) for i in (0, n // 2, n - 1)]
+            owners |= {k for k, _ in locs}
+            assert locs[-1][1] - locs[0][1] == n - 1  # contiguous in the shard
+        assert len(owners) == 1
+        owner = owners.pop()
+        # owner from the tile's first p character pairs: kappa_i = a_i ^ b_i ^ 1
+        key = 0
+        for i in range(1, p + 1):
+            a_i = (tau >> (2 * (h - i) + 1)) & 1
+            b_i = (tau >> (2 * (h - i))) & 1
+            key = (key << 1) | (a_i ^ b_i ^ 1)
+        assert key == owner
+        per_shard[owner] += 1
+        for base, n in windows if taup != tau else windows[:1]:
+            covered[base:base + n] += 1
+        for base, n in runs:
+            k0, l0 = L.lcsb_shard_locate(ell, shards, base)
+            k1, l1 = L.lcsb_shard_locate(ell, shards, base + n - 1)
+            assert k0 == k1 and l1 - l0 == n - 1
+            written[base:base + n] += 1
+    assert np.all(covered == 1)   # every stored entry is read by exactly one item
+    assert np.all(written == 1)   # and written by exactly one item
+    assert max(per_shard) - min(per_shard) <= max(per_shard) // 4 + 2  # balanced
+
+
+# ------------------------------------------------------------------ world size 2 on CPU (gloo)
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _gloo_worker(rank, world, port, ell, M, result_dir):
+    import torch.distributed as dist
+    from paper_2407_10925_b200 import dist as pdist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    # 1. the ncclUniqueId broadcast used by create_sharded (bytes from rank 0 on every rank)
+    fake = bytes(range(128)) if rank == 0 else None
+    got = pdist.broadcast_id(fake)
+    # 2. each rank's owned items (the kernel's enumeration, re-derived), gathered everywhere
+    p = world.bit_length() - 1
+    h = ell - 1 - M
+    mine = []
+    for tau, taup, windows, runs in _items(ell, M):
+        k, _ = L.lcsb_shard_locate(ell, world, windows[0][0])
+        if k == rank:
+            mine.append(tau)
+    allv = [None] * world
+    dist.all_gather_object(allv, mine)
+    np.save(os.path.join(result_dir, f"r{rank}.npy"),
+            np.array([got == bytes(range(128)), len(mine)] + sorted(sum(allv, []))))
+    dist.destroy_process_group()
+    del p, h
+
+
+def test_world_size_2_gloo_plumbing(tmp_path):
+    import torch.multiprocessing as mp
+    ell, M, world = 8, 4, 2
+    port = _free_port()
+    mp.spawn(_gloo_worker, args=(world, port, ell, M, str(tmp_path)), nprocs=world, join=True)
+    r0 = np.load(tmp_path / "r0.npy")
+    r1 = np.load(tmp_path / "r1.npy")
+    assert r0[0] == 1 and r1[0] == 1                      # id arrived intact on both ranks
+    all_items = sorted(t for t, *_ in _items(ell, M))
+    assert list(r0[2:]) == all_items == list(r1[2:])      # the ranks' items partition them
+    assert r0[1] + r1[1] == len(all_items) and r0[1] > 0 and r1[1] > 0
+
+
+# ------------------------------------------------------------------ GPU: virtual shards
+
+@pytest.mark.gpu
+@pytest.mark.skipif(not has_cuda(), reason="needs a CUDA device")
+@pytest.mark.parametrize("ell,shards,dtype", [(8, 2, "f32"), (8, 4, "f32"), (9, 8, "f32"),
+                                              (8, 2, "f64"), (9, 4, "f64"), (12, 2, "f32"),
+                                              (12, 8, "f32")])
+def test_virtual_shards_bitwise_equal_unsharded(ell, shards, dtype):
+    import torch
+    from paper_2407_10925_b200 import Lcsb
+    from oracle import ft_oracle as fo
+    a = Lcsb(2, 2, ell, dtype=dtype)
+    b = Lcsb(2, 2, ell, dtype=dtype, shards=shards, virtual_shards=True)
+    assert b.num_shards == shards
+    for k in (1, 2, 9):
+        a.sweep(k)
+        b.sweep(k)
+        assert np.array_equal(a.table(0), b.table(0))
+        assert np.array_equal(a.table(1), b.table(1))
+        ba, bb = a.bound(), b.bound()
+        assert (ba.R_max, ba.R_min, ba.E_at_Rmax, ba.E_at_Rmin) == \
+               (bb.R_max, bb.R_min, bb.E_at_Rmax, bb.E_at_Rmin)
+    if ell <= 9:
+        ref = fo.feasible_triplet(2, 2, ell, 12, form="two_array", dtype=dtype)
+        tab = b.table(0)
+        if dtype == "f32":
+            assert np.array_equal(tab, ref["table"])
+        else:
+            np.testing.assert_allclose(tab, ref["table"], rtol=1e-12)
+    a.destroy()
+    b.destroy()
+    torch.cuda.empty_cache()
