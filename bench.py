@@ -6,10 +6,11 @@ lcsb_sweep(S) + lcsb_bound.  metric = logical state-updates per second (sigma^(d
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--workload config4] [--impl ours|reference]
 
-Prints ONE JSON line on rank 0.  Under torchrun (N > 1) every rank runs its own replica of the
-workload (the sharded l = 18 path is not built yet), timed as the max over
-ranks.  `--impl reference` times the CPU oracle (oracle/, the reference arm of this tier) on a
-bounded sample of the same workload.
+Prints ONE JSON line on rank 0.  N = 1 runs config 4 (l = 17, the largest single-GPU config);
+under torchrun (N > 1) the ranks run config 5 (l = 18) with the half table sharded over the N
+GPUs (NCCL communicator + CUDA-IPC peer stores inside the library), timed as the
+max over ranks.  `--impl reference` times the CPU oracle (oracle/, the reference arm of this
+tier) on a bounded sample of the same workload.
 """
 from __future__ import annotations
 
@@ -31,6 +32,8 @@ WORKLOADS = {
     "config2": dict(sigma=3, d=3, ell=4, dtype="f64", form="ks", sweeps=300),
     "config3": dict(sigma=4, d=2, ell=8, dtype="f32", form="ks", sweeps=100),
     "config4": dict(sigma=2, d=2, ell=17, dtype="f32", form="two_array", sweeps=50),
+    # l = 18: 2 x 128 GiB fp32 half tables, sharded over the ranks (needs >= 2 GPUs)
+    "config5": dict(sigma=2, d=2, ell=18, dtype="f32", form="two_array", sweeps=30),
 }
 METRIC = "state-updates/sec per sweep (1/2/4/8 B200) and % of HBM roofline"
 SAMPLE_SEED = 0x240710925
@@ -121,7 +124,14 @@ def run_ours(args, w, ws, rank, local):
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     stream = torch.cuda.current_stream(dev)
-    h = Lcsb(w["sigma"], w["d"], w["ell"], dtype=w["dtype"], form=w["form"])
+
+    def make():
+        if ws > 1:
+            from paper_2407_10925_b200.dist import create_sharded
+            return create_sharded(w["ell"], dtype=w["dtype"], stream=stream)
+        return Lcsb(w["sigma"], w["d"], w["ell"], dtype=w["dtype"], form=w["form"])
+
+    h = make()
     S = w["sweeps"]
     n_logical = h.num_states
     stored = h.stored_states
@@ -164,10 +174,10 @@ def run_ours(args, w, ws, rank, local):
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         ms_total = float(t.item())
     ms_per_step = ms_total / args.steps
-    value = ws * n_logical * S / (ms_per_step / 1e3)
+    value = n_logical * S / (ms_per_step / 1e3)  # all ranks together (sharded: one table)
     # dominant kernel: the sweep; one launch per sweep on `stream`
     launch_ms = statistics.mean(sweep_ms) / S
-    alg_bytes = algorithmic_bytes_per_sweep(w, stored)
+    alg_bytes = algorithmic_bytes_per_sweep(w, stored // ws)  # per GPU (its shard)
     peak, peak_kind = _peaks()
     achieved = alg_bytes / (launch_ms / 1e3) / 1e9
     traffic = None
@@ -191,15 +201,20 @@ def run_ours(args, w, ws, rank, local):
     for rep in range(2):
         torch.cuda.synchronize()
         te = time.perf_counter()
-        h2 = Lcsb(w["sigma"], w["d"], w["ell"], dtype=w["dtype"], form=w["form"])
+        h2 = make()
         h2.sweep(S)
         be = h2.bound()
-        h2.table_gather(idx_pinned.numpy().view(np.uint64), out=out_pinned.numpy())
+        if rank == 0:
+            h2.table_gather(idx_pinned.numpy().view(np.uint64), out=out_pinned.numpy())
         h2.destroy()
         torch.cuda.synchronize()
         e2e_times.append(time.perf_counter() - te)
     e2e_s = min(e2e_times[1:] or e2e_times)
-    e2e_value = ws * n_logical * S / e2e_s
+    if ws > 1:
+        t = torch.tensor([e2e_s], device=dev, dtype=torch.float64)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        e2e_s = float(t.item())
+    e2e_value = n_logical * S / e2e_s
 
     res = {
         "metric": METRIC,
@@ -210,7 +225,7 @@ def run_ours(args, w, ws, rank, local):
         "warmup": args.warmup,
         "ms_per_step": ms_per_step,
         "higher_is_better": True,
-        "scaling": "weak",
+        "scaling": "strong" if ws > 1 else "weak",
         "vs_baseline": None,
         "dtype": "f64" if w["dtype"] == "f64" else "f32-storage/f64-arith",
         "data": "synthetic (the method's only input is (sigma, d, l) and W_0 = 0)",
@@ -219,19 +234,22 @@ def run_ours(args, w, ws, rank, local):
                         f"{w['form']} form, {w['dtype']} storage, {S} sweeps + 1 bound per step",
             "states": n_logical, "stored_states": stored, "sweeps_per_step": S,
             "kernel": kernel_name,
-            "parallelism": "replicas" if ws > 1 else "single-gpu",
+            "parallelism": f"sharded over {ws} GPUs (NCCL + CUDA IPC peer stores)" if ws > 1
+                           else "single-gpu",
             "l2_flush": "inputs larger than L2 (each table %.1f GiB vs 126 MB L2)"
                         % (stored * (4 if w["dtype"] == "f32" else 8) / 2**30)
             if stored * 4 > 2**27 else "working set L2-resident (latency-bound config)",
             "sweep_ms_per_launch": launch_ms,
             "bound": b.bound, "bound_at_Rmin": b.bound_at_Rmin,
             "sweeps_per_s": S / (ms_per_step / 1e3),
-            "sweep_only_state_updates_per_s": ws * n_logical / (launch_ms / 1e3),
+            "sweep_only_state_updates_per_s": n_logical / (launch_ms / 1e3),
         },
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic,
                      "peak_kind": peak_kind,
                      "algorithmic_bytes_per_launch": alg_bytes,
+                     "nvlink_bytes_per_launch": int((stored // ws) * (4 if w["dtype"] == "f32"
+                                                    else 8) * (1 - 1 / ws)),
                      "kernel": kernel_name + " sweep kernel"},
         "e2e": {"value": e2e_value, "unit": "state-updates/s",
                 "h2d_bytes_per_step": int(idx.nbytes),
@@ -290,14 +308,19 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--workload", default="config4", choices=sorted(WORKLOADS))
+    ap.add_argument("--workload", default=None, choices=sorted(WORKLOADS),
+                    help="default: config4 at N=1, config5 (sharded l=18) at N>1")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3  # timing rule: at least 3 warm-up steps
     ws, rank, local = _dist()
+    if args.workload is None:
+        args.workload = "config4" if ws == 1 else "config5"
     w = WORKLOADS[args.workload]
+    if ws > 1 and args.workload != "config5":
+        raise SystemExit("N > 1 runs the sharded config5 workload")
 
     if args.impl == "reference":
         if rank != 0:

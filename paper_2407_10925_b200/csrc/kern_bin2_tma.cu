@@ -150,6 +150,11 @@ __global__ void __launch_bounds__(kThreads) bin2_tma_kernel(Bin2Args a) {
     R1 = dec_ord(a.red_in[1]);
   }
 
+  // shard table pointers in shared memory (a dynamic index into the kernel-parameter array
+  // would force the parameter block through local memory)
+  __shared__ void* s_tabs[kMaxShards];
+  if (tid < kMaxShards)
+    s_tabs[tid] = WMODE ? const_cast<void*>(a.src_shards[tid]) : a.dst_shards[tid];
   uint64_t pc = 0, ptau = 0;  // producer cursor (thread 0 only)
   if (tid == 0) {
     for (int s = 0; s < S; ++s) mbar_init(&bars[s], 1);
@@ -186,7 +191,7 @@ __global__ void __launch_bounds__(kThreads) bin2_tma_kernel(Bin2Args a) {
     const bool self = (taup == ctau);
     const uint64_t wb = win_base(g, x0), wp = win_base(g, p0);
     // the six output runs (each lies in one shard)
-    void* const* tabs = WMODE ? const_cast<void* const*>(a.src_shards) : a.dst_shards;
+    void* const* tabs = s_tabs;
     T* runQ1 = out_ptr<T>(g, tabs, x0);
     T* runQ1p = out_ptr<T>(g, tabs, p0);
     T* runF = out_ptr<T>(g, tabs, wb >> 2);
