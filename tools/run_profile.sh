@@ -1,6 +1,7 @@
 #!/bin/bash
 # Profiling recipe (B200_PROFILING.md): plain run first, then the launch list of the bench
 # command, then one --set full capture of the sweep kernel.  Run under gpurun from the repo root.
+#   bash tools/run_profile.sh config4 bin2_tma_kernel
 set -u
 WL=${1:-config4}
 KREGEX=${2:-bin2_tma_kernel}
@@ -14,4 +15,4 @@ python tools/ncu_driver.py --workload $WL --sweeps 4 > $OUT/plain_driver_$WL.log
 ncu --set full --clock-control none --import-source on -k regex:$KREGEX -s 2 -c 1 \
     -o $OUT/prof_$WL -f python tools/ncu_driver.py --workload $WL --sweeps 4 \
     > $OUT/ncu_full_$WL.log 2>&1
-echo "profile rc=$?"
+echo "profile $WL rc=$?"
