@@ -49,14 +49,17 @@ __device__ __forceinline__ double q0_val(double v0, double v1, double v2, double
 
 constexpr int kThreads = 256;
 
-template <typename T, int M, int S, int OB>
+template <typename T, int M, int S, int OB, bool WMODE = false>
 struct TmaCfg {
   static constexpr uint32_t TT = 1u << (2 * M);   // Q1 outputs per tile
   static constexpr uint32_t WIN = 2 * TT;         // entries per adv_b window
   static constexpr uint32_t WIN_BYTES = WIN * sizeof(T);
   static constexpr uint32_t OUTN = 4 * TT;        // outputs per tile pair
+  // W pass: the stage also holds u at the item's outputs (Q1 tile t, and the row / mirror runs of
+  // both windows): 3T more entries
+  static constexpr uint32_t STAGE = 2 * WIN + (WMODE ? 3 * TT : 0);
   // OB = 0: outputs are stored straight from registers (sector-complete runs), no smem staging
-  static constexpr size_t SMEM = (size_t)S * 2 * WIN * sizeof(T) + OB * (size_t)OUTN * sizeof(T) +
+  static constexpr size_t SMEM = (size_t)S * STAGE * sizeof(T) + OB * (size_t)OUTN * sizeof(T) +
                                  (size_t)S * sizeof(uint64_t);
 };
 
@@ -119,15 +122,46 @@ __device__ __forceinline__ T* out_ptr(const Geo& g, void* const* tabs, uint64_t 
   return reinterpret_cast<T*>(tabs[sh]) + local_of_stored(global, g.L, g.p);
 }
 
+// Issue the TMA loads of one item into a stage (thread 0): the two adv_b windows and, for the
+// W pass on an unsharded table, u at the item's outputs.
 template <typename T, int M, int S, int OB, bool WMODE>
-__global__ void __launch_bounds__(kThreads) bin2_tma_kernel(Bin2Args a) {
-  using C = TmaCfg<T, M, S, OB>;
+__device__ __forceinline__ void issue_item(const Geo& g, uint64_t tau, T* buf, uint64_t* bar,
+                                           const T* src) {
+  using C = TmaCfg<T, M, S, OB, WMODE>;
+  constexpr uint32_t TT = C::TT, WIN = C::WIN;
+  constexpr uint32_t LOG = 2 * M;
+  uint64_t x0, p0, taup;
+  tile_info(g, tau, LOG, x0, p0, taup);
+  const uint64_t wb = win_base(g, x0), wp = win_base(g, p0);
+  const bool with_u = WMODE && g.p == 0;
+  const bool self = (taup == tau);
+  uint32_t bytes = 2 * C::WIN_BYTES;
+  if (with_u) bytes += (self ? 2 : 3) * TT * (uint32_t)sizeof(T);
+  mbar_expect_tx(bar, bytes);
+  tma_load_1d(buf, src + local_of_stored(wb, g.L, g.p), C::WIN_BYTES, bar);
+  tma_load_1d(buf + WIN, src + local_of_stored(wp, g.L, g.p), C::WIN_BYTES, bar);
+  if (with_u) {
+    T* u = buf + 2 * WIN;
+    constexpr uint32_t HB = TT / 2 * sizeof(T);
+    tma_load_1d(u, src + x0, TT * sizeof(T), bar);
+    tma_load_1d(u + TT, src + (wb >> 2), HB, bar);
+    tma_load_1d(u + TT + TT / 2, src + (g.q1 - (wb >> 2) - TT / 2), HB, bar);
+    if (!self) {
+      tma_load_1d(u + 2 * TT, src + (wp >> 2), HB, bar);
+      tma_load_1d(u + 2 * TT + TT / 2, src + (g.q1 - (wp >> 2) - TT / 2), HB, bar);
+    }
+  }
+}
+
+template <typename T, int M, int S, int OB, bool WMODE, int MINB = 1>
+__global__ void __launch_bounds__(kThreads, MINB) bin2_tma_kernel(Bin2Args a) {
+  using C = TmaCfg<T, M, S, OB, WMODE>;
   using V2 = typename Vec<T>::v2;
   constexpr uint32_t TT = C::TT, WIN = C::WIN, OUTN = C::OUTN;
   constexpr uint32_t LOG = 2 * M;
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  T* in = reinterpret_cast<T*>(smem_raw);                 // [S][2][WIN]
-  T* out = in + (size_t)S * 2 * WIN;                      // [OB][OUTN] (OB may be 0)
+  T* in = reinterpret_cast<T*>(smem_raw);                 // [S][STAGE]
+  T* out = in + (size_t)S * C::STAGE;                     // [OB][OUTN] (OB may be 0)
   uint64_t* bars = reinterpret_cast<uint64_t*>(out + OB * OUTN);
 
   Geo g;
@@ -164,13 +198,7 @@ __global__ void __launch_bounds__(kThreads) bin2_tma_kernel(Bin2Args a) {
   if (tid == 0) {
     pc = next_item(g, blockIdx.x, G, LOG, ptau);
     for (int s = 0; s < S && pc < g.nloc; ++s) {
-      uint64_t x0, p0, taup;
-      tile_info(g, ptau, LOG, x0, p0, taup);
-      T* buf = in + (size_t)s * 2 * WIN;
-      mbar_expect_tx(&bars[s], 2 * C::WIN_BYTES);
-      tma_load_1d(buf, src + local_of_stored(win_base(g, x0), g.L, g.p), C::WIN_BYTES, &bars[s]);
-      tma_load_1d(buf + WIN, src + local_of_stored(win_base(g, p0), g.L, g.p), C::WIN_BYTES,
-                  &bars[s]);
+      issue_item<T, M, S, OB, WMODE>(g, ptau, in + (size_t)s * C::STAGE, &bars[s], src);
       pc = next_item(g, pc + G, G, LOG, ptau);
     }
   }
@@ -181,7 +209,9 @@ __global__ void __launch_bounds__(kThreads) bin2_tma_kernel(Bin2Args a) {
        cc = next_item(g, cc + G, G, LOG, ctau), ++i) {
     const uint32_t s = i % S;
     const uint32_t parity = (i / S) & 1u;
-    T* buf = in + (size_t)s * 2 * WIN;
+    T* buf = in + (size_t)s * C::STAGE;
+    const T* us = buf + 2 * WIN;  // W pass, unsharded: u at this item's outputs
+    const bool u_in_smem = WMODE && g.p == 0;
     T* ob = OB ? out + (size_t)(i % (OB ? OB : 1)) * OUTN : nullptr;
     if (OB && tid == 0) bulk_wait_read<(OB ? OB - 1 : 0)>();  // stores from ob OB items ago have read it
     mbar_wait(&bars[s], parity);
@@ -211,7 +241,7 @@ __global__ void __launch_bounds__(kThreads) bin2_tma_kernel(Bin2Args a) {
       if (bp > v) v = bp;
       if (WMODE) {
         // W = (u + R) - F'(u); W(psi x) = W(x) exactly (both entries hold the same value)
-        const double ux = (double)runQ1[o];
+        const double ux = u_in_smem ? (double)us[o] : (double)runQ1[o];
         wm0 = fmax(wm0, (ux + R0) - v);
         wm1 = fmax(wm1, (ux + R1) - v);
       } else if (OB) {
@@ -235,7 +265,9 @@ __global__ void __launch_bounds__(kThreads) bin2_tma_kernel(Bin2Args a) {
       T* rf = half ? runFp : runF;
       T* rm = half ? runMp : runM;
       if (WMODE) {
-        const double uf = (double)rf[r], um = (double)rm[TT / 2 - 1 - r];
+        const double uf = u_in_smem ? (double)us[TT + half * TT + r] : (double)rf[r];
+        const double um = u_in_smem ? (double)us[TT + half * TT + TT / 2 + (TT / 2 - 1 - r)]
+                                    : (double)rm[TT / 2 - 1 - r];
         wm0 = fmax(wm0, (uf + R0) - fwd);
         wm1 = fmax(wm1, (uf + R1) - fwd);
         wm0 = fmax(wm0, (um + R0) - mir);
@@ -266,13 +298,7 @@ __global__ void __launch_bounds__(kThreads) bin2_tma_kernel(Bin2Args a) {
         bulk_commit();
       }
       if (pc < g.nloc) {  // refill the stage this item just vacated
-        uint64_t px0, pp0, ptaup;
-        tile_info(g, ptau, LOG, px0, pp0, ptaup);
-        mbar_expect_tx(&bars[s], 2 * C::WIN_BYTES);
-        tma_load_1d(buf, src + local_of_stored(win_base(g, px0), g.L, g.p), C::WIN_BYTES,
-                    &bars[s]);
-        tma_load_1d(buf + WIN, src + local_of_stored(win_base(g, pp0), g.L, g.p), C::WIN_BYTES,
-                    &bars[s]);
+        issue_item<T, M, S, OB, WMODE>(g, ptau, buf, &bars[s], src);
         pc = next_item(g, pc + G, G, LOG, ptau);
       }
     }
@@ -282,16 +308,17 @@ __global__ void __launch_bounds__(kThreads) bin2_tma_kernel(Bin2Args a) {
   if (WMODE) block_max2_to(wm0, wm1, a.red_out);
 }
 
-template <typename T, int M, int S, int OB, bool WMODE>
+template <typename T, int M, int S, int OB, bool WMODE, int MINB = 1>
 cudaError_t launch_tma(const Bin2Args& a, cudaStream_t s, int sms) {
-  using C = TmaCfg<T, M, S, OB>;
+  using C = TmaCfg<T, M, S, OB, WMODE>;
   static uint64_t cap = 0;
   if (cap == 0) {
-    cudaError_t e = cudaFuncSetAttribute(bin2_tma_kernel<T, M, S, OB, WMODE>,
+    cudaError_t e = cudaFuncSetAttribute(bin2_tma_kernel<T, M, S, OB, WMODE, MINB>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
     if (e != cudaSuccess) return e;
     int per_sm = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, bin2_tma_kernel<T, M, S, OB, WMODE>,
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm,
+                                                      bin2_tma_kernel<T, M, S, OB, WMODE, MINB>,
                                                       kThreads, C::SMEM) != cudaSuccess ||
         per_sm < 1) {
       cudaGetLastError();
@@ -303,28 +330,32 @@ cudaError_t launch_tma(const Bin2Args& a, cudaStream_t s, int sms) {
   const uint64_t nloc = (1ull << (2 * (a.ell - 1 - M))) >> a.shard_bits;
   uint64_t blocks = cap < nloc ? cap : nloc;
   if (blocks < 1) blocks = 1;
-  bin2_tma_kernel<T, M, S, OB, WMODE><<<(unsigned)blocks, kThreads, C::SMEM, s>>>(a);
+  bin2_tma_kernel<T, M, S, OB, WMODE, MINB><<<(unsigned)blocks, kThreads, C::SMEM, s>>>(a);
   return cudaGetLastError();
 }
 
 struct VariantDesc {
-  int m, s, ob;
+  int m, s, ob, mb;  // tile exponent, stages, out buffers, min CTAs/SM (register cap)
 };
 // (M, S, OB) per variant id, fp32 and fp64 storage
 constexpr VariantDesc kF32[] = {{0, 0, 0}, {5, 4, 2}, {4, 8, 2}, {5, 2, 2}, {4, 4, 2}, {0, 0, 0},
                                 {5, 1, 2}, {5, 3, 2}, {4, 2, 2}, {5, 2, 1}, {5, 1, 1}, {6, 1, 1},
-                                {6, 1, 0}, {6, 2, 0}, {5, 2, 0}, {5, 4, 0}, {6, 3, 0}, {4, 2, 0}};
+                                {6, 1, 0}, {6, 2, 0}, {5, 2, 0}, {5, 4, 0}, {6, 3, 0}, {4, 2, 0},
+                                {6, 1, 0, 3}, {5, 2, 0, 3}, {5, 1, 0, 4}};
 constexpr VariantDesc kF64[] = {{0, 0, 0}, {4, 4, 2}, {4, 8, 2}, {4, 2, 2}, {3, 8, 2}, {0, 0, 0},
                                 {4, 1, 2}, {4, 3, 2}, {5, 1, 1}, {4, 2, 1}, {4, 1, 1}, {3, 4, 2},
-                                {5, 1, 0}, {5, 2, 0}, {4, 2, 0}, {4, 4, 0}, {5, 3, 0}, {3, 2, 0}};
-constexpr int kNumVariants = 18;
+                                {5, 1, 0}, {5, 2, 0}, {4, 2, 0}, {4, 4, 0}, {5, 3, 0}, {3, 2, 0},
+                                {5, 1, 0, 3}, {4, 2, 0, 3}, {5, 1, 1, 3}};
+constexpr int kNumVariants = 21;
 
 }  // namespace
 
 cudaError_t launch_bin2_tma_sweep(const Bin2Args& a, int dtype, int variant, cudaStream_t s,
                                   int sms) {
 #define LCSB_V(T, M, S, OB) \
-  if (d.m == M && d.s == S && d.ob == OB) return launch_tma<T, M, S, OB, false>(a, s, sms);
+  if (d.m == M && d.s == S && d.ob == OB && d.mb <= 1) return launch_tma<T, M, S, OB, false>(a, s, sms);
+#define LCSB_VB(T, M, S, OB, MB) \
+  if (d.m == M && d.s == S && d.ob == OB && d.mb == MB) return launch_tma<T, M, S, OB, false, MB>(a, s, sms);
   if (variant <= 0 || variant >= kNumVariants) return cudaErrorInvalidValue;
   if (dtype == LCSB_F32) {
     const VariantDesc d = kF32[variant];
@@ -332,14 +363,17 @@ cudaError_t launch_bin2_tma_sweep(const Bin2Args& a, int dtype, int variant, cud
     LCSB_V(float, 5, 1, 2) LCSB_V(float, 5, 3, 2) LCSB_V(float, 4, 2, 2) LCSB_V(float, 5, 2, 1)
     LCSB_V(float, 5, 1, 1) LCSB_V(float, 6, 1, 1) LCSB_V(float, 6, 1, 0) LCSB_V(float, 6, 2, 0)
     LCSB_V(float, 5, 2, 0) LCSB_V(float, 5, 4, 0) LCSB_V(float, 6, 3, 0) LCSB_V(float, 4, 2, 0)
+    LCSB_VB(float, 6, 1, 0, 3) LCSB_VB(float, 5, 2, 0, 3) LCSB_VB(float, 5, 1, 0, 4)
   } else {
     const VariantDesc d = kF64[variant];
     LCSB_V(double, 4, 4, 2) LCSB_V(double, 4, 8, 2) LCSB_V(double, 4, 2, 2) LCSB_V(double, 3, 8, 2)
     LCSB_V(double, 4, 1, 2) LCSB_V(double, 4, 3, 2) LCSB_V(double, 5, 1, 1) LCSB_V(double, 4, 2, 1)
     LCSB_V(double, 4, 1, 1) LCSB_V(double, 3, 4, 2) LCSB_V(double, 5, 1, 0) LCSB_V(double, 5, 2, 0)
     LCSB_V(double, 4, 2, 0) LCSB_V(double, 4, 4, 0) LCSB_V(double, 5, 3, 0) LCSB_V(double, 3, 2, 0)
+    LCSB_VB(double, 5, 1, 0, 3) LCSB_VB(double, 4, 2, 0, 3) LCSB_VB(double, 5, 1, 1, 3)
   }
 #undef LCSB_V
+#undef LCSB_VB
   return cudaErrorInvalidValue;
 }
 

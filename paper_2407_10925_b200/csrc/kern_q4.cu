@@ -61,13 +61,15 @@ __device__ __forceinline__ double sum4(const T* p, double sh) {
   return r;
 }
 
-template <typename T, int M, int S>
+template <typename T, int M, int S, bool WMODE = false>
 struct Q4Cfg {
   static constexpr uint32_t TT = 1u << (4 * M);  // tails per unit
   static constexpr uint32_t PR = 16 * TT;        // g2 entries (rows) per unit
   static constexpr uint32_t WB = 4 * TT;         // g1 entries per adv_b window
   static constexpr uint32_t UNIT = PR + 4 * WB;  // entries staged per unit
-  static constexpr uint32_t STAGE = 2 * UNIT;
+  // W pass: also u at the unit pair's 32 output runs (16 head pairs x T tails, per side)
+  static constexpr uint32_t UOUT = WMODE ? 2 * 16 * TT : 0;
+  static constexpr uint32_t STAGE = 2 * UNIT + UOUT;
   static constexpr size_t SMEM = (size_t)S * STAGE * sizeof(T) + (size_t)S * sizeof(uint64_t);
 };
 
@@ -87,10 +89,10 @@ __device__ __forceinline__ uint64_t q4_next(const Q4Geo& g, uint64_t c, uint64_t
   return c;
 }
 
-template <typename T, int M, int S>
+template <typename T, int M, int S, bool WMODE>
 __device__ __forceinline__ void q4_issue(const Q4Geo& g, uint64_t u, T* buf, uint64_t* bar,
                                          const T* g1, const T* g2) {
-  using C = Q4Cfg<T, M, S>;
+  using C = Q4Cfg<T, M, S, WMODE>;
   mbar_expect_tx(bar, C::STAGE * (uint32_t)sizeof(T));
 #pragma unroll
   for (int side = 0; side < 2; ++side) {
@@ -104,12 +106,21 @@ __device__ __forceinline__ void q4_issue(const Q4Geo& g, uint64_t u, T* buf, uin
       const uint64_t yb = ((uint64_t)h << (g.tail_bits + 2)) | low;
       tma_load_1d(ub + C::PR + h * C::WB, g1 + yb, C::WB * sizeof(T), bar);
     }
+    if (WMODE) {  // u (= g1, the newest table) at the 16 output runs of this side
+      T* uo = buf + 2 * C::UNIT + side * 16 * C::TT;
+#pragma unroll
+      for (int hh = 0; hh < 16; ++hh) {
+        const uint64_t hx = ((uint64_t)(hh >> 2) << (g.tail_bits + 2)) |
+                            ((uint64_t)(hh & 3) << g.tail_bits);
+        tma_load_1d(uo + hh * C::TT, g1 + (hx | t0), C::TT * sizeof(T), bar);
+      }
+    }
   }
 }
 
 template <typename T, int M, int S, bool WMODE>
 __global__ void __launch_bounds__(kThreads) q4_kernel(Q4Args a) {
-  using C = Q4Cfg<T, M, S>;
+  using C = Q4Cfg<T, M, S, WMODE>;
   using V4 = typename V4T<T>::type;
   constexpr uint32_t TT = C::TT;
   extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -143,7 +154,7 @@ __global__ void __launch_bounds__(kThreads) q4_kernel(Q4Args a) {
   if (tid == 0) {
     pc = q4_next<M>(g, blockIdx.x, G);
     for (int s = 0; s < S && pc < g.nunits; ++s) {
-      q4_issue<T, M, S>(g, pc, in + (size_t)s * C::STAGE, &bars[s], g1, g2);
+      q4_issue<T, M, S, WMODE>(g, pc, in + (size_t)s * C::STAGE, &bars[s], g1, g2);
       pc = q4_next<M>(g, pc + G, G);
     }
   }
@@ -211,8 +222,13 @@ __global__ void __launch_bounds__(kThreads) q4_kernel(Q4Args a) {
               if (!self) dst[xs] = (T)vs;
             } else {
               const double twoR = 2.0 * R[m];
-              wmax[m] = fmax(wmax[m], ((double)g1[xu] + twoR) - vu);
-              if (!self) wmax[m] = fmax(wmax[m], ((double)g1[xs] + twoR) - vs);
+              const T* uo = buf + 2 * C::UNIT;
+              const double uu = (double)uo[(ha * 4 + hb) * TT + i];
+              const double usv = (double)uo[16 * TT + (ha * 4 + hb) * TT + i2];
+              wmax[m] = fmax(wmax[m], (uu + twoR) - vu);
+              if (!self) wmax[m] = fmax(wmax[m], (usv + twoR) - vs);
+              (void)xu;
+              (void)xs;
             }
           }
         }
@@ -220,7 +236,7 @@ __global__ void __launch_bounds__(kThreads) q4_kernel(Q4Args a) {
     }
     __syncthreads();
     if (tid == 0 && pc < g.nunits) {
-      q4_issue<T, M, S>(g, pc, buf, &bars[s], g1, g2);
+      q4_issue<T, M, S, WMODE>(g, pc, buf, &bars[s], g1, g2);
       pc = q4_next<M>(g, pc + G, G);
     }
   }
@@ -229,7 +245,7 @@ __global__ void __launch_bounds__(kThreads) q4_kernel(Q4Args a) {
 
 template <typename T, int M, int S, bool WMODE>
 cudaError_t launch_q4_t(const Q4Args& a, cudaStream_t s, int sms) {
-  using C = Q4Cfg<T, M, S>;
+  using C = Q4Cfg<T, M, S, WMODE>;
   static uint64_t cap = 0;
   if (cap == 0) {
     cudaError_t e = cudaFuncSetAttribute(q4_kernel<T, M, S, WMODE>,
