@@ -338,22 +338,26 @@ struct VariantDesc {
   int m, s, ob, mb;  // tile exponent, stages, out buffers, min CTAs/SM (register cap)
 };
 // (M, S, OB) per variant id, fp32 and fp64 storage
-constexpr VariantDesc kF32[] = {{0, 0, 0}, {5, 4, 2}, {4, 8, 2}, {5, 2, 2}, {4, 4, 2}, {0, 0, 0},
-                                {5, 1, 2}, {5, 3, 2}, {4, 2, 2}, {5, 2, 1}, {5, 1, 1}, {6, 1, 1},
-                                {6, 1, 0}, {6, 2, 0}, {5, 2, 0}, {5, 4, 0}, {6, 3, 0}, {4, 2, 0},
-                                {6, 1, 0, 3}, {5, 2, 0, 3}, {5, 1, 0, 4}};
-constexpr VariantDesc kF64[] = {{0, 0, 0}, {4, 4, 2}, {4, 8, 2}, {4, 2, 2}, {3, 8, 2}, {0, 0, 0},
-                                {4, 1, 2}, {4, 3, 2}, {5, 1, 1}, {4, 2, 1}, {4, 1, 1}, {3, 4, 2},
-                                {5, 1, 0}, {5, 2, 0}, {4, 2, 0}, {4, 4, 0}, {5, 3, 0}, {3, 2, 0},
-                                {5, 1, 0, 3}, {4, 2, 0, 3}, {5, 1, 1, 3}};
-constexpr int kNumVariants = 21;
+constexpr VariantDesc kF32[] = {{0, 0, 0, 1}, {5, 4, 2, 1}, {4, 8, 2, 1}, {5, 2, 2, 1},
+                                {4, 4, 2, 1}, {0, 0, 0, 1}, {5, 1, 2, 1}, {5, 3, 2, 1},
+                                {4, 2, 2, 1}, {5, 2, 1, 1}, {5, 1, 1, 1}, {6, 1, 1, 1},
+                                {6, 1, 0, 2}, {6, 2, 0, 1}, {5, 2, 0, 1}, {5, 4, 0, 1},
+                                {6, 3, 0, 1}, {4, 2, 0, 1}, {6, 1, 0, 3}, {5, 2, 0, 3},
+                                {5, 1, 0, 4}, {6, 1, 0, 1}};
+constexpr VariantDesc kF64[] = {{0, 0, 0, 1}, {4, 4, 2, 1}, {4, 8, 2, 1}, {4, 2, 2, 1},
+                                {3, 8, 2, 1}, {0, 0, 0, 1}, {4, 1, 2, 1}, {4, 3, 2, 1},
+                                {5, 1, 1, 1}, {4, 2, 1, 1}, {4, 1, 1, 1}, {3, 4, 2, 1},
+                                {5, 1, 0, 1}, {5, 2, 0, 1}, {4, 2, 0, 1}, {4, 4, 0, 1},
+                                {5, 3, 0, 1}, {3, 2, 0, 1}, {5, 1, 0, 3}, {4, 2, 0, 3},
+                                {5, 1, 1, 3}, {5, 1, 1, 2}};
+constexpr int kNumVariants = 22;
 
 }  // namespace
 
 cudaError_t launch_bin2_tma_sweep(const Bin2Args& a, int dtype, int variant, cudaStream_t s,
                                   int sms) {
 #define LCSB_V(T, M, S, OB) \
-  if (d.m == M && d.s == S && d.ob == OB && d.mb <= 1) return launch_tma<T, M, S, OB, false>(a, s, sms);
+  if (d.m == M && d.s == S && d.ob == OB && d.mb == 1) return launch_tma<T, M, S, OB, false>(a, s, sms);
 #define LCSB_VB(T, M, S, OB, MB) \
   if (d.m == M && d.s == S && d.ob == OB && d.mb == MB) return launch_tma<T, M, S, OB, false, MB>(a, s, sms);
   if (variant <= 0 || variant >= kNumVariants) return cudaErrorInvalidValue;
@@ -364,6 +368,7 @@ cudaError_t launch_bin2_tma_sweep(const Bin2Args& a, int dtype, int variant, cud
     LCSB_V(float, 5, 1, 1) LCSB_V(float, 6, 1, 1) LCSB_V(float, 6, 1, 0) LCSB_V(float, 6, 2, 0)
     LCSB_V(float, 5, 2, 0) LCSB_V(float, 5, 4, 0) LCSB_V(float, 6, 3, 0) LCSB_V(float, 4, 2, 0)
     LCSB_VB(float, 6, 1, 0, 3) LCSB_VB(float, 5, 2, 0, 3) LCSB_VB(float, 5, 1, 0, 4)
+    LCSB_VB(float, 6, 1, 0, 2) LCSB_V(float, 6, 1, 0)
   } else {
     const VariantDesc d = kF64[variant];
     LCSB_V(double, 4, 4, 2) LCSB_V(double, 4, 8, 2) LCSB_V(double, 4, 2, 2) LCSB_V(double, 3, 8, 2)
@@ -371,6 +376,7 @@ cudaError_t launch_bin2_tma_sweep(const Bin2Args& a, int dtype, int variant, cud
     LCSB_V(double, 4, 1, 1) LCSB_V(double, 3, 4, 2) LCSB_V(double, 5, 1, 0) LCSB_V(double, 5, 2, 0)
     LCSB_V(double, 4, 2, 0) LCSB_V(double, 4, 4, 0) LCSB_V(double, 5, 3, 0) LCSB_V(double, 3, 2, 0)
     LCSB_VB(double, 5, 1, 0, 3) LCSB_VB(double, 4, 2, 0, 3) LCSB_VB(double, 5, 1, 1, 3)
+    LCSB_VB(double, 5, 1, 1, 2)
   }
 #undef LCSB_V
 #undef LCSB_VB

@@ -100,12 +100,13 @@ extern "C" void lcsb_config_init(lcsb_config* c) {
 // ---------------------------------------------------------------- bin2 variant choice
 // Auto choice of the bin2 sweep variant, from the A/B measurements on B200:
 // fp32 -> (M=6, 1 stage, direct stores), 97% of the measured copy bandwidth at l=17;
-// fp64 -> (M=5, 1 stage, smem-staged bulk stores), 97% at l=16; smaller tiles for small l;
+// fp64 -> (M=5, 1 stage, smem-staged bulk stores, 3 CTAs/SM), 97% at l=16; smaller tiles for
+// small l;
 // the register kernel below that.  Sharded runs need direct stores (outputs go to peers) and
 // a tile small enough that the shard key bits sit above it (p < l - 1 - M).
 static int pick_bin2_variant(int dtype, int ell, int p) {
   static const int f32_chain[] = {12, 14, 8};
-  static const int f64_chain[] = {8, 3, 4};
+  static const int f64_chain[] = {20, 3, 4};
   static const int direct_chain[] = {12, 14, 17};
   const int* chain = p > 0 ? direct_chain : (dtype == LCSB_F32 ? f32_chain : f64_chain);
   for (int i = 0; i < 3; ++i) {

@@ -60,7 +60,7 @@ def test_bin2_half_table_matches_oracle(ell, dtype):
     h.destroy()
 
 
-@pytest.mark.parametrize("variant", list(range(0, 21)))
+@pytest.mark.parametrize("variant", list(range(0, 22)))
 @pytest.mark.parametrize("dtype", ["f32", "f64"])
 def test_bin2_every_variant_matches_oracle(variant, dtype, monkeypatch):
     """Every sweep variant (register kernel, TMA pipelines of each tile size / stage count /
