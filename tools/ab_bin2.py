@@ -18,6 +18,7 @@ def main():
     ap.add_argument("--dtype", default="f32")
     ap.add_argument("--sweeps", type=int, default=20)
     ap.add_argument("--variants", default="0,5,1,2,3,4")
+    ap.add_argument("--shards", default="1", help="comma list of virtual shard counts")
     args = ap.parse_args()
     import numpy as np
     import torch
@@ -26,9 +27,10 @@ def main():
     idx = splitmix64_indices(7, 1 << 16, 1 << (2 * args.ell))
     ref = None
     esize = 4 if args.dtype == "f32" else 8
-    for v in [int(x) for x in args.variants.split(",")]:
+    runs = [(int(v), int(p)) for v in args.variants.split(",") for p in args.shards.split(",")]
+    for v, p in runs:
         os.environ["LCSB_BIN2_VARIANT"] = str(v)
-        h = Lcsb(2, 2, args.ell, dtype=args.dtype)
+        h = Lcsb(2, 2, args.ell, dtype=args.dtype, shards=p, virtual_shards=p > 1)
         h.sweep(3)
         torch.cuda.synchronize()
         s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -44,7 +46,7 @@ def main():
         else:
             same = bool(np.array_equal(ref, vals))
         gbs = 2 * h.stored_states * esize / (ms / 1e3) / 1e9
-        print(json.dumps({"variant": v, "ell": args.ell, "dtype": args.dtype, "ms_per_sweep": ms,
+        print(json.dumps({"variant": v, "shards": p, "ell": args.ell, "dtype": args.dtype, "ms_per_sweep": ms,
                           "alg_GBps": gbs, "frac_of_6557": gbs / 6557.1, "same_as_first": same}),
               flush=True)
         h.destroy()
