@@ -167,7 +167,8 @@ uint64_t lcsb_num_states(const lcsb_t* h);   /* logical states sigma^(d l) */
 uint64_t lcsb_stored_states(const lcsb_t* h);/* entries per stored table */
 uint64_t lcsb_device_bytes(const lcsb_t* h); /* device bytes owned */
 int32_t lcsb_kernel_in_use(const lcsb_t* h); /* 1 generic, 2 binary half-table paired,
-                                                3 sigma=4 d=2 KS swap-paired */
+                                                3 sigma=4 d=2 KS swap-paired,
+                                                4 register-resident small (sigma, d) */
 
 /* Launches of the library's own kernels enqueued by this handle so far (for bench accounting). */
 int64_t lcsb_launch_count(const lcsb_t* h);

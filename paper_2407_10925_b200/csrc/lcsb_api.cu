@@ -44,6 +44,10 @@ struct lcsb {
   unsigned long long* red_host;  // pinned
   ncclComm_t comm;
   int* barrier_buf;
+  // CUDA-graph replay of G consecutive sweeps for launch-latency-bound (small) tables
+  cudaStream_t cap_stream;
+  cudaGraphExec_t graph[kMaxGen];
+  int graph_sweeps;
   int64_t sweeps_done;
   int64_t launches;
   double best_rho[2];
@@ -217,6 +221,8 @@ static int plan_config(const lcsb_config* c, Plan* p, char* why, size_t whylen) 
   if (!sym && c->sigma == 4 && c->d == 2 && form == LCSB_FORM_KS && c->ell >= 3 &&
       c->kernel == LCSB_KERNEL_AUTO)
     p->kernel = 3;  // sigma = 4, d = 2 swap-paired TMA kernel (kern_q4.cu)
+  else if (p->kernel == 1 && c->kernel == LCSB_KERNEL_AUTO && small_supported(c->sigma, c->d, n))
+    p->kernel = 4;  // register-resident compile-time (sigma, d) kernel (kern_small.cu)
   p->ntab = (form == LCSB_FORM_KS) ? c->d + 1 : 2;  // Alg. 2: d+1 rows; two-array: 2
   p->P = P;
   p->p = lp;
@@ -321,6 +327,9 @@ extern "C" void lcsb_destroy(lcsb_t* h) {
       for (int i = 0; i < h->ntab; ++i) dev_free(h, h->tabs[k][i], h->tab_bytes);
   dev_free(h, h->red, 256);
   if (h->barrier_buf) cudaFree(h->barrier_buf);
+  for (int i = 0; i < kMaxGen; ++i)
+    if (h->graph[i]) cudaGraphExecDestroy(h->graph[i]);
+  if (h->cap_stream) cudaStreamDestroy(h->cap_stream);
   if (h->comm) ncclCommDestroy(h->comm);
   if (h->red_host) cudaFreeHost(h->red_host);
   cudaStreamSynchronize(s);
@@ -521,11 +530,69 @@ static void fill_bin2(const lcsb_t* h, Bin2Args* a, int shard, int in_slot, int 
   }
 }
 
+static int enqueue_sweeps(lcsb_t* h, int64_t n, cudaStream_t s);
+
+// Small tables are launch-latency bound: replay a captured graph of G sweeps (G a multiple of
+// the ring length, so the ring slots are the same before and after) instead of G launches.
+static bool graph_worthy(const lcsb_t* h) {
+  return h->mode == MODE_SINGLE && (uint64_t)h->tab_bytes <= (64ull << 20);
+}
+
+static int sweep_graph(lcsb_t* h, cudaStream_t s) {
+  const int start = h->cur;
+  if (!h->graph[start]) {
+    if (!h->cap_stream) CU(h, cudaStreamCreateWithFlags(&h->cap_stream, cudaStreamNonBlocking));
+    const int64_t done = h->sweeps_done, launches = h->launches;
+    CU(h, cudaStreamBeginCapture(h->cap_stream, cudaStreamCaptureModeThreadLocal));
+    int rc = enqueue_sweeps(h, h->graph_sweeps, h->cap_stream);
+    cudaGraph_t g = nullptr;
+    cudaError_t e = cudaStreamEndCapture(h->cap_stream, &g);
+    if (rc != LCSB_OK) {
+      if (g) cudaGraphDestroy(g);
+      return rc;
+    }
+    if (e != cudaSuccess) return set_err(h, LCSB_ECUDA, "graph capture: %s", cudaGetErrorString(e));
+    e = cudaGraphInstantiate(&h->graph[start], g, 0);
+    cudaGraphDestroy(g);
+    if (e != cudaSuccess) {
+      h->graph[start] = nullptr;
+      return set_err(h, LCSB_ECUDA, "graph instantiate: %s", cudaGetErrorString(e));
+    }
+    h->sweeps_done = done;  // the capture only recorded the sweeps
+    h->launches = launches;
+    h->cur = start;
+  }
+  CU(h, cudaGraphLaunch(h->graph[start], s));
+  h->sweeps_done += h->graph_sweeps;
+  h->launches += h->graph_sweeps;
+  return LCSB_OK;
+}
+
 extern "C" int lcsb_sweep(lcsb_t* h, int64_t n) {
   if (!h) return set_err(nullptr, LCSB_EINVAL, "handle is NULL");
   if (n < 0) return set_err(h, LCSB_EINVAL, "n must be >= 0");
   CU(h, cudaSetDevice(h->device));
   cudaStream_t s = (cudaStream_t)h->cfg.stream;
+  if (graph_worthy(h) && !getenv("LCSB_NO_GRAPHS")) {
+    if (!h->graph_sweeps) {
+      h->graph_sweeps = h->ntab;
+      while (h->graph_sweeps < 32) h->graph_sweeps += h->ntab;
+    }
+    if (h->sweeps_done == 0 && n > 0) {  // one plain sweep first (initialises launch caches)
+      int rc = enqueue_sweeps(h, 1, s);
+      if (rc != LCSB_OK) return rc;
+      --n;
+    }
+    while (n >= h->graph_sweeps) {
+      int rc = sweep_graph(h, s);
+      if (rc != LCSB_OK) return rc;
+      n -= h->graph_sweeps;
+    }
+  }
+  return enqueue_sweeps(h, n, s);
+}
+
+static int enqueue_sweeps(lcsb_t* h, int64_t n, cudaStream_t s) {
   for (int64_t it = 0; it < n; ++it) {
     const int out = (h->cur + 1) % h->ntab;  // the slot of the oldest table
     cudaError_t e = cudaSuccess;
@@ -565,7 +632,8 @@ extern "C" int lcsb_sweep(lcsb_t* h, int64_t n) {
         a.src[k - 1] = (h->form == LCSB_FORM_KS) ? h->tabs[0][slot_back(h, k - 1)]
                                                  : h->tabs[0][h->cur];
       a.dst = h->tabs[0][out];
-      e = launch_generic_sweep(a, h->cfg.dtype, s, h->sms);
+      e = (h->kernel == 4) ? launch_small(a, h->cfg.dtype, false, s, h->sms)
+                           : launch_generic_sweep(a, h->cfg.dtype, s, h->sms);
       h->launches += 1;
     }
     if (e != cudaSuccess)
@@ -630,7 +698,10 @@ extern "C" int lcsb_bound(lcsb_t* h, lcsb_bound_t* out) {
     a.center = h->tabs[0][h->cur];
     a.red_in = h->red;
     a.red_out = h->red + 2;
-    CU(h, launch_generic_wpass(a, h->cfg.dtype, s, h->sms));
+    if (h->kernel == 4)
+      CU(h, launch_small(a, h->cfg.dtype, true, s, h->sms));
+    else
+      CU(h, launch_generic_wpass(a, h->cfg.dtype, s, h->sms));
     h->launches += 1;
   }
   if (h->mode == MODE_PROCESS)

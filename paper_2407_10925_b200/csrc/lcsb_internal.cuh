@@ -169,6 +169,8 @@ int bin2_tma_wpass_m(int dtype, int ell, int p);
 cudaError_t launch_q4_sweep(const Q4Args& a, int dtype, cudaStream_t s, int sms);
 cudaError_t launch_q4_wpass(const Q4Args& a, int dtype, cudaStream_t s, int sms);
 int q4_min_ell();
+bool small_supported(int sigma, int d, uint64_t n);
+cudaError_t launch_small(const GenericArgs& a, int dtype, bool wpass, cudaStream_t s, int sms);
 cudaError_t launch_red_init(unsigned long long* red, cudaStream_t s);
 cudaError_t launch_rdiff(const void* newest, const void* prev, uint64_t n, int dtype,
                          unsigned long long* red, cudaStream_t s, int sms);

@@ -267,7 +267,7 @@ class Lcsb:
 
     @property
     def kernel_in_use(self) -> str:
-        return {1: "generic", 2: "bin2", 3: "q4"}.get(int(self._lib.lcsb_kernel_in_use(self._h)), "?")
+        return {1: "generic", 2: "bin2", 3: "q4", 4: "small"}.get(int(self._lib.lcsb_kernel_in_use(self._h)), "?")
 
     @property
     def launch_count(self) -> int:

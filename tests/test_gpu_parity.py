@@ -161,6 +161,56 @@ def test_q4_matches_generic_kernel_l5(dtype):
     b.destroy()
 
 
+@pytest.mark.parametrize("sigma,d,ell,form,dtype", [
+    (3, 3, 3, "ks", "f64"), (3, 3, 2, "ks", "f32"), (2, 2, 6, "ks", "f64"),
+    (2, 2, 6, "two_array", "f32"), (3, 2, 4, "ks", "f64"), (2, 3, 3, "ks", "f32")])
+def test_small_kernel_matches_generic(sigma, d, ell, form, dtype):
+    """The register-resident compile-time (sigma, d) kernel against the generic kernel: tables
+    of every ring slot and the bound, bit for bit."""
+    Lcsb = _lcsb()
+    a = Lcsb(sigma, d, ell, dtype=dtype, form=form, symmetry=0)
+    b = Lcsb(sigma, d, ell, dtype=dtype, form=form, symmetry=0, kernel="generic")
+    assert a.kernel_in_use == "small" and b.kernel_in_use == "generic"
+    for n in (1, 3, 20):
+        a.sweep(n)
+        b.sweep(n)
+        for k in range(d if form == "ks" else 2):
+            assert np.array_equal(a.table(k), b.table(k))
+        ba, bb = a.bound(), b.bound()
+        assert (ba.R_max, ba.R_min, ba.E_at_Rmax, ba.E_at_Rmin) == \
+               (bb.R_max, bb.R_min, bb.E_at_Rmax, bb.E_at_Rmin)
+    a.destroy()
+    b.destroy()
+
+
+@pytest.mark.parametrize("sigma,d,ell,dtype", [(2, 2, 6, "f64"), (3, 3, 3, "f64"),
+                                               (2, 2, 8, "f32")])
+def test_graph_replay_equals_plain_launches(sigma, d, ell, dtype, monkeypatch):
+    """Small tables replay captured CUDA graphs of sweeps; the result must equal plain launches
+    (including sweep counts that are not multiples of the graph length)."""
+    Lcsb = _lcsb()
+    a = Lcsb(sigma, d, ell, dtype=dtype)
+    monkeypatch.setenv("LCSB_NO_GRAPHS", "1")
+    b = Lcsb(sigma, d, ell, dtype=dtype)
+    for n in (77, 5, 64):
+        monkeypatch.delenv("LCSB_NO_GRAPHS")
+        a.sweep(n)
+        monkeypatch.setenv("LCSB_NO_GRAPHS", "1")
+        b.sweep(n)
+        assert a.sweeps_done == b.sweeps_done
+        assert np.array_equal(a.table(0), b.table(0))
+        assert np.array_equal(a.table(1), b.table(1))
+    monkeypatch.delenv("LCSB_NO_GRAPHS")
+    a.reset()
+    a.sweep(77)
+    b.reset()
+    b.sweep(77)
+    assert np.array_equal(a.table(0), b.table(0))
+    assert a.bound().bound == b.bound().bound
+    a.destroy()
+    b.destroy()
+
+
 def test_generic_two_array_l1():
     # l = 1 cannot use the half-table kernel; AUTO falls back to the full-table generic kernel
     Lcsb = _lcsb()
