@@ -236,9 +236,13 @@ cudaError_t launch_m(const Bin2Args& a, cudaStream_t s, int sms) {
 
 }  // namespace
 
+// register-kernel tile: 4^m outputs, small enough that small tables still give every SM work
+// (at least ~2 x 148 tile pairs), at most 4^5
 int bin2_tile_m(int ell) {
-  int m = ell - 1;
+  int m = ell - 6;
   if (m > 5) m = 5;
+  if (m < 1) m = 1;
+  if (m > ell - 1) m = ell - 1;
   return m;
 }
 
