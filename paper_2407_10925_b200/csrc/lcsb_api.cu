@@ -116,6 +116,8 @@ static int pick_bin2_variant(int dtype, int ell, int p) {
   for (int i = 0; i < 3; ++i) {
     const int v = chain[i];
     const int M = bin2_tma_m(dtype, v);
+    // small tables: keep >= ~256 tile pairs so every SM has work (M <= l - 6)
+    if (p == 0 && M > ell - 6) continue;
     if (M > 0 && ell >= M + 1 && p < ell - 1 - M) return v;
   }
   return p > 0 ? 0 : 5;  // 5 = register kernel (unsharded only); 0 = none

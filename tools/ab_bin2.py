@@ -19,6 +19,7 @@ def main():
     ap.add_argument("--sweeps", type=int, default=20)
     ap.add_argument("--variants", default="0,5,1,2,3,4")
     ap.add_argument("--shards", default="1", help="comma list of virtual shard counts")
+    ap.add_argument("--warm", type=int, default=3, help="untimed sweeps first (graph capture)")
     args = ap.parse_args()
     import numpy as np
     import torch
@@ -31,7 +32,7 @@ def main():
     for v, p in runs:
         os.environ["LCSB_BIN2_VARIANT"] = str(v)
         h = Lcsb(2, 2, args.ell, dtype=args.dtype, shards=p, virtual_shards=p > 1)
-        h.sweep(3)
+        h.sweep(args.warm)
         torch.cuda.synchronize()
         s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         s.record()
