@@ -270,12 +270,17 @@ def cpu_baseline(w, budget_s=15.0):
     reading a full-size logical input table (np.zeros: W_0, sweep 1 of the run)."""
     import numpy as np
     from oracle import ft_oracle as fo
+    w = dict(w)
     n = fo.n_states(w["sigma"], w["d"], w["ell"])
     try:
         src = np.zeros(n, dtype=np.float64)
         table_note = "full-size fp64 logical input table"
-    except MemoryError:
-        return None
+    except MemoryError:  # host too small for the logical table: same recurrence at l - 3
+        w["ell"] -= 3
+        n = fo.n_states(w["sigma"], w["d"], w["ell"])
+        src = np.zeros(n, dtype=np.float64)
+        table_note = (f"host RAM too small for the full table; l reduced to {w['ell']} "
+                      "(per-state cost of the same recurrence)")
     d = w["d"]
     count = 1 << 16
     cores = fo.num_threads()
