@@ -196,7 +196,7 @@ static int plan_config(const lcsb_config* c, Plan* p, char* why, size_t whylen) 
     snprintf(why, whylen, "shards must be 1, 2, 4 or 8");
     return LCSB_EINVAL;
   }
-  if (P > 1) {
+  if (P > 1 || (c->nccl_id && !c->virtual_shards)) {
     if (!sym) {
       snprintf(why, whylen, "sharding needs the complement-folded binary two-array table");
       return LCSB_EINVAL;
@@ -228,7 +228,10 @@ static int plan_config(const lcsb_config* c, Plan* p, char* why, size_t whylen) 
   p->ntab = (form == LCSB_FORM_KS) ? c->d + 1 : 2;  // Alg. 2: d+1 rows; two-array: 2
   p->P = P;
   p->p = lp;
-  p->mode = P == 1 ? MODE_SINGLE : (c->virtual_shards ? MODE_VIRTUAL : MODE_PROCESS);
+  // process mode also with a single rank when an NCCL id is given (exercises the communicator,
+  // the IPC exchange and the collective barrier/bound path on one GPU)
+  p->mode = c->virtual_shards ? (P == 1 ? MODE_SINGLE : MODE_VIRTUAL)
+                              : ((P > 1 || c->nccl_id) ? MODE_PROCESS : MODE_SINGLE);
   p->n_logical = n;
   p->n_stored = sym ? n / 2 : n;
   p->n_local = p->n_stored / (uint64_t)P;

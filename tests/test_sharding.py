@@ -176,3 +176,43 @@ def test_virtual_shards_bitwise_equal_unsharded(ell, shards, dtype):
     a.destroy()
     b.destroy()
     torch.cuda.empty_cache()
+
+
+def _pm_worker(rank, world, port, out_dir):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+    from paper_2407_10925_b200 import Lcsb
+    from paper_2407_10925_b200.dist import create_sharded
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(0)
+    dist.init_process_group("nccl", rank=rank, world_size=world,
+                            device_id=torch.device("cuda", 0))
+    h = create_sharded(10, dtype="f32")   # process mode: own NCCL comm, IPC exchange, barriers
+    ref = Lcsb(2, 2, 10, dtype="f32")
+    h.sweep(23)
+    ref.sweep(23)
+    same = np.array_equal(h.table(0), ref.table(0)) and np.array_equal(h.table(1), ref.table(1))
+    bh, br = h.bound(), ref.bound()
+    h.reset()
+    h.sweep(5)
+    ref.reset()
+    ref.sweep(5)
+    same2 = np.array_equal(h.table(0), ref.table(0))
+    np.save(os.path.join(out_dir, "pm.npy"), np.array([same, bh.bound == br.bound,
+                                                       bh.R_min == br.R_min, same2]))
+    h.destroy()
+    ref.destroy()
+    dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+@pytest.mark.skipif(not has_cuda(), reason="needs a CUDA device")
+def test_process_mode_single_rank_equals_single_gpu(tmp_path):
+    """The NCCL process mode with one rank (communicator, IPC handle all-gather, per-sweep
+    barrier all-reduce, bound all-reduces, collective reset/destroy) gives the single-GPU
+    results bit for bit.  Runs in a spawned process (own CUDA context / process group)."""
+    import torch.multiprocessing as mp
+    mp.spawn(_pm_worker, args=(1, _free_port(), str(tmp_path)), nprocs=1, join=True)
+    assert np.load(tmp_path / "pm.npy").all()
