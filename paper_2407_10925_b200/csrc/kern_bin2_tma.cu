@@ -12,6 +12,7 @@
 // HBM therefore sees one streaming read of every stored entry and full-line writes of every
 // output; the SM only does the fp64 means/max in between.
 #include <math.h>
+#include <stdlib.h>
 
 #include "lcsb_internal.cuh"
 #include "tma.cuh"
@@ -383,24 +384,40 @@ cudaError_t launch_bin2_tma_sweep(const Bin2Args& a, int dtype, int variant, cud
   return cudaErrorInvalidValue;
 }
 
-// W pass on the same pipeline (two stages, no output staging); M = tile exponent
+// W pass on the same pipeline (no output staging); M = tile exponent.  LCSB_WPASS_STAGES=1
+// selects the single-stage register-capped form (A/B knob).
 cudaError_t launch_bin2_tma_wpass(const Bin2Args& a, int dtype, int M, cudaStream_t s, int sms) {
+  static int one_stage = -1;
+  if (one_stage < 0) {
+    const char* e = getenv("LCSB_WPASS_STAGES");
+    one_stage = (e && atoi(e) == 1) ? 1 : 0;
+  }
   if (dtype == LCSB_F32) {
-    if (M == 5) return launch_tma<float, 5, 2, 0, true>(a, s, sms);
+    if (M == 6) return one_stage ? launch_tma<float, 6, 1, 0, true, 2>(a, s, sms)
+                                 : launch_tma<float, 6, 2, 0, true>(a, s, sms);
+    if (M == 5) return one_stage ? launch_tma<float, 5, 1, 0, true, 3>(a, s, sms)
+                                 : launch_tma<float, 5, 2, 0, true>(a, s, sms);
     if (M == 4) return launch_tma<float, 4, 2, 0, true>(a, s, sms);
     if (M == 3) return launch_tma<float, 3, 2, 0, true>(a, s, sms);
   } else {
+    if (M == 5) return one_stage ? launch_tma<double, 5, 1, 0, true, 2>(a, s, sms)
+                                 : launch_tma<double, 5, 2, 0, true>(a, s, sms);
     if (M == 4) return launch_tma<double, 4, 2, 0, true>(a, s, sms);
     if (M == 3) return launch_tma<double, 3, 2, 0, true>(a, s, sms);
   }
   return cudaErrorInvalidValue;
 }
-// largest W-pass tile exponent usable at this l and shard count (0 = none)
+// largest W-pass tile exponent usable at this l and shard count (0 = none); LCSB_WPASS_M caps it
 int bin2_tma_wpass_m(int dtype, int ell, int p) {
-  const int ms32[] = {5, 4, 3}, ms64[] = {4, 3, 0};
+  static int cap = -1;
+  if (cap < 0) {
+    const char* e = getenv("LCSB_WPASS_M");
+    cap = e ? atoi(e) : 5;
+  }
+  const int ms32[] = {6, 5, 4, 3}, ms64[] = {5, 4, 3, 0};
   const int* ms = (dtype == LCSB_F32) ? ms32 : ms64;
-  for (int i = 0; i < 3; ++i)
-    if (ms[i] && ell >= ms[i] + 1 && p < ell - 1 - ms[i]) return ms[i];
+  for (int i = 0; i < 4; ++i)
+    if (ms[i] && ms[i] <= cap && ell >= ms[i] + 1 && p < ell - 1 - ms[i]) return ms[i];
   return 0;
 }
 
