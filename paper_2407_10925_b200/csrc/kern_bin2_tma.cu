@@ -384,14 +384,16 @@ cudaError_t launch_bin2_tma_sweep(const Bin2Args& a, int dtype, int variant, cud
   return cudaErrorInvalidValue;
 }
 
-// W pass on the same pipeline (no output staging); M = tile exponent.  LCSB_WPASS_STAGES=1
-// selects the single-stage register-capped form (A/B knob).
+// W pass on the same pipeline (no output staging); M = tile exponent.  Defaults from the A/B
+// (tools/ab_wpass.py): fp32 M=6 single stage (2 CTAs/SM), fp64 M=5 two stages;
+// LCSB_WPASS_STAGES=1/2 overrides the stage count.
 cudaError_t launch_bin2_tma_wpass(const Bin2Args& a, int dtype, int M, cudaStream_t s, int sms) {
-  static int one_stage = -1;
-  if (one_stage < 0) {
+  static int stages = -1;
+  if (stages < 0) {
     const char* e = getenv("LCSB_WPASS_STAGES");
-    one_stage = (e && atoi(e) == 1) ? 1 : 0;
+    stages = e ? atoi(e) : 0;
   }
+  const bool one_stage = stages == 1 || (stages == 0 && dtype == LCSB_F32);
   if (dtype == LCSB_F32) {
     if (M == 6) return one_stage ? launch_tma<float, 6, 1, 0, true, 2>(a, s, sms)
                                  : launch_tma<float, 6, 2, 0, true>(a, s, sms);
@@ -412,7 +414,7 @@ int bin2_tma_wpass_m(int dtype, int ell, int p) {
   static int cap = -1;
   if (cap < 0) {
     const char* e = getenv("LCSB_WPASS_M");
-    cap = e ? atoi(e) : 5;
+    cap = e ? atoi(e) : 6;
   }
   const int ms32[] = {6, 5, 4, 3}, ms64[] = {5, 4, 3, 0};
   const int* ms = (dtype == LCSB_F32) ? ms32 : ms64;
