@@ -126,7 +126,7 @@ def run_ours(args, w, ws, rank, local):
     stream = torch.cuda.current_stream(dev)
 
     def make():
-        if ws > 1:
+        if ws > 1 or args.force_sharded:
             from paper_2407_10925_b200.dist import create_sharded
             return create_sharded(w["ell"], dtype=w["dtype"], stream=stream)
         return Lcsb(w["sigma"], w["d"], w["ell"], dtype=w["dtype"], form=w["form"])
@@ -317,6 +317,8 @@ def main():
                     help="default: config4 at N=1, config5 (sharded l=18) at N>1")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--force-sharded", action="store_true",
+                    help="use the NCCL process-sharded path even at N = 1 (tests the N > 1 code)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3  # timing rule: at least 3 warm-up steps
@@ -343,14 +345,18 @@ def main():
         return
 
     import torch
-    if ws > 1:
+    if ws > 1 or args.force_sharded:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29517")
+        os.environ.setdefault("RANK", str(rank))
+        os.environ.setdefault("WORLD_SIZE", str(ws))
         torch.distributed.init_process_group("nccl", device_id=torch.device("cuda", local))
     res = run_ours(args, w, ws, rank, local)
     if rank == 0:
         if not args.no_cpu_baseline and ws == 1:
             res["cpu_baseline"] = cpu_baseline(w)
         print(json.dumps(res), flush=True)
-    if ws > 1:
+    if torch.distributed.is_initialized():
         torch.distributed.destroy_process_group()
 
 
