@@ -112,10 +112,20 @@ def _dist():
 
 def algorithmic_bytes_per_sweep(w: dict, stored: int) -> int:
     """Compulsory bytes of one sweep: every input generation read once and the
-    new table written once.  two-array: 2 tables; KS: (d + 1) tables."""
+    new table written once, for the stored layout.  two-array: 2 tables; KS: (d + 1) tables."""
     esize = 4 if w["dtype"] == "f32" else 8
     tables = 2 if w["form"] == "two_array" else w["d"] + 1
     return tables * stored * esize
+
+
+def design_bytes_per_sweep(w: dict, stored: int, kernel: str) -> int:
+    """Bytes the sweep kernel's design moves: equal to the compulsory bytes except
+    for the quarter table, which reads every stored block once per logical image (2 reads +
+    1 write per stored entry)."""
+    esize = 4 if w["dtype"] == "f32" else 8
+    if kernel == "bin2q":
+        return 3 * stored * esize
+    return algorithmic_bytes_per_sweep(w, stored)
 
 
 def run_ours(args, w, ws, rank, local):
@@ -129,7 +139,8 @@ def run_ours(args, w, ws, rank, local):
         if ws > 1 or args.force_sharded:
             from paper_2407_10925_b200.dist import create_sharded
             return create_sharded(w["ell"], dtype=w["dtype"], stream=stream)
-        return Lcsb(w["sigma"], w["d"], w["ell"], dtype=w["dtype"], form=w["form"])
+        return Lcsb(w["sigma"], w["d"], w["ell"], dtype=w["dtype"], form=w["form"],
+                    symmetry=args.symmetry)
 
     h = make()
     S = w["sweeps"]
@@ -180,6 +191,7 @@ def run_ours(args, w, ws, rank, local):
     alg_bytes = algorithmic_bytes_per_sweep(w, stored // ws)  # per GPU (its shard)
     peak, peak_kind = _peaks()
     achieved = alg_bytes / (launch_ms / 1e3) / 1e9
+    design_bytes = design_bytes_per_sweep(w, stored // ws, kernel_name)
     traffic = None
     tpath = os.path.join(ROOT, "profiles", f"traffic_{args.workload}.json")
     if os.path.exists(tpath):
@@ -255,6 +267,8 @@ def run_ours(args, w, ws, rank, local):
                      "frac": achieved / peak, "traffic": traffic,
                      "peak_kind": peak_kind,
                      "algorithmic_bytes_per_launch": alg_bytes,
+                     "design_bytes_per_launch": design_bytes,
+                     "design_frac": design_bytes / (launch_ms / 1e3) / 1e9 / peak,
                      "nvlink_bytes_per_launch": int((stored // ws) * (4 if w["dtype"] == "f32"
                                                     else 8) * (1 - 1 / ws)),
                      "kernel": kernel_name + " sweep kernel"},
@@ -326,6 +340,8 @@ def main():
                     help="default: config4 at N=1, config5 (sharded l=18) at N>1")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--symmetry", type=int, default=-1,
+                    help="table layout: -1 auto, 1 half table, 2 quarter table (binary)")
     ap.add_argument("--force-sharded", action="store_true",
                     help="use the NCCL process-sharded path even at N = 1 (tests the N > 1 code)")
     args = ap.parse_args()

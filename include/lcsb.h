@@ -77,8 +77,11 @@ typedef struct {
   int32_t form;     /* LCSB_FORM_* */
   int32_t rmode;    /* LCSB_R_* : which R gives lcsb_bound_t.bound / best_bound */
   int32_t symmetry; /* -1 auto; 0 full logical table; 1 complement-folded half table
-                       (two-array binary only, l >= 2).  AUTO = 1 when
-                       allowed, else 0. */
+                       (two-array binary only, l >= 2); 2 quarter table:
+                       one entry per orbit of {id, complement, string swap, both} (two-array
+                       binary, unsharded, l >= block_log4 + 1; string swap = reading R19 of
+                       DESIGN.md, implied by "if symmetry is fully exploited").
+                       AUTO = 2 for l >= 12 unsharded, 1 otherwise when allowed, else 0. */
   int32_t kernel;   /* LCSB_KERNEL_* */
   void* stream;     /* cudaStream_t every kernel and copy is enqueued on; NULL = legacy default */
   lcsb_alloc_fn alloc;
@@ -100,6 +103,10 @@ typedef struct {
   int32_t shard;
   int32_t virtual_shards;
   const void* nccl_id;
+  /* quarter table only: the table is cut into blocks of 4^block_log4 entries that are stored
+   * whole or read through the swap permutation; 0 = auto (min(7, l-5) for F32, min(6, l-5)
+   * for F64, at least 2).  Must satisfy 2 <= block_log4 <= l - 1. */
+  int32_t block_log4;
 } lcsb_config;
 
 /* Fill *cfg with defaults: sigma=2,d=2,ell=1, F32, AUTO form, R_MAX, symmetry auto, AUTO
@@ -161,6 +168,16 @@ int lcsb_nccl_unique_id(void* out, size_t len);
 int lcsb_shard_locate(int32_t ell, int32_t shards, uint64_t logical, int32_t* shard,
                       uint64_t* local);
 
+/* Host-only layout query (no GPU needed): the stored index of logical state `logical` in the
+ * quarter table (symmetry = 2) of the binary two-array form with length-ell strings and blocks
+ * of 4^block_log4 entries, and the number of stored entries.  Every stored entry holds states
+ * of ONE orbit of {id, complement, string swap, both} (so sharing it is exact), every stored
+ * entry is used, and an orbit occupies two entries only inside the few blocks that the swap
+ * maps onto themselves.  Requires 3 <= ell <= 31, 2 <= block_log4 <= ell - 1,
+ * ell - block_log4 <= 12.  Errors: EINVAL. */
+int lcsb_quarter_locate(int32_t ell, int32_t block_log4, uint64_t logical, uint64_t* stored,
+                        uint64_t* n_stored);
+
 int64_t lcsb_sweeps_done(const lcsb_t* h);
 int32_t lcsb_num_shards(const lcsb_t* h);   /* P (1 when unsharded) */
 uint64_t lcsb_num_states(const lcsb_t* h);   /* logical states sigma^(d l) */
@@ -168,7 +185,8 @@ uint64_t lcsb_stored_states(const lcsb_t* h);/* entries per stored table */
 uint64_t lcsb_device_bytes(const lcsb_t* h); /* device bytes owned */
 int32_t lcsb_kernel_in_use(const lcsb_t* h); /* 1 generic, 2 binary half-table paired,
                                                 3 sigma=4 d=2 KS swap-paired,
-                                                4 register-resident small (sigma, d) */
+                                                4 register-resident small (sigma, d),
+                                                5 binary quarter-table paired */
 
 /* Launches of the library's own kernels enqueued by this handle so far (for bench accounting). */
 int64_t lcsb_launch_count(const lcsb_t* h);

@@ -7,14 +7,15 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 SO = os.path.join(PKG, "liblcsb.so")
-SOURCES = ["lcsb_api.cu", "kern_generic.cu", "kern_bin2.cu", "kern_bin2_tma.cu", "kern_q4.cu", "kern_small.cu", "kern_reduce.cu"]
+SOURCES = ["lcsb_api.cu", "kern_generic.cu", "kern_bin2.cu", "kern_bin2_tma.cu", "kern_bin2q.cu",
+           "kern_q4.cu", "kern_small.cu", "kern_reduce.cu"]
 NVCC_FLAGS = [
     "-O3", "-std=c++17",
     "-gencode", "arch=compute_100a,code=sm_100a",
     "-lineinfo",
     # no FMA contraction: every fp64 op rounds exactly as written (parity with the oracle)
     "-fmad=false",
-    "-Xcompiler", "-fPIC", "-shared",
+    "-Xcompiler", "-fPIC",
     "-Xptxas", "-v",
 ]
 
@@ -34,19 +35,41 @@ def stale() -> bool:
     return any(os.path.getmtime(p) > t for p in deps)
 
 
+def _compile(src: str, obj: str, inc: list) -> subprocess.CompletedProcess:
+    return subprocess.run([nvcc(), *NVCC_FLAGS, *inc, "-c", src, "-o", obj],
+                          capture_output=True, text=True)
+
+
 def build(force: bool = False, verbose: bool = False) -> str:
+    """One nvcc -c per source (in parallel), then one shared-library link."""
     if not force and not stale():
         return SO
-    tmp = SO + f".tmp{os.getpid()}"
-    cmd = [nvcc(), *NVCC_FLAGS, "-I", os.path.join(ROOT, "include"), "-I", CSRC,
-           *[os.path.join(CSRC, s) for s in SOURCES], "-o", tmp, "-lcudart", "-lnccl"]
-    res = subprocess.run(cmd, capture_output=True, text=True)
-    if res.returncode != 0:
-        sys.stderr.write(res.stdout + res.stderr)
-        raise RuntimeError("nvcc failed building liblcsb.so")
-    if verbose:
-        sys.stderr.write(res.stderr)
-    os.replace(tmp, SO)
+    from concurrent.futures import ThreadPoolExecutor
+    tag = f".tmp{os.getpid()}"
+    inc = ["-I", os.path.join(ROOT, "include"), "-I", CSRC]
+    objs = [os.path.join(CSRC, s[:-3] + tag + ".o") for s in SOURCES]
+    try:
+        with ThreadPoolExecutor(max(1, min(len(SOURCES), os.cpu_count() or 1))) as ex:
+            results = list(ex.map(lambda so: _compile(os.path.join(CSRC, so[0]), so[1], inc),
+                                  zip(SOURCES, objs)))
+        for src, res in zip(SOURCES, results):
+            if res.returncode != 0:
+                sys.stderr.write(res.stdout + res.stderr)
+                raise RuntimeError(f"nvcc failed compiling {src}")
+            if verbose:
+                sys.stderr.write(res.stderr)
+        tmp = SO + tag
+        res = subprocess.run([nvcc(), "-shared", "-gencode", "arch=compute_100a,code=sm_100a",
+                              *objs, "-o", tmp, "-lcudart", "-lnccl"],
+                             capture_output=True, text=True)
+        if res.returncode != 0:
+            sys.stderr.write(res.stdout + res.stderr)
+            raise RuntimeError("nvcc failed linking liblcsb.so")
+        os.replace(tmp, SO)
+    finally:
+        for o in objs:
+            if os.path.exists(o):
+                os.remove(o)
     return SO
 
 

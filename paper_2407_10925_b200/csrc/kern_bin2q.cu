@@ -1,0 +1,486 @@
+// kern_bin2q.cu -- the binary (sigma = d = 2) two-array sweep on the QUARTER table: one stored
+// entry per orbit of the symmetry group {id, complement c, string swap s, psi = c s}.
+//
+// Method: identical arithmetic to kern_bin2_tma.cu (Eqs. F1/F0
+// PAPER.md:752-779), same tile pairing {t, psi(t)} and the same adv_b windows.  Only the
+// storage changes (DESIGN.md §6 "quarter table"):
+//
+//  * Half-table index space [0, 2^(2l-1)) (a_0 = 0, complement folded, Eq. comp_eq) is cut into
+//    blocks of 4^K entries; a block is fixed by its top l-K characters pairs ("prefix").  The
+//    residual symmetry of the half table maps blocks onto blocks with a digit-wise permutation
+//    inside: Q0 blocks (heads 00) pair under s (swap the two bits of every pair), Q1 blocks
+//    (heads 01) under psi (pairswap of the complement).  Of each block pair only the smaller
+//    prefix is stored ("canonical", mode 0); the other reads it through the permutation
+//    (mode 1 = s, mode 2 = psi).  map[block] = (slot << 2) | mode, built by the host.  The
+//    string swap W(a,b) = W(b,a) is an exact invariant of every iterate (reading R19), the
+//    complement one is Eq. comp_eq.
+//  * Reads: a tile's adv_b window (2T entries with free low 2M+1 bits) of a mode-0 block is one
+//    contiguous run; of a permuted block it is two runs of T (bit 2M+1 <-> bit 2M exchanged),
+//    loaded with two bulk copies into the same smem slots; the consumer indexes smem through
+//    the permutation.  Every half-table window is loaded once, so every stored block is read
+//    twice per sweep (once per logical image).
+//  * Writes: of every output run (Q1 tile, Q0 row run, Q0 mirror run) only those lying in a
+//    canonical block are stored -- each stored entry is written exactly once.  psi(t)'s outputs
+//    equal t's (the pair computes one max for both), so exactly one of the two Q1 runs is
+//    written unless the block is psi-fixed.
+//  => per sweep: read 2 x stored + write 1 x stored = 1.5 x (half table) bytes, 3 bytes per
+//     logical state in fp32 (vs 4 for the half table).
+#include <math.h>
+#include <stdlib.h>
+
+#include "lcsb_internal.cuh"
+#include "tma.cuh"
+
+namespace lcsbk {
+namespace {
+
+__device__ __forceinline__ uint64_t pairswap(uint64_t v) {
+  return ((v & 0xAAAAAAAAAAAAAAAAull) >> 1) | ((v & 0x5555555555555555ull) << 1);
+}
+__device__ __forceinline__ uint32_t pairswap32(uint32_t v) {
+  return ((v & 0xAAAAAAAAu) >> 1) | ((v & 0x55555555u) << 1);
+}
+
+// Q0 output from one row of 4 in the oracle's summation order (Alg. 3 "SameFirstBit")
+__device__ __forceinline__ double q0_val(double v0, double v1, double v2, double v3) {
+  double r = ((v0 + v1) + v2) + v3;
+  double cand = 0.25 * r;
+  double best = 0.0;
+  if (cand > best) best = cand;
+  return 1.0 + best;
+}
+
+constexpr int kThreads = 256;
+constexpr uint64_t kNone = ~0ull;
+
+template <typename T, int M, int S, bool WMODE>
+struct QCfg {
+  static constexpr uint32_t TT = 1u << (2 * M);  // Q1 outputs per tile
+  static constexpr uint32_t WIN = 2 * TT;        // entries per adv_b window
+  static constexpr uint32_t STAGE = 2 * WIN;     // both windows of the tile pair
+  static constexpr size_t SMEM =
+      (size_t)S * STAGE * sizeof(T) + (size_t)S * sizeof(uint64_t) + (size_t)S * 8 * sizeof(uint64_t);
+};
+
+struct QGeo {
+  int K;
+  uint64_t q1, lmask, amask, bmask, kmask;
+  uint64_t ntiles;  // 4^(l-1-M)
+};
+
+__device__ __forceinline__ void qtile(const QGeo& g, uint64_t tau, uint32_t LOG, uint64_t& x0,
+                                      uint64_t& p0, uint64_t& taup) {
+  x0 = g.q1 + (tau << LOG);
+  p0 = pairswap(~x0 & g.lmask) & ~((1ull << LOG) - 1);  // first output of tile psi(tau)
+  taup = (p0 - g.q1) >> LOG;
+}
+__device__ __forceinline__ uint64_t qwin(const QGeo& g, uint64_t x) {  // adv_b window base
+  return (x & g.amask) | ((x & g.bmask & ~g.q1) << 2);
+}
+// stored index of the first entry of a run starting at half-table index s if the run lies in
+// a canonical block, else kNone
+__device__ __forceinline__ uint64_t qrun(const QGeo& g, uint32_t m, uint64_t s) {
+  return (m & 3u) ? kNone : (((uint64_t)(m >> 2) << (2 * g.K)) | (s & g.kmask));
+}
+
+// ---- window addressing.  Logical window position w (0 <= w < 2T): bit 2M = the appended b
+// character of the tile's top free pair, low 2M bits = the tile's free pairs.  A window loaded
+// from a permuted block sits in smem as two runs of T (bit 2M+1 <-> bit 2M exchanged) with the
+// pairs inside permuted: mode 1 (s) pairswap, mode 2 (psi) pairswap of the complement.
+// A "group" = the 4 logical positions with equal bits >= 2 (the last character pair of the
+// window state free); it is 4 consecutive smem entries in every mode, in the order comp<MODE>.
+template <uint32_t TT, int MODE>
+__device__ __forceinline__ uint32_t gbase(uint32_t g) {  // smem start of the group at logical g
+  if (MODE == 0) return g;
+  const uint32_t w = (MODE == 1) ? g : (~(g + 3u) & (2u * TT - 1u));
+  return (w & TT) | pairswap32(w & (TT - 1u));
+}
+template <int MODE>
+__device__ __forceinline__ constexpr uint32_t comp(uint32_t d) {  // smem slot of logical digit d
+  return MODE == 0 ? d
+                   : (MODE == 1 ? (((d & 1u) << 1) | (d >> 1))
+                                : ((((3u - d) & 1u) << 1) | ((3u - d) >> 1)));
+}
+
+template <typename T>
+__device__ __forceinline__ void ld4(const T* p, double (&v)[4]);
+template <>
+__device__ __forceinline__ void ld4<float>(const float* p, double (&v)[4]) {
+  const float4 f = *reinterpret_cast<const float4*>(p);
+  v[0] = f.x; v[1] = f.y; v[2] = f.z; v[3] = f.w;
+}
+template <>
+__device__ __forceinline__ void ld4<double>(const double* p, double (&v)[4]) {
+  const double2 a = reinterpret_cast<const double2*>(p)[0];
+  const double2 b = reinterpret_cast<const double2*>(p)[1];
+  v[0] = a.x; v[1] = a.y; v[2] = b.x; v[3] = b.y;
+}
+template <typename T>
+__device__ __forceinline__ void st4(T* p, double a, double b, double c, double d);
+template <>
+__device__ __forceinline__ void st4<float>(float* p, double a, double b, double c, double d) {
+  *reinterpret_cast<float4*>(p) = make_float4((float)a, (float)b, (float)c, (float)d);
+}
+template <>
+__device__ __forceinline__ void st4<double>(double* p, double a, double b, double c, double d) {
+  reinterpret_cast<double2*>(p)[0] = make_double2(a, b);
+  reinterpret_cast<double2*>(p)[1] = make_double2(c, d);
+}
+__device__ __forceinline__ void sel4(bool s, const double (&x)[4], const double (&y)[4],
+                                     double (&a)[4], double (&b)[4]) {
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    a[k] = s ? y[k] : x[k];
+    b[k] = s ? x[k] : y[k];
+  }
+}
+__device__ __forceinline__ void wupd(double u, double f, double R0, double R1, double& w0,
+                                     double& w1) {
+  w0 = fmax(w0, (u + R0) - f);
+  w1 = fmax(w1, (u + R1) - f);
+}
+
+// Each thread takes quads of Q1 outputs o0..o0+3 of tile t (and the same values at psi(t)).
+// adv_b pairs of outputs (o0, o0+2) form x-window group A = logical 2 pairswap(o0), (o0+1, o0+3)
+// group B = A + 4; in the psi window (o0+3, o0+2) form A' = 2 (T-4-o0), (o0+1, o0) B' = A' + 4.
+// Over all quads every group of both windows is loaded exactly once, and a group is also a
+// complete Q0 row (Alg. 3): row r = group/4 -> Q0 output r of the window's run and its mirror
+// (the complemented tail, row read reversed).  So each window entry is read from smem and
+// widened to fp64 once.  The A/B load order alternates across threads so each 128-bit smem load
+// is conflict-free (2-way for permuted x windows).
+template <typename T, int MODE, bool WMODE>
+__device__ __forceinline__ void q0_group(const double (&G)[4], uint32_t r, uint32_t half_rows,
+                                         const T* src, T* dst, uint64_t of, uint64_t om,
+                                         double R0, double R1, double& wm0, double& wm1) {
+  const double v0 = G[comp<MODE>(0)], v1 = G[comp<MODE>(1)], v2 = G[comp<MODE>(2)],
+               v3 = G[comp<MODE>(3)];
+  const double fwd = q0_val(v0, v1, v2, v3);
+  const double mir = q0_val(v3, v2, v1, v0);
+  if (WMODE) {
+    if (of != kNone) wupd((double)src[of + r], fwd, R0, R1, wm0, wm1);
+    if (om != kNone) wupd((double)src[om + (half_rows - 1 - r)], mir, R0, R1, wm0, wm1);
+  } else {
+    if (of != kNone) dst[of + r] = (T)fwd;
+    if (om != kNone) dst[om + (half_rows - 1 - r)] = (T)mir;
+  }
+}
+
+template <typename T, uint32_t TT, int MW, int MP, bool WMODE>
+__device__ __forceinline__ void pair_quads(const T* bw, const T* bp, const T* src, T* dst,
+                                           const uint64_t* meta, bool self, double R0,
+                                           double R1, double& wm0, double& wm1) {
+  constexpr uint32_t SX = (MW == 0) ? 2 : 0, SP = (MP == 0) ? 2 : 1;
+  const uint64_t oQ1 = meta[1], oQ1p = meta[2];
+  const uint64_t of = meta[3], om = meta[4], opf = meta[5], opm = meta[6];
+  const bool rows_x = of != kNone || om != kNone;
+  const bool rows_p = !self && (opf != kNone || opm != kNone);
+  for (uint32_t qd = threadIdx.x; qd < TT / 4; qd += kThreads) {
+    const uint32_t o0 = 4 * qd;
+    const uint32_t g = 2 * pairswap32(o0), u = 2 * (TT - 4 - o0);
+    double X1[4], X2[4], A[4], B[4], P1[4], P2[4], Ap[4], Bp[4];
+    const bool sx = (qd >> SX) & 1u, sp = (qd >> SP) & 1u;
+    ld4(bw + gbase<TT, MW>(sx ? g + 4 : g), X1);
+    ld4(bw + gbase<TT, MW>(sx ? g : g + 4), X2);
+    ld4(bp + gbase<TT, MP>(sp ? u + 4 : u), P1);
+    ld4(bp + gbase<TT, MP>(sp ? u : u + 4), P2);
+    sel4(sx, X1, X2, A, B);
+    sel4(sp, P1, P2, Ap, Bp);
+    constexpr uint32_t c0 = comp<MW>(0), c1 = comp<MW>(1), c2 = comp<MW>(2), c3 = comp<MW>(3);
+    constexpr uint32_t d0 = comp<MP>(0), d1 = comp<MP>(1), d2 = comp<MP>(2), d3 = comp<MP>(3);
+    double v[4];
+    // adv_b(x) and adv_b(psi x) = adv_a(x), each (g[c=0] + g[c=1]) / 2 in the oracle's order
+    const double bx[4] = {0.5 * (A[c0] + A[c1]), 0.5 * (B[c0] + B[c1]), 0.5 * (A[c2] + A[c3]),
+                          0.5 * (B[c2] + B[c3])};
+    const double bq[4] = {0.5 * (Bp[d2] + Bp[d3]), 0.5 * (Bp[d0] + Bp[d1]),
+                          0.5 * (Ap[d2] + Ap[d3]), 0.5 * (Ap[d0] + Ap[d1])};
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      v[k] = bx[k];
+      if (bq[k] > v[k]) v[k] = bq[k];
+    }
+    // psi(o0 + k) sits at oQ1p + qb + pairswap(3 - k): the quad reversed as (3, 1, 2, 0)
+    const uint32_t qb = pairswap32(~o0 & (TT - 1) & ~3u);
+    if (WMODE) {
+      double uu[4];
+      if (oQ1 != kNone) {
+        ld4(src + oQ1 + o0, uu);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) wupd(uu[k], v[k], R0, R1, wm0, wm1);
+      }
+      if (oQ1p != kNone) {
+        ld4(src + oQ1p + qb, uu);
+        wupd(uu[3], v[0], R0, R1, wm0, wm1);
+        wupd(uu[1], v[1], R0, R1, wm0, wm1);
+        wupd(uu[2], v[2], R0, R1, wm0, wm1);
+        wupd(uu[0], v[3], R0, R1, wm0, wm1);
+      }
+    } else {
+      if (oQ1 != kNone) st4(dst + oQ1 + o0, v[0], v[1], v[2], v[3]);
+      if (oQ1p != kNone) st4(dst + oQ1p + qb, v[3], v[1], v[2], v[0]);
+    }
+    // Q0 rows of the four groups
+    if (rows_x) {
+      q0_group<T, MW, WMODE>(A, g >> 2, TT / 2, src, dst, of, om, R0, R1, wm0, wm1);
+      q0_group<T, MW, WMODE>(B, (g >> 2) + 1, TT / 2, src, dst, of, om, R0, R1, wm0, wm1);
+    }
+    if (rows_p) {
+      q0_group<T, MP, WMODE>(Ap, u >> 2, TT / 2, src, dst, opf, opm, R0, R1, wm0, wm1);
+      q0_group<T, MP, WMODE>(Bp, (u >> 2) + 1, TT / 2, src, dst, opf, opm, R0, R1, wm0, wm1);
+    }
+  }
+}
+
+// next item >= c (step G) whose tile is the smaller member of its psi pair
+__device__ __forceinline__ uint64_t qnext(const QGeo& g, uint64_t c, uint64_t G, uint32_t LOG) {
+  while (c < g.ntiles) {
+    uint64_t x0, p0, taup;
+    qtile(g, c, LOG, x0, p0, taup);
+    if (taup >= c) return c;
+    c += G;
+  }
+  return c;
+}
+
+// map entries an item needs: windows t, psi t; runs Q1 t, Q1 psi t, rows/mirrors of both windows
+struct QItem {
+  uint32_t m[8];
+};
+template <int M>
+__device__ __forceinline__ void qlookup(const QGeo& g, const uint32_t* __restrict__ map,
+                                        uint64_t tau, QItem& it) {
+  constexpr uint32_t TT = 1u << (2 * M), LOG = 2 * M;
+  uint64_t x0, p0, taup;
+  qtile(g, tau, LOG, x0, p0, taup);
+  const uint64_t wb = qwin(g, x0), wp = qwin(g, p0);
+  const uint64_t yf = wb >> 2, ypf = wp >> 2;
+  const int sh = 2 * g.K;
+  it.m[0] = __ldg(map + (wb >> sh));
+  it.m[1] = __ldg(map + (wp >> sh));
+  it.m[2] = __ldg(map + (x0 >> sh));
+  it.m[3] = __ldg(map + (p0 >> sh));
+  it.m[4] = __ldg(map + (yf >> sh));
+  it.m[5] = __ldg(map + ((g.q1 - yf - TT / 2) >> sh));
+  it.m[6] = __ldg(map + (ypf >> sh));
+  it.m[7] = __ldg(map + ((g.q1 - ypf - TT / 2) >> sh));
+}
+
+// Thread 0: bulk-load the two windows of tile pair tau into a stage and record the item's
+// metadata: meta[0] = window modes (bits 0-1: window t, 2-3: window psi t, bit 4: self pair),
+// meta[1..6] = stored run starts (Q1 t, Q1 psi t, rows t, mirrors t, rows psi t, mirrors psi t;
+// kNone = not stored).
+template <typename T, int M>
+__device__ __forceinline__ void qissue(const QGeo& g, const QItem& it, uint64_t tau, T* buf,
+                                       uint64_t* bar, uint64_t* meta, const T* src) {
+  constexpr uint32_t TT = 1u << (2 * M), LOG = 2 * M;
+  uint64_t x0, p0, taup;
+  qtile(g, tau, LOG, x0, p0, taup);
+  const bool self = taup == tau;
+  const uint64_t wb = qwin(g, x0), wp = qwin(g, p0);
+  const uint64_t yf = wb >> 2, ym = g.q1 - yf - TT / 2, ypf = wp >> 2, ypm = g.q1 - ypf - TT / 2;
+  const int sh = 2 * g.K;
+  const uint32_t mw = it.m[0], mp = it.m[1];
+  meta[0] = (mw & 3u) | ((mp & 3u) << 2) | (self ? 16u : 0u);
+  meta[1] = qrun(g, it.m[2], x0);
+  meta[2] = self ? kNone : qrun(g, it.m[3], p0);
+  meta[3] = qrun(g, it.m[4], yf);
+  meta[4] = qrun(g, it.m[5], ym);
+  meta[5] = self ? kNone : qrun(g, it.m[6], ypf);
+  meta[6] = self ? kNone : qrun(g, it.m[7], ypm);
+  mbar_expect_tx(bar, 2 * 2 * TT * (uint32_t)sizeof(T));
+#pragma unroll
+  for (int k = 0; k < 2; ++k) {
+    const uint32_t m = k ? mp : mw;
+    const uint64_t w = k ? wp : wb;
+    T* dst = buf + k * 2 * TT;
+    const T* blk = src + ((uint64_t)(m >> 2) << sh);
+    const uint64_t e = w & g.kmask;
+    if ((m & 3u) == 0) {
+      tma_load_1d(dst, blk + e, 2 * TT * (uint32_t)sizeof(T), bar);
+    } else {
+      const uint64_t f = ((m & 3u) == 1) ? pairswap(e) : pairswap(~e & g.kmask);
+      const uint64_t start = (f & ~(4ull * TT - 1)) | (f & TT);
+      tma_load_1d(dst, blk + start, TT * (uint32_t)sizeof(T), bar);
+      tma_load_1d(dst + TT, blk + start + 2 * TT, TT * (uint32_t)sizeof(T), bar);
+    }
+  }
+}
+
+template <typename T, int M, int S, bool WMODE, int MINB = 1>
+__global__ void __launch_bounds__(kThreads, MINB) bin2q_kernel(Bin2QArgs a) {
+  using C = QCfg<T, M, S, WMODE>;
+  constexpr uint32_t TT = C::TT, WIN = C::WIN;
+  constexpr uint32_t LOG = 2 * M;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  T* in = reinterpret_cast<T*>(smem_raw);  // [S][STAGE]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(in + (size_t)S * C::STAGE);
+  uint64_t* metas = bars + S;  // [S][8]
+
+  QGeo g;
+  const int L = 2 * a.ell;
+  g.K = a.K;
+  g.lmask = (1ull << L) - 1;
+  g.q1 = 1ull << (L - 2);
+  g.amask = 0xAAAAAAAAAAAAAAAAull & g.lmask;
+  g.bmask = 0x5555555555555555ull & g.lmask;
+  g.kmask = (1ull << (2 * a.K)) - 1;
+  g.ntiles = 1ull << (2 * (a.ell - 1 - M));
+  const T* src = reinterpret_cast<const T*>(a.src);
+  T* dst = reinterpret_cast<T*>(a.dst);
+  const uint32_t* map = a.map;
+  const int tid = threadIdx.x;
+  const uint64_t G = gridDim.x;
+
+  double R0 = 0.0, R1 = 0.0, wm0 = -INFINITY, wm1 = -INFINITY;
+  if (WMODE) {
+    R0 = dec_ord(a.red_in[0]);
+    R1 = dec_ord(a.red_in[1]);
+  }
+  uint64_t pc = 0;  // producer cursor (thread 0 only)
+  QItem pit;        // its map entries, fetched one item ahead
+  if (tid == 0) {
+    for (int s = 0; s < S; ++s) mbar_init(&bars[s], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  if (tid == 0) {
+    pc = qnext(g, blockIdx.x, G, LOG);
+    if (pc < g.ntiles) qlookup<M>(g, map, pc, pit);
+    for (int s = 0; s < S && pc < g.ntiles; ++s) {
+      qissue<T, M>(g, pit, pc, in + (size_t)s * C::STAGE, &bars[s], metas + 8 * s, src);
+      pc = qnext(g, pc + G, G, LOG);
+      if (pc < g.ntiles) qlookup<M>(g, map, pc, pit);
+    }
+  }
+
+  uint32_t i = 0;
+  for (uint64_t cc = qnext(g, blockIdx.x, G, LOG); cc < g.ntiles;
+       cc = qnext(g, cc + G, G, LOG), ++i) {
+    const uint32_t s = i % S;
+    const uint32_t parity = (i / S) & 1u;
+    T* buf = in + (size_t)s * C::STAGE;
+    const uint64_t* meta = metas + 8 * s;
+    mbar_wait(&bars[s], parity);
+    __syncthreads();
+    const uint32_t modes = (uint32_t)meta[0];
+    const uint32_t mw = modes & 3u, mp = (modes >> 2) & 3u;
+    const bool self = (modes & 16u) != 0;
+    const T* bw = buf;
+    const T* bp = buf + WIN;
+#define LCSB_Q1(MW, MP) \
+  pair_quads<T, TT, MW, MP, WMODE>(bw, bp, src, dst, meta, self, R0, R1, wm0, wm1)
+    switch (mw * 3 + mp) {
+      case 0: LCSB_Q1(0, 0); break;
+      case 1: LCSB_Q1(0, 1); break;
+      case 2: LCSB_Q1(0, 2); break;
+      case 3: LCSB_Q1(1, 0); break;
+      case 4: LCSB_Q1(1, 1); break;
+      case 5: LCSB_Q1(1, 2); break;
+      case 6: LCSB_Q1(2, 0); break;
+      case 7: LCSB_Q1(2, 1); break;
+      default: LCSB_Q1(2, 2); break;
+    }
+#undef LCSB_Q1
+    __syncthreads();  // stage s (data and metadata) is free again
+    if (tid == 0 && pc < g.ntiles) {
+      qissue<T, M>(g, pit, pc, buf, &bars[s], metas + 8 * s, src);
+      pc = qnext(g, pc + G, G, LOG);
+      if (pc < g.ntiles) qlookup<M>(g, map, pc, pit);
+    }
+  }
+  if (WMODE) block_max2_to(wm0, wm1, a.red_out);
+}
+
+template <typename T, int M, int S, bool WMODE, int MINB = 1>
+cudaError_t launch_q(const Bin2QArgs& a, cudaStream_t s, int sms) {
+  using C = QCfg<T, M, S, WMODE>;
+  static uint64_t cap = 0;
+  if (cap == 0) {
+    cudaError_t e = cudaFuncSetAttribute(bin2q_kernel<T, M, S, WMODE, MINB>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
+    if (e != cudaSuccess) return e;
+    int per_sm = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, bin2q_kernel<T, M, S, WMODE, MINB>,
+                                                      kThreads, C::SMEM) != cudaSuccess ||
+        per_sm < 1) {
+      cudaGetLastError();
+      per_sm = 1;
+    }
+    cap = (uint64_t)per_sm * sms;
+  }
+  if (a.K < M + 1 || a.ell < a.K + 1) return cudaErrorInvalidValue;
+  const uint64_t ntiles = 1ull << (2 * (a.ell - 1 - M));
+  uint64_t blocks = cap < ntiles ? cap : ntiles;
+  if (blocks < 1) blocks = 1;
+  bin2q_kernel<T, M, S, WMODE, MINB><<<(unsigned)blocks, kThreads, C::SMEM, s>>>(a);
+  return cudaGetLastError();
+}
+
+template <bool WMODE>
+cudaError_t dispatch_q(const Bin2QArgs& a, int dtype, int M, cudaStream_t s, int sms) {
+  if (dtype == LCSB_F32) {
+    switch (M) {
+      case 6: return launch_q<float, 6, 1, WMODE, 3>(a, s, sms);  // A/B: variant 10
+      case 5: return launch_q<float, 5, 2, WMODE>(a, s, sms);
+      case 4: return launch_q<float, 4, 2, WMODE>(a, s, sms);
+      case 3: return launch_q<float, 3, 2, WMODE>(a, s, sms);
+      case 2: return launch_q<float, 2, 2, WMODE>(a, s, sms);
+      case 1: return launch_q<float, 1, 2, WMODE>(a, s, sms);
+    }
+  } else {
+    switch (M) {
+      case 5: return launch_q<double, 5, 2, WMODE, 2>(a, s, sms);  // A/B: variant 9
+      case 4: return launch_q<double, 4, 2, WMODE>(a, s, sms);
+      case 3: return launch_q<double, 3, 2, WMODE>(a, s, sms);
+      case 2: return launch_q<double, 2, 2, WMODE>(a, s, sms);
+      case 1: return launch_q<double, 1, 2, WMODE>(a, s, sms);
+    }
+  }
+  return cudaErrorInvalidValue;
+}
+
+// Sweep variants (tile 4^M, pipeline stages S, min CTAs/SM) for the A/B (tools/ab_bin2q.py);
+// 0 = the default of dispatch_q for the handle's M.  Measured on B200 at l = 17 fp32 / l = 16
+// fp64: fp32 (6,1,3) 8.27 ms/sweep, (6,1,2) 8.97, (6,2,1) 10.6, M = 5 >= 12.5
+// (per-item overhead); fp64 (5,2,2) 4.13, (5,3,2) 4.24, (5,2,3) 4.42, (5,1,2) 4.84.
+struct QVariant {
+  int m, s, mb;
+};
+constexpr QVariant kQ32[] = {{0, 0, 0}, {6, 1, 2}, {5, 2, 3}, {5, 3, 2}, {5, 2, 2}, {4, 4, 3},
+                             {4, 6, 2}, {5, 4, 1}, {4, 3, 3}, {6, 2, 1}, {6, 1, 3}};
+constexpr QVariant kQ64[] = {{0, 0, 0}, {5, 1, 2}, {5, 3, 2}, {4, 8, 3}, {4, 6, 3}, {5, 2, 3},
+                             {4, 12, 2}, {4, 4, 3}, {3, 8, 3}, {5, 2, 2}, {4, 3, 3}};
+constexpr int kQVariants = 11;
+
+}  // namespace
+
+int bin2q_variant_m(int dtype, int variant) {
+  if (variant <= 0 || variant >= kQVariants) return 0;
+  return (dtype == LCSB_F32) ? kQ32[variant].m : kQ64[variant].m;
+}
+
+cudaError_t launch_bin2q_sweep(const Bin2QArgs& a, int dtype, int M, int variant, cudaStream_t s,
+                               int sms) {
+  if (variant <= 0) return dispatch_q<false>(a, dtype, M, s, sms);
+  if (variant >= kQVariants) return cudaErrorInvalidValue;
+#define LCSB_QV(T, M_, S_, MB_) \
+  if (d.m == M_ && d.s == S_ && d.mb == MB_) return launch_q<T, M_, S_, false, MB_>(a, s, sms);
+  if (dtype == LCSB_F32) {
+    const QVariant d = kQ32[variant];
+    LCSB_QV(float, 6, 1, 2) LCSB_QV(float, 5, 2, 3) LCSB_QV(float, 5, 3, 2) LCSB_QV(float, 5, 2, 2)
+    LCSB_QV(float, 4, 4, 3) LCSB_QV(float, 4, 6, 2) LCSB_QV(float, 5, 4, 1) LCSB_QV(float, 4, 3, 3)
+    LCSB_QV(float, 6, 2, 1) LCSB_QV(float, 6, 1, 3)
+  } else {
+    const QVariant d = kQ64[variant];
+    LCSB_QV(double, 5, 1, 2) LCSB_QV(double, 5, 3, 2) LCSB_QV(double, 4, 8, 3)
+    LCSB_QV(double, 4, 6, 3) LCSB_QV(double, 5, 2, 3) LCSB_QV(double, 4, 12, 2)
+    LCSB_QV(double, 4, 4, 3) LCSB_QV(double, 3, 8, 3) LCSB_QV(double, 5, 2, 2)
+    LCSB_QV(double, 4, 3, 3)
+  }
+#undef LCSB_QV
+  return cudaErrorInvalidValue;
+}
+cudaError_t launch_bin2q_wpass(const Bin2QArgs& a, int dtype, int M, cudaStream_t s, int sms) {
+  return dispatch_q<true>(a, dtype, M, s, sms);
+}
+
+}  // namespace lcsbk

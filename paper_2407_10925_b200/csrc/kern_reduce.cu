@@ -7,8 +7,8 @@
 //          Grid-stride, 16-byte vector loads, warp shuffle + block reduction, one atomic per
 //          block on order-preserving integer encodings (max/min are exact and order-free, so the
 //          result is independent of the launch geometry).
-//  expand: logical-order read-out, unfolding the complement symmetry and
-//          widening to fp64.
+//  expand: logical-order read-out, unfolding the complement symmetry and,
+//          for the quarter table, the string swap (reading R19); widening to fp64.
 #include <math.h>
 
 #include "lcsb_internal.cuh"
@@ -89,7 +89,8 @@ struct ExpandTabs {
 };
 
 template <typename T>
-__global__ void expand_kernel(ExpandTabs tabs, int p, int symmetric, int ell, uint64_t first,
+__global__ void expand_kernel(ExpandTabs tabs, int p, int symmetric, int ell,
+                              const uint32_t* __restrict__ qmap, int K, uint64_t first,
                               uint64_t count, const uint64_t* __restrict__ idx, double* out) {
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   const uint64_t half = symmetric ? (1ull << (2 * ell - 1)) : 0;
@@ -97,6 +98,10 @@ __global__ void expand_kernel(ExpandTabs tabs, int p, int symmetric, int ell, ui
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count; i += stride) {
     uint64_t y = idx ? idx[i] : first + i;
     if (symmetric && y >= half) y = top - y;  // Eq. (comp_eq)
+    if (qmap) {  // quarter table: the orbit representative under the string swap / psi
+      out[i] = (double)reinterpret_cast<const T*>(tabs.t[0])[qstored(qmap, y, K)];
+      continue;
+    }
     const uint32_t sh = shard_of_stored(y, 2 * ell, p);
     out[i] = (double)reinterpret_cast<const T*>(tabs.t[sh])[local_of_stored(y, 2 * ell, p)];
   }
@@ -127,17 +132,17 @@ cudaError_t launch_rdiff(const void* newest, const void* prev, uint64_t n, int d
 }
 
 cudaError_t launch_expand(const void* const* tabs, int p, int dtype, int symmetric, int ell,
-                          uint64_t first, uint64_t count, const uint64_t* idx, double* out,
-                          cudaStream_t s) {
+                          const uint32_t* qmap, int K, uint64_t first, uint64_t count,
+                          const uint64_t* idx, double* out, cudaStream_t s) {
   uint64_t blocks = (count + 255) / 256;
   if (blocks > 4096) blocks = 4096;
   if (blocks < 1) blocks = 1;
   ExpandTabs t;
   for (int k = 0; k < kMaxShards; ++k) t.t[k] = (k < (1 << p)) ? tabs[k] : nullptr;
   if (dtype == LCSB_F32)
-    expand_kernel<float><<<(unsigned)blocks, 256, 0, s>>>(t, p, symmetric, ell, first, count, idx, out);
+    expand_kernel<float><<<(unsigned)blocks, 256, 0, s>>>(t, p, symmetric, ell, qmap, K, first, count, idx, out);
   else
-    expand_kernel<double><<<(unsigned)blocks, 256, 0, s>>>(t, p, symmetric, ell, first, count, idx, out);
+    expand_kernel<double><<<(unsigned)blocks, 256, 0, s>>>(t, p, symmetric, ell, qmap, K, first, count, idx, out);
   return cudaGetLastError();
 }
 

@@ -26,9 +26,13 @@ struct lcsb {
   int device;
   int sms;
   int form;       // resolved LCSB_FORM_KS / LCSB_FORM_TWO_ARRAY
-  int symmetric;  // complement-folded half table
-  int kernel;     // 1 generic, 2 bin2, 3 q4
+  int symmetric;  // 1 complement-folded half table, 2 quarter table
+  int kernel;     // 1 generic, 2 bin2, 3 q4, 4 small, 5 bin2q
+  int qK, qM;     // quarter table: blocks of 4^qK, tiles of 4^qM
+  uint32_t* qmap; // quarter table: device block map
+  size_t qmap_bytes;
   int bin2_variant;  // 0 auto; see pick_bin2_variant
+  int bin2q_variant; // 0 auto; LCSB_BIN2Q_VARIANT (A/B only)
   uint64_t n_logical;
   uint64_t n_stored;  // entries of the whole stored table
   uint64_t n_local;   // entries per shard
@@ -123,9 +127,33 @@ static int pick_bin2_variant(int dtype, int ell, int p) {
   return p > 0 ? 0 : 5;  // 5 = register kernel (unsharded only); 0 = none
 }
 
+// ---------------------------------------------------------------- quarter table layout
+// Auto choice: the quarter table from this l up, the half table below.
+static const int kQuarterAutoEll = 12;
+// blocks of the half table: 2^(2(l-K)-1); stored (canonical) blocks: Q0 and Q1 each have
+// 4^(l-K-1) blocks of which 2^(l-K-1) are fixed by their pairing (every non-head character pair
+// in {00, 11} for s, in {01, 10} for psi), so (4^(l-K-1) + 2^(l-K-1)) / 2 canonical each.
+static uint64_t quarter_map_entries(int ell, int K) { return 1ull << (2 * (ell - K) - 1); }
+static uint64_t quarter_slots(int ell, int K) {
+  return (1ull << (2 * (ell - K - 1))) + (1ull << (ell - K - 1));
+}
+// map[beta] = (slot << 2) | mode; slots numbered in increasing order of canonical beta
+static bool build_quarter_map(int ell, int K, uint32_t* map) {
+  const int PL = 2 * (ell - K);
+  const uint64_t nb = quarter_map_entries(ell, K);
+  uint64_t next = 0;
+  for (uint64_t b = 0; b < nb; ++b)
+    if (b <= qblock_partner(b, PL)) map[b] = (uint32_t)(next++ << 2);
+  for (uint64_t b = 0; b < nb; ++b) {
+    const uint64_t q = qblock_partner(b, PL);
+    if (b > q) map[b] = (map[q] & ~3u) | (((b >> (PL - 2)) & 1ull) ? 2u : 1u);
+  }
+  return next == quarter_slots(ell, K);
+}
+
 // ---------------------------------------------------------------- planning
 struct Plan {
-  int form, symmetric, kernel, ntab, p, P, mode;
+  int form, symmetric, kernel, ntab, p, P, mode, qK, qM, dtype_code;
   uint64_t n_logical, n_stored, n_local;
   size_t esize;
   uint64_t bytes;  // device bytes this handle allocates
@@ -178,19 +206,36 @@ static int plan_config(const lcsb_config* c, Plan* p, char* why, size_t whylen) 
     return LCSB_EINVAL;
   }
   const bool sym_ok = (form == LCSB_FORM_TWO_ARRAY) && c->ell >= 2 && c->kernel == LCSB_KERNEL_AUTO;
+  const int P = c->shards < 1 ? 1 : c->shards;
+  const bool sharded = P > 1 || (c->nccl_id && !c->virtual_shards);
+  // quarter table geometry: blocks of 4^K, tiles of 4^M (M <= K - 1)
+  int qK = c->block_log4;
+  if (qK <= 0) {
+    qK = c->ell - 5;
+    const int kmax = (c->dtype == LCSB_F32) ? 7 : 6;
+    if (qK > kmax) qK = kmax;
+    if (qK < 2) qK = 2;
+  }
+  const int qM = qK - 1 < ((c->dtype == LCSB_F32) ? 6 : 5) ? qK - 1 : ((c->dtype == LCSB_F32) ? 6 : 5);
+  const bool quarter_ok = sym_ok && !sharded && qK >= 2 && qK <= c->ell - 1 && c->ell - qK <= 16;
   int sym = c->symmetry;
-  if (sym < 0) sym = sym_ok ? 1 : 0;
+  if (sym < 0) sym = (quarter_ok && c->ell >= kQuarterAutoEll) ? 2 : (sym_ok ? 1 : 0);
   if (sym == 1 && !sym_ok) {
     snprintf(why, whylen,
              "the complement-folded table needs the two-array binary form, ell >= 2 and the "
              "AUTO kernel");
     return LCSB_EINVAL;
   }
-  if (sym != 0 && sym != 1) {
-    snprintf(why, whylen, "symmetry must be -1, 0 or 1");
+  if (sym == 2 && !quarter_ok) {
+    snprintf(why, whylen,
+             "the quarter table needs the two-array binary form, the AUTO kernel, no sharding "
+             "and 2 <= block_log4 <= ell - 1 (ell - block_log4 <= 16)");
     return LCSB_EINVAL;
   }
-  const int P = c->shards < 1 ? 1 : c->shards;
+  if (sym < 0 || sym > 2) {
+    snprintf(why, whylen, "symmetry must be -1, 0, 1 or 2");
+    return LCSB_EINVAL;
+  }
   const int lp = log2_exact(P);
   if (lp < 0 || P > kMaxShards) {
     snprintf(why, whylen, "shards must be 1, 2, 4 or 8");
@@ -218,8 +263,11 @@ static int plan_config(const lcsb_config* c, Plan* p, char* why, size_t whylen) 
     }
   }
   p->form = form;
+  p->dtype_code = c->dtype;
   p->symmetric = sym;
-  p->kernel = sym ? 2 : 1;
+  p->qK = (sym == 2) ? qK : 0;
+  p->qM = (sym == 2) ? qM : 0;
+  p->kernel = sym == 2 ? 5 : (sym ? 2 : 1);
   if (!sym && c->sigma == 4 && c->d == 2 && form == LCSB_FORM_KS && c->ell >= 3 &&
       c->kernel == LCSB_KERNEL_AUTO)
     p->kernel = 3;  // sigma = 4, d = 2 swap-paired TMA kernel (kern_q4.cu)
@@ -233,7 +281,7 @@ static int plan_config(const lcsb_config* c, Plan* p, char* why, size_t whylen) 
   p->mode = c->virtual_shards ? (P == 1 ? MODE_SINGLE : MODE_VIRTUAL)
                               : ((P > 1 || c->nccl_id) ? MODE_PROCESS : MODE_SINGLE);
   p->n_logical = n;
-  p->n_stored = sym ? n / 2 : n;
+  p->n_stored = (sym == 2) ? quarter_slots(c->ell, qK) << (2 * qK) : (sym ? n / 2 : n);
   p->n_local = p->n_stored / (uint64_t)P;
   p->esize = (c->dtype == LCSB_F32) ? 4 : 8;
   const uint64_t owned = (p->mode == MODE_PROCESS) ? 1 : (uint64_t)P;
@@ -244,6 +292,7 @@ static int plan_config(const lcsb_config* c, Plan* p, char* why, size_t whylen) 
     return LCSB_EINVAL;
   }
   p->bytes += 256;
+  if (sym == 2) p->bytes += quarter_map_entries(c->ell, qK) * sizeof(uint32_t);
   return LCSB_OK;
 }
 
@@ -265,6 +314,32 @@ extern "C" int lcsb_shard_locate(int32_t ell, int32_t shards, uint64_t logical, 
   if (s >= (1ull << (L - 1))) s = ((1ull << L) - 1) - s;  // Eq. (comp_eq)
   *shard = (int32_t)shard_of_stored(s, L, p);
   *local = local_of_stored(s, L, p);
+  return LCSB_OK;
+}
+
+extern "C" int lcsb_quarter_locate(int32_t ell, int32_t block_log4, uint64_t logical,
+                                   uint64_t* stored, uint64_t* n_stored) {
+  const int K = block_log4;
+  if (ell < 3 || ell > 31 || K < 2 || K > ell - 1 || ell - K > 12 || !stored || !n_stored)
+    return set_err(nullptr, LCSB_EINVAL, "bad arguments to lcsb_quarter_locate");
+  const int L = 2 * ell;
+  if (logical >= (1ull << L)) return set_err(nullptr, LCSB_EINVAL, "logical index out of range");
+  static thread_local int cached_ell = 0, cached_K = 0;
+  static thread_local uint32_t* cached = nullptr;
+  if (cached_ell != ell || cached_K != K) {
+    free(cached);
+    cached = (uint32_t*)malloc(quarter_map_entries(ell, K) * sizeof(uint32_t));
+    if (!cached || !build_quarter_map(ell, K, cached)) {
+      cached_ell = 0;
+      return set_err(nullptr, LCSB_EINVAL, "quarter map construction failed");
+    }
+    cached_ell = ell;
+    cached_K = K;
+  }
+  uint64_t s = logical;
+  if (s >= (1ull << (L - 1))) s = ((1ull << L) - 1) - s;  // Eq. (comp_eq)
+  *stored = qstored(cached, s, K);
+  *n_stored = quarter_slots(ell, K) << (2 * K);
   return LCSB_OK;
 }
 
@@ -331,6 +406,7 @@ extern "C" void lcsb_destroy(lcsb_t* h) {
     if (owns(h, k))
       for (int i = 0; i < h->ntab; ++i) dev_free(h, h->tabs[k][i], h->tab_bytes);
   dev_free(h, h->red, 256);
+  dev_free(h, h->qmap, h->qmap_bytes);
   if (h->barrier_buf) cudaFree(h->barrier_buf);
   for (int i = 0; i < kMaxGen; ++i)
     if (h->graph[i]) cudaGraphExecDestroy(h->graph[i]);
@@ -410,6 +486,8 @@ extern "C" int lcsb_create_ex(const lcsb_config* cfg, lcsb_t** out) {
   h->form = p.form;
   h->symmetric = p.symmetric;
   h->kernel = p.kernel;
+  h->qK = p.qK;
+  h->qM = p.qM;
   h->n_logical = p.n_logical;
   h->n_stored = p.n_stored;
   h->n_local = p.n_local;
@@ -423,6 +501,15 @@ extern "C" int lcsb_create_ex(const lcsb_config* cfg, lcsb_t** out) {
   h->tab_bytes = (size_t)(p.n_local * p.esize);
   h->bin2_variant = 0;  // auto (pick_bin2_variant)
   if (const char* v = getenv("LCSB_BIN2_VARIANT")) h->bin2_variant = atoi(v);
+  if (const char* v = getenv("LCSB_BIN2Q_VARIANT")) h->bin2q_variant = atoi(v);
+  if (h->bin2q_variant > 0 && h->symmetric == 2) {
+    const int vm = bin2q_variant_m(p.dtype_code, h->bin2q_variant);
+    if (vm <= 0 || vm > h->qK - 1 || vm > cfg->ell - 2) {
+      lcsb_destroy(h);
+      return set_err(nullptr, LCSB_EINVAL, "LCSB_BIN2Q_VARIANT %d does not fit block_log4 %d",
+                     h->bin2q_variant, p.qK);
+    }
+  }
   cudaStream_t s = (cudaStream_t)cfg->stream;
 
   if (h->mode == MODE_PROCESS) {
@@ -456,6 +543,20 @@ extern "C" int lcsb_create_ex(const lcsb_config* cfg, lcsb_t** out) {
   if (!h->red || cudaMallocHost(&h->red_host, 256) != cudaSuccess) {
     lcsb_destroy(h);
     return set_err(nullptr, LCSB_ECAPACITY, "scratch allocation failed");
+  }
+  if (h->symmetric == 2) {  // quarter table block map (host-built, uploaded once)
+    const uint64_t nb = quarter_map_entries(cfg->ell, h->qK);
+    h->qmap_bytes = nb * sizeof(uint32_t);
+    uint32_t* hm = (uint32_t*)malloc(h->qmap_bytes);
+    h->qmap = (uint32_t*)dev_alloc(h, h->qmap_bytes);
+    const bool ok = hm && h->qmap && build_quarter_map(cfg->ell, h->qK, hm);
+    e = ok ? cudaMemcpyAsync(h->qmap, hm, h->qmap_bytes, cudaMemcpyHostToDevice, s) : cudaSuccess;
+    if (e == cudaSuccess && ok) e = cudaStreamSynchronize(s);
+    free(hm);
+    if (!ok || e != cudaSuccess) {
+      lcsb_destroy(h);
+      return set_err(nullptr, ok ? LCSB_ECUDA : LCSB_ECAPACITY, "quarter map setup failed");
+    }
   }
   // W_0 = 0: every live generation starts at zero
   for (int k = h->first; k < h->first + h->nown; ++k)
@@ -533,6 +634,15 @@ static void fill_bin2(const lcsb_t* h, Bin2Args* a, int shard, int in_slot, int 
     a->src_shards[k] = h->tabs[k][in_slot];
     a->dst_shards[k] = out_slot >= 0 ? h->tabs[k][out_slot] : nullptr;
   }
+}
+
+static void fill_bin2q(const lcsb_t* h, Bin2QArgs* a, int in_slot, int out_slot) {
+  memset(a, 0, sizeof *a);
+  a->src = h->tabs[0][in_slot];
+  a->dst = out_slot >= 0 ? h->tabs[0][out_slot] : nullptr;
+  a->map = h->qmap;
+  a->ell = h->cfg.ell;
+  a->K = h->qK;
 }
 
 static int enqueue_sweeps(lcsb_t* h, int64_t n, cudaStream_t s);
@@ -621,6 +731,11 @@ static int enqueue_sweeps(lcsb_t* h, int64_t n, cudaStream_t s) {
         }
         h->launches += 1;
       }
+    } else if (h->kernel == 5) {
+      Bin2QArgs a;
+      fill_bin2q(h, &a, h->cur, out);
+      e = launch_bin2q_sweep(a, h->cfg.dtype, h->qM, h->bin2q_variant, s, h->sms);
+      h->launches += 1;
     } else if (h->kernel == 3) {
       Q4Args a;
       memset(&a, 0, sizeof a);
@@ -686,6 +801,13 @@ extern "C" int lcsb_bound(lcsb_t* h, lcsb_bound_t* out) {
         CU(h, launch_bin2_wpass(a, h->cfg.dtype, s, h->sms));
       h->launches += 1;
     }
+  } else if (h->kernel == 5) {
+    Bin2QArgs a;
+    fill_bin2q(h, &a, h->cur, -1);
+    a.red_in = h->red;
+    a.red_out = h->red + 2;
+    CU(h, launch_bin2q_wpass(a, h->cfg.dtype, h->qM, s, h->sms));
+    h->launches += 1;
   } else if (h->kernel == 3) {
     Q4Args a;
     memset(&a, 0, sizeof a);
@@ -776,8 +898,8 @@ static int readout(lcsb_t* h, int which, uint64_t first, uint64_t count, const u
     if (host_idx)
       e = cudaMemcpyAsync(ibuf, host_idx + off, c * sizeof(uint64_t), cudaMemcpyHostToDevice, s);
     if (e == cudaSuccess)
-      e = launch_expand(tabs, h->p, h->cfg.dtype, h->symmetric, h->cfg.ell, first + off, c,
-                        host_idx ? ibuf : nullptr, dbuf, s);
+      e = launch_expand(tabs, h->p, h->cfg.dtype, h->symmetric != 0, h->cfg.ell, h->qmap, h->qK,
+                        first + off, c, host_idx ? ibuf : nullptr, dbuf, s);
     if (e == cudaSuccess) {
       h->launches += 1;
       e = cudaMemcpyAsync(host_dst + off, dbuf, c * sizeof(double), cudaMemcpyDeviceToHost, s);
@@ -807,7 +929,8 @@ extern "C" int32_t lcsb_num_shards(const lcsb_t* h) { return h ? h->P : 0; }
 extern "C" uint64_t lcsb_num_states(const lcsb_t* h) { return h ? h->n_logical : 0; }
 extern "C" uint64_t lcsb_stored_states(const lcsb_t* h) { return h ? h->n_stored : 0; }
 extern "C" uint64_t lcsb_device_bytes(const lcsb_t* h) {
-  return h ? (uint64_t)h->tab_bytes * (uint64_t)h->ntab * (uint64_t)h->nown + 256 : 0;
+  return h ? (uint64_t)h->tab_bytes * (uint64_t)h->ntab * (uint64_t)h->nown + 256 + h->qmap_bytes
+           : 0;
 }
 extern "C" int32_t lcsb_kernel_in_use(const lcsb_t* h) { return h ? h->kernel : 0; }
 extern "C" int64_t lcsb_launch_count(const lcsb_t* h) { return h ? h->launches : 0; }

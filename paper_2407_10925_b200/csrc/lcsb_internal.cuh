@@ -110,6 +110,39 @@ __host__ __device__ inline uint64_t global_of_local(uint32_t shard, uint64_t loc
   return s;
 }
 
+// Quarter table (kern_bin2q.cu): the half table cut into blocks of 4^K entries; map[block] =
+// (slot << 2) | mode, mode 0 = stored here (canonical), 1 = read through the string swap s,
+// 2 = through psi = complement o swap, from the block stored at `slot`.
+struct Bin2QArgs {
+  const void* src;  // input quarter table
+  void* dst;        // output quarter table (sweep mode)
+  const uint32_t* map;
+  int ell;
+  int K;
+  const unsigned long long* red_in;
+  unsigned long long* red_out;
+};
+
+__host__ __device__ inline uint64_t pairswap_hd(uint64_t v) {
+  return ((v & 0xAAAAAAAAAAAAAAAAull) >> 1) | ((v & 0x5555555555555555ull) << 1);
+}
+// partner of half-table block `beta` (prefix of PL = 2(l-K) bits, top bit a_0 = 0 implicit):
+// Q0 blocks (b_0 = 0) pair under the string swap, Q1 blocks (b_0 = 1) under psi
+__host__ __device__ inline uint64_t qblock_partner(uint64_t beta, int PL) {
+  const uint64_t pm = (1ull << PL) - 1;
+  const bool q1 = (beta >> (PL - 2)) & 1ull;
+  return pairswap_hd(q1 ? (~beta & pm) : beta) & pm;
+}
+// stored index of half-table index s (map as above)
+__host__ __device__ inline uint64_t qstored(const uint32_t* map, uint64_t s, int K) {
+  const uint32_t m = map[s >> (2 * K)];
+  const uint64_t kmask = (1ull << (2 * K)) - 1;
+  uint64_t e = s & kmask;
+  if ((m & 3u) == 1u) e = pairswap_hd(e) & kmask;
+  else if ((m & 3u) == 2u) e = pairswap_hd(~e & kmask) & kmask;
+  return ((uint64_t)(m >> 2) << (2 * K)) | e;
+}
+
 struct Q4Args {
   const void* g1;   // table one sweep back (W pass: the newest table)
   const void* g2;   // table two sweeps back (W pass: the newest table)
@@ -166,6 +199,11 @@ int bin2_tma_m(int dtype, int variant);
 int bin2_tma_direct(int dtype, int variant);
 cudaError_t launch_bin2_tma_wpass(const Bin2Args& a, int dtype, int M, cudaStream_t s, int sms);
 int bin2_tma_wpass_m(int dtype, int ell, int p);
+// variant 0: the default pipeline for tile 4^M; v > 0: the (M, stages, CTAs/SM) of table entry v
+cudaError_t launch_bin2q_sweep(const Bin2QArgs& a, int dtype, int M, int variant, cudaStream_t s,
+                               int sms);
+int bin2q_variant_m(int dtype, int variant);
+cudaError_t launch_bin2q_wpass(const Bin2QArgs& a, int dtype, int M, cudaStream_t s, int sms);
 cudaError_t launch_q4_sweep(const Q4Args& a, int dtype, cudaStream_t s, int sms);
 cudaError_t launch_q4_wpass(const Q4Args& a, int dtype, cudaStream_t s, int sms);
 int q4_min_ell();
@@ -174,9 +212,10 @@ cudaError_t launch_small(const GenericArgs& a, int dtype, bool wpass, cudaStream
 cudaError_t launch_red_init(unsigned long long* red, cudaStream_t s);
 cudaError_t launch_rdiff(const void* newest, const void* prev, uint64_t n, int dtype,
                          unsigned long long* red, cudaStream_t s, int sms);
-// tabs[k]: the table of shard k (unsharded: tabs[0]); p = log2(shards)
+// tabs[k]: the table of shard k (unsharded: tabs[0]); p = log2(shards); qmap != NULL: quarter
+// table with blocks of 4^K
 cudaError_t launch_expand(const void* const* tabs, int p, int dtype, int symmetric, int ell,
-                          uint64_t first, uint64_t count, const uint64_t* idx, double* out,
-                          cudaStream_t s);
+                          const uint32_t* qmap, int K, uint64_t first, uint64_t count,
+                          const uint64_t* idx, double* out, cudaStream_t s);
 
 }  // namespace lcsbk

@@ -34,7 +34,7 @@ class LcsbConfig(ctypes.Structure):
                 ("stream", ctypes.c_void_p), ("alloc", _ALLOC_FN), ("free_", _FREE_FN),
                 ("alloc_ctx", ctypes.c_void_p), ("shards", ctypes.c_int32),
                 ("shard", ctypes.c_int32), ("virtual_shards", ctypes.c_int32),
-                ("nccl_id", ctypes.c_void_p)]
+                ("nccl_id", ctypes.c_void_p), ("block_log4", ctypes.c_int32)]
 
 
 class LcsbBound(ctypes.Structure):
@@ -48,7 +48,7 @@ class LcsbBound(ctypes.Structure):
 # every symbol include/lcsb.h declares (checked by tests/test_abi.py)
 EXPORTS = ["lcsb_config_init", "lcsb_required_bytes", "lcsb_create", "lcsb_create_ex",
            "lcsb_reset", "lcsb_sweep", "lcsb_bound", "lcsb_table", "lcsb_table_gather",
-           "lcsb_nccl_unique_id", "lcsb_shard_locate", "lcsb_sweeps_done", "lcsb_num_shards",
+           "lcsb_nccl_unique_id", "lcsb_shard_locate", "lcsb_quarter_locate", "lcsb_sweeps_done", "lcsb_num_shards",
            "lcsb_num_states", "lcsb_stored_states", "lcsb_device_bytes", "lcsb_kernel_in_use",
            "lcsb_launch_count", "lcsb_last_error", "lcsb_destroy"]
 NCCL_ID_BYTES = 128
@@ -96,6 +96,10 @@ def load_library():
                                       ctypes.POINTER(ctypes.c_int32),
                                       ctypes.POINTER(ctypes.c_uint64)]
     lib.lcsb_shard_locate.restype = ctypes.c_int
+    lib.lcsb_quarter_locate.argtypes = [ctypes.c_int32, ctypes.c_int32, ctypes.c_uint64,
+                                        ctypes.POINTER(ctypes.c_uint64),
+                                        ctypes.POINTER(ctypes.c_uint64)]
+    lib.lcsb_quarter_locate.restype = ctypes.c_int
     for name, rt in [("lcsb_sweeps_done", ctypes.c_int64), ("lcsb_num_states", ctypes.c_uint64),
                      ("lcsb_num_shards", ctypes.c_int32),
                      ("lcsb_stored_states", ctypes.c_uint64),
@@ -148,7 +152,8 @@ class _TorchAllocator:
 
 
 def make_config(sigma, d, ell, dtype="f32", form="auto", rmode="max", symmetry=-1,
-                kernel="auto", shards=1, shard=0, virtual_shards=False) -> LcsbConfig:
+                kernel="auto", shards=1, shard=0, virtual_shards=False,
+                block_log4=0) -> LcsbConfig:
     cfg = LcsbConfig()
     load_library().lcsb_config_init(ctypes.byref(cfg))
     cfg.sigma, cfg.d, cfg.ell = sigma, d, ell
@@ -160,13 +165,14 @@ def make_config(sigma, d, ell, dtype="f32", form="auto", rmode="max", symmetry=-
     cfg.shards = int(shards)
     cfg.shard = int(shard)
     cfg.virtual_shards = 1 if virtual_shards else 0
+    cfg.block_log4 = int(block_log4)
     return cfg
 
 
 def lcsb_required_bytes(sigma, d, ell, dtype="f32", form="auto", symmetry=-1,
-                        kernel="auto", shards=1, virtual_shards=True) -> int:
+                        kernel="auto", shards=1, virtual_shards=True, block_log4=0) -> int:
     cfg = make_config(sigma, d, ell, dtype, form, "max", symmetry, kernel, shards, 0,
-                      virtual_shards)
+                      virtual_shards, block_log4)
     return int(load_library().lcsb_required_bytes(ctypes.byref(cfg)))
 
 
@@ -189,7 +195,7 @@ class Lcsb:
 
     def __init__(self, sigma, d, ell, dtype="f32", form="auto", rmode="max", symmetry=-1,
                  kernel="auto", stream=None, torch_allocator=True, shards=1, shard=0,
-                 virtual_shards=False, nccl_id: bytes | None = None):
+                 virtual_shards=False, nccl_id: bytes | None = None, block_log4: int = 0):
         import torch
         if not torch.cuda.is_available():
             raise LcsbError(4, "no CUDA device (the library has no CPU path)")
@@ -198,7 +204,7 @@ class Lcsb:
         self.device = torch.cuda.current_device()
         self.stream = stream if stream is not None else torch.cuda.current_stream()
         cfg = make_config(sigma, d, ell, dtype, form, rmode, symmetry, kernel, shards, shard,
-                          virtual_shards)
+                          virtual_shards, block_log4)
         cfg.stream = ctypes.c_void_p(self.stream.cuda_stream)
         self._nccl_id = None
         if nccl_id is not None:
@@ -267,7 +273,8 @@ class Lcsb:
 
     @property
     def kernel_in_use(self) -> str:
-        return {1: "generic", 2: "bin2", 3: "q4", 4: "small"}.get(int(self._lib.lcsb_kernel_in_use(self._h)), "?")
+        return {1: "generic", 2: "bin2", 3: "q4", 4: "small", 5: "bin2q"}.get(
+            int(self._lib.lcsb_kernel_in_use(self._h)), "?")
 
     @property
     def launch_count(self) -> int:
@@ -333,3 +340,12 @@ def lcsb_table_gather(h: Lcsb, idx, which=0) -> np.ndarray:
 
 def lcsb_destroy(h: Lcsb):
     h.destroy()
+
+
+def lcsb_quarter_locate(ell: int, block_log4: int, logical: int):
+    """(stored index, stored entries) of a logical binary state in the quarter table (host-only)."""
+    st = ctypes.c_uint64()
+    n = ctypes.c_uint64()
+    _check(load_library().lcsb_quarter_locate(int(ell), int(block_log4), int(logical),
+                                              ctypes.byref(st), ctypes.byref(n)))
+    return int(st.value), int(n.value)

@@ -258,7 +258,7 @@ def test_config3_sigma4_l8_sampled_after_3_sweeps():
 def test_config4_binary_l17_sampled_after_3_sweeps():
     """BASELINE config 4 (2^34 states, fp32 half table): 2^20 seeded states after 3 sweeps."""
     Lcsb = _lcsb()
-    h = Lcsb(2, 2, 17, dtype="f32")
+    h = Lcsb(2, 2, 17, dtype="f32", symmetry=1)  # the quarter table: tests/test_quarter.py
     assert h.kernel_in_use == "bin2"
     idx = _splitmix(SEED, 1 << 20, 1 << 34)
     h.sweep(3)

@@ -1,0 +1,173 @@
+"""The quarter table (symmetry = 2, kern_bin2q.cu): one stored entry per orbit of
+{id, complement, string swap, complement o swap} of the binary two-array iterate.
+
+CPU: the library's host-side layout (lcsb_quarter_locate) against orbits enumerated here from the
+paper's state encoding (interleaved pair), complement (Eq. comp_eq,
+PAPER.md:404-411) and string swap (reading R19) -- no code shared with the library.
+GPU: the quarter-table kernels against the oracle, element by element (fp32 bit-exact, fp64
+1e-12 relative), across block sizes, tile sizes and the sampled config-4 check.
+"""
+import numpy as np
+import pytest
+
+from tests.conftest import has_cuda
+
+from paper_2407_10925_b200 import lcsb as L
+
+
+def _decode(x, ell):
+    a = [(x >> (2 * (ell - 1 - k) + 1)) & 1 for k in range(ell)]
+    b = [(x >> (2 * (ell - 1 - k))) & 1 for k in range(ell)]
+    return a, b
+
+
+def _encode(a, b):
+    ell = len(a)
+    return sum((a[k] << (2 * (ell - 1 - k) + 1)) | (b[k] << (2 * (ell - 1 - k))) for k in range(ell))
+
+
+def _orbit(x, ell):
+    a, b = _decode(x, ell)
+    ca, cb = [1 - c for c in a], [1 - c for c in b]
+    return min(_encode(a, b), _encode(ca, cb), _encode(b, a), _encode(cb, ca))
+
+
+@pytest.mark.parametrize("ell,K", [(3, 2), (4, 2), (4, 3), (5, 2), (5, 3), (6, 2), (6, 3),
+                                   (6, 5), (7, 3), (7, 4)])
+def test_quarter_layout_holds_one_orbit_per_entry(ell, K):
+    L.load_library()
+    owner = {}
+    n_stored = None
+    for x in range(1 << (2 * ell)):
+        st, n = L.lcsb_quarter_locate(ell, K, x)
+        n_stored = n
+        orb = _orbit(x, ell)
+        assert owner.setdefault(st, orb) == orb, (x, st)  # never two orbits in one entry
+    assert sorted(owner) == list(range(n_stored))        # every stored entry is used
+    # size: (4^(l-K-1) + 2^(l-K-1)) blocks of 4^K -> a quarter of 4^l plus the swap-fixed blocks
+    assert n_stored == ((1 << (2 * (ell - K - 1))) + (1 << (ell - K - 1))) << (2 * K)
+    assert len(set(owner.values())) == len({_orbit(x, ell) for x in range(1 << (2 * ell))})
+
+
+def test_quarter_layout_orbit_mates_share_outside_fixed_blocks():
+    """At l = 8, K = 3 all but a 2^-(l-K-1) fraction of the orbits occupy one entry."""
+    L.load_library()
+    ell, K = 8, 3
+    entries_per_orbit = {}
+    for x in range(1 << (2 * ell)):
+        st, n = L.lcsb_quarter_locate(ell, K, x)
+        entries_per_orbit.setdefault(_orbit(x, ell), set()).add(st)
+    doubled = sum(1 for s in entries_per_orbit.values() if len(s) > 1)
+    assert all(len(s) <= 2 for s in entries_per_orbit.values())
+    assert doubled <= len(entries_per_orbit) / (1 << (ell - K - 2))
+
+
+def test_quarter_layout_rejects_bad_arguments():
+    L.load_library()
+    for ell, K, x in [(2, 2, 0), (5, 1, 0), (5, 5, 0), (5, 3, 1 << 10)]:
+        with pytest.raises(L.LcsbError):
+            L.lcsb_quarter_locate(ell, K, x)
+
+
+def test_quarter_required_bytes_is_about_half_of_half_table():
+    L.load_library()
+    half = L.lcsb_required_bytes(2, 2, 17, "f32", symmetry=1)
+    quarter = L.lcsb_required_bytes(2, 2, 17, "f32", symmetry=2)
+    assert 0.5 < quarter / half < 0.51
+    # l = 18 in fp32 fits one B200 as a quarter table (2 x 64 GiB + map), not as a half table
+    assert L.lcsb_required_bytes(2, 2, 18, "f32", symmetry=2) < 140 * 2 ** 30
+    assert L.lcsb_required_bytes(2, 2, 18, "f32", symmetry=1) > 256 * 2 ** 30 - 1
+    # sharding and the quarter table are exclusive; KS form has no quarter table
+    assert L.lcsb_required_bytes(2, 2, 17, "f32", symmetry=2, shards=2) == 0
+    assert L.lcsb_required_bytes(2, 2, 17, "f32", form="ks", symmetry=2) == 0
+
+
+# ------------------------------------------------------------------------------------ GPU
+
+def _cmp(gpu_tab, ref, dtype):
+    if dtype == "f32":
+        assert np.array_equal(gpu_tab, ref), np.max(np.abs(gpu_tab - ref))
+    else:
+        np.testing.assert_allclose(gpu_tab, ref, rtol=1e-12, atol=1e-300)
+
+
+def _cmp_bound(gb, rb, dtype):
+    for key in ("R_max", "R_min", "E_at_Rmax", "E_at_Rmin", "bound_at_Rmax", "bound_at_Rmin"):
+        g, r = getattr(gb, key), rb[key]
+        if dtype == "f32":
+            assert g == r, (key, g, r)
+        else:
+            assert abs(g - r) <= 1e-12 * max(1.0, abs(r)), (key, g, r)
+
+
+@pytest.mark.gpu
+@pytest.mark.skipif(not has_cuda(), reason="needs a CUDA device")
+@pytest.mark.parametrize("ell,K,dtype,sweeps", [
+    (3, 2, "f32", 10), (3, 2, "f64", 10), (4, 2, "f64", 14), (4, 3, "f32", 14),
+    (5, 2, "f32", 20), (5, 4, "f64", 20), (6, 3, "f32", 25), (6, 2, "f64", 25),
+    (7, 3, "f32", 30), (7, 6, "f32", 12), (8, 4, "f64", 30), (8, 5, "f32", 30),
+    (9, 5, "f32", 40), (9, 6, "f64", 24), (10, 6, "f32", 24), (10, 7, "f32", 24),
+])
+def test_quarter_matches_oracle(ell, K, dtype, sweeps):
+    from oracle import ft_oracle as fo
+    h = L.Lcsb(2, 2, ell, dtype=dtype, symmetry=2, block_log4=K)
+    assert h.kernel_in_use == "bin2q"
+    run = fo.Run(2, 2, ell, "two_array", dtype)
+    for s in range(1, sweeps + 1):
+        h.sweep(1)
+        run.sweep(1)
+        if s in (1, 2, 3, sweeps // 2, sweeps):
+            _cmp(h.table(0), run.newest, dtype)
+            _cmp(h.table(1), run.prev, dtype)
+    _cmp_bound(h.bound(), run.bound(), dtype)
+    h.destroy()
+
+
+@pytest.mark.gpu
+@pytest.mark.skipif(not has_cuda(), reason="needs a CUDA device")
+@pytest.mark.parametrize("dtype", ["f32", "f64"])
+def test_quarter_equals_half_table_l13(dtype):
+    """Quarter and half table give the same values (fp32: bitwise) on 2^20 sampled states and
+    the same bound, l = 13 (auto block size), 30 sweeps."""
+    from seeded_inputs import splitmix64_indices
+    a = L.Lcsb(2, 2, 13, dtype=dtype, symmetry=2)
+    b = L.Lcsb(2, 2, 13, dtype=dtype, symmetry=1)
+    assert a.kernel_in_use == "bin2q" and b.kernel_in_use == "bin2"
+    assert a.stored_states * 2 < b.stored_states * 1.04  # + the swap-fixed blocks (1/32)
+    a.sweep(30)
+    b.sweep(30)
+    idx = splitmix64_indices(0x240710925, 1 << 20, 1 << 26)
+    _cmp(a.table_gather(idx), b.table_gather(idx), dtype)
+    ba, bb = a.bound(), b.bound()
+    for key in ("R_max", "R_min", "bound_at_Rmax", "bound_at_Rmin"):
+        g, r = getattr(ba, key), getattr(bb, key)
+        assert (g == r) if dtype == "f32" else abs(g - r) <= 1e-12, (key, g, r)
+    a.destroy()
+    b.destroy()
+
+
+@pytest.mark.gpu
+@pytest.mark.skipif(not has_cuda(), reason="needs a CUDA device")
+def test_quarter_config4_sampled_after_3_sweeps():
+    """BASELINE config 4 (2^34 states, fp32) on the quarter table: 2^20 seeded states after 3
+    (and 2) sweeps against the oracle's sampled mode, bit-exact."""
+    from oracle import ft_oracle as fo
+    from seeded_inputs import splitmix64_indices
+    h = L.Lcsb(2, 2, 17, dtype="f32", symmetry=2)
+    assert h.kernel_in_use == "bin2q"
+    idx = splitmix64_indices(0x240710925, 1 << 20, 1 << 34)
+    h.sweep(3)
+    assert np.array_equal(h.table_gather(idx),
+                          fo.sample_values(2, 2, 17, 3, idx, form="two_array", dtype="f32"))
+    assert np.array_equal(h.table_gather(idx, which=1),
+                          fo.sample_values(2, 2, 17, 2, idx, form="two_array", dtype="f32"))
+    h.destroy()
+
+
+@pytest.fixture(autouse=True)
+def _release_cached_memory():
+    yield
+    if has_cuda():
+        import torch
+        torch.cuda.synchronize()
+        torch.cuda.empty_cache()

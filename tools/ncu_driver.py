@@ -16,13 +16,15 @@ def main():
     ap.add_argument("--workload", default="config4", choices=sorted(WORKLOADS))
     ap.add_argument("--sweeps", type=int, default=3)
     ap.add_argument("--ell", type=int, default=None, help="override l (same kernel, smaller table)")
+    ap.add_argument("--symmetry", type=int, default=-1, help="-1 auto, 1 half, 2 quarter table")
     args = ap.parse_args()
     import torch
     from paper_2407_10925_b200 import Lcsb
     w = dict(WORKLOADS[args.workload])
     if args.ell:
         w["ell"] = args.ell
-    h = Lcsb(w["sigma"], w["d"], w["ell"], dtype=w["dtype"], form=w["form"])
+    h = Lcsb(w["sigma"], w["d"], w["ell"], dtype=w["dtype"], form=w["form"],
+             symmetry=args.symmetry)
     h.sweep(args.sweeps)
     b = h.bound()
     torch.cuda.synchronize()
