@@ -193,7 +193,8 @@ def run_ours(args, w, ws, rank, local):
     achieved = alg_bytes / (launch_ms / 1e3) / 1e9
     design_bytes = design_bytes_per_sweep(w, stored // ws, kernel_name)
     traffic = None
-    tpath = os.path.join(ROOT, "profiles", f"traffic_{args.workload}.json")
+    # ncu DRAM bytes per launch of this workload's sweep kernel (tools/summarize_ncu.py)
+    tpath = os.path.join(ROOT, "profiles", f"traffic_{args.workload}_{kernel_name}.json")
     if os.path.exists(tpath):
         try:
             with open(tpath) as f:

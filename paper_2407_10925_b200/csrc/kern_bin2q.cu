@@ -57,7 +57,10 @@ template <typename T, int M, int S, bool WMODE>
 struct QCfg {
   static constexpr uint32_t TT = 1u << (2 * M);  // Q1 outputs per tile
   static constexpr uint32_t WIN = 2 * TT;        // entries per adv_b window
-  static constexpr uint32_t STAGE = 2 * WIN;     // both windows of the tile pair
+  // W pass: u at the item's stored outputs is staged by TMA too (one Q1 run of T, four Q0 runs
+  // of T/2) when the runs are whole 16-byte multiples
+  static constexpr bool UTMA = WMODE && (TT / 2 * sizeof(T) >= 16);
+  static constexpr uint32_t STAGE = 2 * WIN + (UTMA ? 3 * TT : 0);
   static constexpr size_t SMEM =
       (size_t)S * STAGE * sizeof(T) + (size_t)S * sizeof(uint64_t) + (size_t)S * 8 * sizeof(uint64_t);
 };
@@ -148,17 +151,21 @@ __device__ __forceinline__ void wupd(double u, double f, double R0, double R1, d
 // (the complemented tail, row read reversed).  So each window entry is read from smem and
 // widened to fp64 once.  The A/B load order alternates across threads so each 128-bit smem load
 // is conflict-free (2-way for permuted x windows).
+// us != nullptr (W pass): u of the row run at us[r], of the mirror run at us[half_rows + ...]
 template <typename T, int MODE, bool WMODE>
 __device__ __forceinline__ void q0_group(const double (&G)[4], uint32_t r, uint32_t half_rows,
                                          const T* src, T* dst, uint64_t of, uint64_t om,
-                                         double R0, double R1, double& wm0, double& wm1) {
+                                         const T* us, double R0, double R1, double& wm0,
+                                         double& wm1) {
   const double v0 = G[comp<MODE>(0)], v1 = G[comp<MODE>(1)], v2 = G[comp<MODE>(2)],
                v3 = G[comp<MODE>(3)];
   const double fwd = q0_val(v0, v1, v2, v3);
   const double mir = q0_val(v3, v2, v1, v0);
   if (WMODE) {
-    if (of != kNone) wupd((double)src[of + r], fwd, R0, R1, wm0, wm1);
-    if (om != kNone) wupd((double)src[om + (half_rows - 1 - r)], mir, R0, R1, wm0, wm1);
+    const uint32_t rm = half_rows - 1 - r;
+    if (of != kNone) wupd(us ? (double)us[r] : (double)src[of + r], fwd, R0, R1, wm0, wm1);
+    if (om != kNone)
+      wupd(us ? (double)us[half_rows + rm] : (double)src[om + rm], mir, R0, R1, wm0, wm1);
   } else {
     if (of != kNone) dst[of + r] = (T)fwd;
     if (om != kNone) dst[om + (half_rows - 1 - r)] = (T)mir;
@@ -167,8 +174,8 @@ __device__ __forceinline__ void q0_group(const double (&G)[4], uint32_t r, uint3
 
 template <typename T, uint32_t TT, int MW, int MP, bool WMODE>
 __device__ __forceinline__ void pair_quads(const T* bw, const T* bp, const T* src, T* dst,
-                                           const uint64_t* meta, bool self, double R0,
-                                           double R1, double& wm0, double& wm1) {
+                                           const uint64_t* meta, bool self, const T* us,
+                                           double R0, double R1, double& wm0, double& wm1) {
   constexpr uint32_t SX = (MW == 0) ? 2 : 0, SP = (MP == 0) ? 2 : 1;
   const uint64_t oQ1 = meta[1], oQ1p = meta[2];
   const uint64_t of = meta[3], om = meta[4], opf = meta[5], opm = meta[6];
@@ -201,14 +208,14 @@ __device__ __forceinline__ void pair_quads(const T* bw, const T* bp, const T* sr
     // psi(o0 + k) sits at oQ1p + qb + pairswap(3 - k): the quad reversed as (3, 1, 2, 0)
     const uint32_t qb = pairswap32(~o0 & (TT - 1) & ~3u);
     if (WMODE) {
+      // W(psi x) = W(x): both stored copies (psi-fixed blocks) hold the same u
       double uu[4];
       if (oQ1 != kNone) {
-        ld4(src + oQ1 + o0, uu);
+        ld4(us ? us + o0 : src + oQ1 + o0, uu);
 #pragma unroll
         for (int k = 0; k < 4; ++k) wupd(uu[k], v[k], R0, R1, wm0, wm1);
-      }
-      if (oQ1p != kNone) {
-        ld4(src + oQ1p + qb, uu);
+      } else if (oQ1p != kNone) {
+        ld4(us ? us + qb : src + oQ1p + qb, uu);
         wupd(uu[3], v[0], R0, R1, wm0, wm1);
         wupd(uu[1], v[1], R0, R1, wm0, wm1);
         wupd(uu[2], v[2], R0, R1, wm0, wm1);
@@ -219,13 +226,16 @@ __device__ __forceinline__ void pair_quads(const T* bw, const T* bp, const T* sr
       if (oQ1p != kNone) st4(dst + oQ1p + qb, v[3], v[1], v[2], v[0]);
     }
     // Q0 rows of the four groups
+    const T* ux = us ? us + TT : nullptr;
+    const T* up = us ? us + 2 * TT : nullptr;
     if (rows_x) {
-      q0_group<T, MW, WMODE>(A, g >> 2, TT / 2, src, dst, of, om, R0, R1, wm0, wm1);
-      q0_group<T, MW, WMODE>(B, (g >> 2) + 1, TT / 2, src, dst, of, om, R0, R1, wm0, wm1);
+      q0_group<T, MW, WMODE>(A, g >> 2, TT / 2, src, dst, of, om, ux, R0, R1, wm0, wm1);
+      q0_group<T, MW, WMODE>(B, (g >> 2) + 1, TT / 2, src, dst, of, om, ux, R0, R1, wm0, wm1);
     }
     if (rows_p) {
-      q0_group<T, MP, WMODE>(Ap, u >> 2, TT / 2, src, dst, opf, opm, R0, R1, wm0, wm1);
-      q0_group<T, MP, WMODE>(Bp, (u >> 2) + 1, TT / 2, src, dst, opf, opm, R0, R1, wm0, wm1);
+      q0_group<T, MP, WMODE>(Ap, u >> 2, TT / 2, src, dst, opf, opm, up, R0, R1, wm0, wm1);
+      q0_group<T, MP, WMODE>(Bp, (u >> 2) + 1, TT / 2, src, dst, opf, opm, up, R0, R1, wm0,
+                             wm1);
     }
   }
 }
@@ -268,7 +278,7 @@ __device__ __forceinline__ void qlookup(const QGeo& g, const uint32_t* __restric
 // metadata: meta[0] = window modes (bits 0-1: window t, 2-3: window psi t, bit 4: self pair),
 // meta[1..6] = stored run starts (Q1 t, Q1 psi t, rows t, mirrors t, rows psi t, mirrors psi t;
 // kNone = not stored).
-template <typename T, int M>
+template <typename T, int M, bool UTMA>
 __device__ __forceinline__ void qissue(const QGeo& g, const QItem& it, uint64_t tau, T* buf,
                                        uint64_t* bar, uint64_t* meta, const T* src) {
   constexpr uint32_t TT = 1u << (2 * M), LOG = 2 * M;
@@ -286,7 +296,21 @@ __device__ __forceinline__ void qissue(const QGeo& g, const QItem& it, uint64_t 
   meta[4] = qrun(g, it.m[5], ym);
   meta[5] = self ? kNone : qrun(g, it.m[6], ypf);
   meta[6] = self ? kNone : qrun(g, it.m[7], ypm);
-  mbar_expect_tx(bar, 2 * 2 * TT * (uint32_t)sizeof(T));
+  uint32_t bytes = 2 * 2 * TT * (uint32_t)sizeof(T);
+  if (UTMA) {  // u runs: [Q1 (t if stored, else psi t) | rows t | mirrors t | rows psi t | mirrors]
+    if (meta[1] != kNone || meta[2] != kNone) bytes += TT * (uint32_t)sizeof(T);
+    for (int k = 3; k < 7; ++k)
+      if (meta[k] != kNone) bytes += TT / 2 * (uint32_t)sizeof(T);
+  }
+  mbar_expect_tx(bar, bytes);
+  if (UTMA) {
+    T* us = buf + 4 * TT;
+    const uint64_t q = meta[1] != kNone ? meta[1] : meta[2];
+    if (q != kNone) tma_load_1d(us, src + q, TT * (uint32_t)sizeof(T), bar);
+    for (int k = 3; k < 7; ++k)
+      if (meta[k] != kNone)
+        tma_load_1d(us + TT + (k - 3) * (TT / 2), src + meta[k], TT / 2 * (uint32_t)sizeof(T), bar);
+  }
 #pragma unroll
   for (int k = 0; k < 2; ++k) {
     const uint32_t m = k ? mp : mw;
@@ -346,7 +370,7 @@ __global__ void __launch_bounds__(kThreads, MINB) bin2q_kernel(Bin2QArgs a) {
     pc = qnext(g, blockIdx.x, G, LOG);
     if (pc < g.ntiles) qlookup<M>(g, map, pc, pit);
     for (int s = 0; s < S && pc < g.ntiles; ++s) {
-      qissue<T, M>(g, pit, pc, in + (size_t)s * C::STAGE, &bars[s], metas + 8 * s, src);
+      qissue<T, M, C::UTMA>(g, pit, pc, in + (size_t)s * C::STAGE, &bars[s], metas + 8 * s, src);
       pc = qnext(g, pc + G, G, LOG);
       if (pc < g.ntiles) qlookup<M>(g, map, pc, pit);
     }
@@ -366,8 +390,9 @@ __global__ void __launch_bounds__(kThreads, MINB) bin2q_kernel(Bin2QArgs a) {
     const bool self = (modes & 16u) != 0;
     const T* bw = buf;
     const T* bp = buf + WIN;
+    const T* us = C::UTMA ? buf + 2 * WIN : nullptr;
 #define LCSB_Q1(MW, MP) \
-  pair_quads<T, TT, MW, MP, WMODE>(bw, bp, src, dst, meta, self, R0, R1, wm0, wm1)
+  pair_quads<T, TT, MW, MP, WMODE>(bw, bp, src, dst, meta, self, us, R0, R1, wm0, wm1)
     switch (mw * 3 + mp) {
       case 0: LCSB_Q1(0, 0); break;
       case 1: LCSB_Q1(0, 1); break;
@@ -382,7 +407,7 @@ __global__ void __launch_bounds__(kThreads, MINB) bin2q_kernel(Bin2QArgs a) {
 #undef LCSB_Q1
     __syncthreads();  // stage s (data and metadata) is free again
     if (tid == 0 && pc < g.ntiles) {
-      qissue<T, M>(g, pit, pc, buf, &bars[s], metas + 8 * s, src);
+      qissue<T, M, C::UTMA>(g, pit, pc, buf, &bars[s], metas + 8 * s, src);
       pc = qnext(g, pc + G, G, LOG);
       if (pc < g.ntiles) qlookup<M>(g, map, pc, pit);
     }
@@ -417,6 +442,8 @@ cudaError_t launch_q(const Bin2QArgs& a, cudaStream_t s, int sms) {
 
 template <bool WMODE>
 cudaError_t dispatch_q(const Bin2QArgs& a, int dtype, int M, cudaStream_t s, int sms) {
+  if (WMODE && dtype == LCSB_F32 && M == 6) return launch_q<float, 6, 1, true, 2>(a, s, sms);
+  if (WMODE && dtype == LCSB_F64 && M == 5) return launch_q<double, 5, 1, true, 3>(a, s, sms);
   if (dtype == LCSB_F32) {
     switch (M) {
       case 6: return launch_q<float, 6, 1, WMODE, 3>(a, s, sms);  // A/B: variant 10

@@ -45,7 +45,7 @@ struct lcsb {
   size_t tab_bytes;   // bytes per shard table
   int cur;            // ring slot of the newest table
   unsigned long long* red;       // device reduction slots
-  unsigned long long* red_host;  // pinned
+  unsigned long long red_host[kRedSlots];  // pageable: a 32-byte read-back needs no pinning
   ncclComm_t comm;
   int* barrier_buf;
   // CUDA-graph replay of G consecutive sweeps for launch-latency-bound (small) tables
@@ -412,7 +412,6 @@ extern "C" void lcsb_destroy(lcsb_t* h) {
     if (h->graph[i]) cudaGraphExecDestroy(h->graph[i]);
   if (h->cap_stream) cudaStreamDestroy(h->cap_stream);
   if (h->comm) ncclCommDestroy(h->comm);
-  if (h->red_host) cudaFreeHost(h->red_host);
   cudaStreamSynchronize(s);
   delete h;
 }
@@ -540,7 +539,7 @@ extern "C" int lcsb_create_ex(const lcsb_config* cfg, lcsb_t** out) {
     }
   }
   h->red = (unsigned long long*)dev_alloc(h, 256);
-  if (!h->red || cudaMallocHost(&h->red_host, 256) != cudaSuccess) {
+  if (!h->red) {
     lcsb_destroy(h);
     return set_err(nullptr, LCSB_ECAPACITY, "scratch allocation failed");
   }

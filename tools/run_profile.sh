@@ -4,7 +4,7 @@
 #   bash tools/run_profile.sh config4 bin2_tma_kernel
 set -u
 WL=${1:-config4}
-KREGEX=${2:-bin2_tma_kernel}
+KREGEX=${2:-bin2q_kernel}
 OUT=gpurun_out
 mkdir -p $OUT
 BENCH="python bench.py --workload $WL --steps 1 --warmup 3 --no-cpu-baseline"

@@ -1,5 +1,5 @@
 """Summarise ncu outputs into profiles/ (run here, no GPU):
-  python tools/summarize_ncu.py <round> <workload>
+  python tools/summarize_ncu.py <round> <workload> [<kernel tag>]
 reads gpurun_out/launches_<wl>.csv and gpurun_out/prof_<wl>.ncu-rep, writes
 profiles/<round>_<wl>_launches.csv (per-kernel totals and shares), profiles/<round>_<wl>_ncu.json
 (key --set full metrics of the captured launch) and profiles/traffic_<wl>.json (the DRAM bytes
@@ -26,6 +26,8 @@ WANT = ["dram__bytes_read.sum", "dram__bytes_write.sum", "gpu__time_duration.sum
 
 def main():
     rnd, wl = sys.argv[1], sys.argv[2]
+    tag = sys.argv[3] if len(sys.argv) > 3 else ""  # kernel short name (bench: kernel_in_use)
+    base = f"{rnd}_{wl}_{tag}" if tag else f"{rnd}_{wl}"
     out = os.path.join(ROOT, "profiles")
     os.makedirs(out, exist_ok=True)
     txt = open(os.path.join(ROOT, "gpurun_out", f"launches_{wl}.csv")).read()
@@ -35,7 +37,7 @@ def main():
         agg[r["Kernel Name"]][0] += 1
         agg[r["Kernel Name"]][1] += float(r["Metric Value"])
     tot = sum(v[1] for v in agg.values())
-    with open(os.path.join(out, f"{rnd}_{wl}_launches.csv"), "w") as f:
+    with open(os.path.join(out, f"{base}_launches.csv"), "w") as f:
         f.write("kernel,launches,total_ms,avg_ms,share_pct\n")
         for k, (n, t) in sorted(agg.items(), key=lambda x: -x[1][1]):
             f.write(f'"{k}",{n},{t / 1e6:.3f},{t / n / 1e6:.4f},{100 * t / tot:.2f}\n')
@@ -52,12 +54,13 @@ def main():
     summary = {"round": rnd, "workload": wl, "kernel": m.get("Kernel Name", ("?", ""))[0],
                "metrics": {k: f"{v} {u}".strip() for k, (v, u) in m.items() if k != "Kernel Name"},
                "dram_bytes_per_launch": dram}
-    json.dump(summary, open(os.path.join(out, f"{rnd}_{wl}_ncu.json"), "w"), indent=1)
+    json.dump(summary, open(os.path.join(out, f"{base}_ncu.json"), "w"), indent=1)
     json.dump({"workload": wl, "round": rnd, "kernel": summary["kernel"],
                "dram_bytes_per_launch": dram, "source": f"profiles/{rnd}_{wl}_ncu.json"},
-              open(os.path.join(out, f"traffic_{wl}.json"), "w"), indent=1)
+              open(os.path.join(out, f"traffic_{wl}_{tag}.json" if tag else f"traffic_{wl}.json"), "w"),
+              indent=1)
     print(json.dumps(summary, indent=1))
-    print(open(os.path.join(out, f"{rnd}_{wl}_launches.csv")).read())
+    print(open(os.path.join(out, f"{base}_launches.csv")).read())
 
 
 if __name__ == "__main__":
