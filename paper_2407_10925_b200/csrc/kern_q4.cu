@@ -14,15 +14,23 @@
 //   y = h_a<<(4l-2) | (t & A) | ((t & B) << 4) | c     (A / B = a / b digit bits of each group).
 //
 // B200 design: a unit is 16^M consecutive tails t for all 16 head pairs
-// (16 x 16^M outputs).  Its P rows are one contiguous run of 16 x 16^M entries of g2; for each
-// h_a its adv_b reads are one contiguous window of 4 x 16^M entries of g1.  adv_a is taken from
-// the string swap W(a,b) = W(b,a): adv_a(h_a,h_b,t) = adv_b(h_b,h_a,swap(t)), and swap maps the
-// unit onto the unit of swapped tails (offset i -> ds(i), the two digits of every group
-// exchanged).  One CTA takes the pair {unit, swap(unit)}: TMA bulk-loads its 2 x (16 + 4 x 4)
-// x 16^M entries into shared memory (mbarrier-completed, S stages), then writes all 32 x 16^M
-// outputs with coalesced stores.  Per sweep g1 and g2 are each read once and the new table
-// written once: 3 x table bytes, the compulsory traffic of the KS form.
+// (16 x 16^M outputs).  For each h_a its adv_b reads are one contiguous window of 4 x 16^M
+// entries of g1.  adv_a is taken from the string swap W(a,b) = W(b,a):
+// adv_a(h_a,h_b,t) = adv_b(h_b,h_a,swap(t)), and swap maps the unit onto the unit of swapped
+// tails (offset i -> ds(i), the two digits of every group exchanged).  One CTA takes the pair
+// {unit, swap(unit)}, TMA bulk-loads it into shared memory (mbarrier-completed, S stages), and
+// writes all 32 x 16^M outputs with coalesced stores.
+//
+// Pooled history: g2 (two sweeps back) is read ONLY through P, the mean of a 16-entry row, and
+// P depends only on the tails t.  So every sweep also writes the row means of the table it
+// produces (pout[x >> 4], fp64, N/16 entries: each output row of 16 is summed in Alg. 1's
+// order from the stored -- rounded -- values, in shared memory), and the sweep two later reads
+// those TT means per unit side instead of 16 TT entries of g2.  The full g2 table is never read,
+// so the ring holds 2 full tables (+ 3 mean arrays): per sweep read g1 + means, write the new
+// table + means = 2 x table + 2 x table/16 x 2 bytes ratio (9 B per state in fp32 instead of
+// 12 for the three-table KS ring).
 #include <math.h>
+#include <stdlib.h>
 
 #include "lcsb_internal.cuh"
 #include "tma.cuh"
@@ -64,13 +72,19 @@ __device__ __forceinline__ double sum4(const T* p, double sh) {
 template <typename T, int M, int S, bool WMODE = false>
 struct Q4Cfg {
   static constexpr uint32_t TT = 1u << (4 * M);  // tails per unit
-  static constexpr uint32_t PR = 16 * TT;        // g2 entries (rows) per unit
+  static constexpr uint32_t PR = TT * 8 / sizeof(T);  // the unit's TT row means (fp64), in T slots
   static constexpr uint32_t WB = 4 * TT;         // g1 entries per adv_b window
   static constexpr uint32_t UNIT = PR + 4 * WB;  // entries staged per unit
   // W pass: also u at the unit pair's 32 output runs (16 head pairs x T tails, per side)
   static constexpr uint32_t UOUT = WMODE ? 2 * 16 * TT : 0;
   static constexpr uint32_t STAGE = 2 * UNIT + UOUT;
-  static constexpr size_t SMEM = (size_t)S * STAGE * sizeof(T) + (size_t)S * sizeof(uint64_t);
+  // sweep: the unit pair's outputs staged for the row means of the new table, transposed so a
+  // row's 16 values are 16 "c-rows" apart: [side][head pair][c][NR + 1] (NR = TT/16 rows per
+  // head pair, +1 pad: stores and in-order row reads are bank-conflict-free)
+  static constexpr uint32_t NR = TT / 16;
+  static constexpr uint32_t OUTS = WMODE ? 0 : 2 * 16 * 16 * (NR + 1);
+  static constexpr size_t SMEM =
+      (size_t)S * STAGE * sizeof(T) + (size_t)OUTS * sizeof(T) + (size_t)S * sizeof(uint64_t);
 };
 
 struct Q4Geo {
@@ -91,7 +105,7 @@ __device__ __forceinline__ uint64_t q4_next(const Q4Geo& g, uint64_t c, uint64_t
 
 template <typename T, int M, int S, bool WMODE>
 __device__ __forceinline__ void q4_issue(const Q4Geo& g, uint64_t u, T* buf, uint64_t* bar,
-                                         const T* g1, const T* g2) {
+                                         const T* g1, const double* pin) {
   using C = Q4Cfg<T, M, S, WMODE>;
   mbar_expect_tx(bar, C::STAGE * (uint32_t)sizeof(T));
 #pragma unroll
@@ -99,7 +113,7 @@ __device__ __forceinline__ void q4_issue(const Q4Geo& g, uint64_t u, T* buf, uin
     const uint64_t uu = side ? digit_swap(u) : u;
     const uint64_t t0 = uu << (4 * M);
     T* ub = buf + side * C::UNIT;
-    tma_load_1d(ub, g2 + (t0 << 4), C::PR * sizeof(T), bar);
+    tma_load_1d(ub, pin + t0, C::TT * sizeof(double), bar);
     const uint64_t low = (t0 & kA4) | ((t0 & kB4) << 4);
 #pragma unroll
     for (int h = 0; h < 4; ++h) {
@@ -121,18 +135,19 @@ __device__ __forceinline__ void q4_issue(const Q4Geo& g, uint64_t u, T* buf, uin
 template <typename T, int M, int S, bool WMODE>
 __global__ void __launch_bounds__(kThreads) q4_kernel(Q4Args a) {
   using C = Q4Cfg<T, M, S, WMODE>;
-  using V4 = typename V4T<T>::type;
   constexpr uint32_t TT = C::TT;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   T* in = reinterpret_cast<T*>(smem_raw);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(in + (size_t)S * C::STAGE);
+  T* outs = in + (size_t)S * C::STAGE;  // Q4Cfg::OUTS layout (sweep only)
+  uint64_t* bars = reinterpret_cast<uint64_t*>(outs + C::OUTS);
 
   Q4Geo g;
   g.ell = a.ell;
   g.tail_bits = 4u * (uint32_t)(a.ell - 1);
   g.nunits = 1ull << (g.tail_bits - 4 * M);
   const T* g1 = reinterpret_cast<const T*>(a.g1);
-  const T* g2 = reinterpret_cast<const T*>(a.g2);
+  const double* pin = a.pin;
+  double* pout = a.pout;
   T* dst = reinterpret_cast<T*>(a.dst);
   const int tid = threadIdx.x;
   const uint64_t G = gridDim.x;
@@ -154,7 +169,7 @@ __global__ void __launch_bounds__(kThreads) q4_kernel(Q4Args a) {
   if (tid == 0) {
     pc = q4_next<M>(g, blockIdx.x, G);
     for (int s = 0; s < S && pc < g.nunits; ++s) {
-      q4_issue<T, M, S, WMODE>(g, pc, in + (size_t)s * C::STAGE, &bars[s], g1, g2);
+      q4_issue<T, M, S, WMODE>(g, pc, in + (size_t)s * C::STAGE, &bars[s], g1, pin);
       pc = q4_next<M>(g, pc + G, G);
     }
   }
@@ -177,23 +192,10 @@ __global__ void __launch_bounds__(kThreads) q4_kernel(Q4Args a) {
       const uint32_t i2 = (uint32_t)digit_swap(i);       // the swapped tails' offset
       const uint32_t offU = (uint32_t)((i & kA4) | ((i & kB4) << 4));
       const uint32_t offS = (uint32_t)((i2 & kA4) | ((i2 & kB4) << 4));
-      // P: 16-entry rows, |N| = 2 (shift (d-2) R = 0)
-      double pu = 0.0, ps = 0.0;
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        const V4 u4 = reinterpret_cast<const V4*>(PU + 16 * i)[k];
-        const V4 s4 = reinterpret_cast<const V4*>(PS + 16 * i2)[k];
-        pu = pu + ((double)u4.x + 0.0);
-        pu = pu + ((double)u4.y + 0.0);
-        pu = pu + ((double)u4.z + 0.0);
-        pu = pu + ((double)u4.w + 0.0);
-        ps = ps + ((double)s4.x + 0.0);
-        ps = ps + ((double)s4.y + 0.0);
-        ps = ps + ((double)s4.z + 0.0);
-        ps = ps + ((double)s4.w + 0.0);
-      }
-      pu = 0.0625 * pu;
-      ps = 0.0625 * ps;
+      // P: mean of the 16-entry row of the table two sweeps back, |N| = 2 (shift (d-2) R = 0);
+      // pooled when that table was written
+      const double pu = reinterpret_cast<const double*>(PU)[i];
+      const double ps = reinterpret_cast<const double*>(PS)[i2];
 #pragma unroll
       for (int m = 0; m < (WMODE ? 2 : 1); ++m) {
         const double sh = WMODE ? R[m] : 0.0;  // |N| = 1: shift (d-1) R = R
@@ -220,6 +222,9 @@ __global__ void __launch_bounds__(kThreads) q4_kernel(Q4Args a) {
             if (!WMODE) {
               dst[xu] = (T)vu;
               if (!self) dst[xs] = (T)vs;
+              constexpr uint32_t NR1 = C::NR + 1;
+              outs[((ha * 4 + hb) * 16 + (i & 15)) * NR1 + (i >> 4)] = (T)vu;
+              outs[((16 + ha * 4 + hb) * 16 + (i2 & 15)) * NR1 + (i2 >> 4)] = (T)vs;
             } else {
               const double twoR = 2.0 * R[m];
               const T* uo = buf + 2 * C::UNIT;
@@ -235,8 +240,25 @@ __global__ void __launch_bounds__(kThreads) q4_kernel(Q4Args a) {
       }
     }
     __syncthreads();
+    if (!WMODE) {
+      // row means of the new table: output rows (h_a, h_b, t >> 4) of both sides, each summed
+      // in Alg. 1's order over its 16 stored values (read all 16, then add in order)
+      constexpr uint32_t RPS = 16 * C::NR, NR1 = C::NR + 1;  // rows per side
+      for (uint32_t j = tid; j < (self ? 1u : 2u) * RPS; j += kThreads) {
+        const uint32_t side = j / RPS, jr = j % RPS;
+        const uint32_t hh = jr / C::NR, r = jr % C::NR;
+        const T* row = outs + (side * 16 + hh) * 16 * NR1 + r;
+        double sum = 0.0;
+#pragma unroll
+        for (int k = 0; k < 16; ++k) sum = sum + ((double)row[k * NR1] + 0.0);
+        const uint64_t hx = ((uint64_t)(hh >> 2) << hbit_a) | ((uint64_t)(hh & 3) << hbit_b);
+        const uint64_t t0 = side ? t0S : t0U;
+        pout[(hx | t0) >> 4 | r] = 0.0625 * sum;
+      }
+      __syncthreads();  // outs is reused by the next item
+    }
     if (tid == 0 && pc < g.nunits) {
-      q4_issue<T, M, S, WMODE>(g, pc, buf, &bars[s], g1, g2);
+      q4_issue<T, M, S, WMODE>(g, pc, buf, &bars[s], g1, pin);
       pc = q4_next<M>(g, pc + G, G);
     }
   }
@@ -271,8 +293,17 @@ cudaError_t launch_q4_t(const Q4Args& a, cudaStream_t s, int sms) {
 int q4_min_ell() { return 3; }  // the unit (16^2 tails) must fit in the 4^(2(l-1)) tail pairs
 
 cudaError_t launch_q4_sweep(const Q4Args& a, int dtype, cudaStream_t s, int sms) {
-  return dtype == LCSB_F32 ? launch_q4_t<float, 2, 1, false>(a, s, sms)
-                           : launch_q4_t<double, 2, 1, false>(a, s, sms);
+  static int variant = -1;  // LCSB_Q4_STAGES (A/B only): pipeline stages per CTA
+  if (variant < 0) {
+    const char* e = getenv("LCSB_Q4_STAGES");
+    variant = e ? atoi(e) : 1;
+  }
+  if (dtype == LCSB_F32) {
+    if (variant == 2) return launch_q4_t<float, 2, 2, false>(a, s, sms);
+    if (variant == 3) return launch_q4_t<float, 2, 3, false>(a, s, sms);
+    return launch_q4_t<float, 2, 1, false>(a, s, sms);
+  }
+  return launch_q4_t<double, 2, 1, false>(a, s, sms);
 }
 cudaError_t launch_q4_wpass(const Q4Args& a, int dtype, cudaStream_t s, int sms) {
   return dtype == LCSB_F32 ? launch_q4_t<float, 2, 1, true>(a, s, sms)

@@ -38,6 +38,11 @@ struct lcsb {
   uint64_t n_local;   // entries per shard
   size_t esize;
   int ntab;           // tables in the ring
+  // kernel 3 (q4, pooled-history KS): ring of 3 row-mean arrays (fp64, n/16 entries each);
+  // pools[pcur] holds the row means of the newest table
+  double* pools[3];
+  size_t pool_bytes;
+  int pcur;
   int p, P;           // shards: P = 2^p
   int mode;           // MODE_*
   int first, nown;    // owned shards [first, first + nown)
@@ -274,6 +279,8 @@ static int plan_config(const lcsb_config* c, Plan* p, char* why, size_t whylen) 
   else if (p->kernel == 1 && c->kernel == LCSB_KERNEL_AUTO && small_supported(c->sigma, c->d, n))
     p->kernel = 4;  // register-resident compile-time (sigma, d) kernel (kern_small.cu)
   p->ntab = (form == LCSB_FORM_KS) ? c->d + 1 : 2;  // Alg. 2: d+1 rows; two-array: 2
+  // q4: v_{n-2} is only read through its row means (kern_q4.cu): 2 full tables + 3 mean arrays
+  if (p->kernel == 3) p->ntab = 2;
   p->P = P;
   p->p = lp;
   // process mode also with a single rank when an NCCL id is given (exercises the communicator,
@@ -292,6 +299,7 @@ static int plan_config(const lcsb_config* c, Plan* p, char* why, size_t whylen) 
     return LCSB_EINVAL;
   }
   p->bytes += 256;
+  if (p->kernel == 3) p->bytes += 3 * (n / 16) * sizeof(double);
   if (sym == 2) p->bytes += quarter_map_entries(c->ell, qK) * sizeof(uint32_t);
   return LCSB_OK;
 }
@@ -407,6 +415,7 @@ extern "C" void lcsb_destroy(lcsb_t* h) {
       for (int i = 0; i < h->ntab; ++i) dev_free(h, h->tabs[k][i], h->tab_bytes);
   dev_free(h, h->red, 256);
   dev_free(h, h->qmap, h->qmap_bytes);
+  for (int i = 0; i < 3; ++i) dev_free(h, h->pools[i], h->pool_bytes);
   if (h->barrier_buf) cudaFree(h->barrier_buf);
   for (int i = 0; i < kMaxGen; ++i)
     if (h->graph[i]) cudaGraphExecDestroy(h->graph[i]);
@@ -543,6 +552,16 @@ extern "C" int lcsb_create_ex(const lcsb_config* cfg, lcsb_t** out) {
     lcsb_destroy(h);
     return set_err(nullptr, LCSB_ECAPACITY, "scratch allocation failed");
   }
+  if (h->kernel == 3) {  // row-mean ring of the pooled-history KS sweep, zero (W_0 = 0)
+    h->pool_bytes = (size_t)(h->n_logical / 16) * sizeof(double);
+    for (int i = 0; i < 3; ++i) {
+      h->pools[i] = (double*)dev_alloc(h, h->pool_bytes);
+      if (!h->pools[i] || cudaMemsetAsync(h->pools[i], 0, h->pool_bytes, s) != cudaSuccess) {
+        lcsb_destroy(h);
+        return set_err(nullptr, LCSB_ECAPACITY, "row-mean array allocation failed");
+      }
+    }
+  }
   if (h->symmetric == 2) {  // quarter table block map (host-built, uploaded once)
     const uint64_t nb = quarter_map_entries(cfg->ell, h->qK);
     h->qmap_bytes = nb * sizeof(uint32_t);
@@ -601,7 +620,11 @@ extern "C" int lcsb_reset(lcsb_t* h) {
       CU(h, cudaMemsetAsync(h->tabs[k][i], 0, h->tab_bytes, (cudaStream_t)h->cfg.stream));
   rc = barrier(h);  // everyone's tables are zero before anyone sweeps into them
   if (rc != LCSB_OK) return rc;
+  for (int i = 0; i < 3; ++i)
+    if (h->pools[i])
+      CU(h, cudaMemsetAsync(h->pools[i], 0, h->pool_bytes, (cudaStream_t)h->cfg.stream));
   h->cur = 0;
+  h->pcur = 0;
   h->sweeps_done = 0;
   h->best_rho[0] = h->best_rho[1] = 0.0;
   h->best_sweep[0] = h->best_sweep[1] = 0;
@@ -653,7 +676,7 @@ static bool graph_worthy(const lcsb_t* h) {
 }
 
 static int sweep_graph(lcsb_t* h, cudaStream_t s) {
-  const int start = h->cur;
+  const int start = h->cur + h->ntab * h->pcur;  // ring state (both rings line up after G)
   if (!h->graph[start]) {
     if (!h->cap_stream) CU(h, cudaStreamCreateWithFlags(&h->cap_stream, cudaStreamNonBlocking));
     const int64_t done = h->sweeps_done, launches = h->launches;
@@ -674,7 +697,8 @@ static int sweep_graph(lcsb_t* h, cudaStream_t s) {
     }
     h->sweeps_done = done;  // the capture only recorded the sweeps
     h->launches = launches;
-    h->cur = start;
+    h->cur = start % h->ntab;
+    h->pcur = start / h->ntab;
   }
   CU(h, cudaGraphLaunch(h->graph[start], s));
   h->sweeps_done += h->graph_sweeps;
@@ -689,8 +713,9 @@ extern "C" int lcsb_sweep(lcsb_t* h, int64_t n) {
   cudaStream_t s = (cudaStream_t)h->cfg.stream;
   if (graph_worthy(h) && !getenv("LCSB_NO_GRAPHS")) {
     if (!h->graph_sweeps) {
-      h->graph_sweeps = h->ntab;
-      while (h->graph_sweeps < 32) h->graph_sweeps += h->ntab;
+      const int period = (h->kernel == 3) ? 6 : h->ntab;  // q4: lcm(2 tables, 3 mean arrays)
+      h->graph_sweeps = period;
+      while (h->graph_sweeps < 32) h->graph_sweeps += period;
     }
     if (h->sweeps_done == 0 && n > 0) {  // one plain sweep first (initialises launch caches)
       int rc = enqueue_sweeps(h, 1, s);
@@ -739,11 +764,13 @@ static int enqueue_sweeps(lcsb_t* h, int64_t n, cudaStream_t s) {
       Q4Args a;
       memset(&a, 0, sizeof a);
       a.g1 = h->tabs[0][slot_back(h, 0)];
-      a.g2 = h->tabs[0][slot_back(h, 1)];
+      a.pin = h->pools[(h->pcur + 2) % 3];   // row means of v_{n-2}
+      a.pout = h->pools[(h->pcur + 1) % 3];  // row means of the table written now
       a.dst = h->tabs[0][out];
       a.ell = h->cfg.ell;
       e = launch_q4_sweep(a, h->cfg.dtype, s, h->sms);
       h->launches += 1;
+      h->pcur = (h->pcur + 1) % 3;
     } else {
       GenericArgs a;
       fill_generic(h, &a);
@@ -811,7 +838,7 @@ extern "C" int lcsb_bound(lcsb_t* h, lcsb_bound_t* out) {
     Q4Args a;
     memset(&a, 0, sizeof a);
     a.g1 = h->tabs[0][h->cur];
-    a.g2 = h->tabs[0][h->cur];
+    a.pin = h->pools[h->pcur];  // |N| = 2 reads v_n itself in the W pass (shift 0)
     a.ell = h->cfg.ell;
     a.red_in = h->red;
     a.red_out = h->red + 2;
@@ -928,7 +955,8 @@ extern "C" int32_t lcsb_num_shards(const lcsb_t* h) { return h ? h->P : 0; }
 extern "C" uint64_t lcsb_num_states(const lcsb_t* h) { return h ? h->n_logical : 0; }
 extern "C" uint64_t lcsb_stored_states(const lcsb_t* h) { return h ? h->n_stored : 0; }
 extern "C" uint64_t lcsb_device_bytes(const lcsb_t* h) {
-  return h ? (uint64_t)h->tab_bytes * (uint64_t)h->ntab * (uint64_t)h->nown + 256 + h->qmap_bytes
+  return h ? (uint64_t)h->tab_bytes * (uint64_t)h->ntab * (uint64_t)h->nown + 256 + h->qmap_bytes +
+                 3 * (uint64_t)h->pool_bytes
            : 0;
 }
 extern "C" int32_t lcsb_kernel_in_use(const lcsb_t* h) { return h ? h->kernel : 0; }

@@ -144,9 +144,10 @@ __host__ __device__ inline uint64_t qstored(const uint32_t* map, uint64_t s, int
 }
 
 struct Q4Args {
-  const void* g1;   // table one sweep back (W pass: the newest table)
-  const void* g2;   // table two sweeps back (W pass: the newest table)
-  void* dst;        // output (sweep mode)
+  const void* g1;     // table one sweep back (W pass: the newest table)
+  const double* pin;  // row means (x >> 4) of the table two sweeps back (W pass: of the newest)
+  double* pout;       // sweep: row means of the table written
+  void* dst;          // output (sweep mode)
   int ell;
   const unsigned long long* red_in;
   unsigned long long* red_out;

@@ -45,8 +45,10 @@ def test_required_bytes_and_validation():
         2 * ((1 << 18) + (1 << 9)) * (1 << 14) * 4 + 256 + (1 << 19) * 4
     # full table when symmetry is off
     assert L.lcsb_required_bytes(2, 2, 17, "f32", symmetry=0) == 2 * (1 << 34) * 4 + 256
-    # config 3: KS ring of d+1 = 3 tables of 4^16 fp32
-    assert L.lcsb_required_bytes(4, 2, 8, "f32") == 3 * (1 << 32) * 4 + 256
+    # config 3: pooled-history KS (kern_q4.cu): 2 tables of 4^16 fp32 + 3 row-mean arrays of
+    # 4^16 / 16 fp64 (the generic kernel keeps the d+1 = 3 tables of Alg. 2)
+    assert L.lcsb_required_bytes(4, 2, 8, "f32") == 2 * (1 << 32) * 4 + 256 + 3 * (1 << 28) * 8
+    assert L.lcsb_required_bytes(4, 2, 8, "f32", kernel="generic") == 3 * (1 << 32) * 4 + 256
     # config 2: 4 tables of 3^12 fp64
     assert L.lcsb_required_bytes(3, 3, 4, "f64") == 4 * 3 ** 12 * 8 + 256
     # invalid: two-array for sigma != 2, d > 16, sigma^(d l) too large, symmetry without binary
