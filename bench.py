@@ -138,6 +138,12 @@ def design_bytes_per_sweep(w: dict, stored: int, kernel: str) -> int:
     return algorithmic_bytes_for_kernel(w, stored, kernel)
 
 
+def workload_name(args, w) -> str:
+    """The `config.workload` string (identical in both arms)."""
+    return (f"{args.workload}: sigma={w['sigma']}, d={w['d']}, l={w['ell']}, {w['form']} form, "
+            f"{w['dtype']} storage, {w['sweeps']} sweeps + 1 bound per step")
+
+
 def run_ours(args, w, ws, rank, local):
     import torch
     from paper_2407_10925_b200 import Lcsb
@@ -260,12 +266,12 @@ def run_ours(args, w, ws, rank, local):
         "dtype": "f64" if w["dtype"] == "f64" else "f32-storage/f64-arith",
         "data": "synthetic (the method's only input is (sigma, d, l) and W_0 = 0)",
         "config": {
-            "workload": f"{args.workload}: sigma={w['sigma']}, d={w['d']}, l={w['ell']}, "
-                        f"{w['form']} form, {w['dtype']} storage, {S} sweeps + 1 bound per step",
+            "workload": workload_name(args, w),
             "states": n_logical, "stored_states": stored, "sweeps_per_step": S,
             "kernel": kernel_name,
             "parallelism": f"sharded over {ws} GPUs (NCCL + CUDA IPC peer stores)" if ws > 1
-                           else "single-gpu",
+                           else ("process-sharded mode, 1 rank" if args.force_sharded
+                                 else "single-gpu"),
             "l2_flush": "inputs larger than L2 (each table %.1f GiB vs 126 MB L2)"
                         % (stored * (4 if w["dtype"] == "f32" else 8) / 2**30)
             if stored * 4 > 2**27 else "working set L2-resident (latency-bound config)",
@@ -373,7 +379,9 @@ def main():
                "unit": "state-updates/s", "n_gpus": ws, "steps": args.steps,
                "warmup": args.warmup, "higher_is_better": True, "scaling": "weak",
                "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-               "config": {"workload": args.workload},
+               "config": {"workload": workload_name(args, w),
+                          "states": w["sigma"] ** (w["d"] * w["ell"]),
+                          "sweeps_per_step": w["sweeps"]},
                "cpu_baseline": base,
                "e2e": {"value": base["value"], "unit": "state-updates/s",
                        "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -382,6 +390,9 @@ def main():
 
     import torch
     if ws > 1 or args.force_sharded:
+        # NCCL's version banner goes to stdout; keep stdout to the one JSON line
+        if os.environ.get("NCCL_DEBUG", "").upper() in ("", "VERSION"):
+            os.environ["NCCL_DEBUG"] = "WARN"
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
         os.environ.setdefault("MASTER_PORT", "29517")
         os.environ.setdefault("RANK", str(rank))
