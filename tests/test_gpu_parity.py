@@ -183,15 +183,18 @@ def test_small_kernel_matches_generic(sigma, d, ell, form, dtype):
     b.destroy()
 
 
-@pytest.mark.parametrize("sigma,d,ell,dtype", [(2, 2, 6, "f64"), (3, 3, 3, "f64"),
-                                               (2, 2, 8, "f32")])
-def test_graph_replay_equals_plain_launches(sigma, d, ell, dtype, monkeypatch):
+@pytest.mark.parametrize("sigma,d,ell,dtype,kw", [
+    (2, 2, 6, "f64", {}), (3, 3, 3, "f64", {}), (2, 2, 8, "f32", {}),
+    (4, 2, 4, "f32", {}),                                  # q4: 2 tables + 3 mean arrays
+    (2, 2, 9, "f32", {"symmetry": 2, "block_log4": 4}),    # bin2q quarter table
+    (2, 2, 10, "f64", {"symmetry": 2})])
+def test_graph_replay_equals_plain_launches(sigma, d, ell, dtype, kw, monkeypatch):
     """Small tables replay captured CUDA graphs of sweeps; the result must equal plain launches
     (including sweep counts that are not multiples of the graph length)."""
     Lcsb = _lcsb()
-    a = Lcsb(sigma, d, ell, dtype=dtype)
+    a = Lcsb(sigma, d, ell, dtype=dtype, **kw)
     monkeypatch.setenv("LCSB_NO_GRAPHS", "1")
-    b = Lcsb(sigma, d, ell, dtype=dtype)
+    b = Lcsb(sigma, d, ell, dtype=dtype, **kw)
     for n in (77, 5, 64):
         monkeypatch.delenv("LCSB_NO_GRAPHS")
         a.sweep(n)

@@ -126,6 +126,24 @@ def test_quarter_matches_oracle(ell, K, dtype, sweeps):
 @pytest.mark.gpu
 @pytest.mark.skipif(not has_cuda(), reason="needs a CUDA device")
 @pytest.mark.parametrize("dtype", ["f32", "f64"])
+def test_quarter_many_sweeps_per_call_matches_oracle(dtype):
+    """60 sweeps in one call (the CUDA-graph replay path of small tables) then the bound and
+    the best-so-far bookkeeping, against the oracle; l = 8, blocks of 4^4."""
+    from oracle import ft_oracle as fo
+    h = L.Lcsb(2, 2, 8, dtype=dtype, symmetry=2, block_log4=4)
+    run = fo.Run(2, 2, 8, "two_array", dtype)
+    for n in (60, 7):
+        h.sweep(n)
+        run.sweep(n)
+        _cmp(h.table(0), run.newest, dtype)
+        _cmp(h.table(1), run.prev, dtype)
+        _cmp_bound(h.bound(), run.bound(), dtype)
+    h.destroy()
+
+
+@pytest.mark.gpu
+@pytest.mark.skipif(not has_cuda(), reason="needs a CUDA device")
+@pytest.mark.parametrize("dtype", ["f32", "f64"])
 def test_quarter_equals_half_table_l13(dtype):
     """Quarter and half table give the same values (fp32: bitwise) on 2^20 sampled states and
     the same bound, l = 13 (auto block size), 30 sweeps."""
