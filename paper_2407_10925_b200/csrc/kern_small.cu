@@ -6,6 +6,16 @@
 //
 // Config 2's whole ring (4 x 4.05 MiB) is L2-resident, so the kernel is bound by L1/L2 gather
 // throughput and launch latency rather than HBM; one thread per logical state, 32-bit indices.
+//
+// Pooled means (sweep only): an option that advances the strings in N (|N| = k >= 2) reads its
+// generation only through the mean over N's appended characters, and those sigma^k entries lie
+// in one "row" (the sigma^d states that differ only in the last character group) with the
+// unchanged strings' last characters fixed.  So every sweep also writes, per row of the table it
+// produces, those means for every mask of popcount k >= 2 and every value of the unchanged last
+// characters (summed in Alg. 1's order from the stored values, staged in shared memory), and the
+// options read one pooled value instead of sigma^k entries (config 2: ~35 gathers per state ->
+// ~5).  The W pass adds a shift to every entry before summing (Alg. 2 line 6), so it keeps the
+// raw gathers.
 #include <math.h>
 
 #include "lcsb_internal.cuh"
@@ -51,10 +61,35 @@ __device__ __forceinline__ double option_mean(const T* __restrict__ src, uint32_
   return inv * r;
 }
 
-template <typename T, int SIG, int D, int MASK>
-__device__ __forceinline__ double option_at(const T* const* src, const double* sh,
-                                            const uint32_t* contrib, const uint32_t* head,
-                                            uint32_t headw_top) {
+// ---- pooled-mean layout (per table, per k = |N| >= 2): per row, the masks of popcount k in
+// increasing order, each with sigma^(d-k) values indexed by the unchanged strings' last
+// characters (base sigma, string order)
+__host__ __device__ constexpr int popc_c(int m) { return m ? (m & 1) + popc_c(m >> 1) : 0; }
+__host__ __device__ constexpr int mask_rank(int mask) {  // rank among masks of equal popcount
+  int r = 0;
+  for (int m = 0; m < mask; ++m)
+    if (popc_c(m) == popc_c(mask)) ++r;
+  return r;
+}
+__host__ __device__ constexpr int nmasks(int d, int k) {
+  int c = 0;
+  for (int m = 0; m < (1 << d); ++m)
+    if (popc_c(m) == k) ++c;
+  return c;
+}
+template <int SIG, int D, int K>
+struct PoolRow {  // pooled values per row for |N| = K
+  static constexpr uint32_t PER_MASK = ipow_c(SIG, D - K);
+  static constexpr uint32_t PER_ROW = (uint32_t)nmasks(D, K) * PER_MASK;
+};
+__host__ __device__ constexpr uint32_t pool_per_row(int sig, int d, int k) {
+  return (uint32_t)nmasks(d, k) * ipow_c((uint32_t)sig, d - k);
+}
+
+template <typename T, int SIG, int D, int MASK, bool POOL>
+__device__ __forceinline__ double option_at(const T* const* src, const double* const* pin,
+                                            const double* sh, const uint32_t* contrib,
+                                            const uint32_t* head, uint32_t headw_top) {
   constexpr int K = __builtin_popcount(MASK);
   constexpr uint32_t SIGD = ipow_c(SIG, D);
   uint32_t base = 0;
@@ -65,25 +100,38 @@ __device__ __forceinline__ double option_at(const T* const* src, const double* s
     else
       base += contrib[j];
   }
-  return option_mean<T, SIG, D, MASK>(src[K - 1], base, sh[K - 1]);
+  if constexpr (POOL && K >= 2) {
+    // the unchanged strings' last characters (base % SIGD), in string order
+    uint32_t fixed = 0;
+#pragma unroll
+    for (int j = 0; j < D; ++j)
+      if (!(MASK & (1 << j))) fixed = fixed * SIG + (base / ipow_c(SIG, D - 1 - j)) % SIG;
+    using PR = PoolRow<SIG, D, K>;
+    return pin[K - 1][(base / SIGD) * PR::PER_ROW + mask_rank(MASK) * PR::PER_MASK + fixed];
+  } else {
+    return option_mean<T, SIG, D, MASK>(src[K - 1], base, sh[K - 1]);
+  }
 }
 
-template <typename T, int SIG, int D, int MASK = 1>
-__device__ __forceinline__ double dispatch_mask(int mask, const T* const* src, const double* sh,
+template <typename T, int SIG, int D, bool POOL, int MASK = 1>
+__device__ __forceinline__ double dispatch_mask(int mask, const T* const* src,
+                                                const double* const* pin, const double* sh,
                                                 const uint32_t* contrib, const uint32_t* head,
                                                 uint32_t headw_top) {
   if constexpr (MASK < (1 << D)) {
-    if (mask == MASK) return option_at<T, SIG, D, MASK>(src, sh, contrib, head, headw_top);
-    return dispatch_mask<T, SIG, D, MASK + 1>(mask, src, sh, contrib, head, headw_top);
+    if (mask == MASK)
+      return option_at<T, SIG, D, MASK, POOL>(src, pin, sh, contrib, head, headw_top);
+    return dispatch_mask<T, SIG, D, POOL, MASK + 1>(mask, src, pin, sh, contrib, head, headw_top);
   } else {
     return 0.0;
   }
 }
 
 // F(src...)[x] (Eq. ineq3): b + max over the distinct option masks
-template <typename T, int SIG, int D>
+template <typename T, int SIG, int D, bool POOL = false>
 __device__ __forceinline__ double F_small(const T* const* src, const double* sh, uint32_t x,
-                                          int ell, uint32_t headw_top) {
+                                          int ell, uint32_t headw_top,
+                                          const double* const* pin = nullptr) {
   uint32_t contrib[D], head[D];
 #pragma unroll
   for (int j = 0; j < D; ++j) contrib[j] = 0;
@@ -115,11 +163,13 @@ __device__ __forceinline__ double F_small(const T* const* src, const double* sh,
 #pragma unroll
     for (int i = 0; i < D; ++i)
       if (head[i] != hz) mask |= 1 << i;
-    const double cand = mask ? dispatch_mask<T, SIG, D>(mask, src, sh, contrib, head, headw_top) : 0.0;
+    const double cand =
+        mask ? dispatch_mask<T, SIG, D, POOL>(mask, src, pin, sh, contrib, head, headw_top) : 0.0;
     if (cand > best) best = cand;
   }
   if (nseen < SIG) {  // some z is no string's head: N = all strings
-    const double cand = option_at<T, SIG, D, (1 << D) - 1>(src, sh, contrib, head, headw_top);
+    const double cand =
+        option_at<T, SIG, D, (1 << D) - 1, POOL>(src, pin, sh, contrib, head, headw_top);
     if (cand > best) best = cand;
   }
   return (double)b + best;
@@ -164,6 +214,124 @@ __global__ void __launch_bounds__(256) small_kernel(GenericArgs a) {
   }
 }
 
+// Pooled sweep: a CTA takes RPB consecutive rows (one thread per state), computes them with the
+// pooled reads, stores them, stages them in shared memory and writes the pooled means of its rows
+// for every k = 2..D.
+template <int SIG, int D>
+struct SmallPool {
+  static constexpr uint32_t SIGD = ipow_c(SIG, D);
+  static constexpr uint32_t RPB = 256 / SIGD;  // rows per CTA
+  static constexpr uint32_t THREADS = RPB * SIGD;
+  static constexpr uint32_t SUMS_PER_ROW = [] {
+    uint32_t c = 0;
+    for (int k = 2; k <= D; ++k) c += pool_per_row(SIG, D, k);
+    return c;
+  }();
+};
+
+template <typename T, int SIG, int D, int K, int MASK = 0>
+__device__ __forceinline__ double pooled_sum(int maskidx, const T* row, uint32_t fixed) {
+  // the mean over MASK's appended characters with the other strings' last characters = fixed,
+  // in Alg. 1's order (lexicographic, lowest string index most significant)
+  if constexpr (MASK < (1 << D)) {
+    if constexpr (popc_c(MASK) == K) {
+      if (mask_rank(MASK) == maskidx) {
+        uint32_t foff = 0, ff = fixed;
+#pragma unroll
+        for (int j = D - 1; j >= 0; --j)
+          if (!(MASK & (1 << j))) {
+            foff += (ff % SIG) * ipow_c(SIG, D - 1 - j);
+            ff /= SIG;
+          }
+        constexpr uint32_t COMBOS = ipow_c(SIG, K);
+        double r = 0.0;
+#pragma unroll
+        for (uint32_t t = 0; t < COMBOS; ++t) {
+          uint32_t off = 0, tt = t;
+#pragma unroll
+          for (int j = D - 1; j >= 0; --j) {
+            if (MASK & (1 << j)) {
+              off += (tt % SIG) * ipow_c(SIG, D - 1 - j);
+              tt /= SIG;
+            }
+          }
+          r = r + ((double)row[foff + off] + 0.0);
+        }
+        const double inv = 1.0 / (double)COMBOS;
+        return inv * r;
+      }
+    }
+    return pooled_sum<T, SIG, D, K, MASK + 1>(maskidx, row, fixed);
+  } else {
+    return 0.0;
+  }
+}
+
+template <typename T, int SIG, int D>
+__global__ void __launch_bounds__(SmallPool<SIG, D>::THREADS)
+    small_pooled_kernel(GenericArgs a) {
+  using SP = SmallPool<SIG, D>;
+  constexpr uint32_t SIGD = SP::SIGD, RPB = SP::RPB;
+  __shared__ T rows[RPB * SIGD];
+  const T* src[D];
+  const double* pin[D];
+#pragma unroll
+  for (int k = 0; k < D; ++k) {
+    src[k] = reinterpret_cast<const T*>(a.src[k]);
+    pin[k] = a.pin[k];
+  }
+  uint32_t headw_top = 1;
+  for (int i = 0; i < D * (a.ell - 1); ++i) headw_top *= SIG;
+  const uint32_t nrows = (uint32_t)(a.n / SIGD);
+  double zero[D];
+#pragma unroll
+  for (int k = 0; k < D; ++k) zero[k] = 0.0;
+  T* dst = reinterpret_cast<T*>(a.dst);
+  const uint32_t tid = threadIdx.x;
+  for (uint32_t r0 = blockIdx.x * RPB; r0 < nrows; r0 += gridDim.x * RPB) {
+    const uint32_t x = r0 * SIGD + tid;
+    if (r0 + tid / SIGD < nrows) {
+      const T v = (T)F_small<T, SIG, D, true>(src, zero, x, a.ell, headw_top, pin);
+      dst[x] = v;
+      rows[tid] = v;
+    }
+    __syncthreads();
+    // pooled means of these rows for k = 2..D (SUMS_PER_ROW per row)
+    for (uint32_t j = tid; j < RPB * SP::SUMS_PER_ROW; j += SP::THREADS) {
+      const uint32_t rr = j / SP::SUMS_PER_ROW;
+      if (r0 + rr >= nrows) continue;
+      uint32_t q = j % SP::SUMS_PER_ROW;
+      const T* row = rows + rr * SIGD;
+#pragma unroll
+      for (int k = 2; k <= D; ++k) {
+        const uint32_t per = pool_per_row(SIG, D, k), pm = ipow_c(SIG, D - k);
+        if (q < per) {
+          double m = 0.0;
+          if (k == 2) m = pooled_sum<T, SIG, D, 2>((int)(q / pm), row, q % pm);
+          if (D >= 3 && k == 3) m = pooled_sum<T, SIG, D, (D >= 3 ? 3 : 2)>((int)(q / pm), row, q % pm);
+          a.pout[k - 1][(uint64_t)(r0 + rr) * per + q] = m;
+          break;
+        }
+        q -= per;
+      }
+    }
+    __syncthreads();  // rows[] is reused
+  }
+}
+
+template <typename T, int SIG, int D>
+cudaError_t launch_small_pooled_t(const GenericArgs& a, cudaStream_t s, int sms) {
+  using SP = SmallPool<SIG, D>;
+  static uint64_t cap = 0;
+  if (!cap) cap = resident_blocks(small_pooled_kernel<T, SIG, D>, SP::THREADS, sms);
+  const uint64_t nrows = a.n / SP::SIGD;
+  uint64_t blocks = (nrows + SP::RPB - 1) / SP::RPB;
+  if (blocks > cap) blocks = cap;
+  if (blocks < 1) blocks = 1;
+  small_pooled_kernel<T, SIG, D><<<(unsigned)blocks, SP::THREADS, 0, s>>>(a);
+  return cudaGetLastError();
+}
+
 template <typename T, int SIG, int D, bool WMODE>
 cudaError_t launch_small_t(const GenericArgs& a, cudaStream_t s, int sms) {
   static uint64_t cap = 0;
@@ -185,6 +353,22 @@ cudaError_t launch_small_sd(const GenericArgs& a, int dtype, bool wpass, cudaStr
 }
 
 }  // namespace
+
+// pooled sweeps: (sigma, d) with d = 3 (|N| = 2 and 3 pooled) or sigma^d >= 9 for d = 2
+bool small_pooled_supported(int sigma, int d) {
+  return (sigma == 3 && d == 3) || (sigma == 2 && d == 3) || (sigma == 3 && d == 2);
+}
+uint32_t small_pool_per_row(int sigma, int d, int k) { return pool_per_row(sigma, d, k); }
+
+cudaError_t launch_small_pooled(const GenericArgs& a, int dtype, cudaStream_t s, int sms) {
+#define LCSB_SP(SIG, D)                                                    \
+  if (a.sigma == SIG && a.d == D)                                          \
+    return dtype == LCSB_F32 ? launch_small_pooled_t<float, SIG, D>(a, s, sms) \
+                             : launch_small_pooled_t<double, SIG, D>(a, s, sms);
+  LCSB_SP(3, 3) LCSB_SP(2, 3) LCSB_SP(3, 2)
+#undef LCSB_SP
+  return cudaErrorInvalidValue;
+}
 
 bool small_supported(int sigma, int d, uint64_t n) {
   if (n >= (1ull << 31)) return false;

@@ -43,6 +43,11 @@ struct lcsb {
   double* pools[3];
   size_t pool_bytes;
   int pcur;
+  // kernel 4 (small, KS, pooled sweep): spools[k][slot] = pooled means (|N| = k >= 2) of the
+  // table in ring slot `slot` (kern_small.cu)
+  int spooled;
+  double* spools[kMaxD + 1][kMaxGen];
+  size_t spool_bytes[kMaxD + 1];
   int p, P;           // shards: P = 2^p
   int mode;           // MODE_*
   int first, nown;    // owned shards [first, first + nown)
@@ -300,6 +305,13 @@ static int plan_config(const lcsb_config* c, Plan* p, char* why, size_t whylen) 
   }
   p->bytes += 256;
   if (p->kernel == 3) p->bytes += 3 * (n / 16) * sizeof(double);
+  if (p->kernel == 4 && form == LCSB_FORM_KS && small_pooled_supported(c->sigma, c->d)) {
+    uint64_t sigd = 1;
+    for (int j = 0; j < c->d; ++j) sigd *= (uint64_t)c->sigma;
+    for (int k = 2; k <= c->d; ++k)
+      p->bytes += (uint64_t)p->ntab * (n / sigd) * small_pool_per_row(c->sigma, c->d, k) *
+                  sizeof(double);
+  }
   if (sym == 2) p->bytes += quarter_map_entries(c->ell, qK) * sizeof(uint32_t);
   return LCSB_OK;
 }
@@ -416,6 +428,8 @@ extern "C" void lcsb_destroy(lcsb_t* h) {
   dev_free(h, h->red, 256);
   dev_free(h, h->qmap, h->qmap_bytes);
   for (int i = 0; i < 3; ++i) dev_free(h, h->pools[i], h->pool_bytes);
+  for (int k = 0; k <= kMaxD; ++k)
+    for (int i = 0; i < kMaxGen; ++i) dev_free(h, h->spools[k][i], h->spool_bytes[k]);
   if (h->barrier_buf) cudaFree(h->barrier_buf);
   for (int i = 0; i < kMaxGen; ++i)
     if (h->graph[i]) cudaGraphExecDestroy(h->graph[i]);
@@ -562,6 +576,24 @@ extern "C" int lcsb_create_ex(const lcsb_config* cfg, lcsb_t** out) {
       }
     }
   }
+  if (h->kernel == 4 && h->form == LCSB_FORM_KS && small_pooled_supported(cfg->sigma, cfg->d) &&
+      !getenv("LCSB_NO_SMALL_POOL")) {  // pooled means of every ring slot, zero (W_0 = 0)
+    h->spooled = 1;
+    uint64_t sigd = 1;
+    for (int j = 0; j < cfg->d; ++j) sigd *= (uint64_t)cfg->sigma;
+    for (int k = 2; k <= cfg->d; ++k) {
+      h->spool_bytes[k] = (size_t)(h->n_logical / sigd) *
+                          small_pool_per_row(cfg->sigma, cfg->d, k) * sizeof(double);
+      for (int i = 0; i < h->ntab; ++i) {
+        h->spools[k][i] = (double*)dev_alloc(h, h->spool_bytes[k]);
+        if (!h->spools[k][i] ||
+            cudaMemsetAsync(h->spools[k][i], 0, h->spool_bytes[k], s) != cudaSuccess) {
+          lcsb_destroy(h);
+          return set_err(nullptr, LCSB_ECAPACITY, "pooled-mean array allocation failed");
+        }
+      }
+    }
+  }
   if (h->symmetric == 2) {  // quarter table block map (host-built, uploaded once)
     const uint64_t nb = quarter_map_entries(cfg->ell, h->qK);
     h->qmap_bytes = nb * sizeof(uint32_t);
@@ -623,6 +655,10 @@ extern "C" int lcsb_reset(lcsb_t* h) {
   for (int i = 0; i < 3; ++i)
     if (h->pools[i])
       CU(h, cudaMemsetAsync(h->pools[i], 0, h->pool_bytes, (cudaStream_t)h->cfg.stream));
+  for (int k = 0; k <= kMaxD; ++k)
+    for (int i = 0; i < kMaxGen; ++i)
+      if (h->spools[k][i])
+        CU(h, cudaMemsetAsync(h->spools[k][i], 0, h->spool_bytes[k], (cudaStream_t)h->cfg.stream));
   h->cur = 0;
   h->pcur = 0;
   h->sweeps_done = 0;
@@ -778,8 +814,16 @@ static int enqueue_sweeps(lcsb_t* h, int64_t n, cudaStream_t s) {
         a.src[k - 1] = (h->form == LCSB_FORM_KS) ? h->tabs[0][slot_back(h, k - 1)]
                                                  : h->tabs[0][h->cur];
       a.dst = h->tabs[0][out];
-      e = (h->kernel == 4) ? launch_small(a, h->cfg.dtype, false, s, h->sms)
-                           : launch_generic_sweep(a, h->cfg.dtype, s, h->sms);
+      if (h->spooled) {  // the table k back is read through its pooled means (k >= 2)
+        for (int k = 2; k <= h->cfg.d; ++k) {
+          a.pin[k - 1] = h->spools[k][slot_back(h, k - 1)];
+          a.pout[k - 1] = h->spools[k][out];
+        }
+        e = launch_small_pooled(a, h->cfg.dtype, s, h->sms);
+      } else {
+        e = (h->kernel == 4) ? launch_small(a, h->cfg.dtype, false, s, h->sms)
+                             : launch_generic_sweep(a, h->cfg.dtype, s, h->sms);
+      }
       h->launches += 1;
     }
     if (e != cudaSuccess)
@@ -955,9 +999,13 @@ extern "C" int32_t lcsb_num_shards(const lcsb_t* h) { return h ? h->P : 0; }
 extern "C" uint64_t lcsb_num_states(const lcsb_t* h) { return h ? h->n_logical : 0; }
 extern "C" uint64_t lcsb_stored_states(const lcsb_t* h) { return h ? h->n_stored : 0; }
 extern "C" uint64_t lcsb_device_bytes(const lcsb_t* h) {
-  return h ? (uint64_t)h->tab_bytes * (uint64_t)h->ntab * (uint64_t)h->nown + 256 + h->qmap_bytes +
-                 3 * (uint64_t)h->pool_bytes
-           : 0;
+  if (!h) return 0;
+  uint64_t b = (uint64_t)h->tab_bytes * (uint64_t)h->ntab * (uint64_t)h->nown + 256 +
+               h->qmap_bytes + 3 * (uint64_t)h->pool_bytes;
+  for (int k = 0; k <= kMaxD; ++k)
+    for (int i = 0; i < kMaxGen; ++i)
+      if (h->spools[k][i]) b += h->spool_bytes[k];
+  return b;
 }
 extern "C" int32_t lcsb_kernel_in_use(const lcsb_t* h) { return h ? h->kernel : 0; }
 extern "C" int64_t lcsb_launch_count(const lcsb_t* h) { return h ? h->launches : 0; }

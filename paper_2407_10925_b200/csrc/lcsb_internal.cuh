@@ -57,6 +57,10 @@ struct GenericArgs {
   int form;                         // LCSB_FORM_KS / LCSB_FORM_TWO_ARRAY
   const unsigned long long* red_in; // W mode: encoded R_max, R_min
   unsigned long long* red_out;      // W mode: encoded max W slots
+  // pooled small sweep (kern_small.cu): pin[k-1] = pooled means of the table read when
+  // |N| = k (k >= 2); pout[k-1] = pooled means of the table written
+  const double* pin[kMaxD];
+  double* pout[kMaxD];
 };
 
 constexpr int kMaxShards = 8;
@@ -210,6 +214,9 @@ cudaError_t launch_q4_wpass(const Q4Args& a, int dtype, cudaStream_t s, int sms)
 int q4_min_ell();
 bool small_supported(int sigma, int d, uint64_t n);
 cudaError_t launch_small(const GenericArgs& a, int dtype, bool wpass, cudaStream_t s, int sms);
+bool small_pooled_supported(int sigma, int d);
+uint32_t small_pool_per_row(int sigma, int d, int k);  // pooled means per row for |N| = k
+cudaError_t launch_small_pooled(const GenericArgs& a, int dtype, cudaStream_t s, int sms);
 cudaError_t launch_red_init(unsigned long long* red, cudaStream_t s);
 cudaError_t launch_rdiff(const void* newest, const void* prev, uint64_t n, int dtype,
                          unsigned long long* red, cudaStream_t s, int sms);

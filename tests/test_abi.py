@@ -49,8 +49,9 @@ def test_required_bytes_and_validation():
     # 4^16 / 16 fp64 (the generic kernel keeps the d+1 = 3 tables of Alg. 2)
     assert L.lcsb_required_bytes(4, 2, 8, "f32") == 2 * (1 << 32) * 4 + 256 + 3 * (1 << 28) * 8
     assert L.lcsb_required_bytes(4, 2, 8, "f32", kernel="generic") == 3 * (1 << 32) * 4 + 256
-    # config 2: 4 tables of 3^12 fp64
-    assert L.lcsb_required_bytes(3, 3, 4, "f64") == 4 * 3 ** 12 * 8 + 256
+    # config 2: 4 tables of 3^12 fp64 + the pooled means of every ring slot (kern_small.cu):
+    # per row of 27, 9 means for |N| = 2 and 1 for |N| = 3
+    assert L.lcsb_required_bytes(3, 3, 4, "f64") == 4 * 3 ** 12 * 8 + 256 + 4 * 3 ** 9 * 10 * 8
     # invalid: two-array for sigma != 2, d > 16, sigma^(d l) too large, symmetry without binary
     assert L.lcsb_required_bytes(3, 2, 2, "f32", form="two_array") == 0
     assert L.lcsb_required_bytes(2, 17, 1, "f32") == 0

@@ -183,6 +183,30 @@ def test_small_kernel_matches_generic(sigma, d, ell, form, dtype):
     b.destroy()
 
 
+@pytest.mark.parametrize("sigma,d,ell,dtype", [(3, 3, 3, "f64"), (3, 3, 2, "f32"),
+                                               (2, 3, 4, "f32"), (3, 2, 4, "f64")])
+def test_small_pooled_sweep_matches_raw_gathers_and_oracle(sigma, d, ell, dtype, monkeypatch):
+    """The pooled small-table sweep (generations k >= 2 read through their stored partial-row
+    means) equals the raw-gather sweep and the oracle, every generation of the ring."""
+    Lcsb = _lcsb()
+    a = Lcsb(sigma, d, ell, dtype=dtype, form="ks")
+    monkeypatch.setenv("LCSB_NO_SMALL_POOL", "1")
+    b = Lcsb(sigma, d, ell, dtype=dtype, form="ks")
+    monkeypatch.delenv("LCSB_NO_SMALL_POOL")
+    assert a.kernel_in_use == "small" and a.device_bytes > b.device_bytes
+    run = fo.Run(sigma, d, ell, "ks", dtype)
+    for n in (1, 1, 1, 4, 25):
+        a.sweep(n)
+        b.sweep(n)
+        run.sweep(n)
+        for k in range(d):
+            assert np.array_equal(a.table(k), b.table(k))
+            _cmp_tables(a.table(k), run.gens[k], dtype)
+    _cmp_bound(a.bound(), run.bound(), dtype)
+    a.destroy()
+    b.destroy()
+
+
 @pytest.mark.parametrize("sigma,d,ell,dtype,kw", [
     (2, 2, 6, "f64", {}), (3, 3, 3, "f64", {}), (2, 2, 8, "f32", {}),
     (4, 2, 4, "f32", {}),                                  # q4: 2 tables + 3 mean arrays
