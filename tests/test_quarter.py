@@ -182,6 +182,37 @@ def test_quarter_config4_sampled_after_3_sweeps():
     h.destroy()
 
 
+@pytest.mark.gpu
+@pytest.mark.skipif(not has_cuda(), reason="needs a CUDA device")
+def test_config5_l18_on_one_gpu_sampled_and_properties():
+    """BASELINE config 5 (2^36 states, fp32) at full size on ONE GPU through the quarter table
+    (2 x 64 GiB): 2^20 seeded states after 3 sweeps bit-exact against the oracle's sampled mode;
+    then the configured 30 sweeps, with properties that hold at any size: the new table dominates
+    the old (R_min >= 0), the certified bound lies below Lueker's upper bound 0.82628
+    (PAPER.md:551), and sampled states equal their complement and swap images."""
+    from oracle import ft_oracle as fo
+    from seeded_inputs import splitmix64_indices
+    N = 1 << 36
+    h = L.Lcsb(2, 2, 18, dtype="f32")
+    assert h.kernel_in_use == "bin2q" and h.device_bytes < 140 * 2 ** 30
+    idx = splitmix64_indices(0x240710925, 1 << 20, N)
+    h.sweep(3)
+    assert np.array_equal(h.table_gather(idx),
+                          fo.sample_values(2, 2, 18, 3, idx, form="two_array", dtype="f32"))
+    h.sweep(27)
+    b = h.bound()
+    assert b.sweeps_done == 30 and b.R_min >= 0.0 and 0.0 <= b.bound < 0.82628
+    sub = idx[: 1 << 18]
+    comp = np.uint64(N - 1) - sub
+    a_bits = sub & np.uint64(0xAAAAAAAAAAAAAAAA)
+    b_bits = sub & np.uint64(0x5555555555555555)
+    swap = (a_bits >> np.uint64(1)) | (b_bits << np.uint64(1))
+    v = h.table_gather(sub)
+    assert np.array_equal(v, h.table_gather(comp))
+    assert np.array_equal(v, h.table_gather(swap))
+    h.destroy()
+
+
 @pytest.fixture(autouse=True)
 def _release_cached_memory():
     yield
