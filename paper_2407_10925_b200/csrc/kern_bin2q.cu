@@ -118,6 +118,24 @@ __device__ __forceinline__ void ld4<double>(const double* p, double (&v)[4]) {
   const double2 b = reinterpret_cast<const double2*>(p)[1];
   v[0] = a.x; v[1] = a.y; v[2] = b.x; v[3] = b.y;
 }
+// raw 4-entry group in the storage type (no widening)
+__device__ __forceinline__ void ld4r(const float* p, float (&v)[4]) {
+  const float4 f = *reinterpret_cast<const float4*>(p);
+  v[0] = f.x; v[1] = f.y; v[2] = f.z; v[3] = f.w;
+}
+__device__ __forceinline__ void sel4f(bool s, const float (&x)[4], const float (&y)[4],
+                                      float (&a)[4], float (&b)[4]) {
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    a[k] = s ? y[k] : x[k];
+    b[k] = s ? x[k] : y[k];
+  }
+}
+__device__ __forceinline__ void widen4(const float (&x)[4], double (&v)[4]) {
+#pragma unroll
+  for (int k = 0; k < 4; ++k) v[k] = (double)x[k];
+}
+
 template <typename T>
 __device__ __forceinline__ void st4(T* p, double a, double b, double c, double d);
 template <>
@@ -181,6 +199,57 @@ __device__ __forceinline__ void pair_quads(const T* bw, const T* bp, const T* sr
   const uint64_t of = meta[3], om = meta[4], opf = meta[5], opm = meta[6];
   const bool rows_x = of != kNone || om != kNone;
   const bool rows_p = !self && (opf != kNone || opm != kNone);
+  if constexpr (sizeof(T) == 4 && !WMODE) {
+    // fp32 storage, sweep: the Q1 value round32(max(0.5 (x0 + x1), 0.5 (y0 + y1))) of fp64
+    // arithmetic equals the same expression evaluated in fp32 (a two-term fp32 sum is exact in
+    // fp64 or off by less than half an fp32 ulp, so no double rounding; halving and max commute
+    // with rounding), so Q1 stays in fp32; only the Q0 rows that are stored widen to fp64 (their
+    // four-term sums are not exact in fp32).
+    for (uint32_t qd = threadIdx.x; qd < TT / 4; qd += kThreads) {
+      const uint32_t o0 = 4 * qd;
+      const uint32_t g = 2 * pairswap32(o0), u = 2 * (TT - 4 - o0);
+      float X1[4], X2[4], A[4], B[4], P1[4], P2[4], Ap[4], Bp[4];
+      const bool sx = (qd >> SX) & 1u, sp = (qd >> SP) & 1u;
+      ld4r(reinterpret_cast<const float*>(bw) + gbase<TT, MW>(sx ? g + 4 : g), X1);
+      ld4r(reinterpret_cast<const float*>(bw) + gbase<TT, MW>(sx ? g : g + 4), X2);
+      ld4r(reinterpret_cast<const float*>(bp) + gbase<TT, MP>(sp ? u + 4 : u), P1);
+      ld4r(reinterpret_cast<const float*>(bp) + gbase<TT, MP>(sp ? u : u + 4), P2);
+      sel4f(sx, X1, X2, A, B);
+      sel4f(sp, P1, P2, Ap, Bp);
+      constexpr uint32_t c0 = comp<MW>(0), c1 = comp<MW>(1), c2 = comp<MW>(2), c3 = comp<MW>(3);
+      constexpr uint32_t d0 = comp<MP>(0), d1 = comp<MP>(1), d2 = comp<MP>(2), d3 = comp<MP>(3);
+      const float bx[4] = {0.5f * (A[c0] + A[c1]), 0.5f * (B[c0] + B[c1]),
+                           0.5f * (A[c2] + A[c3]), 0.5f * (B[c2] + B[c3])};
+      const float bq[4] = {0.5f * (Bp[d2] + Bp[d3]), 0.5f * (Bp[d0] + Bp[d1]),
+                           0.5f * (Ap[d2] + Ap[d3]), 0.5f * (Ap[d0] + Ap[d1])};
+      float v[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        v[k] = bx[k];
+        if (bq[k] > v[k]) v[k] = bq[k];
+      }
+      const uint32_t qb = pairswap32(~o0 & (TT - 1) & ~3u);
+      float* df = reinterpret_cast<float*>(dst);
+      if (oQ1 != kNone) *reinterpret_cast<float4*>(df + oQ1 + o0) = make_float4(v[0], v[1], v[2], v[3]);
+      if (oQ1p != kNone) *reinterpret_cast<float4*>(df + oQ1p + qb) = make_float4(v[3], v[1], v[2], v[0]);
+      double G[4];
+      if (rows_x) {
+        widen4(A, G);
+        q0_group<T, MW, false>(G, g >> 2, TT / 2, src, dst, of, om, nullptr, R0, R1, wm0, wm1);
+        widen4(B, G);
+        q0_group<T, MW, false>(G, (g >> 2) + 1, TT / 2, src, dst, of, om, nullptr, R0, R1, wm0,
+                               wm1);
+      }
+      if (rows_p) {
+        widen4(Ap, G);
+        q0_group<T, MP, false>(G, u >> 2, TT / 2, src, dst, opf, opm, nullptr, R0, R1, wm0, wm1);
+        widen4(Bp, G);
+        q0_group<T, MP, false>(G, (u >> 2) + 1, TT / 2, src, dst, opf, opm, nullptr, R0, R1, wm0,
+                               wm1);
+      }
+    }
+    return;
+  }
   for (uint32_t qd = threadIdx.x; qd < TT / 4; qd += kThreads) {
     const uint32_t o0 = 4 * qd;
     const uint32_t g = 2 * pairswap32(o0), u = 2 * (TT - 4 - o0);
@@ -359,6 +428,12 @@ __global__ void __launch_bounds__(kThreads, MINB) bin2q_kernel(Bin2QArgs a) {
     R0 = dec_ord(a.red_in[0]);
     R1 = dec_ord(a.red_in[1]);
   }
+  // items: with a schedule, item c is the tile pair of tile sched[c] (c = blockIdx.x + k G);
+  // without one, the pair representatives in tile order
+  const uint32_t* sched = (a.sched && a.sched_m == M) ? a.sched : nullptr;
+  const uint64_t nitems = sched ? a.nitems : g.ntiles;
+  auto first = [&](uint64_t c) { return sched ? c : qnext(g, c, G, LOG); };
+  auto tile_of = [&](uint64_t c) -> uint64_t { return sched ? (uint64_t)__ldg(sched + c) : c; };
   uint64_t pc = 0;  // producer cursor (thread 0 only)
   QItem pit;        // its map entries, fetched one item ahead
   if (tid == 0) {
@@ -367,18 +442,22 @@ __global__ void __launch_bounds__(kThreads, MINB) bin2q_kernel(Bin2QArgs a) {
   }
   __syncthreads();
   if (tid == 0) {
-    pc = qnext(g, blockIdx.x, G, LOG);
-    if (pc < g.ntiles) qlookup<M>(g, map, pc, pit);
-    for (int s = 0; s < S && pc < g.ntiles; ++s) {
-      qissue<T, M, C::UTMA>(g, pit, pc, in + (size_t)s * C::STAGE, &bars[s], metas + 8 * s, src);
-      pc = qnext(g, pc + G, G, LOG);
-      if (pc < g.ntiles) qlookup<M>(g, map, pc, pit);
+    pc = first(blockIdx.x);
+    uint64_t ptau = pc < nitems ? tile_of(pc) : 0;
+    if (pc < nitems) qlookup<M>(g, map, ptau, pit);
+    for (int s = 0; s < S && pc < nitems; ++s) {
+      qissue<T, M, C::UTMA>(g, pit, ptau, in + (size_t)s * C::STAGE, &bars[s], metas + 8 * s,
+                            src);
+      pc = first(pc + G);
+      if (pc < nitems) {
+        ptau = tile_of(pc);
+        qlookup<M>(g, map, ptau, pit);
+      }
     }
   }
 
   uint32_t i = 0;
-  for (uint64_t cc = qnext(g, blockIdx.x, G, LOG); cc < g.ntiles;
-       cc = qnext(g, cc + G, G, LOG), ++i) {
+  for (uint64_t cc = first(blockIdx.x); cc < nitems; cc = first(cc + G), ++i) {
     const uint32_t s = i % S;
     const uint32_t parity = (i / S) & 1u;
     T* buf = in + (size_t)s * C::STAGE;
@@ -406,10 +485,10 @@ __global__ void __launch_bounds__(kThreads, MINB) bin2q_kernel(Bin2QArgs a) {
     }
 #undef LCSB_Q1
     __syncthreads();  // stage s (data and metadata) is free again
-    if (tid == 0 && pc < g.ntiles) {
-      qissue<T, M, C::UTMA>(g, pit, pc, buf, &bars[s], metas + 8 * s, src);
-      pc = qnext(g, pc + G, G, LOG);
-      if (pc < g.ntiles) qlookup<M>(g, map, pc, pit);
+    if (tid == 0 && pc < nitems) {
+      qissue<T, M, C::UTMA>(g, pit, tile_of(pc), buf, &bars[s], metas + 8 * s, src);
+      pc = first(pc + G);
+      if (pc < nitems) qlookup<M>(g, map, tile_of(pc), pit);
     }
   }
   if (WMODE) block_max2_to(wm0, wm1, a.red_out);
@@ -433,7 +512,8 @@ cudaError_t launch_q(const Bin2QArgs& a, cudaStream_t s, int sms) {
     cap = (uint64_t)per_sm * sms;
   }
   if (a.K < M + 1 || a.ell < a.K + 1) return cudaErrorInvalidValue;
-  const uint64_t ntiles = 1ull << (2 * (a.ell - 1 - M));
+  const uint64_t ntiles =
+      (a.sched && a.sched_m == M) ? a.nitems : (1ull << (2 * (a.ell - 1 - M)));
   uint64_t blocks = cap < ntiles ? cap : ntiles;
   if (blocks < 1) blocks = 1;
   bin2q_kernel<T, M, S, WMODE, MINB><<<(unsigned)blocks, kThreads, C::SMEM, s>>>(a);

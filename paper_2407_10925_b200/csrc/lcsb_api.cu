@@ -9,7 +9,9 @@
 #include <stdlib.h>
 #include <string.h>
 
+#include <mutex>
 #include <new>
+#include <vector>
 
 #include "lcsb_internal.cuh"
 
@@ -31,6 +33,9 @@ struct lcsb {
   int qK, qM;     // quarter table: blocks of 4^qK, tiles of 4^qM
   uint32_t* qmap; // quarter table: device block map
   size_t qmap_bytes;
+  uint32_t* qsched;  // quarter table: item order of the sweep (NULL = natural order)
+  size_t qsched_bytes;
+  uint64_t qsched_n;
   int bin2_variant;  // 0 auto; see pick_bin2_variant
   int bin2q_variant; // 0 auto; LCSB_BIN2Q_VARIANT (A/B only)
   uint64_t n_logical;
@@ -159,6 +164,109 @@ static bool build_quarter_map(int ell, int K, uint32_t* map) {
     if (b > q) map[b] = (map[q] & ~3u) | (((b >> (PL - 2)) & 1ull) ? 2u : 1u);
   }
   return next == quarter_slots(ell, K);
+}
+
+// Item order of the quarter sweep ("L2 schedule").  Block graph: nodes = stored
+// blocks, edges = tile pairs {t, psi t} joining the stored blocks of their two adv_b windows;
+// every block has four window ends (two per logical image).  A 2-colouring that cuts most edges
+// (BFS colouring + local search) gives a side A whose blocks have their tile pairs mostly on
+// the other side; listing each A-block's tile pairs consecutively makes them run concurrently on
+// neighbouring CTAs, so the block's four windows -- its two logical images -- come from DRAM once
+// and from L2 after.  The order is a permutation of the pair representatives; the arithmetic of
+// every item is unchanged.  Cached per (l, K, M): it depends on nothing else.
+static bool quarter_schedule(int ell, int K, int M, const uint32_t* map,
+                             std::vector<uint32_t>& out) {
+  static std::mutex mu;
+  static int c_ell = 0, c_K = 0, c_M = 0;
+  static std::vector<uint32_t> cache;
+  std::lock_guard<std::mutex> lock(mu);
+  if (c_ell == ell && c_K == K && c_M == M) {
+    out = cache;
+    return true;
+  }
+  const int L = 2 * ell;
+  const uint64_t lmask = (1ull << L) - 1, q1 = 1ull << (L - 2);
+  const uint64_t amask = 0xAAAAAAAAAAAAAAAAull & lmask, bmask = 0x5555555555555555ull & lmask;
+  const uint64_t T = 1ull << (2 * M);
+  const uint64_t ntiles = 1ull << (2 * (ell - 1 - M));
+  const uint64_t nslots = quarter_slots(ell, K);
+  auto win = [&](uint64_t x) { return (x & amask) | ((x & bmask & ~q1) << 2); };
+  std::vector<uint32_t> etau, eu, ev;
+  for (uint64_t tau = 0; tau < ntiles; ++tau) {
+    const uint64_t x0 = q1 + tau * T;
+    const uint64_t p0 = pairswap_hd(~x0 & lmask) & ~(T - 1);
+    if (((p0 - q1) >> (2 * M)) < tau) continue;  // the pair is an item at its smaller tile
+    etau.push_back((uint32_t)tau);
+    eu.push_back(map[win(x0) >> (2 * K)] >> 2);
+    ev.push_back(map[win(p0) >> (2 * K)] >> 2);
+  }
+  const size_t E = etau.size();
+  std::vector<uint32_t> off(nslots + 1, 0);
+  for (size_t e = 0; e < E; ++e) {
+    off[eu[e] + 1]++;
+    if (ev[e] != eu[e]) off[ev[e] + 1]++;
+  }
+  for (uint64_t v = 0; v < nslots; ++v) off[v + 1] += off[v];
+  std::vector<uint32_t> adj(off[nslots]), fill(off.begin(), off.end() - 1);
+  for (size_t e = 0; e < E; ++e) {
+    adj[fill[eu[e]]++] = (uint32_t)e;
+    if (ev[e] != eu[e]) adj[fill[ev[e]]++] = (uint32_t)e;
+  }
+  auto other = [&](uint32_t e, uint32_t v) { return eu[e] == v ? ev[e] : eu[e]; };
+  std::vector<int8_t> col(nslots, -1);
+  std::vector<uint32_t> order;
+  order.reserve(nslots);
+  for (uint64_t s0 = 0; s0 < nslots; ++s0) {
+    if (col[s0] >= 0) continue;
+    col[s0] = 0;
+    size_t head = order.size();
+    order.push_back((uint32_t)s0);
+    while (head < order.size()) {
+      const uint32_t u = order[head++];
+      for (uint32_t i = off[u]; i < off[u + 1]; ++i) {
+        const uint32_t w = other(adj[i], u);
+        if (col[w] < 0) {
+          col[w] = (int8_t)(1 - col[u]);
+          order.push_back(w);
+        }
+      }
+    }
+  }
+  for (int pass = 0; pass < 16; ++pass) {  // local search: fewer same-coloured edges
+    size_t flips = 0;
+    for (uint64_t v = 0; v < nslots; ++v) {
+      int same = 0, diff = 0;
+      for (uint32_t i = off[v]; i < off[v + 1]; ++i) {
+        const uint32_t w = other(adj[i], (uint32_t)v);
+        if (w == v) continue;
+        if (col[w] == col[v]) ++same; else ++diff;
+      }
+      if (same > diff) {
+        col[v] ^= 1;
+        ++flips;
+      }
+    }
+    if (!flips) break;
+  }
+  std::vector<uint8_t> done(E, 0);
+  out.clear();
+  out.reserve(E);
+  for (uint32_t v : order) {
+    if (col[v] != 0) continue;
+    for (uint32_t i = off[v]; i < off[v + 1]; ++i)
+      if (!done[adj[i]]) {
+        done[adj[i]] = 1;
+        out.push_back(etau[adj[i]]);
+      }
+  }
+  for (size_t e = 0; e < E; ++e)
+    if (!done[e]) out.push_back(etau[e]);
+  if (out.size() != E) return false;
+  cache = out;
+  c_ell = ell;
+  c_K = K;
+  c_M = M;
+  return true;
 }
 
 // ---------------------------------------------------------------- planning
@@ -427,6 +535,7 @@ extern "C" void lcsb_destroy(lcsb_t* h) {
       for (int i = 0; i < h->ntab; ++i) dev_free(h, h->tabs[k][i], h->tab_bytes);
   dev_free(h, h->red, 256);
   dev_free(h, h->qmap, h->qmap_bytes);
+  dev_free(h, h->qsched, h->qsched_bytes);
   for (int i = 0; i < 3; ++i) dev_free(h, h->pools[i], h->pool_bytes);
   for (int k = 0; k <= kMaxD; ++k)
     for (int i = 0; i < kMaxGen; ++i) dev_free(h, h->spools[k][i], h->spool_bytes[k]);
@@ -602,6 +711,18 @@ extern "C" int lcsb_create_ex(const lcsb_config* cfg, lcsb_t** out) {
     const bool ok = hm && h->qmap && build_quarter_map(cfg->ell, h->qK, hm);
     e = ok ? cudaMemcpyAsync(h->qmap, hm, h->qmap_bytes, cudaMemcpyHostToDevice, s) : cudaSuccess;
     if (e == cudaSuccess && ok) e = cudaStreamSynchronize(s);
+    if (ok && e == cudaSuccess && !getenv("LCSB_NO_QSCHED") && cfg->ell - h->qM - 1 >= 4) {
+      std::vector<uint32_t> sched;  // the L2 item order of the sweep (large tables)
+      if (quarter_schedule(cfg->ell, h->qK, h->qM, hm, sched)) {
+        h->qsched_n = sched.size();
+        h->qsched_bytes = sched.size() * sizeof(uint32_t);
+        h->qsched = (uint32_t*)dev_alloc(h, h->qsched_bytes);
+        if (h->qsched) {
+          e = cudaMemcpyAsync(h->qsched, sched.data(), h->qsched_bytes, cudaMemcpyHostToDevice, s);
+          if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+        }
+      }
+    }
     free(hm);
     if (!ok || e != cudaSuccess) {
       lcsb_destroy(h);
@@ -701,6 +822,9 @@ static void fill_bin2q(const lcsb_t* h, Bin2QArgs* a, int in_slot, int out_slot)
   a->map = h->qmap;
   a->ell = h->cfg.ell;
   a->K = h->qK;
+  a->sched = h->qsched;
+  a->nitems = h->qsched_n;
+  a->sched_m = h->qM;
 }
 
 static int enqueue_sweeps(lcsb_t* h, int64_t n, cudaStream_t s);
@@ -1001,7 +1125,7 @@ extern "C" uint64_t lcsb_stored_states(const lcsb_t* h) { return h ? h->n_stored
 extern "C" uint64_t lcsb_device_bytes(const lcsb_t* h) {
   if (!h) return 0;
   uint64_t b = (uint64_t)h->tab_bytes * (uint64_t)h->ntab * (uint64_t)h->nown + 256 +
-               h->qmap_bytes + 3 * (uint64_t)h->pool_bytes;
+               h->qmap_bytes + h->qsched_bytes + 3 * (uint64_t)h->pool_bytes;
   for (int k = 0; k <= kMaxD; ++k)
     for (int i = 0; i < kMaxGen; ++i)
       if (h->spools[k][i]) b += h->spool_bytes[k];

@@ -125,6 +125,11 @@ struct Bin2QArgs {
   int K;
   const unsigned long long* red_in;
   unsigned long long* red_out;
+  // optional item order (the sweep of tile M == sched_m only): sched[c] = tile index of the c-th
+  // tile pair; NULL = the natural order of the pair representatives
+  const uint32_t* sched;
+  uint64_t nitems;
+  int sched_m;
 };
 
 __host__ __device__ inline uint64_t pairswap_hd(uint64_t v) {

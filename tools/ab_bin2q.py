@@ -3,8 +3,9 @@
   python tools/ab_bin2q.py --ell 17 --dtype f32 --sweeps 20 --variants 0,1,2,3
 Each variant runs in a fresh handle; the sweep is timed with CUDA events; every variant must
 give the same sampled entries as the half table.  alg_GBps counts the layout's compulsory bytes
-(2 x stored: read once, write once); moved_GBps the bytes the kernel moves (half table: 2 x
-stored; quarter table: 3 x stored -- every stored block is read once per logical image).
+(2 x stored: read once, write once); moved_GBps the bytes the kernel requests (half table: 2 x
+stored; quarter table: 3 x stored -- every stored block is loaded once per logical image; with
+the L2 item schedule part of the second loads hit L2, so this can exceed the DRAM peak).
 """
 import argparse
 import json
