@@ -177,7 +177,7 @@ static bool build_quarter_map(int ell, int K, uint32_t* map) {
 static bool quarter_schedule(int ell, int K, int M, const uint32_t* map,
                              std::vector<uint32_t>& out) {
   static std::mutex mu;
-  static int c_ell = 0, c_K = 0, c_M = 0;
+  static int c_ell = 0, c_K = 0, c_M = 0;  // (A/B: LCSB_QSCHED=1 / 2 is read once per process)
   static std::vector<uint32_t> cache;
   std::lock_guard<std::mutex> lock(mu);
   if (c_ell == ell && c_K == K && c_M == M) {
@@ -248,16 +248,29 @@ static bool quarter_schedule(int ell, int K, int M, const uint32_t* map,
     }
     if (!flips) break;
   }
-  std::vector<uint8_t> done(E, 0);
+  std::vector<uint8_t> done(E, 0), grouped(nslots, 0);
   out.clear();
   out.reserve(E);
-  for (uint32_t v : order) {
-    if (col[v] != 0) continue;
+  auto emit_group = [&](uint32_t v) {  // an A-block's not yet listed tile pairs, consecutively
+    grouped[v] = 1;
     for (uint32_t i = off[v]; i < off[v + 1]; ++i)
       if (!done[adj[i]]) {
         done[adj[i]] = 1;
         out.push_back(etau[adj[i]]);
       }
+  };
+  // v2 (default): walking the BFS order, a B-block emits the groups of all its A-neighbours
+  // together, so its own windows (read by those groups) are consumed close in time as well
+  static const int version = getenv("LCSB_QSCHED") ? atoi(getenv("LCSB_QSCHED")) : 2;
+  for (uint32_t v : order) {
+    if (col[v] == 0) {
+      if (!grouped[v]) emit_group(v);
+    } else if (version >= 2) {
+      for (uint32_t i = off[v]; i < off[v + 1]; ++i) {
+        const uint32_t w = other(adj[i], v);
+        if (col[w] == 0 && !grouped[w]) emit_group(w);
+      }
+    }
   }
   for (size_t e = 0; e < E; ++e)
     if (!done[e]) out.push_back(etau[e]);
