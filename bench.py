@@ -348,7 +348,34 @@ def _parallel_apply_at(fo, w, src, idx, cores):
         list(ex.map(lambda p: fo.apply_F_at(w["sigma"], w["d"], w["ell"], src, p), parts))
 
 
+class _JsonOnlyStdout:
+    """Library chatter written to file descriptor 1 by C code (e.g. NCCL's version banner) goes
+    to stderr while the bench runs; only the JSON line is printed to the real stdout."""
+
+    def __enter__(self):
+        sys.stdout.flush()
+        self.saved = os.dup(1)
+        os.dup2(2, 1)
+        return self
+
+    def emit(self, line: str):
+        sys.stdout.flush()
+        os.dup2(self.saved, 1)
+        print(line, flush=True)
+        os.dup2(2, 1)
+
+    def __exit__(self, *exc):
+        sys.stdout.flush()
+        os.dup2(self.saved, 1)
+        os.close(self.saved)
+
+
 def main():
+    with _JsonOnlyStdout() as out:
+        _main(out)
+
+
+def _main(out):
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
@@ -385,14 +412,11 @@ def main():
                "cpu_baseline": base,
                "e2e": {"value": base["value"], "unit": "state-updates/s",
                        "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
-        print(json.dumps(res), flush=True)
+        out.emit(json.dumps(res))
         return
 
     import torch
     if ws > 1 or args.force_sharded:
-        # NCCL's version banner goes to stdout; keep stdout to the one JSON line
-        if os.environ.get("NCCL_DEBUG", "").upper() in ("", "VERSION"):
-            os.environ["NCCL_DEBUG"] = "WARN"
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
         os.environ.setdefault("MASTER_PORT", "29517")
         os.environ.setdefault("RANK", str(rank))
@@ -402,7 +426,7 @@ def main():
     if rank == 0:
         if not args.no_cpu_baseline and ws == 1:
             res["cpu_baseline"] = cpu_baseline(w)
-        print(json.dumps(res), flush=True)
+        out.emit(json.dumps(res))
     if torch.distributed.is_initialized():
         torch.distributed.destroy_process_group()
 

@@ -742,9 +742,13 @@ extern "C" int lcsb_create_ex(const lcsb_config* cfg, lcsb_t** out) {
       return set_err(nullptr, ok ? LCSB_ECUDA : LCSB_ECAPACITY, "quarter map setup failed");
     }
   }
-  // W_0 = 0: every live generation starts at zero
+  // W_0 = 0: every generation the first sweep reads starts at zero.  The
+  // slot the first sweep writes, (cur + 1) % ntab with cur = 0, is overwritten entirely (every
+  // stored entry is written once per sweep) before anything reads it; generations older than
+  // the start read out as W_0 = 0 (readout).
   for (int k = h->first; k < h->first + h->nown; ++k)
     for (int i = 0; i < h->ntab; ++i) {
+      if (i == 1 % h->ntab && h->ntab > 1) continue;
       e = cudaMemsetAsync(h->tabs[k][i], 0, h->tab_bytes, s);
       if (e != cudaSuccess) {
         lcsb_destroy(h);
@@ -781,9 +785,12 @@ extern "C" int lcsb_reset(lcsb_t* h) {
   CU(h, cudaSetDevice(h->device));
   int rc = barrier(h);  // nobody is still sweeping into our tables
   if (rc != LCSB_OK) return rc;
+  // zero the generations the first sweep reads (cur = 0); its output slot 1 is overwritten
+  // entirely by that sweep (see lcsb_create)
   for (int k = h->first; k < h->first + h->nown; ++k)
     for (int i = 0; i < h->ntab; ++i)
-      CU(h, cudaMemsetAsync(h->tabs[k][i], 0, h->tab_bytes, (cudaStream_t)h->cfg.stream));
+      if (!(i == 1 % h->ntab && h->ntab > 1))
+        CU(h, cudaMemsetAsync(h->tabs[k][i], 0, h->tab_bytes, (cudaStream_t)h->cfg.stream));
   rc = barrier(h);  // everyone's tables are zero before anyone sweeps into them
   if (rc != LCSB_OK) return rc;
   for (int i = 0; i < 3; ++i)
@@ -1084,6 +1091,10 @@ static int readout(lcsb_t* h, int which, uint64_t first, uint64_t count, const u
       if (host_idx[i] >= h->n_logical)
         return set_err(h, LCSB_EINVAL, "index %llu out of range", (unsigned long long)host_idx[i]);
   if (count == 0) return LCSB_OK;
+  if (which > h->sweeps_done) {  // a generation before the start: W_0 = 0 (never stored)
+    memset(host_dst, 0, count * sizeof(double));
+    return LCSB_OK;
+  }
   CU(h, cudaSetDevice(h->device));
   cudaStream_t s = (cudaStream_t)h->cfg.stream;
   const int slot = slot_back(h, which);
