@@ -77,8 +77,10 @@ typedef struct {
   int32_t form;     /* LCSB_FORM_* */
   int32_t rmode;    /* LCSB_R_* : which R gives lcsb_bound_t.bound / best_bound */
   int32_t symmetry; /* -1 auto; 0 full logical table; 1 complement-folded half table
-                       (two-array binary only, l >= 2); 2 quarter table:
-                       one entry per orbit of {id, complement, string swap, both} (two-array
+                       (two-array binary only, l >= 2); 2 symmetry-folded
+                       ("quarter") table: one entry per orbit of {id, complement, string swap,
+                       both}, same-head states also folded under the tail complement
+                       (v'[00t] = v'[00t~]): 3/16 of the states (two-array
                        binary, unsharded, l >= block_log4 + 1; string swap = reading R19 of
                        DESIGN.md, implied by "if symmetry is fully exploited").
                        AUTO = 2 for l >= 12 unsharded, 1 otherwise when allowed, else 0. */
@@ -171,9 +173,9 @@ int lcsb_shard_locate(int32_t ell, int32_t shards, uint64_t logical, int32_t* sh
 /* Host-only layout query (no GPU needed): the stored index of logical state `logical` in the
  * quarter table (symmetry = 2) of the binary two-array form with length-ell strings and blocks
  * of 4^block_log4 entries, and the number of stored entries.  Every stored entry holds states
- * of ONE orbit of {id, complement, string swap, both} (so sharing it is exact), every stored
- * entry is used, and an orbit occupies two entries only inside the few blocks that the swap
- * maps onto themselves.  Requires 3 <= ell <= 31, 2 <= block_log4 <= ell - 1,
+ * of ONE class -- an orbit of {id, complement, string swap, both}, for same-head states joined
+ * with its tail complement -- so sharing it is exact; every stored entry is used; a class
+ * occupies two entries only inside the few blocks that a symmetry maps onto themselves.  Requires 3 <= ell <= 31, 2 <= block_log4 <= ell - 1,
  * ell - block_log4 <= 12.  Errors: EINVAL. */
 int lcsb_quarter_locate(int32_t ell, int32_t block_log4, uint64_t logical, uint64_t* stored,
                         uint64_t* n_stored);

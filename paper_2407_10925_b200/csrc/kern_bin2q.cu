@@ -1,5 +1,7 @@
-// kern_bin2q.cu -- the binary (sigma = d = 2) two-array sweep on the QUARTER table: one stored
-// entry per orbit of the symmetry group {id, complement c, string swap s, psi = c s}.
+// kern_bin2q.cu -- the binary (sigma = d = 2) two-array sweep on the symmetry-folded ("quarter")
+// table: one stored entry per class of states with provably equal values -- orbits of
+// {id, complement c, string swap s, psi = c s}, and for same-head states also the tail
+// complement t (reading R18) -- 3/16 of the logical states.
 //
 // Method: identical arithmetic to kern_bin2_tma.cu (Eqs. F1/F0
 // PAPER.md:752-779), same tile pairing {t, psi(t)} and the same adv_b windows.  Only the
@@ -7,13 +9,14 @@
 //
 //  * Half-table index space [0, 2^(2l-1)) (a_0 = 0, complement folded, Eq. comp_eq) is cut into
 //    blocks of 4^K entries; a block is fixed by its top l-K characters pairs ("prefix").  The
-//    residual symmetry of the half table maps blocks onto blocks with a digit-wise permutation
-//    inside: Q0 blocks (heads 00) pair under s (swap the two bits of every pair), Q1 blocks
-//    (heads 01) under psi (pairswap of the complement).  Of each block pair only the smaller
-//    prefix is stored ("canonical", mode 0); the other reads it through the permutation
-//    (mode 1 = s, mode 2 = psi).  map[block] = (slot << 2) | mode, built by the host.  The
-//    string swap W(a,b) = W(b,a) is an exact invariant of every iterate (reading R19), the
-//    complement one is Eq. comp_eq.
+//    residual symmetries of the half table map blocks onto blocks with a digit-wise permutation
+//    inside: Q1 blocks (heads 01) pair under psi (pairswap of the complement); Q0 blocks
+//    (heads 00) fold under {id, s, t, s t} (s: swap the two bits of every pair; t: complement
+//    every tail digit, i.e. reverse the block).  Of each block orbit only the smallest prefix is
+//    stored ("canonical", mode 0); the others read it through the permutation (mode 1 = s,
+//    2 = psi or s t, 3 = t).  map[block] = (slot << 2) | mode, built by the host.  The string
+//    swap W(a,b) = W(b,a) is an exact invariant of every iterate (reading R19), the complement
+//    one is Eq. comp_eq, the tail complement of same-head states is v'[00t] = v'[00t~] (R18).
 //  * Reads: a tile's adv_b window (2T entries with free low 2M+1 bits) of a mode-0 block is one
 //    contiguous run; of a permuted block it is two runs of T (bit 2M+1 <-> bit 2M exchanged),
 //    loaded with two bulk copies into the same smem slots; the consumer indexes smem through
@@ -22,9 +25,11 @@
 //  * Writes: of every output run (Q1 tile, Q0 row run, Q0 mirror run) only those lying in a
 //    canonical block are stored -- each stored entry is written exactly once.  psi(t)'s outputs
 //    equal t's (the pair computes one max for both), so exactly one of the two Q1 runs is
-//    written unless the block is psi-fixed.
-//  => per sweep: read 2 x stored + write 1 x stored = 1.5 x (half table) bytes, 3 bytes per
-//     logical state in fp32 (vs 4 for the half table).
+//    written unless the block is psi-fixed; a Q0 row run and its mirror run are t-images, so
+//    one of the two is written.
+//  => per sweep every logical window of the half table is loaded once (the L2 item schedule,
+//     lcsb_api.cu, serves most repeated loads of a stored block from L2) and 3/8 of the half
+//     table is written.
 #include <math.h>
 #include <stdlib.h>
 
@@ -95,6 +100,7 @@ __device__ __forceinline__ uint64_t qrun(const QGeo& g, uint32_t m, uint64_t s) 
 template <uint32_t TT, int MODE>
 __device__ __forceinline__ uint32_t gbase(uint32_t g) {  // smem start of the group at logical g
   if (MODE == 0) return g;
+  if (MODE == 3) return 2u * TT - 4u - g;  // tail complement: the window reversed
   const uint32_t w = (MODE == 1) ? g : (~(g + 3u) & (2u * TT - 1u));
   return (w & TT) | pairswap32(w & (TT - 1u));
 }
@@ -102,7 +108,7 @@ template <int MODE>
 __device__ __forceinline__ constexpr uint32_t comp(uint32_t d) {  // smem slot of logical digit d
   return MODE == 0 ? d
                    : (MODE == 1 ? (((d & 1u) << 1) | (d >> 1))
-                                : ((((3u - d) & 1u) << 1) | ((3u - d) >> 1)));
+                                : (MODE == 3 ? 3u - d : ((((3u - d) & 1u) << 1) | ((3u - d) >> 1))));
 }
 
 template <typename T>
@@ -194,7 +200,9 @@ template <typename T, uint32_t TT, int MW, int MP, bool WMODE>
 __device__ __forceinline__ void pair_quads(const T* bw, const T* bp, const T* src, T* dst,
                                            const uint64_t* meta, bool self, const T* us,
                                            double R0, double R1, double& wm0, double& wm1) {
-  constexpr uint32_t SX = (MW == 0) ? 2 : 0, SP = (MP == 0) ? 2 : 1;
+  // A/B load order select bits (bank conflicts): modes 0 and 3 (contiguous, possibly reversed)
+  // alternate on bit 2, the pairswapped modes on bit 0 (x window) / bit 1 (psi window)
+  constexpr uint32_t SX = (MW == 0 || MW == 3) ? 2 : 0, SP = (MP == 0 || MP == 3) ? 2 : 1;
   const uint64_t oQ1 = meta[1], oQ1p = meta[2];
   const uint64_t of = meta[3], om = meta[4], opf = meta[5], opm = meta[6];
   const bool rows_x = of != kNone || om != kNone;
@@ -389,6 +397,8 @@ __device__ __forceinline__ void qissue(const QGeo& g, const QItem& it, uint64_t 
     const uint64_t e = w & g.kmask;
     if ((m & 3u) == 0) {
       tma_load_1d(dst, blk + e, 2 * TT * (uint32_t)sizeof(T), bar);
+    } else if ((m & 3u) == 3) {  // tail complement: one contiguous run, read reversed
+      tma_load_1d(dst, blk + ((~e & g.kmask) & ~(2ull * TT - 1)), 2 * TT * (uint32_t)sizeof(T), bar);
     } else {
       const uint64_t f = ((m & 3u) == 1) ? pairswap(e) : pairswap(~e & g.kmask);
       const uint64_t start = (f & ~(4ull * TT - 1)) | (f & TT);
@@ -465,23 +475,30 @@ __global__ void __launch_bounds__(kThreads, MINB) bin2q_kernel(Bin2QArgs a) {
     mbar_wait(&bars[s], parity);
     __syncthreads();
     const uint32_t modes = (uint32_t)meta[0];
-    const uint32_t mw = modes & 3u, mp = (modes >> 2) & 3u;
+    const uint32_t mw = modes & 3u, mp = (modes >> 2) & 3u;  // 3 only for Q0 (same-head) blocks
     const bool self = (modes & 16u) != 0;
     const T* bw = buf;
     const T* bp = buf + WIN;
     const T* us = C::UTMA ? buf + 2 * WIN : nullptr;
 #define LCSB_Q1(MW, MP) \
   pair_quads<T, TT, MW, MP, WMODE>(bw, bp, src, dst, meta, self, us, R0, R1, wm0, wm1)
-    switch (mw * 3 + mp) {
+    switch (mw * 4 + mp) {
       case 0: LCSB_Q1(0, 0); break;
       case 1: LCSB_Q1(0, 1); break;
       case 2: LCSB_Q1(0, 2); break;
-      case 3: LCSB_Q1(1, 0); break;
-      case 4: LCSB_Q1(1, 1); break;
-      case 5: LCSB_Q1(1, 2); break;
-      case 6: LCSB_Q1(2, 0); break;
-      case 7: LCSB_Q1(2, 1); break;
-      default: LCSB_Q1(2, 2); break;
+      case 3: LCSB_Q1(0, 3); break;
+      case 4: LCSB_Q1(1, 0); break;
+      case 5: LCSB_Q1(1, 1); break;
+      case 6: LCSB_Q1(1, 2); break;
+      case 7: LCSB_Q1(1, 3); break;
+      case 8: LCSB_Q1(2, 0); break;
+      case 9: LCSB_Q1(2, 1); break;
+      case 10: LCSB_Q1(2, 2); break;
+      case 11: LCSB_Q1(2, 3); break;
+      case 12: LCSB_Q1(3, 0); break;
+      case 13: LCSB_Q1(3, 1); break;
+      case 14: LCSB_Q1(3, 2); break;
+      default: LCSB_Q1(3, 3); break;
     }
 #undef LCSB_Q1
     __syncthreads();  // stage s (data and metadata) is free again

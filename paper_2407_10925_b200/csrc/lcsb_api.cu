@@ -145,24 +145,43 @@ static int pick_bin2_variant(int dtype, int ell, int p) {
 // ---------------------------------------------------------------- quarter table layout
 // Auto choice: the quarter table from this l up, the half table below.
 static const int kQuarterAutoEll = 12;
-// blocks of the half table: 2^(2(l-K)-1); stored (canonical) blocks: Q0 and Q1 each have
-// 4^(l-K-1) blocks of which 2^(l-K-1) are fixed by their pairing (every non-head character pair
-// in {00, 11} for s, in {01, 10} for psi), so (4^(l-K-1) + 2^(l-K-1)) / 2 canonical each.
+// blocks of the half table: 2^(2(l-K)-1), m = l-K-1 non-head prefix digits each.  Stored
+// (canonical) blocks, by Burnside: Q1 under {id, psi}: (4^m + 2^m) / 2 (psi fixes prefixes with
+// every digit in {01, 10}); Q0 under {id, s, t, s t}: (4^m + 2^m + 0 + 2^m) / 4 (s fixes digits
+// in {00, 11}, s t those in {01, 10}, t none).
 static uint64_t quarter_map_entries(int ell, int K) { return 1ull << (2 * (ell - K) - 1); }
 static uint64_t quarter_slots(int ell, int K) {
-  return (1ull << (2 * (ell - K - 1))) + (1ull << (ell - K - 1));
+  const int m = ell - K - 1;
+  if (m == 0) return 2;  // the two head blocks
+  return ((1ull << (2 * m)) + (1ull << m)) / 2 + ((1ull << (2 * m)) + (2ull << m)) / 4;
 }
-// map[beta] = (slot << 2) | mode; slots numbered in increasing order of canonical beta
+// map[beta] = (slot << 2) | mode; slots numbered in increasing order of canonical beta (the
+// smallest prefix of its orbit); mode = the symmetry mapping the canonical block to beta
 static bool build_quarter_map(int ell, int K, uint32_t* map) {
   const int PL = 2 * (ell - K);
   const uint64_t nb = quarter_map_entries(ell, K);
   uint64_t next = 0;
-  for (uint64_t b = 0; b < nb; ++b)
-    if (b <= qblock_partner(b, PL)) map[b] = (uint32_t)(next++ << 2);
+  std::vector<uint64_t> canon(nb);
+  std::vector<int> how(nb);
   for (uint64_t b = 0; b < nb; ++b) {
-    const uint64_t q = qblock_partner(b, PL);
-    if (b > q) map[b] = (map[q] & ~3u) | (((b >> (PL - 2)) & 1ull) ? 2u : 1u);
+    const bool q1 = (b >> (PL - 2)) & 1ull;
+    uint64_t c = b;
+    int g = 0;
+    for (int gg = 1; gg <= 3; ++gg) {
+      if (q1 && gg != 2) continue;
+      const uint64_t im = qblock_image(b, PL, gg);
+      if (im < c) {
+        c = im;
+        g = gg;  // b = g(c): every g here is an involution
+      }
+    }
+    canon[b] = c;
+    how[b] = g;
   }
+  for (uint64_t b = 0; b < nb; ++b)
+    if (canon[b] == b) map[b] = (uint32_t)(next++ << 2);
+  for (uint64_t b = 0; b < nb; ++b)
+    if (canon[b] != b) map[b] = (map[canon[b]] & ~3u) | (uint32_t)how[b];
   return next == quarter_slots(ell, K);
 }
 

@@ -115,8 +115,10 @@ __host__ __device__ inline uint64_t global_of_local(uint32_t shard, uint64_t loc
 }
 
 // Quarter table (kern_bin2q.cu): the half table cut into blocks of 4^K entries; map[block] =
-// (slot << 2) | mode, mode 0 = stored here (canonical), 1 = read through the string swap s,
-// 2 = through psi = complement o swap, from the block stored at `slot`.
+// (slot << 2) | mode, mode 0 = stored here (canonical), else read from the block stored at
+// `slot` through the in-block permutation of the symmetry that maps it there: 1 = string swap s
+// (pairswap), 2 = psi = complement o swap (pairswap of the complement; for Q0 blocks the tail
+// complement composed with s), 3 = tail complement t of a same-head block (complement).
 struct Bin2QArgs {
   const void* src;  // input quarter table
   void* dst;        // output quarter table (sweep mode)
@@ -135,12 +137,20 @@ struct Bin2QArgs {
 __host__ __device__ inline uint64_t pairswap_hd(uint64_t v) {
   return ((v & 0xAAAAAAAAAAAAAAAAull) >> 1) | ((v & 0x5555555555555555ull) << 1);
 }
-// partner of half-table block `beta` (prefix of PL = 2(l-K) bits, top bit a_0 = 0 implicit):
-// Q0 blocks (b_0 = 0) pair under the string swap, Q1 blocks (b_0 = 1) under psi
-__host__ __device__ inline uint64_t qblock_partner(uint64_t beta, int PL) {
+// Images of half-table block `beta` (prefix of PL = 2(l-K) bits, top bit a_0 = 0 implicit)
+// under the symmetries the quarter table folds (reading R19, R18):
+//   Q1 blocks (heads 01): psi = complement o swap (pairswap of the complement);
+//   Q0 blocks (heads 00): the string swap s, the tail complement t (the same-head value depends
+//   only on the tails and is complement-invariant: v'[00t] = v'[00t~]) and s t.
+// qblock_image(beta, PL, g) for g = 1 (s), 2 (psi / s t), 3 (t); g = 1, 3 only for Q0 blocks.
+__host__ __device__ inline uint64_t qblock_image(uint64_t beta, int PL, int g) {
   const uint64_t pm = (1ull << PL) - 1;
+  const uint64_t tail = (1ull << (PL - 2)) - 1;  // every prefix digit but the heads
   const bool q1 = (beta >> (PL - 2)) & 1ull;
-  return pairswap_hd(q1 ? (~beta & pm) : beta) & pm;
+  if (q1) return pairswap_hd(~beta & pm) & pm;  // psi (heads 01 -> 01)
+  if (g == 1) return pairswap_hd(beta) & pm;
+  if (g == 3) return beta ^ tail;
+  return pairswap_hd(beta ^ tail) & pm;  // s t
 }
 // stored index of half-table index s (map as above)
 __host__ __device__ inline uint64_t qstored(const uint32_t* map, uint64_t s, int K) {
@@ -149,6 +159,7 @@ __host__ __device__ inline uint64_t qstored(const uint32_t* map, uint64_t s, int
   uint64_t e = s & kmask;
   if ((m & 3u) == 1u) e = pairswap_hd(e) & kmask;
   else if ((m & 3u) == 2u) e = pairswap_hd(~e & kmask) & kmask;
+  else if ((m & 3u) == 3u) e = ~e & kmask;
   return ((uint64_t)(m >> 2) << (2 * K)) | e;
 }
 

@@ -39,10 +39,10 @@ def test_required_bytes_and_validation():
     lib = pkg.load_library()
     # config 4: two-array half table, 2 x 2^33 fp32 entries = 64 GiB (+ scratch)
     assert L.lcsb_required_bytes(2, 2, 17, "f32", symmetry=1) == 2 * (1 << 33) * 4 + 256
-    # default (auto) for l >= 12: the quarter table, 2 x (4^9 + 2^9) blocks of 4^7 fp32 + the
-    # block map (2^19 uint32)
+    # default (auto) for l >= 12: the quarter table, 2 x ((4^9 + 2^9)/2 + (4^9 + 2^10)/4) blocks
+    # of 4^7 fp32 + the block map (2^19 uint32)
     assert L.lcsb_required_bytes(2, 2, 17, "f32") == \
-        2 * ((1 << 18) + (1 << 9)) * (1 << 14) * 4 + 256 + (1 << 19) * 4
+        2 * (131328 + 65792) * (1 << 14) * 4 + 256 + (1 << 19) * 4
     # full table when symmetry is off
     assert L.lcsb_required_bytes(2, 2, 17, "f32", symmetry=0) == 2 * (1 << 34) * 4 + 256
     # config 3: pooled-history KS (kern_q4.cu): 2 tables of 4^16 fp32 + 3 row-mean arrays of

@@ -1,9 +1,12 @@
-"""The quarter table (symmetry = 2, kern_bin2q.cu): one stored entry per orbit of
-{id, complement, string swap, complement o swap} of the binary two-array iterate.
+"""The quarter table (symmetry = 2, kern_bin2q.cu): one stored entry per class of
+states with provably equal values in every binary two-array iterate: orbits of {id, complement,
+string swap, complement o swap}, and for same-head states also the tail complement (the
+same-head value depends only on the tails and is complement-invariant, reading R18).
 
-CPU: the library's host-side layout (lcsb_quarter_locate) against orbits enumerated here from the
-paper's state encoding (interleaved pair), complement (Eq. comp_eq,
-PAPER.md:404-411) and string swap (reading R19) -- no code shared with the library.
+CPU: the library's host-side layout (lcsb_quarter_locate) against classes enumerated here from
+the paper's state encoding (interleaved pair), complement (Eq. comp_eq,
+PAPER.md:404-411), string swap (reading R19) and the mirror identity (R18) -- no code shared
+with the library.
 GPU: the quarter-table kernels against the oracle, element by element (fp32 bit-exact, fp64
 1e-12 relative), across block sizes, tile sizes and the sampled config-4 check.
 """
@@ -29,7 +32,13 @@ def _encode(a, b):
 def _orbit(x, ell):
     a, b = _decode(x, ell)
     ca, cb = [1 - c for c in a], [1 - c for c in b]
-    return min(_encode(a, b), _encode(ca, cb), _encode(b, a), _encode(cb, ca))
+    imgs = [(a, b), (ca, cb), (b, a), (cb, ca)]
+    if a[0] == b[0]:  # same heads: the value depends only on the tails, complement-invariant
+        ta = [a[0]] + [1 - c for c in a[1:]]
+        tb = [b[0]] + [1 - c for c in b[1:]]
+        cta, ctb = [1 - c for c in ta], [1 - c for c in tb]
+        imgs += [(ta, tb), (cta, ctb), (tb, ta), (ctb, cta)]
+    return min(_encode(p, q) for p, q in imgs)
 
 
 @pytest.mark.parametrize("ell,K", [(3, 2), (4, 2), (4, 3), (5, 2), (5, 3), (6, 2), (6, 3),
@@ -44,13 +53,17 @@ def test_quarter_layout_holds_one_orbit_per_entry(ell, K):
         orb = _orbit(x, ell)
         assert owner.setdefault(st, orb) == orb, (x, st)  # never two orbits in one entry
     assert sorted(owner) == list(range(n_stored))        # every stored entry is used
-    # size: (4^(l-K-1) + 2^(l-K-1)) blocks of 4^K -> a quarter of 4^l plus the swap-fixed blocks
-    assert n_stored == ((1 << (2 * (ell - K - 1))) + (1 << (ell - K - 1))) << (2 * K)
+    # size (Burnside over block prefixes, m = l-K-1 non-head digits): Q1 blocks pair under psi,
+    # (4^m + 2^m)/2; Q0 blocks fold under {id, s, t, s t}, (4^m + 2 2^m)/4 -> 3/8 of 4^l / 2
+    m = ell - K - 1
+    slots = 2 if m == 0 else ((4 ** m + 2 ** m) // 2 + (4 ** m + 2 * 2 ** m) // 4)
+    assert n_stored == slots << (2 * K)
     assert len(set(owner.values())) == len({_orbit(x, ell) for x in range(1 << (2 * ell))})
 
 
 def test_quarter_layout_orbit_mates_share_outside_fixed_blocks():
-    """At l = 8, K = 3 all but a 2^-(l-K-1) fraction of the orbits occupy one entry."""
+    """At l = 8, K = 3 all but a small fraction of the classes occupy one entry (the rest: two,
+    inside blocks a symmetry maps onto themselves)."""
     L.load_library()
     ell, K = 8, 3
     entries_per_orbit = {}
@@ -59,7 +72,7 @@ def test_quarter_layout_orbit_mates_share_outside_fixed_blocks():
         entries_per_orbit.setdefault(_orbit(x, ell), set()).add(st)
     doubled = sum(1 for s in entries_per_orbit.values() if len(s) > 1)
     assert all(len(s) <= 2 for s in entries_per_orbit.values())
-    assert doubled <= len(entries_per_orbit) / (1 << (ell - K - 2))
+    assert doubled <= len(entries_per_orbit) / (1 << (ell - K - 3))
 
 
 def test_quarter_layout_rejects_bad_arguments():
@@ -69,11 +82,11 @@ def test_quarter_layout_rejects_bad_arguments():
             L.lcsb_quarter_locate(ell, K, x)
 
 
-def test_quarter_required_bytes_is_about_half_of_half_table():
+def test_quarter_required_bytes_is_three_eighths_of_half_table():
     L.load_library()
     half = L.lcsb_required_bytes(2, 2, 17, "f32", symmetry=1)
     quarter = L.lcsb_required_bytes(2, 2, 17, "f32", symmetry=2)
-    assert 0.5 < quarter / half < 0.51
+    assert 0.375 < quarter / half < 0.38
     # l = 18 in fp32 fits one B200 as a quarter table (2 x 64 GiB + map), not as a half table
     assert L.lcsb_required_bytes(2, 2, 18, "f32", symmetry=2) < 140 * 2 ** 30
     assert L.lcsb_required_bytes(2, 2, 18, "f32", symmetry=1) > 256 * 2 ** 30 - 1
@@ -151,7 +164,7 @@ def test_quarter_equals_half_table_l13(dtype):
     a = L.Lcsb(2, 2, 13, dtype=dtype, symmetry=2)
     b = L.Lcsb(2, 2, 13, dtype=dtype, symmetry=1)
     assert a.kernel_in_use == "bin2q" and b.kernel_in_use == "bin2"
-    assert a.stored_states * 2 < b.stored_states * 1.04  # + the swap-fixed blocks (1/32)
+    assert a.stored_states < 0.40 * b.stored_states  # 3/8 + the self-paired blocks (4 % at l = 13)
     a.sweep(30)
     b.sweep(30)
     idx = splitmix64_indices(0x240710925, 1 << 20, 1 << 26)
@@ -194,7 +207,7 @@ def test_config5_l18_on_one_gpu_sampled_and_properties():
     from seeded_inputs import splitmix64_indices
     N = 1 << 36
     h = L.Lcsb(2, 2, 18, dtype="f32")
-    assert h.kernel_in_use == "bin2q" and h.device_bytes < 140 * 2 ** 30
+    assert h.kernel_in_use == "bin2q" and h.device_bytes < 100 * 2 ** 30
     idx = splitmix64_indices(0x240710925, 1 << 20, N)
     h.sweep(3)
     assert np.array_equal(h.table_gather(idx),
