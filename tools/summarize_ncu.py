@@ -56,7 +56,7 @@ def main():
                "dram_bytes_per_launch": dram}
     json.dump(summary, open(os.path.join(out, f"{base}_ncu.json"), "w"), indent=1)
     json.dump({"workload": wl, "round": rnd, "kernel": summary["kernel"],
-               "dram_bytes_per_launch": dram, "source": f"profiles/{rnd}_{wl}_ncu.json"},
+               "dram_bytes_per_launch": dram, "source": f"profiles/{base}_ncu.json"},
               open(os.path.join(out, f"traffic_{wl}_{tag}.json" if tag else f"traffic_{wl}.json"), "w"),
               indent=1)
     print(json.dumps(summary, indent=1))
