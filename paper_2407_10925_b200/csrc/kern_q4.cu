@@ -1,5 +1,5 @@
-// kern_q4.cu -- KS-form sweep (and W pass) for d = 2 strings over sigma = 4 (BASELINE config 3),
-// full logical table, reading each input generation once per sweep.
+// kern_q4.cu -- KS-form sweep (and W pass) for d = 2 strings over sigma = 4 (BASELINE config 3) on
+// the complement-folded table, reading each stored entry once per sweep.
 //
 // Recurrence (Eq. ineq3, Alg. 1, reading R1): for the pair
 // (a, b) = (h_a alpha, h_b beta) with tails alpha, beta of length l-1,
@@ -9,26 +9,27 @@
 //   adv_b = 1/4  sum_c      g1[(h_a alpha, beta c)]           (|N| = 1 reads one sweep back)
 //   adv_a = 1/4  sum_c      g1[(alpha c, h_b beta)]
 // Layout (reading R14): x = h_a<<(4l-2) | h_b<<(4l-4) | t with t = interleave(alpha, beta), one
-// 4-bit group (a digit, b digit) per character position.  The 16 entries read by P are the
-// contiguous row t<<4 .. t<<4|15; adv_b's 4 entries are contiguous at
+// 4-bit group (a digit, b digit) per character position.  adv_b's 4 entries are contiguous at
 //   y = h_a<<(4l-2) | (t & A) | ((t & B) << 4) | c     (A / B = a / b digit bits of each group).
 //
-// B200 design: a unit is 16^M consecutive tails t for all 16 head pairs
-// (16 x 16^M outputs).  For each h_a its adv_b reads are one contiguous window of 4 x 16^M
-// entries of g1.  adv_a is taken from the string swap W(a,b) = W(b,a):
-// adv_a(h_a,h_b,t) = adv_b(h_b,h_a,swap(t)), and swap maps the unit onto the unit of swapped
-// tails (offset i -> ds(i), the two digits of every group exchanged).  One CTA takes the pair
-// {unit, swap(unit)}, TMA bulk-loads it into shared memory (mbarrier-completed, S stages), and
-// writes all 32 x 16^M outputs with coalesced stores.
+// Storage:
+//  * complement fold: relabelling every symbol d -> 3-d is an alphabet permutation, under which
+//    every iterate is invariant (reading R19 generalised; Eq. comp_eq for sigma = 2), and it maps
+//    x to N-1-x.  Only h_a in {0, 1} is stored (x < N/2); the rest is read at N-1-x;
+//  * pooled history: g2 is read ONLY through P, the mean of a 16-entry row, and P depends only on
+//    the tails t.  Every sweep also writes the row means of the table it produces (fp64, one per
+//    stored row, each summed in Alg. 1's order from the stored values in shared memory), and the
+//    sweep two later reads those instead of g2: the ring holds 2 tables + 3 mean arrays.
 //
-// Pooled history: g2 (two sweeps back) is read ONLY through P, the mean of a 16-entry row, and
-// P depends only on the tails t.  So every sweep also writes the row means of the table it
-// produces (pout[x >> 4], fp64, N/16 entries: each output row of 16 is summed in Alg. 1's
-// order from the stored -- rounded -- values, in shared memory), and the sweep two later reads
-// those TT means per unit side instead of 16 TT entries of g2.  The full g2 table is never read,
-// so the ring holds 2 full tables (+ 3 mean arrays): per sweep read g1 + means, write the new
-// table + means = 2 x table + 2 x table/16 x 2 bytes ratio (9 B per state in fp32 instead of
-// 12 for the three-table KS ring).
+// Work unit: a unit is 16^M consecutive tails.  adv_a is adv_b of the string-swapped state:
+// adv_a(h_a, h_b, t) = adv_b(h_b, h_a, swap t); for h_b >= 2 that window is folded -- it is the
+// window of head 3-h_b of the complemented tails, read reversed.  So a CTA takes the group
+// {u, s u, c u, c s u} (s = swap the two digits of every tail group, c = complement) and loads,
+// for each unit of the group, its two stored adv_b windows (heads 0, 1) and, for the units whose
+// first tail character is < 2, their row means of g2 (the others read their complement's,
+// reversed).  From these it computes all stored outputs of the four units (h_a in {0,1}, every
+// h_b): every stored window is read exactly once per sweep, every stored entry written once:
+// 2 x (stored table) + 2 x (stored means) bytes per sweep, 4.5 B per logical state in fp32.
 #include <math.h>
 #include <stdlib.h>
 
@@ -57,32 +58,43 @@ struct V4T<double> {
   using type = double4;
 };
 
-template <typename T>
+// r <- r + (v + shift), c = 0..3 in order (Alg. 1 line 8); REV: the window is folded, logical
+// c is stored entry 3-c
+template <typename T, bool REV>
 __device__ __forceinline__ double sum4(const T* p, double sh) {
-  // r <- r + (v + shift), c = 0..3 in order (Alg. 1 line 8); p is 4-entry aligned
   const typename V4T<T>::type v = *reinterpret_cast<const typename V4T<T>::type*>(p);
   double r = 0.0;
-  r = r + ((double)v.x + sh);
-  r = r + ((double)v.y + sh);
-  r = r + ((double)v.z + sh);
-  r = r + ((double)v.w + sh);
+  if (!REV) {
+    r = r + ((double)v.x + sh);
+    r = r + ((double)v.y + sh);
+    r = r + ((double)v.z + sh);
+    r = r + ((double)v.w + sh);
+  } else {
+    r = r + ((double)v.w + sh);
+    r = r + ((double)v.z + sh);
+    r = r + ((double)v.y + sh);
+    r = r + ((double)v.x + sh);
+  }
   return r;
 }
+
+constexpr int kGroup = 4;  // units per item (u, s u, c u, c s u), deduplicated
 
 template <typename T, int M, int S, bool WMODE = false>
 struct Q4Cfg {
   static constexpr uint32_t TT = 1u << (4 * M);  // tails per unit
-  static constexpr uint32_t PR = TT * 8 / sizeof(T);  // the unit's TT row means (fp64), in T slots
   static constexpr uint32_t WB = 4 * TT;         // g1 entries per adv_b window
-  static constexpr uint32_t UNIT = PR + 4 * WB;  // entries staged per unit
-  // W pass: also u at the unit pair's 32 output runs (16 head pairs x T tails, per side)
-  static constexpr uint32_t UOUT = WMODE ? 2 * 16 * TT : 0;
-  static constexpr uint32_t STAGE = 2 * UNIT + UOUT;
-  // sweep: the unit pair's outputs staged for the row means of the new table, transposed so a
-  // row's 16 values are 16 "c-rows" apart: [side][head pair][c][NR + 1] (NR = TT/16 rows per
+  static constexpr uint32_t WIN = 2 * WB;        // the two stored windows of a unit (heads 0, 1)
+  static constexpr uint32_t PR = TT * 8 / sizeof(T);  // a unit's TT row means (fp64), in T slots
+  // W pass: also u at the unit's 8 stored output runs (h_a < 2, every h_b; TT tails each)
+  static constexpr uint32_t UOUT = WMODE ? 8 * TT : 0;
+  static constexpr uint32_t UNIT = WIN + PR + UOUT;
+  static constexpr uint32_t STAGE = kGroup * UNIT;
+  // sweep: the group's outputs staged for the row means of the new table, transposed so a row's
+  // 16 values are 16 "c-rows" apart: [unit][head pair (8)][c][NR + 1] (NR = TT/16 rows per
   // head pair, +1 pad: stores and in-order row reads are bank-conflict-free)
   static constexpr uint32_t NR = TT / 16;
-  static constexpr uint32_t OUTS = WMODE ? 0 : 2 * 16 * 16 * (NR + 1);
+  static constexpr uint32_t OUTS = WMODE ? 0 : kGroup * 8 * 16 * (NR + 1);
   static constexpr size_t SMEM =
       (size_t)S * STAGE * sizeof(T) + (size_t)OUTS * sizeof(T) + (size_t)S * sizeof(uint64_t);
 };
@@ -90,14 +102,48 @@ struct Q4Cfg {
 struct Q4Geo {
   int ell;
   uint32_t tail_bits;  // 4 (l - 1)
+  uint32_t ubits;      // tail_bits - 4M: bits of a unit index
   uint64_t nunits;
 };
 
-// next unit >= c (step G) that is the smaller member of its swap pair
-template <int M>
+__device__ __forceinline__ uint64_t unit_comp(const Q4Geo& g, uint64_t u) {
+  return ~u & (g.nunits - 1);
+}
+// first tail character of the unit's tails (its a digit) < 2: its row means are stored
+__device__ __forceinline__ bool unit_low(const Q4Geo& g, uint64_t u) {
+  return ((u >> (g.ubits - 1)) & 1ull) == 0;
+}
+__device__ __forceinline__ uint64_t group_min(const Q4Geo& g, uint64_t u) {
+  const uint64_t su = digit_swap(u), cu = unit_comp(g, u), csu = unit_comp(g, su);
+  uint64_t m = u < su ? u : su;
+  m = m < cu ? m : cu;
+  return m < csu ? m : csu;
+}
+// the group's distinct units in the fixed order (u, s u, c u, c s u); returns the count
+__device__ __forceinline__ int group_units(const Q4Geo& g, uint64_t u, uint64_t (&U)[kGroup]) {
+  const uint64_t cand[kGroup] = {u, digit_swap(u), unit_comp(g, u), unit_comp(g, digit_swap(u))};
+  int n = 0;
+#pragma unroll
+  for (int k = 0; k < kGroup; ++k) {
+    bool dup = false;
+#pragma unroll
+    for (int j = 0; j < k; ++j) dup = dup || (cand[j] == cand[k]);
+    if (!dup) U[n++] = cand[k];
+  }
+  return n;
+}
+__device__ __forceinline__ int slot_of(const uint64_t (&U)[kGroup], int n, uint64_t v) {
+  int k = 0;
+#pragma unroll
+  for (int j = 0; j < kGroup; ++j)
+    if (j < n && U[j] == v) k = j;
+  return k;
+}
+
+// next item >= c (step G): a unit that is the smallest of its group
 __device__ __forceinline__ uint64_t q4_next(const Q4Geo& g, uint64_t c, uint64_t G) {
   while (c < g.nunits) {
-    if (digit_swap(c) >= c) return c;
+    if (group_min(g, c) == c) return c;
     c += G;
   }
   return c;
@@ -107,23 +153,29 @@ template <typename T, int M, int S, bool WMODE>
 __device__ __forceinline__ void q4_issue(const Q4Geo& g, uint64_t u, T* buf, uint64_t* bar,
                                          const T* g1, const double* pin) {
   using C = Q4Cfg<T, M, S, WMODE>;
-  mbar_expect_tx(bar, C::STAGE * (uint32_t)sizeof(T));
-#pragma unroll
-  for (int side = 0; side < 2; ++side) {
-    const uint64_t uu = side ? digit_swap(u) : u;
-    const uint64_t t0 = uu << (4 * M);
-    T* ub = buf + side * C::UNIT;
-    tma_load_1d(ub, pin + t0, C::TT * sizeof(double), bar);
+  uint64_t U[kGroup];
+  const int n = group_units(g, u, U);
+  uint32_t bytes = 0;
+  for (int k = 0; k < n; ++k) {
+    bytes += C::WIN * (uint32_t)sizeof(T);
+    if (unit_low(g, U[k])) bytes += C::TT * (uint32_t)sizeof(double);
+    if (WMODE) bytes += C::UOUT * (uint32_t)sizeof(T);
+  }
+  mbar_expect_tx(bar, bytes);
+  for (int k = 0; k < n; ++k) {
+    const uint64_t t0 = U[k] << (4 * M);
+    T* ub = buf + (size_t)k * C::UNIT;
     const uint64_t low = (t0 & kA4) | ((t0 & kB4) << 4);
 #pragma unroll
-    for (int h = 0; h < 4; ++h) {
+    for (int h = 0; h < 2; ++h) {
       const uint64_t yb = ((uint64_t)h << (g.tail_bits + 2)) | low;
-      tma_load_1d(ub + C::PR + h * C::WB, g1 + yb, C::WB * sizeof(T), bar);
+      tma_load_1d(ub + h * C::WB, g1 + yb, C::WB * sizeof(T), bar);
     }
-    if (WMODE) {  // u (= g1, the newest table) at the 16 output runs of this side
-      T* uo = buf + 2 * C::UNIT + side * 16 * C::TT;
+    if (unit_low(g, U[k])) tma_load_1d(ub + C::WIN, pin + t0, C::TT * sizeof(double), bar);
+    if (WMODE) {  // u (= g1, the newest table) at the unit's 8 stored output runs
+      T* uo = ub + C::WIN + C::PR;
 #pragma unroll
-      for (int hh = 0; hh < 16; ++hh) {
+      for (int hh = 0; hh < 8; ++hh) {
         const uint64_t hx = ((uint64_t)(hh >> 2) << (g.tail_bits + 2)) |
                             ((uint64_t)(hh & 3) << g.tail_bits);
         tma_load_1d(uo + hh * C::TT, g1 + (hx | t0), C::TT * sizeof(T), bar);
@@ -144,7 +196,8 @@ __global__ void __launch_bounds__(kThreads) q4_kernel(Q4Args a) {
   Q4Geo g;
   g.ell = a.ell;
   g.tail_bits = 4u * (uint32_t)(a.ell - 1);
-  g.nunits = 1ull << (g.tail_bits - 4 * M);
+  g.ubits = g.tail_bits - 4 * M;
+  g.nunits = 1ull << g.ubits;
   const T* g1 = reinterpret_cast<const T*>(a.g1);
   const double* pin = a.pin;
   double* pout = a.pout;
@@ -167,73 +220,75 @@ __global__ void __launch_bounds__(kThreads) q4_kernel(Q4Args a) {
   }
   __syncthreads();
   if (tid == 0) {
-    pc = q4_next<M>(g, blockIdx.x, G);
+    pc = q4_next(g, blockIdx.x, G);
     for (int s = 0; s < S && pc < g.nunits; ++s) {
       q4_issue<T, M, S, WMODE>(g, pc, in + (size_t)s * C::STAGE, &bars[s], g1, pin);
-      pc = q4_next<M>(g, pc + G, G);
+      pc = q4_next(g, pc + G, G);
     }
   }
 
   uint32_t it = 0;
-  for (uint64_t cu = q4_next<M>(g, blockIdx.x, G); cu < g.nunits; cu = q4_next<M>(g, cu + G, G), ++it) {
+  for (uint64_t cu = q4_next(g, blockIdx.x, G); cu < g.nunits; cu = q4_next(g, cu + G, G), ++it) {
     const uint32_t s = it % S;
     T* buf = in + (size_t)s * C::STAGE;
     mbar_wait(&bars[s], (it / S) & 1u);
     __syncthreads();
-    const uint64_t su = digit_swap(cu);
-    const bool self = (su == cu);
-    const uint64_t t0U = cu << (4 * M), t0S = su << (4 * M);
-    const T* PU = buf;
-    const T* WU = buf + C::PR;
-    const T* PS = buf + C::UNIT;
-    const T* WS = buf + C::UNIT + C::PR;
+    uint64_t U[kGroup];
+    const int n = group_units(g, cu, U);
 
-    for (uint32_t i = tid; i < TT; i += kThreads) {
-      const uint32_t i2 = (uint32_t)digit_swap(i);       // the swapped tails' offset
+    for (uint32_t j = tid; j < (uint32_t)n * TT; j += kThreads) {
+      const int k = (int)(j / TT);
+      const uint32_t i = j % TT;
+      const uint64_t X = U[k];
+      const uint64_t sX = digit_swap(X);
+      const uint64_t cX = unit_comp(g, X), csX = unit_comp(g, sX);
+      const T* ubX = buf + (size_t)k * C::UNIT;
+      const T* ubS = buf + (size_t)slot_of(U, n, sX) * C::UNIT;
+      const T* ubCS = buf + (size_t)slot_of(U, n, csX) * C::UNIT;
+      // P: the mean of the g2 row of these tails (|N| = 2, shift (d-2) R = 0); stored for units
+      // whose first tail character is < 2, else the complement unit's, reversed
+      double pu;
+      if (unit_low(g, X)) {
+        pu = reinterpret_cast<const double*>(ubX + C::WIN)[i];
+      } else {
+        const T* ubC = buf + (size_t)slot_of(U, n, cX) * C::UNIT;
+        pu = reinterpret_cast<const double*>(ubC + C::WIN)[TT - 1 - i];
+      }
+      const uint32_t i2 = (uint32_t)digit_swap(i);  // this tail's offset in the swapped unit
       const uint32_t offU = (uint32_t)((i & kA4) | ((i & kB4) << 4));
       const uint32_t offS = (uint32_t)((i2 & kA4) | ((i2 & kB4) << 4));
-      // P: mean of the 16-entry row of the table two sweeps back, |N| = 2 (shift (d-2) R = 0);
-      // pooled when that table was written
-      const double pu = reinterpret_cast<const double*>(PU)[i];
-      const double ps = reinterpret_cast<const double*>(PS)[i2];
+      const uint32_t i3 = TT - 1 - i2;  // in the complemented swapped unit
+      const uint32_t offCS = (uint32_t)((i3 & kA4) | ((i3 & kB4) << 4));
 #pragma unroll
       for (int m = 0; m < (WMODE ? 2 : 1); ++m) {
         const double sh = WMODE ? R[m] : 0.0;  // |N| = 1: shift (d-1) R = R
-        double bU[4], bS[4];
+        double bU[2], bS[4];
 #pragma unroll
-        for (int h = 0; h < 4; ++h) {
-          bU[h] = 0.25 * sum4(WU + h * C::WB + offU, sh);
-          bS[h] = 0.25 * sum4(WS + h * C::WB + offS, sh);
-        }
+        for (int h = 0; h < 2; ++h) bU[h] = 0.25 * sum4<T, false>(ubX + h * C::WB + offU, sh);
+        // adv_a(h_a, h_b, t) = adv_b(h_b, h_a, swap t): stored for h_b < 2; for h_b >= 2 the
+        // folded window of head 3 - h_b of the complemented swapped tails, read reversed
+        bS[0] = 0.25 * sum4<T, false>(ubS + 0 * C::WB + offS, sh);
+        bS[1] = 0.25 * sum4<T, false>(ubS + 1 * C::WB + offS, sh);
+        bS[2] = 0.25 * sum4<T, true>(ubCS + 1 * C::WB + offCS, sh);
+        bS[3] = 0.25 * sum4<T, true>(ubCS + 0 * C::WB + offCS, sh);
 #pragma unroll
-        for (int ha = 0; ha < 4; ++ha) {
+        for (int ha = 0; ha < 2; ++ha) {
 #pragma unroll
           for (int hb = 0; hb < 4; ++hb) {
-            double vu, vs;
-            if (ha == hb) {
-              vu = 1.0 + fmax(0.0, pu);
-              vs = 1.0 + fmax(0.0, ps);
-            } else {
-              vu = fmax(fmax(bU[ha], bS[hb]), pu);  // adv_b, adv_a (= adv_b of the swap), P
-              vs = fmax(fmax(bS[ha], bU[hb]), ps);
-            }
-            const uint64_t hx = ((uint64_t)ha << hbit_a) | ((uint64_t)hb << hbit_b);
-            const uint64_t xu = hx | (t0U + i), xs = hx | (t0S + i2);
+            double v;
+            if (ha == hb)
+              v = 1.0 + fmax(0.0, pu);
+            else
+              v = fmax(fmax(bU[ha], bS[hb]), pu);  // adv_b, adv_a, P
+            const int hh = ha * 4 + hb;
             if (!WMODE) {
-              dst[xu] = (T)vu;
-              if (!self) dst[xs] = (T)vs;
+              const uint64_t hx = ((uint64_t)ha << hbit_a) | ((uint64_t)hb << hbit_b);
+              dst[hx | ((X << (4 * M)) + i)] = (T)v;
               constexpr uint32_t NR1 = C::NR + 1;
-              outs[((ha * 4 + hb) * 16 + (i & 15)) * NR1 + (i >> 4)] = (T)vu;
-              outs[((16 + ha * 4 + hb) * 16 + (i2 & 15)) * NR1 + (i2 >> 4)] = (T)vs;
+              outs[(((uint32_t)k * 8 + hh) * 16 + (i & 15)) * NR1 + (i >> 4)] = (T)v;
             } else {
-              const double twoR = 2.0 * R[m];
-              const T* uo = buf + 2 * C::UNIT;
-              const double uu = (double)uo[(ha * 4 + hb) * TT + i];
-              const double usv = (double)uo[16 * TT + (ha * 4 + hb) * TT + i2];
-              wmax[m] = fmax(wmax[m], (uu + twoR) - vu);
-              if (!self) wmax[m] = fmax(wmax[m], (usv + twoR) - vs);
-              (void)xu;
-              (void)xs;
+              const T* uo = ubX + C::WIN + C::PR;
+              wmax[m] = fmax(wmax[m], ((double)uo[hh * TT + i] + 2.0 * R[m]) - v);
             }
           }
         }
@@ -241,25 +296,25 @@ __global__ void __launch_bounds__(kThreads) q4_kernel(Q4Args a) {
     }
     __syncthreads();
     if (!WMODE) {
-      // row means of the new table: output rows (h_a, h_b, t >> 4) of both sides, each summed
-      // in Alg. 1's order over its 16 stored values (read all 16, then add in order)
-      constexpr uint32_t RPS = 16 * C::NR, NR1 = C::NR + 1;  // rows per side
-      for (uint32_t j = tid; j < (self ? 1u : 2u) * RPS; j += kThreads) {
-        const uint32_t side = j / RPS, jr = j % RPS;
+      // row means of the new table: output rows (h_a < 2, h_b, t >> 4) of the group's units, each
+      // summed in Alg. 1's order over its 16 stored values
+      constexpr uint32_t NR1 = C::NR + 1;
+      const uint32_t rows = (uint32_t)n * 8 * C::NR;
+      for (uint32_t j = tid; j < rows; j += kThreads) {
+        const uint32_t k = j / (8 * C::NR), jr = j % (8 * C::NR);
         const uint32_t hh = jr / C::NR, r = jr % C::NR;
-        const T* row = outs + (side * 16 + hh) * 16 * NR1 + r;
+        const T* row = outs + ((k * 8 + hh) * 16) * NR1 + r;
         double sum = 0.0;
 #pragma unroll
-        for (int k = 0; k < 16; ++k) sum = sum + ((double)row[k * NR1] + 0.0);
+        for (int c = 0; c < 16; ++c) sum = sum + ((double)row[c * NR1] + 0.0);
         const uint64_t hx = ((uint64_t)(hh >> 2) << hbit_a) | ((uint64_t)(hh & 3) << hbit_b);
-        const uint64_t t0 = side ? t0S : t0U;
-        pout[(hx | t0) >> 4 | r] = 0.0625 * sum;
+        pout[((hx | (U[k] << (4 * M))) >> 4) | r] = 0.0625 * sum;
       }
       __syncthreads();  // outs is reused by the next item
     }
     if (tid == 0 && pc < g.nunits) {
       q4_issue<T, M, S, WMODE>(g, pc, buf, &bars[s], g1, pin);
-      pc = q4_next<M>(g, pc + G, G);
+      pc = q4_next(g, pc + G, G);
     }
   }
   if (WMODE) block_max2_to(wmax[0], wmax[1], a.red_out);
@@ -290,7 +345,9 @@ cudaError_t launch_q4_t(const Q4Args& a, cudaStream_t s, int sms) {
 
 }  // namespace
 
-int q4_min_ell() { return 3; }  // the unit (16^2 tails) must fit in the 4^(2(l-1)) tail pairs
+// the unit (16^2 tails) must leave at least one tail group above it (the folded row means are
+// indexed by the first tail character)
+int q4_min_ell() { return 4; }
 
 cudaError_t launch_q4_sweep(const Q4Args& a, int dtype, cudaStream_t s, int sms) {
   static int variant = -1;  // LCSB_Q4_STAGES (A/B only): pipeline stages per CTA
@@ -300,7 +357,6 @@ cudaError_t launch_q4_sweep(const Q4Args& a, int dtype, cudaStream_t s, int sms)
   }
   if (dtype == LCSB_F32) {
     if (variant == 2) return launch_q4_t<float, 2, 2, false>(a, s, sms);
-    if (variant == 3) return launch_q4_t<float, 2, 3, false>(a, s, sms);
     return launch_q4_t<float, 2, 1, false>(a, s, sms);
   }
   return launch_q4_t<double, 2, 1, false>(a, s, sms);

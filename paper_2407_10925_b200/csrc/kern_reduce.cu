@@ -89,12 +89,12 @@ struct ExpandTabs {
 };
 
 template <typename T>
-__global__ void expand_kernel(ExpandTabs tabs, int p, int symmetric, int ell,
+__global__ void expand_kernel(ExpandTabs tabs, int p, int symmetric, uint64_t nlogical, int ell,
                               const uint32_t* __restrict__ qmap, int K, uint64_t first,
                               uint64_t count, const uint64_t* __restrict__ idx, double* out) {
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-  const uint64_t half = symmetric ? (1ull << (2 * ell - 1)) : 0;
-  const uint64_t top = symmetric ? ((1ull << (2 * ell)) - 1) : 0;
+  const uint64_t half = symmetric ? nlogical / 2 : 0;
+  const uint64_t top = symmetric ? nlogical - 1 : 0;
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count; i += stride) {
     uint64_t y = idx ? idx[i] : first + i;
     if (symmetric && y >= half) y = top - y;  // Eq. (comp_eq)
@@ -131,7 +131,8 @@ cudaError_t launch_rdiff(const void* newest, const void* prev, uint64_t n, int d
   return cudaGetLastError();
 }
 
-cudaError_t launch_expand(const void* const* tabs, int p, int dtype, int symmetric, int ell,
+cudaError_t launch_expand(const void* const* tabs, int p, int dtype, int symmetric,
+                          uint64_t nlogical, int ell,
                           const uint32_t* qmap, int K, uint64_t first, uint64_t count,
                           const uint64_t* idx, double* out, cudaStream_t s) {
   uint64_t blocks = (count + 255) / 256;
@@ -140,9 +141,9 @@ cudaError_t launch_expand(const void* const* tabs, int p, int dtype, int symmetr
   ExpandTabs t;
   for (int k = 0; k < kMaxShards; ++k) t.t[k] = (k < (1 << p)) ? tabs[k] : nullptr;
   if (dtype == LCSB_F32)
-    expand_kernel<float><<<(unsigned)blocks, 256, 0, s>>>(t, p, symmetric, ell, qmap, K, first, count, idx, out);
+    expand_kernel<float><<<(unsigned)blocks, 256, 0, s>>>(t, p, symmetric, nlogical, ell, qmap, K, first, count, idx, out);
   else
-    expand_kernel<double><<<(unsigned)blocks, 256, 0, s>>>(t, p, symmetric, ell, qmap, K, first, count, idx, out);
+    expand_kernel<double><<<(unsigned)blocks, 256, 0, s>>>(t, p, symmetric, nlogical, ell, qmap, K, first, count, idx, out);
   return cudaGetLastError();
 }
 

@@ -418,7 +418,7 @@ static int plan_config(const lcsb_config* c, Plan* p, char* why, size_t whylen) 
   p->qK = (sym == 2) ? qK : 0;
   p->qM = (sym == 2) ? qM : 0;
   p->kernel = sym == 2 ? 5 : (sym ? 2 : 1);
-  if (!sym && c->sigma == 4 && c->d == 2 && form == LCSB_FORM_KS && c->ell >= 3 &&
+  if (!sym && c->sigma == 4 && c->d == 2 && form == LCSB_FORM_KS && c->ell >= q4_min_ell() &&
       c->kernel == LCSB_KERNEL_AUTO)
     p->kernel = 3;  // sigma = 4, d = 2 swap-paired TMA kernel (kern_q4.cu)
   else if (p->kernel == 1 && c->kernel == LCSB_KERNEL_AUTO && small_supported(c->sigma, c->d, n))
@@ -433,7 +433,9 @@ static int plan_config(const lcsb_config* c, Plan* p, char* why, size_t whylen) 
   p->mode = c->virtual_shards ? (P == 1 ? MODE_SINGLE : MODE_VIRTUAL)
                               : ((P > 1 || c->nccl_id) ? MODE_PROCESS : MODE_SINGLE);
   p->n_logical = n;
-  p->n_stored = (sym == 2) ? quarter_slots(c->ell, qK) << (2 * qK) : (sym ? n / 2 : n);
+  // q4: complement-folded table (heads h_a < 2 stored, kern_q4.cu)
+  p->n_stored = (sym == 2) ? quarter_slots(c->ell, qK) << (2 * qK)
+                           : ((sym || p->kernel == 3) ? n / 2 : n);
   p->n_local = p->n_stored / (uint64_t)P;
   p->esize = (c->dtype == LCSB_F32) ? 4 : 8;
   const uint64_t owned = (p->mode == MODE_PROCESS) ? 1 : (uint64_t)P;
@@ -444,7 +446,7 @@ static int plan_config(const lcsb_config* c, Plan* p, char* why, size_t whylen) 
     return LCSB_EINVAL;
   }
   p->bytes += 256;
-  if (p->kernel == 3) p->bytes += 3 * (n / 16) * sizeof(double);
+  if (p->kernel == 3) p->bytes += 3 * (n / 32) * sizeof(double);
   if (p->kernel == 4 && form == LCSB_FORM_KS && small_pooled_supported(c->sigma, c->d)) {
     uint64_t sigd = 1;
     for (int j = 0; j < c->d; ++j) sigd *= (uint64_t)c->sigma;
@@ -708,7 +710,7 @@ extern "C" int lcsb_create_ex(const lcsb_config* cfg, lcsb_t** out) {
     return set_err(nullptr, LCSB_ECAPACITY, "scratch allocation failed");
   }
   if (h->kernel == 3) {  // row-mean ring of the pooled-history KS sweep, zero (W_0 = 0)
-    h->pool_bytes = (size_t)(h->n_logical / 16) * sizeof(double);
+    h->pool_bytes = (size_t)(h->n_logical / 32) * sizeof(double);  // rows of stored states
     for (int i = 0; i < 3; ++i) {
       h->pools[i] = (double*)dev_alloc(h, h->pool_bytes);
       if (!h->pools[i] || cudaMemsetAsync(h->pools[i], 0, h->pool_bytes, s) != cudaSuccess) {
@@ -1135,7 +1137,8 @@ static int readout(lcsb_t* h, int which, uint64_t first, uint64_t count, const u
     if (host_idx)
       e = cudaMemcpyAsync(ibuf, host_idx + off, c * sizeof(uint64_t), cudaMemcpyHostToDevice, s);
     if (e == cudaSuccess)
-      e = launch_expand(tabs, h->p, h->cfg.dtype, h->symmetric != 0, h->cfg.ell, h->qmap, h->qK,
+      e = launch_expand(tabs, h->p, h->cfg.dtype, h->symmetric != 0 || h->kernel == 3,
+                        h->n_logical, h->cfg.ell, h->qmap, h->qK,
                         first + off, c, host_idx ? ibuf : nullptr, dbuf, s);
     if (e == cudaSuccess) {
       h->launches += 1;

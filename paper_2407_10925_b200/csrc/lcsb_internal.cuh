@@ -238,7 +238,10 @@ cudaError_t launch_rdiff(const void* newest, const void* prev, uint64_t n, int d
                          unsigned long long* red, cudaStream_t s, int sms);
 // tabs[k]: the table of shard k (unsharded: tabs[0]); p = log2(shards); qmap != NULL: quarter
 // table with blocks of 4^K
-cudaError_t launch_expand(const void* const* tabs, int p, int dtype, int symmetric, int ell,
+// symmetric: the table holds the logical states [0, nlogical/2); y >= nlogical/2 reads
+// nlogical-1-y (the complement: Eq. comp_eq for sigma = 2, d -> 3-d for sigma = 4)
+cudaError_t launch_expand(const void* const* tabs, int p, int dtype, int symmetric,
+                          uint64_t nlogical, int ell,
                           const uint32_t* qmap, int K, uint64_t first, uint64_t count,
                           const uint64_t* idx, double* out, cudaStream_t s);
 

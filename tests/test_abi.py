@@ -45,9 +45,9 @@ def test_required_bytes_and_validation():
         2 * (131328 + 65792) * (1 << 14) * 4 + 256 + (1 << 19) * 4
     # full table when symmetry is off
     assert L.lcsb_required_bytes(2, 2, 17, "f32", symmetry=0) == 2 * (1 << 34) * 4 + 256
-    # config 3: pooled-history KS (kern_q4.cu): 2 tables of 4^16 fp32 + 3 row-mean arrays of
-    # 4^16 / 16 fp64 (the generic kernel keeps the d+1 = 3 tables of Alg. 2)
-    assert L.lcsb_required_bytes(4, 2, 8, "f32") == 2 * (1 << 32) * 4 + 256 + 3 * (1 << 28) * 8
+    # config 3: complement-folded pooled-history KS (kern_q4.cu): 2 half tables of 4^16 / 2 fp32
+    # + 3 row-mean arrays of 4^16 / 32 fp64 (the generic kernel keeps the d+1 = 3 full tables)
+    assert L.lcsb_required_bytes(4, 2, 8, "f32") == 2 * (1 << 31) * 4 + 256 + 3 * (1 << 27) * 8
     assert L.lcsb_required_bytes(4, 2, 8, "f32", kernel="generic") == 3 * (1 << 32) * 4 + 256
     # config 2: 4 tables of 3^12 fp64 + the pooled means of every ring slot (kern_small.cu):
     # per row of 27, 9 means for |N| = 2 and 1 for |N| = 3

@@ -127,10 +127,10 @@ def test_generic_ks_matches_oracle(sigma, d, ell, dtype, sweeps):
     h.destroy()
 
 
-@pytest.mark.parametrize("ell,dtype", [(3, "f32"), (3, "f64"), (4, "f32"), (4, "f64")])
+@pytest.mark.parametrize("ell,dtype", [(4, "f32"), (4, "f64"), (5, "f32")])
 def test_q4_kernel_matches_oracle(ell, dtype):
-    """sigma = 4, d = 2, KS form: the swap-paired TMA kernel against the oracle, every table of
-    the ring after several sweeps, and the bound (both R readings)."""
+    """sigma = 4, d = 2, KS form: the complement-folded, swap/complement-grouped TMA kernel against
+    the oracle, every table of the ring after several sweeps, and the bound (both R readings)."""
     Lcsb = _lcsb()
     h = Lcsb(4, 2, ell, dtype=dtype, form="ks")
     assert h.kernel_in_use == "q4"
