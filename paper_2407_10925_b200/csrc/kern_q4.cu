@@ -59,22 +59,19 @@ struct V4T<double> {
 };
 
 // r <- r + (v + shift), c = 0..3 in order (Alg. 1 line 8); REV: the window is folded, logical
-// c is stored entry 3-c
-template <typename T, bool REV>
+// c is stored entry 3-c.  SHIFT = false (sweeps, shift 0): v + 0.0 == v exactly for the
+// non-negative iterate values (never -0.0), so the add is dropped.
+template <typename T, bool REV, bool SHIFT>
 __device__ __forceinline__ double sum4(const T* p, double sh) {
   const typename V4T<T>::type v = *reinterpret_cast<const typename V4T<T>::type*>(p);
+  const double x = v.x, y = v.y, z = v.z, w = v.w;
+  const double a0 = REV ? w : x, a1 = REV ? z : y, a2 = REV ? y : z, a3 = REV ? x : w;
+  if (!SHIFT) return ((a0 + a1) + a2) + a3;
   double r = 0.0;
-  if (!REV) {
-    r = r + ((double)v.x + sh);
-    r = r + ((double)v.y + sh);
-    r = r + ((double)v.z + sh);
-    r = r + ((double)v.w + sh);
-  } else {
-    r = r + ((double)v.w + sh);
-    r = r + ((double)v.z + sh);
-    r = r + ((double)v.y + sh);
-    r = r + ((double)v.x + sh);
-  }
+  r = r + (a0 + sh);
+  r = r + (a1 + sh);
+  r = r + (a2 + sh);
+  r = r + (a3 + sh);
   return r;
 }
 
@@ -264,13 +261,13 @@ __global__ void __launch_bounds__(kThreads) q4_kernel(Q4Args a) {
         const double sh = WMODE ? R[m] : 0.0;  // |N| = 1: shift (d-1) R = R
         double bU[2], bS[4];
 #pragma unroll
-        for (int h = 0; h < 2; ++h) bU[h] = 0.25 * sum4<T, false>(ubX + h * C::WB + offU, sh);
+        for (int h = 0; h < 2; ++h) bU[h] = 0.25 * sum4<T, false, WMODE>(ubX + h * C::WB + offU, sh);
         // adv_a(h_a, h_b, t) = adv_b(h_b, h_a, swap t): stored for h_b < 2; for h_b >= 2 the
         // folded window of head 3 - h_b of the complemented swapped tails, read reversed
-        bS[0] = 0.25 * sum4<T, false>(ubS + 0 * C::WB + offS, sh);
-        bS[1] = 0.25 * sum4<T, false>(ubS + 1 * C::WB + offS, sh);
-        bS[2] = 0.25 * sum4<T, true>(ubCS + 1 * C::WB + offCS, sh);
-        bS[3] = 0.25 * sum4<T, true>(ubCS + 0 * C::WB + offCS, sh);
+        bS[0] = 0.25 * sum4<T, false, WMODE>(ubS + 0 * C::WB + offS, sh);
+        bS[1] = 0.25 * sum4<T, false, WMODE>(ubS + 1 * C::WB + offS, sh);
+        bS[2] = 0.25 * sum4<T, true, WMODE>(ubCS + 1 * C::WB + offCS, sh);
+        bS[3] = 0.25 * sum4<T, true, WMODE>(ubCS + 0 * C::WB + offCS, sh);
 #pragma unroll
         for (int ha = 0; ha < 2; ++ha) {
 #pragma unroll
@@ -306,7 +303,7 @@ __global__ void __launch_bounds__(kThreads) q4_kernel(Q4Args a) {
         const T* row = outs + ((k * 8 + hh) * 16) * NR1 + r;
         double sum = 0.0;
 #pragma unroll
-        for (int c = 0; c < 16; ++c) sum = sum + ((double)row[c * NR1] + 0.0);
+        for (int c = 0; c < 16; ++c) sum = sum + (double)row[c * NR1];  // (+ 0.0: exact no-op)
         const uint64_t hx = ((uint64_t)(hh >> 2) << hbit_a) | ((uint64_t)(hh & 3) << hbit_b);
         pout[((hx | (U[k] << (4 * M))) >> 4) | r] = 0.0625 * sum;
       }
