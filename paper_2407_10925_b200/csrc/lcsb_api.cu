@@ -280,7 +280,7 @@ static bool quarter_schedule(int ell, int K, int M, const uint32_t* map,
   };
   // v2 (default): walking the BFS order, a B-block emits the groups of all its A-neighbours
   // together, so its own windows (read by those groups) are consumed close in time as well
-  static const int version = getenv("LCSB_QSCHED") ? atoi(getenv("LCSB_QSCHED")) : 2;
+  static const int version = getenv("LCSB_QSCHED") ? atoi(getenv("LCSB_QSCHED")) : 4;
   for (uint32_t v : order) {
     if (col[v] == 0) {
       if (!grouped[v]) emit_group(v);
@@ -294,6 +294,104 @@ static bool quarter_schedule(int ell, int K, int M, const uint32_t* map,
   for (size_t e = 0; e < E; ++e)
     if (!done[e]) out.push_back(etau[e]);
   if (out.size() != E) return false;
+  if (version >= 4) {
+    // v4 (default): re-cut the v2 order into waves of `kWave` items (about one wave of the
+    // persistent grid: its items run concurrently, so a stored quarter-block loaded in a wave is
+    // in L2 for the rest of it).  A wave grows greedily: always the item with the most of its
+    // (<= 4) quarter-block pieces already loaded by the wave; a new seed comes from the v2 order.
+    const int kWave = 444;
+    std::vector<uint32_t> idx_of_tau(ntiles, 0);
+    for (size_t e = 0; e < E; ++e) idx_of_tau[etau[e]] = (uint32_t)e;
+    const uint64_t kmask = (1ull << (2 * K)) - 1;
+    auto window_pieces = [&](uint64_t w, uint32_t* pc) {  // the 2 stored quarter-blocks of w
+      const uint32_t m = map[w >> (2 * K)];
+      const uint64_t slot = m >> 2, e = w & kmask;
+      uint64_t o0, o1;
+      if ((m & 3u) == 0) {
+        o0 = e;
+        o1 = e + T;
+      } else if ((m & 3u) == 3u) {
+        o0 = (~e & kmask) & ~(2 * T - 1);
+        o1 = o0 + T;
+      } else {
+        const uint64_t f = ((m & 3u) == 1u) ? (pairswap_hd(e) & kmask) : (pairswap_hd(~e & kmask) & kmask);
+        o0 = (f & ~(4 * T - 1)) | (f & T);
+        o1 = o0 + 2 * T;
+      }
+      pc[0] = (uint32_t)((slot << 2) | ((o0 / T) & 3));
+      pc[1] = (uint32_t)((slot << 2) | ((o1 / T) & 3));
+    };
+    std::vector<uint32_t> pcs(4 * E);
+    std::vector<uint8_t> npc(E);
+    const uint64_t npieces = nslots * 4;
+    std::vector<uint32_t> poff(npieces + 1, 0);
+    for (size_t e = 0; e < E; ++e) {
+      const uint64_t x0 = q1 + (uint64_t)etau[e] * T;
+      const uint64_t p0 = pairswap_hd(~x0 & lmask) & ~(T - 1);
+      uint32_t q[4];
+      window_pieces(win(x0), q);
+      window_pieces(win(p0), q + 2);
+      int n = 0;
+      for (int k = 0; k < 4; ++k) {
+        bool dup = false;
+        for (int j = 0; j < n; ++j) dup = dup || pcs[4 * e + j] == q[k];
+        if (!dup) pcs[4 * e + n++] = q[k];
+      }
+      npc[e] = (uint8_t)n;
+      for (int k = 0; k < n; ++k) poff[pcs[4 * e + k] + 1]++;
+    }
+    for (uint64_t q = 0; q < npieces; ++q) poff[q + 1] += poff[q];
+    std::vector<uint32_t> pinv(poff[npieces]), pfill(poff.begin(), poff.end() - 1);
+    for (size_t e = 0; e < E; ++e)
+      for (int k = 0; k < npc[e]; ++k) pinv[pfill[pcs[4 * e + k]]++] = (uint32_t)e;
+    std::vector<uint32_t> v2(out);  // seeds, in v2 order
+    std::vector<uint8_t> taken(E, 0), score(E, 0);
+    std::vector<uint32_t> pwave(npieces, ~0u), touched;
+    std::vector<uint32_t> bucket[5];
+    out.clear();
+    size_t seed = 0;
+    for (uint32_t wave = 0; out.size() < E; ++wave) {
+      int cnt = 0;
+      for (auto& b : bucket) b.clear();
+      for (uint32_t j : touched) score[j] = 0;
+      touched.clear();
+      auto add = [&](uint32_t i) {
+        taken[i] = 1;
+        out.push_back(etau[i]);
+        ++cnt;
+        for (int k = 0; k < npc[i]; ++k) {
+          const uint32_t q = pcs[4 * i + k];
+          if (pwave[q] == wave) continue;
+          pwave[q] = wave;
+          for (uint32_t t = poff[q]; t < poff[q + 1]; ++t) {
+            const uint32_t j = pinv[t];
+            if (taken[j]) continue;
+            if (!score[j]) touched.push_back(j);
+            bucket[++score[j]].push_back(j);
+          }
+        }
+      };
+      while (cnt < kWave && out.size() < E) {
+        int pick = -1;
+        for (int sc = 4; sc >= 1 && pick < 0; --sc)
+          while (!bucket[sc].empty()) {
+            const uint32_t j = bucket[sc].back();
+            bucket[sc].pop_back();
+            if (!taken[j] && score[j] == sc) {
+              pick = (int)j;
+              break;
+            }
+          }
+        if (pick < 0) {
+          while (seed < E && taken[idx_of_tau[v2[seed]]]) ++seed;
+          if (seed >= E) break;
+          pick = (int)idx_of_tau[v2[seed]];
+        }
+        add((uint32_t)pick);
+      }
+    }
+    if (out.size() != E) return false;
+  }
   cache = out;
   c_ell = ell;
   c_K = K;
