@@ -442,7 +442,14 @@ __global__ void __launch_bounds__(kThreads, MINB) bin2q_kernel(Bin2QArgs a) {
   // without one, the pair representatives in tile order
   const uint32_t* sched = (a.sched && a.sched_m == M) ? a.sched : nullptr;
   const uint64_t nitems = sched ? a.nitems : g.ntiles;
+  // item claims (thread 0): dynamic -- the next index of the shared counter; static -- this
+  // CTA's next representative in round-robin order
+  unsigned long long* counter = sched ? a.counter : nullptr;
   auto first = [&](uint64_t c) { return sched ? c : qnext(g, c, G, LOG); };
+  auto claim = [&](uint64_t prev) -> uint64_t {
+    if (counter) return (uint64_t)atomicAdd(counter, 1ull);
+    return first(prev == ~0ull ? (uint64_t)blockIdx.x : prev + G);
+  };
   auto tile_of = [&](uint64_t c) -> uint64_t { return sched ? (uint64_t)__ldg(sched + c) : c; };
   uint64_t pc = 0;  // producer cursor (thread 0 only)
   QItem pit;        // its map entries, fetched one item ahead
@@ -451,29 +458,35 @@ __global__ void __launch_bounds__(kThreads, MINB) bin2q_kernel(Bin2QArgs a) {
     fence_mbar_init();
   }
   __syncthreads();
-  if (tid == 0) {
-    pc = first(blockIdx.x);
-    uint64_t ptau = pc < nitems ? tile_of(pc) : 0;
-    if (pc < nitems) qlookup<M>(g, map, ptau, pit);
-    for (int s = 0; s < S && pc < nitems; ++s) {
-      qissue<T, M, C::UTMA>(g, pit, ptau, in + (size_t)s * C::STAGE, &bars[s], metas + 8 * s,
-                            src);
-      pc = first(pc + G);
-      if (pc < nitems) {
-        ptau = tile_of(pc);
-        qlookup<M>(g, map, ptau, pit);
-      }
+  // a stage either receives an item (meta[7] = 0, TMA completes its phase) or the end marker
+  // (meta[7] = 1, a plain arrive completes it); the claims are monotone, so after the first end
+  // marker every later stage is an end marker too
+  auto fill = [&](int s, T* sbuf) {
+    uint64_t* meta = metas + 8 * s;
+    if (pc < nitems) {
+      meta[7] = 0;
+      qissue<T, M, C::UTMA>(g, pit, tile_of(pc), sbuf, &bars[s], meta, src);
+      pc = claim(pc);
+      if (pc < nitems) qlookup<M>(g, map, tile_of(pc), pit);
+    } else {
+      meta[7] = 1;
+      mbar_arrive(&bars[s]);
     }
+  };
+  if (tid == 0) {
+    pc = claim(~0ull);
+    if (pc < nitems) qlookup<M>(g, map, tile_of(pc), pit);
+    for (int s = 0; s < S; ++s) fill(s, in + (size_t)s * C::STAGE);
   }
 
-  uint32_t i = 0;
-  for (uint64_t cc = first(blockIdx.x); cc < nitems; cc = first(cc + G), ++i) {
+  for (uint32_t i = 0;; ++i) {
     const uint32_t s = i % S;
     const uint32_t parity = (i / S) & 1u;
     T* buf = in + (size_t)s * C::STAGE;
     const uint64_t* meta = metas + 8 * s;
     mbar_wait(&bars[s], parity);
     __syncthreads();
+    if (meta[7]) break;  // end marker: no more items for this CTA
     const uint32_t modes = (uint32_t)meta[0];
     const uint32_t mw = modes & 3u, mp = (modes >> 2) & 3u;  // 3 only for Q0 (same-head) blocks
     const bool self = (modes & 16u) != 0;
@@ -502,11 +515,7 @@ __global__ void __launch_bounds__(kThreads, MINB) bin2q_kernel(Bin2QArgs a) {
     }
 #undef LCSB_Q1
     __syncthreads();  // stage s (data and metadata) is free again
-    if (tid == 0 && pc < nitems) {
-      qissue<T, M, C::UTMA>(g, pit, tile_of(pc), buf, &bars[s], metas + 8 * s, src);
-      pc = first(pc + G);
-      if (pc < nitems) qlookup<M>(g, map, tile_of(pc), pit);
-    }
+    if (tid == 0) fill((int)s, buf);
   }
   if (WMODE) block_max2_to(wm0, wm1, a.red_out);
 }

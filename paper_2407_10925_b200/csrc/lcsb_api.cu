@@ -36,6 +36,7 @@ struct lcsb {
   uint32_t* qsched;  // quarter table: item order of the sweep (NULL = natural order)
   size_t qsched_bytes;
   uint64_t qsched_n;
+  unsigned long long* qcounter;  // quarter table: work counter of the scheduled kernels
   int bin2_variant;  // 0 auto; see pick_bin2_variant
   int bin2q_variant; // 0 auto; LCSB_BIN2Q_VARIANT (A/B only)
   uint64_t n_logical;
@@ -299,7 +300,7 @@ static bool quarter_schedule(int ell, int K, int M, const uint32_t* map,
     // persistent grid: its items run concurrently, so a stored quarter-block loaded in a wave is
     // in L2 for the rest of it).  A wave grows greedily: always the item with the most of its
     // (<= 4) quarter-block pieces already loaded by the wave; a new seed comes from the v2 order.
-    const int kWave = 444;
+    static const int kWave = getenv("LCSB_QWAVE") ? atoi(getenv("LCSB_QWAVE")) : 444;
     std::vector<uint32_t> idx_of_tau(ntiles, 0);
     for (size_t e = 0; e < E; ++e) idx_of_tau[etau[e]] = (uint32_t)e;
     const uint64_t kmask = (1ull << (2 * K)) - 1;
@@ -668,6 +669,7 @@ extern "C" void lcsb_destroy(lcsb_t* h) {
   dev_free(h, h->red, 256);
   dev_free(h, h->qmap, h->qmap_bytes);
   dev_free(h, h->qsched, h->qsched_bytes);
+  dev_free(h, h->qcounter, 256);
   for (int i = 0; i < 3; ++i) dev_free(h, h->pools[i], h->pool_bytes);
   for (int k = 0; k <= kMaxD; ++k)
     for (int i = 0; i < kMaxGen; ++i) dev_free(h, h->spools[k][i], h->spool_bytes[k]);
@@ -849,6 +851,7 @@ extern "C" int lcsb_create_ex(const lcsb_config* cfg, lcsb_t** out) {
         h->qsched_n = sched.size();
         h->qsched_bytes = sched.size() * sizeof(uint32_t);
         h->qsched = (uint32_t*)dev_alloc(h, h->qsched_bytes);
+        if (h->qsched && !getenv("LCSB_QSTATIC")) h->qcounter = (unsigned long long*)dev_alloc(h, 256);
         if (h->qsched) {
           e = cudaMemcpyAsync(h->qsched, sched.data(), h->qsched_bytes, cudaMemcpyHostToDevice, s);
           if (e == cudaSuccess) e = cudaStreamSynchronize(s);
@@ -964,6 +967,7 @@ static void fill_bin2q(const lcsb_t* h, Bin2QArgs* a, int in_slot, int out_slot)
   a->sched = h->qsched;
   a->nitems = h->qsched_n;
   a->sched_m = h->qM;
+  a->counter = h->qcounter;
 }
 
 static int enqueue_sweeps(lcsb_t* h, int64_t n, cudaStream_t s);
@@ -1057,7 +1061,8 @@ static int enqueue_sweeps(lcsb_t* h, int64_t n, cudaStream_t s) {
     } else if (h->kernel == 5) {
       Bin2QArgs a;
       fill_bin2q(h, &a, h->cur, out);
-      e = launch_bin2q_sweep(a, h->cfg.dtype, h->qM, h->bin2q_variant, s, h->sms);
+      if (a.counter) e = cudaMemsetAsync(a.counter, 0, sizeof(unsigned long long), s);
+      if (e == cudaSuccess) e = launch_bin2q_sweep(a, h->cfg.dtype, h->qM, h->bin2q_variant, s, h->sms);
       h->launches += 1;
     } else if (h->kernel == 3) {
       Q4Args a;
@@ -1139,6 +1144,7 @@ extern "C" int lcsb_bound(lcsb_t* h, lcsb_bound_t* out) {
     fill_bin2q(h, &a, h->cur, -1);
     a.red_in = h->red;
     a.red_out = h->red + 2;
+    if (a.counter) CU(h, cudaMemsetAsync(a.counter, 0, sizeof(unsigned long long), s));
     CU(h, launch_bin2q_wpass(a, h->cfg.dtype, h->qM, s, h->sms));
     h->launches += 1;
   } else if (h->kernel == 3) {

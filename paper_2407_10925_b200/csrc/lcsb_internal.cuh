@@ -132,6 +132,10 @@ struct Bin2QArgs {
   const uint32_t* sched;
   uint64_t nitems;
   int sched_m;
+  // optional work counter (zeroed before the launch): CTAs claim items in schedule order with an
+  // atomic, so the items in flight stay within about one grid-width of the list; NULL = static
+  // round-robin assignment
+  unsigned long long* counter;
 };
 
 __host__ __device__ inline uint64_t pairswap_hd(uint64_t v) {

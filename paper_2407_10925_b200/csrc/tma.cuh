@@ -16,6 +16,9 @@ static __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t by
                "r"(bytes)
                : "memory");
 }
+static __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {  // arrive without transactions
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
 static __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   uint32_t done = 0;
   do {
