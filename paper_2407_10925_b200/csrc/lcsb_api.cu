@@ -851,7 +851,11 @@ extern "C" int lcsb_create_ex(const lcsb_config* cfg, lcsb_t** out) {
         h->qsched_n = sched.size();
         h->qsched_bytes = sched.size() * sizeof(uint32_t);
         h->qsched = (uint32_t*)dev_alloc(h, h->qsched_bytes);
-        if (h->qsched && !getenv("LCSB_QSTATIC")) h->qcounter = (unsigned long long*)dev_alloc(h, 256);
+        // dynamic claiming pays for the 4^6 tiles of fp32 (20.7 vs 26.6 GB read at l = 17); with
+        // the 4x more, smaller items of fp64 (4^5 tiles) the single counter costs more than it
+        // saves (l = 16: 3.99 vs 3.28 ms static)
+        if (h->qsched && h->qM >= 6 && !getenv("LCSB_QSTATIC"))
+          h->qcounter = (unsigned long long*)dev_alloc(h, 256);
         if (h->qsched) {
           e = cudaMemcpyAsync(h->qsched, sched.data(), h->qsched_bytes, cudaMemcpyHostToDevice, s);
           if (e == cudaSuccess) e = cudaStreamSynchronize(s);
