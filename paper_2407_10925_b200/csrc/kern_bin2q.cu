@@ -196,6 +196,67 @@ __device__ __forceinline__ void q0_group(const double (&G)[4], uint32_t r, uint3
   }
 }
 
+// fp32 storage, sweep: the Q1 values in fp32 (see the comment inside), the rest as pair_quads
+template <typename T, uint32_t TT, int MW, int MP>
+__device__ __forceinline__ void pair_quads_f32(const T* bw, const T* bp, const T* src, T* dst,
+                                               const uint64_t* meta, bool self) {
+  constexpr uint32_t SX = (MW == 0 || MW == 3) ? 2 : 0, SP = (MP == 0 || MP == 3) ? 2 : 1;
+  const uint64_t oQ1 = meta[1], oQ1p = meta[2];
+  const uint64_t of = meta[3], om = meta[4], opf = meta[5], opm = meta[6];
+  const bool rows_x = of != kNone || om != kNone;
+  const bool rows_p = !self && (opf != kNone || opm != kNone);
+  const double R0 = 0.0, R1 = 0.0;
+  double wm0 = 0.0, wm1 = 0.0;
+  // fp32 storage, sweep: the Q1 value round32(max(0.5 (x0 + x1), 0.5 (y0 + y1))) of fp64
+  // arithmetic equals the same expression evaluated in fp32 (a two-term fp32 sum is exact in
+  // fp64 or off by less than half an fp32 ulp, so no double rounding; halving and max commute
+  // with rounding), so Q1 stays in fp32; only the Q0 rows that are stored widen to fp64 (their
+  // four-term sums are not exact in fp32).
+  for (uint32_t qd = threadIdx.x; qd < TT / 4; qd += kThreads) {
+    const uint32_t o0 = 4 * qd;
+    const uint32_t g = 2 * pairswap32(o0), u = 2 * (TT - 4 - o0);
+    float X1[4], X2[4], A[4], B[4], P1[4], P2[4], Ap[4], Bp[4];
+    const bool sx = (qd >> SX) & 1u, sp = (qd >> SP) & 1u;
+    ld4r(reinterpret_cast<const float*>(bw) + gbase<TT, MW>(sx ? g + 4 : g), X1);
+    ld4r(reinterpret_cast<const float*>(bw) + gbase<TT, MW>(sx ? g : g + 4), X2);
+    ld4r(reinterpret_cast<const float*>(bp) + gbase<TT, MP>(sp ? u + 4 : u), P1);
+    ld4r(reinterpret_cast<const float*>(bp) + gbase<TT, MP>(sp ? u : u + 4), P2);
+    sel4f(sx, X1, X2, A, B);
+    sel4f(sp, P1, P2, Ap, Bp);
+    constexpr uint32_t c0 = comp<MW>(0), c1 = comp<MW>(1), c2 = comp<MW>(2), c3 = comp<MW>(3);
+    constexpr uint32_t d0 = comp<MP>(0), d1 = comp<MP>(1), d2 = comp<MP>(2), d3 = comp<MP>(3);
+    const float bx[4] = {0.5f * (A[c0] + A[c1]), 0.5f * (B[c0] + B[c1]),
+                         0.5f * (A[c2] + A[c3]), 0.5f * (B[c2] + B[c3])};
+    const float bq[4] = {0.5f * (Bp[d2] + Bp[d3]), 0.5f * (Bp[d0] + Bp[d1]),
+                         0.5f * (Ap[d2] + Ap[d3]), 0.5f * (Ap[d0] + Ap[d1])};
+    float v[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      v[k] = bx[k];
+      if (bq[k] > v[k]) v[k] = bq[k];
+    }
+    const uint32_t qb = pairswap32(~o0 & (TT - 1) & ~3u);
+    float* df = reinterpret_cast<float*>(dst);
+    if (oQ1 != kNone) *reinterpret_cast<float4*>(df + oQ1 + o0) = make_float4(v[0], v[1], v[2], v[3]);
+    if (oQ1p != kNone) *reinterpret_cast<float4*>(df + oQ1p + qb) = make_float4(v[3], v[1], v[2], v[0]);
+    double G[4];
+    if (rows_x) {
+      widen4(A, G);
+      q0_group<T, MW, false>(G, g >> 2, TT / 2, src, dst, of, om, nullptr, R0, R1, wm0, wm1);
+      widen4(B, G);
+      q0_group<T, MW, false>(G, (g >> 2) + 1, TT / 2, src, dst, of, om, nullptr, R0, R1, wm0,
+                             wm1);
+    }
+    if (rows_p) {
+      widen4(Ap, G);
+      q0_group<T, MP, false>(G, u >> 2, TT / 2, src, dst, opf, opm, nullptr, R0, R1, wm0, wm1);
+      widen4(Bp, G);
+      q0_group<T, MP, false>(G, (u >> 2) + 1, TT / 2, src, dst, opf, opm, nullptr, R0, R1, wm0,
+                             wm1);
+    }
+  }
+}
+
 template <typename T, uint32_t TT, int MW, int MP, bool WMODE>
 __device__ __forceinline__ void pair_quads(const T* bw, const T* bp, const T* src, T* dst,
                                            const uint64_t* meta, bool self, const T* us,
@@ -207,57 +268,6 @@ __device__ __forceinline__ void pair_quads(const T* bw, const T* bp, const T* sr
   const uint64_t of = meta[3], om = meta[4], opf = meta[5], opm = meta[6];
   const bool rows_x = of != kNone || om != kNone;
   const bool rows_p = !self && (opf != kNone || opm != kNone);
-  if constexpr (sizeof(T) == 4 && !WMODE) {
-    // fp32 storage, sweep: the Q1 value round32(max(0.5 (x0 + x1), 0.5 (y0 + y1))) of fp64
-    // arithmetic equals the same expression evaluated in fp32 (a two-term fp32 sum is exact in
-    // fp64 or off by less than half an fp32 ulp, so no double rounding; halving and max commute
-    // with rounding), so Q1 stays in fp32; only the Q0 rows that are stored widen to fp64 (their
-    // four-term sums are not exact in fp32).
-    for (uint32_t qd = threadIdx.x; qd < TT / 4; qd += kThreads) {
-      const uint32_t o0 = 4 * qd;
-      const uint32_t g = 2 * pairswap32(o0), u = 2 * (TT - 4 - o0);
-      float X1[4], X2[4], A[4], B[4], P1[4], P2[4], Ap[4], Bp[4];
-      const bool sx = (qd >> SX) & 1u, sp = (qd >> SP) & 1u;
-      ld4r(reinterpret_cast<const float*>(bw) + gbase<TT, MW>(sx ? g + 4 : g), X1);
-      ld4r(reinterpret_cast<const float*>(bw) + gbase<TT, MW>(sx ? g : g + 4), X2);
-      ld4r(reinterpret_cast<const float*>(bp) + gbase<TT, MP>(sp ? u + 4 : u), P1);
-      ld4r(reinterpret_cast<const float*>(bp) + gbase<TT, MP>(sp ? u : u + 4), P2);
-      sel4f(sx, X1, X2, A, B);
-      sel4f(sp, P1, P2, Ap, Bp);
-      constexpr uint32_t c0 = comp<MW>(0), c1 = comp<MW>(1), c2 = comp<MW>(2), c3 = comp<MW>(3);
-      constexpr uint32_t d0 = comp<MP>(0), d1 = comp<MP>(1), d2 = comp<MP>(2), d3 = comp<MP>(3);
-      const float bx[4] = {0.5f * (A[c0] + A[c1]), 0.5f * (B[c0] + B[c1]),
-                           0.5f * (A[c2] + A[c3]), 0.5f * (B[c2] + B[c3])};
-      const float bq[4] = {0.5f * (Bp[d2] + Bp[d3]), 0.5f * (Bp[d0] + Bp[d1]),
-                           0.5f * (Ap[d2] + Ap[d3]), 0.5f * (Ap[d0] + Ap[d1])};
-      float v[4];
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        v[k] = bx[k];
-        if (bq[k] > v[k]) v[k] = bq[k];
-      }
-      const uint32_t qb = pairswap32(~o0 & (TT - 1) & ~3u);
-      float* df = reinterpret_cast<float*>(dst);
-      if (oQ1 != kNone) *reinterpret_cast<float4*>(df + oQ1 + o0) = make_float4(v[0], v[1], v[2], v[3]);
-      if (oQ1p != kNone) *reinterpret_cast<float4*>(df + oQ1p + qb) = make_float4(v[3], v[1], v[2], v[0]);
-      double G[4];
-      if (rows_x) {
-        widen4(A, G);
-        q0_group<T, MW, false>(G, g >> 2, TT / 2, src, dst, of, om, nullptr, R0, R1, wm0, wm1);
-        widen4(B, G);
-        q0_group<T, MW, false>(G, (g >> 2) + 1, TT / 2, src, dst, of, om, nullptr, R0, R1, wm0,
-                               wm1);
-      }
-      if (rows_p) {
-        widen4(Ap, G);
-        q0_group<T, MP, false>(G, u >> 2, TT / 2, src, dst, opf, opm, nullptr, R0, R1, wm0, wm1);
-        widen4(Bp, G);
-        q0_group<T, MP, false>(G, (u >> 2) + 1, TT / 2, src, dst, opf, opm, nullptr, R0, R1, wm0,
-                               wm1);
-      }
-    }
-    return;
-  }
   for (uint32_t qd = threadIdx.x; qd < TT / 4; qd += kThreads) {
     const uint32_t o0 = 4 * qd;
     const uint32_t g = 2 * pairswap32(o0), u = 2 * (TT - 4 - o0);
@@ -493,8 +503,11 @@ __global__ void __launch_bounds__(kThreads, MINB) bin2q_kernel(Bin2QArgs a) {
     const T* bw = buf;
     const T* bp = buf + WIN;
     const T* us = C::UTMA ? buf + 2 * WIN : nullptr;
-#define LCSB_Q1(MW, MP) \
-  pair_quads<T, TT, MW, MP, WMODE>(bw, bp, src, dst, meta, self, us, R0, R1, wm0, wm1)
+#define LCSB_Q1(MW, MP)                                                            \
+  if constexpr (sizeof(T) == 4 && !WMODE)                                          \
+    pair_quads_f32<T, TT, MW, MP>(bw, bp, src, dst, meta, self);                   \
+  else                                                                             \
+    pair_quads<T, TT, MW, MP, WMODE>(bw, bp, src, dst, meta, self, us, R0, R1, wm0, wm1)
     switch (mw * 4 + mp) {
       case 0: LCSB_Q1(0, 0); break;
       case 1: LCSB_Q1(0, 1); break;
