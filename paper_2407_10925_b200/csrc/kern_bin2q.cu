@@ -18,18 +18,22 @@
 //    swap W(a,b) = W(b,a) is an exact invariant of every iterate (reading R19), the complement
 //    one is Eq. comp_eq, the tail complement of same-head states is v'[00t] = v'[00t~] (R18).
 //  * Reads: a tile's adv_b window (2T entries with free low 2M+1 bits) of a mode-0 block is one
-//    contiguous run; of a permuted block it is two runs of T (bit 2M+1 <-> bit 2M exchanged),
-//    loaded with two bulk copies into the same smem slots; the consumer indexes smem through
-//    the permutation.  Every half-table window is loaded once, so every stored block is read
-//    twice per sweep (once per logical image).
+//    contiguous run; of a pairswapped block two runs of T (bit 2M+1 <-> bit 2M exchanged),
+//    loaded with two bulk copies into the same smem slots; of a tail-complemented block one run
+//    read reversed.  The consumer indexes smem through the permutation.  Every half-table
+//    window is loaded once, so a stored block is requested once per logical image (twice for
+//    Q1 blocks, four times for Q0 blocks).
+//  * Item order: the host's L2 schedule (lcsb_api.cu quarter_schedule) lists the tile pairs in
+//    waves that share stored blocks, and thread 0 of each CTA claims items in that order from a
+//    global counter, so the items in flight stay within about one grid-width of the list and
+//    most repeated block loads hit L2.
 //  * Writes: of every output run (Q1 tile, Q0 row run, Q0 mirror run) only those lying in a
 //    canonical block are stored -- each stored entry is written exactly once.  psi(t)'s outputs
 //    equal t's (the pair computes one max for both), so exactly one of the two Q1 runs is
 //    written unless the block is psi-fixed; a Q0 row run and its mirror run are t-images, so
 //    one of the two is written.
-//  => per sweep every logical window of the half table is loaded once (the L2 item schedule,
-//     lcsb_api.cu, serves most repeated loads of a stored block from L2) and 3/8 of the half
-//     table is written.
+//  => per sweep every logical window of the half table is loaded once (from DRAM ~1.6 x the
+//     stored table at l = 17) and 3/8 of the half table is written.
 #include <math.h>
 #include <stdlib.h>
 
