@@ -6,6 +6,8 @@
 #include <string.h>
 #include <math.h>
 
+#include <vector>
+
 #include "lcsb.h"
 
 namespace lcsbk {
@@ -166,6 +168,12 @@ __host__ __device__ inline uint64_t qstored(const uint32_t* map, uint64_t s, int
   else if ((m & 3u) == 3u) e = ~e & kmask;
   return ((uint64_t)(m >> 2) << (2 * K)) | e;
 }
+
+// quarter_host.cu: the folded table's stored sizes, block map and item schedule
+uint64_t quarter_map_entries(int ell, int K);  // half-table blocks of 4^K entries
+uint64_t quarter_slots(int ell, int K);        // stored (canonical) blocks
+bool build_quarter_map(int ell, int K, uint32_t* map);
+bool quarter_schedule(int ell, int K, int M, const uint32_t* map, std::vector<uint32_t>& out);
 
 struct Q4Args {
   const void* g1;     // table one sweep back (W pass: the newest table)

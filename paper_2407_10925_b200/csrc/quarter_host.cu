@@ -1,0 +1,266 @@
+// quarter_host.cu -- host side of the symmetry-folded ("quarter") binary table (kern_bin2q.cu,
+// DESIGN.md §6): stored sizes, the block map, and the L2 item schedule of the sweep.
+#include <stdlib.h>
+
+#include <mutex>
+#include <vector>
+
+#include "lcsb_internal.cuh"
+
+namespace lcsbk {
+
+// blocks of the half table: 2^(2(l-K)-1), m = l-K-1 non-head prefix digits each.  Stored
+// (canonical) blocks, by Burnside: Q1 under {id, psi}: (4^m + 2^m) / 2 (psi fixes prefixes with
+// every digit in {01, 10}); Q0 under {id, s, t, s t}: (4^m + 2^m + 0 + 2^m) / 4 (s fixes digits
+// in {00, 11}, s t those in {01, 10}, t none).
+uint64_t quarter_map_entries(int ell, int K) { return 1ull << (2 * (ell - K) - 1); }
+uint64_t quarter_slots(int ell, int K) {
+  const int m = ell - K - 1;
+  if (m == 0) return 2;  // the two head blocks
+  return ((1ull << (2 * m)) + (1ull << m)) / 2 + ((1ull << (2 * m)) + (2ull << m)) / 4;
+}
+// map[beta] = (slot << 2) | mode; slots numbered in increasing order of canonical beta (the
+// smallest prefix of its orbit); mode = the symmetry mapping the canonical block to beta
+bool build_quarter_map(int ell, int K, uint32_t* map) {
+  const int PL = 2 * (ell - K);
+  const uint64_t nb = quarter_map_entries(ell, K);
+  uint64_t next = 0;
+  std::vector<uint64_t> canon(nb);
+  std::vector<int> how(nb);
+  for (uint64_t b = 0; b < nb; ++b) {
+    const bool q1 = (b >> (PL - 2)) & 1ull;
+    uint64_t c = b;
+    int g = 0;
+    for (int gg = 1; gg <= 3; ++gg) {
+      if (q1 && gg != 2) continue;
+      const uint64_t im = qblock_image(b, PL, gg);
+      if (im < c) {
+        c = im;
+        g = gg;  // b = g(c): every g here is an involution
+      }
+    }
+    canon[b] = c;
+    how[b] = g;
+  }
+  for (uint64_t b = 0; b < nb; ++b)
+    if (canon[b] == b) map[b] = (uint32_t)(next++ << 2);
+  for (uint64_t b = 0; b < nb; ++b)
+    if (canon[b] != b) map[b] = (map[canon[b]] & ~3u) | (uint32_t)how[b];
+  return next == quarter_slots(ell, K);
+}
+
+// Item order of the quarter sweep ("L2 schedule").  Block graph: nodes = stored
+// blocks, edges = tile pairs {t, psi t} joining the stored blocks of their two adv_b windows;
+// every block has four window ends (two per logical image).  A 2-colouring that cuts most edges
+// (BFS colouring + local search) gives a side A whose blocks have their tile pairs mostly on
+// the other side; listing each A-block's tile pairs consecutively makes them run concurrently on
+// neighbouring CTAs, so the block's four windows -- its two logical images -- come from DRAM once
+// and from L2 after.  The order is a permutation of the pair representatives; the arithmetic of
+// every item is unchanged.  Cached per (l, K, M): it depends on nothing else.
+bool quarter_schedule(int ell, int K, int M, const uint32_t* map,
+                             std::vector<uint32_t>& out) {
+  static std::mutex mu;
+  static int c_ell = 0, c_K = 0, c_M = 0;  // (A/B: LCSB_QSCHED=1 / 2 is read once per process)
+  static std::vector<uint32_t> cache;
+  std::lock_guard<std::mutex> lock(mu);
+  if (c_ell == ell && c_K == K && c_M == M) {
+    out = cache;
+    return true;
+  }
+  const int L = 2 * ell;
+  const uint64_t lmask = (1ull << L) - 1, q1 = 1ull << (L - 2);
+  const uint64_t amask = 0xAAAAAAAAAAAAAAAAull & lmask, bmask = 0x5555555555555555ull & lmask;
+  const uint64_t T = 1ull << (2 * M);
+  const uint64_t ntiles = 1ull << (2 * (ell - 1 - M));
+  const uint64_t nslots = quarter_slots(ell, K);
+  auto win = [&](uint64_t x) { return (x & amask) | ((x & bmask & ~q1) << 2); };
+  std::vector<uint32_t> etau, eu, ev;
+  for (uint64_t tau = 0; tau < ntiles; ++tau) {
+    const uint64_t x0 = q1 + tau * T;
+    const uint64_t p0 = pairswap_hd(~x0 & lmask) & ~(T - 1);
+    if (((p0 - q1) >> (2 * M)) < tau) continue;  // the pair is an item at its smaller tile
+    etau.push_back((uint32_t)tau);
+    eu.push_back(map[win(x0) >> (2 * K)] >> 2);
+    ev.push_back(map[win(p0) >> (2 * K)] >> 2);
+  }
+  const size_t E = etau.size();
+  std::vector<uint32_t> off(nslots + 1, 0);
+  for (size_t e = 0; e < E; ++e) {
+    off[eu[e] + 1]++;
+    if (ev[e] != eu[e]) off[ev[e] + 1]++;
+  }
+  for (uint64_t v = 0; v < nslots; ++v) off[v + 1] += off[v];
+  std::vector<uint32_t> adj(off[nslots]), fill(off.begin(), off.end() - 1);
+  for (size_t e = 0; e < E; ++e) {
+    adj[fill[eu[e]]++] = (uint32_t)e;
+    if (ev[e] != eu[e]) adj[fill[ev[e]]++] = (uint32_t)e;
+  }
+  auto other = [&](uint32_t e, uint32_t v) { return eu[e] == v ? ev[e] : eu[e]; };
+  std::vector<int8_t> col(nslots, -1);
+  std::vector<uint32_t> order;
+  order.reserve(nslots);
+  for (uint64_t s0 = 0; s0 < nslots; ++s0) {
+    if (col[s0] >= 0) continue;
+    col[s0] = 0;
+    size_t head = order.size();
+    order.push_back((uint32_t)s0);
+    while (head < order.size()) {
+      const uint32_t u = order[head++];
+      for (uint32_t i = off[u]; i < off[u + 1]; ++i) {
+        const uint32_t w = other(adj[i], u);
+        if (col[w] < 0) {
+          col[w] = (int8_t)(1 - col[u]);
+          order.push_back(w);
+        }
+      }
+    }
+  }
+  for (int pass = 0; pass < 16; ++pass) {  // local search: fewer same-coloured edges
+    size_t flips = 0;
+    for (uint64_t v = 0; v < nslots; ++v) {
+      int same = 0, diff = 0;
+      for (uint32_t i = off[v]; i < off[v + 1]; ++i) {
+        const uint32_t w = other(adj[i], (uint32_t)v);
+        if (w == v) continue;
+        if (col[w] == col[v]) ++same; else ++diff;
+      }
+      if (same > diff) {
+        col[v] ^= 1;
+        ++flips;
+      }
+    }
+    if (!flips) break;
+  }
+  std::vector<uint8_t> done(E, 0), grouped(nslots, 0);
+  out.clear();
+  out.reserve(E);
+  auto emit_group = [&](uint32_t v) {  // an A-block's not yet listed tile pairs, consecutively
+    grouped[v] = 1;
+    for (uint32_t i = off[v]; i < off[v + 1]; ++i)
+      if (!done[adj[i]]) {
+        done[adj[i]] = 1;
+        out.push_back(etau[adj[i]]);
+      }
+  };
+  // v2 (default): walking the BFS order, a B-block emits the groups of all its A-neighbours
+  // together, so its own windows (read by those groups) are consumed close in time as well
+  static const int version = getenv("LCSB_QSCHED") ? atoi(getenv("LCSB_QSCHED")) : 4;
+  for (uint32_t v : order) {
+    if (col[v] == 0) {
+      if (!grouped[v]) emit_group(v);
+    } else if (version >= 2) {
+      for (uint32_t i = off[v]; i < off[v + 1]; ++i) {
+        const uint32_t w = other(adj[i], v);
+        if (col[w] == 0 && !grouped[w]) emit_group(w);
+      }
+    }
+  }
+  for (size_t e = 0; e < E; ++e)
+    if (!done[e]) out.push_back(etau[e]);
+  if (out.size() != E) return false;
+  if (version >= 4) {
+    // v4 (default): re-cut the v2 order into waves of `kWave` items (about one wave of the
+    // persistent grid: its items run concurrently, so a stored quarter-block loaded in a wave is
+    // in L2 for the rest of it).  A wave grows greedily: always the item with the most of its
+    // (<= 4) quarter-block pieces already loaded by the wave; a new seed comes from the v2 order.
+    static const int kWave = getenv("LCSB_QWAVE") ? atoi(getenv("LCSB_QWAVE")) : 444;
+    std::vector<uint32_t> idx_of_tau(ntiles, 0);
+    for (size_t e = 0; e < E; ++e) idx_of_tau[etau[e]] = (uint32_t)e;
+    const uint64_t kmask = (1ull << (2 * K)) - 1;
+    auto window_pieces = [&](uint64_t w, uint32_t* pc) {  // the 2 stored quarter-blocks of w
+      const uint32_t m = map[w >> (2 * K)];
+      const uint64_t slot = m >> 2, e = w & kmask;
+      uint64_t o0, o1;
+      if ((m & 3u) == 0) {
+        o0 = e;
+        o1 = e + T;
+      } else if ((m & 3u) == 3u) {
+        o0 = (~e & kmask) & ~(2 * T - 1);
+        o1 = o0 + T;
+      } else {
+        const uint64_t f = ((m & 3u) == 1u) ? (pairswap_hd(e) & kmask) : (pairswap_hd(~e & kmask) & kmask);
+        o0 = (f & ~(4 * T - 1)) | (f & T);
+        o1 = o0 + 2 * T;
+      }
+      pc[0] = (uint32_t)((slot << 2) | ((o0 / T) & 3));
+      pc[1] = (uint32_t)((slot << 2) | ((o1 / T) & 3));
+    };
+    std::vector<uint32_t> pcs(4 * E);
+    std::vector<uint8_t> npc(E);
+    const uint64_t npieces = nslots * 4;
+    std::vector<uint32_t> poff(npieces + 1, 0);
+    for (size_t e = 0; e < E; ++e) {
+      const uint64_t x0 = q1 + (uint64_t)etau[e] * T;
+      const uint64_t p0 = pairswap_hd(~x0 & lmask) & ~(T - 1);
+      uint32_t q[4];
+      window_pieces(win(x0), q);
+      window_pieces(win(p0), q + 2);
+      int n = 0;
+      for (int k = 0; k < 4; ++k) {
+        bool dup = false;
+        for (int j = 0; j < n; ++j) dup = dup || pcs[4 * e + j] == q[k];
+        if (!dup) pcs[4 * e + n++] = q[k];
+      }
+      npc[e] = (uint8_t)n;
+      for (int k = 0; k < n; ++k) poff[pcs[4 * e + k] + 1]++;
+    }
+    for (uint64_t q = 0; q < npieces; ++q) poff[q + 1] += poff[q];
+    std::vector<uint32_t> pinv(poff[npieces]), pfill(poff.begin(), poff.end() - 1);
+    for (size_t e = 0; e < E; ++e)
+      for (int k = 0; k < npc[e]; ++k) pinv[pfill[pcs[4 * e + k]]++] = (uint32_t)e;
+    std::vector<uint32_t> v2(out);  // seeds, in v2 order
+    std::vector<uint8_t> taken(E, 0), score(E, 0);
+    std::vector<uint32_t> pwave(npieces, ~0u), touched;
+    std::vector<uint32_t> bucket[5];
+    out.clear();
+    size_t seed = 0;
+    for (uint32_t wave = 0; out.size() < E; ++wave) {
+      int cnt = 0;
+      for (auto& b : bucket) b.clear();
+      for (uint32_t j : touched) score[j] = 0;
+      touched.clear();
+      auto add = [&](uint32_t i) {
+        taken[i] = 1;
+        out.push_back(etau[i]);
+        ++cnt;
+        for (int k = 0; k < npc[i]; ++k) {
+          const uint32_t q = pcs[4 * i + k];
+          if (pwave[q] == wave) continue;
+          pwave[q] = wave;
+          for (uint32_t t = poff[q]; t < poff[q + 1]; ++t) {
+            const uint32_t j = pinv[t];
+            if (taken[j]) continue;
+            if (!score[j]) touched.push_back(j);
+            bucket[++score[j]].push_back(j);
+          }
+        }
+      };
+      while (cnt < kWave && out.size() < E) {
+        int pick = -1;
+        for (int sc = 4; sc >= 1 && pick < 0; --sc)
+          while (!bucket[sc].empty()) {
+            const uint32_t j = bucket[sc].back();
+            bucket[sc].pop_back();
+            if (!taken[j] && score[j] == sc) {
+              pick = (int)j;
+              break;
+            }
+          }
+        if (pick < 0) {
+          while (seed < E && taken[idx_of_tau[v2[seed]]]) ++seed;
+          if (seed >= E) break;
+          pick = (int)idx_of_tau[v2[seed]];
+        }
+        add((uint32_t)pick);
+      }
+    }
+    if (out.size() != E) return false;
+  }
+  cache = out;
+  c_ell = ell;
+  c_K = K;
+  c_M = M;
+  return true;
+}
+
+}  // namespace lcsbk
