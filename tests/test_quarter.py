@@ -179,6 +179,34 @@ def test_quarter_equals_half_table_l13(dtype):
 
 @pytest.mark.gpu
 @pytest.mark.skipif(not has_cuda(), reason="needs a CUDA device")
+def test_quarter_dynamic_claiming_under_graph_replay(monkeypatch):
+    """l = 12 fp32: the scheduled sweep with dynamic item claiming (its counter zeroed by a memset
+    node before every launch) replayed from captured CUDA graphs equals plain launches, static
+    claiming and the half table, bitwise."""
+    from seeded_inputs import splitmix64_indices
+    idx = splitmix64_indices(0x240710925, 1 << 18, 1 << 24)
+    vals = []
+    for env in ({}, {"LCSB_NO_GRAPHS": "1"}, {"LCSB_QSTATIC": "1"}):
+        for k, v in env.items():
+            monkeypatch.setenv(k, v)
+        h = L.Lcsb(2, 2, 12, dtype="f32")
+        assert h.kernel_in_use == "bin2q"
+        h.sweep(70)
+        h.sweep(33)
+        vals.append((h.table_gather(idx), h.table_gather(idx, which=1), h.bound().bound))
+        h.destroy()
+        for k in env:
+            monkeypatch.delenv(k)
+    ref = L.Lcsb(2, 2, 12, dtype="f32", symmetry=1)
+    ref.sweep(103)
+    rv = (ref.table_gather(idx), ref.table_gather(idx, which=1), ref.bound().bound)
+    ref.destroy()
+    for v in vals:
+        assert np.array_equal(v[0], rv[0]) and np.array_equal(v[1], rv[1]) and v[2] == rv[2]
+
+
+@pytest.mark.gpu
+@pytest.mark.skipif(not has_cuda(), reason="needs a CUDA device")
 def test_quarter_config4_sampled_after_3_sweeps():
     """BASELINE config 4 (2^34 states, fp32) on the quarter table: 2^20 seeded states after 3
     (and 2) sweeps against the oracle's sampled mode, bit-exact."""
