@@ -40,7 +40,9 @@ enum { LCSB_F64 = 0, LCSB_F32 = 1 };
  *              back (reading R1); d+1 tables live.
  *   TWO_ARRAY: Lueker's two-array form for sigma = d = 2 ("storing only two arrays",
  *              PAPER.md:400): every option reads the previous sweep; 2 tables live; the bound
- *              is 2 rho / (1 + rho) with rho = R - E (reading R10).
+ *              is 2 rho / (1 + rho) with rho = R - E (reading R10).  Also accepted for d = 2
+ *              and any sigma (beyond the paper, reading R20): the option that drops
+ *              both heads when they differ is not offered.  d > 2 is rejected (LCSB_EINVAL).
  *   AUTO:      TWO_ARRAY for sigma = d = 2, KS otherwise. */
 enum { LCSB_FORM_AUTO = 0, LCSB_FORM_KS = 1, LCSB_FORM_TWO_ARRAY = 2 };
 

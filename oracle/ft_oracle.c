@@ -25,6 +25,8 @@
  *       r * (1.0 / sigma^|N|) with sigma^|N| an exact integer; r accumulates in the loop
  *       order of Alg. 1: c over Sigma^{|N|} lexicographically, c_1 (the lowest string index in
  *       N) most significant.
+ *   R20 two-array form for d = 2, any sigma (extension of PAPER.md:400): the drop-both option
+ *       (heads differ, N = both strings) is not offered; the others are as in Alg. 1.
  *
  * Storage rounding (dtype = f32) is applied by the caller (ft_oracle.py) after each sweep, as
  * a round-to-nearest-even cast of the fp64 result, which is what storing fp32 does.
@@ -72,9 +74,12 @@ uint64_t fo_encode(int sigma, int d, int ell, const int* A) {
  *   shift[k-1] : a constant added to every value read from src[k-1]; this is how the W pass
  *                F(v + (d-1)R 1, ..., v + 0 R 1) of Alg. 2 line 6 is formed literally
  *                (value = v[y] + shift, in fp64, before summation).
+ *   two_array  : 1 = two-array form with d = 2 and sigma > 2 (reading R20): the option
+ *                that drops both heads when they differ (|N| = d with b = 0) is not offered.  For
+ *                sigma = 2 that option never exists, so the binary form is unaffected.
  */
 static double fo_F_at(int sigma, int d, int ell, const double* const* src, const double* shift,
-                      uint64_t x) {
+                      int two_array, uint64_t x) {
     int A[FO_MAXD * FO_MAXL];
     int S[FO_MAXD * FO_MAXL];
     int N[FO_MAXD];
@@ -92,6 +97,7 @@ static double fo_F_at(int sigma, int d, int ell, const double* const* src, const
         int nN = 0;
         for (int j = 0; j < d; ++j)
             if (A[j * ell + 0] != z) N[nN++] = j;
+        if (two_array && nN == d && !b) continue; /* R20: drop-both not offered */
         double cand;
         if (nN == 0) {
             cand = 0.0; /* R3 */
@@ -129,8 +135,9 @@ static double fo_F_at(int sigma, int d, int ell, const double* const* src, const
  * thread count does not change any value.
  */
 int fo_apply_F(int sigma, int d, int ell, const double* const* src, const double* shift,
-               double* out, int threads) {
+               double* out, int threads, int two_array) {
     if (sigma < 2 || d < 2 || ell < 1 || d > FO_MAXD || ell > FO_MAXL) return 1;
+    if (two_array && d != 2) return 1;
     uint64_t n = fo_ipow((uint64_t)sigma, d * ell);
     double zero[FO_MAXD] = {0};
     const double* sh = shift ? shift : zero;
@@ -138,18 +145,19 @@ int fo_apply_F(int sigma, int d, int ell, const double* const* src, const double
     if (threads > 0) omp_set_num_threads(threads);
 #pragma omp parallel for schedule(static)
 #endif
-    for (int64_t x = 0; x < (int64_t)n; ++x) out[x] = fo_F_at(sigma, d, ell, src, sh, (uint64_t)x);
+    for (int64_t x = 0; x < (int64_t)n; ++x) out[x] = fo_F_at(sigma, d, ell, src, sh, two_array, (uint64_t)x);
     (void)threads;
     return 0;
 }
 
 /* F at a list of coordinates only (used by the sampled mode in ft_oracle.py). */
 int fo_apply_F_at(int sigma, int d, int ell, const double* const* src, const double* shift,
-                  const uint64_t* idx, int64_t count, double* out) {
+                  const uint64_t* idx, int64_t count, double* out, int two_array) {
     if (sigma < 2 || d < 2 || ell < 1 || d > FO_MAXD || ell > FO_MAXL) return 1;
+    if (two_array && d != 2) return 1;
     double zero[FO_MAXD] = {0};
     const double* sh = shift ? shift : zero;
-    for (int64_t i = 0; i < count; ++i) out[i] = fo_F_at(sigma, d, ell, src, sh, idx[i]);
+    for (int64_t i = 0; i < count; ++i) out[i] = fo_F_at(sigma, d, ell, src, sh, two_array, idx[i]);
     return 0;
 }
 
@@ -180,6 +188,7 @@ static double fo_value_rec(int sigma, int d, int ell, int form, int f32, int s, 
         int nN = 0;
         for (int j = 0; j < d; ++j)
             if (A[j * ell + 0] != z) N[nN++] = j;
+        if (form == 2 && nN == d && !b) continue; /* R20 (as in fo_F_at) */
         double cand;
         if (nN == 0) {
             cand = 0.0;
@@ -215,6 +224,7 @@ static double fo_value_rec(int sigma, int d, int ell, int form, int f32, int s, 
 int fo_sample(int sigma, int d, int ell, int form, int f32, int sweeps, const uint64_t* idx,
               int64_t count, double* out, int threads) {
     if (sigma < 2 || d < 2 || ell < 1 || d > FO_MAXD || ell > FO_MAXL) return 1;
+    if (form == 2 && d != 2) return 1;
 #ifdef _OPENMP
     if (threads > 0) omp_set_num_threads(threads);
 #pragma omp parallel for schedule(dynamic, 256)

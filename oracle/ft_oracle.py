@@ -10,7 +10,8 @@ through the iteration and bound bookkeeping of
 * Alg. 2 "The Feasible Triplet Algorithm"            PAPER.md:696-717
 * Alg. 5 "The Binary Feasible Triplet Algorithm"     PAPER.md:728-750
 * Lueker's two-array form for sigma=2, d=2 ("storing only two arrays ... with the bound
-  calculation adjusted appropriately")               PAPER.md:400   (reading R10 in DESIGN.md)
+  calculation adjusted appropriately")               PAPER.md:400   (reading R10 in DESIGN.md),
+  extended to d = 2 and any sigma with the drop-both option removed (reading R20)
 
 Everything is fp64 over the FULL logical table.  ``dtype='f32'`` emulates fp32 storage: the
 result of every sweep is rounded to fp32 (round-to-nearest-even) and widened back, exactly what
@@ -66,7 +67,8 @@ def _lib():
             lib = ctypes.CDLL(build())
             dpp = ctypes.POINTER(ctypes.c_void_p)
             lib.fo_apply_F.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, dpp,
-                                       ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int]
+                                       ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int,
+                                       ctypes.c_int]
             lib.fo_apply_F.restype = ctypes.c_int
             lib.fo_apply_F_at.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, dpp,
                                           ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64,
@@ -148,9 +150,11 @@ def _as_f64(v) -> np.ndarray:
     return v
 
 
-def apply_F(sigma: int, d: int, ell: int, src, shift=None, threads: int = 0) -> np.ndarray:
+def apply_F(sigma: int, d: int, ell: int, src, shift=None, threads: int = 0,
+            two_array: bool = False) -> np.ndarray:
     """F(src[0], ..., src[d-1]): src[k-1] is read when |N| = k (reading R1).  ``shift[k-1]`` is
-    added to every value read from src[k-1] (used for Alg. 2 line 6)."""
+    added to every value read from src[k-1] (used for Alg. 2 line 6).  ``two_array`` (d = 2):
+    the drop-both option (both heads differ, |N| = 2) is not offered (reading R20)."""
     n = n_states(sigma, d, ell)
     if len(src) != d:
         raise ValueError("need d source vectors")
@@ -162,20 +166,21 @@ def apply_F(sigma: int, d: int, ell: int, src, shift=None, threads: int = 0) -> 
     sh = np.zeros(d, dtype=np.float64) if shift is None else np.ascontiguousarray(shift, np.float64)
     out = np.empty(n, dtype=np.float64)
     rc = _lib().fo_apply_F(sigma, d, ell, ctypes.cast(ptrs, ctypes.POINTER(ctypes.c_void_p)),
-                           sh.ctypes.data, out.ctypes.data, int(threads))
+                           sh.ctypes.data, out.ctypes.data, int(threads), int(bool(two_array)))
     if rc:
         raise ValueError("fo_apply_F rejected the parameters")
     return out
 
 
-def apply_F_at(sigma, d, ell, src, idx, shift=None) -> np.ndarray:
+def apply_F_at(sigma, d, ell, src, idx, shift=None, two_array: bool = False) -> np.ndarray:
     arrs = [_as_f64(s) for s in src]
     ptrs = (ctypes.c_void_p * d)(*[a.ctypes.data for a in arrs])
     sh = np.zeros(d, dtype=np.float64) if shift is None else np.ascontiguousarray(shift, np.float64)
     idx = np.ascontiguousarray(idx, dtype=np.uint64)
     out = np.empty(idx.shape[0], dtype=np.float64)
     rc = _lib().fo_apply_F_at(sigma, d, ell, ctypes.cast(ptrs, ctypes.POINTER(ctypes.c_void_p)),
-                              sh.ctypes.data, idx.ctypes.data, idx.shape[0], out.ctypes.data)
+                              sh.ctypes.data, idx.ctypes.data, idx.shape[0], out.ctypes.data,
+                              int(bool(two_array)))
     if rc:
         raise ValueError("fo_apply_F_at rejected the parameters")
     return out
@@ -196,8 +201,9 @@ def resolve_form(sigma: int, d: int, form: str) -> int:
     if form == "ks":
         return FORM_KS
     if form == "two_array":
-        if (sigma, d) != (2, 2):
-            raise ValueError("two-array form is defined for sigma=2, d=2 only (PAPER.md:400)")
+        # PAPER.md:400 states it for sigma = d = 2; reading R20 extends it to d = 2, any sigma
+        if d != 2:
+            raise ValueError("two-array form is defined for d = 2 only (PAPER.md:400, reading R20)")
         return FORM_TWO_ARRAY
     raise ValueError(form)
 
@@ -237,7 +243,8 @@ class Run:
                 self.gens = [new] + self.gens[:-1]          # shift the rows (line 11)
             else:
                 g = self.gens[0]
-                new = apply_F(self.sigma, self.d, self.ell, [g] * self.d, threads=self.threads)
+                new = apply_F(self.sigma, self.d, self.ell, [g] * self.d, threads=self.threads,
+                              two_array=True)
                 new = round_storage(new, self.dtype)
                 self.prev = g
                 self.gens = [new]
@@ -254,7 +261,7 @@ class Run:
             shift = np.array([float(d - k) * R for k in range(1, d + 1)])
             Fv = apply_F(self.sigma, d, self.ell, [v] * d, shift=shift, threads=self.threads)
             return (v + float(d) * R) - Fv
-        Fv = apply_F(self.sigma, d, self.ell, [v] * d, threads=self.threads)
+        Fv = apply_F(self.sigma, d, self.ell, [v] * d, threads=self.threads, two_array=True)
         return (v + R) - Fv
 
     def bound_from(self, R: float, E: float) -> float:

@@ -5,7 +5,8 @@
 //   F_z      = sigma^{-|N|} * sum_{c in Sigma^{|N|}} v_{|N|}[A with s_j <- T(s_j) c_j, j in N]
 //                                                                            Alg. 1
 // with N = (j : h(a_j) != z), F_z = 0 for empty N (reading R3), and v_{|N|} the table |N| sweeps
-// back (KS form, reading R1) or the previous sweep (two-array form).
+// back (KS form, reading R1) or the previous sweep (two-array form; for sigma > 2,
+// d = 2 without the drop-both option, reading R20).
 //
 // Index arithmetic (reading R14, heads in the top digit group): with contrib_j the part of x
 // contributed by string j and W_j = sigma^(d(l-1) + (d-1-j)) the weight of its head, advancing
@@ -136,7 +137,9 @@ struct Gen {
       double cand = mask ? option_mean(a, contrib, head, mask, shift) : 0.0;
       if (cand > best) best = cand;
     }
-    if (nseen < sigma) {  // some z is no string's head: N = all strings
+    // some z is no string's head: N = all strings; not offered by the two-array form (d = 2)
+    // when the heads differ (drop-both, reading R20)
+    if (nseen < sigma && !(a.form == LCSB_FORM_TWO_ARRAY && !b)) {
       double cand = option_mean(a, contrib, head, full, shift);
       if (cand > best) best = cand;
     }

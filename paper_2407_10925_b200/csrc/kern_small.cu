@@ -131,7 +131,8 @@ __device__ __forceinline__ double dispatch_mask(int mask, const T* const* src,
 template <typename T, int SIG, int D, bool POOL = false>
 __device__ __forceinline__ double F_small(const T* const* src, const double* sh, uint32_t x,
                                           int ell, uint32_t headw_top,
-                                          const double* const* pin = nullptr) {
+                                          const double* const* pin = nullptr,
+                                          bool two_array = false) {
   uint32_t contrib[D], head[D];
 #pragma unroll
   for (int j = 0; j < D; ++j) contrib[j] = 0;
@@ -167,7 +168,9 @@ __device__ __forceinline__ double F_small(const T* const* src, const double* sh,
         mask ? dispatch_mask<T, SIG, D, POOL>(mask, src, pin, sh, contrib, head, headw_top) : 0.0;
     if (cand > best) best = cand;
   }
-  if (nseen < SIG) {  // some z is no string's head: N = all strings
+  // some z is no string's head: N = all strings; the two-array form (d = 2) does not offer it
+  // when the heads differ (drop-both, reading R20)
+  if (nseen < SIG && !(two_array && !b)) {
     const double cand =
         option_at<T, SIG, D, (1 << D) - 1, POOL>(src, pin, sh, contrib, head, headw_top);
     if (cand > best) best = cand;
@@ -184,13 +187,14 @@ __global__ void __launch_bounds__(256) small_kernel(GenericArgs a) {
   for (int i = 0; i < D * (a.ell - 1); ++i) headw_top *= SIG;
   const uint32_t n = (uint32_t)a.n;
   const uint32_t stride = gridDim.x * blockDim.x;
+  const bool ta = (a.form == LCSB_FORM_TWO_ARRAY);
   if (!WMODE) {
     double zero[D];
 #pragma unroll
     for (int k = 0; k < D; ++k) zero[k] = 0.0;
     T* dst = reinterpret_cast<T*>(a.dst);
     for (uint32_t x = blockIdx.x * blockDim.x + threadIdx.x; x < n; x += stride)
-      dst[x] = (T)F_small<T, SIG, D>(src, zero, x, a.ell, headw_top);
+      dst[x] = (T)F_small<T, SIG, D>(src, zero, x, a.ell, headw_top, nullptr, ta);
   } else {
     const double R0 = dec_ord(a.red_in[0]), R1 = dec_ord(a.red_in[1]);
     const bool ks = (a.form == LCSB_FORM_KS);
@@ -205,7 +209,7 @@ __global__ void __launch_bounds__(256) small_kernel(GenericArgs a) {
     double w0 = -INFINITY, w1 = -INFINITY;
     for (uint32_t x = blockIdx.x * blockDim.x + threadIdx.x; x < n; x += stride) {
       const double v = (double)center[x];
-      const double F0 = F_small<T, SIG, D>(src, sh0, x, a.ell, headw_top);
+      const double F0 = F_small<T, SIG, D>(src, sh0, x, a.ell, headw_top, nullptr, ta);
       const double F1 = ks ? F_small<T, SIG, D>(src, sh1, x, a.ell, headw_top) : F0;
       w0 = fmax(w0, (v + dR0) - F0);
       w1 = fmax(w1, (v + dR1) - F1);

@@ -193,15 +193,17 @@ static int plan_config(const lcsb_config* c, Plan* p, char* why, size_t whylen) 
     snprintf(why, whylen, "unknown form %d", c->form);
     return LCSB_EINVAL;
   }
-  if (form == LCSB_FORM_TWO_ARRAY && !binary) {
-    snprintf(why, whylen, "the two-array form is defined for sigma = d = 2 only (PAPER.md:400)");
+  if (form == LCSB_FORM_TWO_ARRAY && c->d != 2) {
+    snprintf(why, whylen,
+             "the two-array form is defined for d = 2 only (PAPER.md:400; sigma > 2: reading R20)");
     return LCSB_EINVAL;
   }
   if (c->kernel != LCSB_KERNEL_AUTO && c->kernel != LCSB_KERNEL_GENERIC) {
     snprintf(why, whylen, "unknown kernel %d", c->kernel);
     return LCSB_EINVAL;
   }
-  const bool sym_ok = (form == LCSB_FORM_TWO_ARRAY) && c->ell >= 2 && c->kernel == LCSB_KERNEL_AUTO;
+  const bool sym_ok =
+      binary && (form == LCSB_FORM_TWO_ARRAY) && c->ell >= 2 && c->kernel == LCSB_KERNEL_AUTO;
   const int P = c->shards < 1 ? 1 : c->shards;
   const bool sharded = P > 1 || (c->nccl_id && !c->virtual_shards);
   // quarter table geometry: blocks of 4^K, tiles of 4^M (M <= K - 1)

@@ -52,8 +52,11 @@ def test_required_bytes_and_validation():
     # config 2: 4 tables of 3^12 fp64 + the pooled means of every ring slot (kern_small.cu):
     # per row of 27, 9 means for |N| = 2 and 1 for |N| = 3
     assert L.lcsb_required_bytes(3, 3, 4, "f64") == 4 * 3 ** 12 * 8 + 256 + 4 * 3 ** 9 * 10 * 8
-    # invalid: two-array for sigma != 2, d > 16, sigma^(d l) too large, symmetry without binary
-    assert L.lcsb_required_bytes(3, 2, 2, "f32", form="two_array") == 0
+    # two-array for d = 2, sigma > 2 (reading R20): 2 full tables
+    assert L.lcsb_required_bytes(3, 2, 2, "f32", form="two_array") == 2 * 81 * 4 + 256
+    # invalid: two-array for d > 2, d > 16, sigma^(d l) too large, symmetry without binary
+    assert L.lcsb_required_bytes(2, 3, 2, "f32", form="two_array") == 0
+    assert L.lcsb_required_bytes(3, 2, 2, "f32", form="two_array", symmetry=1) == 0
     assert L.lcsb_required_bytes(2, 17, 1, "f32") == 0
     assert L.lcsb_required_bytes(2, 2, 40, "f32") == 0
     assert L.lcsb_required_bytes(3, 2, 2, "f32", symmetry=1) == 0

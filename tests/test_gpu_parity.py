@@ -250,6 +250,73 @@ def test_generic_two_array_l1():
     h.destroy()
 
 
+# ------------------------------------------------ two-array form for d = 2, sigma > 2 (reading R20)
+
+@pytest.mark.parametrize("sigma,ell,dtype,sweeps", [
+    (3, 1, "f64", 30), (3, 2, "f64", 40), (3, 3, "f32", 30), (3, 4, "f64", 12),
+    (4, 2, "f64", 30), (4, 3, "f32", 25), (5, 2, "f32", 20), (10, 1, "f64", 30)])
+def test_two_array_sigma_gt2_matches_oracle(sigma, ell, dtype, sweeps):
+    Lcsb = _lcsb()
+    h = Lcsb(sigma, 2, ell, dtype=dtype, form="two_array")
+    assert h.kernel_in_use in ("small", "generic")
+    run = fo.Run(sigma, 2, ell, "two_array", dtype)
+    for s in range(1, sweeps + 1):
+        h.sweep(1)
+        run.sweep(1)
+        if s in (1, 2, 5, sweeps):
+            _cmp_tables(h.table(0), run.gens[0], dtype)
+            _cmp_tables(h.table(1), run.prev, dtype)
+    _cmp_bound(h.bound(), run.bound(), dtype)
+    h.destroy()
+
+
+@pytest.mark.parametrize("dtype", ["f32", "f64"])
+def test_two_array_sigma3_small_matches_generic(dtype):
+    Lcsb = _lcsb()
+    a = Lcsb(3, 2, 5, dtype=dtype, form="two_array")
+    b = Lcsb(3, 2, 5, dtype=dtype, form="two_array", kernel="generic")
+    assert a.kernel_in_use == "small" and b.kernel_in_use == "generic"
+    for n in (1, 4, 30):
+        a.sweep(n)
+        b.sweep(n)
+        for k in range(2):
+            assert np.array_equal(a.table(k), b.table(k))
+        ba, bb = a.bound(), b.bound()
+        assert (ba.R_max, ba.R_min, ba.E_at_Rmax, ba.E_at_Rmin) == \
+               (bb.R_max, bb.R_min, bb.E_at_Rmax, bb.E_at_Rmin)
+    a.destroy()
+    b.destroy()
+
+
+@pytest.mark.parametrize("sigma,ell,printed,line", [(4, 4, 0.589484, 280), (3, 5, 0.665874, 297),
+                                                    (5, 4, 0.539129, 280)])
+def test_two_array_sigma_gt2_converges_to_appendix3(sigma, ell, printed, line):
+    """The GPU two-array run converges to the value Appendix 3 prints for the KS form."""
+    Lcsb = _lcsb()
+    h = Lcsb(sigma, 2, ell, dtype="f64", form="two_array")
+    value = None
+    for _ in range(40):
+        h.sweep(25)
+        value = h.bound().best_bound
+        if printed - 5e-7 <= value < printed + 1e-6:
+            break
+    assert printed - 5e-7 <= value < printed + 1e-6, (value, printed, f"PAPER.md:{line}")
+    h.destroy()
+
+
+def test_two_array_sigma4_l8_sampled_after_3_sweeps():
+    """Config-3 size (4^16 states, fp32) in the two-array form: 2 tables instead of KS's 3."""
+    Lcsb = _lcsb()
+    h = Lcsb(4, 2, 8, dtype="f32", form="two_array")
+    idx = _splitmix(SEED, 1 << 18, 4 ** 16)
+    h.sweep(3)
+    ref = fo.sample_values(4, 2, 8, 3, idx, form="two_array", dtype="f32")
+    assert np.array_equal(h.table_gather(idx), ref)
+    ref2 = fo.sample_values(4, 2, 8, 2, idx, form="two_array", dtype="f32")
+    assert np.array_equal(h.table_gather(idx, which=1), ref2)
+    h.destroy()
+
+
 def test_config2_sigma3_d3_l4_f64_300_sweeps():
     """BASELINE config 2: 3^12 states, fp64, KS, 300 sweeps (paper 0.556649)."""
     Lcsb = _lcsb()
@@ -372,7 +439,7 @@ def test_errors_and_edge_cases():
         Lcsb(2, 2, 20, dtype="f64", symmetry=0)   # 2 x 8 TiB
     assert e.value.code == 2
     with pytest.raises(LcsbError) as e:
-        Lcsb(3, 2, 2, form="two_array")
+        Lcsb(3, 3, 2, form="two_array")   # two-array needs d = 2 (reading R20)
     assert e.value.code == 1
 
 

@@ -232,6 +232,65 @@ def test_appendix3_cell(sigma, d, ell, printed, line, typo):
         assert _in_band(value, printed), (value, printed, f"PAPER.md:{line}")
 
 
+# ------------------------------------------ two-array form for d = 2, sigma > 2 (reading R20)
+
+def _appendix_d2():
+    return {(int(r[0]), int(r[2])): (float(r[3]), int(r[4]))
+            for r in _load("appendix3.txt") if r[1] == "2" and len(r) == 5}
+
+
+def _converge(run, printed, max_sweeps=600):
+    value = None
+    for k in range(1, max_sweeps + 1):
+        run.sweep()
+        if k % 25 == 0:
+            value = run.bound()["bound_at_Rmax"]
+            if _in_band(value, printed):
+                break
+    return value
+
+
+@pytest.mark.parametrize("sigma,ell", [(3, 1), (3, 2), (3, 3), (3, 4), (4, 1), (4, 2), (4, 3),
+                                       (5, 1), (5, 2), (5, 3), (7, 2)])
+def test_two_array_d2_matches_appendix3(sigma, ell):
+    # The two-array form with the drop-both option removed (every remaining option consumes
+    # 1 + gain characters, so 2 rho / (1 + rho) is a certified bound, reading R20) converges to
+    # the value Appendix 3 prints for the KS form.
+    printed, line = _appendix_d2()[(sigma, ell)]
+    value = _converge(fo.Run(sigma, 2, ell, "two_array"), printed)
+    assert _in_band(value, printed), (value, printed, f"PAPER.md:{line}")
+
+
+@pytest.mark.parametrize("sigma", range(2, 11))
+def test_two_array_d2_ell1_closed_form(sigma):
+    # l = 1: growth 1/(sigma+1) per character in both forms, gamma >= 2/(sigma+1)
+    res = fo.feasible_triplet(sigma, 2, 1, 300, form="two_array")
+    assert res["bound_at_Rmax"] == pytest.approx(2.0 / (sigma + 1), abs=1e-10)
+
+
+def test_two_array_d2_drop_both_must_be_excluded():
+    # Keeping the drop-both option in the two-array form (cost 1 step for 2 characters, gain 0)
+    # breaks the tau = 1 + gain identity and overshoots the paper's value: sigma = 3, l = 2 reaches
+    # 2/3 against the printed 0.620690.  The rule therefore has to be in the oracle.
+    sigma, ell = 3, 2
+    g = np.zeros(fo.n_states(sigma, 2, ell))
+    for _ in range(200):
+        prev, g = g, fo.apply_F(sigma, 2, ell, [g, g], two_array=False)
+    R = float((g - prev).max())
+    E = max(0.0, float(((g + R) - fo.apply_F(sigma, 2, ell, [g, g])).max()))
+    rho = R - E
+    assert 2 * rho / (1 + rho) > 0.620690 + 0.01
+    res = fo.feasible_triplet(sigma, 2, ell, 200, form="two_array")
+    assert _in_band(res["bound_at_Rmax"], 0.620690)
+
+
+def test_two_array_rejects_d_above_2():
+    with pytest.raises(ValueError):
+        fo.Run(3, 3, 1, "two_array")
+    with pytest.raises(ValueError):
+        fo.apply_F(2, 3, 1, [np.zeros(8)] * 3, two_array=True)
+
+
 # ---------------------------------------------------------------- brute force
 
 @pytest.mark.parametrize("sigma,nmax", [(2, 6), (3, 3)])
@@ -337,12 +396,13 @@ def test_sampled_mode_equals_full_table(form, dtype):
         run.sweep()
         samp = fo.sample_values(2, 2, ell, s, idx, form=form, dtype=dtype)
         assert np.array_equal(samp, run.newest)
-    run = fo.Run(3, 2, 2, "ks", dtype)
-    idx = np.arange(81, dtype=np.uint64)
-    for s in range(1, 4):
-        run.sweep()
-        assert np.array_equal(fo.sample_values(3, 2, 2, s, idx, form="ks", dtype=dtype),
-                              run.newest)
+    for f in ("ks", "two_array"):
+        run = fo.Run(3, 2, 2, f, dtype)
+        idx = np.arange(81, dtype=np.uint64)
+        for s in range(1, 4):
+            run.sweep()
+            assert np.array_equal(fo.sample_values(3, 2, 2, s, idx, form=f, dtype=dtype),
+                                  run.newest)
 
 
 def test_f32_storage_drift_small():
