@@ -40,6 +40,16 @@ namespace lcsbk {
 namespace {
 
 constexpr int kThreads = 256;
+// Q4Args::flags: issue the next item's loads as soon as the input stage is consumed (before the
+// row-mean phase), and the bank-conflict-free tail order below
+constexpr int kQ4EarlyIssue = 1, kQ4TailPerm = 2;
+// Thread order of the 16 tails (a0, b0) of a row (i & 15 = 4 a0 + b0): each quarter-warp's 8
+// 128-bit window loads (adv_b at 16 a0 + 64 b0 bytes, adv_a of the swapped and complemented
+// swapped units at 16 b0 + 64 a0) then fall in 8 distinct 16-byte bank groups.
+constexpr uint64_t kTailPerm = 0xFE985432DCBA7610ull;  // nibble k = tail of lane k
+__device__ __forceinline__ uint32_t tail_of(uint32_t j, bool perm) {
+  return perm ? ((j & ~15u) | (uint32_t)((kTailPerm >> (4 * (j & 15))) & 15)) : j;
+}
 constexpr uint64_t kA4 = 0xCCCCCCCCCCCCCCCCull;  // a digit (bits 2-3) of every 4-bit group
 constexpr uint64_t kB4 = 0x3333333333333333ull;  // b digit (bits 0-1)
 
@@ -233,9 +243,10 @@ __global__ void __launch_bounds__(kThreads) q4_kernel(Q4Args a) {
     uint64_t U[kGroup];
     const int n = group_units(g, cu, U);
 
+    const bool perm = (a.flags & kQ4TailPerm) != 0;
     for (uint32_t j = tid; j < (uint32_t)n * TT; j += kThreads) {
       const int k = (int)(j / TT);
-      const uint32_t i = j % TT;
+      const uint32_t i = tail_of(j % TT, perm);
       const uint64_t X = U[k];
       const uint64_t sX = digit_swap(X);
       const uint64_t cX = unit_comp(g, X), csX = unit_comp(g, sX);
@@ -292,6 +303,11 @@ __global__ void __launch_bounds__(kThreads) q4_kernel(Q4Args a) {
       }
     }
     __syncthreads();
+    const bool early = (a.flags & kQ4EarlyIssue) != 0;
+    if (early && tid == 0 && pc < g.nunits) {  // the input stage is consumed: refill it now
+      q4_issue<T, M, S, WMODE>(g, pc, buf, &bars[s], g1, pin);
+      pc = q4_next(g, pc + G, G);
+    }
     if (!WMODE) {
       // row means of the new table: output rows (h_a < 2, h_b, t >> 4) of the group's units, each
       // summed in Alg. 1's order over its 16 stored values
@@ -309,7 +325,7 @@ __global__ void __launch_bounds__(kThreads) q4_kernel(Q4Args a) {
       }
       __syncthreads();  // outs is reused by the next item
     }
-    if (tid == 0 && pc < g.nunits) {
+    if (!early && tid == 0 && pc < g.nunits) {
       q4_issue<T, M, S, WMODE>(g, pc, buf, &bars[s], g1, pin);
       pc = q4_next(g, pc + G, G);
     }
@@ -346,19 +362,32 @@ cudaError_t launch_q4_t(const Q4Args& a, cudaStream_t s, int sms) {
 // indexed by the first tail character)
 int q4_min_ell() { return 4; }
 
-cudaError_t launch_q4_sweep(const Q4Args& a, int dtype, cudaStream_t s, int sms) {
+static int q4_flags() {  // LCSB_Q4_FLAGS (A/B only): kQ4* bits, default both
+  static int f = -1;
+  if (f < 0) {
+    const char* e = getenv("LCSB_Q4_FLAGS");
+    f = e ? atoi(e) : (kQ4EarlyIssue | kQ4TailPerm);
+  }
+  return f;
+}
+
+cudaError_t launch_q4_sweep(const Q4Args& a0, int dtype, cudaStream_t s, int sms) {
   static int variant = -1;  // LCSB_Q4_STAGES (A/B only): pipeline stages per CTA
   if (variant < 0) {
     const char* e = getenv("LCSB_Q4_STAGES");
     variant = e ? atoi(e) : 1;
   }
+  Q4Args a = a0;
+  a.flags = q4_flags();
   if (dtype == LCSB_F32) {
     if (variant == 2) return launch_q4_t<float, 2, 2, false>(a, s, sms);
     return launch_q4_t<float, 2, 1, false>(a, s, sms);
   }
   return launch_q4_t<double, 2, 1, false>(a, s, sms);
 }
-cudaError_t launch_q4_wpass(const Q4Args& a, int dtype, cudaStream_t s, int sms) {
+cudaError_t launch_q4_wpass(const Q4Args& a0, int dtype, cudaStream_t s, int sms) {
+  Q4Args a = a0;
+  a.flags = q4_flags();
   return dtype == LCSB_F32 ? launch_q4_t<float, 2, 1, true>(a, s, sms)
                            : launch_q4_t<double, 2, 1, true>(a, s, sms);
 }

@@ -183,6 +183,7 @@ struct Q4Args {
   int ell;
   const unsigned long long* red_in;
   unsigned long long* red_out;
+  int flags;          // kern_q4.cu kQ4* bits (set by launch_q4_*; A/B knobs)
 };
 
 #ifdef __CUDACC__
