@@ -62,13 +62,14 @@ __device__ __forceinline__ double q0_val(double v0, double v1, double v2, double
 constexpr int kThreads = 256;
 constexpr uint64_t kNone = ~0ull;
 
-template <typename T, int M, int S, bool WMODE>
+template <typename T, int M, int S, bool WMODE, int MINB = 1>
 struct QCfg {
   static constexpr uint32_t TT = 1u << (2 * M);  // Q1 outputs per tile
   static constexpr uint32_t WIN = 2 * TT;        // entries per adv_b window
   // W pass: u at the item's stored outputs is staged by TMA too (one Q1 run of T, four Q0 runs
-  // of T/2) when the runs are whole 16-byte multiples
-  static constexpr bool UTMA = WMODE && (TT / 2 * sizeof(T) >= 16);
+  // of T/2) when the runs are whole 16-byte multiples -- except for the 3-CTA/SM W pass, whose
+  // stage holds the windows only and reads u straight from global memory
+  static constexpr bool UTMA = WMODE && MINB < 3 && (TT / 2 * sizeof(T) >= 16);
   static constexpr uint32_t STAGE = 2 * WIN + (UTMA ? 3 * TT : 0);
   static constexpr size_t SMEM =
       (size_t)S * STAGE * sizeof(T) + (size_t)S * sizeof(uint64_t) + (size_t)S * 8 * sizeof(uint64_t);
@@ -424,7 +425,7 @@ __device__ __forceinline__ void qissue(const QGeo& g, const QItem& it, uint64_t 
 
 template <typename T, int M, int S, bool WMODE, int MINB = 1>
 __global__ void __launch_bounds__(kThreads, MINB) bin2q_kernel(Bin2QArgs a) {
-  using C = QCfg<T, M, S, WMODE>;
+  using C = QCfg<T, M, S, WMODE, MINB>;
   constexpr uint32_t TT = C::TT, WIN = C::WIN;
   constexpr uint32_t LOG = 2 * M;
   extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -539,7 +540,7 @@ __global__ void __launch_bounds__(kThreads, MINB) bin2q_kernel(Bin2QArgs a) {
 
 template <typename T, int M, int S, bool WMODE, int MINB = 1>
 cudaError_t launch_q(const Bin2QArgs& a, cudaStream_t s, int sms) {
-  using C = QCfg<T, M, S, WMODE>;
+  using C = QCfg<T, M, S, WMODE, MINB>;
   static uint64_t cap = 0;
   if (cap == 0) {
     cudaError_t e = cudaFuncSetAttribute(bin2q_kernel<T, M, S, WMODE, MINB>,
@@ -565,7 +566,15 @@ cudaError_t launch_q(const Bin2QArgs& a, cudaStream_t s, int sms) {
 
 template <bool WMODE>
 cudaError_t dispatch_q(const Bin2QArgs& a, int dtype, int M, cudaStream_t s, int sms) {
-  if (WMODE && dtype == LCSB_F32 && M == 6) return launch_q<float, 6, 1, true, 2>(a, s, sms);
+  if (WMODE && dtype == LCSB_F32 && M == 6) {
+    static int wv = -1;  // LCSB_BIN2Q_WDIRECT=1 (A/B): u read from global, 3 CTAs/SM
+    if (wv < 0) {
+      const char* e = getenv("LCSB_BIN2Q_WDIRECT");
+      wv = e ? atoi(e) : 0;
+    }
+    if (wv == 1) return launch_q<float, 6, 1, true, 3>(a, s, sms);
+    return launch_q<float, 6, 1, true, 2>(a, s, sms);
+  }
   if (WMODE && dtype == LCSB_F64 && M == 5) return launch_q<double, 5, 1, true, 3>(a, s, sms);
   if (dtype == LCSB_F32) {
     switch (M) {

@@ -129,13 +129,19 @@ __device__ __forceinline__ uint64_t group_min(const Q4Geo& g, uint64_t u) {
 // the group's distinct units in the fixed order (u, s u, c u, c s u); returns the count
 __device__ __forceinline__ int group_units(const Q4Geo& g, uint64_t u, uint64_t (&U)[kGroup]) {
   const uint64_t cand[kGroup] = {u, digit_swap(u), unit_comp(g, u), unit_comp(g, digit_swap(u))};
-  int n = 0;
+  int n = 1;
+  U[0] = u;
 #pragma unroll
-  for (int k = 0; k < kGroup; ++k) {
+  for (int k = 1; k < kGroup; ++k) {
     bool dup = false;
 #pragma unroll
     for (int j = 0; j < k; ++j) dup = dup || (cand[j] == cand[k]);
-    if (!dup) U[n++] = cand[k];
+    if (!dup) {  // U[n++] = cand[k], with constant indices (U stays in registers)
+#pragma unroll
+      for (int p = 1; p <= k; ++p)
+        if (n == p) U[p] = cand[k];
+      ++n;
+    }
   }
   return n;
 }
@@ -234,19 +240,27 @@ __global__ void __launch_bounds__(kThreads) q4_kernel(Q4Args a) {
     }
   }
 
+  static_assert(TT == kThreads, "one tail per thread and unit");
+  const uint32_t i = tail_of((uint32_t)tid, (a.flags & kQ4TailPerm) != 0);
+  const uint32_t i2 = (uint32_t)digit_swap(i);  // this tail's offset in the swapped unit
+  const uint32_t offU = (uint32_t)((i & kA4) | ((i & kB4) << 4));
+  const uint32_t offS = (uint32_t)((i2 & kA4) | ((i2 & kB4) << 4));
+  const uint32_t i3 = TT - 1 - i2;  // in the complemented swapped unit
+  const uint32_t offCS = (uint32_t)((i3 & kA4) | ((i3 & kB4) << 4));
   uint32_t it = 0;
   for (uint64_t cu = q4_next(g, blockIdx.x, G); cu < g.nunits; cu = q4_next(g, cu + G, G), ++it) {
     const uint32_t s = it % S;
     T* buf = in + (size_t)s * C::STAGE;
     mbar_wait(&bars[s], (it / S) & 1u);
     __syncthreads();
-    uint64_t U[kGroup];
+    uint64_t U[kGroup] = {0, 0, 0, 0};
     const int n = group_units(g, cu, U);
 
-    const bool perm = (a.flags & kQ4TailPerm) != 0;
-    for (uint32_t j = tid; j < (uint32_t)n * TT; j += kThreads) {
-      const int k = (int)(j / TT);
-      const uint32_t i = tail_of(j % TT, perm);
+    // one tail per thread and unit (TT == kThreads): i and its window offsets are per-thread
+    // constants (hoisted above the item loop)
+#pragma unroll
+    for (int k = 0; k < kGroup; ++k) {  // unrolled: U[] stays in registers
+      if (k >= n) break;
       const uint64_t X = U[k];
       const uint64_t sX = digit_swap(X);
       const uint64_t cX = unit_comp(g, X), csX = unit_comp(g, sX);
@@ -262,11 +276,6 @@ __global__ void __launch_bounds__(kThreads) q4_kernel(Q4Args a) {
         const T* ubC = buf + (size_t)slot_of(U, n, cX) * C::UNIT;
         pu = reinterpret_cast<const double*>(ubC + C::WIN)[TT - 1 - i];
       }
-      const uint32_t i2 = (uint32_t)digit_swap(i);  // this tail's offset in the swapped unit
-      const uint32_t offU = (uint32_t)((i & kA4) | ((i & kB4) << 4));
-      const uint32_t offS = (uint32_t)((i2 & kA4) | ((i2 & kB4) << 4));
-      const uint32_t i3 = TT - 1 - i2;  // in the complemented swapped unit
-      const uint32_t offCS = (uint32_t)((i3 & kA4) | ((i3 & kB4) << 4));
 #pragma unroll
       for (int m = 0; m < (WMODE ? 2 : 1); ++m) {
         const double sh = WMODE ? R[m] : 0.0;  // |N| = 1: shift (d-1) R = R
@@ -312,16 +321,21 @@ __global__ void __launch_bounds__(kThreads) q4_kernel(Q4Args a) {
       // row means of the new table: output rows (h_a < 2, h_b, t >> 4) of the group's units, each
       // summed in Alg. 1's order over its 16 stored values
       constexpr uint32_t NR1 = C::NR + 1;
-      const uint32_t rows = (uint32_t)n * 8 * C::NR;
-      for (uint32_t j = tid; j < rows; j += kThreads) {
-        const uint32_t k = j / (8 * C::NR), jr = j % (8 * C::NR);
-        const uint32_t hh = jr / C::NR, r = jr % C::NR;
+      // 8 NR = 128 rows per unit: threads 0-127 take the even units, 128-255 the odd ones
+      static_assert(8 * C::NR * 2 == kThreads, "two units of rows per pass");
+      const uint32_t jr = (uint32_t)tid % (8 * C::NR), odd = (uint32_t)tid / (8 * C::NR);
+      const uint32_t hh = jr / C::NR, r = jr % C::NR;
+      const uint64_t hx = ((uint64_t)(hh >> 2) << hbit_a) | ((uint64_t)(hh & 3) << hbit_b);
+#pragma unroll
+      for (int k2 = 0; k2 < kGroup; k2 += 2) {
+        const uint32_t k = (uint32_t)k2 + odd;
+        if ((int)k >= n) break;
+        const uint64_t Uk = odd ? U[k2 + 1] : U[k2];
         const T* row = outs + ((k * 8 + hh) * 16) * NR1 + r;
         double sum = 0.0;
 #pragma unroll
         for (int c = 0; c < 16; ++c) sum = sum + (double)row[c * NR1];  // (+ 0.0: exact no-op)
-        const uint64_t hx = ((uint64_t)(hh >> 2) << hbit_a) | ((uint64_t)(hh & 3) << hbit_b);
-        pout[((hx | (U[k] << (4 * M))) >> 4) | r] = 0.0625 * sum;
+        pout[((hx | (Uk << (4 * M))) >> 4) | r] = 0.0625 * sum;
       }
       __syncthreads();  // outs is reused by the next item
     }
