@@ -1,4 +1,5 @@
-// kern_q4.cu -- KS-form sweep (and W pass) for d = 2 strings over sigma = 4 (BASELINE config 3) on
+// kern_q4.cu -- KS-form (and two-array) sweep and W pass for d = 2 strings over sigma = 4
+// (BASELINE config 3) on
 // the complement-folded table, reading each stored entry once per sweep.
 //
 // Recurrence (Eq. ineq3, Alg. 1, reading R1): for the pair
@@ -20,6 +21,11 @@
 //    the tails t.  Every sweep also writes the row means of the table it produces (fp64, one per
 //    stored row, each summed in Alg. 1's order from the stored values in shared memory), and the
 //    sweep two later reads those instead of g2: the ring holds 2 tables + 3 mean arrays.
+//
+// Two-array form (Q4Args::flags & kQ4TwoArray, reading R20): every option reads the
+// previous sweep and h_a != h_b offers no P (the drop-both option), so
+//   h_a == h_b :  v' = 1 + max(0, P1),  h_a != h_b :  v' = max(adv_b, adv_a)
+// with P1 the row means of g1 itself -- the means the previous sweep wrote (ring of 2 suffices).
 //
 // Work unit: a unit is 16^M consecutive tails.  adv_a is adv_b of the string-swapped state:
 // adv_a(h_a, h_b, t) = adv_b(h_b, h_a, swap t); for h_b >= 2 that window is folded -- it is the
@@ -240,6 +246,7 @@ __global__ void __launch_bounds__(kThreads) q4_kernel(Q4Args a) {
     }
   }
 
+  const bool ta = (a.flags & kQ4TwoArray) != 0;
   static_assert(TT == kThreads, "one tail per thread and unit");
   const uint32_t i = tail_of((uint32_t)tid, (a.flags & kQ4TailPerm) != 0);
   const uint32_t i2 = (uint32_t)digit_swap(i);  // this tail's offset in the swapped unit
@@ -278,7 +285,7 @@ __global__ void __launch_bounds__(kThreads) q4_kernel(Q4Args a) {
       }
 #pragma unroll
       for (int m = 0; m < (WMODE ? 2 : 1); ++m) {
-        const double sh = WMODE ? R[m] : 0.0;  // |N| = 1: shift (d-1) R = R
+        const double sh = (WMODE && !ta) ? R[m] : 0.0;  // KS |N| = 1: shift (d-1) R = R
         double bU[2], bS[4];
 #pragma unroll
         for (int h = 0; h < 2; ++h) bU[h] = 0.25 * sum4<T, false, WMODE>(ubX + h * C::WB + offU, sh);
@@ -295,6 +302,8 @@ __global__ void __launch_bounds__(kThreads) q4_kernel(Q4Args a) {
             double v;
             if (ha == hb)
               v = 1.0 + fmax(0.0, pu);
+            else if (ta)
+              v = fmax(bU[ha], bS[hb]);  // two-array: no drop-both option (reading R20)
             else
               v = fmax(fmax(bU[ha], bS[hb]), pu);  // adv_b, adv_a, P
             const int hh = ha * 4 + hb;
@@ -305,7 +314,7 @@ __global__ void __launch_bounds__(kThreads) q4_kernel(Q4Args a) {
               outs[(((uint32_t)k * 8 + hh) * 16 + (i & 15)) * NR1 + (i >> 4)] = (T)v;
             } else {
               const T* uo = ubX + C::WIN + C::PR;
-              wmax[m] = fmax(wmax[m], ((double)uo[hh * TT + i] + 2.0 * R[m]) - v);
+              wmax[m] = fmax(wmax[m], ((double)uo[hh * TT + i] + (ta ? R[m] : 2.0 * R[m])) - v);
             }
           }
         }
@@ -392,7 +401,7 @@ cudaError_t launch_q4_sweep(const Q4Args& a0, int dtype, cudaStream_t s, int sms
     variant = e ? atoi(e) : 1;
   }
   Q4Args a = a0;
-  a.flags = q4_flags();
+  a.flags = q4_flags() | (a0.flags & kQ4TwoArray);
   if (dtype == LCSB_F32) {
     if (variant == 2) return launch_q4_t<float, 2, 2, false>(a, s, sms);
     return launch_q4_t<float, 2, 1, false>(a, s, sms);
@@ -401,7 +410,7 @@ cudaError_t launch_q4_sweep(const Q4Args& a0, int dtype, cudaStream_t s, int sms
 }
 cudaError_t launch_q4_wpass(const Q4Args& a0, int dtype, cudaStream_t s, int sms) {
   Q4Args a = a0;
-  a.flags = q4_flags();
+  a.flags = q4_flags() | (a0.flags & kQ4TwoArray);
   return dtype == LCSB_F32 ? launch_q4_t<float, 2, 1, true>(a, s, sms)
                            : launch_q4_t<double, 2, 1, true>(a, s, sms);
 }

@@ -266,7 +266,7 @@ static int plan_config(const lcsb_config* c, Plan* p, char* why, size_t whylen) 
   p->qK = (sym == 2) ? qK : 0;
   p->qM = (sym == 2) ? qM : 0;
   p->kernel = sym == 2 ? 5 : (sym ? 2 : 1);
-  if (!sym && c->sigma == 4 && c->d == 2 && form == LCSB_FORM_KS && c->ell >= q4_min_ell() &&
+  if (!sym && c->sigma == 4 && c->d == 2 && c->ell >= q4_min_ell() &&
       c->kernel == LCSB_KERNEL_AUTO)
     p->kernel = 3;  // sigma = 4, d = 2 swap-paired TMA kernel (kern_q4.cu)
   else if (p->kernel == 1 && c->kernel == LCSB_KERNEL_AUTO && small_supported(c->sigma, c->d, n))
@@ -821,7 +821,9 @@ static int enqueue_sweeps(lcsb_t* h, int64_t n, cudaStream_t s) {
       Q4Args a;
       memset(&a, 0, sizeof a);
       a.g1 = h->tabs[0][slot_back(h, 0)];
-      a.pin = h->pools[(h->pcur + 2) % 3];   // row means of v_{n-2}
+      // row means of v_{n-2} (KS) / of v_{n-1}, the table this sweep reads (two-array)
+      a.pin = h->pools[(h->form == LCSB_FORM_KS) ? (h->pcur + 2) % 3 : h->pcur];
+      a.flags = (h->form == LCSB_FORM_TWO_ARRAY) ? kQ4TwoArray : 0;
       a.pout = h->pools[(h->pcur + 1) % 3];  // row means of the table written now
       a.dst = h->tabs[0][out];
       a.ell = h->cfg.ell;
@@ -905,6 +907,7 @@ extern "C" int lcsb_bound(lcsb_t* h, lcsb_bound_t* out) {
     memset(&a, 0, sizeof a);
     a.g1 = h->tabs[0][h->cur];
     a.pin = h->pools[h->pcur];  // |N| = 2 reads v_n itself in the W pass (shift 0)
+    a.flags = (h->form == LCSB_FORM_TWO_ARRAY) ? kQ4TwoArray : 0;
     a.ell = h->cfg.ell;
     a.red_in = h->red;
     a.red_out = h->red + 2;

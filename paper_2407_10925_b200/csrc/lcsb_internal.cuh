@@ -183,8 +183,9 @@ struct Q4Args {
   int ell;
   const unsigned long long* red_in;
   unsigned long long* red_out;
-  int flags;          // kern_q4.cu kQ4* bits (set by launch_q4_*; A/B knobs)
+  int flags;          // kQ4TwoArray from the caller; kern_q4.cu adds its A/B bits
 };
+constexpr int kQ4TwoArray = 4;  // Q4Args::flags: two-array form (reading R20)
 
 #ifdef __CUDACC__
 __device__ __forceinline__ double dec_ord(unsigned long long u) {

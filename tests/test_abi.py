@@ -54,6 +54,9 @@ def test_required_bytes_and_validation():
     assert L.lcsb_required_bytes(3, 3, 4, "f64") == 4 * 3 ** 12 * 8 + 256 + 4 * 3 ** 9 * 10 * 8
     # two-array for d = 2, sigma > 2 (reading R20): 2 full tables
     assert L.lcsb_required_bytes(3, 2, 2, "f32", form="two_array") == 2 * 81 * 4 + 256
+    # sigma = 4 two-array runs on q4 too: the same folded tables + row-mean ring as KS
+    assert L.lcsb_required_bytes(4, 2, 8, "f32", form="two_array") == \
+        2 * (1 << 31) * 4 + 256 + 3 * (1 << 27) * 8
     # invalid: two-array for d > 2, d > 16, sigma^(d l) too large, symmetry without binary
     assert L.lcsb_required_bytes(2, 3, 2, "f32", form="two_array") == 0
     assert L.lcsb_required_bytes(3, 2, 2, "f32", form="two_array", symmetry=1) == 0

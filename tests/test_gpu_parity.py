@@ -288,6 +288,30 @@ def test_two_array_sigma3_small_matches_generic(dtype):
     b.destroy()
 
 
+@pytest.mark.parametrize("ell,dtype,sweeps", [(4, "f32", 25), (4, "f64", 25), (5, "f32", 12)])
+def test_q4_two_array_matches_oracle_and_generic(ell, dtype, sweeps):
+    """sigma = 4, d = 2 two-array form on the complement-folded q4 kernel (P from the row means
+    of the table it reads, no drop-both option) against the oracle and the generic kernel."""
+    Lcsb = _lcsb()
+    h = Lcsb(4, 2, ell, dtype=dtype, form="two_array")
+    gk = Lcsb(4, 2, ell, dtype=dtype, form="two_array", kernel="generic")
+    assert h.kernel_in_use == "q4" and gk.kernel_in_use == "generic"
+    run = fo.Run(4, 2, ell, "two_array", dtype)
+    for s in range(1, sweeps + 1):
+        h.sweep(1)
+        gk.sweep(1)
+        run.sweep(1)
+        if s in (1, 2, 3, sweeps):
+            _cmp_tables(h.table(0), run.gens[0], dtype)
+            _cmp_tables(h.table(1), run.prev, dtype)
+            assert np.array_equal(h.table(0), gk.table(0))
+    _cmp_bound(h.bound(), run.bound(), dtype)
+    gb, bb = h.bound(), gk.bound()
+    assert (gb.R_max, gb.E_at_Rmax, gb.bound) == (bb.R_max, bb.E_at_Rmax, bb.bound)
+    h.destroy()
+    gk.destroy()
+
+
 @pytest.mark.parametrize("sigma,ell,printed,line", [(4, 4, 0.589484, 280), (3, 5, 0.665874, 297),
                                                     (5, 4, 0.539129, 280)])
 def test_two_array_sigma_gt2_converges_to_appendix3(sigma, ell, printed, line):
