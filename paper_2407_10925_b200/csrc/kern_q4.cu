@@ -389,7 +389,7 @@ static int q4_flags() {  // LCSB_Q4_FLAGS (A/B only): kQ4* bits, default both
   static int f = -1;
   if (f < 0) {
     const char* e = getenv("LCSB_Q4_FLAGS");
-    f = e ? atoi(e) : (kQ4EarlyIssue | kQ4TailPerm);
+    f = (e ? atoi(e) : (kQ4EarlyIssue | kQ4TailPerm)) & (kQ4EarlyIssue | kQ4TailPerm);
   }
   return f;
 }

@@ -304,10 +304,13 @@ def test_q4_two_array_matches_oracle_and_generic(ell, dtype, sweeps):
         if s in (1, 2, 3, sweeps):
             _cmp_tables(h.table(0), run.gens[0], dtype)
             _cmp_tables(h.table(1), run.prev, dtype)
-            assert np.array_equal(h.table(0), gk.table(0))
+            # fp64: the folded kernel reads complement images, whose sums run in the reverse
+            # order, so it matches the full-table kernels to rounding (bit-exact in fp32)
+            _cmp_tables(h.table(0), gk.table(0), dtype)
     _cmp_bound(h.bound(), run.bound(), dtype)
-    gb, bb = h.bound(), gk.bound()
-    assert (gb.R_max, gb.E_at_Rmax, gb.bound) == (bb.R_max, bb.E_at_Rmax, bb.bound)
+    bb = gk.bound()
+    _cmp_bound(h.bound(), {k: getattr(bb, k) for k in ("R_max", "R_min", "E_at_Rmax", "E_at_Rmin",
+                                                      "bound_at_Rmax", "bound_at_Rmin")}, dtype)
     h.destroy()
     gk.destroy()
 
