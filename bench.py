@@ -172,14 +172,17 @@ def run_ours(args, w, ws, rank, local):
         h.sweep(S)
         if ev is not None:
             ev[1].record(stream)
-        return h.bound()
+        out = h.bound()
+        if ev is not None:
+            ev[2].record(stream)
+        return out
 
     for _ in range(args.warmup):
         b = step()
     if ws > 1:
         torch.distributed.barrier()
     torch.cuda.synchronize()
-    sweep_evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+    sweep_evs = [tuple(torch.cuda.Event(enable_timing=True) for _ in range(3))
                  for _ in range(args.steps)]
     t0 = torch.cuda.Event(enable_timing=True)
     t1 = torch.cuda.Event(enable_timing=True)
@@ -196,7 +199,8 @@ def run_ours(args, w, ws, rank, local):
     if ws > 1:
         torch.distributed.barrier()
     ms_total = t0.elapsed_time(t1)
-    sweep_ms = [s.elapsed_time(e) for s, e in sweep_evs]
+    sweep_ms = [s.elapsed_time(e) for s, e, _ in sweep_evs]
+    bound_ms = statistics.mean(e.elapsed_time(f) for _, e, f in sweep_evs)
     if ws > 1:
         t = torch.tensor([ms_total], device=dev, dtype=torch.float64)
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
@@ -277,6 +281,8 @@ def run_ours(args, w, ws, rank, local):
                         % (stored * (4 if w["dtype"] == "f32" else 8) / 2**30)
             if stored * 4 > 2**27 else "working set L2-resident (latency-bound config)",
             "sweep_ms_per_launch": launch_ms,
+            "bound_ms_per_step": bound_ms,  # lcsb_bound: R reduction + W pass + E
+            "dram_bytes_per_state_update": (traffic / (n_logical / ws)) if traffic else None,
             "bound": b.bound, "bound_at_Rmin": b.bound_at_Rmin,
             "sweeps_per_s": S / (ms_per_step / 1e3),
             "sweep_only_state_updates_per_s": n_logical / (launch_ms / 1e3),

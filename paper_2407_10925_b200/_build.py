@@ -40,17 +40,25 @@ def _compile(src: str, obj: str, inc: list) -> subprocess.CompletedProcess:
                           capture_output=True, text=True)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    """One nvcc -c per source (in parallel), then one shared-library link."""
-    if not force and not stale():
+def _compile_d(src: str, obj: str, inc: list, defines) -> subprocess.CompletedProcess:
+    return subprocess.run([nvcc(), *NVCC_FLAGS, *defines, *inc, "-c", src, "-o", obj],
+                          capture_output=True, text=True)
+
+
+def build(force: bool = False, verbose: bool = False, out: str = SO, defines=()) -> str:
+    """One nvcc -c per source (in parallel), then one shared-library link.  ``out`` / ``defines``
+    (A/B builds only, e.g. build/liblcsb_spin.so with -DLCSB_MBAR_SPIN; loaded through LCSB_SO)."""
+    if out == SO and not defines and not force and not stale():
         return SO
+    os.makedirs(os.path.dirname(os.path.abspath(out)), exist_ok=True)
     from concurrent.futures import ThreadPoolExecutor
     tag = f".tmp{os.getpid()}"
     inc = ["-I", os.path.join(ROOT, "include"), "-I", CSRC]
     objs = [os.path.join(CSRC, s[:-3] + tag + ".o") for s in SOURCES]
     try:
         with ThreadPoolExecutor(max(1, min(len(SOURCES), os.cpu_count() or 1))) as ex:
-            results = list(ex.map(lambda so: _compile(os.path.join(CSRC, so[0]), so[1], inc),
+            results = list(ex.map(lambda so: _compile_d(os.path.join(CSRC, so[0]), so[1], inc,
+                                                        list(defines)),
                                   zip(SOURCES, objs)))
         for src, res in zip(SOURCES, results):
             if res.returncode != 0:
@@ -58,19 +66,19 @@ def build(force: bool = False, verbose: bool = False) -> str:
                 raise RuntimeError(f"nvcc failed compiling {src}")
             if verbose:
                 sys.stderr.write(res.stderr)
-        tmp = SO + tag
+        tmp = out + tag
         res = subprocess.run([nvcc(), "-shared", "-gencode", "arch=compute_100a,code=sm_100a",
                               *objs, "-o", tmp, "-lcudart", "-lnccl"],
                              capture_output=True, text=True)
         if res.returncode != 0:
             sys.stderr.write(res.stdout + res.stderr)
             raise RuntimeError("nvcc failed linking liblcsb.so")
-        os.replace(tmp, SO)
+        os.replace(tmp, out)
     finally:
         for o in objs:
             if os.path.exists(o):
                 os.remove(o)
-    return SO
+    return out
 
 
 if __name__ == "__main__":

@@ -276,14 +276,29 @@ __device__ __forceinline__ void pair_quads(const T* bw, const T* bp, const T* sr
   for (uint32_t qd = threadIdx.x; qd < TT / 4; qd += kThreads) {
     const uint32_t o0 = 4 * qd;
     const uint32_t g = 2 * pairswap32(o0), u = 2 * (TT - 4 - o0);
-    double X1[4], X2[4], A[4], B[4], P1[4], P2[4], Ap[4], Bp[4];
+    double A[4], B[4], Ap[4], Bp[4];
     const bool sx = (qd >> SX) & 1u, sp = (qd >> SP) & 1u;
-    ld4(bw + gbase<TT, MW>(sx ? g + 4 : g), X1);
-    ld4(bw + gbase<TT, MW>(sx ? g : g + 4), X2);
-    ld4(bp + gbase<TT, MP>(sp ? u + 4 : u), P1);
-    ld4(bp + gbase<TT, MP>(sp ? u : u + 4), P2);
-    sel4(sx, X1, X2, A, B);
-    sel4(sp, P1, P2, Ap, Bp);
+    if constexpr (sizeof(T) == 4) {  // select the raw floats, then widen (half the selects)
+      float X1[4], X2[4], P1[4], P2[4], a[4], b[4], ap[4], bpp[4];
+      ld4r(reinterpret_cast<const float*>(bw) + gbase<TT, MW>(sx ? g + 4 : g), X1);
+      ld4r(reinterpret_cast<const float*>(bw) + gbase<TT, MW>(sx ? g : g + 4), X2);
+      ld4r(reinterpret_cast<const float*>(bp) + gbase<TT, MP>(sp ? u + 4 : u), P1);
+      ld4r(reinterpret_cast<const float*>(bp) + gbase<TT, MP>(sp ? u : u + 4), P2);
+      sel4f(sx, X1, X2, a, b);
+      sel4f(sp, P1, P2, ap, bpp);
+      widen4(a, A);
+      widen4(b, B);
+      widen4(ap, Ap);
+      widen4(bpp, Bp);
+    } else {
+      double X1[4], X2[4], P1[4], P2[4];
+      ld4(bw + gbase<TT, MW>(sx ? g + 4 : g), X1);
+      ld4(bw + gbase<TT, MW>(sx ? g : g + 4), X2);
+      ld4(bp + gbase<TT, MP>(sp ? u + 4 : u), P1);
+      ld4(bp + gbase<TT, MP>(sp ? u : u + 4), P2);
+      sel4(sx, X1, X2, A, B);
+      sel4(sp, P1, P2, Ap, Bp);
+    }
     constexpr uint32_t c0 = comp<MW>(0), c1 = comp<MW>(1), c2 = comp<MW>(2), c3 = comp<MW>(3);
     constexpr uint32_t d0 = comp<MP>(0), d1 = comp<MP>(1), d2 = comp<MP>(2), d3 = comp<MP>(3);
     double v[4];

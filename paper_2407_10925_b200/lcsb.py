@@ -13,7 +13,8 @@ from dataclasses import dataclass
 import numpy as np
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-SO_PATH = os.path.join(_PKG, "liblcsb.so")
+# LCSB_SO: an alternative build of the same library (A/B of compile-time variants only)
+SO_PATH = os.environ.get("LCSB_SO") or os.path.join(_PKG, "liblcsb.so")
 
 LCSB_F64, LCSB_F32 = 0, 1
 LCSB_FORM_AUTO, LCSB_FORM_KS, LCSB_FORM_TWO_ARRAY = 0, 1, 2
