@@ -168,15 +168,15 @@ __global__ void __launch_bounds__(kTPB) bin2_kernel(Bin2Args a) {
         // W = (u + R) - F'(u); u is the table itself.  W(psi x) = W(x) exactly (both entries
         // were written with the same value), so only x is evaluated for Q1.
         const double ux = (double)src[xo];
-        wm0 = fmax(wm0, (ux + R0) - v);
-        wm1 = fmax(wm1, (ux + R1) - v);
+        wm0 = dmax(wm0, (ux + R0) - v);
+        wm1 = dmax(wm1, (ux + R1) - v);
         const double uq = (double)src[q0x];
-        wm0 = fmax(wm0, (uq + R0) - q0);
-        wm1 = fmax(wm1, (uq + R1) - q0);
+        wm0 = dmax(wm0, (uq + R0) - q0);
+        wm1 = dmax(wm1, (uq + R1) - q0);
         if (!self) {
           const double uqp = (double)src[q0px];
-          wm0 = fmax(wm0, (uqp + R0) - q0p);
-          wm1 = fmax(wm1, (uqp + R1) - q0p);
+          wm0 = dmax(wm0, (uqp + R0) - q0p);
+          wm1 = dmax(wm1, (uqp + R1) - q0p);
         }
       }
     }
@@ -185,8 +185,8 @@ __global__ void __launch_bounds__(kTPB) bin2_kernel(Bin2Args a) {
   if (WMODE) {
     __shared__ double s0[kTPB / 32], s1[kTPB / 32];
     for (int o = 16; o > 0; o >>= 1) {
-      wm0 = fmax(wm0, __shfl_xor_sync(0xffffffffu, wm0, o));
-      wm1 = fmax(wm1, __shfl_xor_sync(0xffffffffu, wm1, o));
+      wm0 = dmax(wm0, __shfl_xor_sync(0xffffffffu, wm0, o));
+      wm1 = dmax(wm1, __shfl_xor_sync(0xffffffffu, wm1, o));
     }
     const int lane = tid & 31, wid = tid >> 5;
     if (lane == 0) {
@@ -198,8 +198,8 @@ __global__ void __launch_bounds__(kTPB) bin2_kernel(Bin2Args a) {
       wm0 = lane < kTPB / 32 ? s0[lane] : -INFINITY;
       wm1 = lane < kTPB / 32 ? s1[lane] : -INFINITY;
       for (int o = 16; o > 0; o >>= 1) {
-        wm0 = fmax(wm0, __shfl_xor_sync(0xffffffffu, wm0, o));
-        wm1 = fmax(wm1, __shfl_xor_sync(0xffffffffu, wm1, o));
+        wm0 = dmax(wm0, __shfl_xor_sync(0xffffffffu, wm0, o));
+        wm1 = dmax(wm1, __shfl_xor_sync(0xffffffffu, wm1, o));
       }
       if (lane == 0) {
         atomicMax(a.red_out + 0, ord_enc(wm0));

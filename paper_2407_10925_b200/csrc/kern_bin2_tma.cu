@@ -243,8 +243,8 @@ __global__ void __launch_bounds__(kThreads, MINB) bin2_tma_kernel(Bin2Args a) {
       if (WMODE) {
         // W = (u + R) - F'(u); W(psi x) = W(x) exactly (both entries hold the same value)
         const double ux = u_in_smem ? (double)us[o] : (double)runQ1[o];
-        wm0 = fmax(wm0, (ux + R0) - v);
-        wm1 = fmax(wm1, (ux + R1) - v);
+        wm0 = dmax(wm0, (ux + R0) - v);
+        wm1 = dmax(wm1, (ux + R1) - v);
       } else if (OB) {
         ob[o] = (T)v;
         ob[TT + pairswap32(~o & (TT - 1))] = (T)v;
@@ -269,10 +269,10 @@ __global__ void __launch_bounds__(kThreads, MINB) bin2_tma_kernel(Bin2Args a) {
         const double uf = u_in_smem ? (double)us[TT + half * TT + r] : (double)rf[r];
         const double um = u_in_smem ? (double)us[TT + half * TT + TT / 2 + (TT / 2 - 1 - r)]
                                     : (double)rm[TT / 2 - 1 - r];
-        wm0 = fmax(wm0, (uf + R0) - fwd);
-        wm1 = fmax(wm1, (uf + R1) - fwd);
-        wm0 = fmax(wm0, (um + R0) - mir);
-        wm1 = fmax(wm1, (um + R1) - mir);
+        wm0 = dmax(wm0, (uf + R0) - fwd);
+        wm1 = dmax(wm1, (uf + R1) - fwd);
+        wm0 = dmax(wm0, (um + R0) - mir);
+        wm1 = dmax(wm1, (um + R1) - mir);
       } else if (OB) {
         T* q0 = ob + 2 * TT + half * TT;
         q0[r] = (T)fwd;

@@ -168,8 +168,8 @@ __device__ __forceinline__ void sel4(bool s, const double (&x)[4], const double 
 }
 __device__ __forceinline__ void wupd(double u, double f, double R0, double R1, double& w0,
                                      double& w1) {
-  w0 = fmax(w0, (u + R0) - f);
-  w1 = fmax(w1, (u + R1) - f);
+  w0 = dmax(w0, (u + R0) - f);
+  w1 = dmax(w1, (u + R1) - f);
 }
 
 // Each thread takes quads of Q1 outputs o0..o0+3 of tile t (and the same values at psi(t)).

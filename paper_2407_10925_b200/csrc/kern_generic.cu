@@ -164,8 +164,8 @@ __global__ void __launch_bounds__(256) generic_sweep_kernel(GenericArgs a) {
 __device__ inline void block_max2(double w0, double w1, unsigned long long* out) {
   __shared__ double s0[32], s1[32];
   for (int o = 16; o > 0; o >>= 1) {
-    w0 = fmax(w0, __shfl_xor_sync(0xffffffffu, w0, o));
-    w1 = fmax(w1, __shfl_xor_sync(0xffffffffu, w1, o));
+    w0 = dmax(w0, __shfl_xor_sync(0xffffffffu, w0, o));
+    w1 = dmax(w1, __shfl_xor_sync(0xffffffffu, w1, o));
   }
   int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   if (lane == 0) {
@@ -178,8 +178,8 @@ __device__ inline void block_max2(double w0, double w1, unsigned long long* out)
     w0 = lane < nw ? s0[lane] : -INFINITY;
     w1 = lane < nw ? s1[lane] : -INFINITY;
     for (int o = 16; o > 0; o >>= 1) {
-      w0 = fmax(w0, __shfl_xor_sync(0xffffffffu, w0, o));
-      w1 = fmax(w1, __shfl_xor_sync(0xffffffffu, w1, o));
+      w0 = dmax(w0, __shfl_xor_sync(0xffffffffu, w0, o));
+      w1 = dmax(w1, __shfl_xor_sync(0xffffffffu, w1, o));
     }
     if (lane == 0) {
       atomicMax(out + 0, ord_enc(w0));
@@ -211,8 +211,8 @@ __global__ void __launch_bounds__(256) generic_wpass_kernel(GenericArgs a) {
     double v = ld<T>(a.center, x);
     double F0 = g.F_at(a, x, sh0);
     double F1 = ks ? g.F_at(a, x, sh1) : F0;
-    w0 = fmax(w0, (v + dR0) - F0);
-    w1 = fmax(w1, (v + dR1) - F1);
+    w0 = dmax(w0, (v + dR0) - F0);
+    w1 = dmax(w1, (v + dR1) - F1);
   }
   block_max2(w0, w1, a.red_out);
 }

@@ -301,11 +301,11 @@ __global__ void __launch_bounds__(kThreads) q4_kernel(Q4Args a) {
           for (int hb = 0; hb < 4; ++hb) {
             double v;
             if (ha == hb)
-              v = 1.0 + fmax(0.0, pu);
+              v = 1.0 + dmax(0.0, pu);
             else if (ta)
-              v = fmax(bU[ha], bS[hb]);  // two-array: no drop-both option (reading R20)
+              v = dmax(bU[ha], bS[hb]);  // two-array: no drop-both option (reading R20)
             else
-              v = fmax(fmax(bU[ha], bS[hb]), pu);  // adv_b, adv_a, P
+              v = dmax(dmax(bU[ha], bS[hb]), pu);  // adv_b, adv_a, P
             const int hh = ha * 4 + hb;
             if (!WMODE) {
               const uint64_t hx = ((uint64_t)ha << hbit_a) | ((uint64_t)hb << hbit_b);
@@ -314,7 +314,7 @@ __global__ void __launch_bounds__(kThreads) q4_kernel(Q4Args a) {
               outs[(((uint32_t)k * 8 + hh) * 16 + (i & 15)) * NR1 + (i >> 4)] = (T)v;
             } else {
               const T* uo = ubX + C::WIN + C::PR;
-              wmax[m] = fmax(wmax[m], ((double)uo[hh * TT + i] + (ta ? R[m] : 2.0 * R[m])) - v);
+              wmax[m] = dmax(wmax[m], ((double)uo[hh * TT + i] + (ta ? R[m] : 2.0 * R[m])) - v);
             }
           }
         }

@@ -25,8 +25,8 @@ __global__ void red_init_kernel(unsigned long long* red) {
 }
 
 __device__ __forceinline__ void acc(double dd, double& mx, double& mn) {
-  mx = fmax(mx, dd);
-  mn = fmin(mn, dd);
+  mx = dmax(mx, dd);
+  mn = dmin(mn, dd);
 }
 
 template <typename T>
@@ -60,8 +60,8 @@ __global__ void __launch_bounds__(256) rdiff_kernel(const T* __restrict__ a, con
   }
   __shared__ double smx[8], smn[8];
   for (int o = 16; o > 0; o >>= 1) {
-    mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-    mn = fmin(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+    mx = dmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    mn = dmin(mn, __shfl_xor_sync(0xffffffffu, mn, o));
   }
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   if (lane == 0) {
@@ -74,8 +74,8 @@ __global__ void __launch_bounds__(256) rdiff_kernel(const T* __restrict__ a, con
     mx = lane < nw ? smx[lane] : -INFINITY;
     mn = lane < nw ? smn[lane] : INFINITY;
     for (int o = 16; o > 0; o >>= 1) {
-      mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-      mn = fmin(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+      mx = dmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+      mn = dmin(mn, __shfl_xor_sync(0xffffffffu, mn, o));
     }
     if (lane == 0) {
       atomicMax(red + 0, ord_enc(mx));

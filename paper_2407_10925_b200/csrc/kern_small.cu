@@ -211,8 +211,8 @@ __global__ void __launch_bounds__(256) small_kernel(GenericArgs a) {
       const double v = (double)center[x];
       const double F0 = F_small<T, SIG, D>(src, sh0, x, a.ell, headw_top, nullptr, ta);
       const double F1 = ks ? F_small<T, SIG, D>(src, sh1, x, a.ell, headw_top) : F0;
-      w0 = fmax(w0, (v + dR0) - F0);
-      w1 = fmax(w1, (v + dR1) - F1);
+      w0 = dmax(w0, (v + dR0) - F0);
+      w1 = dmax(w1, (v + dR1) - F1);
     }
     block_max2_to(w0, w1, a.red_out);
   }

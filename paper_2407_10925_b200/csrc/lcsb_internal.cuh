@@ -188,6 +188,10 @@ struct Q4Args {
 constexpr int kQ4TwoArray = 4;  // Q4Args::flags: two-array form (reading R20)
 
 #ifdef __CUDACC__
+// max / min by one compare and a select: the iterates and W values are never NaN, so the NaN
+// handling of fmax/fmin (several extra instructions per call in SASS) is dead weight on hot paths
+__device__ __forceinline__ double dmax(double a, double b) { return a > b ? a : b; }
+__device__ __forceinline__ double dmin(double a, double b) { return a < b ? a : b; }
 __device__ __forceinline__ double dec_ord(unsigned long long u) {
   unsigned long long b = (u & 0x8000000000000000ull) ? (u & 0x7fffffffffffffffull) : ~u;
   return __longlong_as_double((long long)b);
@@ -197,8 +201,8 @@ __device__ __forceinline__ double dec_ord(unsigned long long u) {
 __device__ __forceinline__ void block_max2_to(double w0, double w1, unsigned long long* out) {
   __shared__ double s0[32], s1[32];
   for (int o = 16; o > 0; o >>= 1) {
-    w0 = fmax(w0, __shfl_xor_sync(0xffffffffu, w0, o));
-    w1 = fmax(w1, __shfl_xor_sync(0xffffffffu, w1, o));
+    w0 = dmax(w0, __shfl_xor_sync(0xffffffffu, w0, o));
+    w1 = dmax(w1, __shfl_xor_sync(0xffffffffu, w1, o));
   }
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   if (lane == 0) {
@@ -211,8 +215,8 @@ __device__ __forceinline__ void block_max2_to(double w0, double w1, unsigned lon
     w0 = lane < nw ? s0[lane] : -INFINITY;
     w1 = lane < nw ? s1[lane] : -INFINITY;
     for (int o = 16; o > 0; o >>= 1) {
-      w0 = fmax(w0, __shfl_xor_sync(0xffffffffu, w0, o));
-      w1 = fmax(w1, __shfl_xor_sync(0xffffffffu, w1, o));
+      w0 = dmax(w0, __shfl_xor_sync(0xffffffffu, w0, o));
+      w1 = dmax(w1, __shfl_xor_sync(0xffffffffu, w1, o));
     }
     if (lane == 0) {
       atomicMax(out + 0, ord_enc(w0));
