@@ -92,6 +92,11 @@ __device__ __forceinline__ double sum4(const T* p, double sh) {
 }
 
 constexpr int kGroup = 4;  // units per item (u, s u, c u, c s u), deduplicated
+// per-stage item record written by the producer with the loads (the consumers read it after the
+// mbarrier wait instead of recomputing the claim walk and the group): [0] = n | slot bits
+// (kNoItem = end of work), [1..4] = the units
+constexpr int kMeta = 6;
+constexpr uint64_t kNoItem = ~0ull;
 
 template <typename T, int M, int S, bool WMODE = false>
 struct Q4Cfg {
@@ -109,7 +114,8 @@ struct Q4Cfg {
   static constexpr uint32_t NR = TT / 16;
   static constexpr uint32_t OUTS = WMODE ? 0 : kGroup * 8 * 16 * (NR + 1);
   static constexpr size_t SMEM =
-      (size_t)S * STAGE * sizeof(T) + (size_t)OUTS * sizeof(T) + (size_t)S * sizeof(uint64_t);
+      (size_t)S * STAGE * sizeof(T) + (size_t)OUTS * sizeof(T) + (size_t)S * sizeof(uint64_t) +
+      (size_t)S * kMeta * sizeof(uint64_t);
 };
 
 struct Q4Geo {
@@ -170,10 +176,26 @@ __device__ __forceinline__ uint64_t q4_next(const Q4Geo& g, uint64_t c, uint64_t
 
 template <typename T, int M, int S, bool WMODE>
 __device__ __forceinline__ void q4_issue(const Q4Geo& g, uint64_t u, T* buf, uint64_t* bar,
-                                         const T* g1, const double* pin) {
+                                         uint64_t* meta, const T* g1, const double* pin) {
   using C = Q4Cfg<T, M, S, WMODE>;
-  uint64_t U[kGroup];
+  if (u >= g.nunits) {  // no item left: an end marker completes the stage's phase
+    meta[0] = kNoItem;
+    mbar_arrive(bar);
+    return;
+  }
+  uint64_t U[kGroup] = {0, 0, 0, 0};
   const int n = group_units(g, u, U);
+  // slots (2 bits each) of the swapped, complemented-swapped and complemented unit of each unit
+  uint64_t rec = (uint64_t)n;
+#pragma unroll
+  for (int k = 0; k < kGroup; ++k) {
+    const uint64_t X = U[k], sX = digit_swap(X);
+    const uint64_t slots = (uint64_t)slot_of(U, n, sX) | ((uint64_t)slot_of(U, n, unit_comp(g, sX)) << 2) |
+                           ((uint64_t)slot_of(U, n, unit_comp(g, X)) << 4);
+    rec |= slots << (8 + 8 * k);
+    meta[1 + k] = X;
+  }
+  meta[0] = rec;
   uint32_t bytes = 0;
   for (int k = 0; k < n; ++k) {
     bytes += C::WIN * (uint32_t)sizeof(T);
@@ -211,6 +233,7 @@ __global__ void __launch_bounds__(kThreads) q4_kernel(Q4Args a) {
   T* in = reinterpret_cast<T*>(smem_raw);
   T* outs = in + (size_t)S * C::STAGE;  // Q4Cfg::OUTS layout (sweep only)
   uint64_t* bars = reinterpret_cast<uint64_t*>(outs + C::OUTS);
+  uint64_t* metas = bars + S;  // [S][kMeta]
 
   Q4Geo g;
   g.ell = a.ell;
@@ -240,9 +263,10 @@ __global__ void __launch_bounds__(kThreads) q4_kernel(Q4Args a) {
   __syncthreads();
   if (tid == 0) {
     pc = q4_next(g, blockIdx.x, G);
-    for (int s = 0; s < S && pc < g.nunits; ++s) {
-      q4_issue<T, M, S, WMODE>(g, pc, in + (size_t)s * C::STAGE, &bars[s], g1, pin);
-      pc = q4_next(g, pc + G, G);
+    for (int s = 0; s < S; ++s) {
+      q4_issue<T, M, S, WMODE>(g, pc, in + (size_t)s * C::STAGE, &bars[s], metas + s * kMeta, g1,
+                               pin);
+      if (pc < g.nunits) pc = q4_next(g, pc + G, G);
     }
   }
 
@@ -254,14 +278,18 @@ __global__ void __launch_bounds__(kThreads) q4_kernel(Q4Args a) {
   const uint32_t offS = (uint32_t)((i2 & kA4) | ((i2 & kB4) << 4));
   const uint32_t i3 = TT - 1 - i2;  // in the complemented swapped unit
   const uint32_t offCS = (uint32_t)((i3 & kA4) | ((i3 & kB4) << 4));
-  uint32_t it = 0;
-  for (uint64_t cu = q4_next(g, blockIdx.x, G); cu < g.nunits; cu = q4_next(g, cu + G, G), ++it) {
+  for (uint32_t it = 0;; ++it) {
     const uint32_t s = it % S;
     T* buf = in + (size_t)s * C::STAGE;
     mbar_wait(&bars[s], (it / S) & 1u);
-    __syncthreads();
-    uint64_t U[kGroup] = {0, 0, 0, 0};
-    const int n = group_units(g, cu, U);
+    const uint64_t* meta = metas + s * kMeta;
+    const uint64_t rec = meta[0];
+    if (rec == kNoItem) break;
+    const int n = (int)(rec & 7u);
+    uint64_t U[kGroup];
+#pragma unroll
+    for (int k = 0; k < kGroup; ++k) U[k] = meta[1 + k];
+    __syncthreads();  // every thread has the record before the producer may overwrite it
 
     // one tail per thread and unit (TT == kThreads): i and its window offsets are per-thread
     // constants (hoisted above the item loop)
@@ -269,18 +297,18 @@ __global__ void __launch_bounds__(kThreads) q4_kernel(Q4Args a) {
     for (int k = 0; k < kGroup; ++k) {  // unrolled: U[] stays in registers
       if (k >= n) break;
       const uint64_t X = U[k];
-      const uint64_t sX = digit_swap(X);
-      const uint64_t cX = unit_comp(g, X), csX = unit_comp(g, sX);
+      const uint32_t sl = (uint32_t)(rec >> (8 + 8 * k));
+      T* const drow = WMODE ? nullptr : dst + ((X << (4 * M)) + i);
       const T* ubX = buf + (size_t)k * C::UNIT;
-      const T* ubS = buf + (size_t)slot_of(U, n, sX) * C::UNIT;
-      const T* ubCS = buf + (size_t)slot_of(U, n, csX) * C::UNIT;
+      const T* ubS = buf + (size_t)(sl & 3u) * C::UNIT;
+      const T* ubCS = buf + (size_t)((sl >> 2) & 3u) * C::UNIT;
       // P: the mean of the g2 row of these tails (|N| = 2, shift (d-2) R = 0); stored for units
       // whose first tail character is < 2, else the complement unit's, reversed
       double pu;
       if (unit_low(g, X)) {
         pu = reinterpret_cast<const double*>(ubX + C::WIN)[i];
       } else {
-        const T* ubC = buf + (size_t)slot_of(U, n, cX) * C::UNIT;
+        const T* ubC = buf + (size_t)((sl >> 4) & 3u) * C::UNIT;
         pu = reinterpret_cast<const double*>(ubC + C::WIN)[TT - 1 - i];
       }
 #pragma unroll
@@ -308,8 +336,8 @@ __global__ void __launch_bounds__(kThreads) q4_kernel(Q4Args a) {
               v = dmax(dmax(bU[ha], bS[hb]), pu);  // adv_b, adv_a, P
             const int hh = ha * 4 + hb;
             if (!WMODE) {
-              const uint64_t hx = ((uint64_t)ha << hbit_a) | ((uint64_t)hb << hbit_b);
-              dst[hx | ((X << (4 * M)) + i)] = (T)v;
+              // the head bits sit above the tail bits: | == +, so the row pointer is per unit
+              drow[((uint64_t)ha << hbit_a) + ((uint64_t)hb << hbit_b)] = (T)v;
               constexpr uint32_t NR1 = C::NR + 1;
               outs[(((uint32_t)k * 8 + hh) * 16 + (i & 15)) * NR1 + (i >> 4)] = (T)v;
             } else {
@@ -322,9 +350,9 @@ __global__ void __launch_bounds__(kThreads) q4_kernel(Q4Args a) {
     }
     __syncthreads();
     const bool early = (a.flags & kQ4EarlyIssue) != 0;
-    if (early && tid == 0 && pc < g.nunits) {  // the input stage is consumed: refill it now
-      q4_issue<T, M, S, WMODE>(g, pc, buf, &bars[s], g1, pin);
-      pc = q4_next(g, pc + G, G);
+    if (early && tid == 0) {  // the input stage is consumed: refill it now
+      q4_issue<T, M, S, WMODE>(g, pc, buf, &bars[s], metas + s * kMeta, g1, pin);
+      if (pc < g.nunits) pc = q4_next(g, pc + G, G);
     }
     if (!WMODE) {
       // row means of the new table: output rows (h_a < 2, h_b, t >> 4) of the group's units, each
@@ -348,9 +376,9 @@ __global__ void __launch_bounds__(kThreads) q4_kernel(Q4Args a) {
       }
       __syncthreads();  // outs is reused by the next item
     }
-    if (!early && tid == 0 && pc < g.nunits) {
-      q4_issue<T, M, S, WMODE>(g, pc, buf, &bars[s], g1, pin);
-      pc = q4_next(g, pc + G, G);
+    if (!early && tid == 0) {
+      q4_issue<T, M, S, WMODE>(g, pc, buf, &bars[s], metas + s * kMeta, g1, pin);
+      if (pc < g.nunits) pc = q4_next(g, pc + G, G);
     }
   }
   if (WMODE) block_max2_to(wmax[0], wmax[1], a.red_out);
