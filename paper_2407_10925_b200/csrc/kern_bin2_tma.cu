@@ -40,12 +40,10 @@ __device__ __forceinline__ uint32_t pairswap32(uint32_t v) {
   return ((v & 0xAAAAAAAAu) >> 1) | ((v & 0x55555555u) << 1);
 }
 
+// 1 + max(0, cand): the iterates are non-negative, so cand >= 0 and the max is cand (as kern_bin2q.cu)
 __device__ __forceinline__ double q0_val(double v0, double v1, double v2, double v3) {
-  double r = ((v0 + v1) + v2) + v3;
-  double cand = 0.25 * r;
-  double best = 0.0;
-  if (cand > best) best = cand;
-  return 1.0 + best;
+  const double r = ((v0 + v1) + v2) + v3;
+  return 1.0 + 0.25 * r;
 }
 
 constexpr int kThreads = 256;

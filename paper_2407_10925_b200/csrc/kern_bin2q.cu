@@ -50,13 +50,13 @@ __device__ __forceinline__ uint32_t pairswap32(uint32_t v) {
   return ((v & 0xAAAAAAAAu) >> 1) | ((v & 0x55555555u) << 1);
 }
 
-// Q0 output from one row of 4 in the oracle's summation order (Alg. 3 "SameFirstBit")
+// Q0 output from one row of 4 in the oracle's summation order (Alg. 3 "SameFirstBit"):
+// 1 + max(0, cand) with the z = head option's 0 (reading R3).  The iterates are non-negative
+// (v_0 = 0 and F maps non-negative tables to non-negative tables), so cand >= 0 and the max is
+// cand itself: the compare is dropped, the value is unchanged.
 __device__ __forceinline__ double q0_val(double v0, double v1, double v2, double v3) {
-  double r = ((v0 + v1) + v2) + v3;
-  double cand = 0.25 * r;
-  double best = 0.0;
-  if (cand > best) best = cand;
-  return 1.0 + best;
+  const double r = ((v0 + v1) + v2) + v3;
+  return 1.0 + 0.25 * r;
 }
 
 constexpr int kThreads = 256;
@@ -236,10 +236,7 @@ __device__ __forceinline__ void pair_quads_f32(const T* bw, const T* bp, const T
                          0.5f * (Ap[d2] + Ap[d3]), 0.5f * (Ap[d0] + Ap[d1])};
     float v[4];
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      v[k] = bx[k];
-      if (bq[k] > v[k]) v[k] = bq[k];
-    }
+    for (int k = 0; k < 4; ++k) v[k] = fmaxf(bx[k], bq[k]);  // one FMNMX (no NaN, no -0)
     const uint32_t qb = pairswap32(~o0 & (TT - 1) & ~3u);
     float* df = reinterpret_cast<float*>(dst);
     if (oQ1 != kNone) *reinterpret_cast<float4*>(df + oQ1 + o0) = make_float4(v[0], v[1], v[2], v[3]);
