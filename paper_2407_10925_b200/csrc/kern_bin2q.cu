@@ -220,20 +220,24 @@ __device__ __forceinline__ void pair_quads_f32(const T* bw, const T* bp, const T
   for (uint32_t qd = threadIdx.x; qd < TT / 4; qd += kThreads) {
     const uint32_t o0 = 4 * qd;
     const uint32_t g = 2 * pairswap32(o0), u = 2 * (TT - 4 - o0);
-    float X1[4], X2[4], A[4], B[4], P1[4], P2[4], Ap[4], Bp[4];
+    // X1 / X2 hold the groups A (row g/4) and B (row g/4 + 1) in a per-thread order (sx: B
+    // first) that keeps the 128-bit smem loads conflict-free; the pair sums are formed per loaded
+    // group and only they are put back in A/B order (4 selects instead of 8 per window)
+    float X1[4], X2[4], P1[4], P2[4];
     const bool sx = (qd >> SX) & 1u, sp = (qd >> SP) & 1u;
     ld4r(reinterpret_cast<const float*>(bw) + gbase<TT, MW>(sx ? g + 4 : g), X1);
     ld4r(reinterpret_cast<const float*>(bw) + gbase<TT, MW>(sx ? g : g + 4), X2);
     ld4r(reinterpret_cast<const float*>(bp) + gbase<TT, MP>(sp ? u + 4 : u), P1);
     ld4r(reinterpret_cast<const float*>(bp) + gbase<TT, MP>(sp ? u : u + 4), P2);
-    sel4f(sx, X1, X2, A, B);
-    sel4f(sp, P1, P2, Ap, Bp);
     constexpr uint32_t c0 = comp<MW>(0), c1 = comp<MW>(1), c2 = comp<MW>(2), c3 = comp<MW>(3);
     constexpr uint32_t d0 = comp<MP>(0), d1 = comp<MP>(1), d2 = comp<MP>(2), d3 = comp<MP>(3);
-    const float bx[4] = {0.5f * (A[c0] + A[c1]), 0.5f * (B[c0] + B[c1]),
-                         0.5f * (A[c2] + A[c3]), 0.5f * (B[c2] + B[c3])};
-    const float bq[4] = {0.5f * (Bp[d2] + Bp[d3]), 0.5f * (Bp[d0] + Bp[d1]),
-                         0.5f * (Ap[d2] + Ap[d3]), 0.5f * (Ap[d0] + Ap[d1])};
+    const float x1l = 0.5f * (X1[c0] + X1[c1]), x1h = 0.5f * (X1[c2] + X1[c3]);
+    const float x2l = 0.5f * (X2[c0] + X2[c1]), x2h = 0.5f * (X2[c2] + X2[c3]);
+    const float p1l = 0.5f * (P1[d0] + P1[d1]), p1h = 0.5f * (P1[d2] + P1[d3]);
+    const float p2l = 0.5f * (P2[d0] + P2[d1]), p2h = 0.5f * (P2[d2] + P2[d3]);
+    // bx = {A lo, B lo, A hi, B hi}; bq = {Bp hi, Bp lo, Ap hi, Ap lo}
+    const float bx[4] = {sx ? x2l : x1l, sx ? x1l : x2l, sx ? x2h : x1h, sx ? x1h : x2h};
+    const float bq[4] = {sp ? p1h : p2h, sp ? p1l : p2l, sp ? p2h : p1h, sp ? p2l : p1l};
     float v[4];
 #pragma unroll
     for (int k = 0; k < 4; ++k) v[k] = fmaxf(bx[k], bq[k]);  // one FMNMX (no NaN, no -0)
@@ -242,19 +246,21 @@ __device__ __forceinline__ void pair_quads_f32(const T* bw, const T* bp, const T
     if (oQ1 != kNone) *reinterpret_cast<float4*>(df + oQ1 + o0) = make_float4(v[0], v[1], v[2], v[3]);
     if (oQ1p != kNone) *reinterpret_cast<float4*>(df + oQ1p + qb) = make_float4(v[3], v[1], v[2], v[0]);
     double G[4];
-    if (rows_x) {
-      widen4(A, G);
-      q0_group<T, MW, false>(G, g >> 2, TT / 2, src, dst, of, om, nullptr, R0, R1, wm0, wm1);
-      widen4(B, G);
-      q0_group<T, MW, false>(G, (g >> 2) + 1, TT / 2, src, dst, of, om, nullptr, R0, R1, wm0,
+    if (rows_x) {  // X1 is row g/4 + sx, X2 row g/4 + 1 - sx
+      widen4(X1, G);
+      q0_group<T, MW, false>(G, (g >> 2) + sx, TT / 2, src, dst, of, om, nullptr, R0, R1, wm0,
+                             wm1);
+      widen4(X2, G);
+      q0_group<T, MW, false>(G, (g >> 2) + 1 - sx, TT / 2, src, dst, of, om, nullptr, R0, R1, wm0,
                              wm1);
     }
     if (rows_p) {
-      widen4(Ap, G);
-      q0_group<T, MP, false>(G, u >> 2, TT / 2, src, dst, opf, opm, nullptr, R0, R1, wm0, wm1);
-      widen4(Bp, G);
-      q0_group<T, MP, false>(G, (u >> 2) + 1, TT / 2, src, dst, opf, opm, nullptr, R0, R1, wm0,
+      widen4(P1, G);
+      q0_group<T, MP, false>(G, (u >> 2) + sp, TT / 2, src, dst, opf, opm, nullptr, R0, R1, wm0,
                              wm1);
+      widen4(P2, G);
+      q0_group<T, MP, false>(G, (u >> 2) + 1 - sp, TT / 2, src, dst, opf, opm, nullptr, R0, R1,
+                             wm0, wm1);
     }
   }
 }
