@@ -62,6 +62,18 @@ __device__ __forceinline__ double q0_val(double v0, double v1, double v2, double
 constexpr int kThreads = 256;
 constexpr uint64_t kNone = ~0ull;
 
+// output stores: nothing in a sweep re-reads them, so they are streaming stores (st.global.cs,
+// evict-first) that leave L2 to the input windows (A/B at l = 17 fp32: 5.161 -> 5.132 ms;
+// LCSB_BIN2Q_NO_STCS builds the plain stores)
+template <typename V>
+__device__ __forceinline__ void st_out(V* p, V v) {
+#ifndef LCSB_BIN2Q_NO_STCS
+  __stcs(p, v);
+#else
+  *p = v;
+#endif
+}
+
 template <typename T, int M, int S, bool WMODE, int MINB = 1>
 struct QCfg {
   static constexpr uint32_t TT = 1u << (2 * M);  // Q1 outputs per tile
@@ -196,8 +208,8 @@ __device__ __forceinline__ void q0_group(const double (&G)[4], uint32_t r, uint3
     if (om != kNone)
       wupd(us ? (double)us[half_rows + rm] : (double)src[om + rm], mir, R0, R1, wm0, wm1);
   } else {
-    if (of != kNone) dst[of + r] = (T)fwd;
-    if (om != kNone) dst[om + (half_rows - 1 - r)] = (T)mir;
+    if (of != kNone) st_out(dst + of + r, (T)fwd);
+    if (om != kNone) st_out(dst + om + (half_rows - 1 - r), (T)mir);
   }
 }
 
@@ -243,8 +255,10 @@ __device__ __forceinline__ void pair_quads_f32(const T* bw, const T* bp, const T
     for (int k = 0; k < 4; ++k) v[k] = fmaxf(bx[k], bq[k]);  // one FMNMX (no NaN, no -0)
     const uint32_t qb = pairswap32(~o0 & (TT - 1) & ~3u);
     float* df = reinterpret_cast<float*>(dst);
-    if (oQ1 != kNone) *reinterpret_cast<float4*>(df + oQ1 + o0) = make_float4(v[0], v[1], v[2], v[3]);
-    if (oQ1p != kNone) *reinterpret_cast<float4*>(df + oQ1p + qb) = make_float4(v[3], v[1], v[2], v[0]);
+    if (oQ1 != kNone)
+      st_out(reinterpret_cast<float4*>(df + oQ1 + o0), make_float4(v[0], v[1], v[2], v[3]));
+    if (oQ1p != kNone)
+      st_out(reinterpret_cast<float4*>(df + oQ1p + qb), make_float4(v[3], v[1], v[2], v[0]));
     double G[4];
     if (rows_x) {  // X1 is row g/4 + sx, X2 row g/4 + 1 - sx
       widen4(X1, G);
