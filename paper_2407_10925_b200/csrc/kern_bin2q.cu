@@ -404,7 +404,8 @@ __device__ __forceinline__ void qlookup(const QGeo& g, const uint32_t* __restric
 // kNone = not stored).
 template <typename T, int M, bool UTMA>
 __device__ __forceinline__ void qissue(const QGeo& g, const QItem& it, uint64_t tau, T* buf,
-                                       uint64_t* bar, uint64_t* meta, const T* src) {
+                                       uint64_t* bar, uint64_t* meta, const T* src,
+                                       uint32_t hints, uint64_t keep) {
   constexpr uint32_t TT = 1u << (2 * M), LOG = 2 * M;
   uint64_t x0, p0, taup;
   qtile(g, tau, LOG, x0, p0, taup);
@@ -442,15 +443,20 @@ __device__ __forceinline__ void qissue(const QGeo& g, const QItem& it, uint64_t 
     T* dst = buf + k * 2 * TT;
     const T* blk = src + ((uint64_t)(m >> 2) << sh);
     const uint64_t e = w & g.kmask;
+    // L2 policy per piece (quarter_schedule): reloaded soon -> `keep`, else evict-first
+    const uint32_t hb = hints >> (2 * k);
+    const uint64_t pol0 = (hb & 1u) ? keep : kL2EvictFirst, pol1 = (hb & 2u) ? keep : kL2EvictFirst;
+    const uint64_t pol01 = (hb & 3u) ? keep : kL2EvictFirst;
     if ((m & 3u) == 0) {
-      tma_load_1d(dst, blk + e, 2 * TT * (uint32_t)sizeof(T), bar);
+      tma_load_1d_hint(dst, blk + e, 2 * TT * (uint32_t)sizeof(T), bar, pol01);
     } else if ((m & 3u) == 3) {  // tail complement: one contiguous run, read reversed
-      tma_load_1d(dst, blk + ((~e & g.kmask) & ~(2ull * TT - 1)), 2 * TT * (uint32_t)sizeof(T), bar);
+      tma_load_1d_hint(dst, blk + ((~e & g.kmask) & ~(2ull * TT - 1)), 2 * TT * (uint32_t)sizeof(T),
+                       bar, pol01);
     } else {
       const uint64_t f = ((m & 3u) == 1) ? pairswap(e) : pairswap(~e & g.kmask);
       const uint64_t start = (f & ~(4ull * TT - 1)) | (f & TT);
-      tma_load_1d(dst, blk + start, TT * (uint32_t)sizeof(T), bar);
-      tma_load_1d(dst + TT, blk + start + 2 * TT, TT * (uint32_t)sizeof(T), bar);
+      tma_load_1d_hint(dst, blk + start, TT * (uint32_t)sizeof(T), bar, pol0);
+      tma_load_1d_hint(dst + TT, blk + start + 2 * TT, TT * (uint32_t)sizeof(T), bar, pol1);
     }
   }
 }
@@ -497,7 +503,12 @@ __global__ void __launch_bounds__(kThreads, MINB) bin2q_kernel(Bin2QArgs a) {
     if (counter) return (uint64_t)atomicAdd(counter, 1ull);
     return first(prev == ~0ull ? (uint64_t)blockIdx.x : prev + G);
   };
-  auto tile_of = [&](uint64_t c) -> uint64_t { return sched ? (uint64_t)__ldg(sched + c) : c; };
+  auto entry = [&](uint64_t c) -> uint32_t { return sched ? __ldg(sched + c) : (uint32_t)c; };
+  auto tile_of = [&](uint64_t c) -> uint64_t {
+    return sched ? (uint64_t)(__ldg(sched + c) & kQTileMask) : c;
+  };
+  // hint bits only come with a schedule; without one every piece keeps the default policy
+  const uint64_t keep = (a.l2keep != 0) ? kL2EvictLast : kL2EvictNormal;
   uint64_t pc = 0;  // producer cursor (thread 0 only)
   QItem pit;        // its map entries, fetched one item ahead
   if (tid == 0) {
@@ -512,7 +523,9 @@ __global__ void __launch_bounds__(kThreads, MINB) bin2q_kernel(Bin2QArgs a) {
     uint64_t* meta = metas + 8 * s;
     if (pc < nitems) {
       meta[7] = 0;
-      qissue<T, M, C::UTMA>(g, pit, tile_of(pc), sbuf, &bars[s], meta, src);
+      const uint32_t ent = entry(pc);
+      qissue<T, M, C::UTMA>(g, pit, sched ? (uint64_t)(ent & kQTileMask) : (uint64_t)ent, sbuf,
+                            &bars[s], meta, src, sched ? (ent >> kQHintShift) : 0xFu, keep);
       pc = claim(pc);
       if (pc < nitems) qlookup<M>(g, map, tile_of(pc), pit);
     } else {

@@ -720,6 +720,8 @@ static void fill_bin2q(const lcsb_t* h, Bin2QArgs* a, int in_slot, int out_slot)
   a->sched = h->qsched;
   a->nitems = h->qsched_n;
   a->sched_m = h->qM;
+  static const int l2keep = getenv("LCSB_QKEEP") ? atoi(getenv("LCSB_QKEEP")) : 0;  // A/B
+  a->l2keep = l2keep;
   a->counter = h->qcounter;
 }
 

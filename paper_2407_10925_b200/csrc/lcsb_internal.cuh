@@ -138,7 +138,11 @@ struct Bin2QArgs {
   // atomic, so the items in flight stay within about one grid-width of the list; NULL = static
   // round-robin assignment
   unsigned long long* counter;
+  int l2keep;  // policy of the pieces the schedule marks as reloaded soon: 0 normal, 1 evict-last
 };
+// schedule entries: tile index in the low bits, L2 hint bits (one per window piece) at the top
+constexpr int kQHintShift = 28;
+constexpr uint32_t kQTileMask = (1u << kQHintShift) - 1;
 
 __host__ __device__ inline uint64_t pairswap_hd(uint64_t v) {
   return ((v & 0xAAAAAAAAAAAAAAAAull) >> 1) | ((v & 0x5555555555555555ull) << 1);

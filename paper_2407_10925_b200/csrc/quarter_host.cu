@@ -256,6 +256,52 @@ bool quarter_schedule(int ell, int K, int M, const uint32_t* map,
     }
     if (out.size() != E) return false;
   }
+  // L2 eviction hints (bits kQHintShift.. of each entry; see kern_bin2q.cu qissue): for each of
+  // the item's 4 window pieces, set = the piece is loaded again within the next kQHintDist items
+  // of the order (keep it in L2), clear = it is not (load it evict-first, so it does not push out
+  // pieces that will be reused).  Default off (every bit set): measured at l = 17 fp32, the
+  // evict-first loads RAISE the DRAM reads (20.65 -> 21.9 GB) and the sweep time (5.13 -> 5.32 ms)
+  // for every distance tried (800, 1500, 3000; with evict-last for the kept pieces 5.25 ms).
+  // LCSB_QHINT=<distance> (A/B) turns them on.
+  {
+    static const long hint_dist = getenv("LCSB_QHINT") ? atol(getenv("LCSB_QHINT")) : 0;
+    const uint64_t ntiles_all = 1ull << (2 * (ell - 1 - M));
+    const uint64_t kmask = (1ull << (2 * K)) - 1;
+    if (ntiles_all <= (1ull << kQHintShift)) {
+      auto pieces = [&](uint64_t w, uint32_t* pc) {  // as window_pieces above (any version)
+        const uint32_t m = map[w >> (2 * K)];
+        const uint64_t slot = m >> 2, e = w & kmask;
+        uint64_t o0;
+        uint64_t step = T;
+        if ((m & 3u) == 0) {
+          o0 = e;
+        } else if ((m & 3u) == 3u) {
+          o0 = (~e & kmask) & ~(2 * T - 1);
+        } else {
+          const uint64_t f = ((m & 3u) == 1u) ? (pairswap_hd(e) & kmask) : (pairswap_hd(~e & kmask) & kmask);
+          o0 = (f & ~(4 * T - 1)) | (f & T);
+          step = 2 * T;
+        }
+        pc[0] = (uint32_t)((slot << 2) | ((o0 / T) & 3));
+        pc[1] = (uint32_t)((slot << 2) | (((o0 + step) / T) & 3));
+      };
+      std::vector<uint32_t> next_seen(nslots * 4, ~0u);
+      for (size_t c = E; c-- > 0;) {
+        const uint64_t tau = out[c];
+        const uint64_t x0 = q1 + tau * T;
+        const uint64_t p0 = pairswap_hd(~x0 & lmask) & ~(T - 1);
+        uint32_t q[4];
+        pieces(win(x0), q);
+        pieces(win(p0), q + 2);
+        uint32_t bits = 0;
+        for (int k = 0; k < 4; ++k)
+          if (hint_dist <= 0 || (next_seen[q[k]] != ~0u && (long)(next_seen[q[k]] - c) <= hint_dist))
+            bits |= 1u << k;
+        for (int k = 0; k < 4; ++k) next_seen[q[k]] = (uint32_t)c;
+        out[c] = (uint32_t)tau | (bits << kQHintShift);
+      }
+    }
+  }
   cache = out;
   c_ell = ell;
   c_K = K;

@@ -55,6 +55,19 @@ static __device__ __forceinline__ void tma_load_1d(void* dst_smem, const void* s
       "l"(src), "r"(bytes), "r"(smem_u32(bar))
       : "memory");
 }
+// L2 cache policies (the createpolicy encodings CUTLASS names CacheHintSm90::EVICT_*)
+constexpr uint64_t kL2EvictFirst = 0x12F0000000000000ull;
+constexpr uint64_t kL2EvictNormal = 0x1000000000000000ull;
+constexpr uint64_t kL2EvictLast = 0x14F0000000000000ull;
+static __device__ __forceinline__ void tma_load_1d_hint(void* dst_smem, const void* src,
+                                                        uint32_t bytes, uint64_t* bar,
+                                                        uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], "
+      "%2, [%3], %4;" ::"r"(smem_u32(dst_smem)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
+      : "memory");
+}
 static __device__ __forceinline__ void tma_store_1d(void* dst, const void* src_smem, uint32_t bytes) {
   asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst),
                "r"(smem_u32(src_smem)), "r"(bytes)
