@@ -32,8 +32,13 @@ struct SmallConst {
   }();
 };
 
-__host__ __device__ constexpr uint32_t ipow_c(uint32_t b, int e) {
-  return e == 0 ? 1u : b * ipow_c(b, e - 1);
+// iterative (not recursive) so that calls with loop-variable exponents inline and fold once the
+// loops are unrolled; the recursive form stayed a real CALL in SASS (a quarter of config 2's
+// instructions)
+__host__ __device__ __forceinline__ constexpr uint32_t ipow_c(uint32_t b, int e) {
+  uint32_t r = 1;
+  for (int i = 0; i < e; ++i) r *= b;
+  return r;
 }
 
 // mean over the appended characters for the compile-time mask MASK (bit j = string j advances),
@@ -64,14 +69,18 @@ __device__ __forceinline__ double option_mean(const T* __restrict__ src, uint32_
 // ---- pooled-mean layout (per table, per k = |N| >= 2): per row, the masks of popcount k in
 // increasing order, each with sigma^(d-k) values indexed by the unchanged strings' last
 // characters (base sigma, string order)
-__host__ __device__ constexpr int popc_c(int m) { return m ? (m & 1) + popc_c(m >> 1) : 0; }
-__host__ __device__ constexpr int mask_rank(int mask) {  // rank among masks of equal popcount
+__host__ __device__ __forceinline__ constexpr int popc_c(int m) {
+  int c = 0;
+  for (; m; m >>= 1) c += m & 1;
+  return c;
+}
+__host__ __device__ __forceinline__ constexpr int mask_rank(int mask) {  // rank among masks of equal popcount
   int r = 0;
   for (int m = 0; m < mask; ++m)
     if (popc_c(m) == popc_c(mask)) ++r;
   return r;
 }
-__host__ __device__ constexpr int nmasks(int d, int k) {
+__host__ __device__ __forceinline__ constexpr int nmasks(int d, int k) {
   int c = 0;
   for (int m = 0; m < (1 << d); ++m)
     if (popc_c(m) == k) ++c;
@@ -82,7 +91,7 @@ struct PoolRow {  // pooled values per row for |N| = K
   static constexpr uint32_t PER_MASK = ipow_c(SIG, D - K);
   static constexpr uint32_t PER_ROW = (uint32_t)nmasks(D, K) * PER_MASK;
 };
-__host__ __device__ constexpr uint32_t pool_per_row(int sig, int d, int k) {
+__host__ __device__ __forceinline__ constexpr uint32_t pool_per_row(int sig, int d, int k) {
   return (uint32_t)nmasks(d, k) * ipow_c((uint32_t)sig, d - k);
 }
 
