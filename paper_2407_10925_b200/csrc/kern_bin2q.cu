@@ -200,16 +200,18 @@ __device__ __forceinline__ void q0_group(const double (&G)[4], uint32_t r, uint3
                                          double& wm1) {
   const double v0 = G[comp<MODE>(0)], v1 = G[comp<MODE>(1)], v2 = G[comp<MODE>(2)],
                v3 = G[comp<MODE>(3)];
-  const double fwd = q0_val(v0, v1, v2, v3);
-  const double mir = q0_val(v3, v2, v1, v0);
+  // a row run and its mirror run are images of each other, so usually only one is stored:
+  // each value is formed only when its run is (the branches are uniform per item)
   if (WMODE) {
     const uint32_t rm = half_rows - 1 - r;
-    if (of != kNone) wupd(us ? (double)us[r] : (double)src[of + r], fwd, R0, R1, wm0, wm1);
+    if (of != kNone)
+      wupd(us ? (double)us[r] : (double)src[of + r], q0_val(v0, v1, v2, v3), R0, R1, wm0, wm1);
     if (om != kNone)
-      wupd(us ? (double)us[half_rows + rm] : (double)src[om + rm], mir, R0, R1, wm0, wm1);
+      wupd(us ? (double)us[half_rows + rm] : (double)src[om + rm], q0_val(v3, v2, v1, v0), R0,
+           R1, wm0, wm1);
   } else {
-    if (of != kNone) st_out(dst + of + r, (T)fwd);
-    if (om != kNone) st_out(dst + om + (half_rows - 1 - r), (T)mir);
+    if (of != kNone) st_out(dst + of + r, (T)q0_val(v0, v1, v2, v3));
+    if (om != kNone) st_out(dst + om + (half_rows - 1 - r), (T)q0_val(v3, v2, v1, v0));
   }
 }
 

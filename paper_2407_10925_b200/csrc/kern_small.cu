@@ -192,8 +192,7 @@ __global__ void __launch_bounds__(256) small_kernel(GenericArgs a) {
   const T* src[D];
 #pragma unroll
   for (int k = 0; k < D; ++k) src[k] = reinterpret_cast<const T*>(a.src[k]);
-  uint32_t headw_top = 1;
-  for (int i = 0; i < D * (a.ell - 1); ++i) headw_top *= SIG;
+  const uint32_t headw_top = (uint32_t)a.headw_top;  // sigma^(d(l-1)), from the host
   const uint32_t n = (uint32_t)a.n;
   const uint32_t stride = gridDim.x * blockDim.x;
   const bool ta = (a.form == LCSB_FORM_TWO_ARRAY);
@@ -293,8 +292,7 @@ __global__ void __launch_bounds__(SmallPool<SIG, D>::THREADS)
     src[k] = reinterpret_cast<const T*>(a.src[k]);
     pin[k] = a.pin[k];
   }
-  uint32_t headw_top = 1;
-  for (int i = 0; i < D * (a.ell - 1); ++i) headw_top *= SIG;
+  const uint32_t headw_top = (uint32_t)a.headw_top;  // sigma^(d(l-1)), from the host
   const uint32_t nrows = (uint32_t)(a.n / SIGD);
   double zero[D];
 #pragma unroll

@@ -694,6 +694,8 @@ static void fill_generic(const lcsb_t* h, GenericArgs* a) {
   a->ell = h->cfg.ell;
   a->n = h->n_logical;
   a->form = h->form;
+  a->headw_top = 1;
+  for (int i = 0; i < a->d * (a->ell - 1); ++i) a->headw_top *= (uint64_t)a->sigma;
 }
 
 static void fill_bin2(const lcsb_t* h, Bin2Args* a, int shard, int in_slot, int out_slot) {

@@ -63,6 +63,7 @@ struct GenericArgs {
   // |N| = k (k >= 2); pout[k-1] = pooled means of the table written
   const double* pin[kMaxD];
   double* pout[kMaxD];
+  uint64_t headw_top;               // sigma^(d(l-1)): weight of the head digit group
 };
 
 constexpr int kMaxShards = 8;
