@@ -250,6 +250,27 @@ cudaError_t dispatch(const GenericArgs& a, int dtype, cudaStream_t s, int sms, b
   if (a.sigma == 4 && a.d == 2) return launch_pair<4, 2>(a, dtype, s, sms, wpass);
   if (a.sigma == 3 && a.d == 2) return launch_pair<3, 2>(a, dtype, s, sms, wpass);
   if (a.sigma == 2 && a.d == 3) return launch_pair<2, 3>(a, dtype, s, sms, wpass);
+  // compile-time alphabets for the larger Table-3 cells (digit arithmetic by constant divisors
+  // instead of 64-bit division calls)
+  if (a.d == 2) {
+    switch (a.sigma) {
+      case 5: return launch_pair<5, 2>(a, dtype, s, sms, wpass);
+      case 6: return launch_pair<6, 2>(a, dtype, s, sms, wpass);
+      case 7: return launch_pair<7, 2>(a, dtype, s, sms, wpass);
+      case 8: return launch_pair<8, 2>(a, dtype, s, sms, wpass);
+    }
+  }
+  if (a.sigma == 2 && a.d >= 4 && a.d <= 7) {
+    switch (a.d) {
+      case 4: return launch_pair<2, 4>(a, dtype, s, sms, wpass);
+      case 5: return launch_pair<2, 5>(a, dtype, s, sms, wpass);
+      case 6: return launch_pair<2, 6>(a, dtype, s, sms, wpass);
+      case 7: return launch_pair<2, 7>(a, dtype, s, sms, wpass);
+    }
+  }
+  if (a.sigma == 3 && a.d == 4) return launch_pair<3, 4>(a, dtype, s, sms, wpass);
+  if (a.sigma == 4 && a.d == 3) return launch_pair<4, 3>(a, dtype, s, sms, wpass);
+  if (a.sigma == 5 && a.d == 3) return launch_pair<5, 3>(a, dtype, s, sms, wpass);
   return launch_pair<0, 0>(a, dtype, s, sms, wpass);
 }
 
