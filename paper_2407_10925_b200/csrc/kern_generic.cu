@@ -258,10 +258,13 @@ cudaError_t dispatch(const GenericArgs& a, int dtype, cudaStream_t s, int sms, b
       case 6: return launch_pair<6, 2>(a, dtype, s, sms, wpass);
       case 7: return launch_pair<7, 2>(a, dtype, s, sms, wpass);
       case 8: return launch_pair<8, 2>(a, dtype, s, sms, wpass);
+      case 9: return launch_pair<9, 2>(a, dtype, s, sms, wpass);
+      case 10: return launch_pair<10, 2>(a, dtype, s, sms, wpass);
     }
   }
-  if (a.sigma == 2 && a.d >= 4 && a.d <= 7) {
+  if (a.sigma == 2 && a.d >= 4 && a.d <= 8) {
     switch (a.d) {
+      case 8: return launch_pair<2, 8>(a, dtype, s, sms, wpass);
       case 4: return launch_pair<2, 4>(a, dtype, s, sms, wpass);
       case 5: return launch_pair<2, 5>(a, dtype, s, sms, wpass);
       case 6: return launch_pair<2, 6>(a, dtype, s, sms, wpass);
