@@ -231,7 +231,7 @@ __device__ __forceinline__ void pair_quads_f32(const T* bw, const T* bp, const T
   // fp64 or off by less than half an fp32 ulp, so no double rounding; halving and max commute
   // with rounding), so Q1 stays in fp32; only the Q0 rows that are stored widen to fp64 (their
   // four-term sums are not exact in fp32).
-  for (uint32_t qd = threadIdx.x; qd < TT / 4; qd += kThreads) {
+  for (uint32_t qd = threadIdx.x; qd < TT / 4; qd += blockDim.x) {
     const uint32_t o0 = 4 * qd;
     const uint32_t g = 2 * pairswap32(o0), u = 2 * (TT - 4 - o0);
     // X1 / X2 hold the groups A (row g/4) and B (row g/4 + 1) in a per-thread order (sx: B
@@ -292,7 +292,7 @@ __device__ __forceinline__ void pair_quads(const T* bw, const T* bp, const T* sr
   const uint64_t of = meta[3], om = meta[4], opf = meta[5], opm = meta[6];
   const bool rows_x = of != kNone || om != kNone;
   const bool rows_p = !self && (opf != kNone || opm != kNone);
-  for (uint32_t qd = threadIdx.x; qd < TT / 4; qd += kThreads) {
+  for (uint32_t qd = threadIdx.x; qd < TT / 4; qd += blockDim.x) {
     const uint32_t o0 = 4 * qd;
     const uint32_t g = 2 * pairswap32(o0), u = 2 * (TT - 4 - o0);
     double A[4], B[4], Ap[4], Bp[4];
@@ -463,8 +463,8 @@ __device__ __forceinline__ void qissue(const QGeo& g, const QItem& it, uint64_t 
   }
 }
 
-template <typename T, int M, int S, bool WMODE, int MINB = 1>
-__global__ void __launch_bounds__(kThreads, MINB) bin2q_kernel(Bin2QArgs a) {
+template <typename T, int M, int S, bool WMODE, int MINB = 1, int NT = kThreads>
+__global__ void __launch_bounds__(NT, MINB) bin2q_kernel(Bin2QArgs a) {
   using C = QCfg<T, M, S, WMODE, MINB>;
   constexpr uint32_t TT = C::TT, WIN = C::WIN;
   constexpr uint32_t LOG = 2 * M;
@@ -585,17 +585,17 @@ __global__ void __launch_bounds__(kThreads, MINB) bin2q_kernel(Bin2QArgs a) {
   if (WMODE) block_max2_to(wm0, wm1, a.red_out);
 }
 
-template <typename T, int M, int S, bool WMODE, int MINB = 1>
+template <typename T, int M, int S, bool WMODE, int MINB = 1, int NT = kThreads>
 cudaError_t launch_q(const Bin2QArgs& a, cudaStream_t s, int sms) {
   using C = QCfg<T, M, S, WMODE, MINB>;
   static uint64_t cap = 0;
   if (cap == 0) {
-    cudaError_t e = cudaFuncSetAttribute(bin2q_kernel<T, M, S, WMODE, MINB>,
+    cudaError_t e = cudaFuncSetAttribute(bin2q_kernel<T, M, S, WMODE, MINB, NT>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
     if (e != cudaSuccess) return e;
     int per_sm = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, bin2q_kernel<T, M, S, WMODE, MINB>,
-                                                      kThreads, C::SMEM) != cudaSuccess ||
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, bin2q_kernel<T, M, S, WMODE, MINB, NT>,
+                                                      NT, C::SMEM) != cudaSuccess ||
         per_sm < 1) {
       cudaGetLastError();
       per_sm = 1;
@@ -607,7 +607,7 @@ cudaError_t launch_q(const Bin2QArgs& a, cudaStream_t s, int sms) {
       (a.sched && a.sched_m == M) ? a.nitems : (1ull << (2 * (a.ell - 1 - M)));
   uint64_t blocks = cap < ntiles ? cap : ntiles;
   if (blocks < 1) blocks = 1;
-  bin2q_kernel<T, M, S, WMODE, MINB><<<(unsigned)blocks, kThreads, C::SMEM, s>>>(a);
+  bin2q_kernel<T, M, S, WMODE, MINB, NT><<<(unsigned)blocks, NT, C::SMEM, s>>>(a);
   return cudaGetLastError();
 }
 
@@ -620,6 +620,8 @@ cudaError_t dispatch_q(const Bin2QArgs& a, int dtype, int M, cudaStream_t s, int
       wv = e ? atoi(e) : 0;
     }
     if (wv == 1) return launch_q<float, 6, 1, true, 3>(a, s, sms);
+    // LCSB_BIN2Q_WDIRECT=2 (A/B): one 512-thread CTA per SM with two stages (prefetch overlap)
+    if (wv == 2) return launch_q<float, 6, 2, true, 1, 512>(a, s, sms);
     return launch_q<float, 6, 1, true, 2>(a, s, sms);
   }
   if (WMODE && dtype == LCSB_F64 && M == 5) return launch_q<double, 5, 1, true, 3>(a, s, sms);
