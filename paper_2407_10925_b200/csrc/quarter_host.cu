@@ -2,6 +2,7 @@
 // DESIGN.md §6): stored sizes, the block map, and the L2 item schedule of the sweep.
 #include <stdlib.h>
 
+#include <algorithm>
 #include <mutex>
 #include <vector>
 
@@ -255,6 +256,16 @@ bool quarter_schedule(int ell, int K, int M, const uint32_t* map,
       }
     }
     if (out.size() != E) return false;
+    // LCSB_QSPREAD=P (A/B): permute each wave by j -> (j P) mod kWave, so the items that share a
+    // piece (adjacent after the greedy growth) are claimed apart in time instead of together
+    static const long spread = getenv("LCSB_QSPREAD") ? atol(getenv("LCSB_QSPREAD")) : 0;
+    if (spread > 1) {
+      std::vector<uint32_t> w(kWave);
+      for (size_t w0 = 0; w0 + (size_t)kWave <= E; w0 += (size_t)kWave) {
+        for (int j = 0; j < kWave; ++j) w[(size_t)((long)j * spread % kWave)] = out[w0 + j];
+        std::copy(w.begin(), w.end(), out.begin() + (long)w0);
+      }
+    }
   }
   // L2 eviction hints (bits kQHintShift.. of each entry; see kern_bin2q.cu qissue): for each of
   // the item's 4 window pieces, set = the piece is loaded again within the next kQHintDist items
