@@ -31,6 +31,8 @@ WORKLOADS = {
     "config1": dict(sigma=2, d=2, ell=8, dtype="f64", form="two_array", sweeps=500),
     "config2": dict(sigma=3, d=3, ell=4, dtype="f64", form="ks", sweeps=300),
     "config3": dict(sigma=4, d=2, ell=8, dtype="f32", form="ks", sweeps=100),
+    # config 3's shape in the two-array form (d = 2, any sigma: DESIGN.md reading R20)
+    "config3ta": dict(sigma=4, d=2, ell=8, dtype="f32", form="two_array", sweeps=100),
     "config4": dict(sigma=2, d=2, ell=17, dtype="f32", form="two_array", sweeps=50),
     # l = 18: 2 x 128 GiB fp32 half tables, sharded over the ranks (needs >= 2 GPUs)
     "config5": dict(sigma=2, d=2, ell=18, dtype="f32", form="two_array", sweeps=30),
@@ -351,7 +353,9 @@ def _parallel_apply_at(fo, w, src, idx, cores):
     from concurrent.futures import ThreadPoolExecutor
     parts = [idx[i::cores] for i in range(cores)]
     with ThreadPoolExecutor(cores) as ex:  # ctypes releases the GIL during the C call
-        list(ex.map(lambda p: fo.apply_F_at(w["sigma"], w["d"], w["ell"], src, p), parts))
+        two = (w["form"] == "two_array")  # d = 2: no drop-both option (reading R20)
+        list(ex.map(lambda p: fo.apply_F_at(w["sigma"], w["d"], w["ell"], src, p,
+                                            two_array=two), parts))
 
 
 class _JsonOnlyStdout:
