@@ -36,6 +36,12 @@
 // reversed).  From these it computes all stored outputs of the four units (h_a in {0,1}, every
 // h_b): every stored window is read exactly once per sweep, every stored entry written once:
 // 2 x (stored table) + 2 x (stored means) bytes per sweep, 4.5 B per logical state in fp32.
+//
+// Pipeline: a persistent grid (3 CTAs/SM); thread 0 walks this CTA's items (every G-th unit that
+// is the smallest of its group), issues the TMA loads of the next item as soon as the current
+// stage is consumed, and publishes the item's record (its units and the slots of their swapped /
+// complemented partners) in shared memory with the loads; an end-of-work record completes the
+// stage's mbarrier phase with a plain arrive.  Each thread owns one tail of every unit.
 #include <math.h>
 #include <stdlib.h>
 
