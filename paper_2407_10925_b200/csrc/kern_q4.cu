@@ -334,8 +334,8 @@ __global__ void __launch_bounds__(kThreads) q4_kernel(Q4Args a) {
 #pragma unroll
           for (int hb = 0; hb < 4; ++hb) {
             double v;
-            if (ha == hb)
-              v = 1.0 + dmax(0.0, pu);
+            if (ha == hb)  // 1 + max(0, P): P is a mean of non-negative iterates, so P >= 0
+              v = 1.0 + pu;
             else if (ta)
               v = dmax(bU[ha], bS[hb]);  // two-array: no drop-both option (reading R20)
             else
