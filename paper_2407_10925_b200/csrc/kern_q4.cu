@@ -104,7 +104,7 @@ constexpr int kGroup = 4;  // units per item (u, s u, c u, c s u), deduplicated
 constexpr int kMeta = 6;
 constexpr uint64_t kNoItem = ~0ull;
 
-template <typename T, int M, int S, bool WMODE = false>
+template <typename T, int M, int S, bool WMODE = false, bool GR = false>
 struct Q4Cfg {
   static constexpr uint32_t TT = 1u << (4 * M);  // tails per unit
   static constexpr uint32_t WB = 4 * TT;         // g1 entries per adv_b window
@@ -118,7 +118,8 @@ struct Q4Cfg {
   // 16 values are 16 "c-rows" apart: [unit][head pair (8)][c][NR + 1] (NR = TT/16 rows per
   // head pair, +1 pad: stores and in-order row reads are bank-conflict-free)
   static constexpr uint32_t NR = TT / 16;
-  static constexpr uint32_t OUTS = WMODE ? 0 : kGroup * 8 * 16 * (NR + 1);
+  // GR: no staging -- the row means re-read the just-written rows from global memory (L2)
+  static constexpr uint32_t OUTS = (WMODE || GR) ? 0 : kGroup * 8 * 16 * (NR + 1);
   static constexpr size_t SMEM =
       (size_t)S * STAGE * sizeof(T) + (size_t)OUTS * sizeof(T) + (size_t)S * sizeof(uint64_t) +
       (size_t)S * kMeta * sizeof(uint64_t);
@@ -231,9 +232,34 @@ __device__ __forceinline__ void q4_issue(const Q4Geo& g, uint64_t u, T* buf, uin
   }
 }
 
-template <typename T, int M, int S, bool WMODE>
-__global__ void __launch_bounds__(kThreads) q4_kernel(Q4Args a) {
-  using C = Q4Cfg<T, M, S, WMODE>;
+// sum of the 16 values of a row in order (Alg. 1: c = (c1, c2) lexicographic), read from global
+// memory through L2 only (.cg: the rows were written by this CTA before the barrier)
+template <typename T>
+__device__ __forceinline__ double row16_sum(const T* p) {
+  double sum = 0.0;
+  if constexpr (sizeof(T) == 4) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const float4 v = __ldcg(reinterpret_cast<const float4*>(p) + q);
+      sum = sum + (double)v.x;
+      sum = sum + (double)v.y;
+      sum = sum + (double)v.z;
+      sum = sum + (double)v.w;
+    }
+  } else {
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const double2 v = __ldcg(reinterpret_cast<const double2*>(p) + q);
+      sum = sum + v.x;
+      sum = sum + v.y;
+    }
+  }
+  return sum;
+}
+
+template <typename T, int M, int S, bool WMODE, bool GR = false>
+__global__ void __launch_bounds__(kThreads, GR ? 4 : (WMODE ? 1 : 3)) q4_kernel(Q4Args a) {
+  using C = Q4Cfg<T, M, S, WMODE, GR>;
   constexpr uint32_t TT = C::TT;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   T* in = reinterpret_cast<T*>(smem_raw);
@@ -344,8 +370,10 @@ __global__ void __launch_bounds__(kThreads) q4_kernel(Q4Args a) {
             if (!WMODE) {
               // the head bits sit above the tail bits: | == +, so the row pointer is per unit
               drow[((uint64_t)ha << hbit_a) + ((uint64_t)hb << hbit_b)] = (T)v;
-              constexpr uint32_t NR1 = C::NR + 1;
-              outs[(((uint32_t)k * 8 + hh) * 16 + (i & 15)) * NR1 + (i >> 4)] = (T)v;
+              if constexpr (!GR) {
+                constexpr uint32_t NR1 = C::NR + 1;
+                outs[(((uint32_t)k * 8 + hh) * 16 + (i & 15)) * NR1 + (i >> 4)] = (T)v;
+              }
             } else {
               const T* uo = ubX + C::WIN + C::PR;
               wmax[m] = dmax(wmax[m], ((double)uo[hh * TT + i] + (ta ? R[m] : 2.0 * R[m])) - v);
@@ -374,10 +402,14 @@ __global__ void __launch_bounds__(kThreads) q4_kernel(Q4Args a) {
         const uint32_t k = (uint32_t)k2 + odd;
         if ((int)k >= n) break;
         const uint64_t Uk = odd ? U[k2 + 1] : U[k2];
-        const T* row = outs + ((k * 8 + hh) * 16) * NR1 + r;
         double sum = 0.0;
+        if constexpr (GR) {
+          sum = row16_sum<T>(dst + (hx | (Uk << (4 * M))) + 16 * r);
+        } else {
+          const T* row = outs + ((k * 8 + hh) * 16) * NR1 + r;
 #pragma unroll
-        for (int c = 0; c < 16; ++c) sum = sum + (double)row[c * NR1];  // (+ 0.0: exact no-op)
+          for (int c = 0; c < 16; ++c) sum = sum + (double)row[c * NR1];  // (+ 0.0: exact no-op)
+        }
         pout[((hx | (Uk << (4 * M))) >> 4) | r] = 0.0625 * sum;
       }
       __syncthreads();  // outs is reused by the next item
@@ -390,17 +422,17 @@ __global__ void __launch_bounds__(kThreads) q4_kernel(Q4Args a) {
   if (WMODE) block_max2_to(wmax[0], wmax[1], a.red_out);
 }
 
-template <typename T, int M, int S, bool WMODE>
+template <typename T, int M, int S, bool WMODE, bool GR = false>
 cudaError_t launch_q4_t(const Q4Args& a, cudaStream_t s, int sms) {
-  using C = Q4Cfg<T, M, S, WMODE>;
+  using C = Q4Cfg<T, M, S, WMODE, GR>;
   static uint64_t cap = 0;
   if (cap == 0) {
-    cudaError_t e = cudaFuncSetAttribute(q4_kernel<T, M, S, WMODE>,
+    cudaError_t e = cudaFuncSetAttribute(q4_kernel<T, M, S, WMODE, GR>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
     if (e != cudaSuccess) return e;
     int per_sm = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, q4_kernel<T, M, S, WMODE>, kThreads,
-                                                      C::SMEM) != cudaSuccess ||
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, q4_kernel<T, M, S, WMODE, GR>,
+                                                      kThreads, C::SMEM) != cudaSuccess ||
         per_sm < 1) {
       cudaGetLastError();
       per_sm = 1;
@@ -409,7 +441,7 @@ cudaError_t launch_q4_t(const Q4Args& a, cudaStream_t s, int sms) {
   }
   const uint64_t nunits = 1ull << (4 * (a.ell - 1) - 4 * M);
   uint64_t blocks = cap < nunits ? cap : nunits;
-  q4_kernel<T, M, S, WMODE><<<(unsigned)blocks, kThreads, C::SMEM, s>>>(a);
+  q4_kernel<T, M, S, WMODE, GR><<<(unsigned)blocks, kThreads, C::SMEM, s>>>(a);
   return cudaGetLastError();
 }
 
@@ -436,8 +468,15 @@ cudaError_t launch_q4_sweep(const Q4Args& a0, int dtype, cudaStream_t s, int sms
   }
   Q4Args a = a0;
   a.flags = q4_flags() | (a0.flags & kQ4TwoArray);
+  static int grows = -1;  // LCSB_Q4_GROWS (A/B): row means re-read from global, 4 CTAs/SM
+  if (grows < 0) {
+    const char* e = getenv("LCSB_Q4_GROWS");
+    grows = e ? atoi(e) : 0;
+  }
   if (dtype == LCSB_F32) {
     if (variant == 2) return launch_q4_t<float, 2, 2, false>(a, s, sms);
+    if (grows == 1) return launch_q4_t<float, 2, 1, false, true>(a, s, sms);
+    if (grows == 2) return launch_q4_t<float, 2, 2, false, true>(a, s, sms);
     return launch_q4_t<float, 2, 1, false>(a, s, sms);
   }
   return launch_q4_t<double, 2, 1, false>(a, s, sms);
