@@ -322,15 +322,11 @@ __device__ __forceinline__ void pair_quads(const T* bw, const T* bp, const T* sr
     constexpr uint32_t d0 = comp<MP>(0), d1 = comp<MP>(1), d2 = comp<MP>(2), d3 = comp<MP>(3);
     double v[4];
     // adv_b(x) and adv_b(psi x) = adv_a(x), each (g[c=0] + g[c=1]) / 2 in the oracle's order
-    const double bx[4] = {0.5 * (A[c0] + A[c1]), 0.5 * (B[c0] + B[c1]), 0.5 * (A[c2] + A[c3]),
-                          0.5 * (B[c2] + B[c3])};
-    const double bq[4] = {0.5 * (Bp[d2] + Bp[d3]), 0.5 * (Bp[d0] + Bp[d1]),
-                          0.5 * (Ap[d2] + Ap[d3]), 0.5 * (Ap[d0] + Ap[d1])};
+    // max(s/2, t/2) = max(s, t)/2 exactly (halving is exact and monotone): one multiply per output
+    const double tx[4] = {A[c0] + A[c1], B[c0] + B[c1], A[c2] + A[c3], B[c2] + B[c3]};
+    const double tq[4] = {Bp[d2] + Bp[d3], Bp[d0] + Bp[d1], Ap[d2] + Ap[d3], Ap[d0] + Ap[d1]};
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      v[k] = bx[k];
-      if (bq[k] > v[k]) v[k] = bq[k];
-    }
+    for (int k = 0; k < 4; ++k) v[k] = 0.5 * dmax(tx[k], tq[k]);
     // psi(o0 + k) sits at oQ1p + qb + pairswap(3 - k): the quad reversed as (3, 1, 2, 0)
     const uint32_t qb = pairswap32(~o0 & (TT - 1) & ~3u);
     if (WMODE) {
