@@ -274,6 +274,9 @@ cudaError_t dispatch(const GenericArgs& a, int dtype, cudaStream_t s, int sms, b
   if (a.sigma == 3 && a.d == 4) return launch_pair<3, 4>(a, dtype, s, sms, wpass);
   if (a.sigma == 4 && a.d == 3) return launch_pair<4, 3>(a, dtype, s, sms, wpass);
   if (a.sigma == 5 && a.d == 3) return launch_pair<5, 3>(a, dtype, s, sms, wpass);
+  if (a.sigma == 6 && a.d == 3) return launch_pair<6, 3>(a, dtype, s, sms, wpass);
+  if (a.sigma == 4 && a.d == 4) return launch_pair<4, 4>(a, dtype, s, sms, wpass);
+  if (a.sigma == 3 && a.d == 8) return launch_pair<3, 8>(a, dtype, s, sms, wpass);
   return launch_pair<0, 0>(a, dtype, s, sms, wpass);
 }
 
