@@ -127,6 +127,24 @@ def test_generic_ks_matches_oracle(sigma, d, ell, dtype, sweeps):
     h.destroy()
 
 
+@pytest.mark.parametrize("sigma,d,ell", [
+    (5, 2, 2), (6, 2, 2), (7, 2, 1), (8, 2, 1), (9, 2, 1), (2, 6, 1), (2, 7, 1), (2, 8, 1),
+    (3, 4, 1), (4, 3, 1), (5, 3, 1), (6, 3, 1), (4, 4, 1), (3, 8, 1)])
+def test_generic_compile_time_alphabets_match_oracle(sigma, d, ell):
+    """Every compile-time (sigma, d) instantiation of the generic kernel (kern_generic.cu) against
+    the oracle: tables of every ring slot and the bound after 15 KS sweeps, fp64."""
+    Lcsb = _lcsb()
+    h = Lcsb(sigma, d, ell, dtype="f64", form="ks")
+    assert h.kernel_in_use == "generic"
+    run = fo.Run(sigma, d, ell, "ks", "f64")
+    h.sweep(15)
+    run.sweep(15)
+    for k in range(d):
+        _cmp_tables(h.table(k), run.gens[k], "f64")
+    _cmp_bound(h.bound(), run.bound(), "f64")
+    h.destroy()
+
+
 @pytest.mark.parametrize("ell,dtype", [(4, "f32"), (4, "f64"), (5, "f32")])
 def test_q4_kernel_matches_oracle(ell, dtype):
     """sigma = 4, d = 2, KS form: the complement-folded, swap/complement-grouped TMA kernel against
