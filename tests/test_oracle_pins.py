@@ -410,3 +410,111 @@ def test_f32_storage_drift_small():
     b = fo.feasible_triplet(2, 2, 6, 150, form="two_array", dtype="f32")["bound_at_Rmax"]
     assert abs(a - b) / a < 2e-5
     assert math.isfinite(b)
+
+
+# ---------------------------------------------------------------- best-so-far (Alg. 2 l.2, 8-10)
+#
+# Alg. 2 and Alg. 5 start from the triplet (v_0, 0, 0)
+# (line 2 / line 4) and replace it whenever R - E >= r - eps (line 8 / line 11: ">=", so a
+# tie replaces).  The oracle reports best as a bound: d * best (KS) or 2 best / (1 + best)
+# (two-array, reading R10).
+
+def _ell1_ks_exact_bounds(sweeps):
+    """Exact (R, E) after every sweep of Alg. 2 at sigma = d = 2, l = 1, from the hand
+    specialisation above (x = v[00] = v[11], y = v[01] = v[10], m = (x + y)/2).  Line 6 with
+    d = 2, F(v + R, v): a same-head state takes the match (reads the 2nd argument, unshifted,
+    through its 4-entry mean; the z = head option gives 0 <= m), a different-head state averages
+    the 1st argument over its 2 appended characters:
+      W[00] = x + 2R - (1 + m),   W[01] = y + 2R - (m + R)."""
+    xs, ys = _ell1_binary_ks(sweeps)
+    px, py = Fraction(0), Fraction(0)
+    out = []
+    for x, y in zip(xs, ys):
+        m = (x + y) / 2
+        rs = {"max": max(x - px, y - py), "min": min(x - px, y - py)}
+        row = {}
+        for mode, R in rs.items():
+            E = max(Fraction(0), x + 2 * R - (1 + m), y + 2 * R - (m + R))
+            row[mode] = (R, E)
+        out.append(row)
+        px, py = x, y
+    return out
+
+
+def test_best_ell1_ks_exact_every_sweep():
+    """Every sweep's R, E and bound d(R - E) equal the exact rationals; best = d * (the largest
+    R - E so far, or 0 from the initial triplet); best_sweep = the last sweep reaching it."""
+    exact = _ell1_ks_exact_bounds(40)
+    run = fo.Run(2, 2, 1, "ks")
+    best = {"max": (Fraction(0), 0), "min": (Fraction(0), 0)}
+    for n, row in enumerate(exact, start=1):
+        run.sweep()
+        res = run.bound()
+        for mode in ("max", "min"):
+            R, E = row[mode]
+            assert res["R_" + mode] == float(R)
+            assert res["E_at_R" + mode] == pytest.approx(float(E), abs=1e-15)
+            assert res["bound_at_R" + mode] == pytest.approx(float(2 * (R - E)), abs=1e-15)
+            if R - E >= best[mode][0]:
+                best[mode] = (R - E, n)
+            assert res["best_at_R" + mode] == pytest.approx(float(2 * best[mode][0]), abs=1e-15)
+            assert run.best_sweep[mode] == best[mode][1]
+    # converged: 2/(sigma+1) = 2/3 (closed form, PAPER.md:210)
+    assert res["best_at_Rmax"] == pytest.approx(2 / 3, abs=1e-9)
+
+
+def test_best_starts_from_initial_triplet_ks_transient():
+    """KS at l = 10: for the first 20 sweeps every evaluated bound is negative (A.3's
+    "<= 0" transient), so best stays the initial triplet's 0 exactly -- not -inf, not the first
+    evaluated bound -- and best_sweep stays 0."""
+    run = fo.Run(2, 2, 10, "ks")
+    seen = []
+    for _ in range(20):
+        run.sweep()
+        res = run.bound()
+        seen.append(res["bound_at_Rmax"])
+        assert res["bound_at_Rmax"] < 0.0
+        assert res["best_at_Rmax"] == 0.0
+        assert run.best_sweep["max"] == 0
+    assert seen[0] == -2.0          # sweep 1: R = 1 (the b-vector), E = 2
+
+
+def test_best_ties_replace_two_array_ell1():
+    """Two-array l = 1 (exact dyadics): from sweep 1 on R_max - E = 1/2 at every sweep, so
+    the ">=" of Alg. 2 line 8 replaces the triplet every time: best_sweep = the latest sweep.
+    R_min = 0 at sweep 1 gives rho = 0 (a tie with the initial triplet: best_sweep 1, bound 0)."""
+    run = fo.Run(2, 2, 1, "two_array")
+    run.sweep()
+    res = run.bound()
+    assert res["R_max"] == 1.0 and res["E_at_Rmax"] == 0.5
+    assert res["R_min"] == 0.0 and res["E_at_Rmin"] == 0.0
+    assert res["bound_at_Rmin"] == 0.0 and res["best_at_Rmin"] == 0.0
+    assert run.best_sweep == {"max": 1, "min": 1}
+    for k in range(2, 12):
+        run.sweep()
+        res = run.bound()
+        for mode in ("max", "min"):
+            assert res["bound_at_R" + mode] == pytest.approx(2 / 3, abs=1e-15)
+            assert res["best_at_R" + mode] == pytest.approx(2 / 3, abs=1e-15)
+        assert run.best_sweep == {"max": k, "min": k}
+
+
+@pytest.mark.parametrize("form", ["two_array", "ks"])
+def test_best_running_max_to_table2(form):
+    """l = 4, bound after every one of 300 sweeps: best is non-decreasing, equals
+    max(0, every bound so far), and floors to Table 2's 0.758576 for both R
+    readings."""
+    run = fo.Run(2, 2, 4, form)
+    running = {"max": 0.0, "min": 0.0}
+    last = {"max": 0.0, "min": 0.0}
+    for _ in range(300):
+        run.sweep()
+        res = run.bound()
+        for mode in ("max", "min"):
+            b = res["best_at_R" + mode]
+            running[mode] = max(running[mode], res["bound_at_R" + mode])
+            assert b >= last[mode]
+            assert b == pytest.approx(running[mode], abs=1e-15)
+            last[mode] = b
+    assert fo.floor6(last["max"]) == 0.758576
+    assert fo.floor6(last["min"]) == 0.758576
