@@ -215,7 +215,10 @@ static int plan_config(const lcsb_config* c, Plan* p, char* why, size_t whylen) 
     if (qK < 2) qK = 2;
   }
   const int qM = qK - 1 < ((c->dtype == LCSB_F32) ? 6 : 5) ? qK - 1 : ((c->dtype == LCSB_F32) ? 6 : 5);
-  const bool quarter_ok = sym_ok && !sharded && qK >= 2 && qK <= c->ell - 1 && c->ell - qK <= 16;
+  // the item schedule packs a tile index into kQHintShift bits, so the tiles of 4^qM must number
+  // at most 2^kQHintShift (larger counts would alias tiles)
+  const bool quarter_ok = sym_ok && !sharded && qK >= 2 && qK <= c->ell - 1 && c->ell - qK <= 16 &&
+                          2 * (c->ell - 1 - qM) <= kQHintShift;
   int sym = c->symmetry;
   if (sym < 0) sym = (quarter_ok && c->ell >= kQuarterAutoEll) ? 2 : (sym_ok ? 1 : 0);
   if (sym == 1 && !sym_ok) {
@@ -227,7 +230,8 @@ static int plan_config(const lcsb_config* c, Plan* p, char* why, size_t whylen) 
   if (sym == 2 && !quarter_ok) {
     snprintf(why, whylen,
              "the quarter table needs the two-array binary form, the AUTO kernel, no sharding "
-             "and 2 <= block_log4 <= ell - 1 (ell - block_log4 <= 16)");
+             "and 2 <= block_log4 <= ell - 1 (ell - block_log4 <= 16, at most 2^28 tiles of "
+             "4^(block_log4 - 1))");
     return LCSB_EINVAL;
   }
   if (sym < 0 || sym > 2) {

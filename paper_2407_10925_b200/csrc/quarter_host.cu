@@ -64,6 +64,8 @@ bool quarter_schedule(int ell, int K, int M, const uint32_t* map,
   static int c_ell = 0, c_K = 0, c_M = 0;  // (A/B: LCSB_QSCHED=1 / 2 is read once per process)
   static std::vector<uint32_t> cache;
   std::lock_guard<std::mutex> lock(mu);
+  // entries hold the tile index in kQHintShift bits (plan_config rejects larger tile counts)
+  if (2 * (ell - 1 - M) > kQHintShift) return false;
   if (c_ell == ell && c_K == K && c_M == M) {
     out = cache;
     return true;

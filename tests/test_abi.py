@@ -64,6 +64,13 @@ def test_required_bytes_and_validation():
     assert L.lcsb_required_bytes(2, 2, 40, "f32") == 0
     assert L.lcsb_required_bytes(3, 2, 2, "f32", symmetry=1) == 0
     assert L.lcsb_required_bytes(2, 2, 1, "f32", symmetry=1) == 0
+    # quarter table: the item schedule packs tile indices in 28 bits, so tiles of 4^(K-1) must
+    # number <= 2^28: l = 17 with block_log4 = 2 (4^15 tiles) is rejected, while
+    # block_log4 = 3 (4^14 tiles) and the auto block_log4 = 7 are accepted
+    assert L.lcsb_required_bytes(2, 2, 17, "f32", symmetry=2, block_log4=2) == 0
+    assert L.lcsb_required_bytes(2, 2, 17, "f32", symmetry=2, block_log4=3) > 0
+    assert L.lcsb_required_bytes(2, 2, 17, "f32", symmetry=2, block_log4=7) > 0
+    assert L.lcsb_required_bytes(2, 2, 18, "f32", symmetry=2, block_log4=3) == 0
 
 
 @pytest.mark.skipif(has_cuda(), reason="checks the no-GPU failure path")
