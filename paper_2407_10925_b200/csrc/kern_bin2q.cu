@@ -34,6 +34,12 @@
 //    one of the two is written.
 //  => per sweep every logical window of the half table is loaded once (from DRAM ~1.6 x the
 //     stored table at l = 17) and 3/8 of the half table is written.
+//  * Bound pass (WMODE, reading R21): the same item walk without stores; at every stored
+//    output x it reads u[x] (the table the pass reads, = v_n) and v_prev[x] and accumulates
+//    R_max = max(u - v_prev), R_min = min(u - v_prev) (Alg. 5 line 7 / PAPER.md:694) and
+//    D = min(F(u,u) - u) with F(u,u)[x] in fp64 (not rounded to storage), so one pass gives
+//    E = max(0, max W) = max(0, R - D) for both R (W = u + R - F(u,u), PAPER.md:400 with
+//    Alg. 5 line 8): the R reduction and the W pass of the old two-pass bound in one read.
 #include <math.h>
 #include <stdlib.h>
 
@@ -78,11 +84,9 @@ template <typename T, int M, int S, bool WMODE, int MINB = 1>
 struct QCfg {
   static constexpr uint32_t TT = 1u << (2 * M);  // Q1 outputs per tile
   static constexpr uint32_t WIN = 2 * TT;        // entries per adv_b window
-  // W pass: u at the item's stored outputs is staged by TMA too (one Q1 run of T, four Q0 runs
-  // of T/2) when the runs are whole 16-byte multiples -- except for the 3-CTA/SM W pass, whose
-  // stage holds the windows only and reads u straight from global memory
-  static constexpr bool UTMA = WMODE && MINB < 3 && (TT / 2 * sizeof(T) >= 16);
-  static constexpr uint32_t STAGE = 2 * WIN + (UTMA ? 3 * TT : 0);
+  // the stage holds the item's two windows; the bound pass reads u and v_prev at the outputs
+  // straight from global memory (streaming loads, issued before the window reads)
+  static constexpr uint32_t STAGE = 2 * WIN;
   static constexpr size_t SMEM =
       (size_t)S * STAGE * sizeof(T) + (size_t)S * sizeof(uint64_t) + (size_t)S * 8 * sizeof(uint64_t);
 };
@@ -178,10 +182,25 @@ __device__ __forceinline__ void sel4(bool s, const double (&x)[4], const double 
     b[k] = s ? x[k] : y[k];
   }
 }
-__device__ __forceinline__ void wupd(double u, double f, double R0, double R1, double& w0,
-                                     double& w1) {
-  w0 = dmax(w0, (u + R0) - f);
-  w1 = dmax(w1, (u + R1) - f);
+// bound pass accumulators at one stored output: u = v_n[x], p = v_{n-1}[x], f = F(u,u)[x]
+struct BAcc {
+  double rmax, rmin, dmin;
+};
+__device__ __forceinline__ void bacc(double u, double p, double f, BAcc& b) {
+  const double dd = u - p;
+  b.rmax = dmax(b.rmax, dd);
+  b.rmin = dmin(b.rmin, dd);
+  b.dmin = dmin(b.dmin, f - u);
+}
+// streaming 4-entry load in the storage type (widened at use)
+__device__ __forceinline__ void ld4s(const float* p, float (&v)[4]) {
+  const float4 f = __ldcs(reinterpret_cast<const float4*>(p));
+  v[0] = f.x; v[1] = f.y; v[2] = f.z; v[3] = f.w;
+}
+__device__ __forceinline__ void ld4s(const double* p, double (&v)[4]) {
+  const double2 a = __ldcs(reinterpret_cast<const double2*>(p));
+  const double2 b = __ldcs(reinterpret_cast<const double2*>(p) + 1);
+  v[0] = a.x; v[1] = a.y; v[2] = b.x; v[3] = b.y;
 }
 
 // Each thread takes quads of Q1 outputs o0..o0+3 of tile t (and the same values at psi(t)).
@@ -192,12 +211,11 @@ __device__ __forceinline__ void wupd(double u, double f, double R0, double R1, d
 // (the complemented tail, row read reversed).  So each window entry is read from smem and
 // widened to fp64 once.  The A/B load order alternates across threads so each 128-bit smem load
 // is conflict-free (2-way for permuted x windows).
-// us != nullptr (W pass): u of the row run at us[r], of the mirror run at us[half_rows + ...]
+// bound pass (WMODE): src = u = v_n, prev = v_{n-1}; nothing is stored
 template <typename T, int MODE, bool WMODE>
 __device__ __forceinline__ void q0_group(const double (&G)[4], uint32_t r, uint32_t half_rows,
                                          const T* src, T* dst, uint64_t of, uint64_t om,
-                                         const T* us, double R0, double R1, double& wm0,
-                                         double& wm1) {
+                                         const T* prev, BAcc& ba) {
   const double v0 = G[comp<MODE>(0)], v1 = G[comp<MODE>(1)], v2 = G[comp<MODE>(2)],
                v3 = G[comp<MODE>(3)];
   // a row run and its mirror run are images of each other, so usually only one is stored:
@@ -205,10 +223,11 @@ __device__ __forceinline__ void q0_group(const double (&G)[4], uint32_t r, uint3
   if (WMODE) {
     const uint32_t rm = half_rows - 1 - r;
     if (of != kNone)
-      wupd(us ? (double)us[r] : (double)src[of + r], q0_val(v0, v1, v2, v3), R0, R1, wm0, wm1);
+      bacc((double)__ldcs(src + of + r), (double)__ldcs(prev + of + r), q0_val(v0, v1, v2, v3),
+           ba);
     if (om != kNone)
-      wupd(us ? (double)us[half_rows + rm] : (double)src[om + rm], q0_val(v3, v2, v1, v0), R0,
-           R1, wm0, wm1);
+      bacc((double)__ldcs(src + om + rm), (double)__ldcs(prev + om + rm),
+           q0_val(v3, v2, v1, v0), ba);
   } else {
     if (of != kNone) st_out(dst + of + r, (T)q0_val(v0, v1, v2, v3));
     if (om != kNone) st_out(dst + om + (half_rows - 1 - r), (T)q0_val(v3, v2, v1, v0));
@@ -224,8 +243,7 @@ __device__ __forceinline__ void pair_quads_f32(const T* bw, const T* bp, const T
   const uint64_t of = meta[3], om = meta[4], opf = meta[5], opm = meta[6];
   const bool rows_x = of != kNone || om != kNone;
   const bool rows_p = !self && (opf != kNone || opm != kNone);
-  const double R0 = 0.0, R1 = 0.0;
-  double wm0 = 0.0, wm1 = 0.0;
+  BAcc ba;  // unused by the sweep
   // fp32 storage, sweep: the Q1 value round32(max(0.5 (x0 + x1), 0.5 (y0 + y1))) of fp64
   // arithmetic equals the same expression evaluated in fp32 (a two-term fp32 sum is exact in
   // fp64 or off by less than half an fp32 ulp, so no double rounding; halving and max commute
@@ -264,27 +282,23 @@ __device__ __forceinline__ void pair_quads_f32(const T* bw, const T* bp, const T
     double G[4];
     if (rows_x) {  // X1 is row g/4 + sx, X2 row g/4 + 1 - sx
       widen4(X1, G);
-      q0_group<T, MW, false>(G, (g >> 2) + sx, TT / 2, src, dst, of, om, nullptr, R0, R1, wm0,
-                             wm1);
+      q0_group<T, MW, false>(G, (g >> 2) + sx, TT / 2, src, dst, of, om, nullptr, ba);
       widen4(X2, G);
-      q0_group<T, MW, false>(G, (g >> 2) + 1 - sx, TT / 2, src, dst, of, om, nullptr, R0, R1, wm0,
-                             wm1);
+      q0_group<T, MW, false>(G, (g >> 2) + 1 - sx, TT / 2, src, dst, of, om, nullptr, ba);
     }
     if (rows_p) {
       widen4(P1, G);
-      q0_group<T, MP, false>(G, (u >> 2) + sp, TT / 2, src, dst, opf, opm, nullptr, R0, R1, wm0,
-                             wm1);
+      q0_group<T, MP, false>(G, (u >> 2) + sp, TT / 2, src, dst, opf, opm, nullptr, ba);
       widen4(P2, G);
-      q0_group<T, MP, false>(G, (u >> 2) + 1 - sp, TT / 2, src, dst, opf, opm, nullptr, R0, R1,
-                             wm0, wm1);
+      q0_group<T, MP, false>(G, (u >> 2) + 1 - sp, TT / 2, src, dst, opf, opm, nullptr, ba);
     }
   }
 }
 
 template <typename T, uint32_t TT, int MW, int MP, bool WMODE>
 __device__ __forceinline__ void pair_quads(const T* bw, const T* bp, const T* src, T* dst,
-                                           const uint64_t* meta, bool self, const T* us,
-                                           double R0, double R1, double& wm0, double& wm1) {
+                                           const uint64_t* meta, bool self, const T* prev,
+                                           BAcc& ba) {
   // A/B load order select bits (bank conflicts): modes 0 and 3 (contiguous, possibly reversed)
   // alternate on bit 2, the pairswapped modes on bit 0 (x window) / bit 1 (psi window)
   constexpr uint32_t SX = (MW == 0 || MW == 3) ? 2 : 0, SP = (MP == 0 || MP == 3) ? 2 : 1;
@@ -295,6 +309,18 @@ __device__ __forceinline__ void pair_quads(const T* bw, const T* bp, const T* sr
   for (uint32_t qd = threadIdx.x; qd < TT / 4; qd += blockDim.x) {
     const uint32_t o0 = 4 * qd;
     const uint32_t g = 2 * pairswap32(o0), u = 2 * (TT - 4 - o0);
+    // psi(o0 + k) sits at oQ1p + qb + pairswap(3 - k): the quad reversed as (3, 1, 2, 0)
+    const uint32_t qb = pairswap32(~o0 & (TT - 1) & ~3u);
+    // bound pass: u and v_prev at the quad's stored Q1 outputs, loaded first (their latency
+    // overlaps the window reads and the arithmetic); W(psi x) = W(x), so either copy serves
+    T uu[4] = {0, 0, 0, 0}, pp[4] = {0, 0, 0, 0};  // initialised: keeps them out of local memory
+    if (WMODE) {
+      const uint64_t q = oQ1 != kNone ? oQ1 + o0 : (oQ1p != kNone ? oQ1p + qb : kNone);
+      if (q != kNone) {
+        ld4s(src + q, uu);
+        ld4s(prev + q, pp);
+      }
+    }
     double A[4], B[4], Ap[4], Bp[4];
     const bool sx = (qd >> SX) & 1u, sp = (qd >> SP) & 1u;
     if constexpr (sizeof(T) == 4) {  // select the raw floats, then widen (half the selects)
@@ -327,37 +353,28 @@ __device__ __forceinline__ void pair_quads(const T* bw, const T* bp, const T* sr
     const double tq[4] = {Bp[d2] + Bp[d3], Bp[d0] + Bp[d1], Ap[d2] + Ap[d3], Ap[d0] + Ap[d1]};
 #pragma unroll
     for (int k = 0; k < 4; ++k) v[k] = 0.5 * dmax(tx[k], tq[k]);
-    // psi(o0 + k) sits at oQ1p + qb + pairswap(3 - k): the quad reversed as (3, 1, 2, 0)
-    const uint32_t qb = pairswap32(~o0 & (TT - 1) & ~3u);
     if (WMODE) {
-      // W(psi x) = W(x): both stored copies (psi-fixed blocks) hold the same u
-      double uu[4];
       if (oQ1 != kNone) {
-        ld4(us ? us + o0 : src + oQ1 + o0, uu);
 #pragma unroll
-        for (int k = 0; k < 4; ++k) wupd(uu[k], v[k], R0, R1, wm0, wm1);
+        for (int k = 0; k < 4; ++k) bacc((double)uu[k], (double)pp[k], v[k], ba);
       } else if (oQ1p != kNone) {
-        ld4(us ? us + qb : src + oQ1p + qb, uu);
-        wupd(uu[3], v[0], R0, R1, wm0, wm1);
-        wupd(uu[1], v[1], R0, R1, wm0, wm1);
-        wupd(uu[2], v[2], R0, R1, wm0, wm1);
-        wupd(uu[0], v[3], R0, R1, wm0, wm1);
+        bacc((double)uu[3], (double)pp[3], v[0], ba);
+        bacc((double)uu[1], (double)pp[1], v[1], ba);
+        bacc((double)uu[2], (double)pp[2], v[2], ba);
+        bacc((double)uu[0], (double)pp[0], v[3], ba);
       }
     } else {
       if (oQ1 != kNone) st4(dst + oQ1 + o0, v[0], v[1], v[2], v[3]);
       if (oQ1p != kNone) st4(dst + oQ1p + qb, v[3], v[1], v[2], v[0]);
     }
     // Q0 rows of the four groups
-    const T* ux = us ? us + TT : nullptr;
-    const T* up = us ? us + 2 * TT : nullptr;
     if (rows_x) {
-      q0_group<T, MW, WMODE>(A, g >> 2, TT / 2, src, dst, of, om, ux, R0, R1, wm0, wm1);
-      q0_group<T, MW, WMODE>(B, (g >> 2) + 1, TT / 2, src, dst, of, om, ux, R0, R1, wm0, wm1);
+      q0_group<T, MW, WMODE>(A, g >> 2, TT / 2, src, dst, of, om, prev, ba);
+      q0_group<T, MW, WMODE>(B, (g >> 2) + 1, TT / 2, src, dst, of, om, prev, ba);
     }
     if (rows_p) {
-      q0_group<T, MP, WMODE>(Ap, u >> 2, TT / 2, src, dst, opf, opm, up, R0, R1, wm0, wm1);
-      q0_group<T, MP, WMODE>(Bp, (u >> 2) + 1, TT / 2, src, dst, opf, opm, up, R0, R1, wm0,
-                             wm1);
+      q0_group<T, MP, WMODE>(Ap, u >> 2, TT / 2, src, dst, opf, opm, prev, ba);
+      q0_group<T, MP, WMODE>(Bp, (u >> 2) + 1, TT / 2, src, dst, opf, opm, prev, ba);
     }
   }
 }
@@ -400,10 +417,10 @@ __device__ __forceinline__ void qlookup(const QGeo& g, const uint32_t* __restric
 // metadata: meta[0] = window modes (bits 0-1: window t, 2-3: window psi t, bit 4: self pair),
 // meta[1..6] = stored run starts (Q1 t, Q1 psi t, rows t, mirrors t, rows psi t, mirrors psi t;
 // kNone = not stored).
-template <typename T, int M, bool UTMA>
+template <typename T, int M, bool WMODE = false>
 __device__ __forceinline__ void qissue(const QGeo& g, const QItem& it, uint64_t tau, T* buf,
                                        uint64_t* bar, uint64_t* meta, const T* src,
-                                       uint32_t hints, uint64_t keep) {
+                                       uint32_t hints, uint64_t keep, const T* prev = nullptr) {
   constexpr uint32_t TT = 1u << (2 * M), LOG = 2 * M;
   uint64_t x0, p0, taup;
   qtile(g, tau, LOG, x0, p0, taup);
@@ -419,20 +436,21 @@ __device__ __forceinline__ void qissue(const QGeo& g, const QItem& it, uint64_t 
   meta[4] = qrun(g, it.m[5], ym);
   meta[5] = self ? kNone : qrun(g, it.m[6], ypf);
   meta[6] = self ? kNone : qrun(g, it.m[7], ypm);
-  uint32_t bytes = 2 * 2 * TT * (uint32_t)sizeof(T);
-  if (UTMA) {  // u runs: [Q1 (t if stored, else psi t) | rows t | mirrors t | rows psi t | mirrors]
-    if (meta[1] != kNone || meta[2] != kNone) bytes += TT * (uint32_t)sizeof(T);
-    for (int k = 3; k < 7; ++k)
-      if (meta[k] != kNone) bytes += TT / 2 * (uint32_t)sizeof(T);
-  }
-  mbar_expect_tx(bar, bytes);
-  if (UTMA) {
-    T* us = buf + 4 * TT;
+  mbar_expect_tx(bar, 2 * 2 * TT * (uint32_t)sizeof(T));
+  // bound pass: u and v_prev at the item's stored output runs go to L2 now (bulk prefetch), so
+  // the consumers' direct loads of them, one item later, hit L2
+  if (WMODE && ((TT / 2) * sizeof(T)) % 16 == 0) {
     const uint64_t q = meta[1] != kNone ? meta[1] : meta[2];
-    if (q != kNone) tma_load_1d(us, src + q, TT * (uint32_t)sizeof(T), bar);
+    if (q != kNone) {
+      bulk_prefetch_l2(src + q, TT * (uint32_t)sizeof(T));
+      bulk_prefetch_l2(prev + q, TT * (uint32_t)sizeof(T));
+    }
+#pragma unroll
     for (int k = 3; k < 7; ++k)
-      if (meta[k] != kNone)
-        tma_load_1d(us + TT + (k - 3) * (TT / 2), src + meta[k], TT / 2 * (uint32_t)sizeof(T), bar);
+      if (meta[k] != kNone) {
+        bulk_prefetch_l2(src + meta[k], TT / 2 * (uint32_t)sizeof(T));
+        bulk_prefetch_l2(prev + meta[k], TT / 2 * (uint32_t)sizeof(T));
+      }
   }
 #pragma unroll
   for (int k = 0; k < 2; ++k) {
@@ -484,11 +502,8 @@ __global__ void __launch_bounds__(NT, MINB) bin2q_kernel(Bin2QArgs a) {
   const int tid = threadIdx.x;
   const uint64_t G = gridDim.x;
 
-  double R0 = 0.0, R1 = 0.0, wm0 = -INFINITY, wm1 = -INFINITY;
-  if (WMODE) {
-    R0 = dec_ord(a.red_in[0]);
-    R1 = dec_ord(a.red_in[1]);
-  }
+  BAcc ba{-INFINITY, INFINITY, INFINITY};
+  const T* prev = reinterpret_cast<const T*>(a.prev);
   // items: with a schedule, item c is the tile pair of tile sched[c] (c = blockIdx.x + k G);
   // without one, the pair representatives in tile order
   const uint32_t* sched = (a.sched && a.sched_m == M) ? a.sched : nullptr;
@@ -522,8 +537,8 @@ __global__ void __launch_bounds__(NT, MINB) bin2q_kernel(Bin2QArgs a) {
     if (pc < nitems) {
       meta[7] = 0;
       const uint32_t ent = entry(pc);
-      qissue<T, M, C::UTMA>(g, pit, sched ? (uint64_t)(ent & kQTileMask) : (uint64_t)ent, sbuf,
-                            &bars[s], meta, src, sched ? (ent >> kQHintShift) : 0xFu, keep);
+      qissue<T, M, WMODE>(g, pit, sched ? (uint64_t)(ent & kQTileMask) : (uint64_t)ent, sbuf,
+                          &bars[s], meta, src, sched ? (ent >> kQHintShift) : 0xFu, keep, prev);
       pc = claim(pc);
       if (pc < nitems) qlookup<M>(g, map, tile_of(pc), pit);
     } else {
@@ -550,12 +565,11 @@ __global__ void __launch_bounds__(NT, MINB) bin2q_kernel(Bin2QArgs a) {
     const bool self = (modes & 16u) != 0;
     const T* bw = buf;
     const T* bp = buf + WIN;
-    const T* us = C::UTMA ? buf + 2 * WIN : nullptr;
 #define LCSB_Q1(MW, MP)                                                            \
   if constexpr (sizeof(T) == 4 && !WMODE)                                          \
     pair_quads_f32<T, TT, MW, MP>(bw, bp, src, dst, meta, self);                   \
   else                                                                             \
-    pair_quads<T, TT, MW, MP, WMODE>(bw, bp, src, dst, meta, self, us, R0, R1, wm0, wm1)
+    pair_quads<T, TT, MW, MP, WMODE>(bw, bp, src, dst, meta, self, prev, ba)
     switch (mw * 4 + mp) {
       case 0: LCSB_Q1(0, 0); break;
       case 1: LCSB_Q1(0, 1); break;
@@ -578,7 +592,7 @@ __global__ void __launch_bounds__(NT, MINB) bin2q_kernel(Bin2QArgs a) {
     __syncthreads();  // stage s (data and metadata) is free again
     if (tid == 0) fill((int)s, buf);
   }
-  if (WMODE) block_max2_to(wm0, wm1, a.red_out);
+  if (WMODE) block_red3_to(ba.rmax, ba.rmin, ba.dmin, a.red_out);
 }
 
 template <typename T, int M, int S, bool WMODE, int MINB = 1, int NT = kThreads>
@@ -610,15 +624,15 @@ cudaError_t launch_q(const Bin2QArgs& a, cudaStream_t s, int sms) {
 template <bool WMODE>
 cudaError_t dispatch_q(const Bin2QArgs& a, int dtype, int M, cudaStream_t s, int sms) {
   if (WMODE && dtype == LCSB_F32 && M == 6) {
-    static int wv = -1;  // LCSB_BIN2Q_WDIRECT=1 (A/B): u read from global, 3 CTAs/SM
+    static int wv = -1;  // LCSB_BIN2Q_WDIRECT=1 (A/B): the bound pass at 2 CTAs/SM
     if (wv < 0) {
       const char* e = getenv("LCSB_BIN2Q_WDIRECT");
       wv = e ? atoi(e) : 0;
     }
-    if (wv == 1) return launch_q<float, 6, 1, true, 3>(a, s, sms);
+    if (wv == 1) return launch_q<float, 6, 1, true, 2>(a, s, sms);
     // LCSB_BIN2Q_WDIRECT=2 (A/B): one 512-thread CTA per SM with two stages (prefetch overlap)
     if (wv == 2) return launch_q<float, 6, 2, true, 1, 512>(a, s, sms);
-    return launch_q<float, 6, 1, true, 2>(a, s, sms);
+    return launch_q<float, 6, 1, true, 3>(a, s, sms);
   }
   if (WMODE && dtype == LCSB_F64 && M == 5) return launch_q<double, 5, 1, true, 3>(a, s, sms);
   if (dtype == LCSB_F32) {

@@ -16,11 +16,12 @@
 namespace lcsbk {
 namespace {
 
-__global__ void red_init_kernel(unsigned long long* red) {
+__global__ void red_init_kernel(unsigned long long* red, unsigned min_mask) {
   int i = threadIdx.x;
   if (i < kRedSlots) {
-    // slot 1 is a min (R_min): start at +inf; the others are maxima: start at -inf
-    red[i] = (i == 1) ? ord_enc(INFINITY) : ord_enc(-INFINITY);
+    // minima (slot 1 = R_min; slot 2 = min(F(u) - u) of the one-pass bound) start at +inf, the
+    // maxima at -inf
+    red[i] = ((min_mask >> i) & 1u) ? ord_enc(INFINITY) : ord_enc(-INFINITY);
   }
 }
 
@@ -109,8 +110,8 @@ __global__ void expand_kernel(ExpandTabs tabs, int p, int symmetric, uint64_t nl
 
 }  // namespace
 
-cudaError_t launch_red_init(unsigned long long* red, cudaStream_t s) {
-  red_init_kernel<<<1, 32, 0, s>>>(red);
+cudaError_t launch_red_init(unsigned long long* red, cudaStream_t s, unsigned min_mask) {
+  red_init_kernel<<<1, 32, 0, s>>>(red, min_mask);
   return cudaGetLastError();
 }
 

@@ -878,9 +878,13 @@ extern "C" int lcsb_bound(lcsb_t* h, lcsb_bound_t* out) {
   CU(h, cudaSetDevice(h->device));
   cudaStream_t s = (cudaStream_t)h->cfg.stream;
   const int prev = slot_back(h, 1);
-  CU(h, launch_red_init(h->red, s));
+  // quarter table (two-array binary): ONE pass gives R_max, R_min and D = min(F(u,u) - u); then
+  // E = max(0, max W) = max(0, R - D) for both R (reading R21).  Other kernels: the R
+  // reduction, then the W pass at the known R.
+  const bool one_pass = h->kernel == 5;
+  CU(h, launch_red_init(h->red, s, one_pass ? 6u : 2u));
   h->launches += 1;
-  for (int k = h->first; k < h->first + h->nown; ++k) {
+  for (int k = h->first; !one_pass && k < h->first + h->nown; ++k) {
     CU(h, launch_rdiff(h->tabs[k][h->cur], h->tabs[k][prev], h->n_local, h->cfg.dtype, h->red, s,
                        h->sms));
     h->launches += 1;
@@ -905,8 +909,8 @@ extern "C" int lcsb_bound(lcsb_t* h, lcsb_bound_t* out) {
   } else if (h->kernel == 5) {
     Bin2QArgs a;
     fill_bin2q(h, &a, h->cur, -1);
-    a.red_in = h->red;
-    a.red_out = h->red + 2;
+    a.prev = h->tabs[0][prev];
+    a.red_out = h->red;
     if (a.counter) CU(h, cudaMemsetAsync(a.counter, 0, sizeof(unsigned long long), s));
     CU(h, launch_bin2q_wpass(a, h->cfg.dtype, h->qM, s, h->sms));
     h->launches += 1;
@@ -940,7 +944,12 @@ extern "C" int lcsb_bound(lcsb_t* h, lcsb_bound_t* out) {
                         cudaMemcpyDeviceToHost, s));
   CU(h, cudaStreamSynchronize(s));
   const double R[2] = {ord_dec(h->red_host[0]), ord_dec(h->red_host[1])};
-  const double Wm[2] = {ord_dec(h->red_host[2]), ord_dec(h->red_host[3])};
+  double Wm[2] = {ord_dec(h->red_host[2]), ord_dec(h->red_host[3])};
+  if (one_pass) {  // max W = max(u + R - F(u,u)) = R - min(F(u,u) - u)   (reading R21)
+    const double D = ord_dec(h->red_host[2]);
+    Wm[0] = R[0] - D;
+    Wm[1] = R[1] - D;
+  }
   double E[2], B[2];
   for (int i = 0; i < 2; ++i) {
     E[i] = Wm[i] > 0.0 ? Wm[i] : 0.0;  // E = max(0, max W)

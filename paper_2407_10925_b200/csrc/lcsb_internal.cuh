@@ -123,8 +123,9 @@ __host__ __device__ inline uint64_t global_of_local(uint32_t shard, uint64_t loc
 // (pairswap), 2 = psi = complement o swap (pairswap of the complement; for Q0 blocks the tail
 // complement composed with s), 3 = tail complement t of a same-head block (complement).
 struct Bin2QArgs {
-  const void* src;  // input quarter table
+  const void* src;  // input quarter table (bound pass: v_n)
   void* dst;        // output quarter table (sweep mode)
+  const void* prev; // bound pass: v_{n-1}
   const uint32_t* map;
   int ell;
   int K;
@@ -229,6 +230,40 @@ __device__ __forceinline__ void block_max2_to(double w0, double w1, unsigned lon
     }
   }
 }
+
+// block-wide (max a, min b, min c), one atomic each into out[0] (max), out[1], out[2] (min)
+__device__ __forceinline__ void block_red3_to(double a, double b, double c,
+                                              unsigned long long* out) {
+  __shared__ double s0[32], s1[32], s2[32];
+  for (int o = 16; o > 0; o >>= 1) {
+    a = dmax(a, __shfl_xor_sync(0xffffffffu, a, o));
+    b = dmin(b, __shfl_xor_sync(0xffffffffu, b, o));
+    c = dmin(c, __shfl_xor_sync(0xffffffffu, c, o));
+  }
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  if (lane == 0) {
+    s0[wid] = a;
+    s1[wid] = b;
+    s2[wid] = c;
+  }
+  __syncthreads();
+  if (wid == 0) {
+    const int nw = (blockDim.x + 31) >> 5;
+    a = lane < nw ? s0[lane] : -INFINITY;
+    b = lane < nw ? s1[lane] : INFINITY;
+    c = lane < nw ? s2[lane] : INFINITY;
+    for (int o = 16; o > 0; o >>= 1) {
+      a = dmax(a, __shfl_xor_sync(0xffffffffu, a, o));
+      b = dmin(b, __shfl_xor_sync(0xffffffffu, b, o));
+      c = dmin(c, __shfl_xor_sync(0xffffffffu, c, o));
+    }
+    if (lane == 0) {
+      atomicMax(out + 0, ord_enc(a));
+      atomicMin(out + 1, ord_enc(b));
+      atomicMin(out + 2, ord_enc(c));
+    }
+  }
+}
 #endif
 
 // launchers (return cudaError_t of the launch)
@@ -256,7 +291,8 @@ cudaError_t launch_small(const GenericArgs& a, int dtype, bool wpass, cudaStream
 bool small_pooled_supported(int sigma, int d);
 uint32_t small_pool_per_row(int sigma, int d, int k);  // pooled means per row for |N| = k
 cudaError_t launch_small_pooled(const GenericArgs& a, int dtype, cudaStream_t s, int sms);
-cudaError_t launch_red_init(unsigned long long* red, cudaStream_t s);
+// slots whose bit is set in min_mask start at +inf (minima), the others at -inf (maxima)
+cudaError_t launch_red_init(unsigned long long* red, cudaStream_t s, unsigned min_mask = 2u);
 cudaError_t launch_rdiff(const void* newest, const void* prev, uint64_t n, int dtype,
                          unsigned long long* red, cudaStream_t s, int sms);
 // tabs[k]: the table of shard k (unsharded: tabs[0]); p = log2(shards); qmap != NULL: quarter

@@ -68,6 +68,10 @@ static __device__ __forceinline__ void tma_load_1d_hint(void* dst_smem, const vo
       "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
       : "memory");
 }
+// bulk prefetch of [src, src + bytes) into L2 (no shared memory; bytes a multiple of 16)
+static __device__ __forceinline__ void bulk_prefetch_l2(const void* src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
+}
 static __device__ __forceinline__ void tma_store_1d(void* dst, const void* src_smem, uint32_t bytes) {
   asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst),
                "r"(smem_u32(src_smem)), "r"(bytes)
