@@ -61,7 +61,8 @@ enum {
   LCSB_ECAPACITY = 2, /* not enough device memory; lcsb_last_error() states the bytes needed */
   LCSB_ESTATE = 3,    /* call not valid in the handle's state (e.g. bound before any sweep) */
   LCSB_ECUDA = 4,     /* a CUDA runtime call failed */
-  LCSB_ENCCL = 5      /* an NCCL call of the sharded process mode failed */
+  LCSB_ENCCL = 5      /* a communication call of the sharded process mode failed (NCCL, or a
+                         comm hook returned non-zero) */
 };
 
 /* Device allocation hooks (optional).  alloc returns a device pointer of >= bytes, 256-B
@@ -70,6 +71,26 @@ enum {
  * allocator here. */
 typedef void* (*lcsb_alloc_fn)(size_t bytes, void* stream, void* ctx);
 typedef void (*lcsb_free_fn)(void* ptr, size_t bytes, void* stream, void* ctx);
+
+/* Host communication hooks of the process-sharded mode (optional).  When lcsb_config.comm is
+ * non-NULL the library uses these instead of NCCL: the CUDA IPC handles of the tables are
+ * exchanged with allgather, the per-sweep barrier is "synchronise this handle's stream, then
+ * barrier()" (so lcsb_sweep becomes synchronous), and the bound's 4 reduction scalars cross the
+ * ranks through allreduce_max_u64 (the library encodes minima so that a max serves).  No kernel
+ * ever waits on another rank, so several processes may share one GPU (how the multi-process
+ * path is tested on one device: DESIGN.md §9).  Each hook returns 0 on success; a non-zero return
+ * fails the call with LCSB_ENCCL.  The hooks are called only from the calling thread, inside
+ * collective library calls. */
+typedef struct {
+  /* every rank passes `bytes` bytes at `mine`; on return `all` holds the P contributions in rank
+   * order (P * bytes, host memory) */
+  int (*allgather)(const void* mine, void* all, size_t bytes, void* ctx);
+  /* returns once every rank has entered it */
+  int (*barrier)(void* ctx);
+  /* element-wise maximum over the ranks of n unsigned 64-bit values, in place (host memory) */
+  int (*allreduce_max_u64)(uint64_t* vals, int32_t n, void* ctx);
+  void* ctx;
+} lcsb_comm_hooks;
 
 typedef struct {
   int32_t sigma;    /* alphabet size, >= 2 */
@@ -97,11 +118,12 @@ typedef struct {
    * outputs into the owners' tables (peer stores over NVLink).  Two modes:
    *   virtual_shards = 1: this handle holds all P shards on its own GPU (one-GPU mode, used to
    *                       test the sharded kernels; no communication library involved);
-   *   virtual_shards = 0, P > 1: one process per GPU, this process owns shard `shard`; all P
-   *                       processes pass the same 128-byte ncclUniqueId in nccl_id (from
-   *                       lcsb_nccl_unique_id on one rank).  The library builds its own NCCL
+   *   virtual_shards = 0, P > 1: one process per GPU, this process owns shard `shard`; either
+   *                       all P processes pass the same 128-byte ncclUniqueId in nccl_id (from
+   *                       lcsb_nccl_unique_id on one rank) -- the library builds its own NCCL
    *                       communicator, exchanges CUDA IPC handles of the tables through it, and
-   *                       uses NCCL all-reduces for the per-sweep barrier and the bound.  Every
+   *                       uses NCCL all-reduces on the stream for the per-sweep barrier and the
+   *                       bound -- or all pass comm hooks (below; no NCCL involved).  Every
    *                       process must call create / reset / sweep / bound / destroy collectively. */
   int32_t shards;
   int32_t shard;
@@ -111,6 +133,9 @@ typedef struct {
    * whole or read through the swap permutation; 0 = auto (min(7, l-5) for F32, min(6, l-5)
    * for F64, at least 2).  Must satisfy 2 <= block_log4 <= l - 1. */
   int32_t block_log4;
+  /* process-sharded mode: host communication hooks instead of NCCL (see lcsb_comm_hooks); the
+   * struct must stay valid until lcsb_destroy returns.  NULL = NCCL (nccl_id). */
+  const lcsb_comm_hooks* comm;
 } lcsb_config;
 
 /* Fill *cfg with defaults: sigma=2,d=2,ell=1, F32, AUTO form, R_MAX, symmetry auto, AUTO
@@ -132,7 +157,10 @@ int lcsb_reset(lcsb_t* h);
 
 /* Enqueue n >= 0 sweeps on the handle's stream and return (asynchronous).  One sweep computes
  * v_new = F(v_{n-1}, ..., v_{n-d}) at every state (Eq. ineq3) and rotates the
- * generations (Alg. 2 line 11).  Errors: EINVAL (n < 0), ECUDA (launch failure). */
+ * generations (Alg. 2 line 11).  Process-sharded mode: collective; a barrier precedes the first
+ * sweep (so rank-local table reads made since the last collective call are complete before any
+ * rank overwrites a generation) and follows every sweep.  Errors: EINVAL (n < 0), ECUDA (launch
+ * failure), ENCCL. */
 int lcsb_sweep(lcsb_t* h, int64_t n);
 
 typedef struct {

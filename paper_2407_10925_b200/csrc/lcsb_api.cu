@@ -205,7 +205,12 @@ static int plan_config(const lcsb_config* c, Plan* p, char* why, size_t whylen) 
   const bool sym_ok =
       binary && (form == LCSB_FORM_TWO_ARRAY) && c->ell >= 2 && c->kernel == LCSB_KERNEL_AUTO;
   const int P = c->shards < 1 ? 1 : c->shards;
-  const bool sharded = P > 1 || (c->nccl_id && !c->virtual_shards);
+  const bool has_comm = c->nccl_id || c->comm;
+  if (c->comm && (!c->comm->allgather || !c->comm->barrier || !c->comm->allreduce_max_u64)) {
+    snprintf(why, whylen, "comm hooks need allgather, barrier and allreduce_max_u64");
+    return LCSB_EINVAL;
+  }
+  const bool sharded = P > 1 || (has_comm && !c->virtual_shards);
   // quarter table geometry: blocks of 4^K, tiles of 4^M (M <= K - 1)
   int qK = c->block_log4;
   if (qK <= 0) {
@@ -243,7 +248,7 @@ static int plan_config(const lcsb_config* c, Plan* p, char* why, size_t whylen) 
     snprintf(why, whylen, "shards must be 1, 2, 4 or 8");
     return LCSB_EINVAL;
   }
-  if (P > 1 || (c->nccl_id && !c->virtual_shards)) {
+  if (sharded) {
     if (!sym) {
       snprintf(why, whylen, "sharding needs the complement-folded binary two-array table");
       return LCSB_EINVAL;
@@ -258,8 +263,8 @@ static int plan_config(const lcsb_config* c, Plan* p, char* why, size_t whylen) 
         snprintf(why, whylen, "shard must be in [0, %d)", P);
         return LCSB_EINVAL;
       }
-      if (!c->nccl_id) {
-        snprintf(why, whylen, "process-sharded mode needs nccl_id");
+      if (!has_comm) {
+        snprintf(why, whylen, "process-sharded mode needs nccl_id or comm hooks");
         return LCSB_EINVAL;
       }
     }
@@ -283,7 +288,7 @@ static int plan_config(const lcsb_config* c, Plan* p, char* why, size_t whylen) 
   // process mode also with a single rank when an NCCL id is given (exercises the communicator,
   // the IPC exchange and the collective barrier/bound path on one GPU)
   p->mode = c->virtual_shards ? (P == 1 ? MODE_SINGLE : MODE_VIRTUAL)
-                              : ((P > 1 || c->nccl_id) ? MODE_PROCESS : MODE_SINGLE);
+                              : ((P > 1 || has_comm) ? MODE_PROCESS : MODE_SINGLE);
   p->n_logical = n;
   // q4: complement-folded table (heads h_a < 2 stored, kern_q4.cu)
   p->n_stored = (sym == 2) ? quarter_slots(c->ell, qK) << (2 * qK)
@@ -396,10 +401,47 @@ static void dev_free(lcsb_t* h, void* p, size_t bytes) {
 
 static bool owns(const lcsb_t* h, int k) { return k >= h->first && k < h->first + h->nown; }
 
+static const lcsb_comm_hooks* hooks(const lcsb_t* h) {
+  return h->mode == MODE_PROCESS ? h->cfg.comm : nullptr;
+}
+
 static int barrier(lcsb_t* h) {  // process mode: every rank's preceding work is complete
   if (h->mode != MODE_PROCESS) return LCSB_OK;
+  if (const lcsb_comm_hooks* c = hooks(h)) {  // host hooks: drain the stream, then meet
+    CU(h, cudaStreamSynchronize((cudaStream_t)h->cfg.stream));
+    if (c->barrier(c->ctx) != 0) return set_err(h, LCSB_ENCCL, "comm hook barrier failed");
+    return LCSB_OK;
+  }
   NC(h, ncclAllReduce(h->barrier_buf, h->barrier_buf, 1, ncclInt32, ncclSum, h->comm,
                       (cudaStream_t)h->cfg.stream));
+  return LCSB_OK;
+}
+
+// process mode: element-wise max over the ranks of device reduction slots [first, first + n)
+// (slot 1 = R_min is a minimum: the NCCL path reduces it with ncclMin, the hook path by a max of
+// the complemented encoding)
+static int allreduce_slots(lcsb_t* h, int first, int n, unsigned min_mask) {
+  if (h->mode != MODE_PROCESS) return LCSB_OK;
+  cudaStream_t s = (cudaStream_t)h->cfg.stream;
+  if (const lcsb_comm_hooks* c = hooks(h)) {
+    unsigned long long v[kRedSlots];
+    CU(h, cudaMemcpyAsync(v, h->red + first, n * sizeof(unsigned long long),
+                          cudaMemcpyDeviceToHost, s));
+    CU(h, cudaStreamSynchronize(s));
+    for (int i = 0; i < n; ++i)
+      if ((min_mask >> (first + i)) & 1u) v[i] = ~v[i];
+    if (c->allreduce_max_u64(reinterpret_cast<uint64_t*>(v), n, c->ctx) != 0)
+      return set_err(h, LCSB_ENCCL, "comm hook allreduce_max_u64 failed");
+    for (int i = 0; i < n; ++i)
+      if ((min_mask >> (first + i)) & 1u) v[i] = ~v[i];
+    CU(h, cudaMemcpyAsync(h->red + first, v, n * sizeof(unsigned long long),
+                          cudaMemcpyHostToDevice, s));
+    CU(h, cudaStreamSynchronize(s));
+    return LCSB_OK;
+  }
+  for (int i = 0; i < n; ++i)
+    NC(h, ncclAllReduce(h->red + first + i, h->red + first + i, 1, ncclUint64,
+                        ((min_mask >> (first + i)) & 1u) ? ncclMin : ncclMax, h->comm, s));
   return LCSB_OK;
 }
 
@@ -408,7 +450,7 @@ extern "C" void lcsb_destroy(lcsb_t* h) {
   cudaSetDevice(h->device);
   cudaStream_t s = (cudaStream_t)h->cfg.stream;
   cudaStreamSynchronize(s);
-  if (h->mode == MODE_PROCESS && h->comm) {
+  if (h->mode == MODE_PROCESS && (h->comm || hooks(h))) {
     barrier(h);  // no peer may still be writing into our tables
     cudaStreamSynchronize(s);
     for (int k = 0; k < h->P; ++k)
@@ -444,20 +486,26 @@ static int exchange_ipc(lcsb_t* h) {
     CU(h, cudaIpcGetMemHandle(reinterpret_cast<cudaIpcMemHandle_t*>(host_mine + i * hb),
                               h->tabs[h->first][i]));
   char* dbuf = nullptr;
-  CU(h, cudaMalloc(&dbuf, mine * (size_t)(h->P + 1)));
   char* host_all = (char*)malloc(mine * (size_t)h->P);
   int rc = LCSB_OK;
-  cudaError_t e = cudaMemcpyAsync(dbuf + mine * h->P, host_mine, mine, cudaMemcpyHostToDevice, s);
-  ncclResult_t r = ncclSuccess;
-  if (e == cudaSuccess)
-    r = ncclAllGather(dbuf + mine * h->P, dbuf, mine, ncclUint8, h->comm, s);
-  if (e == cudaSuccess && r == ncclSuccess)
-    e = cudaMemcpyAsync(host_all, dbuf, mine * h->P, cudaMemcpyDeviceToHost, s);
-  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
-  if (r != ncclSuccess)
-    rc = set_err(h, LCSB_ENCCL, "IPC handle all-gather: %s", ncclGetErrorString(r));
-  else if (e != cudaSuccess)
-    rc = set_err(h, LCSB_ECUDA, "IPC handle exchange: %s", cudaGetErrorString(e));
+  cudaError_t e = cudaSuccess;
+  if (const lcsb_comm_hooks* c = hooks(h)) {  // host hooks: the handles are plain bytes
+    if (c->allgather(host_mine, host_all, mine, c->ctx) != 0)
+      rc = set_err(h, LCSB_ENCCL, "comm hook allgather of the IPC handles failed");
+  } else {
+    CU(h, cudaMalloc(&dbuf, mine * (size_t)(h->P + 1)));
+    e = cudaMemcpyAsync(dbuf + mine * h->P, host_mine, mine, cudaMemcpyHostToDevice, s);
+    ncclResult_t r = ncclSuccess;
+    if (e == cudaSuccess)
+      r = ncclAllGather(dbuf + mine * h->P, dbuf, mine, ncclUint8, h->comm, s);
+    if (e == cudaSuccess && r == ncclSuccess)
+      e = cudaMemcpyAsync(host_all, dbuf, mine * h->P, cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    if (r != ncclSuccess)
+      rc = set_err(h, LCSB_ENCCL, "IPC handle all-gather: %s", ncclGetErrorString(r));
+    else if (e != cudaSuccess)
+      rc = set_err(h, LCSB_ECUDA, "IPC handle exchange: %s", cudaGetErrorString(e));
+  }
   for (int k = 0; rc == LCSB_OK && k < h->P; ++k) {
     if (owns(h, k)) continue;
     for (int i = 0; i < h->ntab && rc == LCSB_OK; ++i) {
@@ -469,7 +517,7 @@ static int exchange_ipc(lcsb_t* h) {
     }
   }
   free(host_all);
-  cudaFree(dbuf);
+  if (dbuf) cudaFree(dbuf);
   return rc;
 }
 
@@ -530,7 +578,7 @@ extern "C" int lcsb_create_ex(const lcsb_config* cfg, lcsb_t** out) {
   }
   cudaStream_t s = (cudaStream_t)cfg->stream;
 
-  if (h->mode == MODE_PROCESS) {
+  if (h->mode == MODE_PROCESS && !cfg->comm) {
     ncclUniqueId id;
     memcpy(&id, cfg->nccl_id, sizeof id);
     ncclResult_t r = ncclCommInitRank(&h->comm, h->P, id, cfg->shard);
@@ -775,6 +823,12 @@ extern "C" int lcsb_sweep(lcsb_t* h, int64_t n) {
   if (n < 0) return set_err(h, LCSB_EINVAL, "n must be >= 0");
   CU(h, cudaSetDevice(h->device));
   cudaStream_t s = (cudaStream_t)h->cfg.stream;
+  if (n > 0 && h->mode == MODE_PROCESS) {
+    // every rank is done with the tables (e.g. a rank-local lcsb_table read since the last
+    // collective call) before anyone overwrites the oldest generation in the peers' memory
+    int rc = barrier(h);
+    if (rc != LCSB_OK) return rc;
+  }
   if (graph_worthy(h) && !getenv("LCSB_NO_GRAPHS")) {
     if (!h->graph_sweeps) {
       const int period = (h->kernel == 3) ? 6 : h->ntab;  // q4: lcm(2 tables, 3 mean arrays)
@@ -889,9 +943,9 @@ extern "C" int lcsb_bound(lcsb_t* h, lcsb_bound_t* out) {
                        h->sms));
     h->launches += 1;
   }
-  if (h->mode == MODE_PROCESS) {
-    NC(h, ncclAllReduce(h->red + 0, h->red + 0, 1, ncclUint64, ncclMax, h->comm, s));
-    NC(h, ncclAllReduce(h->red + 1, h->red + 1, 1, ncclUint64, ncclMin, h->comm, s));
+  if (!one_pass) {
+    int rc = allreduce_slots(h, 0, 2, 2u);  // the global R before the W pass
+    if (rc != LCSB_OK) return rc;
   }
   if (h->kernel == 2) {
     const int M = bin2_tma_wpass_m(h->cfg.dtype, h->cfg.ell, h->p);
@@ -938,8 +992,10 @@ extern "C" int lcsb_bound(lcsb_t* h, lcsb_bound_t* out) {
       CU(h, launch_generic_wpass(a, h->cfg.dtype, s, h->sms));
     h->launches += 1;
   }
-  if (h->mode == MODE_PROCESS)
-    NC(h, ncclAllReduce(h->red + 2, h->red + 2, 2, ncclUint64, ncclMax, h->comm, s));
+  {
+    int rc = one_pass ? allreduce_slots(h, 0, 3, 6u) : allreduce_slots(h, 2, 2, 0u);
+    if (rc != LCSB_OK) return rc;
+  }
   CU(h, cudaMemcpyAsync(h->red_host, h->red, kRedSlots * sizeof(unsigned long long),
                         cudaMemcpyDeviceToHost, s));
   CU(h, cudaStreamSynchronize(s));

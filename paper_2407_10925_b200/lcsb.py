@@ -26,6 +26,17 @@ STATUS = {0: "LCSB_OK", 1: "LCSB_EINVAL", 2: "LCSB_ECAPACITY", 3: "LCSB_ESTATE",
 _ALLOC_FN = ctypes.CFUNCTYPE(ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p, ctypes.c_void_p)
 _FREE_FN = ctypes.CFUNCTYPE(None, ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p,
                             ctypes.c_void_p)
+ALLGATHER_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t,
+                                ctypes.c_void_p)
+BARRIER_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p)
+ALLREDUCE_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.POINTER(ctypes.c_uint64), ctypes.c_int32,
+                                ctypes.c_void_p)
+
+
+class LcsbCommHooks(ctypes.Structure):
+    """lcsb_comm_hooks (include/lcsb.h): host collectives of the process-sharded mode."""
+    _fields_ = [("allgather", ALLGATHER_FN), ("barrier", BARRIER_FN),
+                ("allreduce_max_u64", ALLREDUCE_FN), ("ctx", ctypes.c_void_p)]
 
 
 class LcsbConfig(ctypes.Structure):
@@ -35,7 +46,8 @@ class LcsbConfig(ctypes.Structure):
                 ("stream", ctypes.c_void_p), ("alloc", _ALLOC_FN), ("free_", _FREE_FN),
                 ("alloc_ctx", ctypes.c_void_p), ("shards", ctypes.c_int32),
                 ("shard", ctypes.c_int32), ("virtual_shards", ctypes.c_int32),
-                ("nccl_id", ctypes.c_void_p), ("block_log4", ctypes.c_int32)]
+                ("nccl_id", ctypes.c_void_p), ("block_log4", ctypes.c_int32),
+                ("comm", ctypes.POINTER(LcsbCommHooks))]
 
 
 class LcsbBound(ctypes.Structure):
@@ -196,7 +208,8 @@ class Lcsb:
 
     def __init__(self, sigma, d, ell, dtype="f32", form="auto", rmode="max", symmetry=-1,
                  kernel="auto", stream=None, torch_allocator=True, shards=1, shard=0,
-                 virtual_shards=False, nccl_id: bytes | None = None, block_log4: int = 0):
+                 virtual_shards=False, nccl_id: bytes | None = None, block_log4: int = 0,
+                 comm_hooks: "LcsbCommHooks | None" = None):
         import torch
         if not torch.cuda.is_available():
             raise LcsbError(4, "no CUDA device (the library has no CPU path)")
@@ -213,6 +226,9 @@ class Lcsb:
                 raise ValueError("nccl_id must be 128 bytes")
             self._nccl_id = ctypes.create_string_buffer(bytes(nccl_id), NCCL_ID_BYTES)
             cfg.nccl_id = ctypes.cast(self._nccl_id, ctypes.c_void_p)
+        self._comm_hooks = comm_hooks  # kept alive with the handle (the library calls into it)
+        if comm_hooks is not None:
+            cfg.comm = ctypes.pointer(comm_hooks)
         self._alloc = _TorchAllocator(self.device) if torch_allocator else None
         if self._alloc is not None:
             cfg.alloc = self._alloc.alloc_cb

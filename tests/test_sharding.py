@@ -216,3 +216,113 @@ def test_process_mode_single_rank_equals_single_gpu(tmp_path):
     import torch.multiprocessing as mp
     mp.spawn(_pm_worker, args=(1, _free_port(), str(tmp_path)), nprocs=1, join=True)
     assert np.load(tmp_path / "pm.npy").all()
+
+
+# ------------------------------------------------------------------ comm hooks (host transport)
+
+def _hooks_worker(rank, world, port, result_dir):
+    """Calls the lcsb_comm_hooks callbacks through their C function pointers, as the library
+    does, over a world-size-`world` gloo group (CPU only)."""
+    import ctypes
+    import torch.distributed as dist
+    from paper_2407_10925_b200 import dist as pdist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    hk = pdist.comm_hooks()
+    # allgather: 64 rank-specific bytes (a cudaIpcMemHandle_t is 64 bytes)
+    mine = bytes((rank * 37 + i) % 256 for i in range(64))
+    allb = ctypes.create_string_buffer(64 * world)
+    rc1 = hk.allgather(ctypes.c_char_p(mine), allb, 64, None)
+    # allreduce_max_u64, with values whose order depends on the top bit (and a complemented min)
+    top = (1 << 64) - 1
+    vals = (ctypes.c_uint64 * 3)(top - rank, rank, top ^ (1000 + rank))
+    rc2 = hk.allreduce_max_u64(vals, 3, None)
+    rc3 = hk.barrier(None)
+    np.save(os.path.join(result_dir, f"h{rank}.npy"),
+            np.array([rc1, rc2, rc3] + list(allb.raw) + [int(v) for v in vals], dtype=object))
+    dist.destroy_process_group()
+
+
+def test_comm_hooks_over_gloo_world_size_2(tmp_path):
+    """The host-transport hooks (paper_2407_10925_b200/dist.py) on CPU: allgather returns every
+    rank's bytes in rank order, allreduce_max_u64 is an unsigned max (also across the top bit;
+    a min passes as the max of complements, as the library encodes R_min), barrier returns 0."""
+    import torch.multiprocessing as mp
+    world = 2
+    mp.spawn(_hooks_worker, args=(world, _free_port(), str(tmp_path)), nprocs=world, join=True)
+    top = (1 << 64) - 1
+    want = b"".join(bytes((r * 37 + i) % 256 for i in range(64)) for r in range(world))
+    for r in range(world):
+        res = list(np.load(tmp_path / f"h{r}.npy", allow_pickle=True))
+        assert res[:3] == [0, 0, 0]
+        assert bytes(res[3:3 + 64 * world]) == want
+        v = res[3 + 64 * world:]
+        assert v[0] == top and v[1] == world - 1
+        assert top ^ v[2] == 1000  # max of complements = complement of the min
+
+
+def _pm_host_worker(rank, world, port, out_dir, ell, dtype):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+    from paper_2407_10925_b200 import Lcsb
+    from paper_2407_10925_b200.dist import create_sharded
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(0)  # every rank on the one GPU: the host transport never spins
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    h = create_sharded(ell, dtype=dtype, transport="host")
+    assert h.num_shards == world
+    out = {}
+    for n in (1, 2, 20):
+        h.sweep(n)
+        b = h.bound()
+        if rank == 0:  # any rank reads any shard (the peers' tables are IPC-mapped)
+            out[n] = (h.table(0), h.table(1), b)
+    h.reset()
+    h.sweep(3)
+    if rank == 0:
+        out["reset"] = (h.table(0),)
+    dist.barrier()
+    h.destroy()  # collective
+    if rank == 0:
+        ok = []
+        ref = Lcsb(2, 2, ell, dtype=dtype, symmetry=1)
+        for n in (1, 2, 20):
+            ref.sweep(n)
+            rb = ref.bound()
+            t0, t1, b = out[n]
+            ok += [np.array_equal(t0, ref.table(0)), np.array_equal(t1, ref.table(1)),
+                   (b.R_max, b.R_min, b.E_at_Rmax, b.E_at_Rmin, b.best_bound) ==
+                   (rb.R_max, rb.R_min, rb.E_at_Rmax, rb.E_at_Rmin, rb.best_bound)]
+        ref.reset()
+        ref.sweep(3)
+        ok.append(np.array_equal(out["reset"][0], ref.table(0)))
+        if ell <= 9:  # and the oracle, element by element (23 sweeps in total before the reset)
+            from oracle import ft_oracle as fo
+            r = fo.feasible_triplet(2, 2, ell, 23, form="two_array", dtype=dtype)
+            t = out[20][0]
+            ok.append(np.array_equal(t, r["table"]) if dtype == "f32" else
+                      bool(np.allclose(t, r["table"], rtol=1e-12, atol=0)))
+        ref.destroy()
+        np.save(os.path.join(out_dir, "pmh.npy"), np.array(ok))
+    dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+@pytest.mark.skipif(not has_cuda(), reason="needs a CUDA device")
+@pytest.mark.parametrize("world,ell,dtype", [(2, 9, "f32"), (2, 10, "f64"), (4, 9, "f64"),
+                                             (4, 11, "f32")])
+def test_process_mode_multi_rank_on_one_gpu(tmp_path, world, ell, dtype):
+    """2 and 4 PROCESSES, one shard each, all on cuda:0, through the host comm hooks (gloo):
+    CUDA-IPC handle exchange, outputs pushed into the other processes' tables, the per-sweep
+    barrier (stream synchronise + host barrier: no kernel waits on another process, so sharing
+    one GPU is safe), the bound's cross-rank reductions, collective reset and destroy.  Tables
+    (both generations) and bounds equal the unsharded single-process run bit for bit, and the
+    oracle at l <= 9."""
+    import torch.multiprocessing as mp
+    mp.spawn(_pm_host_worker, args=(world, _free_port(), str(tmp_path), ell, dtype),
+             nprocs=world, join=True)
+    res = np.load(tmp_path / "pmh.npy")
+    assert res.all(), res
