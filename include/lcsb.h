@@ -200,6 +200,12 @@ int lcsb_nccl_unique_id(void* out, size_t len);
 int lcsb_shard_locate(int32_t ell, int32_t shards, uint64_t logical, int32_t* shard,
                       uint64_t* local);
 
+/* Host-only sharding plan (no GPU needed) of the sigma = 4, d = 2 complement-folded table (the
+ * q4 kernel): shard and shard-local index of logical state `logical` for
+ * `shards` in {1, 2, 4, 8} (l >= 4; l >= 5 for 8 shards).  Errors: EINVAL. */
+int lcsb_shard_locate_sigma4(int32_t ell, int32_t shards, uint64_t logical, int32_t* shard,
+                             uint64_t* local);
+
 /* Host-only layout query (no GPU needed): the stored index of logical state `logical` in the
  * quarter table (symmetry = 2) of the binary two-array form with length-ell strings and blocks
  * of 4^block_log4 entries, and the number of stored entries.  Every stored entry holds states

@@ -130,7 +130,19 @@ struct Q4Geo {
   uint32_t tail_bits;  // 4 (l - 1)
   uint32_t ubits;      // tail_bits - 4M: bits of a unit index
   uint64_t nunits;
+  int p;               // sharded: 2^p shards (0 = unsharded), items of shard `shard` only
+  uint32_t shard;
 };
+
+// shard key of a unit (its first tail groups; lcsb_internal.cuh q4_key): the key of both windows
+// of every unit of its group
+__device__ __forceinline__ uint32_t unit_key(const Q4Geo& g, uint64_t u) {
+  const int B = (int)g.ubits;
+  const uint32_t k1 = q4dig(u, B, 0, 1) ^ q4dig(u, B, 0, 0);
+  if (g.p == 1) return k1 >> 1;
+  if (g.p == 2) return k1;
+  return (k1 << 1) | ((q4dig(u, B, 1, 1) ^ q4dig(u, B, 1, 0)) >> 1);
+}
 
 __device__ __forceinline__ uint64_t unit_comp(const Q4Geo& g, uint64_t u) {
   return ~u & (g.nunits - 1);
@@ -172,10 +184,10 @@ __device__ __forceinline__ int slot_of(const uint64_t (&U)[kGroup], int n, uint6
   return k;
 }
 
-// next item >= c (step G): a unit that is the smallest of its group
+// next item >= c (step G): a unit that is the smallest of its group (sharded: of this shard)
 __device__ __forceinline__ uint64_t q4_next(const Q4Geo& g, uint64_t c, uint64_t G) {
   while (c < g.nunits) {
-    if (group_min(g, c) == c) return c;
+    if (group_min(g, c) == c && (g.p == 0 || unit_key(g, c) == g.shard)) return c;
     c += G;
   }
   return c;
@@ -183,7 +195,8 @@ __device__ __forceinline__ uint64_t q4_next(const Q4Geo& g, uint64_t c, uint64_t
 
 template <typename T, int M, int S, bool WMODE>
 __device__ __forceinline__ void q4_issue(const Q4Geo& g, uint64_t u, T* buf, uint64_t* bar,
-                                         uint64_t* meta, const T* g1, const double* pin) {
+                                         uint64_t* meta, const T* g1, const double* pin,
+                                         const Q4Args& a) {
   using C = Q4Cfg<T, M, S, WMODE>;
   if (u >= g.nunits) {  // no item left: an end marker completes the stage's phase
     meta[0] = kNoItem;
@@ -217,16 +230,24 @@ __device__ __forceinline__ void q4_issue(const Q4Geo& g, uint64_t u, T* buf, uin
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
       const uint64_t yb = ((uint64_t)h << (g.tail_bits + 2)) | low;
-      tma_load_1d(ub + h * C::WB, g1 + yb, C::WB * sizeof(T), bar);
+      // sharded: the window lies in this shard (its key is the item's), contiguously
+      tma_load_1d(ub + h * C::WB, g1 + (g.p ? q4_local(yb, g.ell, g.p) : yb), C::WB * sizeof(T),
+                  bar);
     }
-    if (unit_low(g, U[k])) tma_load_1d(ub + C::WIN, pin + t0, C::TT * sizeof(double), bar);
+    if (unit_low(g, U[k]))
+      tma_load_1d(ub + C::WIN, pin + (g.p ? q4_mlocal(t0, g.ell, g.p) : t0),
+                  C::TT * sizeof(double), bar);
     if (WMODE) {  // u (= g1, the newest table) at the unit's 8 stored output runs
       T* uo = ub + C::WIN + C::PR;
 #pragma unroll
       for (int hh = 0; hh < 8; ++hh) {
         const uint64_t hx = ((uint64_t)(hh >> 2) << (g.tail_bits + 2)) |
                             ((uint64_t)(hh & 3) << g.tail_bits);
-        tma_load_1d(uo + hh * C::TT, g1 + (hx | t0), C::TT * sizeof(T), bar);
+        // sharded: the run's owner (any shard; a peer's table through its mapped pointer)
+        const T* src = g.p ? reinterpret_cast<const T*>(a.g1_sh[q4_key(hx | t0, g.ell, g.p)]) +
+                                 q4_local(hx | t0, g.ell, g.p)
+                           : g1 + (hx | t0);
+        tma_load_1d(uo + hh * C::TT, src, C::TT * sizeof(T), bar);
       }
     }
   }
@@ -257,7 +278,7 @@ __device__ __forceinline__ double row16_sum(const T* p) {
   return sum;
 }
 
-template <typename T, int M, int S, bool WMODE, bool GR = false>
+template <typename T, int M, int S, bool WMODE, bool GR = false, bool SH = false>
 __global__ void __launch_bounds__(kThreads, GR ? 4 : (WMODE ? 1 : 3)) q4_kernel(Q4Args a) {
   using C = Q4Cfg<T, M, S, WMODE, GR>;
   constexpr uint32_t TT = C::TT;
@@ -272,6 +293,8 @@ __global__ void __launch_bounds__(kThreads, GR ? 4 : (WMODE ? 1 : 3)) q4_kernel(
   g.tail_bits = 4u * (uint32_t)(a.ell - 1);
   g.ubits = g.tail_bits - 4 * M;
   g.nunits = 1ull << g.ubits;
+  g.p = SH ? a.p : 0;  // unsharded instantiations: every shard branch folds away
+  g.shard = (uint32_t)a.shard;
   const T* g1 = reinterpret_cast<const T*>(a.g1);
   const double* pin = a.pin;
   double* pout = a.pout;
@@ -297,7 +320,7 @@ __global__ void __launch_bounds__(kThreads, GR ? 4 : (WMODE ? 1 : 3)) q4_kernel(
     pc = q4_next(g, blockIdx.x, G);
     for (int s = 0; s < S; ++s) {
       q4_issue<T, M, S, WMODE>(g, pc, in + (size_t)s * C::STAGE, &bars[s], metas + s * kMeta, g1,
-                               pin);
+                               pin, a);
       if (pc < g.nunits) pc = q4_next(g, pc + G, G);
     }
   }
@@ -330,7 +353,7 @@ __global__ void __launch_bounds__(kThreads, GR ? 4 : (WMODE ? 1 : 3)) q4_kernel(
       if (k >= n) break;
       const uint64_t X = U[k];
       const uint32_t sl = (uint32_t)(rec >> (8 + 8 * k));
-      T* const drow = WMODE ? nullptr : dst + ((X << (4 * M)) + i);
+      T* const drow = (WMODE || g.p) ? nullptr : dst + ((X << (4 * M)) + i);
       const T* ubX = buf + (size_t)k * C::UNIT;
       const T* ubS = buf + (size_t)(sl & 3u) * C::UNIT;
       const T* ubCS = buf + (size_t)((sl >> 2) & 3u) * C::UNIT;
@@ -369,7 +392,14 @@ __global__ void __launch_bounds__(kThreads, GR ? 4 : (WMODE ? 1 : 3)) q4_kernel(
             const int hh = ha * 4 + hb;
             if (!WMODE) {
               // the head bits sit above the tail bits: | == +, so the row pointer is per unit
-              drow[((uint64_t)ha << hbit_a) + ((uint64_t)hb << hbit_b)] = (T)v;
+              if (g.p == 0) {
+                drow[((uint64_t)ha << hbit_a) + ((uint64_t)hb << hbit_b)] = (T)v;
+              } else {  // sharded: the owner of this (h_a, h_b) run (a peer: NVLink store)
+                const uint64_t s0 =
+                    ((uint64_t)ha << hbit_a) | ((uint64_t)hb << hbit_b) | (X << (4 * M));
+                reinterpret_cast<T*>(a.dst_sh[q4_key(s0, g.ell, g.p)])[q4_local(s0, g.ell, g.p) +
+                                                                       i] = (T)v;
+              }
               if constexpr (!GR) {
                 constexpr uint32_t NR1 = C::NR + 1;
                 outs[(((uint32_t)k * 8 + hh) * 16 + (i & 15)) * NR1 + (i >> 4)] = (T)v;
@@ -385,7 +415,7 @@ __global__ void __launch_bounds__(kThreads, GR ? 4 : (WMODE ? 1 : 3)) q4_kernel(
     __syncthreads();
     const bool early = (a.flags & kQ4EarlyIssue) != 0;
     if (early && tid == 0) {  // the input stage is consumed: refill it now
-      q4_issue<T, M, S, WMODE>(g, pc, buf, &bars[s], metas + s * kMeta, g1, pin);
+      q4_issue<T, M, S, WMODE>(g, pc, buf, &bars[s], metas + s * kMeta, g1, pin, a);
       if (pc < g.nunits) pc = q4_next(g, pc + G, G);
     }
     if (!WMODE) {
@@ -410,28 +440,32 @@ __global__ void __launch_bounds__(kThreads, GR ? 4 : (WMODE ? 1 : 3)) q4_kernel(
 #pragma unroll
           for (int c = 0; c < 16; ++c) sum = sum + (double)row[c * NR1];  // (+ 0.0: exact no-op)
         }
-        pout[((hx | (Uk << (4 * M))) >> 4) | r] = 0.0625 * sum;
+        const uint64_t row = ((hx | (Uk << (4 * M))) >> 4) | r;
+        if (g.p == 0)
+          pout[row] = 0.0625 * sum;
+        else  // sharded: the shard of the items that read this row mean
+          a.pout_sh[q4_mkey(row, g.ell, g.p)][q4_mlocal(row, g.ell, g.p)] = 0.0625 * sum;
       }
       __syncthreads();  // outs is reused by the next item
     }
     if (!early && tid == 0) {
-      q4_issue<T, M, S, WMODE>(g, pc, buf, &bars[s], metas + s * kMeta, g1, pin);
+      q4_issue<T, M, S, WMODE>(g, pc, buf, &bars[s], metas + s * kMeta, g1, pin, a);
       if (pc < g.nunits) pc = q4_next(g, pc + G, G);
     }
   }
   if (WMODE) block_max2_to(wmax[0], wmax[1], a.red_out);
 }
 
-template <typename T, int M, int S, bool WMODE, bool GR = false>
-cudaError_t launch_q4_t(const Q4Args& a, cudaStream_t s, int sms) {
+template <typename T, int M, int S, bool WMODE, bool GR = false, bool SH = false>
+cudaError_t launch_q4_one(const Q4Args& a, cudaStream_t s, int sms) {
   using C = Q4Cfg<T, M, S, WMODE, GR>;
   static uint64_t cap = 0;
   if (cap == 0) {
-    cudaError_t e = cudaFuncSetAttribute(q4_kernel<T, M, S, WMODE, GR>,
+    cudaError_t e = cudaFuncSetAttribute(q4_kernel<T, M, S, WMODE, GR, SH>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
     if (e != cudaSuccess) return e;
     int per_sm = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, q4_kernel<T, M, S, WMODE, GR>,
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, q4_kernel<T, M, S, WMODE, GR, SH>,
                                                       kThreads, C::SMEM) != cudaSuccess ||
         per_sm < 1) {
       cudaGetLastError();
@@ -441,8 +475,14 @@ cudaError_t launch_q4_t(const Q4Args& a, cudaStream_t s, int sms) {
   }
   const uint64_t nunits = 1ull << (4 * (a.ell - 1) - 4 * M);
   uint64_t blocks = cap < nunits ? cap : nunits;
-  q4_kernel<T, M, S, WMODE, GR><<<(unsigned)blocks, kThreads, C::SMEM, s>>>(a);
+  q4_kernel<T, M, S, WMODE, GR, SH><<<(unsigned)blocks, kThreads, C::SMEM, s>>>(a);
   return cudaGetLastError();
+}
+// sharded launches (a.p > 0) take the instantiation with the shard indexing compiled in
+template <typename T, int M, int S, bool WMODE, bool GR = false>
+cudaError_t launch_q4_t(const Q4Args& a, cudaStream_t s, int sms) {
+  if (a.p > 0) return launch_q4_one<T, M, S, WMODE, false, true>(a, s, sms);
+  return launch_q4_one<T, M, S, WMODE, GR, false>(a, s, sms);
 }
 
 }  // namespace

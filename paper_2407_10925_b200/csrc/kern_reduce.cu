@@ -90,7 +90,8 @@ struct ExpandTabs {
 };
 
 template <typename T>
-__global__ void expand_kernel(ExpandTabs tabs, int p, int symmetric, uint64_t nlogical, int ell,
+__global__ void expand_kernel(ExpandTabs tabs, int p, int symmetric, int q4, uint64_t nlogical,
+                              int ell,
                               const uint32_t* __restrict__ qmap, int K, uint64_t first,
                               uint64_t count, const uint64_t* __restrict__ idx, double* out) {
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
@@ -101,6 +102,10 @@ __global__ void expand_kernel(ExpandTabs tabs, int p, int symmetric, uint64_t nl
     if (symmetric && y >= half) y = top - y;  // Eq. (comp_eq)
     if (qmap) {  // quarter table: the orbit representative under the string swap / psi
       out[i] = (double)reinterpret_cast<const T*>(tabs.t[0])[qstored(qmap, y, K)];
+      continue;
+    }
+    if (q4) {  // sigma = 4 digit-key shards
+      out[i] = (double)reinterpret_cast<const T*>(tabs.t[q4_key(y, ell, p)])[q4_local(y, ell, p)];
       continue;
     }
     const uint32_t sh = shard_of_stored(y, 2 * ell, p);
@@ -132,7 +137,7 @@ cudaError_t launch_rdiff(const void* newest, const void* prev, uint64_t n, int d
   return cudaGetLastError();
 }
 
-cudaError_t launch_expand(const void* const* tabs, int p, int dtype, int symmetric,
+cudaError_t launch_expand(const void* const* tabs, int p, int dtype, int symmetric, int q4,
                           uint64_t nlogical, int ell,
                           const uint32_t* qmap, int K, uint64_t first, uint64_t count,
                           const uint64_t* idx, double* out, cudaStream_t s) {
@@ -142,9 +147,9 @@ cudaError_t launch_expand(const void* const* tabs, int p, int dtype, int symmetr
   ExpandTabs t;
   for (int k = 0; k < kMaxShards; ++k) t.t[k] = (k < (1 << p)) ? tabs[k] : nullptr;
   if (dtype == LCSB_F32)
-    expand_kernel<float><<<(unsigned)blocks, 256, 0, s>>>(t, p, symmetric, nlogical, ell, qmap, K, first, count, idx, out);
+    expand_kernel<float><<<(unsigned)blocks, 256, 0, s>>>(t, p, symmetric, q4, nlogical, ell, qmap, K, first, count, idx, out);
   else
-    expand_kernel<double><<<(unsigned)blocks, 256, 0, s>>>(t, p, symmetric, nlogical, ell, qmap, K, first, count, idx, out);
+    expand_kernel<double><<<(unsigned)blocks, 256, 0, s>>>(t, p, symmetric, q4, nlogical, ell, qmap, K, first, count, idx, out);
   return cudaGetLastError();
 }
 

@@ -44,9 +44,9 @@ struct lcsb {
   size_t esize;
   int ntab;           // tables in the ring
   // kernel 3 (q4, pooled-history KS): ring of 3 row-mean arrays (fp64, n/16 entries each);
-  // pools[pcur] holds the row means of the newest table
-  double* pools[3];
-  size_t pool_bytes;
+  // pools[k][pcur] holds the row means of the newest table (shard k's rows when sharded)
+  double* pools[kMaxShards][3];
+  size_t pool_bytes;  // per shard
   int pcur;
   // kernel 4 (small, KS, pooled sweep): spools[k][slot] = pooled means (|N| = k >= 2) of the
   // table in ring slot `slot` (kern_small.cu)
@@ -248,9 +248,25 @@ static int plan_config(const lcsb_config* c, Plan* p, char* why, size_t whylen) 
     snprintf(why, whylen, "shards must be 1, 2, 4 or 8");
     return LCSB_EINVAL;
   }
-  if (sharded) {
+  // sigma = 4, d = 2 (q4) shards by a digit key of the first characters: the
+  // unit of 16^2 tails must leave the key's tail groups above it (one group for p <= 2, two for
+  // p = 3)
+  const bool q4_shard = c->sigma == 4 && c->d == 2 && c->kernel == LCSB_KERNEL_AUTO &&
+                        c->ell >= q4_min_ell() && c->ell >= (lp == 3 ? 5 : 4);
+  if (sharded && q4_shard) {
+    if (!c->virtual_shards && (c->shard < 0 || c->shard >= P)) {
+      snprintf(why, whylen, "shard must be in [0, %d)", P);
+      return LCSB_EINVAL;
+    }
+    if (!c->virtual_shards && !has_comm) {
+      snprintf(why, whylen, "process-sharded mode needs nccl_id or comm hooks");
+      return LCSB_EINVAL;
+    }
+  } else if (sharded) {
     if (!sym) {
-      snprintf(why, whylen, "sharding needs the complement-folded binary two-array table");
+      snprintf(why, whylen,
+               "sharding needs the complement-folded binary two-array table or sigma = 4, "
+               "d = 2 (l >= 4; l >= 5 for 8 shards)");
       return LCSB_EINVAL;
     }
     if (pick_bin2_variant(c->dtype, c->ell, lp) == 0 ||
@@ -303,7 +319,7 @@ static int plan_config(const lcsb_config* c, Plan* p, char* why, size_t whylen) 
     return LCSB_EINVAL;
   }
   p->bytes += 256;
-  if (p->kernel == 3) p->bytes += 3 * (n / 32) * sizeof(double);
+  if (p->kernel == 3) p->bytes += 3 * (n / 32 / (uint64_t)P) * owned * sizeof(double);
   if (p->kernel == 4 && form == LCSB_FORM_KS && small_pooled_supported(c->sigma, c->d)) {
     uint64_t sigd = 1;
     for (int j = 0; j < c->d; ++j) sigd *= (uint64_t)c->sigma;
@@ -333,6 +349,21 @@ extern "C" int lcsb_shard_locate(int32_t ell, int32_t shards, uint64_t logical, 
   if (s >= (1ull << (L - 1))) s = ((1ull << L) - 1) - s;  // Eq. (comp_eq)
   *shard = (int32_t)shard_of_stored(s, L, p);
   *local = local_of_stored(s, L, p);
+  return LCSB_OK;
+}
+
+extern "C" int lcsb_shard_locate_sigma4(int32_t ell, int32_t shards, uint64_t logical,
+                                        int32_t* shard, uint64_t* local) {
+  const int p = log2_exact(shards);
+  if (ell < 1 || ell > 15 || p < 0 || shards > kMaxShards || !shard || !local ||
+      (p > 0 && ell < (p == 3 ? 5 : 4)))
+    return set_err(nullptr, LCSB_EINVAL, "bad arguments to lcsb_shard_locate_sigma4");
+  const int L = 4 * ell;
+  if (logical >> L) return set_err(nullptr, LCSB_EINVAL, "logical index out of range");
+  uint64_t s = logical;
+  if (s >= (1ull << (L - 1))) s = ((1ull << L) - 1) - s;  // complement d -> 3 - d (kern_q4.cu)
+  *shard = (int32_t)q4_key(s, ell, p);
+  *local = q4_local(s, ell, p);
   return LCSB_OK;
 }
 
@@ -401,6 +432,13 @@ static void dev_free(lcsb_t* h, void* p, size_t bytes) {
 
 static bool owns(const lcsb_t* h, int k) { return k >= h->first && k < h->first + h->nown; }
 
+// the device buffers of shard k a peer needs: the table ring, then (q4) the row-mean ring
+static int ipc_nbuf(const lcsb_t* h) { return h->ntab + (h->kernel == 3 ? 3 : 0); }
+static void** ipc_buf(lcsb_t* h, int k, int i) {
+  return i < h->ntab ? &h->tabs[k][i] : reinterpret_cast<void**>(&h->pools[k][i - h->ntab]);
+}
+
+
 static const lcsb_comm_hooks* hooks(const lcsb_t* h) {
   return h->mode == MODE_PROCESS ? h->cfg.comm : nullptr;
 }
@@ -455,8 +493,8 @@ extern "C" void lcsb_destroy(lcsb_t* h) {
     cudaStreamSynchronize(s);
     for (int k = 0; k < h->P; ++k)
       if (!owns(h, k))
-        for (int i = 0; i < h->ntab; ++i)
-          if (h->tabs[k][i]) cudaIpcCloseMemHandle(h->tabs[k][i]);
+        for (int i = 0; i < ipc_nbuf(h); ++i)
+          if (*ipc_buf(h, k, i)) cudaIpcCloseMemHandle(*ipc_buf(h, k, i));
   }
   for (int k = 0; k < h->P; ++k)
     if (owns(h, k))
@@ -465,7 +503,9 @@ extern "C" void lcsb_destroy(lcsb_t* h) {
   dev_free(h, h->qmap, h->qmap_bytes);
   dev_free(h, h->qsched, h->qsched_bytes);
   dev_free(h, h->qcounter, 256);
-  for (int i = 0; i < 3; ++i) dev_free(h, h->pools[i], h->pool_bytes);
+  for (int k = 0; k < h->P; ++k)
+    if (owns(h, k))
+      for (int i = 0; i < 3; ++i) dev_free(h, h->pools[k][i], h->pool_bytes);
   for (int k = 0; k <= kMaxD; ++k)
     for (int i = 0; i < kMaxGen; ++i) dev_free(h, h->spools[k][i], h->spool_bytes[k]);
   if (h->barrier_buf) cudaFree(h->barrier_buf);
@@ -480,11 +520,12 @@ extern "C" void lcsb_destroy(lcsb_t* h) {
 static int exchange_ipc(lcsb_t* h) {
   cudaStream_t s = (cudaStream_t)h->cfg.stream;
   const size_t hb = sizeof(cudaIpcMemHandle_t);
-  const size_t mine = hb * (size_t)h->ntab;
-  char host_mine[sizeof(cudaIpcMemHandle_t) * kMaxGen];
-  for (int i = 0; i < h->ntab; ++i)
+  const int nbuf = ipc_nbuf(h);
+  const size_t mine = hb * (size_t)nbuf;
+  char host_mine[sizeof(cudaIpcMemHandle_t) * (kMaxGen + 3)];
+  for (int i = 0; i < nbuf; ++i)
     CU(h, cudaIpcGetMemHandle(reinterpret_cast<cudaIpcMemHandle_t*>(host_mine + i * hb),
-                              h->tabs[h->first][i]));
+                              *ipc_buf(h, h->first, i)));
   char* dbuf = nullptr;
   char* host_all = (char*)malloc(mine * (size_t)h->P);
   int rc = LCSB_OK;
@@ -508,10 +549,10 @@ static int exchange_ipc(lcsb_t* h) {
   }
   for (int k = 0; rc == LCSB_OK && k < h->P; ++k) {
     if (owns(h, k)) continue;
-    for (int i = 0; i < h->ntab && rc == LCSB_OK; ++i) {
+    for (int i = 0; i < nbuf && rc == LCSB_OK; ++i) {
       cudaIpcMemHandle_t mh;
       memcpy(&mh, host_all + (size_t)k * mine + i * hb, hb);
-      e = cudaIpcOpenMemHandle(&h->tabs[k][i], mh, cudaIpcMemLazyEnablePeerAccess);
+      e = cudaIpcOpenMemHandle(ipc_buf(h, k, i), mh, cudaIpcMemLazyEnablePeerAccess);
       if (e != cudaSuccess)
         rc = set_err(h, LCSB_ECUDA, "cudaIpcOpenMemHandle(shard %d): %s", k, cudaGetErrorString(e));
     }
@@ -611,14 +652,17 @@ extern "C" int lcsb_create_ex(const lcsb_config* cfg, lcsb_t** out) {
     return set_err(nullptr, LCSB_ECAPACITY, "scratch allocation failed");
   }
   if (h->kernel == 3) {  // row-mean ring of the pooled-history KS sweep, zero (W_0 = 0)
-    h->pool_bytes = (size_t)(h->n_logical / 32) * sizeof(double);  // rows of stored states
-    for (int i = 0; i < 3; ++i) {
-      h->pools[i] = (double*)dev_alloc(h, h->pool_bytes);
-      if (!h->pools[i] || cudaMemsetAsync(h->pools[i], 0, h->pool_bytes, s) != cudaSuccess) {
-        lcsb_destroy(h);
-        return set_err(nullptr, LCSB_ECAPACITY, "row-mean array allocation failed");
+    // rows of stored states, split evenly over the shards
+    h->pool_bytes = (size_t)(h->n_logical / 32 / (uint64_t)h->P) * sizeof(double);
+    for (int k = h->first; k < h->first + h->nown; ++k)
+      for (int i = 0; i < 3; ++i) {
+        h->pools[k][i] = (double*)dev_alloc(h, h->pool_bytes);
+        if (!h->pools[k][i] ||
+            cudaMemsetAsync(h->pools[k][i], 0, h->pool_bytes, s) != cudaSuccess) {
+          lcsb_destroy(h);
+          return set_err(nullptr, LCSB_ECAPACITY, "row-mean array allocation failed");
+        }
       }
-    }
   }
   if (h->kernel == 4 && h->form == LCSB_FORM_KS && small_pooled_supported(cfg->sigma, cfg->d) &&
       !getenv("LCSB_NO_SMALL_POOL")) {  // pooled means of every ring slot, zero (W_0 = 0)
@@ -720,9 +764,10 @@ extern "C" int lcsb_reset(lcsb_t* h) {
         CU(h, cudaMemsetAsync(h->tabs[k][i], 0, h->tab_bytes, (cudaStream_t)h->cfg.stream));
   rc = barrier(h);  // everyone's tables are zero before anyone sweeps into them
   if (rc != LCSB_OK) return rc;
-  for (int i = 0; i < 3; ++i)
-    if (h->pools[i])
-      CU(h, cudaMemsetAsync(h->pools[i], 0, h->pool_bytes, (cudaStream_t)h->cfg.stream));
+  for (int k = h->first; k < h->first + h->nown; ++k)
+    for (int i = 0; i < 3; ++i)
+      if (h->pools[k][i])
+        CU(h, cudaMemsetAsync(h->pools[k][i], 0, h->pool_bytes, (cudaStream_t)h->cfg.stream));
   for (int k = 0; k <= kMaxD; ++k)
     for (int i = 0; i < kMaxGen; ++i)
       if (h->spools[k][i])
@@ -880,17 +925,27 @@ static int enqueue_sweeps(lcsb_t* h, int64_t n, cudaStream_t s) {
       if (e == cudaSuccess) e = launch_bin2q_sweep(a, h->cfg.dtype, h->qM, h->bin2q_variant, s, h->sms);
       h->launches += 1;
     } else if (h->kernel == 3) {
-      Q4Args a;
-      memset(&a, 0, sizeof a);
-      a.g1 = h->tabs[0][slot_back(h, 0)];
       // row means of v_{n-2} (KS) / of v_{n-1}, the table this sweep reads (two-array)
-      a.pin = h->pools[(h->form == LCSB_FORM_KS) ? (h->pcur + 2) % 3 : h->pcur];
-      a.flags = (h->form == LCSB_FORM_TWO_ARRAY) ? kQ4TwoArray : 0;
-      a.pout = h->pools[(h->pcur + 1) % 3];  // row means of the table written now
-      a.dst = h->tabs[0][out];
-      a.ell = h->cfg.ell;
-      e = launch_q4_sweep(a, h->cfg.dtype, s, h->sms);
-      h->launches += 1;
+      const int pin = (h->form == LCSB_FORM_KS) ? (h->pcur + 2) % 3 : h->pcur;
+      const int pout = (h->pcur + 1) % 3;  // row means of the table written now
+      for (int k = h->first; k < h->first + h->nown && e == cudaSuccess; ++k) {
+        Q4Args a;
+        memset(&a, 0, sizeof a);
+        a.g1 = h->tabs[k][slot_back(h, 0)];
+        a.pin = h->pools[k][pin];
+        a.flags = (h->form == LCSB_FORM_TWO_ARRAY) ? kQ4TwoArray : 0;
+        a.pout = h->pools[k][pout];
+        a.dst = h->tabs[k][out];
+        a.ell = h->cfg.ell;
+        a.p = h->p;
+        a.shard = k;
+        for (int j = 0; j < h->P; ++j) {  // sharded: outputs and row means go to their owners
+          a.dst_sh[j] = h->tabs[j][out];
+          a.pout_sh[j] = h->pools[j][pout];
+        }
+        e = launch_q4_sweep(a, h->cfg.dtype, s, h->sms);
+        h->launches += 1;
+      }
       h->pcur = (h->pcur + 1) % 3;
     } else {
       GenericArgs a;
@@ -969,16 +1024,21 @@ extern "C" int lcsb_bound(lcsb_t* h, lcsb_bound_t* out) {
     CU(h, launch_bin2q_wpass(a, h->cfg.dtype, h->qM, s, h->sms));
     h->launches += 1;
   } else if (h->kernel == 3) {
-    Q4Args a;
-    memset(&a, 0, sizeof a);
-    a.g1 = h->tabs[0][h->cur];
-    a.pin = h->pools[h->pcur];  // |N| = 2 reads v_n itself in the W pass (shift 0)
-    a.flags = (h->form == LCSB_FORM_TWO_ARRAY) ? kQ4TwoArray : 0;
-    a.ell = h->cfg.ell;
-    a.red_in = h->red;
-    a.red_out = h->red + 2;
-    CU(h, launch_q4_wpass(a, h->cfg.dtype, s, h->sms));
-    h->launches += 1;
+    for (int k = h->first; k < h->first + h->nown; ++k) {
+      Q4Args a;
+      memset(&a, 0, sizeof a);
+      a.g1 = h->tabs[k][h->cur];
+      a.pin = h->pools[k][h->pcur];  // |N| = 2 reads v_n itself in the W pass (shift 0)
+      a.flags = (h->form == LCSB_FORM_TWO_ARRAY) ? kQ4TwoArray : 0;
+      a.ell = h->cfg.ell;
+      a.red_in = h->red;
+      a.red_out = h->red + 2;
+      a.p = h->p;
+      a.shard = k;
+      for (int j = 0; j < h->P; ++j) a.g1_sh[j] = h->tabs[j][h->cur];  // u at the outputs
+      CU(h, launch_q4_wpass(a, h->cfg.dtype, s, h->sms));
+      h->launches += 1;
+    }
   } else {
     GenericArgs a;
     fill_generic(h, &a);
@@ -1071,6 +1131,7 @@ static int readout(lcsb_t* h, int which, uint64_t first, uint64_t count, const u
       e = cudaMemcpyAsync(ibuf, host_idx + off, c * sizeof(uint64_t), cudaMemcpyHostToDevice, s);
     if (e == cudaSuccess)
       e = launch_expand(tabs, h->p, h->cfg.dtype, h->symmetric != 0 || h->kernel == 3,
+                        h->kernel == 3,
                         h->n_logical, h->cfg.ell, h->qmap, h->qK,
                         first + off, c, host_idx ? ibuf : nullptr, dbuf, s);
     if (e == cudaSuccess) {
@@ -1104,7 +1165,7 @@ extern "C" uint64_t lcsb_stored_states(const lcsb_t* h) { return h ? h->n_stored
 extern "C" uint64_t lcsb_device_bytes(const lcsb_t* h) {
   if (!h) return 0;
   uint64_t b = (uint64_t)h->tab_bytes * (uint64_t)h->ntab * (uint64_t)h->nown + 256 +
-               h->qmap_bytes + h->qsched_bytes + 3 * (uint64_t)h->pool_bytes;
+               h->qmap_bytes + h->qsched_bytes + 3 * (uint64_t)h->pool_bytes * (uint64_t)h->nown;
   for (int k = 0; k <= kMaxD; ++k)
     for (int i = 0; i < kMaxGen; ++i)
       if (h->spools[k][i]) b += h->spool_bytes[k];

@@ -181,8 +181,58 @@ uint64_t quarter_slots(int ell, int K);        // stored (canonical) blocks
 bool build_quarter_map(int ell, int K, uint32_t* map);
 bool quarter_schedule(int ell, int K, int M, const uint32_t* map, std::vector<uint32_t>& out);
 
+// Sharding of the sigma = 4, d = 2 complement-folded table over 2^p shards.
+// State s: 4l bits, character group g (g = 0 the heads) at bits [4(l-1-g), 4(l-g)), the a digit
+// in the top 2 bits of a group.  Key (p = 1, 2, 3): k = a_1 ^ b_0 (2 bits; p = 1: its top bit),
+// p = 3 appends the top bit of a_2 ^ b_1.  Both windows of every unit of a q4 item group
+// {u, su, cu, csu} have the key a_1 ^ b_1 (... a_2 ^ b_2) of the unit's first tail groups -- the
+// digit swap and the complement d -> 3 - d = d ^ 3 leave a XOR of two digits unchanged -- so
+// every sweep reads only its own shard; outputs and row means are pushed to their owners.
+// Local index: the state with the a_1 digit (p = 1: its top bit) and, for p = 3, the top bit of
+// a_2 removed.  Row means (index r = s >> 4 over stored rows, top group (a_0 < 2, b_0)): key
+// r.a_0 ^ r.b_0 (p = 3: + top bit of r.a_1 ^ r.b_1) = the key of the items that read them; local
+// row index: r with b_0 (p = 1: its top bit) and, for p = 3, the top bit of b_1 removed.
+__host__ __device__ inline uint64_t del_bits(uint64_t x, int q, int n) {  // drop bits [q, q+n)
+  return ((x >> (q + n)) << q) | (x & ((1ull << q) - 1));
+}
+// digit of group g (a: ab = 1, b: ab = 0) of an index of `bits` bits
+__host__ __device__ inline uint32_t q4dig(uint64_t s, int bits, int g, int ab) {
+  return (uint32_t)(s >> (bits - 4 * g - 4 + 2 * ab)) & 3u;
+}
+__host__ __device__ inline uint32_t q4_key(uint64_t s, int ell, int p) {  // stored state
+  const int L = 4 * ell;
+  if (p == 0) return 0;
+  const uint32_t k1 = q4dig(s, L, 1, 1) ^ q4dig(s, L, 0, 0);
+  if (p == 1) return k1 >> 1;
+  if (p == 2) return k1;
+  return (k1 << 1) | ((q4dig(s, L, 2, 1) ^ q4dig(s, L, 1, 0)) >> 1);
+}
+__host__ __device__ inline uint64_t q4_local(uint64_t s, int ell, int p) {
+  const int L = 4 * ell;
+  if (p == 0) return s;
+  // higher bits first (deleting a bit shifts everything above it)
+  s = p == 1 ? del_bits(s, L - 5, 1) : del_bits(s, L - 6, 2);  // a_1 (p = 1: its top bit)
+  if (p == 3) s = del_bits(s, L - 9, 1);                      // top bit of a_2
+  return s;
+}
+__host__ __device__ inline uint32_t q4_mkey(uint64_t r, int ell, int p) {  // row-mean index
+  const int R = 4 * (ell - 1);
+  if (p == 0) return 0;
+  const uint32_t k1 = q4dig(r, R, 0, 1) ^ q4dig(r, R, 0, 0);
+  if (p == 1) return k1 >> 1;
+  if (p == 2) return k1;
+  return (k1 << 1) | ((q4dig(r, R, 1, 1) ^ q4dig(r, R, 1, 0)) >> 1);
+}
+__host__ __device__ inline uint64_t q4_mlocal(uint64_t r, int ell, int p) {
+  const int R = 4 * (ell - 1);
+  if (p == 0) return r;
+  r = p == 1 ? del_bits(r, R - 3, 1) : del_bits(r, R - 4, 2);  // b_0 (p = 1: its top bit)
+  if (p == 3) r = del_bits(r, R - 7, 1);                      // top bit of b_1
+  return r;
+}
+
 struct Q4Args {
-  const void* g1;     // table one sweep back (W pass: the newest table)
+  const void* g1;     // table one sweep back (W pass: the newest table); sharded: this shard's
   const double* pin;  // row means (x >> 4) of the table two sweeps back (W pass: of the newest)
   double* pout;       // sweep: row means of the table written
   void* dst;          // output (sweep mode)
@@ -190,6 +240,12 @@ struct Q4Args {
   const unsigned long long* red_in;
   unsigned long long* red_out;
   int flags;          // kQ4TwoArray from the caller; kern_q4.cu adds its A/B bits
+  // sharded (p > 0): this launch's shard, and every shard's output table / row means (sweep)
+  // or newest table (W pass: u at the outputs)
+  int p, shard;
+  void* dst_sh[kMaxShards];
+  double* pout_sh[kMaxShards];
+  const void* g1_sh[kMaxShards];
 };
 constexpr int kQ4TwoArray = 4;  // Q4Args::flags: two-array form (reading R20)
 
@@ -299,7 +355,8 @@ cudaError_t launch_rdiff(const void* newest, const void* prev, uint64_t n, int d
 // table with blocks of 4^K
 // symmetric: the table holds the logical states [0, nlogical/2); y >= nlogical/2 reads
 // nlogical-1-y (the complement: Eq. comp_eq for sigma = 2, d -> 3-d for sigma = 4)
-cudaError_t launch_expand(const void* const* tabs, int p, int dtype, int symmetric,
+// q4: sigma = 4 digit-key shards (q4_key / q4_local) instead of the binary key
+cudaError_t launch_expand(const void* const* tabs, int p, int dtype, int symmetric, int q4,
                           uint64_t nlogical, int ell,
                           const uint32_t* qmap, int K, uint64_t first, uint64_t count,
                           const uint64_t* idx, double* out, cudaStream_t s);

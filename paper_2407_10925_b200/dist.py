@@ -92,18 +92,24 @@ def comm_hooks(group=None) -> LcsbCommHooks:
 
 
 def create_sharded(ell: int, dtype: str = "f32", rmode: str = "max", group=None,
-                   stream=None, transport: str = "nccl") -> Lcsb:
-    """Collective: every rank of the (torch) process group gets one shard of the sigma = d = 2
-    two-array table of length-ell strings."""
+                   stream=None, transport: str = "nccl", sigma: int = 2,
+                   form: str = "auto") -> Lcsb:
+    """Collective: every rank of the (torch) process group gets one shard of the d = 2 table of
+    length-ell strings: sigma = 2 -- the two-array complement-folded half table (DESIGN.md §9);
+    sigma = 4 -- the complement-folded q4 table, KS or two-array form (§9b)."""
     import torch.distributed as dist
+    if sigma not in (2, 4):
+        raise ValueError("sharded tables exist for sigma = 2 and sigma = 4 (d = 2)")
+    if sigma == 2:
+        form = "two_array"
     ws = dist.get_world_size(group)
     rank = dist.get_rank(group)
     if transport == "host":
-        return Lcsb(2, 2, ell, dtype=dtype, form="two_array", rmode=rmode, shards=ws,
+        return Lcsb(sigma, 2, ell, dtype=dtype, form=form, rmode=rmode, shards=ws,
                     shard=rank, comm_hooks=comm_hooks(group), stream=stream,
                     torch_allocator=False)
     if transport != "nccl":
         raise ValueError("transport must be 'nccl' or 'host'")
     nid = broadcast_id(lcsb_nccl_unique_id() if rank == 0 else None, group)
-    return Lcsb(2, 2, ell, dtype=dtype, form="two_array", rmode=rmode, shards=ws, shard=rank,
+    return Lcsb(sigma, 2, ell, dtype=dtype, form=form, rmode=rmode, shards=ws, shard=rank,
                 nccl_id=nid, stream=stream, torch_allocator=False)

@@ -61,7 +61,8 @@ class LcsbBound(ctypes.Structure):
 # every symbol include/lcsb.h declares (checked by tests/test_abi.py)
 EXPORTS = ["lcsb_config_init", "lcsb_required_bytes", "lcsb_create", "lcsb_create_ex",
            "lcsb_reset", "lcsb_sweep", "lcsb_bound", "lcsb_table", "lcsb_table_gather",
-           "lcsb_nccl_unique_id", "lcsb_shard_locate", "lcsb_quarter_locate", "lcsb_sweeps_done", "lcsb_num_shards",
+           "lcsb_nccl_unique_id", "lcsb_shard_locate", "lcsb_shard_locate_sigma4",
+           "lcsb_quarter_locate", "lcsb_sweeps_done", "lcsb_num_shards",
            "lcsb_num_states", "lcsb_stored_states", "lcsb_device_bytes", "lcsb_kernel_in_use",
            "lcsb_launch_count", "lcsb_last_error", "lcsb_destroy"]
 NCCL_ID_BYTES = 128
@@ -109,6 +110,10 @@ def load_library():
                                       ctypes.POINTER(ctypes.c_int32),
                                       ctypes.POINTER(ctypes.c_uint64)]
     lib.lcsb_shard_locate.restype = ctypes.c_int
+    lib.lcsb_shard_locate_sigma4.argtypes = [ctypes.c_int32, ctypes.c_int32, ctypes.c_uint64,
+                                             ctypes.POINTER(ctypes.c_int32),
+                                             ctypes.POINTER(ctypes.c_uint64)]
+    lib.lcsb_shard_locate_sigma4.restype = ctypes.c_int
     lib.lcsb_quarter_locate.argtypes = [ctypes.c_int32, ctypes.c_int32, ctypes.c_uint64,
                                         ctypes.POINTER(ctypes.c_uint64),
                                         ctypes.POINTER(ctypes.c_uint64)]
@@ -327,6 +332,15 @@ def lcsb_shard_locate(ell: int, shards: int, logical: int):
     loc = ctypes.c_uint64()
     _check(load_library().lcsb_shard_locate(int(ell), int(shards), int(logical), ctypes.byref(sh),
                                             ctypes.byref(loc)))
+    return int(sh.value), int(loc.value)
+
+
+def lcsb_shard_locate_sigma4(ell: int, shards: int, logical: int):
+    """(shard, local index) holding logical sigma = 4, d = 2 state `logical` (host-only plan)."""
+    sh = ctypes.c_int32()
+    loc = ctypes.c_uint64()
+    _check(load_library().lcsb_shard_locate_sigma4(int(ell), int(shards), int(logical),
+                                                   ctypes.byref(sh), ctypes.byref(loc)))
     return int(sh.value), int(loc.value)
 
 

@@ -326,3 +326,165 @@ def test_process_mode_multi_rank_on_one_gpu(tmp_path, world, ell, dtype):
              nprocs=world, join=True)
     res = np.load(tmp_path / "pmh.npy")
     assert res.all(), res
+
+
+# ------------------------------------------------------------------ sigma = 4 shard map (q4)
+
+def _q4_decode(x, ell):
+    """Logical sigma = 4, d = 2 index -> (a, b) digit lists (reading R14: char-position-major,
+    string 0 in the more significant digit of each group)."""
+    a = [(x >> (4 * (ell - 1 - k) + 2)) & 3 for k in range(ell)]
+    b = [(x >> (4 * (ell - 1 - k))) & 3 for k in range(ell)]
+    return a, b
+
+
+def _q4_encode(a, b):
+    ell = len(a)
+    return sum((a[k] << (4 * (ell - 1 - k) + 2)) | (b[k] << (4 * (ell - 1 - k)))
+               for k in range(ell))
+
+
+@pytest.mark.parametrize("ell,shards", [(4, 2), (4, 4), (5, 8), (5, 2)])
+def test_sigma4_shard_map_is_a_balanced_bijection(ell, shards):
+    """lcsb_shard_locate_sigma4: complement images share a location (the fold, d -> 3 - d), the
+    stored half (a_0 < 2) maps one-to-one onto P shards of N / (2P) entries."""
+    L.load_library()
+    N = 4 ** (2 * ell)
+    seen = set()
+    for x in range(N):
+        k, loc = L.lcsb_shard_locate_sigma4(ell, shards, x)
+        a, b = _q4_decode(x, ell)
+        comp = _q4_encode([3 - c for c in a], [3 - c for c in b])
+        assert L.lcsb_shard_locate_sigma4(ell, shards, comp) == (k, loc)
+        if a[0] < 2:
+            assert 0 <= k < shards and 0 <= loc < N // (2 * shards)
+            seen.add((k, loc))
+    assert len(seen) == N // 2
+
+
+@pytest.mark.parametrize("ell,shards", [(4, 2), (4, 4), (5, 8)])
+def test_sigma4_shard_map_keeps_every_sweep_read_local(ell, shards):
+    """For every stored state x = (a, b) (a_0 < 2), the entries the q4 sweep reads for it -- the
+    advance-b row (a, b[1:] c) (|N| = 1 for string b) and, through the string-swap
+    symmetry W(a, b) = W(b, a) (reading R19), the advance-b row of (b, a) in place of the
+    advance-a row -- all lie on ONE shard, and so do those of its swap and complement images
+    (the q4 item group): a sweep reads only its own shard."""
+    L.load_library()
+
+    def home(a, b):  # shard of the advance-b row of (a, b), every appended c
+        ks = {L.lcsb_shard_locate_sigma4(ell, shards, _q4_encode(a, b[1:] + [c]))[0]
+              for c in range(4)}
+        assert len(ks) == 1
+        return ks.pop()
+
+    rng = np.random.default_rng(7)
+    xs = rng.integers(0, 4 ** (2 * ell), size=3000)
+    for x in xs:
+        a, b = _q4_decode(int(x), ell)
+        if a[0] >= 2:
+            continue
+        k = home(a, b)
+        assert home(b, a) == k                                   # adv_a via the swap
+        ca, cb = [3 - c for c in a], [3 - c for c in b]
+        assert home(ca, cb) == k and home(cb, ca) == k           # complement images
+
+
+@pytest.mark.gpu
+@pytest.mark.skipif(not has_cuda(), reason="needs a CUDA device")
+@pytest.mark.parametrize("ell,shards,dtype,form", [
+    (4, 2, "f32", "ks"), (4, 4, "f64", "ks"), (5, 8, "f32", "ks"), (5, 4, "f32", "two_array"),
+    (6, 2, "f64", "two_array"), (6, 8, "f64", "ks")])
+def test_sigma4_virtual_shards_bitwise_equal_unsharded(ell, shards, dtype, form):
+    """sigma = 4 (q4) on P virtual shards of one GPU: both table generations and the bound equal
+    the unsharded run bit for bit after 1, 2, 3 and 12 sweeps, and the oracle at l <= 5."""
+    import torch
+    from paper_2407_10925_b200 import Lcsb
+    from oracle import ft_oracle as fo
+    a = Lcsb(4, 2, ell, dtype=dtype, form=form)
+    b = Lcsb(4, 2, ell, dtype=dtype, form=form, shards=shards, virtual_shards=True)
+    assert a.kernel_in_use == "q4" and b.kernel_in_use == "q4" and b.num_shards == shards
+    for k in (1, 1, 1, 9):
+        a.sweep(k)
+        b.sweep(k)
+        assert np.array_equal(a.table(0), b.table(0))
+        assert np.array_equal(a.table(1), b.table(1))
+        ba, bb = a.bound(), b.bound()
+        assert (ba.R_max, ba.R_min, ba.E_at_Rmax, ba.E_at_Rmin) == \
+               (bb.R_max, bb.R_min, bb.E_at_Rmax, bb.E_at_Rmin)
+    if ell <= 5:
+        ref = fo.feasible_triplet(4, 2, ell, 12, form=form, dtype=dtype)
+        tab = b.table(0)
+        if dtype == "f32":
+            assert np.array_equal(tab, ref["table"])
+        else:
+            np.testing.assert_allclose(tab, ref["table"], rtol=1e-12)
+    a.destroy()
+    b.destroy()
+    torch.cuda.empty_cache()
+
+
+@pytest.mark.gpu
+@pytest.mark.skipif(not has_cuda(), reason="needs a CUDA device")
+def test_sigma4_config3_virtual_shards_sampled():
+    """BASELINE config 3 at full size (4^16 states, fp32, KS) on 2 virtual shards: 2^20 seeded
+    states after 3 sweeps against the oracle's sampled mode, bit-exact (config 3 is the sigma = 4
+    workload BASELINE runs at 1/2/4/8 GPUs)."""
+    import torch
+    from paper_2407_10925_b200 import Lcsb
+    from oracle import ft_oracle as fo
+    from seeded_inputs import splitmix64_indices
+    h = Lcsb(4, 2, 8, dtype="f32", shards=2, virtual_shards=True)
+    idx = splitmix64_indices(0x240710925, 1 << 20, 4 ** 16)
+    h.sweep(3)
+    assert np.array_equal(h.table_gather(idx),
+                          fo.sample_values(4, 2, 8, 3, idx, form="ks", dtype="f32"))
+    b = h.bound()  # KS after 3 sweeps: a negative (transient) bound; best stays the initial 0
+    assert b.R_min >= 0.0 and b.bound < 1.0 and b.best_bound == 0.0
+    h.destroy()
+    torch.cuda.empty_cache()
+
+
+def _pm_sigma4_worker(rank, world, port, out_dir, ell, dtype, form):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+    from paper_2407_10925_b200 import Lcsb
+    from paper_2407_10925_b200.dist import create_sharded
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    h = create_sharded(ell, dtype=dtype, transport="host", sigma=4, form=form)
+    out = {}
+    for n in (1, 2, 10):
+        h.sweep(n)
+        b = h.bound()
+        if rank == 0:
+            out[n] = (h.table(0), h.table(1), b)
+    dist.barrier()
+    h.destroy()
+    if rank == 0:
+        ok = []
+        ref = Lcsb(4, 2, ell, dtype=dtype, form=form)
+        for n in (1, 2, 10):
+            ref.sweep(n)
+            rb = ref.bound()
+            t0, t1, b = out[n]
+            ok += [np.array_equal(t0, ref.table(0)), np.array_equal(t1, ref.table(1)),
+                   (b.R_max, b.R_min, b.E_at_Rmax, b.E_at_Rmin) ==
+                   (rb.R_max, rb.R_min, rb.E_at_Rmax, rb.E_at_Rmin)]
+        ref.destroy()
+        np.save(os.path.join(out_dir, "pm4.npy"), np.array(ok))
+    dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+@pytest.mark.skipif(not has_cuda(), reason="needs a CUDA device")
+@pytest.mark.parametrize("world,ell,dtype,form", [(2, 5, "f32", "ks"), (4, 5, "f64", "two_array")])
+def test_sigma4_process_mode_multi_rank_on_one_gpu(tmp_path, world, ell, dtype, form):
+    """sigma = 4 over 2 and 4 PROCESSES sharing cuda:0 (host comm hooks): the row means and the
+    outputs pushed into the other processes' tables; tables and bounds equal the unsharded run."""
+    import torch.multiprocessing as mp
+    mp.spawn(_pm_sigma4_worker, args=(world, _free_port(), str(tmp_path), ell, dtype, form),
+             nprocs=world, join=True)
+    assert np.load(tmp_path / "pm4.npy").all()
