@@ -9,8 +9,11 @@ lcsb_sweep(S) + lcsb_bound.  metric = logical state-updates per second (sigma^(d
 Prints ONE JSON line on rank 0.  N = 1 runs config 4 (l = 17, the largest single-GPU config);
 under torchrun (N > 1) the ranks run config 5 (l = 18) with the half table sharded over the N
 GPUs (NCCL communicator + CUDA-IPC peer stores inside the library), timed as the
-max over ranks.  `--impl reference` times the CPU oracle (oracle/, the reference arm of this
-tier) on a bounded sample of the same workload.
+max over ranks, or `--workload config3` (sigma = 4, the q4 table sharded, §9b; strong scaling of
+the same workload as its N = 1 line).  For config 5 rank 0 also times the same sharded-path
+kernel on one GPU at l = 17 (`config.u1_same_kernel`), so U_P / (P U_1) is
+computable from the line.  `--impl reference` times the CPU oracle (oracle/, the reference arm
+of this tier) on a bounded sample of the same workload.
 """
 from __future__ import annotations
 
@@ -109,6 +112,11 @@ def _dist():
     ws = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # LCSB_BENCH_DEVICE=k (tests only): every rank on device k -- exercises the N > 1 code path
+    # on a one-GPU box with --transport host (no kernel waits on another rank); its timings
+    # are not scaling numbers
+    if os.environ.get("LCSB_BENCH_DEVICE") is not None:
+        local = int(os.environ["LCSB_BENCH_DEVICE"])
     return ws, rank, local
 
 
@@ -147,21 +155,55 @@ def workload_name(args, w) -> str:
             f"{w['dtype']} storage, {w['sweeps']} sweeps + 1 bound per step")
 
 
+def same_kernel_1gpu(w, stream, sweeps=8):
+    """State-updates/s of the sharded path's kernel (the binary half table, bin2) on ONE GPU at
+    l = 17 (config 4's size): the U_1 of SURVEY §8(e)'s efficiency U_P / (P U_1) for config 5,
+    whose l = 18 tables need the sharded layout's >= 2 GPUs."""
+    import torch
+    from paper_2407_10925_b200 import Lcsb
+    h = Lcsb(2, 2, 17, dtype=w["dtype"], form="two_array", symmetry=1, stream=stream)
+    h.sweep(3)
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s.record(stream)
+    h.sweep(sweeps)
+    e.record(stream)
+    torch.cuda.synchronize()
+    ms = s.elapsed_time(e) / sweeps
+    kernel = h.kernel_in_use
+    h.destroy()
+    torch.cuda.empty_cache()
+    return {"value": (1 << 34) / (ms / 1e3), "unit": "state-updates/s", "ms_per_sweep": ms,
+            "kernel": kernel, "what": "l = 17 (config 4 size), fp32, the half table (bin2), one "
+            "GPU, sweeps only"}
+
+
 def run_ours(args, w, ws, rank, local):
     import torch
     from paper_2407_10925_b200 import Lcsb
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     stream = torch.cuda.current_stream(dev)
+    sharded = ws > 1 or args.force_sharded
+
+    u1 = None
+    if sharded and w["sigma"] == 2 and not args.no_u1:
+        if rank == 0:
+            u1 = same_kernel_1gpu(w, stream)
+        torch.distributed.barrier()
 
     def make():
-        if ws > 1 or args.force_sharded:
+        if sharded:
             from paper_2407_10925_b200.dist import create_sharded
-            return create_sharded(w["ell"], dtype=w["dtype"], stream=stream)
+            return create_sharded(w["ell"], dtype=w["dtype"], stream=stream,
+                                  transport=args.transport, sigma=w["sigma"], form=w["form"])
         return Lcsb(w["sigma"], w["d"], w["ell"], dtype=w["dtype"], form=w["form"],
                     symmetry=args.symmetry)
 
-    h = make()
+    tc = time.perf_counter()
+    h = make()  # the first create of the process: cold (host map; schedule thread started)
+    cold_create_ms = (time.perf_counter() - tc) * 1e3
+    h.ready(wait=True)  # the L2 item schedule (host thread) is in place before warm-up
+    ready_ms = (time.perf_counter() - tc) * 1e3
     S = w["sweeps"]
     n_logical = h.num_states
     stored = h.stored_states
@@ -204,7 +246,8 @@ def run_ours(args, w, ws, rank, local):
     sweep_ms = [s.elapsed_time(e) for s, e, _ in sweep_evs]
     bound_ms = statistics.mean(e.elapsed_time(f) for _, e, f in sweep_evs)
     if ws > 1:
-        t = torch.tensor([ms_total], device=dev, dtype=torch.float64)
+        t = torch.tensor([ms_total], device=dev if args.transport == "nccl" else "cpu",
+                         dtype=torch.float64)
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         ms_total = float(t.item())
     ms_per_step = ms_total / args.steps
@@ -218,7 +261,7 @@ def run_ours(args, w, ws, rank, local):
     traffic = None
     # ncu DRAM bytes per launch of this workload's sweep kernel (tools/summarize_ncu.py)
     tpath = os.path.join(ROOT, "profiles", f"traffic_{args.workload}_{kernel_name}.json")
-    if os.path.exists(tpath):
+    if os.path.exists(tpath) and ws == 1:  # the committed profiles are single-GPU captures
         try:
             with open(tpath) as f:
                 traffic = json.load(f).get("dram_bytes_per_launch")
@@ -254,7 +297,8 @@ def run_ours(args, w, ws, rank, local):
     best = min(range(1, len(e2e_times)), key=lambda i: e2e_times[i])
     e2e_s = e2e_times[best]
     if ws > 1:
-        t = torch.tensor([e2e_s], device=dev, dtype=torch.float64)
+        t = torch.tensor([e2e_s], device=dev if args.transport == "nccl" else "cpu",
+                         dtype=torch.float64)
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         e2e_s = float(t.item())
     e2e_value = n_logical * S / e2e_s
@@ -268,7 +312,9 @@ def run_ours(args, w, ws, rank, local):
         "warmup": args.warmup,
         "ms_per_step": ms_per_step,
         "higher_is_better": True,
-        "scaling": "strong" if ws > 1 else "weak",
+        # config 4 / 5 (binary): per-GPU logical work roughly fixed as N grows (2^34 at N = 1,
+        # 2^36 / N at N > 1); config 3 and the others: the same workload at every N
+        "scaling": "weak" if w["sigma"] == 2 and w["ell"] >= 17 else "strong",
         "vs_baseline": None,
         "dtype": "f64" if w["dtype"] == "f64" else "f32-storage/f64-arith",
         "data": "synthetic (the method's only input is (sigma, d, l) and W_0 = 0)",
@@ -276,15 +322,25 @@ def run_ours(args, w, ws, rank, local):
             "workload": workload_name(args, w),
             "states": n_logical, "stored_states": stored, "sweeps_per_step": S,
             "kernel": kernel_name,
-            "parallelism": f"sharded over {ws} GPUs (NCCL + CUDA IPC peer stores)" if ws > 1
+            "parallelism": (f"sharded over {ws} GPUs ({args.transport} collectives + CUDA IPC "
+                            "peer stores)") if ws > 1
                            else ("process-sharded mode, 1 rank" if args.force_sharded
                                  else "single-gpu"),
+            "scaling_definition": ("U_P / (P U_1) with U_1 = u1_same_kernel (SURVEY 8(e))"
+                                   if u1 else "value_N / (N value_1), same workload"),
+            "u1_same_kernel": u1,
+            "cold_create_ms": cold_create_ms,
+            "create_to_schedule_ready_ms": ready_ms,
             "l2_flush": "inputs larger than L2 (each table %.1f GiB vs 126 MB L2)"
                         % (stored * (4 if w["dtype"] == "f32" else 8) / 2**30)
             if stored * 4 > 2**27 else "working set L2-resident (latency-bound config)",
             "sweep_ms_per_launch": launch_ms,
             "bound_ms_per_step": bound_ms,  # lcsb_bound: R reduction + W pass + E
+            # ncu DRAM bytes of one sweep launch per LOGICAL state update, and per STORED entry
+            # (the table holds 3/16 of the logical states for the quarter table)
             "dram_bytes_per_state_update": (traffic / (n_logical / ws)) if traffic else None,
+            "dram_bytes_per_stored_state": (traffic / (stored / ws)) if traffic else None,
+            "algorithmic_bytes_per_stored_state": alg_bytes / (stored / ws),
             "bound": b.bound, "bound_at_Rmin": b.bound_at_Rmin,
             "sweeps_per_s": S / (ms_per_step / 1e3),
             "sweep_only_state_updates_per_s": n_logical / (launch_ms / 1e3),
@@ -294,8 +350,12 @@ def run_ours(args, w, ws, rank, local):
                      "peak_kind": peak_kind,
                      "algorithmic_bytes_per_launch": alg_bytes,
                      "requested_bytes_per_launch": requested_bytes,
-                     "nvlink_bytes_per_launch": int((stored // ws) * (4 if w["dtype"] == "f32"
-                                                    else 8) * (1 - 1 / ws)),
+                     # peer stores per GPU per sweep: the outputs (and, q4, the row means) whose
+                     # owner is another shard -- a fraction (1 - 1/P) of the shard's (§9, §9b)
+                     "nvlink_bytes_per_launch": int(((stored // ws) * (4 if w["dtype"] == "f32"
+                                                    else 8) + (stored // ws // 16 * 8
+                                                    if kernel_name == "q4" else 0))
+                                                   * (1 - 1 / ws)),
                      "kernel": kernel_name + " sweep kernel"},
         "e2e": {"value": e2e_value, "unit": "state-updates/s",
                 "h2d_bytes_per_step": int(idx.nbytes),
@@ -304,6 +364,10 @@ def run_ours(args, w, ws, rank, local):
                         "seeded states to pinned host memory + lcsb_destroy, wall clock, best of "
                         "2 after one untimed",
                 "phases": phases[best],
+                # the first create of this process (host block map, schedule thread started) and
+                # the time until the L2 item schedule was in place
+                "cold_create_ms": cold_create_ms,
+                "cold_schedule_ready_ms": ready_ms,
                 "bound": be.bound},
         "gpu_launches": int(launches),
         "clocks": clk,
@@ -311,7 +375,25 @@ def run_ours(args, w, ws, rank, local):
     return res
 
 
-def cpu_baseline(w, budget_s=15.0):
+def _host_info():
+    model, ram = None, None
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+        with open("/proc/meminfo") as f:
+            for line in f:
+                if line.startswith("MemTotal"):
+                    ram = round(int(line.split()[1]) / 2**20, 1)
+                    break
+    except OSError:
+        pass
+    return model, ram
+
+
+def cpu_baseline(w, budget_s=15.0, single_s=4.0):
     """The oracle as it stands, timed on this host, on a bounded sample of the same workload:
     one sweep of F (oracle/ft_oracle.c fo_apply_F_at, all OpenMP threads) over a contiguous
     slice of the workload's logical states (the paper's thread-slice unit),
@@ -344,9 +426,24 @@ def cpu_baseline(w, budget_s=15.0):
         done += count
         if dt < budget_s / 20:
             count *= 2
+    # the same on ONE thread (single-thread and all-core numbers)
+    spent1, done1, c1 = 0.0, 0, 1 << 12
+    while spent1 < single_s:
+        idx = np.arange(x0 + done1, x0 + done1 + c1, dtype=np.uint64) % np.uint64(n)
+        t = time.perf_counter()
+        _parallel_apply_at(fo, w, [src] * d, idx, 1)
+        dt = time.perf_counter() - t
+        spent1 += dt
+        done1 += c1
+        if dt < single_s / 20:
+            c1 *= 2
+    model, ram = _host_info()
     return {"value": done / spent, "unit": "state-updates/s", "cores": cores, "kind": "oracle",
             "sample": f"{done} consecutive logical states of one sweep of {w['sigma']},{w['d']},"
-                      f"{w['ell']} ({table_note}), {spent:.1f} s"}
+                      f"{w['ell']} ({table_note}), {spent:.1f} s",
+            "single_thread_value": done1 / spent1,
+            "single_thread_sample": f"{done1} states, {spent1:.1f} s",
+            "cpu_model": model, "ram_gib": ram}
 
 
 def _parallel_apply_at(fo, w, src, idx, cores):
@@ -397,16 +494,26 @@ def _main(out):
     ap.add_argument("--symmetry", type=int, default=-1,
                     help="table layout: -1 auto, 1 half table, 2 quarter table (binary)")
     ap.add_argument("--force-sharded", action="store_true",
-                    help="use the NCCL process-sharded path even at N = 1 (tests the N > 1 code)")
+                    help="use the process-sharded path even at N = 1 (tests the N > 1 code)")
+    ap.add_argument("--transport", default="nccl", choices=["nccl", "host"],
+                    help="sharded collectives: NCCL on the stream (default) or host hooks (gloo)")
+    ap.add_argument("--ell", type=int, default=None,
+                    help="override the workload's l (tests of the code path only; the line's "
+                         "workload then names the changed l)")
+    ap.add_argument("--no-u1", action="store_true",
+                    help="config 5 at N > 1: skip timing the same kernel on one GPU at l = 17")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3  # timing rule: at least 3 warm-up steps
     ws, rank, local = _dist()
     if args.workload is None:
         args.workload = "config4" if ws == 1 else "config5"
-    w = WORKLOADS[args.workload]
-    if ws > 1 and args.workload != "config5":
-        raise SystemExit("N > 1 runs the sharded config5 workload")
+    w = dict(WORKLOADS[args.workload])
+    if args.ell:
+        w["ell"] = args.ell
+    if ws > 1 and args.workload not in ("config5", "config3", "config3ta"):
+        raise SystemExit("N > 1 runs a sharded workload: config5 (binary) or config3/config3ta "
+                         "(sigma = 4)")
 
     if args.impl == "reference":
         if rank != 0:
@@ -431,7 +538,10 @@ def _main(out):
         os.environ.setdefault("MASTER_PORT", "29517")
         os.environ.setdefault("RANK", str(rank))
         os.environ.setdefault("WORLD_SIZE", str(ws))
-        torch.distributed.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if args.transport == "host":
+            torch.distributed.init_process_group("gloo")
+        else:
+            torch.distributed.init_process_group("nccl", device_id=torch.device("cuda", local))
     res = run_ours(args, w, ws, rank, local)
     if rank == 0:
         if not args.no_cpu_baseline and ws == 1:

@@ -216,6 +216,13 @@ int lcsb_shard_locate_sigma4(int32_t ell, int32_t shards, uint64_t logical, int3
 int lcsb_quarter_locate(int32_t ell, int32_t block_log4, uint64_t logical, uint64_t* stored,
                         uint64_t* n_stored);
 
+/* Host preparations that affect only speed -- the quarter table's L2 item schedule, which
+ * lcsb_create builds on a host thread so that it returns without waiting (about 0.4-1.5 s at
+ * l = 17) -- are installed by the first lcsb_sweep / lcsb_bound after they are ready; sweeps
+ * before that run the natural item order, with bit-identical results.  lcsb_ready installs them
+ * if ready and returns 1 (0 = still being built; wait != 0 blocks until they are).  -1 on error. */
+int32_t lcsb_ready(lcsb_t* h, int32_t wait);
+
 int64_t lcsb_sweeps_done(const lcsb_t* h);
 int32_t lcsb_num_shards(const lcsb_t* h);   /* P (1 when unsharded) */
 uint64_t lcsb_num_states(const lcsb_t* h);   /* logical states sigma^(d l) */

@@ -9,8 +9,12 @@
 #include <stdlib.h>
 #include <string.h>
 
+#include <atomic>
 #include <new>
+#include <thread>
 #include <vector>
+
+#include <nvtx3/nvToolsExt.h>  // header-only NVTX v3: no-ops unless a profiler is attached
 
 #include "lcsb_internal.cuh"
 
@@ -36,6 +40,12 @@ struct lcsb {
   size_t qsched_bytes;
   uint64_t qsched_n;
   unsigned long long* qcounter;  // quarter table: work counter of the scheduled kernels
+  // the schedule is built on a host thread (lcsb_create returns without waiting for it); the
+  // sweeps run in the natural item order -- identical results -- until install_schedule
+  // uploads it at the start of a later call
+  std::thread* qthread;
+  std::atomic<int>* qready;
+  std::vector<uint32_t>* qpending;
   int bin2_variant;  // 0 auto; see pick_bin2_variant
   int bin2q_variant; // 0 auto; LCSB_BIN2Q_VARIANT (A/B only)
   uint64_t n_logical;
@@ -65,6 +75,7 @@ struct lcsb {
   int* barrier_buf;
   // CUDA-graph replay of G consecutive sweeps for launch-latency-bound (small) tables
   cudaStream_t cap_stream;
+  int cap_capturing;  // inside a graph capture: no allocation / upload may happen
   cudaGraphExec_t graph[kMaxGen];
   int graph_sweeps;
   int64_t sweeps_done;
@@ -75,6 +86,13 @@ struct lcsb {
 };
 
 static thread_local char g_err[512] = "";
+
+// NVTX ranges (SURVEY §5 tracing): each public call, each sweep enqueue and each barrier shows
+// up on an nsys / ncu timeline (host ranges; the kernels correlate through the CUDA API)
+struct NvtxRange {
+  explicit NvtxRange(const char* m) { nvtxRangePushA(m); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
 
 static int set_err(lcsb_t* h, int code, const char* fmt, ...) {
   char* buf = h ? h->err : g_err;
@@ -445,6 +463,7 @@ static const lcsb_comm_hooks* hooks(const lcsb_t* h) {
 
 static int barrier(lcsb_t* h) {  // process mode: every rank's preceding work is complete
   if (h->mode != MODE_PROCESS) return LCSB_OK;
+  NvtxRange r("lcsb barrier");
   if (const lcsb_comm_hooks* c = hooks(h)) {  // host hooks: drain the stream, then meet
     CU(h, cudaStreamSynchronize((cudaStream_t)h->cfg.stream));
     if (c->barrier(c->ctx) != 0) return set_err(h, LCSB_ENCCL, "comm hook barrier failed");
@@ -501,6 +520,12 @@ extern "C" void lcsb_destroy(lcsb_t* h) {
       for (int i = 0; i < h->ntab; ++i) dev_free(h, h->tabs[k][i], h->tab_bytes);
   dev_free(h, h->red, 256);
   dev_free(h, h->qmap, h->qmap_bytes);
+  if (h->qthread) {  // a schedule still being built is not needed any more
+    h->qthread->join();
+    delete h->qthread;
+  }
+  delete h->qready;
+  delete h->qpending;
   dev_free(h, h->qsched, h->qsched_bytes);
   dev_free(h, h->qcounter, 256);
   for (int k = 0; k < h->P; ++k)
@@ -561,6 +586,8 @@ static int exchange_ipc(lcsb_t* h) {
   if (dbuf) cudaFree(dbuf);
   return rc;
 }
+
+static int install_schedule(lcsb_t* h, bool wait);
 
 extern "C" int lcsb_create_ex(const lcsb_config* cfg, lcsb_t** out) {
   if (!out) return set_err(nullptr, LCSB_EINVAL, "out is NULL");
@@ -691,20 +718,24 @@ extern "C" int lcsb_create_ex(const lcsb_config* cfg, lcsb_t** out) {
     e = ok ? cudaMemcpyAsync(h->qmap, hm, h->qmap_bytes, cudaMemcpyHostToDevice, s) : cudaSuccess;
     if (e == cudaSuccess && ok) e = cudaStreamSynchronize(s);
     if (ok && e == cudaSuccess && !getenv("LCSB_NO_QSCHED") && cfg->ell - h->qM - 1 >= 4) {
-      std::vector<uint32_t> sched;  // the L2 item order of the sweep (large tables)
-      if (quarter_schedule(cfg->ell, h->qK, h->qM, hm, sched)) {
-        h->qsched_n = sched.size();
-        h->qsched_bytes = sched.size() * sizeof(uint32_t);
-        h->qsched = (uint32_t*)dev_alloc(h, h->qsched_bytes);
-        // dynamic claiming pays for the 4^6 tiles of fp32 (20.7 vs 26.6 GB read at l = 17); with
-        // the 4x more, smaller items of fp64 (4^5 tiles) the single counter costs more than it
-        // saves (l = 16: 3.99 vs 3.28 ms static)
-        if (h->qsched && h->qM >= 6 && !getenv("LCSB_QSTATIC"))
-          h->qcounter = (unsigned long long*)dev_alloc(h, 256);
-        if (h->qsched) {
-          e = cudaMemcpyAsync(h->qsched, sched.data(), h->qsched_bytes, cudaMemcpyHostToDevice, s);
-          if (e == cudaSuccess) e = cudaStreamSynchronize(s);
-        }
+      // the L2 item order of the sweep (large tables), built on a host thread: it changes only
+      // the order of the items, never a value (every output is written once from the previous
+      // table), so the first sweeps may run without it
+      h->qpending = new (std::nothrow) std::vector<uint32_t>();
+      h->qready = new (std::nothrow) std::atomic<int>(0);
+      if (h->qpending && h->qready &&
+          quarter_schedule_cached(cfg->ell, h->qK, h->qM, *h->qpending)) {
+        h->qready->store(1);  // built before in this process: installed right below
+        h->qthread = new (std::nothrow) std::thread([] {});
+      } else if (h->qpending && h->qready) {
+        std::vector<uint32_t> mcopy(hm, hm + nb);
+        const int ell = cfg->ell, K = h->qK, M = h->qM;
+        std::vector<uint32_t>* pend = h->qpending;
+        std::atomic<int>* rdy = h->qready;
+        h->qthread = new (std::nothrow) std::thread([ell, K, M, pend, rdy, m = std::move(mcopy)]() {
+          if (!quarter_schedule(ell, K, M, m.data(), *pend)) pend->clear();
+          rdy->store(1, std::memory_order_release);
+        });
       }
     }
     free(hm);
@@ -737,6 +768,14 @@ extern "C" int lcsb_create_ex(const lcsb_config* cfg, lcsb_t** out) {
     }
   }
   h->cur = 0;
+  const bool sync = getenv("LCSB_QSCHED_SYNC") ||
+                    (h->qready && h->qready->load(std::memory_order_acquire));
+  if (sync && install_schedule(h, true) != LCSB_OK) {  // ready (cached) or A/B: no overlap
+    char msg[512];
+    snprintf(msg, sizeof msg, "%s", h->err);
+    lcsb_destroy(h);
+    return set_err(nullptr, LCSB_ECAPACITY, "%s", msg);
+  }
   *out = h;
   return LCSB_OK;
 }
@@ -753,6 +792,7 @@ extern "C" int lcsb_create(int32_t sigma, int32_t d, int32_t ell, int32_t dtype,
 
 extern "C" int lcsb_reset(lcsb_t* h) {
   if (!h) return set_err(nullptr, LCSB_EINVAL, "handle is NULL");
+  NvtxRange r("lcsb_reset");
   CU(h, cudaSetDevice(h->device));
   int rc = barrier(h);  // nobody is still sweeping into our tables
   if (rc != LCSB_OK) return rc;
@@ -809,6 +849,49 @@ static void fill_bin2(const lcsb_t* h, Bin2Args* a, int shard, int in_slot, int 
   }
 }
 
+// Upload the quarter table's item schedule once its host thread has finished (wait: block until
+// then).  Graphs captured before use the natural order: they are dropped and re-captured.
+static int install_schedule(lcsb_t* h, bool wait) {
+  if (!h->qthread) return LCSB_OK;
+  if (!wait && !h->qready->load(std::memory_order_acquire)) return LCSB_OK;
+  h->qthread->join();
+  delete h->qthread;
+  h->qthread = nullptr;
+  std::vector<uint32_t>& sched = *h->qpending;
+  if (!sched.empty()) {
+    cudaStream_t s = (cudaStream_t)h->cfg.stream;
+    const size_t bytes = sched.size() * sizeof(uint32_t);
+    uint32_t* d = (uint32_t*)dev_alloc(h, bytes);
+    if (!d) return set_err(h, LCSB_ECAPACITY, "schedule allocation failed");
+    // pageable source: the call returns once the bytes are staged, so `sched` may be freed
+    CU(h, cudaMemcpyAsync(d, sched.data(), bytes, cudaMemcpyHostToDevice, s));
+    // dynamic claiming pays for the 4^6 tiles of fp32 (20.7 vs 26.6 GB read at l = 17); with
+    // the 4x more, smaller items of fp64 (4^5 tiles) the single counter costs more than it
+    // saves (l = 16: 3.99 vs 3.28 ms static)
+    if (h->qM >= 6 && !getenv("LCSB_QSTATIC")) {
+      h->qcounter = (unsigned long long*)dev_alloc(h, 256);
+      if (!h->qcounter) return set_err(h, LCSB_ECAPACITY, "counter allocation failed");
+    }
+    h->qsched = d;
+    h->qsched_bytes = bytes;
+    h->qsched_n = sched.size();
+    for (int i = 0; i < kMaxGen; ++i)
+      if (h->graph[i]) {
+        cudaGraphExecDestroy(h->graph[i]);
+        h->graph[i] = nullptr;
+      }
+  }
+  sched.clear();
+  sched.shrink_to_fit();
+  return LCSB_OK;
+}
+
+extern "C" int32_t lcsb_ready(lcsb_t* h, int32_t wait) {
+  if (!h) return set_err(nullptr, LCSB_EINVAL, "handle is NULL"), -1;
+  if (install_schedule(h, wait != 0) != LCSB_OK) return -1;
+  return h->qthread ? 0 : 1;
+}
+
 static void fill_bin2q(const lcsb_t* h, Bin2QArgs* a, int in_slot, int out_slot) {
   memset(a, 0, sizeof *a);
   a->src = h->tabs[0][in_slot];
@@ -838,7 +921,9 @@ static int sweep_graph(lcsb_t* h, cudaStream_t s) {
     if (!h->cap_stream) CU(h, cudaStreamCreateWithFlags(&h->cap_stream, cudaStreamNonBlocking));
     const int64_t done = h->sweeps_done, launches = h->launches;
     CU(h, cudaStreamBeginCapture(h->cap_stream, cudaStreamCaptureModeThreadLocal));
+    h->cap_capturing = 1;
     int rc = enqueue_sweeps(h, h->graph_sweeps, h->cap_stream);
+    h->cap_capturing = 0;
     cudaGraph_t g = nullptr;
     cudaError_t e = cudaStreamEndCapture(h->cap_stream, &g);
     if (rc != LCSB_OK) {
@@ -865,8 +950,13 @@ static int sweep_graph(lcsb_t* h, cudaStream_t s) {
 
 extern "C" int lcsb_sweep(lcsb_t* h, int64_t n) {
   if (!h) return set_err(nullptr, LCSB_EINVAL, "handle is NULL");
+  NvtxRange r("lcsb_sweep");
   if (n < 0) return set_err(h, LCSB_EINVAL, "n must be >= 0");
   CU(h, cudaSetDevice(h->device));
+  {
+    int rc = install_schedule(h, false);
+    if (rc != LCSB_OK) return rc;
+  }
   cudaStream_t s = (cudaStream_t)h->cfg.stream;
   if (n > 0 && h->mode == MODE_PROCESS) {
     // every rank is done with the tables (e.g. a rank-local lcsb_table read since the last
@@ -896,6 +986,11 @@ extern "C" int lcsb_sweep(lcsb_t* h, int64_t n) {
 
 static int enqueue_sweeps(lcsb_t* h, int64_t n, cudaStream_t s) {
   for (int64_t it = 0; it < n; ++it) {
+    NvtxRange r("sweep");
+    if (h->qthread && !h->cap_capturing) {  // the schedule finished during a long call
+      int rc = install_schedule(h, false);
+      if (rc != LCSB_OK) return rc;
+    }
     const int out = (h->cur + 1) % h->ntab;  // the slot of the oldest table
     cudaError_t e = cudaSuccess;
     if (h->kernel == 2) {
@@ -983,8 +1078,13 @@ static double bound_from(const lcsb_t* h, double rho) {
 
 extern "C" int lcsb_bound(lcsb_t* h, lcsb_bound_t* out) {
   if (!h || !out) return set_err(h, LCSB_EINVAL, "NULL argument");
+  NvtxRange r("lcsb_bound");
   if (h->sweeps_done < 1) return set_err(h, LCSB_ESTATE, "lcsb_bound needs at least one sweep");
   CU(h, cudaSetDevice(h->device));
+  {
+    int rc = install_schedule(h, false);
+    if (rc != LCSB_OK) return rc;
+  }
   cudaStream_t s = (cudaStream_t)h->cfg.stream;
   const int prev = slot_back(h, 1);
   // quarter table (two-array binary): ONE pass gives R_max, R_min and D = min(F(u,u) - u); then

@@ -180,6 +180,7 @@ uint64_t quarter_map_entries(int ell, int K);  // half-table blocks of 4^K entri
 uint64_t quarter_slots(int ell, int K);        // stored (canonical) blocks
 bool build_quarter_map(int ell, int K, uint32_t* map);
 bool quarter_schedule(int ell, int K, int M, const uint32_t* map, std::vector<uint32_t>& out);
+bool quarter_schedule_cached(int ell, int K, int M, std::vector<uint32_t>& out);  // no build
 
 // Sharding of the sigma = 4, d = 2 complement-folded table over 2^p shards.
 // State s: 4l bits, character group g (g = 0 the heads) at bits [4(l-1-g), 4(l-g)), the a digit

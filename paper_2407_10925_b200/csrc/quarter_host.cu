@@ -58,12 +58,23 @@ bool build_quarter_map(int ell, int K, uint32_t* map) {
 // neighbouring CTAs, so the block's four windows -- its two logical images -- come from DRAM once
 // and from L2 after.  The order is a permutation of the pair representatives; the arithmetic of
 // every item is unchanged.  Cached per (l, K, M): it depends on nothing else.
+static std::mutex g_mu;
+static int c_ell = 0, c_K = 0, c_M = 0;  // (A/B: LCSB_QSCHED=1 / 2 is read once per process)
+static std::vector<uint32_t> g_cache;
+
+bool quarter_schedule_cached(int ell, int K, int M, std::vector<uint32_t>& out) {
+  std::lock_guard<std::mutex> lock(g_mu);
+  if (c_ell == ell && c_K == K && c_M == M) {
+    out = g_cache;
+    return true;
+  }
+  return false;
+}
+
 bool quarter_schedule(int ell, int K, int M, const uint32_t* map,
                              std::vector<uint32_t>& out) {
-  static std::mutex mu;
-  static int c_ell = 0, c_K = 0, c_M = 0;  // (A/B: LCSB_QSCHED=1 / 2 is read once per process)
-  static std::vector<uint32_t> cache;
-  std::lock_guard<std::mutex> lock(mu);
+  std::vector<uint32_t>& cache = g_cache;
+  std::lock_guard<std::mutex> lock(g_mu);
   // entries hold the tile index in kQHintShift bits (plan_config rejects larger tile counts)
   if (2 * (ell - 1 - M) > kQHintShift) return false;
   if (c_ell == ell && c_K == K && c_M == M) {

@@ -15,7 +15,7 @@ from paper_2407_10925_b200 import lcsb as L
 def _header_functions():
     src = open(os.path.join(ROOT, "include", "lcsb.h")).read()
     src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
-    return sorted(set(re.findall(r"\b(lcsb_[a-z_]+)\s*\(", src)))
+    return sorted(set(re.findall(r"\b(lcsb_[a-z_0-9]+)\s*\(", src)))
 
 
 def test_library_exports_every_header_symbol():

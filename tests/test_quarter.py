@@ -199,6 +199,7 @@ def test_quarter_dynamic_claiming_under_graph_replay(monkeypatch):
             monkeypatch.setenv(k, v)
         h = L.Lcsb(2, 2, 12, dtype="f32")
         assert h.kernel_in_use == "bin2q"
+        h.ready(wait=True)  # the schedule (built on a host thread) is used from the first sweep
         h.sweep(70)
         h.sweep(33)
         vals.append((h.table_gather(idx), h.table_gather(idx, which=1), h.bound().bound))
@@ -302,3 +303,36 @@ def test_quarter_one_pass_bound_equals_two_pass_at_config4():
     for key in ("E_at_Rmax", "E_at_Rmin", "bound_at_Rmax", "bound_at_Rmin"):
         g, r = getattr(bq, key), getattr(bh, key)
         assert abs(g - r) <= 1e-12 * max(1.0, abs(r)), (key, g, r)
+
+
+@pytest.mark.gpu
+@pytest.mark.skipif(not has_cuda(), reason="needs a CUDA device")
+def test_quarter_schedule_installed_mid_run_changes_nothing():
+    """lcsb_create returns before the L2 item schedule is built (host thread); sweeps before its
+    installation run the natural item order.  A run that gets the schedule mid-way, one that has
+    it from the first sweep and one that never has it are bit-identical (l = 14 fp32)."""
+    import os
+    from seeded_inputs import splitmix64_indices
+    idx = splitmix64_indices(0x240710925, 1 << 18, 1 << 28)
+    runs = []
+    for mode in ("async", "sync", "none"):
+        if mode == "none":
+            os.environ["LCSB_NO_QSCHED"] = "1"
+        try:
+            h = L.Lcsb(2, 2, 14, dtype="f32")
+        finally:
+            os.environ.pop("LCSB_NO_QSCHED", None)
+        if mode == "sync":
+            assert h.ready(wait=True)
+        h.sweep(2)
+        if mode == "async":
+            h.ready(wait=True)  # installed here, after 2 sweeps in the natural order
+        h.sweep(20)
+        b = h.bound()
+        runs.append((h.table_gather(idx), h.table_gather(idx, which=1), b.R_max, b.R_min,
+                     b.bound_at_Rmax, b.bound_at_Rmin))
+        assert h.ready() is True
+        h.destroy()
+    for r in runs[1:]:
+        assert np.array_equal(r[0], runs[0][0]) and np.array_equal(r[1], runs[0][1])
+        assert r[2:] == runs[0][2:]
