@@ -295,7 +295,7 @@ __device__ __forceinline__ void pair_quads_f32(const T* bw, const T* bp, const T
   }
 }
 
-template <typename T, uint32_t TT, int MW, int MP, bool WMODE>
+template <typename T, uint32_t TT, int MW, int MP, bool WMODE, int NT = kThreads, int UNR = 1>
 __device__ __forceinline__ void pair_quads(const T* bw, const T* bp, const T* src, T* dst,
                                            const uint64_t* meta, bool self, const T* prev,
                                            BAcc& ba) {
@@ -306,7 +306,10 @@ __device__ __forceinline__ void pair_quads(const T* bw, const T* bp, const T* sr
   const uint64_t of = meta[3], om = meta[4], opf = meta[5], opm = meta[6];
   const bool rows_x = of != kNone || om != kNone;
   const bool rows_p = !self && (opf != kNone || opm != kNone);
-  for (uint32_t qd = threadIdx.x; qd < TT / 4; qd += blockDim.x) {
+  // UNR > 1 (bound pass): several quads unrolled, so their global loads of u and v_prev are
+  // issued together (more loads in flight per thread)
+#pragma unroll UNR
+  for (uint32_t qd = threadIdx.x; qd < TT / 4; qd += NT) {
     const uint32_t o0 = 4 * qd;
     const uint32_t g = 2 * pairswap32(o0), u = 2 * (TT - 4 - o0);
     // psi(o0 + k) sits at oQ1p + qb + pairswap(3 - k): the quad reversed as (3, 1, 2, 0)
@@ -477,7 +480,7 @@ __device__ __forceinline__ void qissue(const QGeo& g, const QItem& it, uint64_t 
   }
 }
 
-template <typename T, int M, int S, bool WMODE, int MINB = 1, int NT = kThreads>
+template <typename T, int M, int S, bool WMODE, int MINB = 1, int NT = kThreads, int UNR = 1>
 __global__ void __launch_bounds__(NT, MINB) bin2q_kernel(Bin2QArgs a) {
   using C = QCfg<T, M, S, WMODE, MINB>;
   constexpr uint32_t TT = C::TT, WIN = C::WIN;
@@ -569,7 +572,7 @@ __global__ void __launch_bounds__(NT, MINB) bin2q_kernel(Bin2QArgs a) {
   if constexpr (sizeof(T) == 4 && !WMODE)                                          \
     pair_quads_f32<T, TT, MW, MP>(bw, bp, src, dst, meta, self);                   \
   else                                                                             \
-    pair_quads<T, TT, MW, MP, WMODE>(bw, bp, src, dst, meta, self, prev, ba)
+    pair_quads<T, TT, MW, MP, WMODE, NT, UNR>(bw, bp, src, dst, meta, self, prev, ba)
     switch (mw * 4 + mp) {
       case 0: LCSB_Q1(0, 0); break;
       case 1: LCSB_Q1(0, 1); break;
@@ -595,16 +598,17 @@ __global__ void __launch_bounds__(NT, MINB) bin2q_kernel(Bin2QArgs a) {
   if (WMODE) block_red3_to(ba.rmax, ba.rmin, ba.dmin, a.red_out);
 }
 
-template <typename T, int M, int S, bool WMODE, int MINB = 1, int NT = kThreads>
+template <typename T, int M, int S, bool WMODE, int MINB = 1, int NT = kThreads, int UNR = 1>
 cudaError_t launch_q(const Bin2QArgs& a, cudaStream_t s, int sms) {
   using C = QCfg<T, M, S, WMODE, MINB>;
   static uint64_t cap = 0;
   if (cap == 0) {
-    cudaError_t e = cudaFuncSetAttribute(bin2q_kernel<T, M, S, WMODE, MINB, NT>,
+    cudaError_t e = cudaFuncSetAttribute(bin2q_kernel<T, M, S, WMODE, MINB, NT, UNR>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
     if (e != cudaSuccess) return e;
     int per_sm = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, bin2q_kernel<T, M, S, WMODE, MINB, NT>,
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm,
+                                                      bin2q_kernel<T, M, S, WMODE, MINB, NT, UNR>,
                                                       NT, C::SMEM) != cudaSuccess ||
         per_sm < 1) {
       cudaGetLastError();
@@ -617,7 +621,7 @@ cudaError_t launch_q(const Bin2QArgs& a, cudaStream_t s, int sms) {
       (a.sched && a.sched_m == M) ? a.nitems : (1ull << (2 * (a.ell - 1 - M)));
   uint64_t blocks = cap < ntiles ? cap : ntiles;
   if (blocks < 1) blocks = 1;
-  bin2q_kernel<T, M, S, WMODE, MINB, NT><<<(unsigned)blocks, NT, C::SMEM, s>>>(a);
+  bin2q_kernel<T, M, S, WMODE, MINB, NT, UNR><<<(unsigned)blocks, NT, C::SMEM, s>>>(a);
   return cudaGetLastError();
 }
 
@@ -632,6 +636,10 @@ cudaError_t dispatch_q(const Bin2QArgs& a, int dtype, int M, cudaStream_t s, int
     if (wv == 1) return launch_q<float, 6, 1, true, 2>(a, s, sms);
     // LCSB_BIN2Q_WDIRECT=2 (A/B): one 512-thread CTA per SM with two stages (prefetch overlap)
     if (wv == 2) return launch_q<float, 6, 2, true, 1, 512>(a, s, sms);
+    // 3 / 4 / 5: quads unrolled by 2 (3 CTAs/SM), by 4 (2 CTAs/SM), by 2 (2 CTAs/SM)
+    if (wv == 3) return launch_q<float, 6, 1, true, 3, kThreads, 2>(a, s, sms);
+    if (wv == 4) return launch_q<float, 6, 1, true, 2, kThreads, 4>(a, s, sms);
+    if (wv == 5) return launch_q<float, 6, 1, true, 2, kThreads, 2>(a, s, sms);
     return launch_q<float, 6, 1, true, 3>(a, s, sms);
   }
   if (WMODE && dtype == LCSB_F64 && M == 5) return launch_q<double, 5, 1, true, 3>(a, s, sms);

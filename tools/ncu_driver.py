@@ -25,6 +25,7 @@ def main():
         w["ell"] = args.ell
     h = Lcsb(w["sigma"], w["d"], w["ell"], dtype=w["dtype"], form=w["form"],
              symmetry=args.symmetry)
+    h.ready(wait=True)  # the quarter table's item schedule (host thread) before the first sweep
     h.sweep(args.sweeps)
     b = h.bound()
     torch.cuda.synchronize()

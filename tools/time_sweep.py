@@ -29,6 +29,7 @@ def main():
     from paper_2407_10925_b200 import Lcsb
     from seeded_inputs import splitmix64_indices
     h = Lcsb(args.sigma, args.d, args.ell, dtype=args.dtype, form=args.form)
+    h.ready(wait=True)
     h.sweep(args.warm)
     torch.cuda.synchronize()
     times = []
