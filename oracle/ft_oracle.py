@@ -27,6 +27,13 @@ Bound bookkeeping (both R readings are computed, reading R5 in DESIGN.md):
   best: the largest R - E over the evaluations so far, starting from the triplet (v_0, 0, 0)
         (Alg. 2 lines 2, 8-10), reported as a bound.
 
+Integer offsets (``offsets=True``, two-array form only, DESIGN.md reading
+R23): by translation invariance, F(v + c 1) = F(v) + c 1 (Lemma 1 (2)), so the
+table may hold s_n = v_n - o_n with an integer o_n: each sweep subtracts c_n = floor(min s_n),
+  s_{n+1} = round_storage(F(s_n, s_n) - c_n),   o_{n+1} = o_n + c_n,   o_0 = 0,
+which keeps the stored magnitudes (and so the fp32 rounding) small.  The bound in stored terms:
+R = max(s_n - s_{n-1}) + c_{n-1} (min likewise), W = (s_n + R) - F(s_n, s_n).
+
 Parity pins: tests/test_oracle_pins.py.
 """
 from __future__ import annotations
@@ -218,7 +225,7 @@ class Run:
     """
 
     def __init__(self, sigma: int, d: int, ell: int, form: str = "auto", dtype: str = "f64",
-                 threads: int = 0):
+                 threads: int = 0, offsets: bool = False):
         if sigma < 2 or d < 2 or ell < 1:
             raise ValueError("need sigma >= 2, d >= 2, ell >= 1")
         self.sigma, self.d, self.ell = sigma, d, ell
@@ -232,6 +239,11 @@ class Run:
         self.sweeps_done = 0
         self.best = {"max": 0.0, "min": 0.0}     # best r - eps per R reading (Alg. 2 line 3)
         self.best_sweep = {"max": 0, "min": 0}
+        if offsets and self.form != FORM_TWO_ARRAY:
+            raise ValueError("integer offsets are defined for the two-array form (reading R23)")
+        self.offsets = bool(offsets)
+        self.off = 0.0        # o_n of the newest table (an integer, exact in fp64)
+        self.off_prev = 0.0   # o_{n-1}
 
     # -- one application of F (Alg. 2 line 4 / Alg. 5 line 6) --
     def sweep(self, count: int = 1):
@@ -245,14 +257,25 @@ class Run:
                 g = self.gens[0]
                 new = apply_F(self.sigma, self.d, self.ell, [g] * self.d, threads=self.threads,
                               two_array=True)
+                c = 0.0
+                if self.offsets:  # s_{n+1} = F(s_n) - floor(min s_n)  (translation invariance)
+                    c = float(math.floor(float(g.min())))
+                    new = new - c
                 new = round_storage(new, self.dtype)
                 self.prev = g
                 self.gens = [new]
+                self.off_prev, self.off = self.off, self.off + c
             self.sweeps_done += 1
 
     @property
     def newest(self) -> np.ndarray:
+        """The newest table as stored (with offsets: s_n; the values are s_n + o_n)."""
         return self.gens[0]
+
+    def values(self, which: int = 0) -> np.ndarray:
+        """The iterate's values: stored + integer offset (o_n, or o_{n-1} for which = 1)."""
+        t = self.gens[0] if which == 0 else self.prev
+        return t + (self.off if which == 0 else self.off_prev)
 
     def _W(self, R: float) -> np.ndarray:
         v = self.gens[0]
@@ -275,7 +298,8 @@ class Run:
         if self.sweeps_done < 1:
             raise RuntimeError("bound needs at least one sweep")
         diff = self.gens[0] - self.prev
-        out = {"R_max": float(diff.max()), "R_min": float(diff.min())}
+        c = self.off - self.off_prev  # offsets: v_n - v_{n-1} = s_n - s_{n-1} + c_{n-1}
+        out = {"R_max": float(diff.max()) + c, "R_min": float(diff.min()) + c}
         for mode in ("max", "min"):
             R = out["R_" + mode]
             W = self._W(R)
@@ -291,10 +315,12 @@ class Run:
 
 
 def feasible_triplet(sigma: int, d: int, ell: int, sweeps: int, form: str = "auto",
-                     dtype: str = "f64", bound_every: bool = False, threads: int = 0) -> dict:
+                     dtype: str = "f64", bound_every: bool = False, threads: int = 0,
+                     offsets: bool = False) -> dict:
     """Run `sweeps` sweeps from the zero start; evaluate the bound after every sweep
-    (``bound_every``, as Alg. 2/5 do) or only after the last one (as BASELINE.json's configs)."""
-    run = Run(sigma, d, ell, form, dtype, threads)
+    (``bound_every``, as Alg. 2/5 do) or only after the last one (as BASELINE.json's configs).
+    ``table`` / ``prev`` are the stored tables (with offsets: ``values`` holds s + o)."""
+    run = Run(sigma, d, ell, form, dtype, threads, offsets)
     res = None
     for _ in range(sweeps):
         run.sweep(1)
@@ -304,6 +330,8 @@ def feasible_triplet(sigma: int, d: int, ell: int, sweeps: int, form: str = "aut
         res = run.bound()
     res["table"] = run.newest
     res["prev"] = run.prev
+    res["values"] = run.values(0)
+    res["offset"] = run.off
     return res
 
 

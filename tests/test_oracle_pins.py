@@ -518,3 +518,54 @@ def test_best_running_max_to_table2(form):
             last[mode] = b
     assert fo.floor6(last["max"]) == 0.758576
     assert fo.floor6(last["min"]) == 0.758576
+
+
+# ---------------------------------------------------------------- integer offsets (C17 / R23)
+
+@pytest.mark.parametrize("ell", [1, 3, 6, 8])
+def test_offsets_fp64_equal_plain_run(ell):
+    """Translation invariance (Lemma 1 (2)): the offset run's values s_n + o_n
+    equal the plain iterate (fp64: to rounding, 1e-12 relative) and the bound is the same to
+    1e-12 (Table 2's value at convergence)."""
+    a = fo.Run(2, 2, ell, "two_array", "f64")
+    b = fo.Run(2, 2, ell, "two_array", "f64", offsets=True)
+    for k in range(1, 121):
+        a.sweep()
+        b.sweep()
+        if k in (1, 2, 5, 40, 120):
+            np.testing.assert_allclose(b.values(0), a.newest, rtol=1e-12, atol=1e-12)
+            np.testing.assert_allclose(b.values(1), a.prev, rtol=1e-12, atol=1e-12)
+    ra, rb = a.bound(), b.bound()
+    for key in ("R_max", "R_min", "bound_at_Rmax", "bound_at_Rmin"):
+        assert rb[key] == pytest.approx(ra[key], abs=1e-12), key
+    assert b.off > 0 and b.off == int(b.off)
+
+
+def test_offsets_ell1_exact_and_bounded_storage():
+    """l = 1 two-array with offsets, exact dyadics: values (k+1)/2, (k-1)/2 at sweep k as
+    without offsets; c_n = floor(min s_n) is an integer and the stored minimum stays in [0, 1)
+    after the subtraction."""
+    run = fo.Run(2, 2, 1, "two_array", "f64", offsets=True)
+    for k in range(1, 30):
+        run.sweep()
+        assert list(run.values(0)) == [(k + 1) / 2, (k - 1) / 2, (k - 1) / 2, (k + 1) / 2]
+        assert run.off == int(run.off)
+        assert 0.0 <= run.newest.min() < 1.0 + 0.5   # min(s_n) - c_{n-1} plus one sweep's growth
+    res = run.bound()
+    assert res["bound_at_Rmax"] == pytest.approx(2 / 3, abs=1e-15)
+
+
+def test_offsets_cut_fp32_drift():
+    """fp32 storage: the offset run's bound is closer to the fp64 bound than the plain fp32 run
+    (C17: the stored magnitudes stay small); l = 8, 150 sweeps."""
+    ref = fo.feasible_triplet(2, 2, 8, 150, form="two_array", dtype="f64")["bound_at_Rmax"]
+    plain = fo.feasible_triplet(2, 2, 8, 150, form="two_array", dtype="f32")["bound_at_Rmax"]
+    off = fo.feasible_triplet(2, 2, 8, 150, form="two_array", dtype="f32",
+                              offsets=True)["bound_at_Rmax"]
+    assert abs(off - ref) < abs(plain - ref)
+    assert abs(off - ref) / ref < 2e-6
+
+
+def test_offsets_rejected_for_ks():
+    with pytest.raises(ValueError):
+        fo.Run(2, 2, 3, "ks", offsets=True)
