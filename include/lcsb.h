@@ -136,6 +136,15 @@ typedef struct {
   /* process-sharded mode: host communication hooks instead of NCCL (see lcsb_comm_hooks); the
    * struct must stay valid until lcsb_destroy returns.  NULL = NCCL (nccl_id). */
   const lcsb_comm_hooks* comm;
+  /* integer-offset storage (reading R23), two-array form only:
+   *   0 = none (default);
+   *   1 = each table holds s = v - o with an integer o: before every sweep c = floor(min s) of
+   *       the table it reads, and the sweep stores round(F(s) - c) (F(v + c) = F(v) + c,
+   *       translation invariance, Lemma 1 (2)), so stored magnitudes stay small and
+   *       fp32 storage drifts less.  Values read out (lcsb_table) and the bound are those of v.
+   *       Binary: the quarter table (l >= 3) or, below that, the generic kernel; other sigma
+   *       (d = 2): the generic kernel.  KS form, the half table and sharding: LCSB_EINVAL. */
+  int32_t offset_policy;
 } lcsb_config;
 
 /* Fill *cfg with defaults: sigma=2,d=2,ell=1, F32, AUTO form, R_MAX, symmetry auto, AUTO

@@ -183,8 +183,10 @@ __device__ __forceinline__ void sel4(bool s, const double (&x)[4], const double 
   }
 }
 // bound pass accumulators at one stored output: u = v_n[x], p = v_{n-1}[x], f = F(u,u)[x]
+// (sweep with integer offsets: rmin = min of the stored values, sh = the shift -c, reading R23)
 struct BAcc {
   double rmax, rmin, dmin;
+  double sh;
 };
 __device__ __forceinline__ void bacc(double u, double p, double f, BAcc& b) {
   const double dd = u - p;
@@ -212,7 +214,7 @@ __device__ __forceinline__ void ld4s(const double* p, double (&v)[4]) {
 // widened to fp64 once.  The A/B load order alternates across threads so each 128-bit smem load
 // is conflict-free (2-way for permuted x windows).
 // bound pass (WMODE): src = u = v_n, prev = v_{n-1}; nothing is stored
-template <typename T, int MODE, bool WMODE>
+template <typename T, int MODE, bool WMODE, bool OFS = false>
 __device__ __forceinline__ void q0_group(const double (&G)[4], uint32_t r, uint32_t half_rows,
                                          const T* src, T* dst, uint64_t of, uint64_t om,
                                          const T* prev, BAcc& ba) {
@@ -228,6 +230,17 @@ __device__ __forceinline__ void q0_group(const double (&G)[4], uint32_t r, uint3
     if (om != kNone)
       bacc((double)__ldcs(src + om + rm), (double)__ldcs(prev + om + rm),
            q0_val(v3, v2, v1, v0), ba);
+  } else if (OFS) {  // store round(F(s) - c); track the min of what is stored
+    if (of != kNone) {
+      const T st = (T)(q0_val(v0, v1, v2, v3) + ba.sh);
+      st_out(dst + of + r, st);
+      ba.rmin = dmin(ba.rmin, (double)st);
+    }
+    if (om != kNone) {
+      const T st = (T)(q0_val(v3, v2, v1, v0) + ba.sh);
+      st_out(dst + om + (half_rows - 1 - r), st);
+      ba.rmin = dmin(ba.rmin, (double)st);
+    }
   } else {
     if (of != kNone) st_out(dst + of + r, (T)q0_val(v0, v1, v2, v3));
     if (om != kNone) st_out(dst + om + (half_rows - 1 - r), (T)q0_val(v3, v2, v1, v0));
@@ -295,7 +308,8 @@ __device__ __forceinline__ void pair_quads_f32(const T* bw, const T* bp, const T
   }
 }
 
-template <typename T, uint32_t TT, int MW, int MP, bool WMODE, int NT = kThreads, int UNR = 1>
+template <typename T, uint32_t TT, int MW, int MP, bool WMODE, int NT = kThreads, int UNR = 1,
+          bool OFS = false>
 __device__ __forceinline__ void pair_quads(const T* bw, const T* bp, const T* src, T* dst,
                                            const uint64_t* meta, bool self, const T* prev,
                                            BAcc& ba) {
@@ -366,18 +380,25 @@ __device__ __forceinline__ void pair_quads(const T* bw, const T* bp, const T* sr
         bacc((double)uu[2], (double)pp[2], v[2], ba);
         bacc((double)uu[0], (double)pp[0], v[3], ba);
       }
+    } else if (OFS) {  // round(F(s) - c) (the shift is an integer: exact before the rounding)
+      const T s0 = (T)(v[0] + ba.sh), s1 = (T)(v[1] + ba.sh), s2 = (T)(v[2] + ba.sh),
+              s3 = (T)(v[3] + ba.sh);
+      if (oQ1 != kNone) st4(dst + oQ1 + o0, (double)s0, (double)s1, (double)s2, (double)s3);
+      if (oQ1p != kNone) st4(dst + oQ1p + qb, (double)s3, (double)s1, (double)s2, (double)s0);
+      if (oQ1 != kNone || oQ1p != kNone)
+        ba.rmin = dmin(ba.rmin, dmin(dmin((double)s0, (double)s1), dmin((double)s2, (double)s3)));
     } else {
       if (oQ1 != kNone) st4(dst + oQ1 + o0, v[0], v[1], v[2], v[3]);
       if (oQ1p != kNone) st4(dst + oQ1p + qb, v[3], v[1], v[2], v[0]);
     }
     // Q0 rows of the four groups
     if (rows_x) {
-      q0_group<T, MW, WMODE>(A, g >> 2, TT / 2, src, dst, of, om, prev, ba);
-      q0_group<T, MW, WMODE>(B, (g >> 2) + 1, TT / 2, src, dst, of, om, prev, ba);
+      q0_group<T, MW, WMODE, OFS>(A, g >> 2, TT / 2, src, dst, of, om, prev, ba);
+      q0_group<T, MW, WMODE, OFS>(B, (g >> 2) + 1, TT / 2, src, dst, of, om, prev, ba);
     }
     if (rows_p) {
-      q0_group<T, MP, WMODE>(Ap, u >> 2, TT / 2, src, dst, opf, opm, prev, ba);
-      q0_group<T, MP, WMODE>(Bp, (u >> 2) + 1, TT / 2, src, dst, opf, opm, prev, ba);
+      q0_group<T, MP, WMODE, OFS>(Ap, u >> 2, TT / 2, src, dst, opf, opm, prev, ba);
+      q0_group<T, MP, WMODE, OFS>(Bp, (u >> 2) + 1, TT / 2, src, dst, opf, opm, prev, ba);
     }
   }
 }
@@ -480,7 +501,8 @@ __device__ __forceinline__ void qissue(const QGeo& g, const QItem& it, uint64_t 
   }
 }
 
-template <typename T, int M, int S, bool WMODE, int MINB = 1, int NT = kThreads, int UNR = 1>
+template <typename T, int M, int S, bool WMODE, int MINB = 1, int NT = kThreads, int UNR = 1,
+          bool OFS = false>
 __global__ void __launch_bounds__(NT, MINB) bin2q_kernel(Bin2QArgs a) {
   using C = QCfg<T, M, S, WMODE, MINB>;
   constexpr uint32_t TT = C::TT, WIN = C::WIN;
@@ -505,7 +527,8 @@ __global__ void __launch_bounds__(NT, MINB) bin2q_kernel(Bin2QArgs a) {
   const int tid = threadIdx.x;
   const uint64_t G = gridDim.x;
 
-  BAcc ba{-INFINITY, INFINITY, INFINITY};
+  BAcc ba{-INFINITY, INFINITY, INFINITY, 0.0};
+  if (OFS) ba.sh = a.ost->shift;
   const T* prev = reinterpret_cast<const T*>(a.prev);
   // items: with a schedule, item c is the tile pair of tile sched[c] (c = blockIdx.x + k G);
   // without one, the pair representatives in tile order
@@ -569,10 +592,10 @@ __global__ void __launch_bounds__(NT, MINB) bin2q_kernel(Bin2QArgs a) {
     const T* bw = buf;
     const T* bp = buf + WIN;
 #define LCSB_Q1(MW, MP)                                                            \
-  if constexpr (sizeof(T) == 4 && !WMODE)                                          \
+  if constexpr (sizeof(T) == 4 && !WMODE && !OFS)                                  \
     pair_quads_f32<T, TT, MW, MP>(bw, bp, src, dst, meta, self);                   \
   else                                                                             \
-    pair_quads<T, TT, MW, MP, WMODE, NT, UNR>(bw, bp, src, dst, meta, self, prev, ba)
+    pair_quads<T, TT, MW, MP, WMODE, NT, UNR, OFS>(bw, bp, src, dst, meta, self, prev, ba)
     switch (mw * 4 + mp) {
       case 0: LCSB_Q1(0, 0); break;
       case 1: LCSB_Q1(0, 1); break;
@@ -596,19 +619,21 @@ __global__ void __launch_bounds__(NT, MINB) bin2q_kernel(Bin2QArgs a) {
     if (tid == 0) fill((int)s, buf);
   }
   if (WMODE) block_red3_to(ba.rmax, ba.rmin, ba.dmin, a.red_out);
+  if (OFS && !WMODE) block_min_to(ba.rmin, a.omin);
 }
 
-template <typename T, int M, int S, bool WMODE, int MINB = 1, int NT = kThreads, int UNR = 1>
+template <typename T, int M, int S, bool WMODE, int MINB = 1, int NT = kThreads, int UNR = 1,
+          bool OFS = false>
 cudaError_t launch_q(const Bin2QArgs& a, cudaStream_t s, int sms) {
   using C = QCfg<T, M, S, WMODE, MINB>;
   static uint64_t cap = 0;
   if (cap == 0) {
-    cudaError_t e = cudaFuncSetAttribute(bin2q_kernel<T, M, S, WMODE, MINB, NT, UNR>,
+    cudaError_t e = cudaFuncSetAttribute(bin2q_kernel<T, M, S, WMODE, MINB, NT, UNR, OFS>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
     if (e != cudaSuccess) return e;
     int per_sm = 0;
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm,
-                                                      bin2q_kernel<T, M, S, WMODE, MINB, NT, UNR>,
+                                                      bin2q_kernel<T, M, S, WMODE, MINB, NT, UNR, OFS>,
                                                       NT, C::SMEM) != cudaSuccess ||
         per_sm < 1) {
       cudaGetLastError();
@@ -621,7 +646,7 @@ cudaError_t launch_q(const Bin2QArgs& a, cudaStream_t s, int sms) {
       (a.sched && a.sched_m == M) ? a.nitems : (1ull << (2 * (a.ell - 1 - M)));
   uint64_t blocks = cap < ntiles ? cap : ntiles;
   if (blocks < 1) blocks = 1;
-  bin2q_kernel<T, M, S, WMODE, MINB, NT, UNR><<<(unsigned)blocks, NT, C::SMEM, s>>>(a);
+  bin2q_kernel<T, M, S, WMODE, MINB, NT, UNR, OFS><<<(unsigned)blocks, NT, C::SMEM, s>>>(a);
   return cudaGetLastError();
 }
 
@@ -643,6 +668,28 @@ cudaError_t dispatch_q(const Bin2QArgs& a, int dtype, int M, cudaStream_t s, int
     return launch_q<float, 6, 1, true, 3>(a, s, sms);
   }
   if (WMODE && dtype == LCSB_F64 && M == 5) return launch_q<double, 5, 1, true, 3>(a, s, sms);
+  if (!WMODE && a.ost) {  // integer offsets (reading R23): the fp64 Q1 path, shift and min
+    constexpr int NT = kThreads;
+    if (dtype == LCSB_F32) {
+      switch (M) {
+        case 6: return launch_q<float, 6, 1, false, 3, NT, 1, true>(a, s, sms);
+        case 5: return launch_q<float, 5, 2, false, 1, NT, 1, true>(a, s, sms);
+        case 4: return launch_q<float, 4, 2, false, 1, NT, 1, true>(a, s, sms);
+        case 3: return launch_q<float, 3, 2, false, 1, NT, 1, true>(a, s, sms);
+        case 2: return launch_q<float, 2, 2, false, 1, NT, 1, true>(a, s, sms);
+        case 1: return launch_q<float, 1, 2, false, 1, NT, 1, true>(a, s, sms);
+      }
+    } else {
+      switch (M) {
+        case 5: return launch_q<double, 5, 2, false, 2, NT, 1, true>(a, s, sms);
+        case 4: return launch_q<double, 4, 2, false, 1, NT, 1, true>(a, s, sms);
+        case 3: return launch_q<double, 3, 2, false, 1, NT, 1, true>(a, s, sms);
+        case 2: return launch_q<double, 2, 2, false, 1, NT, 1, true>(a, s, sms);
+        case 1: return launch_q<double, 1, 2, false, 1, NT, 1, true>(a, s, sms);
+      }
+    }
+    return cudaErrorInvalidValue;
+  }
   if (dtype == LCSB_F32) {
     switch (M) {
       case 6: return launch_q<float, 6, 1, WMODE, 3>(a, s, sms);  // A/B: variant 10
@@ -686,7 +733,7 @@ int bin2q_variant_m(int dtype, int variant) {
 
 cudaError_t launch_bin2q_sweep(const Bin2QArgs& a, int dtype, int M, int variant, cudaStream_t s,
                                int sms) {
-  if (variant <= 0) return dispatch_q<false>(a, dtype, M, s, sms);
+  if (variant <= 0 || a.ost) return dispatch_q<false>(a, dtype, M, s, sms);
   if (variant >= kQVariants) return cudaErrorInvalidValue;
 #define LCSB_QV(T, M_, S_, MB_) \
   if (d.m == M_ && d.s == S_ && d.mb == MB_) return launch_q<T, M_, S_, false, MB_>(a, s, sms);

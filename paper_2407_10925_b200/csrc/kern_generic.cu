@@ -155,10 +155,20 @@ __global__ void __launch_bounds__(256) generic_sweep_kernel(GenericArgs a) {
   for (int i = 0; i < kMaxD; ++i) zero[i] = 0.0;
   T* dst = reinterpret_cast<T*>(a.dst);
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  // integer offsets (reading R23): store round(F(s) + shift), reduce the min of the stored values
+  const double sh = a.ost ? a.ost->shift : 0.0;
+  double mn = INFINITY;
   for (uint64_t x = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; x < a.n; x += stride) {
     double v = g.F_at(a, x, zero);
-    dst[x] = (T)v;  // storage rounding: RNE for float
+    if (a.ost) {
+      const T st = (T)(v + sh);  // F(s) + (-c): exact in fp64 (c an integer), then the rounding
+      dst[x] = st;
+      mn = dmin(mn, (double)st);
+    } else {
+      dst[x] = (T)v;  // storage rounding: RNE for float
+    }
   }
+  if (a.ost) block_min_to(mn, a.omin);
 }
 
 __device__ inline void block_max2(double w0, double w1, unsigned long long* out) {

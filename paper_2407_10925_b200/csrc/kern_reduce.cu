@@ -25,6 +25,23 @@ __global__ void red_init_kernel(unsigned long long* red, unsigned min_mask) {
   }
 }
 
+__global__ void offset_init_kernel(OffState* o) {
+  const int i = threadIdx.x;
+  if (i < kMaxGen) {
+    o->off[i] = 0.0;
+    o->mn[i] = ord_enc(0.0);
+  }
+  if (i == 0) o->shift = 0.0;
+}
+
+__global__ void offset_prep_kernel(OffState* o, int cur, int out) {
+  const double m = dec_ord(o->mn[cur]);
+  const double c = floor(m);  // an integer: exact, and so is every shift by it (reading R23)
+  o->off[out] = o->off[cur] + c;
+  o->shift = -c;
+  o->mn[out] = ord_enc(INFINITY);
+}
+
 __device__ __forceinline__ void acc(double dd, double& mx, double& mn) {
   mx = dmax(mx, dd);
   mn = dmin(mn, dd);
@@ -90,18 +107,19 @@ struct ExpandTabs {
 };
 
 template <typename T>
-__global__ void expand_kernel(ExpandTabs tabs, int p, int symmetric, int q4, uint64_t nlogical,
-                              int ell,
+__global__ void expand_kernel(ExpandTabs tabs, int p, int symmetric, int q4,
+                              const double* __restrict__ add, uint64_t nlogical, int ell,
                               const uint32_t* __restrict__ qmap, int K, uint64_t first,
                               uint64_t count, const uint64_t* __restrict__ idx, double* out) {
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  const double off = add ? *add : 0.0;  // integer offset of the generation (exact)
   const uint64_t half = symmetric ? nlogical / 2 : 0;
   const uint64_t top = symmetric ? nlogical - 1 : 0;
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count; i += stride) {
     uint64_t y = idx ? idx[i] : first + i;
     if (symmetric && y >= half) y = top - y;  // Eq. (comp_eq)
     if (qmap) {  // quarter table: the orbit representative under the string swap / psi
-      out[i] = (double)reinterpret_cast<const T*>(tabs.t[0])[qstored(qmap, y, K)];
+      out[i] = (double)reinterpret_cast<const T*>(tabs.t[0])[qstored(qmap, y, K)] + off;
       continue;
     }
     if (q4) {  // sigma = 4 digit-key shards
@@ -109,7 +127,7 @@ __global__ void expand_kernel(ExpandTabs tabs, int p, int symmetric, int q4, uin
       continue;
     }
     const uint32_t sh = shard_of_stored(y, 2 * ell, p);
-    out[i] = (double)reinterpret_cast<const T*>(tabs.t[sh])[local_of_stored(y, 2 * ell, p)];
+    out[i] = (double)reinterpret_cast<const T*>(tabs.t[sh])[local_of_stored(y, 2 * ell, p)] + off;
   }
 }
 
@@ -137,8 +155,17 @@ cudaError_t launch_rdiff(const void* newest, const void* prev, uint64_t n, int d
   return cudaGetLastError();
 }
 
+cudaError_t launch_offset_init(OffState* o, cudaStream_t s) {
+  offset_init_kernel<<<1, 32, 0, s>>>(o);
+  return cudaGetLastError();
+}
+cudaError_t launch_offset_prep(OffState* o, int cur, int out, cudaStream_t s) {
+  offset_prep_kernel<<<1, 1, 0, s>>>(o, cur, out);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_expand(const void* const* tabs, int p, int dtype, int symmetric, int q4,
-                          uint64_t nlogical, int ell,
+                          const double* add, uint64_t nlogical, int ell,
                           const uint32_t* qmap, int K, uint64_t first, uint64_t count,
                           const uint64_t* idx, double* out, cudaStream_t s) {
   uint64_t blocks = (count + 255) / 256;
@@ -147,9 +174,9 @@ cudaError_t launch_expand(const void* const* tabs, int p, int dtype, int symmetr
   ExpandTabs t;
   for (int k = 0; k < kMaxShards; ++k) t.t[k] = (k < (1 << p)) ? tabs[k] : nullptr;
   if (dtype == LCSB_F32)
-    expand_kernel<float><<<(unsigned)blocks, 256, 0, s>>>(t, p, symmetric, q4, nlogical, ell, qmap, K, first, count, idx, out);
+    expand_kernel<float><<<(unsigned)blocks, 256, 0, s>>>(t, p, symmetric, q4, add, nlogical, ell, qmap, K, first, count, idx, out);
   else
-    expand_kernel<double><<<(unsigned)blocks, 256, 0, s>>>(t, p, symmetric, q4, nlogical, ell, qmap, K, first, count, idx, out);
+    expand_kernel<double><<<(unsigned)blocks, 256, 0, s>>>(t, p, symmetric, q4, add, nlogical, ell, qmap, K, first, count, idx, out);
   return cudaGetLastError();
 }
 

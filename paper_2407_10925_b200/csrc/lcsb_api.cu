@@ -76,6 +76,7 @@ struct lcsb {
   // CUDA-graph replay of G consecutive sweeps for launch-latency-bound (small) tables
   cudaStream_t cap_stream;
   int cap_capturing;  // inside a graph capture: no allocation / upload may happen
+  OffState* ost;      // integer offsets (reading R23): per-slot offsets, mins, shift; NULL = off
   cudaGraphExec_t graph[kMaxGen];
   int graph_sweeps;
   int64_t sweeps_done;
@@ -167,7 +168,7 @@ static const int kQuarterAutoEll = 12;
 
 // ---------------------------------------------------------------- planning
 struct Plan {
-  int form, symmetric, kernel, ntab, p, P, mode, qK, qM, dtype_code;
+  int form, symmetric, kernel, ntab, p, P, mode, qK, qM, dtype_code, offsets;
   uint64_t n_logical, n_stored, n_local;
   size_t esize;
   uint64_t bytes;  // device bytes this handle allocates
@@ -242,7 +243,20 @@ static int plan_config(const lcsb_config* c, Plan* p, char* why, size_t whylen) 
   // at most 2^kQHintShift (larger counts would alias tiles)
   const bool quarter_ok = sym_ok && !sharded && qK >= 2 && qK <= c->ell - 1 && c->ell - qK <= 16 &&
                           2 * (c->ell - 1 - qM) <= kQHintShift;
+  // integer offsets (reading R23): two-array form, unsharded; the quarter table or the generic
+  // kernel carry the per-sweep shift and min
+  const int ofs = c->offset_policy;
+  if (ofs != 0 && ofs != 1) {
+    snprintf(why, whylen, "offset_policy must be 0 or 1");
+    return LCSB_EINVAL;
+  }
+  if (ofs && (form != LCSB_FORM_TWO_ARRAY || sharded || c->symmetry == 1)) {
+    snprintf(why, whylen,
+             "integer offsets need the two-array form, no sharding and symmetry -1, 0 or 2");
+    return LCSB_EINVAL;
+  }
   int sym = c->symmetry;
+  if (sym < 0 && ofs) sym = quarter_ok ? 2 : 0;
   if (sym < 0) sym = (quarter_ok && c->ell >= kQuarterAutoEll) ? 2 : (sym_ok ? 1 : 0);
   if (sym == 1 && !sym_ok) {
     snprintf(why, whylen,
@@ -309,7 +323,10 @@ static int plan_config(const lcsb_config* c, Plan* p, char* why, size_t whylen) 
   p->qK = (sym == 2) ? qK : 0;
   p->qM = (sym == 2) ? qM : 0;
   p->kernel = sym == 2 ? 5 : (sym ? 2 : 1);
-  if (!sym && c->sigma == 4 && c->d == 2 && c->ell >= q4_min_ell() &&
+  p->offsets = ofs;
+  if (ofs) {
+    // the quarter table (binary) or the generic full-table kernel: nothing else below
+  } else if (!sym && c->sigma == 4 && c->d == 2 && c->ell >= q4_min_ell() &&
       c->kernel == LCSB_KERNEL_AUTO)
     p->kernel = 3;  // sigma = 4, d = 2 swap-paired TMA kernel (kern_q4.cu)
   else if (p->kernel == 1 && c->kernel == LCSB_KERNEL_AUTO && small_supported(c->sigma, c->d, n))
@@ -346,6 +363,7 @@ static int plan_config(const lcsb_config* c, Plan* p, char* why, size_t whylen) 
                   sizeof(double);
   }
   if (sym == 2) p->bytes += quarter_map_entries(c->ell, qK) * sizeof(uint32_t);
+  if (ofs) p->bytes += 512;  // OffState
   return LCSB_OK;
 }
 
@@ -519,6 +537,7 @@ extern "C" void lcsb_destroy(lcsb_t* h) {
     if (owns(h, k))
       for (int i = 0; i < h->ntab; ++i) dev_free(h, h->tabs[k][i], h->tab_bytes);
   dev_free(h, h->red, 256);
+  dev_free(h, h->ost, 512);
   dev_free(h, h->qmap, h->qmap_bytes);
   if (h->qthread) {  // a schedule still being built is not needed any more
     h->qthread->join();
@@ -678,6 +697,13 @@ extern "C" int lcsb_create_ex(const lcsb_config* cfg, lcsb_t** out) {
     lcsb_destroy(h);
     return set_err(nullptr, LCSB_ECAPACITY, "scratch allocation failed");
   }
+  if (p.offsets) {  // W_0 = 0 with offset 0; min of the zero table = 0
+    h->ost = (OffState*)dev_alloc(h, 512);
+    if (!h->ost || launch_offset_init(h->ost, s) != cudaSuccess) {
+      lcsb_destroy(h);
+      return set_err(nullptr, LCSB_ECAPACITY, "offset state allocation failed");
+    }
+  }
   if (h->kernel == 3) {  // row-mean ring of the pooled-history KS sweep, zero (W_0 = 0)
     // rows of stored states, split evenly over the shards
     h->pool_bytes = (size_t)(h->n_logical / 32 / (uint64_t)h->P) * sizeof(double);
@@ -812,6 +838,7 @@ extern "C" int lcsb_reset(lcsb_t* h) {
     for (int i = 0; i < kMaxGen; ++i)
       if (h->spools[k][i])
         CU(h, cudaMemsetAsync(h->spools[k][i], 0, h->spool_bytes[k], (cudaStream_t)h->cfg.stream));
+  if (h->ost) CU(h, launch_offset_init(h->ost, (cudaStream_t)h->cfg.stream));
   h->cur = 0;
   h->pcur = 0;
   h->sweeps_done = 0;
@@ -1016,7 +1043,14 @@ static int enqueue_sweeps(lcsb_t* h, int64_t n, cudaStream_t s) {
     } else if (h->kernel == 5) {
       Bin2QArgs a;
       fill_bin2q(h, &a, h->cur, out);
-      if (a.counter) e = cudaMemsetAsync(a.counter, 0, sizeof(unsigned long long), s);
+      if (h->ost) {  // integer offsets: c = floor(min s) of the table read, then the sweep
+        e = launch_offset_prep(h->ost, h->cur, out, s);
+        h->launches += 1;
+        a.ost = h->ost;
+        a.omin = &h->ost->mn[out];
+      }
+      if (a.counter && e == cudaSuccess)
+        e = cudaMemsetAsync(a.counter, 0, sizeof(unsigned long long), s);
       if (e == cudaSuccess) e = launch_bin2q_sweep(a, h->cfg.dtype, h->qM, h->bin2q_variant, s, h->sms);
       h->launches += 1;
     } else if (h->kernel == 3) {
@@ -1056,8 +1090,15 @@ static int enqueue_sweeps(lcsb_t* h, int64_t n, cudaStream_t s) {
         }
         e = launch_small_pooled(a, h->cfg.dtype, s, h->sms);
       } else {
-        e = (h->kernel == 4) ? launch_small(a, h->cfg.dtype, false, s, h->sms)
-                             : launch_generic_sweep(a, h->cfg.dtype, s, h->sms);
+        if (h->ost) {  // integer offsets (generic kernel, two-array form)
+          e = launch_offset_prep(h->ost, h->cur, out, s);
+          h->launches += 1;
+          a.ost = h->ost;
+          a.omin = &h->ost->mn[out];
+        }
+        if (e == cudaSuccess)
+          e = (h->kernel == 4) ? launch_small(a, h->cfg.dtype, false, s, h->sms)
+                               : launch_generic_sweep(a, h->cfg.dtype, s, h->sms);
       }
       h->launches += 1;
     }
@@ -1091,6 +1132,14 @@ extern "C" int lcsb_bound(lcsb_t* h, lcsb_bound_t* out) {
   // E = max(0, max W) = max(0, R - D) for both R (reading R21).  Other kernels: the R
   // reduction, then the W pass at the known R.
   const bool one_pass = h->kernel == 5;
+  // integer offsets: v_n - v_{n-1} = s_n - s_{n-1} + (o_n - o_{n-1})  (reading R23)
+  double cofs = 0.0;
+  if (h->ost) {
+    double offs[kMaxGen];
+    CU(h, cudaMemcpyAsync(offs, h->ost->off, sizeof offs, cudaMemcpyDeviceToHost, s));
+    CU(h, cudaStreamSynchronize(s));
+    cofs = offs[h->cur] - offs[prev];
+  }
   CU(h, launch_red_init(h->red, s, one_pass ? 6u : 2u));
   h->launches += 1;
   for (int k = h->first; !one_pass && k < h->first + h->nown; ++k) {
@@ -1101,6 +1150,13 @@ extern "C" int lcsb_bound(lcsb_t* h, lcsb_bound_t* out) {
   if (!one_pass) {
     int rc = allreduce_slots(h, 0, 2, 2u);  // the global R before the W pass
     if (rc != LCSB_OK) return rc;
+    if (h->ost) {  // the W pass reads R from the device: add the offset step there
+      unsigned long long r[2];
+      CU(h, cudaMemcpyAsync(r, h->red, sizeof r, cudaMemcpyDeviceToHost, s));
+      CU(h, cudaStreamSynchronize(s));
+      for (int i = 0; i < 2; ++i) r[i] = ord_enc(ord_dec(r[i]) + cofs);
+      CU(h, cudaMemcpyAsync(h->red, r, sizeof r, cudaMemcpyHostToDevice, s));
+    }
   }
   if (h->kernel == 2) {
     const int M = bin2_tma_wpass_m(h->cfg.dtype, h->cfg.ell, h->p);
@@ -1159,7 +1215,9 @@ extern "C" int lcsb_bound(lcsb_t* h, lcsb_bound_t* out) {
   CU(h, cudaMemcpyAsync(h->red_host, h->red, kRedSlots * sizeof(unsigned long long),
                         cudaMemcpyDeviceToHost, s));
   CU(h, cudaStreamSynchronize(s));
-  const double R[2] = {ord_dec(h->red_host[0]), ord_dec(h->red_host[1])};
+  // (generic two-pass with offsets: red[0..1] already hold the shifted R)
+  const double radd = (one_pass && h->ost) ? cofs : 0.0;
+  const double R[2] = {ord_dec(h->red_host[0]) + radd, ord_dec(h->red_host[1]) + radd};
   double Wm[2] = {ord_dec(h->red_host[2]), ord_dec(h->red_host[3])};
   if (one_pass) {  // max W = max(u + R - F(u,u)) = R - min(F(u,u) - u)   (reading R21)
     const double D = ord_dec(h->red_host[2]);
@@ -1231,7 +1289,7 @@ static int readout(lcsb_t* h, int which, uint64_t first, uint64_t count, const u
       e = cudaMemcpyAsync(ibuf, host_idx + off, c * sizeof(uint64_t), cudaMemcpyHostToDevice, s);
     if (e == cudaSuccess)
       e = launch_expand(tabs, h->p, h->cfg.dtype, h->symmetric != 0 || h->kernel == 3,
-                        h->kernel == 3,
+                        h->kernel == 3, h->ost ? &h->ost->off[slot] : nullptr,
                         h->n_logical, h->cfg.ell, h->qmap, h->qK,
                         first + off, c, host_idx ? ibuf : nullptr, dbuf, s);
     if (e == cudaSuccess) {

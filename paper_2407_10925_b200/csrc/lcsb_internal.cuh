@@ -46,6 +46,16 @@ inline uint64_t resident_blocks(K kernel, int tpb, int sms) {
   return (uint64_t)per_sm * (uint64_t)sms;
 }
 
+// Integer-offset storage (lcsb_config.offset_policy, reading R23; two-array form):
+// ring slot i holds s = v - off[i]; before each sweep (cur -> out) the prep kernel sets
+// c = floor(min s[cur]) (mn[cur], ordered encoding), off[out] = off[cur] + c and shift = -c; the
+// sweep stores round(F(s) + shift) and reduces the min of what it stores into mn[out].
+struct OffState {
+  double off[kMaxGen];
+  unsigned long long mn[kMaxGen];
+  double shift;
+};
+
 // Reduction slots (device, unsigned long long each):
 //   0: R_max  1: R_min  2: max W at R_max  3: max W at R_min
 constexpr int kRedSlots = 4;
@@ -64,6 +74,10 @@ struct GenericArgs {
   const double* pin[kMaxD];
   double* pout[kMaxD];
   uint64_t headw_top;               // sigma^(d(l-1)): weight of the head digit group
+  // integer offsets (sweep mode): add ost->shift to every output before the storage rounding
+  // and reduce the min of the stored values into *omin; NULL = off
+  const OffState* ost;
+  unsigned long long* omin;
 };
 
 constexpr int kMaxShards = 8;
@@ -141,6 +155,9 @@ struct Bin2QArgs {
   // round-robin assignment
   unsigned long long* counter;
   int l2keep;  // policy of the pieces the schedule marks as reloaded soon: 0 normal, 1 evict-last
+  // integer offsets (sweep mode, as GenericArgs); NULL = off
+  const OffState* ost;
+  unsigned long long* omin;
 };
 // schedule entries: tile index in the low bits, L2 hint bits (one per window piece) at the top
 constexpr int kQHintShift = 28;
@@ -288,6 +305,21 @@ __device__ __forceinline__ void block_max2_to(double w0, double w1, unsigned lon
   }
 }
 
+// block-wide min of v, one atomicMin (ordered encoding) into *out (blockDim % 32 == 0)
+__device__ __forceinline__ void block_min_to(double v, unsigned long long* out) {
+  __shared__ double sm[32];
+  for (int o = 16; o > 0; o >>= 1) v = dmin(v, __shfl_xor_sync(0xffffffffu, v, o));
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  if (lane == 0) sm[wid] = v;
+  __syncthreads();
+  if (wid == 0) {
+    const int nw = (blockDim.x + 31) >> 5;
+    v = lane < nw ? sm[lane] : INFINITY;
+    for (int o = 16; o > 0; o >>= 1) v = dmin(v, __shfl_xor_sync(0xffffffffu, v, o));
+    if (lane == 0) atomicMin(out, ord_enc(v));
+  }
+}
+
 // block-wide (max a, min b, min c), one atomic each into out[0] (max), out[1], out[2] (min)
 __device__ __forceinline__ void block_red3_to(double a, double b, double c,
                                               unsigned long long* out) {
@@ -350,6 +382,11 @@ uint32_t small_pool_per_row(int sigma, int d, int k);  // pooled means per row f
 cudaError_t launch_small_pooled(const GenericArgs& a, int dtype, cudaStream_t s, int sms);
 // slots whose bit is set in min_mask start at +inf (minima), the others at -inf (maxima)
 cudaError_t launch_red_init(unsigned long long* red, cudaStream_t s, unsigned min_mask = 2u);
+// integer offsets: zero every slot's offset, min(s) = 0 (the zero tables of W_0), shift 0
+cudaError_t launch_offset_init(OffState* o, cudaStream_t s);
+// before a sweep cur -> out: c = floor(min s[cur]), off[out] = off[cur] + c, shift = -c,
+// mn[out] = +inf (the sweep reduces into it)
+cudaError_t launch_offset_prep(OffState* o, int cur, int out, cudaStream_t s);
 cudaError_t launch_rdiff(const void* newest, const void* prev, uint64_t n, int dtype,
                          unsigned long long* red, cudaStream_t s, int sms);
 // tabs[k]: the table of shard k (unsharded: tabs[0]); p = log2(shards); qmap != NULL: quarter
@@ -358,6 +395,7 @@ cudaError_t launch_rdiff(const void* newest, const void* prev, uint64_t n, int d
 // nlogical-1-y (the complement: Eq. comp_eq for sigma = 2, d -> 3-d for sigma = 4)
 // q4: sigma = 4 digit-key shards (q4_key / q4_local) instead of the binary key
 cudaError_t launch_expand(const void* const* tabs, int p, int dtype, int symmetric, int q4,
+                          const double* add,  // integer offsets: added to every value (or NULL)
                           uint64_t nlogical, int ell,
                           const uint32_t* qmap, int K, uint64_t first, uint64_t count,
                           const uint64_t* idx, double* out, cudaStream_t s);

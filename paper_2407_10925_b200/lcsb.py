@@ -47,7 +47,7 @@ class LcsbConfig(ctypes.Structure):
                 ("alloc_ctx", ctypes.c_void_p), ("shards", ctypes.c_int32),
                 ("shard", ctypes.c_int32), ("virtual_shards", ctypes.c_int32),
                 ("nccl_id", ctypes.c_void_p), ("block_log4", ctypes.c_int32),
-                ("comm", ctypes.POINTER(LcsbCommHooks))]
+                ("comm", ctypes.POINTER(LcsbCommHooks)), ("offset_policy", ctypes.c_int32)]
 
 
 class LcsbBound(ctypes.Structure):
@@ -173,7 +173,7 @@ class _TorchAllocator:
 
 def make_config(sigma, d, ell, dtype="f32", form="auto", rmode="max", symmetry=-1,
                 kernel="auto", shards=1, shard=0, virtual_shards=False,
-                block_log4=0) -> LcsbConfig:
+                block_log4=0, offset_policy=0) -> LcsbConfig:
     cfg = LcsbConfig()
     load_library().lcsb_config_init(ctypes.byref(cfg))
     cfg.sigma, cfg.d, cfg.ell = sigma, d, ell
@@ -186,13 +186,15 @@ def make_config(sigma, d, ell, dtype="f32", form="auto", rmode="max", symmetry=-
     cfg.shard = int(shard)
     cfg.virtual_shards = 1 if virtual_shards else 0
     cfg.block_log4 = int(block_log4)
+    cfg.offset_policy = int(offset_policy)
     return cfg
 
 
 def lcsb_required_bytes(sigma, d, ell, dtype="f32", form="auto", symmetry=-1,
-                        kernel="auto", shards=1, virtual_shards=True, block_log4=0) -> int:
+                        kernel="auto", shards=1, virtual_shards=True, block_log4=0,
+                        offset_policy=0) -> int:
     cfg = make_config(sigma, d, ell, dtype, form, "max", symmetry, kernel, shards, 0,
-                      virtual_shards, block_log4)
+                      virtual_shards, block_log4, offset_policy)
     return int(load_library().lcsb_required_bytes(ctypes.byref(cfg)))
 
 
@@ -216,7 +218,7 @@ class Lcsb:
     def __init__(self, sigma, d, ell, dtype="f32", form="auto", rmode="max", symmetry=-1,
                  kernel="auto", stream=None, torch_allocator=True, shards=1, shard=0,
                  virtual_shards=False, nccl_id: bytes | None = None, block_log4: int = 0,
-                 comm_hooks: "LcsbCommHooks | None" = None):
+                 comm_hooks: "LcsbCommHooks | None" = None, offset_policy: int = 0):
         import torch
         if not torch.cuda.is_available():
             raise LcsbError(4, "no CUDA device (the library has no CPU path)")
@@ -225,7 +227,7 @@ class Lcsb:
         self.device = torch.cuda.current_device()
         self.stream = stream if stream is not None else torch.cuda.current_stream()
         cfg = make_config(sigma, d, ell, dtype, form, rmode, symmetry, kernel, shards, shard,
-                          virtual_shards, block_log4)
+                          virtual_shards, block_log4, offset_policy)
         cfg.stream = ctypes.c_void_p(self.stream.cuda_stream)
         self._nccl_id = None
         if nccl_id is not None:

@@ -71,6 +71,15 @@ def test_required_bytes_and_validation():
     assert L.lcsb_required_bytes(2, 2, 17, "f32", symmetry=2, block_log4=3) > 0
     assert L.lcsb_required_bytes(2, 2, 17, "f32", symmetry=2, block_log4=7) > 0
     assert L.lcsb_required_bytes(2, 2, 18, "f32", symmetry=2, block_log4=3) == 0
+    # integer offsets (reading R23): two-array only, not the half table, not sharded; + 512 B
+    q8 = L.lcsb_required_bytes(2, 2, 8, "f32", symmetry=2)
+    assert L.lcsb_required_bytes(2, 2, 8, "f32", offset_policy=1) == q8 + 512
+    assert L.lcsb_required_bytes(2, 2, 8, "f32", form="ks", offset_policy=1) == 0
+    assert L.lcsb_required_bytes(2, 2, 8, "f32", symmetry=1, offset_policy=1) == 0
+    assert L.lcsb_required_bytes(2, 2, 12, "f32", shards=2, offset_policy=1) == 0
+    assert L.lcsb_required_bytes(2, 2, 8, "f32", offset_policy=2) == 0
+    assert L.lcsb_required_bytes(3, 2, 3, "f32", form="two_array", offset_policy=1) == \
+        2 * 3 ** 6 * 4 + 256 + 512
 
 
 @pytest.mark.skipif(has_cuda(), reason="checks the no-GPU failure path")

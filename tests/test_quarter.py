@@ -336,3 +336,75 @@ def test_quarter_schedule_installed_mid_run_changes_nothing():
     for r in runs[1:]:
         assert np.array_equal(r[0], runs[0][0]) and np.array_equal(r[1], runs[0][1])
         assert r[2:] == runs[0][2:]
+
+
+# ------------------------------------------------------------------ integer offsets (R23)
+
+@pytest.mark.gpu
+@pytest.mark.skipif(not has_cuda(), reason="needs a CUDA device")
+@pytest.mark.parametrize("ell,K,dtype", [(3, 2, "f32"), (6, 3, "f32"), (6, 3, "f64"),
+                                         (9, 5, "f32"), (10, 6, "f64")])
+def test_offsets_quarter_matches_oracle_twin(ell, K, dtype):
+    """offset_policy = 1 on the quarter table against the oracle's offset twin: the values
+    (stored s + integer o) of both generations bit for bit in fp32 (1e-12 in fp64), R exact,
+    E and the bound within 1e-12 (one-pass bound, R21)."""
+    from oracle import ft_oracle as fo
+    h = L.Lcsb(2, 2, ell, dtype=dtype, symmetry=2, block_log4=K, offset_policy=1)
+    assert h.kernel_in_use == "bin2q"
+    run = fo.Run(2, 2, ell, "two_array", dtype, offsets=True)
+    for s in range(1, 41):
+        h.sweep(1)
+        run.sweep(1)
+        if s in (1, 2, 3, 17, 40):
+            _cmp(h.table(0), run.values(0), dtype)
+            _cmp(h.table(1), run.values(1), dtype)
+    _cmp_bound(h.bound(), run.bound(), dtype)
+    h.destroy()
+
+
+@pytest.mark.gpu
+@pytest.mark.skipif(not has_cuda(), reason="needs a CUDA device")
+@pytest.mark.parametrize("sigma,ell,dtype", [(2, 2, "f32"), (3, 3, "f32"), (4, 2, "f64")])
+def test_offsets_generic_two_array_matches_oracle_twin(sigma, ell, dtype):
+    """offset_policy = 1 on the generic kernel (binary l < 3 and d = 2, sigma > 2, two-array
+    form): tables and the two-pass bound bit-exact against the oracle's offset twin (fp32)."""
+    from oracle import ft_oracle as fo
+    h = L.Lcsb(sigma, 2, ell, dtype=dtype, form="two_array", offset_policy=1)
+    assert h.kernel_in_use == "generic"
+    run = fo.Run(sigma, 2, ell, "two_array", dtype, offsets=True)
+    for n in (1, 2, 30):
+        h.sweep(n)
+        run.sweep(n)
+        _cmp(h.table(0), run.values(0), dtype)
+        _cmp(h.table(1), run.values(1), dtype)
+        gb, rb = h.bound(), run.bound()
+        for key in ("R_max", "R_min", "E_at_Rmax", "E_at_Rmin", "bound_at_Rmax", "bound_at_Rmin"):
+            g, r = getattr(gb, key), rb[key]
+            assert (g == r) if dtype == "f32" else abs(g - r) <= 1e-12 * max(1, abs(r)), key
+    h.destroy()
+
+
+@pytest.mark.gpu
+@pytest.mark.skipif(not has_cuda(), reason="needs a CUDA device")
+def test_offsets_graph_replay_and_reset():
+    """Offsets under CUDA-graph replay (l = 8, 77 + 5 sweeps per call) equal plain launches,
+    and a reset restarts from offset 0 (the second run repeats the first bit for bit)."""
+    import os
+    a = L.Lcsb(2, 2, 8, dtype="f32", symmetry=2, block_log4=4, offset_policy=1)
+    os.environ["LCSB_NO_GRAPHS"] = "1"
+    try:
+        b = L.Lcsb(2, 2, 8, dtype="f32", symmetry=2, block_log4=4, offset_policy=1)
+        a.sweep(77)
+        b.sweep(77)
+        first = (a.table(0), a.table(1))
+        assert np.array_equal(first[0], b.table(0)) and np.array_equal(first[1], b.table(1))
+        a.sweep(5)
+        b.sweep(5)
+        assert np.array_equal(a.table(0), b.table(0))
+    finally:
+        os.environ.pop("LCSB_NO_GRAPHS", None)
+    a.reset()
+    a.sweep(77)
+    assert np.array_equal(a.table(0), first[0]) and np.array_equal(a.table(1), first[1])
+    a.destroy()
+    b.destroy()

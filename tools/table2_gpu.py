@@ -33,11 +33,14 @@ def main():
     ap.add_argument("--dtype", default="f64")
     ap.add_argument("--every", type=int, default=20)
     ap.add_argument("--max-sweeps", type=int, default=3000)
+    ap.add_argument("--offsets", action="store_true",
+                    help="integer-offset storage (offset_policy = 1, DESIGN.md reading R23)")
     args = ap.parse_args()
     import torch
     from paper_2407_10925_b200 import Lcsb
     for ell in range(args.lo, args.hi + 1):
-        h = Lcsb(2, 2, ell, dtype=args.dtype)
+        h = Lcsb(2, 2, ell, dtype=args.dtype, offset_policy=1 if args.offsets else 0)
+        h.ready(wait=True)
         t0 = time.perf_counter()
         last = -1.0
         hist = []
@@ -57,6 +60,7 @@ def main():
                           "floor6": floor6(b.best_bound), "paper": paper,
                           "paper_line": f"PAPER.md:{line}",
                           "match": floor6(b.best_bound) == paper, "seconds": dt,
+                          "offsets": bool(args.offsets),
                           "kernel": h.kernel_in_use}), flush=True)
         h.destroy()
         torch.cuda.empty_cache()
