@@ -140,12 +140,13 @@ def algorithmic_bytes_for_kernel(w: dict, stored: int, kernel: str) -> int:
 
 def requested_bytes_per_sweep(w: dict, stored: int, kernel: str) -> int:
     """Bytes the sweep kernel requests from the memory system: equal to the
-    compulsory bytes except for the quarter table, which loads every stored block once per
-    logical image (2 reads + 1 write per stored entry); its L2 item schedule serves part of the
-    second reads from L2, so DRAM sees fewer (roofline.traffic, ncu)."""
+    compulsory bytes except for the quarter table, which loads every logical window of the half
+    table once (2^(2l-1) entries: each stored block once per logical image, 2.67 x stored at
+    l = 17) and writes every stored entry once; its L2 item schedule serves part of the repeated
+    reads from L2, so DRAM sees fewer (roofline.traffic, ncu: 1.6 x stored read)."""
     esize = 4 if w["dtype"] == "f32" else 8
     if kernel == "bin2q":
-        return 3 * stored * esize
+        return (1 << (2 * w["ell"] - 1)) * esize + stored * esize
     return algorithmic_bytes_for_kernel(w, stored, kernel)
 
 
