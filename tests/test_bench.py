@@ -30,7 +30,8 @@ def test_algorithmic_bytes():
     w4 = bench.WORKLOADS["config4"]
     stored = 3229614080  # quarter table of l = 17, K = 7 (tests/test_quarter.py)
     assert bench.algorithmic_bytes_for_kernel(w4, stored, "bin2q") == 2 * stored * 4
-    assert bench.requested_bytes_per_sweep(w4, stored, "bin2q") == 3 * stored * 4
+    # every logical window of the half table (2^33 entries) + every stored entry written
+    assert bench.requested_bytes_per_sweep(w4, stored, "bin2q") == (1 << 33) * 4 + stored * 4
     w3 = bench.WORKLOADS["config3"]
     half = 1 << 31  # complement-folded 4^16 / 2
     # read v_{n-1} and the row means of v_{n-2}, write v_n and its row means
