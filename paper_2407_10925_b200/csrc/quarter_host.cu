@@ -2,6 +2,8 @@
 // DESIGN.md §6): stored sizes, the block map, and the L2 item schedule of the sweep.
 #include <stdlib.h>
 
+#include <stdio.h>
+
 #include <algorithm>
 #include <mutex>
 #include <vector>
@@ -269,6 +271,47 @@ bool quarter_schedule(int ell, int K, int M, const uint32_t* map,
       }
     }
     if (out.size() != E) return false;
+    // model cost of an order (LCSB_QSCHED_MODEL=1, offline harness only): pieces loaded per
+    // wave of kWave items (carry 0), and with a sliding window of W waves (a piece loaded again
+    // only if its previous use is more than W kWave positions back).  At l = 17 the v4 order
+    // costs 20.50 GB per sweep by waves (measured: 20.66 GB), 20.43 / 20.36 / 19.99 / 18.60 GB
+    // with windows of 1 / 8 / 32 / 128 waves: nearly all reuse is inside a wave.  Measured in
+    // the model and dropped (round 2): a local search moving items between waves (20.54 GB) and
+    // a greedy over a sliding window of 0.5-2 waves instead of hard waves (20.42-20.37 GB).
+    static const bool model = getenv("LCSB_QSCHED_MODEL") != nullptr;
+    auto report = [&](const char* tag) {
+      if (!model) return;
+      std::vector<uint32_t> seen(npieces, ~0u), last(npieces, ~0u);
+      uint64_t waves = 0, win1 = 0, win2 = 0;
+      for (size_t c = 0; c < E; ++c) {
+        const uint32_t e = idx_of_tau[out[c] & kQTileMask];
+        const uint32_t wv = (uint32_t)(c / (size_t)kWave);
+        for (int k = 0; k < npc[e]; ++k) {
+          const uint32_t q = pcs[4 * e + k];
+          if (seen[q] != wv) { seen[q] = wv; ++waves; }
+          if (last[q] == ~0u || c - last[q] > (size_t)kWave) ++win1;
+          if (last[q] == ~0u || c - last[q] > 2 * (size_t)kWave) ++win2;
+          last[q] = (uint32_t)c;
+        }
+      }
+      const double gb = (double)T * 4.0 / 1e9;  // fp32 piece bytes
+      fprintf(stderr, "[qsched %s] pieces %llu: waves %.2f GB, window %.2f GB, 2 windows %.2f GB\n",
+              tag, (unsigned long long)npieces, waves * gb, win1 * gb, win2 * gb);
+      for (size_t W : {1, 2, 4, 8, 16, 32, 64, 128}) {
+        std::vector<uint32_t> lst(npieces, ~0u);
+        uint64_t n = 0;
+        for (size_t c = 0; c < E; ++c) {
+          const uint32_t e = idx_of_tau[out[c] & kQTileMask];
+          for (int k = 0; k < npc[e]; ++k) {
+            const uint32_t q = pcs[4 * e + k];
+            if (lst[q] == ~0u || c - lst[q] > W * (size_t)kWave) ++n;
+            lst[q] = (uint32_t)c;
+          }
+        }
+        fprintf(stderr, "   window %zu waves: %.2f GB\n", W, n * gb);
+      }
+    };
+    report("v4");
     // LCSB_QSPREAD=P (A/B): permute each wave by j -> (j P) mod kWave, so the items that share a
     // piece (adjacent after the greedy growth) are claimed apart in time instead of together
     static const long spread = getenv("LCSB_QSPREAD") ? atol(getenv("LCSB_QSPREAD")) : 0;
