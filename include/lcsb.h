@@ -232,6 +232,15 @@ int lcsb_quarter_locate(int32_t ell, int32_t block_log4, uint64_t logical, uint6
  * if ready and returns 1 (0 = still being built; wait != 0 blocks until they are).  -1 on error. */
 int32_t lcsb_ready(lcsb_t* h, int32_t wait);
 
+/* Checkpoint / resume (long converging runs): lcsb_save writes every buffer the next
+ * sweep or bound reads (the table ring, row-mean rings, offsets) and the run's scalar state
+ * (sweeps done, ring positions, best-so-far triplet) to a file at `path`; lcsb_load restores it
+ * into a handle created with the same config (same sigma, d, l, dtype, form, layout), after
+ * which sweeps continue bit-identically to an uninterrupted run.  Synchronous.  Unsharded
+ * handles only.  Errors: EINVAL (path, config mismatch, corrupt or truncated file), ECUDA. */
+int lcsb_save(lcsb_t* h, const char* path);
+int lcsb_load(lcsb_t* h, const char* path);
+
 int64_t lcsb_sweeps_done(const lcsb_t* h);
 int32_t lcsb_num_shards(const lcsb_t* h);   /* P (1 when unsharded) */
 uint64_t lcsb_num_states(const lcsb_t* h);   /* logical states sigma^(d l) */

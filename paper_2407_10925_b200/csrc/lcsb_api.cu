@@ -3,6 +3,7 @@
 // kernels of kern_*.cu.  No CPU fallback exists: every entry point fails with LCSB_ECUDA when the
 // device work cannot be enqueued.
 #include <math.h>
+#include <stddef.h>
 #include <nccl.h>
 #include <stdarg.h>
 #include <stdio.h>
@@ -1314,6 +1315,145 @@ extern "C" int lcsb_table_gather(lcsb_t* h, int32_t which, const uint64_t* host_
                                  double* host_dst) {
   if (!host_idx && n) return set_err(h, LCSB_EINVAL, "host_idx is NULL");
   return readout(h, which, 0, n, host_idx, host_dst);
+}
+
+// ---------------------------------------------------------------- checkpoint / resume
+// File: a header (the run's identity and its scalar state), then every device buffer the next
+// sweep or bound reads, in a fixed order: the table ring, the q4 row-mean ring, the small
+// kernel's pooled means, the offset state.  Raw stored entries (the layout is a function of the
+// config), so a checkpoint restores into a handle created with the same config.
+struct CkptHeader {
+  char magic[8];  // "LCSBCKP1"
+  int32_t sigma, d, ell, dtype, form, symmetric, kernel, qK, ntab, offsets, spooled, pad;
+  uint64_t n_stored, tab_bytes, pool_bytes;
+  int32_t cur, pcur;
+  int64_t sweeps_done;
+  double best_rho[2];
+  int64_t best_sweep[2];
+};
+
+template <typename F>
+static int for_each_buffer(lcsb_t* h, F f) {  // (device pointer, bytes) in the file's order
+  for (int i = 0; i < h->ntab; ++i) {
+    int rc = f(h->tabs[0][i], h->tab_bytes);
+    if (rc != LCSB_OK) return rc;
+  }
+  for (int i = 0; i < 3; ++i)
+    if (h->pools[0][i]) {
+      int rc = f(h->pools[0][i], h->pool_bytes);
+      if (rc != LCSB_OK) return rc;
+    }
+  for (int k = 0; k <= kMaxD; ++k)
+    for (int i = 0; i < kMaxGen; ++i)
+      if (h->spools[k][i]) {
+        int rc = f(h->spools[k][i], h->spool_bytes[k]);
+        if (rc != LCSB_OK) return rc;
+      }
+  if (h->ost) return f(h->ost, sizeof(OffState));
+  return LCSB_OK;
+}
+
+static CkptHeader ckpt_header(const lcsb_t* h) {
+  CkptHeader c;
+  memset(&c, 0, sizeof c);
+  memcpy(c.magic, "LCSBCKP1", 8);
+  c.sigma = h->cfg.sigma;
+  c.d = h->cfg.d;
+  c.ell = h->cfg.ell;
+  c.dtype = h->cfg.dtype;
+  c.form = h->form;
+  c.symmetric = h->symmetric;
+  c.kernel = h->kernel;
+  c.qK = h->qK;
+  c.ntab = h->ntab;
+  c.offsets = h->ost != nullptr;
+  c.spooled = h->spooled;
+  c.n_stored = h->n_stored;
+  c.tab_bytes = h->tab_bytes;
+  c.pool_bytes = h->pool_bytes;
+  return c;
+}
+
+extern "C" int lcsb_save(lcsb_t* h, const char* path) {
+  if (!h || !path) return set_err(h, LCSB_EINVAL, "NULL argument");
+  if (h->mode != MODE_SINGLE)
+    return set_err(h, LCSB_EINVAL, "checkpoints are per handle of one GPU (unsharded)");
+  CU(h, cudaSetDevice(h->device));
+  cudaStream_t s = (cudaStream_t)h->cfg.stream;
+  CU(h, cudaStreamSynchronize(s));
+  FILE* f = fopen(path, "wb");
+  if (!f) return set_err(h, LCSB_EINVAL, "cannot open %s for writing", path);
+  CkptHeader c = ckpt_header(h);
+  c.cur = h->cur;
+  c.pcur = h->pcur;
+  c.sweeps_done = h->sweeps_done;
+  c.best_rho[0] = h->best_rho[0];
+  c.best_rho[1] = h->best_rho[1];
+  c.best_sweep[0] = h->best_sweep[0];
+  c.best_sweep[1] = h->best_sweep[1];
+  const size_t chunk = 64ull << 20;
+  char* buf = (char*)malloc(chunk);
+  int rc = (buf && fwrite(&c, sizeof c, 1, f) == 1) ? LCSB_OK
+                                                    : set_err(h, LCSB_EINVAL, "write failed");
+  if (rc == LCSB_OK)
+    rc = for_each_buffer(h, [&](void* d, size_t bytes) -> int {
+      for (size_t o = 0; o < bytes; o += chunk) {
+        const size_t n = bytes - o < chunk ? bytes - o : chunk;
+        cudaError_t e = cudaMemcpy(buf, (char*)d + o, n, cudaMemcpyDeviceToHost);
+        if (e != cudaSuccess)
+          return set_err(h, LCSB_ECUDA, "checkpoint read-back: %s", cudaGetErrorString(e));
+        if (fwrite(buf, 1, n, f) != n) return set_err(h, LCSB_EINVAL, "write to %s failed", path);
+      }
+      return LCSB_OK;
+    });
+  free(buf);
+  if (fclose(f) != 0 && rc == LCSB_OK) rc = set_err(h, LCSB_EINVAL, "closing %s failed", path);
+  return rc;
+}
+
+extern "C" int lcsb_load(lcsb_t* h, const char* path) {
+  if (!h || !path) return set_err(h, LCSB_EINVAL, "NULL argument");
+  if (h->mode != MODE_SINGLE)
+    return set_err(h, LCSB_EINVAL, "checkpoints are per handle of one GPU (unsharded)");
+  CU(h, cudaSetDevice(h->device));
+  cudaStream_t s = (cudaStream_t)h->cfg.stream;
+  CU(h, cudaStreamSynchronize(s));
+  FILE* f = fopen(path, "rb");
+  if (!f) return set_err(h, LCSB_EINVAL, "cannot open %s", path);
+  CkptHeader c, want = ckpt_header(h);
+  int rc = LCSB_OK;
+  if (fread(&c, sizeof c, 1, f) != 1 || memcmp(c.magic, "LCSBCKP1", 8) != 0)
+    rc = set_err(h, LCSB_EINVAL, "%s is not an lcsb checkpoint", path);
+  else if (memcmp(&c.sigma, &want.sigma, offsetof(CkptHeader, cur) - offsetof(CkptHeader, sigma)))
+    rc = set_err(h, LCSB_EINVAL,
+                 "checkpoint %s was written by a handle of another config or layout", path);
+  else if (c.cur < 0 || c.cur >= h->ntab || c.pcur < 0 || c.pcur > 2 || c.sweeps_done < 0)
+    rc = set_err(h, LCSB_EINVAL, "checkpoint %s has a corrupt header", path);
+  const size_t chunk = 64ull << 20;
+  char* buf = rc == LCSB_OK ? (char*)malloc(chunk) : nullptr;
+  if (rc == LCSB_OK && !buf) rc = set_err(h, LCSB_ECAPACITY, "host buffer allocation failed");
+  if (rc == LCSB_OK)
+    rc = for_each_buffer(h, [&](void* d, size_t bytes) -> int {
+      for (size_t o = 0; o < bytes; o += chunk) {
+        const size_t n = bytes - o < chunk ? bytes - o : chunk;
+        if (fread(buf, 1, n, f) != n) return set_err(h, LCSB_EINVAL, "%s is truncated", path);
+        cudaError_t e = cudaMemcpy((char*)d + o, buf, n, cudaMemcpyHostToDevice);
+        if (e != cudaSuccess)
+          return set_err(h, LCSB_ECUDA, "checkpoint upload: %s", cudaGetErrorString(e));
+      }
+      return LCSB_OK;
+    });
+  free(buf);
+  fclose(f);
+  if (rc != LCSB_OK) return rc;
+  h->cur = c.cur;
+  h->pcur = c.pcur;
+  h->sweeps_done = c.sweeps_done;
+  h->best_rho[0] = c.best_rho[0];
+  h->best_rho[1] = c.best_rho[1];
+  h->best_sweep[0] = c.best_sweep[0];
+  h->best_sweep[1] = c.best_sweep[1];
+  return LCSB_OK;
 }
 
 extern "C" int64_t lcsb_sweeps_done(const lcsb_t* h) { return h ? h->sweeps_done : -1; }

@@ -62,7 +62,8 @@ class LcsbBound(ctypes.Structure):
 EXPORTS = ["lcsb_config_init", "lcsb_required_bytes", "lcsb_create", "lcsb_create_ex",
            "lcsb_reset", "lcsb_sweep", "lcsb_bound", "lcsb_table", "lcsb_table_gather",
            "lcsb_nccl_unique_id", "lcsb_shard_locate", "lcsb_shard_locate_sigma4",
-           "lcsb_quarter_locate", "lcsb_ready", "lcsb_sweeps_done", "lcsb_num_shards",
+           "lcsb_quarter_locate", "lcsb_ready", "lcsb_save", "lcsb_load", "lcsb_sweeps_done",
+           "lcsb_num_shards",
            "lcsb_num_states", "lcsb_stored_states", "lcsb_device_bytes", "lcsb_kernel_in_use",
            "lcsb_launch_count", "lcsb_last_error", "lcsb_destroy"]
 NCCL_ID_BYTES = 128
@@ -126,6 +127,10 @@ def load_library():
                      ("lcsb_launch_count", ctypes.c_int64)]:
         getattr(lib, name).argtypes = [P]
         getattr(lib, name).restype = rt
+    lib.lcsb_save.argtypes = [P, ctypes.c_char_p]
+    lib.lcsb_save.restype = ctypes.c_int
+    lib.lcsb_load.argtypes = [P, ctypes.c_char_p]
+    lib.lcsb_load.restype = ctypes.c_int
     lib.lcsb_ready.argtypes = [P, ctypes.c_int32]
     lib.lcsb_ready.restype = ctypes.c_int32
     lib.lcsb_last_error.argtypes = [P]
@@ -276,6 +281,14 @@ class Lcsb:
                                            idx.ctypes.data_as(ctypes.c_void_p), idx.shape[0],
                                            out.ctypes.data_as(ctypes.c_void_p)), self._h)
         return out
+
+    def save(self, path: str):
+        """lcsb_save: checkpoint the run (tables, rings, offsets, best-so-far) to `path`."""
+        _check(self._lib.lcsb_save(self._h, os.fsencode(path)), self._h)
+
+    def load(self, path: str):
+        """lcsb_load: resume a checkpoint written by a handle of the same config."""
+        _check(self._lib.lcsb_load(self._h, os.fsencode(path)), self._h)
 
     def ready(self, wait: bool = False) -> bool:
         """lcsb_ready: the speed-only host preparations (quarter-table item schedule) are in

@@ -488,3 +488,43 @@ def test_sigma4_process_mode_multi_rank_on_one_gpu(tmp_path, world, ell, dtype, 
     mp.spawn(_pm_sigma4_worker, args=(world, _free_port(), str(tmp_path), ell, dtype, form),
              nprocs=world, join=True)
     assert np.load(tmp_path / "pm4.npy").all()
+
+
+@pytest.mark.gpu
+@pytest.mark.skipif(not has_cuda(), reason="needs a CUDA device")
+def test_comm_hook_failures_fail_loudly():
+    """A process-mode handle whose comm hook reports failure does not come up: lcsb_create
+    returns LCSB_ENCCL (5) with the hook named in the message; hooks missing a function are
+    rejected as LCSB_EINVAL (1).  One rank (P = 1) on the GPU, no torch process group needed."""
+    import ctypes
+    from paper_2407_10925_b200 import Lcsb, LcsbError
+    from paper_2407_10925_b200.lcsb import (ALLGATHER_FN, ALLREDUCE_FN, BARRIER_FN,
+                                            LcsbCommHooks)
+
+    def hooks(fail_allgather):
+        h = LcsbCommHooks()
+        h.allgather = ALLGATHER_FN(
+            lambda mine, all_, n, ctx: 1 if fail_allgather else (ctypes.memmove(all_, mine, n), 0)[1])
+        h.barrier = BARRIER_FN(lambda ctx: 0)
+        h.allreduce_max_u64 = ALLREDUCE_FN(lambda v, n, ctx: 0)
+        return h
+
+    with pytest.raises(LcsbError) as ei:
+        Lcsb(2, 2, 10, dtype="f32", shards=1, shard=0, comm_hooks=hooks(True),
+             torch_allocator=False)
+    assert ei.value.code == 5 and "allgather" in str(ei.value)
+    bad = hooks(False)
+    bad.barrier = BARRIER_FN()  # NULL function pointer
+    with pytest.raises(LcsbError) as ei:
+        Lcsb(2, 2, 10, dtype="f32", shards=1, shard=0, comm_hooks=bad, torch_allocator=False)
+    assert ei.value.code == 1
+    # and a working single-rank hook set gives the unsharded result
+    ok = Lcsb(2, 2, 10, dtype="f32", shards=1, shard=0, comm_hooks=hooks(False),
+              torch_allocator=False)
+    ref = Lcsb(2, 2, 10, dtype="f32")
+    ok.sweep(7)
+    ref.sweep(7)
+    assert np.array_equal(ok.table(0), ref.table(0))
+    assert ok.bound().bound == ref.bound().bound
+    ok.destroy()
+    ref.destroy()
