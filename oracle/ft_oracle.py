@@ -34,6 +34,12 @@ table may hold s_n = v_n - o_n with an integer o_n: each sweep subtracts c_n = f
 which keeps the stored magnitudes (and so the fp32 rounding) small.  The bound in stored terms:
 R = max(s_n - s_{n-1}) + c_{n-1} (min likewise), W = (s_n + R) - F(s_n, s_n).
 
+Residual storage (``Run.rebase()``, offsets on; reading R24): the table is split into
+a fixed base H (the stored table at the rebase, fp32) and a stored residual e, v = H + e + o.
+H + e is exact in fp64, each sweep subtracts c_n = floor(64 min(H + e_n)) / 64 (a dyadic, exact)
+and stores round_storage((F(H + e, H + e) - c_n) - H): the residual's magnitude stays below one
+sweep's growth, so fp32 residuals carry ~64x the precision of fp32 values.
+
 Parity pins: tests/test_oracle_pins.py.
 """
 from __future__ import annotations
@@ -244,6 +250,23 @@ class Run:
         self.offsets = bool(offsets)
         self.off = 0.0        # o_n of the newest table (an integer, exact in fp64)
         self.off_prev = 0.0   # o_{n-1}
+        self.base = None      # residual storage: the fixed base H (rebase), else None
+        self.quantum = 1.0    # offset granularity: 1 (integer offsets), 1/64 after a rebase
+        self.rebase_sweep = -1
+
+    def rebase(self):
+        """Residual storage (reading R24): H := the newest stored table, e := 0."""
+        if not self.offsets or self.form != FORM_TWO_ARRAY:
+            raise ValueError("rebase needs the two-array form with offsets")
+        self.base = self.gens[0].copy()
+        self.gens = [np.zeros(self.n)]
+        self.prev = np.full(self.n, np.nan)   # the previous generation is not representable
+        self.quantum = 1.0 / 64.0
+        self.rebase_sweep = self.sweeps_done
+
+    def _full(self, t):
+        """H + e (exact in fp64: both are storage-rounded values of similar or smaller scale)."""
+        return t if self.base is None else self.base + t
 
     # -- one application of F (Alg. 2 line 4 / Alg. 5 line 6) --
     def sweep(self, count: int = 1):
@@ -255,12 +278,16 @@ class Run:
                 self.gens = [new] + self.gens[:-1]          # shift the rows (line 11)
             else:
                 g = self.gens[0]
-                new = apply_F(self.sigma, self.d, self.ell, [g] * self.d, threads=self.threads,
+                full = self._full(g)
+                new = apply_F(self.sigma, self.d, self.ell, [full] * self.d, threads=self.threads,
                               two_array=True)
                 c = 0.0
                 if self.offsets:  # s_{n+1} = F(s_n) - floor(min s_n)  (translation invariance)
-                    c = float(math.floor(float(g.min())))
+                    q = self.quantum
+                    c = float(math.floor(float(full.min()) / q)) * q
                     new = new - c
+                if self.base is not None:  # the residual against the fixed base (R24)
+                    new = new - self.base
                 new = round_storage(new, self.dtype)
                 self.prev = g
                 self.gens = [new]
@@ -274,11 +301,11 @@ class Run:
 
     def values(self, which: int = 0) -> np.ndarray:
         """The iterate's values: stored + integer offset (o_n, or o_{n-1} for which = 1)."""
-        t = self.gens[0] if which == 0 else self.prev
+        t = self._full(self.gens[0] if which == 0 else self.prev)
         return t + (self.off if which == 0 else self.off_prev)
 
     def _W(self, R: float) -> np.ndarray:
-        v = self.gens[0]
+        v = self._full(self.gens[0])
         d = self.d
         if self.form == FORM_KS:
             shift = np.array([float(d - k) * R for k in range(1, d + 1)])
@@ -297,7 +324,9 @@ class Run:
         """Alg. 2 lines 5-10 for both R readings; updates best-so-far."""
         if self.sweeps_done < 1:
             raise RuntimeError("bound needs at least one sweep")
-        diff = self.gens[0] - self.prev
+        if self.base is not None and self.sweeps_done <= self.rebase_sweep:
+            raise RuntimeError("bound needs a sweep after a rebase")
+        diff = self._full(self.gens[0]) - self._full(self.prev)
         c = self.off - self.off_prev  # offsets: v_n - v_{n-1} = s_n - s_{n-1} + c_{n-1}
         out = {"R_max": float(diff.max()) + c, "R_min": float(diff.min()) + c}
         for mode in ("max", "min"):

@@ -569,3 +569,33 @@ def test_offsets_cut_fp32_drift():
 def test_offsets_rejected_for_ks():
     with pytest.raises(ValueError):
         fo.Run(2, 2, 3, "ks", offsets=True)
+
+
+# ---------------------------------------------------------------- residual storage (R24)
+
+@pytest.mark.parametrize("ell", [6, 8, 10])
+def test_residual_storage_reaches_fp64_precision(ell):
+    """fp32 with offsets for 100 sweeps, then a rebase (H := the stored table, e := 0) and 80
+    residual sweeps: the bound is within 1e-7 relative of the fp64 run (fp32 + offsets alone:
+    ~1e-6), the residual stays below one unit, and the fp64 residual run equals the plain fp64
+    run (translation invariance and exact H + e)."""
+    ref = fo.feasible_triplet(2, 2, ell, 180, form="two_array", dtype="f64")
+    run = fo.Run(2, 2, ell, "two_array", "f32", offsets=True)
+    for _ in range(100):
+        run.sweep()
+    run.rebase()
+    with pytest.raises(RuntimeError):
+        run.bound()                       # no previous generation right after a rebase
+    for _ in range(80):
+        run.sweep()
+    b = run.bound()
+    assert abs(b["bound_at_Rmax"] - ref["bound_at_Rmax"]) / ref["bound_at_Rmax"] < 1e-7
+    assert np.abs(run.newest).max() < 1.0
+    r64 = fo.Run(2, 2, ell, "two_array", "f64", offsets=True)
+    for _ in range(100):
+        r64.sweep()
+    r64.rebase()
+    for _ in range(80):
+        r64.sweep()
+    np.testing.assert_allclose(r64.values(0), ref["table"], rtol=1e-12, atol=1e-12)
+    assert r64.bound()["bound_at_Rmax"] == pytest.approx(ref["bound_at_Rmax"], abs=1e-12)
