@@ -232,6 +232,20 @@ int lcsb_quarter_locate(int32_t ell, int32_t block_log4, uint64_t logical, uint6
  * if ready and returns 1 (0 = still being built; wait != 0 blocks until they are).  -1 on error. */
 int32_t lcsb_ready(lcsb_t* h, int32_t wait);
 
+/* Residual storage (reading R24; quarter table, fp32, offset_policy = 1): the newest
+ * stored table becomes a fixed base H (one more table of device memory), the tables hold the
+ * residual e = v - o - H from then on (e := 0 now), the offset steps become multiples of 1/64,
+ * and every sweep stores round_fp32((F(H + e) - c) - H): H + e is exact in fp64 and the residual
+ * stays below one sweep's growth, so the iterate carries ~64x the precision of fp32 values --
+ * fp64-quality bounds at 12 instead of 16 bytes per stored entry (l = 18 on one B200).  The
+ * generation before the rebase is dropped: lcsb_bound and lcsb_table(which >= 1) need a sweep
+ * after it (LCSB_ESTATE).  Calling it again on a rebased handle folds the residual into the
+ * base (H := round32(H + e), e := the exact rounding residual; the iterate is unchanged) -- for
+ * when the iterate's shape has moved away from H.  lcsb_reset returns to plain storage.  To
+ * resume a rebased checkpoint, call lcsb_rebase on the fresh handle before lcsb_load.
+ * Errors: EINVAL (not that layout), ECAPACITY, ECUDA. */
+int lcsb_rebase(lcsb_t* h);
+
 /* Checkpoint / resume (long converging runs): lcsb_save writes every buffer the next
  * sweep or bound reads (the table ring, row-mean rings, offsets) and the run's scalar state
  * (sweeps done, ring positions, best-so-far triplet) to a file at `path`; lcsb_load restores it

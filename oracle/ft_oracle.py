@@ -255,11 +255,17 @@ class Run:
         self.rebase_sweep = -1
 
     def rebase(self):
-        """Residual storage (reading R24): H := the newest stored table, e := 0."""
+        """Residual storage (reading R24): H := the newest stored table, e := 0; on a rebased
+        run H := round32(H + e) and e := (H + e) - H (the iterate is unchanged)."""
         if not self.offsets or self.form != FORM_TWO_ARRAY:
             raise ValueError("rebase needs the two-array form with offsets")
-        self.base = self.gens[0].copy()
-        self.gens = [np.zeros(self.n)]
+        if self.base is None:
+            self.base = self.gens[0].copy()
+            self.gens = [np.zeros(self.n)]
+        else:
+            full = self.base + self.gens[0]
+            self.base = round_storage(full, self.dtype)
+            self.gens = [full - self.base]
         self.prev = np.full(self.n, np.nan)   # the previous generation is not representable
         self.quantum = 1.0 / 64.0
         self.rebase_sweep = self.sweeps_done

@@ -40,6 +40,9 @@
 //    D = min(F(u,u) - u) with F(u,u)[x] in fp64 (not rounded to storage), so one pass gives
 //    E = max(0, max W) = max(0, R - D) for both R (W = u + R - F(u,u), PAPER.md:400 with
 //    Alg. 5 line 8): the R reduction and the W pass of the old two-pass bound in one read.
+//  * Residual storage (RES, reading R24): the table holds a residual e against a fixed fp32 base
+//    H (v = H + e + o); every window is loaded from both and added in fp64 (exact), outputs
+//    store round((F + shift) - H[x]) and the bound reads H at the outputs too.
 #include <math.h>
 #include <stdlib.h>
 
@@ -80,13 +83,14 @@ __device__ __forceinline__ void st_out(V* p, V v) {
 #endif
 }
 
-template <typename T, int M, int S, bool WMODE, int MINB = 1>
+template <typename T, int M, int S, bool WMODE, int MINB = 1, bool RES = false>
 struct QCfg {
   static constexpr uint32_t TT = 1u << (2 * M);  // Q1 outputs per tile
   static constexpr uint32_t WIN = 2 * TT;        // entries per adv_b window
-  // the stage holds the item's two windows; the bound pass reads u and v_prev at the outputs
-  // straight from global memory (streaming loads, issued before the window reads)
-  static constexpr uint32_t STAGE = 2 * WIN;
+  // the stage holds the item's two windows (RES: of the residual, then of the base); the bound
+  // pass reads u and v_prev at the outputs straight from global memory (streaming loads, issued
+  // before the window reads)
+  static constexpr uint32_t STAGE = 2 * WIN * (RES ? 2 : 1);
   static constexpr size_t SMEM =
       (size_t)S * STAGE * sizeof(T) + (size_t)S * sizeof(uint64_t) + (size_t)S * 8 * sizeof(uint64_t);
 };
@@ -214,32 +218,40 @@ __device__ __forceinline__ void ld4s(const double* p, double (&v)[4]) {
 // widened to fp64 once.  The A/B load order alternates across threads so each 128-bit smem load
 // is conflict-free (2-way for permuted x windows).
 // bound pass (WMODE): src = u = v_n, prev = v_{n-1}; nothing is stored
-template <typename T, int MODE, bool WMODE, bool OFS = false>
+template <typename T, int MODE, bool WMODE, bool OFS = false, bool RES = false>
 __device__ __forceinline__ void q0_group(const double (&G)[4], uint32_t r, uint32_t half_rows,
                                          const T* src, T* dst, uint64_t of, uint64_t om,
-                                         const T* prev, BAcc& ba) {
+                                         const T* prev, BAcc& ba, const T* base = nullptr) {
   const double v0 = G[comp<MODE>(0)], v1 = G[comp<MODE>(1)], v2 = G[comp<MODE>(2)],
                v3 = G[comp<MODE>(3)];
   // a row run and its mirror run are images of each other, so usually only one is stored:
   // each value is formed only when its run is (the branches are uniform per item)
   if (WMODE) {
     const uint32_t rm = half_rows - 1 - r;
-    if (of != kNone)
-      bacc((double)__ldcs(src + of + r), (double)__ldcs(prev + of + r), q0_val(v0, v1, v2, v3),
-           ba);
-    if (om != kNone)
-      bacc((double)__ldcs(src + om + rm), (double)__ldcs(prev + om + rm),
-           q0_val(v3, v2, v1, v0), ba);
-  } else if (OFS) {  // store round(F(s) - c); track the min of what is stored
+    // RES: u = H + e and v_prev = H + e_prev (both exact in fp64)
     if (of != kNone) {
-      const T st = (T)(q0_val(v0, v1, v2, v3) + ba.sh);
-      st_out(dst + of + r, st);
-      ba.rmin = dmin(ba.rmin, (double)st);
+      const double h = RES ? (double)__ldcs(base + of + r) : 0.0;
+      bacc(h + (double)__ldcs(src + of + r), h + (double)__ldcs(prev + of + r),
+           q0_val(v0, v1, v2, v3), ba);
     }
     if (om != kNone) {
-      const T st = (T)(q0_val(v3, v2, v1, v0) + ba.sh);
-      st_out(dst + om + (half_rows - 1 - r), st);
-      ba.rmin = dmin(ba.rmin, (double)st);
+      const double h = RES ? (double)__ldcs(base + om + rm) : 0.0;
+      bacc(h + (double)__ldcs(src + om + rm), h + (double)__ldcs(prev + om + rm),
+           q0_val(v3, v2, v1, v0), ba);
+    }
+  } else if (OFS) {  // store round(F(s) - c) (RES: - H[x]); track the min of s (= H + e)
+    if (of != kNone) {
+      const double h = RES ? (double)__ldcs(base + of + r) : 0.0;
+      const T st = (T)((q0_val(v0, v1, v2, v3) + ba.sh) - h);
+      st_out(dst + of + r, st);
+      ba.rmin = dmin(ba.rmin, h + (double)st);
+    }
+    if (om != kNone) {
+      const uint32_t rm = half_rows - 1 - r;
+      const double h = RES ? (double)__ldcs(base + om + rm) : 0.0;
+      const T st = (T)((q0_val(v3, v2, v1, v0) + ba.sh) - h);
+      st_out(dst + om + rm, st);
+      ba.rmin = dmin(ba.rmin, h + (double)st);
     }
   } else {
     if (of != kNone) st_out(dst + of + r, (T)q0_val(v0, v1, v2, v3));
@@ -309,10 +321,10 @@ __device__ __forceinline__ void pair_quads_f32(const T* bw, const T* bp, const T
 }
 
 template <typename T, uint32_t TT, int MW, int MP, bool WMODE, int NT = kThreads, int UNR = 1,
-          bool OFS = false>
+          bool OFS = false, bool RES = false>
 __device__ __forceinline__ void pair_quads(const T* bw, const T* bp, const T* src, T* dst,
                                            const uint64_t* meta, bool self, const T* prev,
-                                           BAcc& ba) {
+                                           BAcc& ba, const T* base = nullptr) {
   // A/B load order select bits (bank conflicts): modes 0 and 3 (contiguous, possibly reversed)
   // alternate on bit 2, the pairswapped modes on bit 0 (x window) / bit 1 (psi window)
   constexpr uint32_t SX = (MW == 0 || MW == 3) ? 2 : 0, SP = (MP == 0 || MP == 3) ? 2 : 1;
@@ -331,12 +343,17 @@ __device__ __forceinline__ void pair_quads(const T* bw, const T* bp, const T* sr
     // bound pass: u and v_prev at the quad's stored Q1 outputs, loaded first (their latency
     // overlaps the window reads and the arithmetic); W(psi x) = W(x), so either copy serves
     T uu[4] = {0, 0, 0, 0}, pp[4] = {0, 0, 0, 0};  // initialised: keeps them out of local memory
+    T hq[4] = {0, 0, 0, 0}, hp[4] = {0, 0, 0, 0};  // RES: the base at the Q1 outputs
     if (WMODE) {
       const uint64_t q = oQ1 != kNone ? oQ1 + o0 : (oQ1p != kNone ? oQ1p + qb : kNone);
       if (q != kNone) {
         ld4s(src + q, uu);
         ld4s(prev + q, pp);
+        if (RES) ld4s(base + q, hq);
       }
+    } else if (RES) {
+      if (oQ1 != kNone) ld4s(base + oQ1 + o0, hq);
+      if (oQ1p != kNone) ld4s(base + oQ1p + qb, hp);
     }
     double A[4], B[4], Ap[4], Bp[4];
     const bool sx = (qd >> SX) & 1u, sp = (qd >> SP) & 1u;
@@ -352,6 +369,23 @@ __device__ __forceinline__ void pair_quads(const T* bw, const T* bp, const T* sr
       widen4(b, B);
       widen4(ap, Ap);
       widen4(bpp, Bp);
+      if constexpr (RES) {  // + the base's windows (same smem layout, 2 WIN further): H + e
+        const float* hw = reinterpret_cast<const float*>(bw) + 2 * 2 * TT;
+        const float* hpw = reinterpret_cast<const float*>(bp) + 2 * 2 * TT;
+        ld4r(hw + gbase<TT, MW>(sx ? g + 4 : g), X1);
+        ld4r(hw + gbase<TT, MW>(sx ? g : g + 4), X2);
+        ld4r(hpw + gbase<TT, MP>(sp ? u + 4 : u), P1);
+        ld4r(hpw + gbase<TT, MP>(sp ? u : u + 4), P2);
+        sel4f(sx, X1, X2, a, b);
+        sel4f(sp, P1, P2, ap, bpp);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          A[k] = (double)a[k] + A[k];
+          B[k] = (double)b[k] + B[k];
+          Ap[k] = (double)ap[k] + Ap[k];
+          Bp[k] = (double)bpp[k] + Bp[k];
+        }
+      }
     } else {
       double X1[4], X2[4], P1[4], P2[4];
       ld4(bw + gbase<TT, MW>(sx ? g + 4 : g), X1);
@@ -373,12 +407,33 @@ __device__ __forceinline__ void pair_quads(const T* bw, const T* bp, const T* sr
     if (WMODE) {
       if (oQ1 != kNone) {
 #pragma unroll
-        for (int k = 0; k < 4; ++k) bacc((double)uu[k], (double)pp[k], v[k], ba);
+        for (int k = 0; k < 4; ++k)
+          bacc((double)hq[k] + (double)uu[k], (double)hq[k] + (double)pp[k], v[k], ba);
       } else if (oQ1p != kNone) {
-        bacc((double)uu[3], (double)pp[3], v[0], ba);
-        bacc((double)uu[1], (double)pp[1], v[1], ba);
-        bacc((double)uu[2], (double)pp[2], v[2], ba);
-        bacc((double)uu[0], (double)pp[0], v[3], ba);
+        bacc((double)hq[3] + (double)uu[3], (double)hq[3] + (double)pp[3], v[0], ba);
+        bacc((double)hq[1] + (double)uu[1], (double)hq[1] + (double)pp[1], v[1], ba);
+        bacc((double)hq[2] + (double)uu[2], (double)hq[2] + (double)pp[2], v[2], ba);
+        bacc((double)hq[0] + (double)uu[0], (double)hq[0] + (double)pp[0], v[3], ba);
+      }
+    } else if (OFS && RES) {  // round((F(s) - c) - H[x]) at each stored copy; min of H + e
+      if (oQ1 != kNone) {
+        T st[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          st[k] = (T)((v[k] + ba.sh) - (double)hq[k]);
+          ba.rmin = dmin(ba.rmin, (double)hq[k] + (double)st[k]);
+        }
+        st4(dst + oQ1 + o0, (double)st[0], (double)st[1], (double)st[2], (double)st[3]);
+      }
+      if (oQ1p != kNone) {  // position j holds output (3, 1, 2, 0)[j]
+        const double vv[4] = {v[3], v[1], v[2], v[0]};
+        T st[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          st[k] = (T)((vv[k] + ba.sh) - (double)hp[k]);
+          ba.rmin = dmin(ba.rmin, (double)hp[k] + (double)st[k]);
+        }
+        st4(dst + oQ1p + qb, (double)st[0], (double)st[1], (double)st[2], (double)st[3]);
       }
     } else if (OFS) {  // round(F(s) - c) (the shift is an integer: exact before the rounding)
       const T s0 = (T)(v[0] + ba.sh), s1 = (T)(v[1] + ba.sh), s2 = (T)(v[2] + ba.sh),
@@ -393,12 +448,14 @@ __device__ __forceinline__ void pair_quads(const T* bw, const T* bp, const T* sr
     }
     // Q0 rows of the four groups
     if (rows_x) {
-      q0_group<T, MW, WMODE, OFS>(A, g >> 2, TT / 2, src, dst, of, om, prev, ba);
-      q0_group<T, MW, WMODE, OFS>(B, (g >> 2) + 1, TT / 2, src, dst, of, om, prev, ba);
+      q0_group<T, MW, WMODE, OFS, RES>(A, g >> 2, TT / 2, src, dst, of, om, prev, ba, base);
+      q0_group<T, MW, WMODE, OFS, RES>(B, (g >> 2) + 1, TT / 2, src, dst, of, om, prev, ba,
+                                        base);
     }
     if (rows_p) {
-      q0_group<T, MP, WMODE, OFS>(Ap, u >> 2, TT / 2, src, dst, opf, opm, prev, ba);
-      q0_group<T, MP, WMODE, OFS>(Bp, (u >> 2) + 1, TT / 2, src, dst, opf, opm, prev, ba);
+      q0_group<T, MP, WMODE, OFS, RES>(Ap, u >> 2, TT / 2, src, dst, opf, opm, prev, ba, base);
+      q0_group<T, MP, WMODE, OFS, RES>(Bp, (u >> 2) + 1, TT / 2, src, dst, opf, opm, prev,
+                                        ba, base);
     }
   }
 }
@@ -441,10 +498,11 @@ __device__ __forceinline__ void qlookup(const QGeo& g, const uint32_t* __restric
 // metadata: meta[0] = window modes (bits 0-1: window t, 2-3: window psi t, bit 4: self pair),
 // meta[1..6] = stored run starts (Q1 t, Q1 psi t, rows t, mirrors t, rows psi t, mirrors psi t;
 // kNone = not stored).
-template <typename T, int M, bool WMODE = false>
+template <typename T, int M, bool WMODE = false, bool RES = false>
 __device__ __forceinline__ void qissue(const QGeo& g, const QItem& it, uint64_t tau, T* buf,
                                        uint64_t* bar, uint64_t* meta, const T* src,
-                                       uint32_t hints, uint64_t keep, const T* prev = nullptr) {
+                                       uint32_t hints, uint64_t keep, const T* prev = nullptr,
+                                       const T* base = nullptr) {
   constexpr uint32_t TT = 1u << (2 * M), LOG = 2 * M;
   uint64_t x0, p0, taup;
   qtile(g, tau, LOG, x0, p0, taup);
@@ -460,31 +518,40 @@ __device__ __forceinline__ void qissue(const QGeo& g, const QItem& it, uint64_t 
   meta[4] = qrun(g, it.m[5], ym);
   meta[5] = self ? kNone : qrun(g, it.m[6], ypf);
   meta[6] = self ? kNone : qrun(g, it.m[7], ypm);
-  mbar_expect_tx(bar, 2 * 2 * TT * (uint32_t)sizeof(T));
+  mbar_expect_tx(bar, 2 * 2 * TT * (uint32_t)sizeof(T) * (RES ? 2 : 1));
   // bound pass: u and v_prev at the item's stored output runs go to L2 now (bulk prefetch), so
-  // the consumers' direct loads of them, one item later, hit L2
-  if (WMODE && ((TT / 2) * sizeof(T)) % 16 == 0) {
+  // the consumers' direct loads of them, one item later, hit L2 (RES: the base there too, in
+  // the sweep as well)
+  if ((WMODE || RES) && ((TT / 2) * sizeof(T)) % 16 == 0) {
     const uint64_t q = meta[1] != kNone ? meta[1] : meta[2];
     if (q != kNone) {
-      bulk_prefetch_l2(src + q, TT * (uint32_t)sizeof(T));
-      bulk_prefetch_l2(prev + q, TT * (uint32_t)sizeof(T));
+      if (WMODE) {
+        bulk_prefetch_l2(src + q, TT * (uint32_t)sizeof(T));
+        bulk_prefetch_l2(prev + q, TT * (uint32_t)sizeof(T));
+      }
+      if (RES) bulk_prefetch_l2(base + q, TT * (uint32_t)sizeof(T));
     }
+    if (RES && !WMODE && meta[1] != kNone && meta[2] != kNone)
+      bulk_prefetch_l2(base + meta[2], TT * (uint32_t)sizeof(T));
 #pragma unroll
     for (int k = 3; k < 7; ++k)
       if (meta[k] != kNone) {
-        bulk_prefetch_l2(src + meta[k], TT / 2 * (uint32_t)sizeof(T));
-        bulk_prefetch_l2(prev + meta[k], TT / 2 * (uint32_t)sizeof(T));
+        if (WMODE) {
+          bulk_prefetch_l2(src + meta[k], TT / 2 * (uint32_t)sizeof(T));
+          bulk_prefetch_l2(prev + meta[k], TT / 2 * (uint32_t)sizeof(T));
+        }
+        if (RES) bulk_prefetch_l2(base + meta[k], TT / 2 * (uint32_t)sizeof(T));
       }
   }
 #pragma unroll
-  for (int k = 0; k < 2; ++k) {
-    const uint32_t m = k ? mp : mw;
-    const uint64_t w = k ? wp : wb;
+  for (int k = 0; k < (RES ? 4 : 2); ++k) {  // RES: k = 2, 3 load the base's windows
+    const uint32_t m = (k & 1) ? mp : mw;
+    const uint64_t w = (k & 1) ? wp : wb;
     T* dst = buf + k * 2 * TT;
-    const T* blk = src + ((uint64_t)(m >> 2) << sh);
+    const T* blk = (k < 2 ? src : base) + ((uint64_t)(m >> 2) << sh);
     const uint64_t e = w & g.kmask;
     // L2 policy per piece (quarter_schedule): reloaded soon -> `keep`, else evict-first
-    const uint32_t hb = hints >> (2 * k);
+    const uint32_t hb = hints >> (2 * (k & 1));
     const uint64_t pol0 = (hb & 1u) ? keep : kL2EvictFirst, pol1 = (hb & 2u) ? keep : kL2EvictFirst;
     const uint64_t pol01 = (hb & 3u) ? keep : kL2EvictFirst;
     if ((m & 3u) == 0) {
@@ -502,9 +569,9 @@ __device__ __forceinline__ void qissue(const QGeo& g, const QItem& it, uint64_t 
 }
 
 template <typename T, int M, int S, bool WMODE, int MINB = 1, int NT = kThreads, int UNR = 1,
-          bool OFS = false>
+          bool OFS = false, bool RES = false>
 __global__ void __launch_bounds__(NT, MINB) bin2q_kernel(Bin2QArgs a) {
-  using C = QCfg<T, M, S, WMODE, MINB>;
+  using C = QCfg<T, M, S, WMODE, MINB, RES>;
   constexpr uint32_t TT = C::TT, WIN = C::WIN;
   constexpr uint32_t LOG = 2 * M;
   extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -529,6 +596,7 @@ __global__ void __launch_bounds__(NT, MINB) bin2q_kernel(Bin2QArgs a) {
 
   BAcc ba{-INFINITY, INFINITY, INFINITY, 0.0};
   if (OFS) ba.sh = a.ost->shift;
+  const T* base = RES ? reinterpret_cast<const T*>(a.base) : nullptr;
   const T* prev = reinterpret_cast<const T*>(a.prev);
   // items: with a schedule, item c is the tile pair of tile sched[c] (c = blockIdx.x + k G);
   // without one, the pair representatives in tile order
@@ -563,8 +631,9 @@ __global__ void __launch_bounds__(NT, MINB) bin2q_kernel(Bin2QArgs a) {
     if (pc < nitems) {
       meta[7] = 0;
       const uint32_t ent = entry(pc);
-      qissue<T, M, WMODE>(g, pit, sched ? (uint64_t)(ent & kQTileMask) : (uint64_t)ent, sbuf,
-                          &bars[s], meta, src, sched ? (ent >> kQHintShift) : 0xFu, keep, prev);
+      qissue<T, M, WMODE, RES>(g, pit, sched ? (uint64_t)(ent & kQTileMask) : (uint64_t)ent,
+                               sbuf, &bars[s], meta, src, sched ? (ent >> kQHintShift) : 0xFu,
+                               keep, prev, base);
       pc = claim(pc);
       if (pc < nitems) qlookup<M>(g, map, tile_of(pc), pit);
     } else {
@@ -592,10 +661,11 @@ __global__ void __launch_bounds__(NT, MINB) bin2q_kernel(Bin2QArgs a) {
     const T* bw = buf;
     const T* bp = buf + WIN;
 #define LCSB_Q1(MW, MP)                                                            \
-  if constexpr (sizeof(T) == 4 && !WMODE && !OFS)                                  \
+  if constexpr (sizeof(T) == 4 && !WMODE && !OFS && !RES)                          \
     pair_quads_f32<T, TT, MW, MP>(bw, bp, src, dst, meta, self);                   \
   else                                                                             \
-    pair_quads<T, TT, MW, MP, WMODE, NT, UNR, OFS>(bw, bp, src, dst, meta, self, prev, ba)
+    pair_quads<T, TT, MW, MP, WMODE, NT, UNR, OFS, RES>(bw, bp, src, dst, meta, self, prev, ba, \
+                                                        base)
     switch (mw * 4 + mp) {
       case 0: LCSB_Q1(0, 0); break;
       case 1: LCSB_Q1(0, 1); break;
@@ -623,17 +693,17 @@ __global__ void __launch_bounds__(NT, MINB) bin2q_kernel(Bin2QArgs a) {
 }
 
 template <typename T, int M, int S, bool WMODE, int MINB = 1, int NT = kThreads, int UNR = 1,
-          bool OFS = false>
+          bool OFS = false, bool RES = false>
 cudaError_t launch_q(const Bin2QArgs& a, cudaStream_t s, int sms) {
-  using C = QCfg<T, M, S, WMODE, MINB>;
+  using C = QCfg<T, M, S, WMODE, MINB, RES>;
   static uint64_t cap = 0;
   if (cap == 0) {
-    cudaError_t e = cudaFuncSetAttribute(bin2q_kernel<T, M, S, WMODE, MINB, NT, UNR, OFS>,
+    cudaError_t e = cudaFuncSetAttribute(bin2q_kernel<T, M, S, WMODE, MINB, NT, UNR, OFS, RES>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
     if (e != cudaSuccess) return e;
     int per_sm = 0;
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm,
-                                                      bin2q_kernel<T, M, S, WMODE, MINB, NT, UNR, OFS>,
+                                                      bin2q_kernel<T, M, S, WMODE, MINB, NT, UNR, OFS, RES>,
                                                       NT, C::SMEM) != cudaSuccess ||
         per_sm < 1) {
       cudaGetLastError();
@@ -646,12 +716,24 @@ cudaError_t launch_q(const Bin2QArgs& a, cudaStream_t s, int sms) {
       (a.sched && a.sched_m == M) ? a.nitems : (1ull << (2 * (a.ell - 1 - M)));
   uint64_t blocks = cap < ntiles ? cap : ntiles;
   if (blocks < 1) blocks = 1;
-  bin2q_kernel<T, M, S, WMODE, MINB, NT, UNR, OFS><<<(unsigned)blocks, NT, C::SMEM, s>>>(a);
+  bin2q_kernel<T, M, S, WMODE, MINB, NT, UNR, OFS, RES><<<(unsigned)blocks, NT, C::SMEM, s>>>(a);
   return cudaGetLastError();
 }
 
 template <bool WMODE>
 cudaError_t dispatch_q(const Bin2QArgs& a, int dtype, int M, cudaStream_t s, int sms) {
+  if (a.base) {  // residual storage (reading R24): fp32, windows of base and residual, M <= 5
+    if (dtype != LCSB_F32 || (!WMODE && !a.ost)) return cudaErrorInvalidValue;
+    constexpr int NT = kThreads;
+    switch (M < 5 ? M : 5) {
+      case 5: return launch_q<float, 5, 2, WMODE, 1, NT, 1, !WMODE, true>(a, s, sms);
+      case 4: return launch_q<float, 4, 2, WMODE, 1, NT, 1, !WMODE, true>(a, s, sms);
+      case 3: return launch_q<float, 3, 2, WMODE, 1, NT, 1, !WMODE, true>(a, s, sms);
+      case 2: return launch_q<float, 2, 2, WMODE, 1, NT, 1, !WMODE, true>(a, s, sms);
+      case 1: return launch_q<float, 1, 2, WMODE, 1, NT, 1, !WMODE, true>(a, s, sms);
+    }
+    return cudaErrorInvalidValue;
+  }
   if (WMODE && dtype == LCSB_F32 && M == 6) {
     static int wv = -1;  // LCSB_BIN2Q_WDIRECT=1 (A/B): the bound pass at 2 CTAs/SM
     if (wv < 0) {
@@ -733,7 +815,7 @@ int bin2q_variant_m(int dtype, int variant) {
 
 cudaError_t launch_bin2q_sweep(const Bin2QArgs& a, int dtype, int M, int variant, cudaStream_t s,
                                int sms) {
-  if (variant <= 0 || a.ost) return dispatch_q<false>(a, dtype, M, s, sms);
+  if (variant <= 0 || a.ost || a.base) return dispatch_q<false>(a, dtype, M, s, sms);
   if (variant >= kQVariants) return cudaErrorInvalidValue;
 #define LCSB_QV(T, M_, S_, MB_) \
   if (d.m == M_ && d.s == S_ && d.mb == MB_) return launch_q<T, M_, S_, false, MB_>(a, s, sms);

@@ -31,15 +31,32 @@ __global__ void offset_init_kernel(OffState* o) {
     o->off[i] = 0.0;
     o->mn[i] = ord_enc(0.0);
   }
-  if (i == 0) o->shift = 0.0;
+  if (i == 0) {
+    o->shift = 0.0;
+    o->quantum = 1.0;
+  }
 }
 
 __global__ void offset_prep_kernel(OffState* o, int cur, int out) {
   const double m = dec_ord(o->mn[cur]);
-  const double c = floor(m);  // an integer: exact, and so is every shift by it (reading R23)
+  // a multiple of the quantum (1, or 1/64 after a rebase): exact, and so is every shift by it
+  const double q = o->quantum;
+  const double c = floor(m / q) * q;
   o->off[out] = o->off[cur] + c;
   o->shift = -c;
   o->mn[out] = ord_enc(INFINITY);
+}
+
+// residual storage, rebase of a rebased table (reading R24): H' = round32(H + e) and
+// e' = (H + e) - H' (exact: the rounding residual of a 35-bit value has <= 24 significant bits)
+__global__ void rebase_fold_kernel(float* __restrict__ H, float* __restrict__ e, uint64_t n) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    const double v = (double)H[i] + (double)e[i];
+    const float h2 = (float)v;
+    H[i] = h2;
+    e[i] = (float)(v - (double)h2);
+  }
 }
 
 __device__ __forceinline__ void acc(double dd, double& mx, double& mn) {
@@ -108,7 +125,8 @@ struct ExpandTabs {
 
 template <typename T>
 __global__ void expand_kernel(ExpandTabs tabs, int p, int symmetric, int q4,
-                              const double* __restrict__ add, uint64_t nlogical, int ell,
+                              const double* __restrict__ add, const T* __restrict__ base,
+                              uint64_t nlogical, int ell,
                               const uint32_t* __restrict__ qmap, int K, uint64_t first,
                               uint64_t count, const uint64_t* __restrict__ idx, double* out) {
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
@@ -119,7 +137,10 @@ __global__ void expand_kernel(ExpandTabs tabs, int p, int symmetric, int q4,
     uint64_t y = idx ? idx[i] : first + i;
     if (symmetric && y >= half) y = top - y;  // Eq. (comp_eq)
     if (qmap) {  // quarter table: the orbit representative under the string swap / psi
-      out[i] = (double)reinterpret_cast<const T*>(tabs.t[0])[qstored(qmap, y, K)] + off;
+      const uint64_t q = qstored(qmap, y, K);
+      // residual storage (R24): v = H + e + o, H + e exact in fp64
+      const double hb = base ? (double)base[q] : 0.0;
+      out[i] = (hb + (double)reinterpret_cast<const T*>(tabs.t[0])[q]) + off;
       continue;
     }
     if (q4) {  // sigma = 4 digit-key shards
@@ -164,8 +185,17 @@ cudaError_t launch_offset_prep(OffState* o, int cur, int out, cudaStream_t s) {
   return cudaGetLastError();
 }
 
+cudaError_t launch_rebase_fold(void* H, void* e, uint64_t n, cudaStream_t s, int sms) {
+  uint64_t blocks = (n + 255) / 256;
+  const uint64_t cap = (uint64_t)sms * 8;
+  if (blocks > cap) blocks = cap;
+  if (blocks < 1) blocks = 1;
+  rebase_fold_kernel<<<(unsigned)blocks, 256, 0, s>>>((float*)H, (float*)e, n);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_expand(const void* const* tabs, int p, int dtype, int symmetric, int q4,
-                          const double* add, uint64_t nlogical, int ell,
+                          const double* add, const void* base, uint64_t nlogical, int ell,
                           const uint32_t* qmap, int K, uint64_t first, uint64_t count,
                           const uint64_t* idx, double* out, cudaStream_t s) {
   uint64_t blocks = (count + 255) / 256;
@@ -174,9 +204,9 @@ cudaError_t launch_expand(const void* const* tabs, int p, int dtype, int symmetr
   ExpandTabs t;
   for (int k = 0; k < kMaxShards; ++k) t.t[k] = (k < (1 << p)) ? tabs[k] : nullptr;
   if (dtype == LCSB_F32)
-    expand_kernel<float><<<(unsigned)blocks, 256, 0, s>>>(t, p, symmetric, q4, add, nlogical, ell, qmap, K, first, count, idx, out);
+    expand_kernel<float><<<(unsigned)blocks, 256, 0, s>>>(t, p, symmetric, q4, add, (const float*)base, nlogical, ell, qmap, K, first, count, idx, out);
   else
-    expand_kernel<double><<<(unsigned)blocks, 256, 0, s>>>(t, p, symmetric, q4, add, nlogical, ell, qmap, K, first, count, idx, out);
+    expand_kernel<double><<<(unsigned)blocks, 256, 0, s>>>(t, p, symmetric, q4, add, (const double*)base, nlogical, ell, qmap, K, first, count, idx, out);
   return cudaGetLastError();
 }
 

@@ -78,6 +78,8 @@ struct lcsb {
   cudaStream_t cap_stream;
   int cap_capturing;  // inside a graph capture: no allocation / upload may happen
   OffState* ost;      // integer offsets (reading R23): per-slot offsets, mins, shift; NULL = off
+  void* base;         // residual storage (reading R24): the fixed fp32 base H; NULL = off
+  int64_t rebase_sweep;  // sweeps_done at the rebase (the previous generation is invalid there)
   cudaGraphExec_t graph[kMaxGen];
   int graph_sweeps;
   int64_t sweeps_done;
@@ -539,6 +541,7 @@ extern "C" void lcsb_destroy(lcsb_t* h) {
       for (int i = 0; i < h->ntab; ++i) dev_free(h, h->tabs[k][i], h->tab_bytes);
   dev_free(h, h->red, 256);
   dev_free(h, h->ost, 512);
+  dev_free(h, h->base, h->tab_bytes);
   dev_free(h, h->qmap, h->qmap_bytes);
   if (h->qthread) {  // a schedule still being built is not needed any more
     h->qthread->join();
@@ -840,6 +843,15 @@ extern "C" int lcsb_reset(lcsb_t* h) {
       if (h->spools[k][i])
         CU(h, cudaMemsetAsync(h->spools[k][i], 0, h->spool_bytes[k], (cudaStream_t)h->cfg.stream));
   if (h->ost) CU(h, launch_offset_init(h->ost, (cudaStream_t)h->cfg.stream));
+  if (h->base) {  // back to plain storage (W_0 = 0 needs no base)
+    dev_free(h, h->base, h->tab_bytes);
+    h->base = nullptr;
+    for (int i = 0; i < kMaxGen; ++i)
+      if (h->graph[i]) {
+        cudaGraphExecDestroy(h->graph[i]);
+        h->graph[i] = nullptr;
+      }
+  }
   h->cur = 0;
   h->pcur = 0;
   h->sweeps_done = 0;
@@ -933,6 +945,7 @@ static void fill_bin2q(const lcsb_t* h, Bin2QArgs* a, int in_slot, int out_slot)
   static const int l2keep = getenv("LCSB_QKEEP") ? atoi(getenv("LCSB_QKEEP")) : 0;  // A/B
   a->l2keep = l2keep;
   a->counter = h->qcounter;
+  a->base = h->base;
 }
 
 static int enqueue_sweeps(lcsb_t* h, int64_t n, cudaStream_t s);
@@ -1122,6 +1135,8 @@ extern "C" int lcsb_bound(lcsb_t* h, lcsb_bound_t* out) {
   if (!h || !out) return set_err(h, LCSB_EINVAL, "NULL argument");
   NvtxRange r("lcsb_bound");
   if (h->sweeps_done < 1) return set_err(h, LCSB_ESTATE, "lcsb_bound needs at least one sweep");
+  if (h->base && h->sweeps_done <= h->rebase_sweep)
+    return set_err(h, LCSB_ESTATE, "lcsb_bound needs a sweep after lcsb_rebase");
   CU(h, cudaSetDevice(h->device));
   {
     int rc = install_schedule(h, false);
@@ -1264,6 +1279,8 @@ static int readout(lcsb_t* h, int which, uint64_t first, uint64_t count, const u
       if (host_idx[i] >= h->n_logical)
         return set_err(h, LCSB_EINVAL, "index %llu out of range", (unsigned long long)host_idx[i]);
   if (count == 0) return LCSB_OK;
+  if (h->base && which > 0 && h->sweeps_done - which < h->rebase_sweep)
+    return set_err(h, LCSB_ESTATE, "the generation before lcsb_rebase is not kept");
   if (which > h->sweeps_done) {  // a generation before the start: W_0 = 0 (never stored)
     memset(host_dst, 0, count * sizeof(double));
     return LCSB_OK;
@@ -1290,7 +1307,7 @@ static int readout(lcsb_t* h, int which, uint64_t first, uint64_t count, const u
       e = cudaMemcpyAsync(ibuf, host_idx + off, c * sizeof(uint64_t), cudaMemcpyHostToDevice, s);
     if (e == cudaSuccess)
       e = launch_expand(tabs, h->p, h->cfg.dtype, h->symmetric != 0 || h->kernel == 3,
-                        h->kernel == 3, h->ost ? &h->ost->off[slot] : nullptr,
+                        h->kernel == 3, h->ost ? &h->ost->off[slot] : nullptr, h->base,
                         h->n_logical, h->cfg.ell, h->qmap, h->qK,
                         first + off, c, host_idx ? ibuf : nullptr, dbuf, s);
     if (e == cudaSuccess) {
@@ -1317,6 +1334,41 @@ extern "C" int lcsb_table_gather(lcsb_t* h, int32_t which, const uint64_t* host_
   return readout(h, which, 0, n, host_idx, host_dst);
 }
 
+// ---------------------------------------------------------------- residual storage (R24)
+extern "C" int lcsb_rebase(lcsb_t* h) {
+  if (!h) return set_err(nullptr, LCSB_EINVAL, "handle is NULL");
+  if (h->kernel != 5 || h->cfg.dtype != LCSB_F32 || !h->ost || h->mode != MODE_SINGLE)
+    return set_err(h, LCSB_EINVAL,
+                   "lcsb_rebase needs the quarter table with fp32 storage and offset_policy = 1");
+  NvtxRange r("lcsb_rebase");
+  CU(h, cudaSetDevice(h->device));
+  cudaStream_t s = (cudaStream_t)h->cfg.stream;
+  if (h->base) {
+    // already rebased: fold the residual into the base, H := round32(H + e), e := the exact
+    // rounding residual -- the iterate (H + e) is unchanged and e shrinks back to ~ulp(H)
+    CU(h, launch_rebase_fold(h->base, h->tabs[0][h->cur], h->n_stored, s, h->sms));
+    h->launches += 1;
+  } else {
+    h->base = dev_alloc(h, h->tab_bytes);
+    if (!h->base)
+      return set_err(h, LCSB_ECAPACITY, "base table allocation (%llu bytes) failed",
+                     (unsigned long long)h->tab_bytes);
+    // H := the newest stored table s (v = s + o), e := 0; mn[cur] = min(s) = min(H + e) holds
+    CU(h, cudaMemcpyAsync(h->base, h->tabs[0][h->cur], h->tab_bytes, cudaMemcpyDeviceToDevice, s));
+    CU(h, cudaMemsetAsync(h->tabs[0][h->cur], 0, h->tab_bytes, s));
+  }
+  static const double q = 1.0 / 64.0;  // finer offsets: the residual stays below one sweep's growth
+  CU(h, cudaMemcpyAsync(&h->ost->quantum, &q, sizeof q, cudaMemcpyHostToDevice, s));
+  CU(h, cudaStreamSynchronize(s));
+  for (int i = 0; i < kMaxGen; ++i)  // captured sweeps know no base
+    if (h->graph[i]) {
+      cudaGraphExecDestroy(h->graph[i]);
+      h->graph[i] = nullptr;
+    }
+  h->rebase_sweep = h->sweeps_done;
+  return LCSB_OK;
+}
+
 // ---------------------------------------------------------------- checkpoint / resume
 // File: a header (the run's identity and its scalar state), then every device buffer the next
 // sweep or bound reads, in a fixed order: the table ring, the q4 row-mean ring, the small
@@ -1324,12 +1376,13 @@ extern "C" int lcsb_table_gather(lcsb_t* h, int32_t which, const uint64_t* host_
 // config), so a checkpoint restores into a handle created with the same config.
 struct CkptHeader {
   char magic[8];  // "LCSBCKP1"
-  int32_t sigma, d, ell, dtype, form, symmetric, kernel, qK, ntab, offsets, spooled, pad;
+  int32_t sigma, d, ell, dtype, form, symmetric, kernel, qK, ntab, offsets, spooled, based;
   uint64_t n_stored, tab_bytes, pool_bytes;
   int32_t cur, pcur;
   int64_t sweeps_done;
   double best_rho[2];
   int64_t best_sweep[2];
+  int64_t rebase_sweep;
 };
 
 template <typename F>
@@ -1349,6 +1402,10 @@ static int for_each_buffer(lcsb_t* h, F f) {  // (device pointer, bytes) in the 
         int rc = f(h->spools[k][i], h->spool_bytes[k]);
         if (rc != LCSB_OK) return rc;
       }
+  if (h->base) {
+    int rc = f(h->base, h->tab_bytes);
+    if (rc != LCSB_OK) return rc;
+  }
   if (h->ost) return f(h->ost, sizeof(OffState));
   return LCSB_OK;
 }
@@ -1368,6 +1425,7 @@ static CkptHeader ckpt_header(const lcsb_t* h) {
   c.ntab = h->ntab;
   c.offsets = h->ost != nullptr;
   c.spooled = h->spooled;
+  c.based = h->base != nullptr;
   c.n_stored = h->n_stored;
   c.tab_bytes = h->tab_bytes;
   c.pool_bytes = h->pool_bytes;
@@ -1391,6 +1449,7 @@ extern "C" int lcsb_save(lcsb_t* h, const char* path) {
   c.best_rho[1] = h->best_rho[1];
   c.best_sweep[0] = h->best_sweep[0];
   c.best_sweep[1] = h->best_sweep[1];
+  c.rebase_sweep = h->rebase_sweep;
   const size_t chunk = 64ull << 20;
   char* buf = (char*)malloc(chunk);
   int rc = (buf && fwrite(&c, sizeof c, 1, f) == 1) ? LCSB_OK
@@ -1453,6 +1512,7 @@ extern "C" int lcsb_load(lcsb_t* h, const char* path) {
   h->best_rho[1] = c.best_rho[1];
   h->best_sweep[0] = c.best_sweep[0];
   h->best_sweep[1] = c.best_sweep[1];
+  h->rebase_sweep = c.rebase_sweep;
   return LCSB_OK;
 }
 
@@ -1462,7 +1522,7 @@ extern "C" uint64_t lcsb_num_states(const lcsb_t* h) { return h ? h->n_logical :
 extern "C" uint64_t lcsb_stored_states(const lcsb_t* h) { return h ? h->n_stored : 0; }
 extern "C" uint64_t lcsb_device_bytes(const lcsb_t* h) {
   if (!h) return 0;
-  uint64_t b = (uint64_t)h->tab_bytes * (uint64_t)h->ntab * (uint64_t)h->nown + 256 +
+  uint64_t b = (uint64_t)h->tab_bytes * ((uint64_t)h->ntab * (uint64_t)h->nown + (h->base ? 1 : 0)) + 256 +
                h->qmap_bytes + h->qsched_bytes + 3 * (uint64_t)h->pool_bytes * (uint64_t)h->nown;
   for (int k = 0; k <= kMaxD; ++k)
     for (int i = 0; i < kMaxGen; ++i)

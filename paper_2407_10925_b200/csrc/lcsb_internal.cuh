@@ -54,6 +54,7 @@ struct OffState {
   double off[kMaxGen];
   unsigned long long mn[kMaxGen];
   double shift;
+  double quantum;  // granularity of c: 1 (integer offsets), 1/64 with residual storage (R24)
 };
 
 // Reduction slots (device, unsigned long long each):
@@ -158,6 +159,8 @@ struct Bin2QArgs {
   // integer offsets (sweep mode, as GenericArgs); NULL = off
   const OffState* ost;
   unsigned long long* omin;
+  // residual storage (reading R24): the fixed fp32 base H; the tables hold e = v - o - H
+  const void* base;
 };
 // schedule entries: tile index in the low bits, L2 hint bits (one per window piece) at the top
 constexpr int kQHintShift = 28;
@@ -387,6 +390,8 @@ cudaError_t launch_offset_init(OffState* o, cudaStream_t s);
 // before a sweep cur -> out: c = floor(min s[cur]), off[out] = off[cur] + c, shift = -c,
 // mn[out] = +inf (the sweep reduces into it)
 cudaError_t launch_offset_prep(OffState* o, int cur, int out, cudaStream_t s);
+// residual storage: H = round32(H + e), e = (H + e) - H (both fp32 arrays of n entries)
+cudaError_t launch_rebase_fold(void* H, void* e, uint64_t n, cudaStream_t s, int sms);
 cudaError_t launch_rdiff(const void* newest, const void* prev, uint64_t n, int dtype,
                          unsigned long long* red, cudaStream_t s, int sms);
 // tabs[k]: the table of shard k (unsharded: tabs[0]); p = log2(shards); qmap != NULL: quarter
@@ -396,6 +401,7 @@ cudaError_t launch_rdiff(const void* newest, const void* prev, uint64_t n, int d
 // q4: sigma = 4 digit-key shards (q4_key / q4_local) instead of the binary key
 cudaError_t launch_expand(const void* const* tabs, int p, int dtype, int symmetric, int q4,
                           const double* add,  // integer offsets: added to every value (or NULL)
+                          const void* base,   // residual storage: the base table (or NULL)
                           uint64_t nlogical, int ell,
                           const uint32_t* qmap, int K, uint64_t first, uint64_t count,
                           const uint64_t* idx, double* out, cudaStream_t s);

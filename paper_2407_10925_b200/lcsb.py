@@ -62,7 +62,8 @@ class LcsbBound(ctypes.Structure):
 EXPORTS = ["lcsb_config_init", "lcsb_required_bytes", "lcsb_create", "lcsb_create_ex",
            "lcsb_reset", "lcsb_sweep", "lcsb_bound", "lcsb_table", "lcsb_table_gather",
            "lcsb_nccl_unique_id", "lcsb_shard_locate", "lcsb_shard_locate_sigma4",
-           "lcsb_quarter_locate", "lcsb_ready", "lcsb_save", "lcsb_load", "lcsb_sweeps_done",
+           "lcsb_quarter_locate", "lcsb_ready", "lcsb_rebase", "lcsb_save", "lcsb_load",
+           "lcsb_sweeps_done",
            "lcsb_num_shards",
            "lcsb_num_states", "lcsb_stored_states", "lcsb_device_bytes", "lcsb_kernel_in_use",
            "lcsb_launch_count", "lcsb_last_error", "lcsb_destroy"]
@@ -127,6 +128,8 @@ def load_library():
                      ("lcsb_launch_count", ctypes.c_int64)]:
         getattr(lib, name).argtypes = [P]
         getattr(lib, name).restype = rt
+    lib.lcsb_rebase.argtypes = [P]
+    lib.lcsb_rebase.restype = ctypes.c_int
     lib.lcsb_save.argtypes = [P, ctypes.c_char_p]
     lib.lcsb_save.restype = ctypes.c_int
     lib.lcsb_load.argtypes = [P, ctypes.c_char_p]
@@ -281,6 +284,10 @@ class Lcsb:
                                            idx.ctypes.data_as(ctypes.c_void_p), idx.shape[0],
                                            out.ctypes.data_as(ctypes.c_void_p)), self._h)
         return out
+
+    def rebase(self):
+        """lcsb_rebase: residual storage against the newest table (reading R24)."""
+        _check(self._lib.lcsb_rebase(self._h), self._h)
 
     def save(self, path: str):
         """lcsb_save: checkpoint the run (tables, rings, offsets, best-so-far) to `path`."""

@@ -69,3 +69,25 @@ def test_load_rejects_other_config_and_truncated_file(tmp_path):
         h.load(str(tmp_path / "missing.ckpt"))
     h.destroy()
     a.destroy()
+
+
+def test_resume_a_rebased_run(tmp_path):
+    """A checkpoint of a residual-storage run (R24) resumes in a fresh handle rebased first."""
+    from paper_2407_10925_b200 import Lcsb
+    path = str(tmp_path / "res.ckpt")
+    a = Lcsb(2, 2, 10, dtype="f32", offset_policy=1)
+    a.sweep(20)
+    a.rebase()
+    a.sweep(5)
+    a.save(path)
+    a.sweep(6)
+    ta, ba = a.table(0), a.bound()
+    b = Lcsb(2, 2, 10, dtype="f32", offset_policy=1)
+    b.rebase()                          # allocates the base; the load overwrites it
+    b.load(path)
+    b.sweep(6)
+    assert np.array_equal(ta, b.table(0))
+    assert (ba.R_max, ba.bound, ba.best_bound) == (b.bound().R_max, b.bound().bound,
+                                                    b.bound().best_bound)
+    a.destroy()
+    b.destroy()

@@ -599,3 +599,16 @@ def test_residual_storage_reaches_fp64_precision(ell):
         r64.sweep()
     np.testing.assert_allclose(r64.values(0), ref["table"], rtol=1e-12, atol=1e-12)
     assert r64.bound()["bound_at_Rmax"] == pytest.approx(ref["bound_at_Rmax"], abs=1e-12)
+
+
+def test_residual_refold_keeps_the_iterate():
+    """A second rebase folds e into H (H := round32(H + e), e := the exact residual): the values
+    H + e + o are unchanged bit for bit."""
+    run = fo.Run(2, 2, 5, "two_array", "f32", offsets=True)
+    run.sweep(20)
+    run.rebase()
+    run.sweep(10)
+    before = run.values(0).copy()
+    run.rebase()
+    assert np.array_equal(run.values(0), before)
+    assert np.abs(run.newest).max() <= np.abs(run.base).max() * 2.0 ** -24

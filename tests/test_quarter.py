@@ -408,3 +408,80 @@ def test_offsets_graph_replay_and_reset():
     assert np.array_equal(a.table(0), first[0]) and np.array_equal(a.table(1), first[1])
     a.destroy()
     b.destroy()
+
+
+# ------------------------------------------------------------------ residual storage (R24)
+
+@pytest.mark.gpu
+@pytest.mark.skipif(not has_cuda(), reason="needs a CUDA device")
+@pytest.mark.parametrize("ell,K", [(6, 3), (8, 4), (10, 6)])
+def test_residual_storage_matches_oracle_twin(ell, K):
+    """fp32 + offsets for 30 sweeps, lcsb_rebase, 25 residual sweeps: the values (H + e + o) of
+    both generations bit-exact against the oracle's residual twin, R exact, E and the bound
+    within 1e-12 (R21); right after the rebase the bound and the previous generation are
+    unavailable (LCSB_ESTATE)."""
+    from oracle import ft_oracle as fo
+    from paper_2407_10925_b200 import LcsbError
+    h = L.Lcsb(2, 2, ell, dtype="f32", symmetry=2, block_log4=K, offset_policy=1)
+    run = fo.Run(2, 2, ell, "two_array", "f32", offsets=True)
+    h.sweep(30)
+    run.sweep(30)
+    h.rebase()
+    run.rebase()
+    _cmp(h.table(0), run.values(0), "f32")
+    with pytest.raises(LcsbError) as ei:
+        h.bound()
+    assert ei.value.code == 3
+    with pytest.raises(LcsbError):
+        h.table(1)
+    for n in (1, 2, 22):
+        h.sweep(n)
+        run.sweep(n)
+        _cmp(h.table(0), run.values(0), "f32")
+        _cmp(h.table(1), run.values(1), "f32")
+        _cmp_bound(h.bound(), run.bound(), "f32")
+    h.rebase()                          # fold the residual into the base (the iterate stays)
+    run.rebase()
+    _cmp(h.table(0), run.values(0), "f32")
+    h.sweep(9)
+    run.sweep(9)
+    _cmp(h.table(0), run.values(0), "f32")
+    _cmp(h.table(1), run.values(1), "f32")
+    _cmp_bound(h.bound(), run.bound(), "f32")
+    h.reset()                           # back to plain storage
+    h.sweep(3)
+    r2 = fo.Run(2, 2, ell, "two_array", "f32", offsets=True)
+    r2.sweep(3)
+    _cmp(h.table(0), r2.values(0), "f32")
+    h.destroy()
+
+
+@pytest.mark.gpu
+@pytest.mark.skipif(not has_cuda(), reason="needs a CUDA device")
+def test_residual_storage_reaches_fp64_bound_l14():
+    """l = 14, converged (300 sweeps): fp32 + offsets for 150 sweeps, then residual storage for
+    150: the bound agrees with the fp64 quarter-table run to 5e-8 relative, where fp32 + offsets
+    alone is ~1e-6 off, and floors to Table 2's value."""
+    import math
+    import os
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "table2.txt")
+    table = {int(r.split()[0]): float(r.split()[2]) for r in
+             open(path) if r.strip() and not r.startswith("#")}
+    a = L.Lcsb(2, 2, 14, dtype="f64")
+    a.sweep(300)
+    ref = a.bound().bound
+    a.destroy()
+    p = L.Lcsb(2, 2, 14, dtype="f32", offset_policy=1)
+    p.sweep(300)
+    plain = p.bound().bound
+    p.destroy()
+    h = L.Lcsb(2, 2, 14, dtype="f32", offset_policy=1)
+    h.sweep(100)
+    for _ in range(5):                  # rebase every 40 sweeps: the base follows the shape
+        h.rebase()
+        h.sweep(40)
+    b = h.bound().bound
+    h.destroy()
+    assert abs(b - ref) / ref < 5e-8, (b, ref, plain)
+    assert abs(b - ref) < abs(plain - ref) / 10
+    assert math.floor(b * 1e6 + 1e-6) / 1e6 == table[14]
