@@ -726,7 +726,7 @@ cudaError_t dispatch_q(const Bin2QArgs& a, int dtype, int M, cudaStream_t s, int
     if (dtype != LCSB_F32 || (!WMODE && !a.ost)) return cudaErrorInvalidValue;
     constexpr int NT = kThreads;
     switch (M < 5 ? M : 5) {
-      case 5: return launch_q<float, 5, 2, WMODE, 1, NT, 1, !WMODE, true>(a, s, sms);
+      case 5: return launch_q<float, 5, 2, WMODE, 2, NT, 1, !WMODE, true>(a, s, sms);
       case 4: return launch_q<float, 4, 2, WMODE, 1, NT, 1, !WMODE, true>(a, s, sms);
       case 3: return launch_q<float, 3, 2, WMODE, 1, NT, 1, !WMODE, true>(a, s, sms);
       case 2: return launch_q<float, 2, 2, WMODE, 1, NT, 1, !WMODE, true>(a, s, sms);

@@ -24,13 +24,19 @@ def main():
     ap.add_argument("--warm", type=int, default=3)
     ap.add_argument("--reps", type=int, default=3)
     ap.add_argument("--tag", default="")
+    ap.add_argument("--residual", action="store_true",
+                    help="offsets + lcsb_rebase after the warm-up: time the residual sweep (R24)")
     args = ap.parse_args()
     import torch
     from paper_2407_10925_b200 import Lcsb
     from seeded_inputs import splitmix64_indices
-    h = Lcsb(args.sigma, args.d, args.ell, dtype=args.dtype, form=args.form)
+    h = Lcsb(args.sigma, args.d, args.ell, dtype=args.dtype, form=args.form,
+             offset_policy=1 if args.residual else 0)
     h.ready(wait=True)
     h.sweep(args.warm)
+    if args.residual:
+        h.rebase()
+        h.sweep(1)
     torch.cuda.synchronize()
     times = []
     for _ in range(args.reps):
