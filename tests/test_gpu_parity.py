@@ -436,7 +436,7 @@ def test_config4_properties_at_full_size():
 
 # ------------------------------------------------------------------ edge cases and errors
 
-@pytest.mark.parametrize("ell", [9, 10, 11, 12, 13, 14])
+@pytest.mark.parametrize("ell", [9, 10, 11, 12, 13, 14, 15, 16])
 def test_gpu_reproduces_table2_converged(ell):
     """The paper's Table 2, reproduced by the GPU path directly: fp64 storage,
     two-array form, bound evaluated every 20 sweeps until it stops improving; the best bound
