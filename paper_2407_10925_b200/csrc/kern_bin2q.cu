@@ -1,777 +1,12 @@
-// kern_bin2q.cu -- the binary (sigma = d = 2) two-array sweep on the symmetry-folded ("quarter")
-// table: one stored entry per class of states with provably equal values -- orbits of
-// {id, complement c, string swap s, psi = c s}, and for same-head states also the tail
-// complement t (reading R18) -- 3/16 of the logical states.
-//
-// Method: identical arithmetic to kern_bin2_tma.cu (Eqs. F1/F0
-// PAPER.md:752-779), same tile pairing {t, psi(t)} and the same adv_b windows.  Only the
-// storage changes (DESIGN.md §6 "quarter table"):
-//
-//  * Half-table index space [0, 2^(2l-1)) (a_0 = 0, complement folded, Eq. comp_eq) is cut into
-//    blocks of 4^K entries; a block is fixed by its top l-K characters pairs ("prefix").  The
-//    residual symmetries of the half table map blocks onto blocks with a digit-wise permutation
-//    inside: Q1 blocks (heads 01) pair under psi (pairswap of the complement); Q0 blocks
-//    (heads 00) fold under {id, s, t, s t} (s: swap the two bits of every pair; t: complement
-//    every tail digit, i.e. reverse the block).  Of each block orbit only the smallest prefix is
-//    stored ("canonical", mode 0); the others read it through the permutation (mode 1 = s,
-//    2 = psi or s t, 3 = t).  map[block] = (slot << 2) | mode, built by the host.  The string
-//    swap W(a,b) = W(b,a) is an exact invariant of every iterate (reading R19), the complement
-//    one is Eq. comp_eq, the tail complement of same-head states is v'[00t] = v'[00t~] (R18).
-//  * Reads: a tile's adv_b window (2T entries with free low 2M+1 bits) of a mode-0 block is one
-//    contiguous run; of a pairswapped block two runs of T (bit 2M+1 <-> bit 2M exchanged),
-//    loaded with two bulk copies into the same smem slots; of a tail-complemented block one run
-//    read reversed.  The consumer indexes smem through the permutation.  Every half-table
-//    window is loaded once, so a stored block is requested once per logical image (twice for
-//    Q1 blocks, four times for Q0 blocks).
-//  * Item order: the host's L2 schedule (lcsb_api.cu quarter_schedule) lists the tile pairs in
-//    waves that share stored blocks, and thread 0 of each CTA claims items in that order from a
-//    global counter, so the items in flight stay within about one grid-width of the list and
-//    most repeated block loads hit L2.
-//  * Writes: of every output run (Q1 tile, Q0 row run, Q0 mirror run) only those lying in a
-//    canonical block are stored -- each stored entry is written exactly once.  psi(t)'s outputs
-//    equal t's (the pair computes one max for both), so exactly one of the two Q1 runs is
-//    written unless the block is psi-fixed; a Q0 row run and its mirror run are t-images, so
-//    one of the two is written.
-//  => per sweep every logical window of the half table is loaded once (from DRAM ~1.6 x the
-//     stored table at l = 17) and 3/8 of the half table is written.
-//  * Bound pass (WMODE, reading R21): the same item walk without stores; at every stored
-//    output x it reads u[x] (the table the pass reads, = v_n) and v_prev[x] and accumulates
-//    R_max = max(u - v_prev), R_min = min(u - v_prev) (Alg. 5 line 7 / PAPER.md:694) and
-//    D = min(F(u,u) - u) with F(u,u)[x] in fp64 (not rounded to storage), so one pass gives
-//    E = max(0, max W) = max(0, R - D) for both R (W = u + R - F(u,u), PAPER.md:400 with
-//    Alg. 5 line 8): the R reduction and the W pass of the old two-pass bound in one read.
-//  * Residual storage (RES, reading R24): the table holds a residual e against a fixed fp32 base
-//    H (v = H + e + o); every window is loaded from both and added in fp64 (exact), outputs
-//    store round((F + shift) - H[x]) and the bound reads H at the outputs too.
-#include <math.h>
-#include <stdlib.h>
-
-#include "lcsb_internal.cuh"
-#include "tma.cuh"
+// kern_bin2q.cu -- the quarter-table sweep (kernel templates: kern_bin2q.cuh).
+#include "kern_bin2q.cuh"
 
 namespace lcsbk {
 namespace {
 
-__device__ __forceinline__ uint64_t pairswap(uint64_t v) {
-  return ((v & 0xAAAAAAAAAAAAAAAAull) >> 1) | ((v & 0x5555555555555555ull) << 1);
-}
-__device__ __forceinline__ uint32_t pairswap32(uint32_t v) {
-  return ((v & 0xAAAAAAAAu) >> 1) | ((v & 0x55555555u) << 1);
-}
-
-// Q0 output from one row of 4 in the oracle's summation order (Alg. 3 "SameFirstBit"):
-// 1 + max(0, cand) with the z = head option's 0 (reading R3).  The iterates are non-negative
-// (v_0 = 0 and F maps non-negative tables to non-negative tables), so cand >= 0 and the max is
-// cand itself: the compare is dropped, the value is unchanged.
-__device__ __forceinline__ double q0_val(double v0, double v1, double v2, double v3) {
-  const double r = ((v0 + v1) + v2) + v3;
-  return 1.0 + 0.25 * r;
-}
-
-constexpr int kThreads = 256;
-constexpr uint64_t kNone = ~0ull;
-
-// output stores: nothing in a sweep re-reads them, so they are streaming stores (st.global.cs,
-// evict-first) that leave L2 to the input windows (A/B at l = 17 fp32: 5.161 -> 5.132 ms;
-// LCSB_BIN2Q_NO_STCS builds the plain stores)
-template <typename V>
-__device__ __forceinline__ void st_out(V* p, V v) {
-#ifndef LCSB_BIN2Q_NO_STCS
-  __stcs(p, v);
-#else
-  *p = v;
-#endif
-}
-
-template <typename T, int M, int S, bool WMODE, int MINB = 1, bool RES = false>
-struct QCfg {
-  static constexpr uint32_t TT = 1u << (2 * M);  // Q1 outputs per tile
-  static constexpr uint32_t WIN = 2 * TT;        // entries per adv_b window
-  // the stage holds the item's two windows (RES: of the residual, then of the base); the bound
-  // pass reads u and v_prev at the outputs straight from global memory (streaming loads, issued
-  // before the window reads)
-  static constexpr uint32_t STAGE = 2 * WIN * (RES ? 2 : 1);
-  static constexpr size_t SMEM =
-      (size_t)S * STAGE * sizeof(T) + (size_t)S * sizeof(uint64_t) + (size_t)S * 8 * sizeof(uint64_t);
-};
-
-struct QGeo {
-  int K;
-  uint64_t q1, lmask, amask, bmask, kmask;
-  uint64_t ntiles;  // 4^(l-1-M)
-};
-
-__device__ __forceinline__ void qtile(const QGeo& g, uint64_t tau, uint32_t LOG, uint64_t& x0,
-                                      uint64_t& p0, uint64_t& taup) {
-  x0 = g.q1 + (tau << LOG);
-  p0 = pairswap(~x0 & g.lmask) & ~((1ull << LOG) - 1);  // first output of tile psi(tau)
-  taup = (p0 - g.q1) >> LOG;
-}
-__device__ __forceinline__ uint64_t qwin(const QGeo& g, uint64_t x) {  // adv_b window base
-  return (x & g.amask) | ((x & g.bmask & ~g.q1) << 2);
-}
-// stored index of the first entry of a run starting at half-table index s if the run lies in
-// a canonical block, else kNone
-__device__ __forceinline__ uint64_t qrun(const QGeo& g, uint32_t m, uint64_t s) {
-  return (m & 3u) ? kNone : (((uint64_t)(m >> 2) << (2 * g.K)) | (s & g.kmask));
-}
-
-// ---- window addressing.  Logical window position w (0 <= w < 2T): bit 2M = the appended b
-// character of the tile's top free pair, low 2M bits = the tile's free pairs.  A window loaded
-// from a permuted block sits in smem as two runs of T (bit 2M+1 <-> bit 2M exchanged) with the
-// pairs inside permuted: mode 1 (s) pairswap, mode 2 (psi) pairswap of the complement.
-// A "group" = the 4 logical positions with equal bits >= 2 (the last character pair of the
-// window state free); it is 4 consecutive smem entries in every mode, in the order comp<MODE>.
-template <uint32_t TT, int MODE>
-__device__ __forceinline__ uint32_t gbase(uint32_t g) {  // smem start of the group at logical g
-  if (MODE == 0) return g;
-  if (MODE == 3) return 2u * TT - 4u - g;  // tail complement: the window reversed
-  const uint32_t w = (MODE == 1) ? g : (~(g + 3u) & (2u * TT - 1u));
-  return (w & TT) | pairswap32(w & (TT - 1u));
-}
-template <int MODE>
-__device__ __forceinline__ constexpr uint32_t comp(uint32_t d) {  // smem slot of logical digit d
-  return MODE == 0 ? d
-                   : (MODE == 1 ? (((d & 1u) << 1) | (d >> 1))
-                                : (MODE == 3 ? 3u - d : ((((3u - d) & 1u) << 1) | ((3u - d) >> 1))));
-}
-
-template <typename T>
-__device__ __forceinline__ void ld4(const T* p, double (&v)[4]);
-template <>
-__device__ __forceinline__ void ld4<float>(const float* p, double (&v)[4]) {
-  const float4 f = *reinterpret_cast<const float4*>(p);
-  v[0] = f.x; v[1] = f.y; v[2] = f.z; v[3] = f.w;
-}
-template <>
-__device__ __forceinline__ void ld4<double>(const double* p, double (&v)[4]) {
-  const double2 a = reinterpret_cast<const double2*>(p)[0];
-  const double2 b = reinterpret_cast<const double2*>(p)[1];
-  v[0] = a.x; v[1] = a.y; v[2] = b.x; v[3] = b.y;
-}
-// raw 4-entry group in the storage type (no widening)
-__device__ __forceinline__ void ld4r(const float* p, float (&v)[4]) {
-  const float4 f = *reinterpret_cast<const float4*>(p);
-  v[0] = f.x; v[1] = f.y; v[2] = f.z; v[3] = f.w;
-}
-__device__ __forceinline__ void sel4f(bool s, const float (&x)[4], const float (&y)[4],
-                                      float (&a)[4], float (&b)[4]) {
-#pragma unroll
-  for (int k = 0; k < 4; ++k) {
-    a[k] = s ? y[k] : x[k];
-    b[k] = s ? x[k] : y[k];
-  }
-}
-__device__ __forceinline__ void widen4(const float (&x)[4], double (&v)[4]) {
-#pragma unroll
-  for (int k = 0; k < 4; ++k) v[k] = (double)x[k];
-}
-
-template <typename T>
-__device__ __forceinline__ void st4(T* p, double a, double b, double c, double d);
-template <>
-__device__ __forceinline__ void st4<float>(float* p, double a, double b, double c, double d) {
-  *reinterpret_cast<float4*>(p) = make_float4((float)a, (float)b, (float)c, (float)d);
-}
-template <>
-__device__ __forceinline__ void st4<double>(double* p, double a, double b, double c, double d) {
-  reinterpret_cast<double2*>(p)[0] = make_double2(a, b);
-  reinterpret_cast<double2*>(p)[1] = make_double2(c, d);
-}
-__device__ __forceinline__ void sel4(bool s, const double (&x)[4], const double (&y)[4],
-                                     double (&a)[4], double (&b)[4]) {
-#pragma unroll
-  for (int k = 0; k < 4; ++k) {
-    a[k] = s ? y[k] : x[k];
-    b[k] = s ? x[k] : y[k];
-  }
-}
-// bound pass accumulators at one stored output: u = v_n[x], p = v_{n-1}[x], f = F(u,u)[x]
-// (sweep with integer offsets: rmin = min of the stored values, sh = the shift -c, reading R23)
-struct BAcc {
-  double rmax, rmin, dmin;
-  double sh;
-};
-__device__ __forceinline__ void bacc(double u, double p, double f, BAcc& b) {
-  const double dd = u - p;
-  b.rmax = dmax(b.rmax, dd);
-  b.rmin = dmin(b.rmin, dd);
-  b.dmin = dmin(b.dmin, f - u);
-}
-// streaming 4-entry load in the storage type (widened at use)
-__device__ __forceinline__ void ld4s(const float* p, float (&v)[4]) {
-  const float4 f = __ldcs(reinterpret_cast<const float4*>(p));
-  v[0] = f.x; v[1] = f.y; v[2] = f.z; v[3] = f.w;
-}
-__device__ __forceinline__ void ld4s(const double* p, double (&v)[4]) {
-  const double2 a = __ldcs(reinterpret_cast<const double2*>(p));
-  const double2 b = __ldcs(reinterpret_cast<const double2*>(p) + 1);
-  v[0] = a.x; v[1] = a.y; v[2] = b.x; v[3] = b.y;
-}
-
-// Each thread takes quads of Q1 outputs o0..o0+3 of tile t (and the same values at psi(t)).
-// adv_b pairs of outputs (o0, o0+2) form x-window group A = logical 2 pairswap(o0), (o0+1, o0+3)
-// group B = A + 4; in the psi window (o0+3, o0+2) form A' = 2 (T-4-o0), (o0+1, o0) B' = A' + 4.
-// Over all quads every group of both windows is loaded exactly once, and a group is also a
-// complete Q0 row (Alg. 3): row r = group/4 -> Q0 output r of the window's run and its mirror
-// (the complemented tail, row read reversed).  So each window entry is read from smem and
-// widened to fp64 once.  The A/B load order alternates across threads so each 128-bit smem load
-// is conflict-free (2-way for permuted x windows).
-// bound pass (WMODE): src = u = v_n, prev = v_{n-1}; nothing is stored
-template <typename T, int MODE, bool WMODE, bool OFS = false, bool RES = false>
-__device__ __forceinline__ void q0_group(const double (&G)[4], uint32_t r, uint32_t half_rows,
-                                         const T* src, T* dst, uint64_t of, uint64_t om,
-                                         const T* prev, BAcc& ba, const T* base = nullptr) {
-  const double v0 = G[comp<MODE>(0)], v1 = G[comp<MODE>(1)], v2 = G[comp<MODE>(2)],
-               v3 = G[comp<MODE>(3)];
-  // a row run and its mirror run are images of each other, so usually only one is stored:
-  // each value is formed only when its run is (the branches are uniform per item)
-  if (WMODE) {
-    const uint32_t rm = half_rows - 1 - r;
-    // RES: u = H + e and v_prev = H + e_prev (both exact in fp64)
-    if (of != kNone) {
-      const double h = RES ? (double)__ldcs(base + of + r) : 0.0;
-      bacc(h + (double)__ldcs(src + of + r), h + (double)__ldcs(prev + of + r),
-           q0_val(v0, v1, v2, v3), ba);
-    }
-    if (om != kNone) {
-      const double h = RES ? (double)__ldcs(base + om + rm) : 0.0;
-      bacc(h + (double)__ldcs(src + om + rm), h + (double)__ldcs(prev + om + rm),
-           q0_val(v3, v2, v1, v0), ba);
-    }
-  } else if (OFS) {  // store round(F(s) - c) (RES: - H[x]); track the min of s (= H + e)
-    if (of != kNone) {
-      const double h = RES ? (double)__ldcs(base + of + r) : 0.0;
-      const T st = (T)((q0_val(v0, v1, v2, v3) + ba.sh) - h);
-      st_out(dst + of + r, st);
-      ba.rmin = dmin(ba.rmin, h + (double)st);
-    }
-    if (om != kNone) {
-      const uint32_t rm = half_rows - 1 - r;
-      const double h = RES ? (double)__ldcs(base + om + rm) : 0.0;
-      const T st = (T)((q0_val(v3, v2, v1, v0) + ba.sh) - h);
-      st_out(dst + om + rm, st);
-      ba.rmin = dmin(ba.rmin, h + (double)st);
-    }
-  } else {
-    if (of != kNone) st_out(dst + of + r, (T)q0_val(v0, v1, v2, v3));
-    if (om != kNone) st_out(dst + om + (half_rows - 1 - r), (T)q0_val(v3, v2, v1, v0));
-  }
-}
-
-// fp32 storage, sweep: the Q1 values in fp32 (see the comment inside), the rest as pair_quads
-template <typename T, uint32_t TT, int MW, int MP>
-__device__ __forceinline__ void pair_quads_f32(const T* bw, const T* bp, const T* src, T* dst,
-                                               const uint64_t* meta, bool self) {
-  constexpr uint32_t SX = (MW == 0 || MW == 3) ? 2 : 0, SP = (MP == 0 || MP == 3) ? 2 : 1;
-  const uint64_t oQ1 = meta[1], oQ1p = meta[2];
-  const uint64_t of = meta[3], om = meta[4], opf = meta[5], opm = meta[6];
-  const bool rows_x = of != kNone || om != kNone;
-  const bool rows_p = !self && (opf != kNone || opm != kNone);
-  BAcc ba;  // unused by the sweep
-  // fp32 storage, sweep: the Q1 value round32(max(0.5 (x0 + x1), 0.5 (y0 + y1))) of fp64
-  // arithmetic equals the same expression evaluated in fp32 (a two-term fp32 sum is exact in
-  // fp64 or off by less than half an fp32 ulp, so no double rounding; halving and max commute
-  // with rounding), so Q1 stays in fp32; only the Q0 rows that are stored widen to fp64 (their
-  // four-term sums are not exact in fp32).
-  for (uint32_t qd = threadIdx.x; qd < TT / 4; qd += blockDim.x) {
-    const uint32_t o0 = 4 * qd;
-    const uint32_t g = 2 * pairswap32(o0), u = 2 * (TT - 4 - o0);
-    // X1 / X2 hold the groups A (row g/4) and B (row g/4 + 1) in a per-thread order (sx: B
-    // first) that keeps the 128-bit smem loads conflict-free; the pair sums are formed per loaded
-    // group and only they are put back in A/B order (4 selects instead of 8 per window)
-    float X1[4], X2[4], P1[4], P2[4];
-    const bool sx = (qd >> SX) & 1u, sp = (qd >> SP) & 1u;
-    ld4r(reinterpret_cast<const float*>(bw) + gbase<TT, MW>(sx ? g + 4 : g), X1);
-    ld4r(reinterpret_cast<const float*>(bw) + gbase<TT, MW>(sx ? g : g + 4), X2);
-    ld4r(reinterpret_cast<const float*>(bp) + gbase<TT, MP>(sp ? u + 4 : u), P1);
-    ld4r(reinterpret_cast<const float*>(bp) + gbase<TT, MP>(sp ? u : u + 4), P2);
-    constexpr uint32_t c0 = comp<MW>(0), c1 = comp<MW>(1), c2 = comp<MW>(2), c3 = comp<MW>(3);
-    constexpr uint32_t d0 = comp<MP>(0), d1 = comp<MP>(1), d2 = comp<MP>(2), d3 = comp<MP>(3);
-    const float x1l = 0.5f * (X1[c0] + X1[c1]), x1h = 0.5f * (X1[c2] + X1[c3]);
-    const float x2l = 0.5f * (X2[c0] + X2[c1]), x2h = 0.5f * (X2[c2] + X2[c3]);
-    const float p1l = 0.5f * (P1[d0] + P1[d1]), p1h = 0.5f * (P1[d2] + P1[d3]);
-    const float p2l = 0.5f * (P2[d0] + P2[d1]), p2h = 0.5f * (P2[d2] + P2[d3]);
-    // bx = {A lo, B lo, A hi, B hi}; bq = {Bp hi, Bp lo, Ap hi, Ap lo}
-    const float bx[4] = {sx ? x2l : x1l, sx ? x1l : x2l, sx ? x2h : x1h, sx ? x1h : x2h};
-    const float bq[4] = {sp ? p1h : p2h, sp ? p1l : p2l, sp ? p2h : p1h, sp ? p2l : p1l};
-    float v[4];
-#pragma unroll
-    for (int k = 0; k < 4; ++k) v[k] = fmaxf(bx[k], bq[k]);  // one FMNMX (no NaN, no -0)
-    const uint32_t qb = pairswap32(~o0 & (TT - 1) & ~3u);
-    float* df = reinterpret_cast<float*>(dst);
-    if (oQ1 != kNone)
-      st_out(reinterpret_cast<float4*>(df + oQ1 + o0), make_float4(v[0], v[1], v[2], v[3]));
-    if (oQ1p != kNone)
-      st_out(reinterpret_cast<float4*>(df + oQ1p + qb), make_float4(v[3], v[1], v[2], v[0]));
-    double G[4];
-    if (rows_x) {  // X1 is row g/4 + sx, X2 row g/4 + 1 - sx
-      widen4(X1, G);
-      q0_group<T, MW, false>(G, (g >> 2) + sx, TT / 2, src, dst, of, om, nullptr, ba);
-      widen4(X2, G);
-      q0_group<T, MW, false>(G, (g >> 2) + 1 - sx, TT / 2, src, dst, of, om, nullptr, ba);
-    }
-    if (rows_p) {
-      widen4(P1, G);
-      q0_group<T, MP, false>(G, (u >> 2) + sp, TT / 2, src, dst, opf, opm, nullptr, ba);
-      widen4(P2, G);
-      q0_group<T, MP, false>(G, (u >> 2) + 1 - sp, TT / 2, src, dst, opf, opm, nullptr, ba);
-    }
-  }
-}
-
-template <typename T, uint32_t TT, int MW, int MP, bool WMODE, int NT = kThreads, int UNR = 1,
-          bool OFS = false, bool RES = false>
-__device__ __forceinline__ void pair_quads(const T* bw, const T* bp, const T* src, T* dst,
-                                           const uint64_t* meta, bool self, const T* prev,
-                                           BAcc& ba, const T* base = nullptr) {
-  // A/B load order select bits (bank conflicts): modes 0 and 3 (contiguous, possibly reversed)
-  // alternate on bit 2, the pairswapped modes on bit 0 (x window) / bit 1 (psi window)
-  constexpr uint32_t SX = (MW == 0 || MW == 3) ? 2 : 0, SP = (MP == 0 || MP == 3) ? 2 : 1;
-  const uint64_t oQ1 = meta[1], oQ1p = meta[2];
-  const uint64_t of = meta[3], om = meta[4], opf = meta[5], opm = meta[6];
-  const bool rows_x = of != kNone || om != kNone;
-  const bool rows_p = !self && (opf != kNone || opm != kNone);
-  // UNR > 1 (bound pass): several quads unrolled, so their global loads of u and v_prev are
-  // issued together (more loads in flight per thread)
-#pragma unroll UNR
-  for (uint32_t qd = threadIdx.x; qd < TT / 4; qd += NT) {
-    const uint32_t o0 = 4 * qd;
-    const uint32_t g = 2 * pairswap32(o0), u = 2 * (TT - 4 - o0);
-    // psi(o0 + k) sits at oQ1p + qb + pairswap(3 - k): the quad reversed as (3, 1, 2, 0)
-    const uint32_t qb = pairswap32(~o0 & (TT - 1) & ~3u);
-    // bound pass: u and v_prev at the quad's stored Q1 outputs, loaded first (their latency
-    // overlaps the window reads and the arithmetic); W(psi x) = W(x), so either copy serves
-    T uu[4] = {0, 0, 0, 0}, pp[4] = {0, 0, 0, 0};  // initialised: keeps them out of local memory
-    T hq[4] = {0, 0, 0, 0}, hp[4] = {0, 0, 0, 0};  // RES: the base at the Q1 outputs
-    if (WMODE) {
-      const uint64_t q = oQ1 != kNone ? oQ1 + o0 : (oQ1p != kNone ? oQ1p + qb : kNone);
-      if (q != kNone) {
-        ld4s(src + q, uu);
-        ld4s(prev + q, pp);
-        if (RES) ld4s(base + q, hq);
-      }
-    } else if (RES) {
-      if (oQ1 != kNone) ld4s(base + oQ1 + o0, hq);
-      if (oQ1p != kNone) ld4s(base + oQ1p + qb, hp);
-    }
-    double A[4], B[4], Ap[4], Bp[4];
-    const bool sx = (qd >> SX) & 1u, sp = (qd >> SP) & 1u;
-    if constexpr (sizeof(T) == 4) {  // select the raw floats, then widen (half the selects)
-      float X1[4], X2[4], P1[4], P2[4], a[4], b[4], ap[4], bpp[4];
-      ld4r(reinterpret_cast<const float*>(bw) + gbase<TT, MW>(sx ? g + 4 : g), X1);
-      ld4r(reinterpret_cast<const float*>(bw) + gbase<TT, MW>(sx ? g : g + 4), X2);
-      ld4r(reinterpret_cast<const float*>(bp) + gbase<TT, MP>(sp ? u + 4 : u), P1);
-      ld4r(reinterpret_cast<const float*>(bp) + gbase<TT, MP>(sp ? u : u + 4), P2);
-      sel4f(sx, X1, X2, a, b);
-      sel4f(sp, P1, P2, ap, bpp);
-      widen4(a, A);
-      widen4(b, B);
-      widen4(ap, Ap);
-      widen4(bpp, Bp);
-      if constexpr (RES) {  // + the base's windows (same smem layout, 2 WIN further): H + e
-        const float* hw = reinterpret_cast<const float*>(bw) + 2 * 2 * TT;
-        const float* hpw = reinterpret_cast<const float*>(bp) + 2 * 2 * TT;
-        ld4r(hw + gbase<TT, MW>(sx ? g + 4 : g), X1);
-        ld4r(hw + gbase<TT, MW>(sx ? g : g + 4), X2);
-        ld4r(hpw + gbase<TT, MP>(sp ? u + 4 : u), P1);
-        ld4r(hpw + gbase<TT, MP>(sp ? u : u + 4), P2);
-        sel4f(sx, X1, X2, a, b);
-        sel4f(sp, P1, P2, ap, bpp);
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          A[k] = (double)a[k] + A[k];
-          B[k] = (double)b[k] + B[k];
-          Ap[k] = (double)ap[k] + Ap[k];
-          Bp[k] = (double)bpp[k] + Bp[k];
-        }
-      }
-    } else {
-      double X1[4], X2[4], P1[4], P2[4];
-      ld4(bw + gbase<TT, MW>(sx ? g + 4 : g), X1);
-      ld4(bw + gbase<TT, MW>(sx ? g : g + 4), X2);
-      ld4(bp + gbase<TT, MP>(sp ? u + 4 : u), P1);
-      ld4(bp + gbase<TT, MP>(sp ? u : u + 4), P2);
-      sel4(sx, X1, X2, A, B);
-      sel4(sp, P1, P2, Ap, Bp);
-    }
-    constexpr uint32_t c0 = comp<MW>(0), c1 = comp<MW>(1), c2 = comp<MW>(2), c3 = comp<MW>(3);
-    constexpr uint32_t d0 = comp<MP>(0), d1 = comp<MP>(1), d2 = comp<MP>(2), d3 = comp<MP>(3);
-    double v[4];
-    // adv_b(x) and adv_b(psi x) = adv_a(x), each (g[c=0] + g[c=1]) / 2 in the oracle's order
-    // max(s/2, t/2) = max(s, t)/2 exactly (halving is exact and monotone): one multiply per output
-    const double tx[4] = {A[c0] + A[c1], B[c0] + B[c1], A[c2] + A[c3], B[c2] + B[c3]};
-    const double tq[4] = {Bp[d2] + Bp[d3], Bp[d0] + Bp[d1], Ap[d2] + Ap[d3], Ap[d0] + Ap[d1]};
-#pragma unroll
-    for (int k = 0; k < 4; ++k) v[k] = 0.5 * dmax(tx[k], tq[k]);
-    if (WMODE) {
-      if (oQ1 != kNone) {
-#pragma unroll
-        for (int k = 0; k < 4; ++k)
-          bacc((double)hq[k] + (double)uu[k], (double)hq[k] + (double)pp[k], v[k], ba);
-      } else if (oQ1p != kNone) {
-        bacc((double)hq[3] + (double)uu[3], (double)hq[3] + (double)pp[3], v[0], ba);
-        bacc((double)hq[1] + (double)uu[1], (double)hq[1] + (double)pp[1], v[1], ba);
-        bacc((double)hq[2] + (double)uu[2], (double)hq[2] + (double)pp[2], v[2], ba);
-        bacc((double)hq[0] + (double)uu[0], (double)hq[0] + (double)pp[0], v[3], ba);
-      }
-    } else if (OFS && RES) {  // round((F(s) - c) - H[x]) at each stored copy; min of H + e
-      if (oQ1 != kNone) {
-        T st[4];
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          st[k] = (T)((v[k] + ba.sh) - (double)hq[k]);
-          ba.rmin = dmin(ba.rmin, (double)hq[k] + (double)st[k]);
-        }
-        st4(dst + oQ1 + o0, (double)st[0], (double)st[1], (double)st[2], (double)st[3]);
-      }
-      if (oQ1p != kNone) {  // position j holds output (3, 1, 2, 0)[j]
-        const double vv[4] = {v[3], v[1], v[2], v[0]};
-        T st[4];
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          st[k] = (T)((vv[k] + ba.sh) - (double)hp[k]);
-          ba.rmin = dmin(ba.rmin, (double)hp[k] + (double)st[k]);
-        }
-        st4(dst + oQ1p + qb, (double)st[0], (double)st[1], (double)st[2], (double)st[3]);
-      }
-    } else if (OFS) {  // round(F(s) - c) (the shift is an integer: exact before the rounding)
-      const T s0 = (T)(v[0] + ba.sh), s1 = (T)(v[1] + ba.sh), s2 = (T)(v[2] + ba.sh),
-              s3 = (T)(v[3] + ba.sh);
-      if (oQ1 != kNone) st4(dst + oQ1 + o0, (double)s0, (double)s1, (double)s2, (double)s3);
-      if (oQ1p != kNone) st4(dst + oQ1p + qb, (double)s3, (double)s1, (double)s2, (double)s0);
-      if (oQ1 != kNone || oQ1p != kNone)
-        ba.rmin = dmin(ba.rmin, dmin(dmin((double)s0, (double)s1), dmin((double)s2, (double)s3)));
-    } else {
-      if (oQ1 != kNone) st4(dst + oQ1 + o0, v[0], v[1], v[2], v[3]);
-      if (oQ1p != kNone) st4(dst + oQ1p + qb, v[3], v[1], v[2], v[0]);
-    }
-    // Q0 rows of the four groups
-    if (rows_x) {
-      q0_group<T, MW, WMODE, OFS, RES>(A, g >> 2, TT / 2, src, dst, of, om, prev, ba, base);
-      q0_group<T, MW, WMODE, OFS, RES>(B, (g >> 2) + 1, TT / 2, src, dst, of, om, prev, ba,
-                                        base);
-    }
-    if (rows_p) {
-      q0_group<T, MP, WMODE, OFS, RES>(Ap, u >> 2, TT / 2, src, dst, opf, opm, prev, ba, base);
-      q0_group<T, MP, WMODE, OFS, RES>(Bp, (u >> 2) + 1, TT / 2, src, dst, opf, opm, prev,
-                                        ba, base);
-    }
-  }
-}
-
-// next item >= c (step G) whose tile is the smaller member of its psi pair
-__device__ __forceinline__ uint64_t qnext(const QGeo& g, uint64_t c, uint64_t G, uint32_t LOG) {
-  while (c < g.ntiles) {
-    uint64_t x0, p0, taup;
-    qtile(g, c, LOG, x0, p0, taup);
-    if (taup >= c) return c;
-    c += G;
-  }
-  return c;
-}
-
-// map entries an item needs: windows t, psi t; runs Q1 t, Q1 psi t, rows/mirrors of both windows
-struct QItem {
-  uint32_t m[8];
-};
-template <int M>
-__device__ __forceinline__ void qlookup(const QGeo& g, const uint32_t* __restrict__ map,
-                                        uint64_t tau, QItem& it) {
-  constexpr uint32_t TT = 1u << (2 * M), LOG = 2 * M;
-  uint64_t x0, p0, taup;
-  qtile(g, tau, LOG, x0, p0, taup);
-  const uint64_t wb = qwin(g, x0), wp = qwin(g, p0);
-  const uint64_t yf = wb >> 2, ypf = wp >> 2;
-  const int sh = 2 * g.K;
-  it.m[0] = __ldg(map + (wb >> sh));
-  it.m[1] = __ldg(map + (wp >> sh));
-  it.m[2] = __ldg(map + (x0 >> sh));
-  it.m[3] = __ldg(map + (p0 >> sh));
-  it.m[4] = __ldg(map + (yf >> sh));
-  it.m[5] = __ldg(map + ((g.q1 - yf - TT / 2) >> sh));
-  it.m[6] = __ldg(map + (ypf >> sh));
-  it.m[7] = __ldg(map + ((g.q1 - ypf - TT / 2) >> sh));
-}
-
-// Thread 0: bulk-load the two windows of tile pair tau into a stage and record the item's
-// metadata: meta[0] = window modes (bits 0-1: window t, 2-3: window psi t, bit 4: self pair),
-// meta[1..6] = stored run starts (Q1 t, Q1 psi t, rows t, mirrors t, rows psi t, mirrors psi t;
-// kNone = not stored).
-template <typename T, int M, bool WMODE = false, bool RES = false>
-__device__ __forceinline__ void qissue(const QGeo& g, const QItem& it, uint64_t tau, T* buf,
-                                       uint64_t* bar, uint64_t* meta, const T* src,
-                                       uint32_t hints, uint64_t keep, const T* prev = nullptr,
-                                       const T* base = nullptr) {
-  constexpr uint32_t TT = 1u << (2 * M), LOG = 2 * M;
-  uint64_t x0, p0, taup;
-  qtile(g, tau, LOG, x0, p0, taup);
-  const bool self = taup == tau;
-  const uint64_t wb = qwin(g, x0), wp = qwin(g, p0);
-  const uint64_t yf = wb >> 2, ym = g.q1 - yf - TT / 2, ypf = wp >> 2, ypm = g.q1 - ypf - TT / 2;
-  const int sh = 2 * g.K;
-  const uint32_t mw = it.m[0], mp = it.m[1];
-  meta[0] = (mw & 3u) | ((mp & 3u) << 2) | (self ? 16u : 0u);
-  meta[1] = qrun(g, it.m[2], x0);
-  meta[2] = self ? kNone : qrun(g, it.m[3], p0);
-  meta[3] = qrun(g, it.m[4], yf);
-  meta[4] = qrun(g, it.m[5], ym);
-  meta[5] = self ? kNone : qrun(g, it.m[6], ypf);
-  meta[6] = self ? kNone : qrun(g, it.m[7], ypm);
-  mbar_expect_tx(bar, 2 * 2 * TT * (uint32_t)sizeof(T) * (RES ? 2 : 1));
-  // bound pass: u and v_prev at the item's stored output runs go to L2 now (bulk prefetch), so
-  // the consumers' direct loads of them, one item later, hit L2 (RES: the base there too, in
-  // the sweep as well)
-  if ((WMODE || RES) && ((TT / 2) * sizeof(T)) % 16 == 0) {
-    const uint64_t q = meta[1] != kNone ? meta[1] : meta[2];
-    if (q != kNone) {
-      if (WMODE) {
-        bulk_prefetch_l2(src + q, TT * (uint32_t)sizeof(T));
-        bulk_prefetch_l2(prev + q, TT * (uint32_t)sizeof(T));
-      }
-      if (RES) bulk_prefetch_l2(base + q, TT * (uint32_t)sizeof(T));
-    }
-    if (RES && !WMODE && meta[1] != kNone && meta[2] != kNone)
-      bulk_prefetch_l2(base + meta[2], TT * (uint32_t)sizeof(T));
-#pragma unroll
-    for (int k = 3; k < 7; ++k)
-      if (meta[k] != kNone) {
-        if (WMODE) {
-          bulk_prefetch_l2(src + meta[k], TT / 2 * (uint32_t)sizeof(T));
-          bulk_prefetch_l2(prev + meta[k], TT / 2 * (uint32_t)sizeof(T));
-        }
-        if (RES) bulk_prefetch_l2(base + meta[k], TT / 2 * (uint32_t)sizeof(T));
-      }
-  }
-#pragma unroll
-  for (int k = 0; k < (RES ? 4 : 2); ++k) {  // RES: k = 2, 3 load the base's windows
-    const uint32_t m = (k & 1) ? mp : mw;
-    const uint64_t w = (k & 1) ? wp : wb;
-    T* dst = buf + k * 2 * TT;
-    const T* blk = (k < 2 ? src : base) + ((uint64_t)(m >> 2) << sh);
-    const uint64_t e = w & g.kmask;
-    // L2 policy per piece (quarter_schedule): reloaded soon -> `keep`, else evict-first
-    const uint32_t hb = hints >> (2 * (k & 1));
-    const uint64_t pol0 = (hb & 1u) ? keep : kL2EvictFirst, pol1 = (hb & 2u) ? keep : kL2EvictFirst;
-    const uint64_t pol01 = (hb & 3u) ? keep : kL2EvictFirst;
-    if ((m & 3u) == 0) {
-      tma_load_1d_hint(dst, blk + e, 2 * TT * (uint32_t)sizeof(T), bar, pol01);
-    } else if ((m & 3u) == 3) {  // tail complement: one contiguous run, read reversed
-      tma_load_1d_hint(dst, blk + ((~e & g.kmask) & ~(2ull * TT - 1)), 2 * TT * (uint32_t)sizeof(T),
-                       bar, pol01);
-    } else {
-      const uint64_t f = ((m & 3u) == 1) ? pairswap(e) : pairswap(~e & g.kmask);
-      const uint64_t start = (f & ~(4ull * TT - 1)) | (f & TT);
-      tma_load_1d_hint(dst, blk + start, TT * (uint32_t)sizeof(T), bar, pol0);
-      tma_load_1d_hint(dst + TT, blk + start + 2 * TT, TT * (uint32_t)sizeof(T), bar, pol1);
-    }
-  }
-}
-
-template <typename T, int M, int S, bool WMODE, int MINB = 1, int NT = kThreads, int UNR = 1,
-          bool OFS = false, bool RES = false>
-__global__ void __launch_bounds__(NT, MINB) bin2q_kernel(Bin2QArgs a) {
-  using C = QCfg<T, M, S, WMODE, MINB, RES>;
-  constexpr uint32_t TT = C::TT, WIN = C::WIN;
-  constexpr uint32_t LOG = 2 * M;
-  extern __shared__ __align__(128) unsigned char smem_raw[];
-  T* in = reinterpret_cast<T*>(smem_raw);  // [S][STAGE]
-  uint64_t* bars = reinterpret_cast<uint64_t*>(in + (size_t)S * C::STAGE);
-  uint64_t* metas = bars + S;  // [S][8]
-
-  QGeo g;
-  const int L = 2 * a.ell;
-  g.K = a.K;
-  g.lmask = (1ull << L) - 1;
-  g.q1 = 1ull << (L - 2);
-  g.amask = 0xAAAAAAAAAAAAAAAAull & g.lmask;
-  g.bmask = 0x5555555555555555ull & g.lmask;
-  g.kmask = (1ull << (2 * a.K)) - 1;
-  g.ntiles = 1ull << (2 * (a.ell - 1 - M));
-  const T* src = reinterpret_cast<const T*>(a.src);
-  T* dst = reinterpret_cast<T*>(a.dst);
-  const uint32_t* map = a.map;
-  const int tid = threadIdx.x;
-  const uint64_t G = gridDim.x;
-
-  BAcc ba{-INFINITY, INFINITY, INFINITY, 0.0};
-  if (OFS) ba.sh = a.ost->shift;
-  const T* base = RES ? reinterpret_cast<const T*>(a.base) : nullptr;
-  const T* prev = reinterpret_cast<const T*>(a.prev);
-  // items: with a schedule, item c is the tile pair of tile sched[c] (c = blockIdx.x + k G);
-  // without one, the pair representatives in tile order
-  const uint32_t* sched = (a.sched && a.sched_m == M) ? a.sched : nullptr;
-  const uint64_t nitems = sched ? a.nitems : g.ntiles;
-  // item claims (thread 0): dynamic -- the next index of the shared counter; static -- this
-  // CTA's next representative in round-robin order
-  unsigned long long* counter = sched ? a.counter : nullptr;
-  auto first = [&](uint64_t c) { return sched ? c : qnext(g, c, G, LOG); };
-  auto claim = [&](uint64_t prev) -> uint64_t {
-    if (counter) return (uint64_t)atomicAdd(counter, 1ull);
-    return first(prev == ~0ull ? (uint64_t)blockIdx.x : prev + G);
-  };
-  auto entry = [&](uint64_t c) -> uint32_t { return sched ? __ldg(sched + c) : (uint32_t)c; };
-  auto tile_of = [&](uint64_t c) -> uint64_t {
-    return sched ? (uint64_t)(__ldg(sched + c) & kQTileMask) : c;
-  };
-  // hint bits only come with a schedule; without one every piece keeps the default policy
-  const uint64_t keep = (a.l2keep != 0) ? kL2EvictLast : kL2EvictNormal;
-  uint64_t pc = 0;  // producer cursor (thread 0 only)
-  QItem pit;        // its map entries, fetched one item ahead
-  if (tid == 0) {
-    for (int s = 0; s < S; ++s) mbar_init(&bars[s], 1);
-    fence_mbar_init();
-  }
-  __syncthreads();
-  // a stage either receives an item (meta[7] = 0, TMA completes its phase) or the end marker
-  // (meta[7] = 1, a plain arrive completes it); the claims are monotone, so after the first end
-  // marker every later stage is an end marker too
-  auto fill = [&](int s, T* sbuf) {
-    uint64_t* meta = metas + 8 * s;
-    if (pc < nitems) {
-      meta[7] = 0;
-      const uint32_t ent = entry(pc);
-      qissue<T, M, WMODE, RES>(g, pit, sched ? (uint64_t)(ent & kQTileMask) : (uint64_t)ent,
-                               sbuf, &bars[s], meta, src, sched ? (ent >> kQHintShift) : 0xFu,
-                               keep, prev, base);
-      pc = claim(pc);
-      if (pc < nitems) qlookup<M>(g, map, tile_of(pc), pit);
-    } else {
-      meta[7] = 1;
-      mbar_arrive(&bars[s]);
-    }
-  };
-  if (tid == 0) {
-    pc = claim(~0ull);
-    if (pc < nitems) qlookup<M>(g, map, tile_of(pc), pit);
-    for (int s = 0; s < S; ++s) fill(s, in + (size_t)s * C::STAGE);
-  }
-
-  for (uint32_t i = 0;; ++i) {
-    const uint32_t s = i % S;
-    const uint32_t parity = (i / S) & 1u;
-    T* buf = in + (size_t)s * C::STAGE;
-    const uint64_t* meta = metas + 8 * s;
-    mbar_wait(&bars[s], parity);
-    __syncthreads();
-    if (meta[7]) break;  // end marker: no more items for this CTA
-    const uint32_t modes = (uint32_t)meta[0];
-    const uint32_t mw = modes & 3u, mp = (modes >> 2) & 3u;  // 3 only for Q0 (same-head) blocks
-    const bool self = (modes & 16u) != 0;
-    const T* bw = buf;
-    const T* bp = buf + WIN;
-#define LCSB_Q1(MW, MP)                                                            \
-  if constexpr (sizeof(T) == 4 && !WMODE && !OFS && !RES)                          \
-    pair_quads_f32<T, TT, MW, MP>(bw, bp, src, dst, meta, self);                   \
-  else                                                                             \
-    pair_quads<T, TT, MW, MP, WMODE, NT, UNR, OFS, RES>(bw, bp, src, dst, meta, self, prev, ba, \
-                                                        base)
-    switch (mw * 4 + mp) {
-      case 0: LCSB_Q1(0, 0); break;
-      case 1: LCSB_Q1(0, 1); break;
-      case 2: LCSB_Q1(0, 2); break;
-      case 3: LCSB_Q1(0, 3); break;
-      case 4: LCSB_Q1(1, 0); break;
-      case 5: LCSB_Q1(1, 1); break;
-      case 6: LCSB_Q1(1, 2); break;
-      case 7: LCSB_Q1(1, 3); break;
-      case 8: LCSB_Q1(2, 0); break;
-      case 9: LCSB_Q1(2, 1); break;
-      case 10: LCSB_Q1(2, 2); break;
-      case 11: LCSB_Q1(2, 3); break;
-      case 12: LCSB_Q1(3, 0); break;
-      case 13: LCSB_Q1(3, 1); break;
-      case 14: LCSB_Q1(3, 2); break;
-      default: LCSB_Q1(3, 3); break;
-    }
-#undef LCSB_Q1
-    __syncthreads();  // stage s (data and metadata) is free again
-    if (tid == 0) fill((int)s, buf);
-  }
-  if (WMODE) block_red3_to(ba.rmax, ba.rmin, ba.dmin, a.red_out);
-  if (OFS && !WMODE) block_min_to(ba.rmin, a.omin);
-}
-
-template <typename T, int M, int S, bool WMODE, int MINB = 1, int NT = kThreads, int UNR = 1,
-          bool OFS = false, bool RES = false>
-cudaError_t launch_q(const Bin2QArgs& a, cudaStream_t s, int sms) {
-  using C = QCfg<T, M, S, WMODE, MINB, RES>;
-  static uint64_t cap = 0;
-  if (cap == 0) {
-    cudaError_t e = cudaFuncSetAttribute(bin2q_kernel<T, M, S, WMODE, MINB, NT, UNR, OFS, RES>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
-    if (e != cudaSuccess) return e;
-    int per_sm = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm,
-                                                      bin2q_kernel<T, M, S, WMODE, MINB, NT, UNR, OFS, RES>,
-                                                      NT, C::SMEM) != cudaSuccess ||
-        per_sm < 1) {
-      cudaGetLastError();
-      per_sm = 1;
-    }
-    cap = (uint64_t)per_sm * sms;
-  }
-  if (a.K < M + 1 || a.ell < a.K + 1) return cudaErrorInvalidValue;
-  const uint64_t ntiles =
-      (a.sched && a.sched_m == M) ? a.nitems : (1ull << (2 * (a.ell - 1 - M)));
-  uint64_t blocks = cap < ntiles ? cap : ntiles;
-  if (blocks < 1) blocks = 1;
-  bin2q_kernel<T, M, S, WMODE, MINB, NT, UNR, OFS, RES><<<(unsigned)blocks, NT, C::SMEM, s>>>(a);
-  return cudaGetLastError();
-}
-
+// the plain sweep (fp32 Q1 path) for the handle's tile 4^M
 template <bool WMODE>
 cudaError_t dispatch_q(const Bin2QArgs& a, int dtype, int M, cudaStream_t s, int sms) {
-  if (a.base) {  // residual storage (reading R24): fp32, windows of base and residual, M <= 5
-    if (dtype != LCSB_F32 || (!WMODE && !a.ost)) return cudaErrorInvalidValue;
-    constexpr int NT = kThreads;
-    switch (M < 5 ? M : 5) {
-      case 5: return launch_q<float, 5, 2, WMODE, 2, NT, 1, !WMODE, true>(a, s, sms);
-      case 4: return launch_q<float, 4, 2, WMODE, 1, NT, 1, !WMODE, true>(a, s, sms);
-      case 3: return launch_q<float, 3, 2, WMODE, 1, NT, 1, !WMODE, true>(a, s, sms);
-      case 2: return launch_q<float, 2, 2, WMODE, 1, NT, 1, !WMODE, true>(a, s, sms);
-      case 1: return launch_q<float, 1, 2, WMODE, 1, NT, 1, !WMODE, true>(a, s, sms);
-    }
-    return cudaErrorInvalidValue;
-  }
-  if (WMODE && dtype == LCSB_F32 && M == 6) {
-    static int wv = -1;  // LCSB_BIN2Q_WDIRECT=1 (A/B): the bound pass at 2 CTAs/SM
-    if (wv < 0) {
-      const char* e = getenv("LCSB_BIN2Q_WDIRECT");
-      wv = e ? atoi(e) : 0;
-    }
-    if (wv == 1) return launch_q<float, 6, 1, true, 2>(a, s, sms);
-    // LCSB_BIN2Q_WDIRECT=2 (A/B): one 512-thread CTA per SM with two stages (prefetch overlap)
-    if (wv == 2) return launch_q<float, 6, 2, true, 1, 512>(a, s, sms);
-    // 3 / 4 / 5: quads unrolled by 2 (3 CTAs/SM), by 4 (2 CTAs/SM), by 2 (2 CTAs/SM)
-    if (wv == 3) return launch_q<float, 6, 1, true, 3, kThreads, 2>(a, s, sms);
-    if (wv == 4) return launch_q<float, 6, 1, true, 2, kThreads, 4>(a, s, sms);
-    if (wv == 5) return launch_q<float, 6, 1, true, 2, kThreads, 2>(a, s, sms);
-    return launch_q<float, 6, 1, true, 3>(a, s, sms);
-  }
-  if (WMODE && dtype == LCSB_F64 && M == 5) return launch_q<double, 5, 1, true, 3>(a, s, sms);
-  if (!WMODE && a.ost) {  // integer offsets (reading R23): the fp64 Q1 path, shift and min
-    constexpr int NT = kThreads;
-    if (dtype == LCSB_F32) {
-      switch (M) {
-        case 6: return launch_q<float, 6, 1, false, 3, NT, 1, true>(a, s, sms);
-        case 5: return launch_q<float, 5, 2, false, 1, NT, 1, true>(a, s, sms);
-        case 4: return launch_q<float, 4, 2, false, 1, NT, 1, true>(a, s, sms);
-        case 3: return launch_q<float, 3, 2, false, 1, NT, 1, true>(a, s, sms);
-        case 2: return launch_q<float, 2, 2, false, 1, NT, 1, true>(a, s, sms);
-        case 1: return launch_q<float, 1, 2, false, 1, NT, 1, true>(a, s, sms);
-      }
-    } else {
-      switch (M) {
-        case 5: return launch_q<double, 5, 2, false, 2, NT, 1, true>(a, s, sms);
-        case 4: return launch_q<double, 4, 2, false, 1, NT, 1, true>(a, s, sms);
-        case 3: return launch_q<double, 3, 2, false, 1, NT, 1, true>(a, s, sms);
-        case 2: return launch_q<double, 2, 2, false, 1, NT, 1, true>(a, s, sms);
-        case 1: return launch_q<double, 1, 2, false, 1, NT, 1, true>(a, s, sms);
-      }
-    }
-    return cudaErrorInvalidValue;
-  }
   if (dtype == LCSB_F32) {
     switch (M) {
       case 6: return launch_q<float, 6, 1, WMODE, 3>(a, s, sms);  // A/B: variant 10
@@ -815,7 +50,8 @@ int bin2q_variant_m(int dtype, int variant) {
 
 cudaError_t launch_bin2q_sweep(const Bin2QArgs& a, int dtype, int M, int variant, cudaStream_t s,
                                int sms) {
-  if (variant <= 0 || a.ost || a.base) return dispatch_q<false>(a, dtype, M, s, sms);
+  if (a.ost || a.base) return launch_bin2q_sweep_ext(a, dtype, M, s, sms);  // kern_bin2q_ext.cu
+  if (variant <= 0) return dispatch_q<false>(a, dtype, M, s, sms);
   if (variant >= kQVariants) return cudaErrorInvalidValue;
 #define LCSB_QV(T, M_, S_, MB_) \
   if (d.m == M_ && d.s == S_ && d.mb == MB_) return launch_q<T, M_, S_, false, MB_>(a, s, sms);
@@ -833,9 +69,6 @@ cudaError_t launch_bin2q_sweep(const Bin2QArgs& a, int dtype, int M, int variant
   }
 #undef LCSB_QV
   return cudaErrorInvalidValue;
-}
-cudaError_t launch_bin2q_wpass(const Bin2QArgs& a, int dtype, int M, cudaStream_t s, int sms) {
-  return dispatch_q<true>(a, dtype, M, s, sms);
 }
 
 }  // namespace lcsbk

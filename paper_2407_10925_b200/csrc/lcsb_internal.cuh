@@ -375,6 +375,8 @@ cudaError_t launch_bin2q_sweep(const Bin2QArgs& a, int dtype, int M, int variant
                                int sms);
 int bin2q_variant_m(int dtype, int variant);
 cudaError_t launch_bin2q_wpass(const Bin2QArgs& a, int dtype, int M, cudaStream_t s, int sms);
+// the sweep with integer offsets (a.ost) or residual storage (a.base): kern_bin2q_ext.cu
+cudaError_t launch_bin2q_sweep_ext(const Bin2QArgs& a, int dtype, int M, cudaStream_t s, int sms);
 cudaError_t launch_q4_sweep(const Q4Args& a, int dtype, cudaStream_t s, int sms);
 cudaError_t launch_q4_wpass(const Q4Args& a, int dtype, cudaStream_t s, int sms);
 int q4_min_ell();
