@@ -157,12 +157,13 @@ def workload_name(args, w) -> str:
 
 
 def same_kernel_1gpu(w, stream, sweeps=8):
-    """State-updates/s of the sharded path's kernel (the binary half table, bin2) on ONE GPU at
-    l = 17 (config 4's size): the U_1 of SURVEY §8(e)'s efficiency U_P / (P U_1) for config 5,
-    whose l = 18 tables need the sharded layout's >= 2 GPUs."""
+    """State-updates/s of the sharded path's kernel (the quarter table, bin2q -- sharded as in
+    DESIGN.md §9c) on ONE GPU at l = 17 (config 4's size): the U_1 of SURVEY §8(e)'s efficiency
+    U_P / (P U_1) for config 5."""
     import torch
     from paper_2407_10925_b200 import Lcsb
-    h = Lcsb(2, 2, 17, dtype=w["dtype"], form="two_array", symmetry=1, stream=stream)
+    h = Lcsb(2, 2, 17, dtype=w["dtype"], form="two_array", stream=stream)
+    h.ready(wait=True)
     h.sweep(3)
     s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     s.record(stream)
@@ -174,8 +175,8 @@ def same_kernel_1gpu(w, stream, sweeps=8):
     h.destroy()
     torch.cuda.empty_cache()
     return {"value": (1 << 34) / (ms / 1e3), "unit": "state-updates/s", "ms_per_sweep": ms,
-            "kernel": kernel, "what": "l = 17 (config 4 size), fp32, the half table (bin2), one "
-            "GPU, sweeps only"}
+            "kernel": kernel, "what": "l = 17 (config 4 size), fp32, the quarter table (bin2q: the "
+            "kernel of the sharded run), one GPU, sweeps only"}
 
 
 def run_ours(args, w, ws, rank, local):
@@ -269,6 +270,13 @@ def run_ours(args, w, ws, rank, local):
         except Exception:
             traffic = None
 
+    tr = h.shard_traffic() if ws > 1 else None
+    if tr is not None:
+        nvlink_bytes = int(tr[0] + tr[1])
+    else:
+        nvlink_bytes = int(((stored // ws) * (4 if w["dtype"] == "f32" else 8) +
+                            (stored // ws // 16 * 8 if kernel_name == "q4" else 0)) * (1 - 1 / ws))
+
     # ---- end-to-end through the public API with host buffers (create .. gather to host)
     import numpy as np
     from seeded_inputs import splitmix64_indices  # the seeded index generator (no method math)
@@ -323,8 +331,10 @@ def run_ours(args, w, ws, rank, local):
             "workload": workload_name(args, w),
             "states": n_logical, "stored_states": stored, "sweeps_per_step": S,
             "kernel": kernel_name,
-            "parallelism": (f"sharded over {ws} GPUs ({args.transport} collectives + CUDA IPC "
-                            "peer stores)") if ws > 1
+            "parallelism": (f"sharded over {ws} GPUs ({args.transport} collectives; "
+                            + ("one mapped address range per table: peer reads + stores"
+                               if kernel_name == "bin2q" else "CUDA-IPC peer stores") + ")")
+                           if ws > 1
                            else ("process-sharded mode, 1 rank" if args.force_sharded
                                  else "single-gpu"),
             "scaling_definition": ("U_P / (P U_1) with U_1 = u1_same_kernel (SURVEY 8(e))"
@@ -351,12 +361,10 @@ def run_ours(args, w, ws, rank, local):
                      "peak_kind": peak_kind,
                      "algorithmic_bytes_per_launch": alg_bytes,
                      "requested_bytes_per_launch": requested_bytes,
-                     # peer stores per GPU per sweep: the outputs (and, q4, the row means) whose
-                     # owner is another shard -- a fraction (1 - 1/P) of the shard's (§9, §9b)
-                     "nvlink_bytes_per_launch": int(((stored // ws) * (4 if w["dtype"] == "f32"
-                                                    else 8) + (stored // ws // 16 * 8
-                                                    if kernel_name == "q4" else 0))
-                                                   * (1 - 1 / ws)),
+                     # per GPU per sweep: sharded quarter table -- the exact peer reads and
+                     # stores of its items (lcsb_shard_traffic, §9c); otherwise the outputs (and,
+                     # q4, the row means) whose owner is another shard, (1 - 1/P) of the shard's
+                     "nvlink_bytes_per_launch": nvlink_bytes,
                      "kernel": kernel_name + " sweep kernel"},
         "e2e": {"value": e2e_value, "unit": "state-updates/s",
                 "h2d_bytes_per_step": int(idx.nbytes),

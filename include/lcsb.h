@@ -260,7 +260,13 @@ int32_t lcsb_num_shards(const lcsb_t* h);   /* P (1 when unsharded) */
 uint64_t lcsb_num_states(const lcsb_t* h);   /* logical states sigma^(d l) */
 uint64_t lcsb_stored_states(const lcsb_t* h);/* entries per stored table */
 uint64_t lcsb_device_bytes(const lcsb_t* h); /* device bytes owned */
-int32_t lcsb_kernel_in_use(const lcsb_t* h); /* 1 generic, 2 binary half-table paired,
+int32_t lcsb_kernel_in_use(const lcsb_t* h);
+/* Sharded quarter table: the bytes one sweep of this handle's shards moves over
+ * NVLink -- windows read from another shard's memory, outputs stored into another shard's --
+ * and all the bytes it requests (windows + stored outputs), counted at creation from the item
+ * geometry.  Errors: EINVAL (another layout). */
+int lcsb_shard_traffic(const lcsb_t* h, uint64_t* peer_read_bytes, uint64_t* peer_written_bytes,
+                       uint64_t* requested_bytes); /* 1 generic, 2 binary half-table paired,
                                                 3 sigma=4 d=2 KS swap-paired,
                                                 4 register-resident small (sigma, d),
                                                 5 binary quarter-table paired */

@@ -9,7 +9,7 @@ CSRC = os.path.join(PKG, "csrc")
 SO = os.path.join(PKG, "liblcsb.so")
 SOURCES = ["lcsb_api.cu", "quarter_host.cu", "kern_generic.cu", "kern_bin2.cu", "kern_bin2_tma.cu",
            "kern_bin2q.cu", "kern_bin2q_bound.cu", "kern_bin2q_ext.cu", "kern_q4.cu",
-           "kern_small.cu", "kern_reduce.cu"]
+           "kern_small.cu", "kern_reduce.cu", "vmm.cu"]
 NVCC_FLAGS = [
     "-O3", "-std=c++17",
     "-gencode", "arch=compute_100a,code=sm_100a",
@@ -94,7 +94,7 @@ def build(force: bool = False, verbose: bool = False, out: str = SO, defines=())
                 os.replace(o, objs[i])
         tmp = out + tag
         res = subprocess.run([nvcc(), "-shared", "-gencode", "arch=compute_100a,code=sm_100a",
-                              *objs, "-o", tmp, "-lcudart", "-lnccl"],
+                              *objs, "-o", tmp, "-lcudart", "-lnccl", "-Xlinker", "-export-dynamic"],
                              capture_output=True, text=True)
         if res.returncode != 0:
             sys.stderr.write(res.stdout + res.stderr)

@@ -9,6 +9,7 @@
 #include <stdio.h>
 #include <stdlib.h>
 #include <string.h>
+#include <unistd.h>
 
 #include <atomic>
 #include <new>
@@ -40,6 +41,15 @@ struct lcsb {
   uint32_t* qsched;  // quarter table: item order of the sweep (NULL = natural order)
   size_t qsched_bytes;
   uint64_t qsched_n;
+  // sharded quarter table: each table is one virtual address range over the
+  // shards (vt[ring slot]); shard k's items in their own list (the L2 order filtered by owner)
+  int vmm;
+  VmmTable vt[kMaxGen];
+  uint64_t qmaxslots;  // stored blocks per shard stride
+  uint64_t peer_read, peer_written, all_moved;  // per sweep, this rank's shards, entries
+  uint32_t* qsched_sh[kMaxShards];
+  size_t qsched_bytes_sh[kMaxShards];
+  uint64_t qsched_n_sh[kMaxShards];
   unsigned long long* qcounter;  // quarter table: work counter of the scheduled kernels
   // the schedule is built on a host thread (lcsb_create returns without waiting for it); the
   // sweeps run in the natural item order -- identical results -- until install_schedule
@@ -233,6 +243,7 @@ static int plan_config(const lcsb_config* c, Plan* p, char* why, size_t whylen) 
     return LCSB_EINVAL;
   }
   const bool sharded = P > 1 || (has_comm && !c->virtual_shards);
+  const int lp0 = log2_exact(P);
   // quarter table geometry: blocks of 4^K, tiles of 4^M (M <= K - 1)
   int qK = c->block_log4;
   if (qK <= 0) {
@@ -244,8 +255,10 @@ static int plan_config(const lcsb_config* c, Plan* p, char* why, size_t whylen) 
   const int qM = qK - 1 < ((c->dtype == LCSB_F32) ? 6 : 5) ? qK - 1 : ((c->dtype == LCSB_F32) ? 6 : 5);
   // the item schedule packs a tile index into kQHintShift bits, so the tiles of 4^qM must number
   // at most 2^kQHintShift (larger counts would alias tiles)
-  const bool quarter_ok = sym_ok && !sharded && qK >= 2 && qK <= c->ell - 1 && c->ell - qK <= 16 &&
-                          2 * (c->ell - 1 - qM) <= kQHintShift;
+  // sharded (§9c): the shard key needs p non-head pairs in a block prefix (l - K - 1 >= p)
+  const bool quarter_ok = sym_ok && qK >= 2 && qK <= c->ell - 1 && c->ell - qK <= 16 &&
+                          2 * (c->ell - 1 - qM) <= kQHintShift &&
+                          (!sharded || (lp0 >= 0 && c->ell - qK - 1 >= lp0));
   // integer offsets (reading R23): two-array form, unsharded; the quarter table or the generic
   // kernel carry the per-sweep shift and min
   const int ofs = c->offset_policy;
@@ -269,9 +282,9 @@ static int plan_config(const lcsb_config* c, Plan* p, char* why, size_t whylen) 
   }
   if (sym == 2 && !quarter_ok) {
     snprintf(why, whylen,
-             "the quarter table needs the two-array binary form, the AUTO kernel, no sharding "
-             "and 2 <= block_log4 <= ell - 1 (ell - block_log4 <= 16, at most 2^28 tiles of "
-             "4^(block_log4 - 1))");
+             "the quarter table needs the two-array binary form, the AUTO kernel, "
+             "2 <= block_log4 <= ell - 1 (ell - block_log4 <= 16, at most 2^28 tiles of "
+             "4^(block_log4 - 1)) and, sharded, ell - block_log4 - 1 >= log2(shards)");
     return LCSB_EINVAL;
   }
   if (sym < 0 || sym > 2) {
@@ -289,6 +302,15 @@ static int plan_config(const lcsb_config* c, Plan* p, char* why, size_t whylen) 
   const bool q4_shard = c->sigma == 4 && c->d == 2 && c->kernel == LCSB_KERNEL_AUTO &&
                         c->ell >= q4_min_ell() && c->ell >= (lp == 3 ? 5 : 4);
   if (sharded && q4_shard) {
+    if (!c->virtual_shards && (c->shard < 0 || c->shard >= P)) {
+      snprintf(why, whylen, "shard must be in [0, %d)", P);
+      return LCSB_EINVAL;
+    }
+    if (!c->virtual_shards && !has_comm) {
+      snprintf(why, whylen, "process-sharded mode needs nccl_id or comm hooks");
+      return LCSB_EINVAL;
+    }
+  } else if (sharded && sym == 2) {  // the sharded quarter table (§9c)
     if (!c->virtual_shards && (c->shard < 0 || c->shard >= P)) {
       snprintf(why, whylen, "shard must be in [0, %d)", P);
       return LCSB_EINVAL;
@@ -348,6 +370,14 @@ static int plan_config(const lcsb_config* c, Plan* p, char* why, size_t whylen) 
   p->n_stored = (sym == 2) ? quarter_slots(c->ell, qK) << (2 * qK)
                            : ((sym || p->kernel == 3) ? n / 2 : n);
   p->n_local = p->n_stored / (uint64_t)P;
+  if (sym == 2 && P > 1) {  // shard-major slots with the stride of the largest shard (§9c)
+    const uint64_t mx = quarter_shard_maxslots(c->ell, qK, lp);
+    if (!mx) {
+      snprintf(why, whylen, "no shard map for ell = %d, block_log4 = %d, %d shards", c->ell, qK, P);
+      return LCSB_EINVAL;
+    }
+    p->n_local = mx << (2 * qK);
+  }
   p->esize = (c->dtype == LCSB_F32) ? 4 : 8;
   const uint64_t owned = (p->mode == MODE_PROCESS) ? 1 : (uint64_t)P;
   uint64_t tb, all;
@@ -531,14 +561,19 @@ extern "C" void lcsb_destroy(lcsb_t* h) {
   if (h->mode == MODE_PROCESS && (h->comm || hooks(h))) {
     barrier(h);  // no peer may still be writing into our tables
     cudaStreamSynchronize(s);
-    for (int k = 0; k < h->P; ++k)
+    for (int k = 0; k < h->P && !h->vmm; ++k)
       if (!owns(h, k))
         for (int i = 0; i < ipc_nbuf(h); ++i)
           if (*ipc_buf(h, k, i)) cudaIpcCloseMemHandle(*ipc_buf(h, k, i));
   }
-  for (int k = 0; k < h->P; ++k)
-    if (owns(h, k))
-      for (int i = 0; i < h->ntab; ++i) dev_free(h, h->tabs[k][i], h->tab_bytes);
+  if (h->vmm) {
+    for (int i = 0; i < h->ntab; ++i) vmm_release(&h->vt[i]);
+  } else {
+    for (int k = 0; k < h->P; ++k)
+      if (owns(h, k))
+        for (int i = 0; i < h->ntab; ++i) dev_free(h, h->tabs[k][i], h->tab_bytes);
+  }
+  for (int k = 0; k < kMaxShards; ++k) dev_free(h, h->qsched_sh[k], h->qsched_bytes_sh[k]);
   dev_free(h, h->red, 256);
   dev_free(h, h->ost, 512);
   dev_free(h, h->base, h->tab_bytes);
@@ -612,8 +647,99 @@ static int exchange_ipc(lcsb_t* h) {
 
 static int install_schedule(lcsb_t* h, bool wait);
 
+// LCSB_DEBUG: a SIGSEGV handler that prints the native backtrace (diagnosis only)
+#include <execinfo.h>
+#include <signal.h>
+static void segv_backtrace(int sig) {
+  void* fr[64];
+  const int n = backtrace(fr, 64);
+  fprintf(stderr, "[lcsb] signal %d, native backtrace:\n", sig);
+  backtrace_symbols_fd(fr, n, 2);
+  signal(sig, SIG_DFL);
+  raise(sig);
+}
+static void debug_hooks() {
+  static bool done = false;
+  if (!done && getenv("LCSB_DEBUG")) {
+    signal(SIGSEGV, segv_backtrace);
+    done = true;
+  }
+}
+
+// process mode: every rank's bytes (n each, host memory) in rank order, through the comm hooks or
+// the library's NCCL communicator
+static int allgather_host(lcsb_t* h, const void* mine, void* all, size_t n) {
+  if (const lcsb_comm_hooks* c = hooks(h)) {
+    if (c->allgather(mine, all, n, c->ctx) != 0)
+      return set_err(h, LCSB_ENCCL, "comm hook allgather failed");
+    return LCSB_OK;
+  }
+  cudaStream_t s = (cudaStream_t)h->cfg.stream;
+  char* d = nullptr;
+  CU(h, cudaMalloc(&d, n * (size_t)(h->P + 1)));
+  cudaError_t e = cudaMemcpyAsync(d + n * h->P, mine, n, cudaMemcpyHostToDevice, s);
+  ncclResult_t r = ncclSuccess;
+  if (e == cudaSuccess) r = ncclAllGather(d + n * h->P, d, n, ncclUint8, h->comm, s);
+  if (e == cudaSuccess && r == ncclSuccess)
+    e = cudaMemcpyAsync(all, d, n * h->P, cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  cudaFree(d);
+  if (r != ncclSuccess) return set_err(h, LCSB_ENCCL, "allgather: %s", ncclGetErrorString(r));
+  if (e != cudaSuccess) return set_err(h, LCSB_ECUDA, "allgather: %s", cudaGetErrorString(e));
+  return LCSB_OK;
+}
+
+// process mode, sharded quarter table (§9c): map every peer's shard allocations into this
+// process's table ranges -- POSIX fds of the allocations over Unix sockets (vmm.cu)
+static int exchange_vmm(lcsb_t* h) {
+  static const bool dbg = getenv("LCSB_DEBUG") != nullptr;
+#define VDBG(...) do { if (dbg) { fprintf(stderr, "[lcsb r%d] ", h->cfg.shard); fprintf(stderr, __VA_ARGS__); fprintf(stderr, "\n"); } } while (0)
+  uint64_t tok[kMaxShards];
+  uint64_t mine = ((uint64_t)getpid() << 20) ^ (uint64_t)(uintptr_t)h ^ (uint64_t)h->cfg.shard;
+  int rc = allgather_host(h, &mine, tok, sizeof mine);
+  if (rc != LCSB_OK) return rc;
+  const uint64_t token = tok[0];  // rank 0's: one name space per handle
+  char why[256];
+  VDBG("token %llx", (unsigned long long)token);
+  const int ls = fdx_listen(token, h->cfg.shard, why, sizeof why);
+  VDBG("listening %d", ls);
+  if (ls < 0) return set_err(h, LCSB_ECUDA, "sharded quarter table: %s", why);
+  int fds[kMaxGen];
+  int nf = 0;
+  rc = barrier(h);  // every rank listens (the NCCL barrier completes on the stream: wait for it)
+  if (rc == LCSB_OK && cudaStreamSynchronize((cudaStream_t)h->cfg.stream) != cudaSuccess)
+    rc = set_err(h, LCSB_ECUDA, "sharded quarter table: stream synchronisation failed");
+  for (int i = 0; rc == LCSB_OK && i < h->ntab; ++i, ++nf)
+    if (!vmm_export_fd(&h->vt[i], h->cfg.shard, &fds[i], why, sizeof why))
+      rc = set_err(h, LCSB_ECUDA, "sharded quarter table: %s", why);
+  VDBG("exported %d fds rc %d", nf, rc);
+  for (int k = 0; rc == LCSB_OK && k < h->P; ++k)
+    if (k != h->cfg.shard && !fdx_send(token, h->cfg.shard, k, fds, h->ntab, why, sizeof why))
+      rc = set_err(h, LCSB_ECUDA, "sharded quarter table: %s", why);
+  VDBG("sent rc %d", rc);
+  for (int i = 0; i < nf; ++i) close(fds[i]);
+  for (int got = 0; rc == LCSB_OK && got < h->P - 1; ++got) {
+    int from = -1, in[kMaxGen];
+    if (!fdx_recv(ls, &from, in, h->ntab, why, sizeof why)) {
+      rc = set_err(h, LCSB_ECUDA, "sharded quarter table: %s", why);
+      break;
+    }
+    for (int i = 0; i < h->ntab; ++i) {
+      if (rc == LCSB_OK && (from < 0 || from >= h->P || from == h->cfg.shard ||
+                            !vmm_import_fd(&h->vt[i], from, in[i], why, sizeof why)))
+        rc = set_err(h, LCSB_ECUDA, "sharded quarter table (shard %d): %s", from, why);
+      close(in[i]);
+    }
+    VDBG("imported from %d rc %d", from, rc);
+  }
+  close(ls);
+#undef VDBG
+  return rc;
+}
+
 extern "C" int lcsb_create_ex(const lcsb_config* cfg, lcsb_t** out) {
   if (!out) return set_err(nullptr, LCSB_EINVAL, "out is NULL");
+  debug_hooks();
   *out = nullptr;
   Plan p;
   char why[256];
@@ -684,7 +810,27 @@ extern "C" int lcsb_create_ex(const lcsb_config* cfg, lcsb_t** out) {
     }
     cudaMemsetAsync(h->barrier_buf, 0, 256, s);
   }
-  for (int k = h->first; k < h->first + h->nown; ++k) {
+  static const bool cdbg = getenv("LCSB_DEBUG") != nullptr;
+  if (cdbg) fprintf(stderr, "[lcsb] create: tables (mode %d, P %d, sym %d)\n", h->mode, h->P, h->symmetric);
+  h->vmm = h->symmetric == 2 && h->P > 1;
+  if (h->vmm) {  // sharded quarter table: one VA range per ring slot, shard k at k * stride
+    const size_t g = vmm_granularity(dev);
+    h->tab_bytes = (h->tab_bytes + g - 1) / g * g;
+    char why2[256];
+    for (int i = 0; i < h->ntab; ++i) {
+      bool ok = vmm_reserve(&h->vt[i], h->P, h->tab_bytes, dev, why2, sizeof why2);
+      for (int k = h->first; ok && k < h->first + h->nown; ++k)
+        ok = vmm_create_shard(&h->vt[i], k, h->mode == MODE_PROCESS, why2, sizeof why2);
+      if (!ok) {
+        lcsb_destroy(h);
+        return set_err(nullptr, LCSB_ECAPACITY, "sharded quarter table: %s", why2);
+      }
+      for (int k = 0; k < h->P; ++k)
+        h->tabs[k][i] = (char*)h->vt[i].base + (size_t)k * h->tab_bytes;
+    }
+    if (cdbg) fprintf(stderr, "[lcsb] create: vmm tables mapped\n");
+  }
+  for (int k = h->first; !h->vmm && k < h->first + h->nown; ++k) {
     for (int i = 0; i < h->ntab; ++i) {
       h->tabs[k][i] = dev_alloc(h, h->tab_bytes);
       if (!h->tabs[k][i]) {
@@ -739,15 +885,57 @@ extern "C" int lcsb_create_ex(const lcsb_config* cfg, lcsb_t** out) {
       }
     }
   }
+  if (cdbg) fprintf(stderr, "[lcsb] create: map\n");
   if (h->symmetric == 2) {  // quarter table block map (host-built, uploaded once)
     const uint64_t nb = quarter_map_entries(cfg->ell, h->qK);
     h->qmap_bytes = nb * sizeof(uint32_t);
     uint32_t* hm = (uint32_t*)malloc(h->qmap_bytes);
     h->qmap = (uint32_t*)dev_alloc(h, h->qmap_bytes);
-    const bool ok = hm && h->qmap && build_quarter_map(cfg->ell, h->qK, hm);
+    const bool ok = hm && h->qmap &&
+                    (h->vmm ? build_quarter_map_sharded(cfg->ell, h->qK, h->p, hm, &h->qmaxslots)
+                            : build_quarter_map(cfg->ell, h->qK, hm));
     e = ok ? cudaMemcpyAsync(h->qmap, hm, h->qmap_bytes, cudaMemcpyHostToDevice, s) : cudaSuccess;
     if (e == cudaSuccess && ok) e = cudaStreamSynchronize(s);
-    if (ok && e == cudaSuccess && !getenv("LCSB_NO_QSCHED") && cfg->ell - h->qM - 1 >= 4) {
+    if (ok && e == cudaSuccess && h->vmm) {
+      // sharded (§9c): the items of each owned shard -- the L2 order filtered by owner (built
+      // here, synchronously: every rank derives the same lists), dynamic claiming per launch
+      std::vector<uint32_t> sched, mine;
+      if (cdbg) fprintf(stderr, "[lcsb] create: schedule (maxslots %llu)\n", (unsigned long long)h->qmaxslots);
+      if (!getenv("LCSB_NO_QSCHED") && cfg->ell - h->qM - 1 >= 4) {
+        // the L2 order depends only on which items share stored blocks: built (and cached) on
+        // the unsharded slot numbering, whose slot count sizes its arrays
+        std::vector<uint32_t> plain(nb);
+        if (!build_quarter_map(cfg->ell, h->qK, plain.data()) ||
+            !quarter_schedule(cfg->ell, h->qK, h->qM, plain.data(), sched))
+          sched.clear();
+      }
+      if (cdbg) fprintf(stderr, "[lcsb] create: schedule %zu\n", sched.size());
+      for (int k = h->first; k < h->first + h->nown && e == cudaSuccess; ++k) {
+        quarter_shard_items(cfg->ell, h->qK, h->qM, hm, h->qmaxslots, k, sched, mine);
+        if (cdbg) fprintf(stderr, "[lcsb] create: shard %d items %zu\n", k, mine.size());
+        uint64_t tr[3];
+        quarter_shard_traffic(cfg->ell, h->qK, h->qM, hm, h->qmaxslots, k, mine, tr);
+        h->peer_read += tr[0];
+        h->peer_written += tr[1];
+        h->all_moved += tr[2];
+        h->qsched_n_sh[k] = mine.size();
+        h->qsched_bytes_sh[k] = (mine.size() ? mine.size() : 1) * sizeof(uint32_t);
+        h->qsched_sh[k] = (uint32_t*)dev_alloc(h, h->qsched_bytes_sh[k]);
+        if (!h->qsched_sh[k]) {
+          e = cudaErrorMemoryAllocation;
+          break;
+        }
+        if (!mine.empty())
+          e = cudaMemcpyAsync(h->qsched_sh[k], mine.data(), mine.size() * sizeof(uint32_t),
+                              cudaMemcpyHostToDevice, s);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+      }
+      if (e == cudaSuccess && h->qM >= 6 && !getenv("LCSB_QSTATIC")) {
+        h->qcounter = (unsigned long long*)dev_alloc(h, 256);
+        if (!h->qcounter) e = cudaErrorMemoryAllocation;
+      }
+    } else if (ok && e == cudaSuccess && !getenv("LCSB_NO_QSCHED") &&
+               cfg->ell - h->qM - 1 >= 4) {
       // the L2 item order of the sweep (large tables), built on a host thread: it changes only
       // the order of the items, never a value (every output is written once from the previous
       // table), so the first sweeps may run without it
@@ -787,8 +975,9 @@ extern "C" int lcsb_create_ex(const lcsb_config* cfg, lcsb_t** out) {
         return set_err(nullptr, LCSB_ECUDA, "cudaMemsetAsync failed: %s", cudaGetErrorString(e));
       }
     }
+  if (cdbg) fprintf(stderr, "[lcsb] create: exchange\n");
   if (h->mode == MODE_PROCESS) {
-    rc = exchange_ipc(h);
+    rc = h->vmm ? exchange_vmm(h) : exchange_ipc(h);
     if (rc == LCSB_OK) rc = barrier(h);
     if (rc != LCSB_OK) {
       char msg[512];
@@ -1063,10 +1252,19 @@ static int enqueue_sweeps(lcsb_t* h, int64_t n, cudaStream_t s) {
         a.ost = h->ost;
         a.omin = &h->ost->mn[out];
       }
-      if (a.counter && e == cudaSuccess)
-        e = cudaMemsetAsync(a.counter, 0, sizeof(unsigned long long), s);
-      if (e == cudaSuccess) e = launch_bin2q_sweep(a, h->cfg.dtype, h->qM, h->bin2q_variant, s, h->sms);
-      h->launches += 1;
+      // sharded (§9c): one launch per owned shard over its item list; the table pointers span
+      // every shard (reads of other shards' windows and stores of their outputs go to peers)
+      for (int k = h->first; k < h->first + h->nown && e == cudaSuccess; ++k) {
+        if (h->vmm) {
+          a.sched = h->qsched_sh[k];
+          a.nitems = h->qsched_n_sh[k];
+        }
+        if (a.counter) e = cudaMemsetAsync(a.counter, 0, sizeof(unsigned long long), s);
+        if (e == cudaSuccess)
+          e = launch_bin2q_sweep(a, h->cfg.dtype, h->qM, h->bin2q_variant, s, h->sms);
+        h->launches += 1;
+        if (!h->vmm) break;
+      }
     } else if (h->kernel == 3) {
       // row means of v_{n-2} (KS) / of v_{n-1}, the table this sweep reads (two-array)
       const int pin = (h->form == LCSB_FORM_KS) ? (h->pcur + 2) % 3 : h->pcur;
@@ -1192,9 +1390,16 @@ extern "C" int lcsb_bound(lcsb_t* h, lcsb_bound_t* out) {
     fill_bin2q(h, &a, h->cur, -1);
     a.prev = h->tabs[0][prev];
     a.red_out = h->red;
-    if (a.counter) CU(h, cudaMemsetAsync(a.counter, 0, sizeof(unsigned long long), s));
-    CU(h, launch_bin2q_wpass(a, h->cfg.dtype, h->qM, s, h->sms));
-    h->launches += 1;
+    for (int k = h->first; k < h->first + h->nown; ++k) {  // sharded: each owned shard's items
+      if (h->vmm) {
+        a.sched = h->qsched_sh[k];
+        a.nitems = h->qsched_n_sh[k];
+      }
+      if (a.counter) CU(h, cudaMemsetAsync(a.counter, 0, sizeof(unsigned long long), s));
+      CU(h, launch_bin2q_wpass(a, h->cfg.dtype, h->qM, s, h->sms));
+      h->launches += 1;
+      if (!h->vmm) break;
+    }
   } else if (h->kernel == 3) {
     for (int k = h->first; k < h->first + h->nown; ++k) {
       Q4Args a;
@@ -1530,5 +1735,15 @@ extern "C" uint64_t lcsb_device_bytes(const lcsb_t* h) {
   return b;
 }
 extern "C" int32_t lcsb_kernel_in_use(const lcsb_t* h) { return h ? h->kernel : 0; }
+extern "C" int lcsb_shard_traffic(const lcsb_t* h, uint64_t* peer_read_bytes,
+                                  uint64_t* peer_written_bytes, uint64_t* requested_bytes) {
+  if (!h || !peer_read_bytes || !peer_written_bytes || !requested_bytes)
+    return set_err(nullptr, LCSB_EINVAL, "NULL argument");
+  if (!h->vmm) return set_err(nullptr, LCSB_EINVAL, "not a sharded quarter table");
+  *peer_read_bytes = h->peer_read * h->esize;
+  *peer_written_bytes = h->peer_written * h->esize;
+  *requested_bytes = h->all_moved * h->esize;
+  return LCSB_OK;
+}
 extern "C" int64_t lcsb_launch_count(const lcsb_t* h) { return h ? h->launches : 0; }
 extern "C" const char* lcsb_last_error(const lcsb_t* h) { return h ? h->err : g_err; }

@@ -201,6 +201,31 @@ uint64_t quarter_slots(int ell, int K);        // stored (canonical) blocks
 bool build_quarter_map(int ell, int K, uint32_t* map);
 bool quarter_schedule(int ell, int K, int M, const uint32_t* map, std::vector<uint32_t>& out);
 bool quarter_schedule_cached(int ell, int K, int M, std::vector<uint32_t>& out);  // no build
+// sharded quarter table: shard-major slots with a stride of the largest shard
+bool build_quarter_map_sharded(int ell, int K, int p, uint32_t* map, uint64_t* maxslots);
+uint64_t quarter_shard_maxslots(int ell, int K, int p);
+void quarter_shard_items(int ell, int K, int M, const uint32_t* map, uint64_t maxslots, int shard,
+                         const std::vector<uint32_t>& sched, std::vector<uint32_t>& out);
+void quarter_shard_traffic(int ell, int K, int M, const uint32_t* map, uint64_t maxslots,
+                           int shard, const std::vector<uint32_t>& items, uint64_t out[3]);
+
+// vmm.cu: one virtual address range over the shards of a table (shard k at k * stride)
+struct VmmTable {
+  void* base;
+  size_t stride;
+  int P, device;
+  unsigned long long handle[kMaxShards];
+  int mapped[kMaxShards];
+};
+size_t vmm_granularity(int device);
+bool vmm_reserve(VmmTable* t, int P, size_t stride, int device, char* why, size_t wl);
+bool vmm_create_shard(VmmTable* t, int k, bool exportable, char* why, size_t wl);
+bool vmm_export_fd(VmmTable* t, int k, int* fd, char* why, size_t wl);
+bool vmm_import_fd(VmmTable* t, int k, int fd, char* why, size_t wl);
+void vmm_release(VmmTable* t);
+int fdx_listen(uint64_t token, int rank, char* why, size_t wl);
+bool fdx_send(uint64_t token, int from, int to, const int* fds, int n, char* why, size_t wl);
+bool fdx_recv(int lsock, int* from, int* fds, int n, char* why, size_t wl);
 
 // Sharding of the sigma = 4, d = 2 complement-folded table over 2^p shards.
 // State s: 4l bits, character group g (g = 0 the heads) at bits [4(l-1-g), 4(l-g)), the a digit

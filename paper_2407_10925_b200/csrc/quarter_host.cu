@@ -52,6 +52,111 @@ bool build_quarter_map(int ell, int K, uint32_t* map) {
   return next == quarter_slots(ell, K);
 }
 
+// ---- sharded quarter table.  Shard of a canonical block: the xor key of the
+// first p non-head character pairs of its prefix, x_i = a_i ^ b_i -- invariant under the block
+// symmetries (swap, psi, tail complement), so a block and its images agree.  Slots are renumbered
+// shard-major with a fixed stride of `maxslots` per shard (the largest shard), so the slot of a
+// block also names its shard (slot / maxslots) and its place in that shard's memory.
+static uint32_t qblock_key(uint64_t beta, int PL, int p) {
+  uint32_t k = 0;
+  for (int i = 1; i <= p; ++i) {
+    const uint32_t pair = (uint32_t)(beta >> (PL - 2 - 2 * i)) & 3u;
+    k = (k << 1) | ((pair >> 1) ^ (pair & 1u));
+  }
+  return k;
+}
+
+bool build_quarter_map_sharded(int ell, int K, int p, uint32_t* map, uint64_t* maxslots) {
+  if (!build_quarter_map(ell, K, map)) return false;
+  const int PL = 2 * (ell - K);
+  if (p < 0 || ell - K - 1 < p) return false;
+  const uint64_t nb = quarter_map_entries(ell, K), ns = quarter_slots(ell, K);
+  const uint32_t P = 1u << p;
+  std::vector<uint32_t> newslot(ns);
+  std::vector<uint64_t> cnt(P, 0);
+  for (uint64_t b = 0; b < nb; ++b)  // canonical blocks in slot order
+    if ((map[b] & 3u) == 0) newslot[map[b] >> 2] = (uint32_t)(cnt[qblock_key(b, PL, p)]++);
+  uint64_t mx = 0;
+  for (uint32_t k = 0; k < P; ++k) mx = cnt[k] > mx ? cnt[k] : mx;
+  if (mx * P >= (1ull << 30)) return false;  // map entries hold slot << 2 in 32 bits
+  for (uint64_t b = 0; b < nb; ++b)
+    if ((map[b] & 3u) == 0)
+      newslot[map[b] >> 2] += (uint32_t)(qblock_key(b, PL, p) * mx);
+  for (uint64_t b = 0; b < nb; ++b)
+    map[b] = (newslot[map[b] >> 2] << 2) | (map[b] & 3u);
+  *maxslots = mx;
+  return true;
+}
+
+uint64_t quarter_shard_maxslots(int ell, int K, int p) {
+  std::vector<uint32_t> map(quarter_map_entries(ell, K));
+  uint64_t mx = 0;
+  return build_quarter_map_sharded(ell, K, p, map.data(), &mx) ? mx : 0;
+}
+
+// The items (tile pairs) of one shard -- those whose first window (tile t's adv_b window) lies in
+// the shard -- in the order of `sched` (entries with hint bits) or, if empty, in tile order.
+void quarter_shard_items(int ell, int K, int M, const uint32_t* map, uint64_t maxslots,
+                         int shard, const std::vector<uint32_t>& sched, std::vector<uint32_t>& out) {
+  const int L = 2 * ell;
+  const uint64_t lmask = (1ull << L) - 1, q1 = 1ull << (L - 2);
+  const uint64_t amask = 0xAAAAAAAAAAAAAAAAull & lmask, bmask = 0x5555555555555555ull & lmask;
+  const uint64_t T = 1ull << (2 * M);
+  auto owner = [&](uint64_t tau) {
+    const uint64_t x0 = q1 + tau * T;
+    const uint64_t w = (x0 & amask) | ((x0 & bmask & ~q1) << 2);
+    return (int)((map[w >> (2 * K)] >> 2) / maxslots);
+  };
+  out.clear();
+  if (!sched.empty()) {
+    for (uint32_t e : sched)
+      if (owner(e & kQTileMask) == shard) out.push_back(e);
+    return;
+  }
+  const uint64_t ntiles = 1ull << (2 * (ell - 1 - M));
+  for (uint64_t tau = 0; tau < ntiles; ++tau) {
+    const uint64_t x0 = q1 + tau * T;
+    const uint64_t p0 = pairswap_hd(~x0 & lmask) & ~(T - 1);
+    if (((p0 - q1) >> (2 * M)) < tau) continue;  // the pair is an item at its smaller tile
+    if (owner(tau) == shard) out.push_back((uint32_t)tau | (0xFu << kQHintShift));
+  }
+}
+
+// Entries one shard's sweep moves over NVLink (sharded quarter table): for each of its items,
+// the psi window when another shard stores it (read) and every stored output run another shard
+// owns (written) -- the same geometry as the kernel's qissue / qrun.  out[0] = entries read,
+// out[1] = entries written remotely, out[2] = entries read + written in total (local + remote).
+void quarter_shard_traffic(int ell, int K, int M, const uint32_t* map, uint64_t maxslots,
+                           int shard, const std::vector<uint32_t>& items, uint64_t out[3]) {
+  const int L = 2 * ell;
+  const uint64_t lmask = (1ull << L) - 1, q1 = 1ull << (L - 2);
+  const uint64_t amask = 0xAAAAAAAAAAAAAAAAull & lmask, bmask = 0x5555555555555555ull & lmask;
+  const uint64_t T = 1ull << (2 * M);
+  const int sh = 2 * K;
+  auto win = [&](uint64_t x) { return (x & amask) | ((x & bmask & ~q1) << 2); };
+  auto shard_of = [&](uint64_t s) { return (int)((map[s >> sh] >> 2) / maxslots); };
+  auto stored = [&](uint64_t s) { return (map[s >> sh] & 3u) == 0; };
+  out[0] = out[1] = out[2] = 0;
+  for (uint32_t ent : items) {
+    const uint64_t tau = ent & kQTileMask;
+    const uint64_t x0 = q1 + tau * T;
+    const uint64_t p0 = pairswap_hd(~x0 & lmask) & ~(T - 1);
+    const bool self = ((p0 - q1) >> (2 * M)) == tau;
+    const uint64_t wb = win(x0), wp = win(p0);
+    out[2] += 4 * T;  // both windows read
+    if (shard_of(wp) != shard) out[0] += 2 * T;
+    const uint64_t yf = wb >> 2, ypf = wp >> 2;
+    const uint64_t runs[6] = {x0, p0, yf, q1 - yf - T / 2, ypf, q1 - ypf - T / 2};
+    const uint64_t len[6] = {T, T, T / 2, T / 2, T / 2, T / 2};
+    for (int r = 0; r < 6; ++r) {
+      if (self && (r == 1 || r >= 4)) continue;
+      if (!stored(runs[r])) continue;
+      out[2] += len[r];
+      if (shard_of(runs[r]) != shard) out[1] += len[r];
+    }
+  }
+}
+
 // Item order of the quarter sweep ("L2 schedule").  Block graph: nodes = stored
 // blocks, edges = tile pairs {t, psi t} joining the stored blocks of their two adv_b windows;
 // every block has four window ends (two per logical image).  A 2-colouring that cuts most edges

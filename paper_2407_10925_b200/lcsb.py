@@ -66,6 +66,7 @@ EXPORTS = ["lcsb_config_init", "lcsb_required_bytes", "lcsb_create", "lcsb_creat
            "lcsb_sweeps_done",
            "lcsb_num_shards",
            "lcsb_num_states", "lcsb_stored_states", "lcsb_device_bytes", "lcsb_kernel_in_use",
+           "lcsb_shard_traffic",
            "lcsb_launch_count", "lcsb_last_error", "lcsb_destroy"]
 NCCL_ID_BYTES = 128
 
@@ -136,6 +137,8 @@ def load_library():
     lib.lcsb_load.restype = ctypes.c_int
     lib.lcsb_ready.argtypes = [P, ctypes.c_int32]
     lib.lcsb_ready.restype = ctypes.c_int32
+    lib.lcsb_shard_traffic.argtypes = [P] + [ctypes.POINTER(ctypes.c_uint64)] * 3
+    lib.lcsb_shard_traffic.restype = ctypes.c_int
     lib.lcsb_last_error.argtypes = [P]
     lib.lcsb_last_error.restype = ctypes.c_char_p
     lib.lcsb_destroy.argtypes = [P]
@@ -329,6 +332,15 @@ class Lcsb:
     def kernel_in_use(self) -> str:
         return {1: "generic", 2: "bin2", 3: "q4", 4: "small", 5: "bin2q"}.get(
             int(self._lib.lcsb_kernel_in_use(self._h)), "?")
+
+    def shard_traffic(self):
+        """lcsb_shard_traffic: (peer-read, peer-written, requested) bytes per sweep of this
+        handle's shards (sharded quarter table), or None for other layouts."""
+        r, w, a = ctypes.c_uint64(), ctypes.c_uint64(), ctypes.c_uint64()
+        if self._lib.lcsb_shard_traffic(self._h, ctypes.byref(r), ctypes.byref(w),
+                                        ctypes.byref(a)) != 0:
+            return None
+        return int(r.value), int(w.value), int(a.value)
 
     @property
     def launch_count(self) -> int:

@@ -528,3 +528,114 @@ def test_comm_hook_failures_fail_loudly():
     assert ok.bound().bound == ref.bound().bound
     ok.destroy()
     ref.destroy()
+
+
+# ------------------------------------------------------------------ sharded quarter table (§9c)
+
+@pytest.mark.parametrize("ell,K,shards", [(8, 4, 2), (9, 4, 4), (10, 5, 8)])
+def test_quarter_shard_plan_sizes(ell, K, shards):
+    """The sharded quarter table's plan (CPU): every shard gets the stride of the largest shard,
+    and the shards together hold every stored block (balance within 40 % of the mean)."""
+    L.load_library()
+    one = L.lcsb_required_bytes(2, 2, ell, "f32", symmetry=2, block_log4=K, shards=1)
+    sh = L.lcsb_required_bytes(2, 2, ell, "f32", symmetry=2, block_log4=K, shards=shards)
+    map_bytes = 4 << (2 * (ell - K) - 1)
+    tables_one = one - 256 - map_bytes
+    tables_sh = sh - 256 - map_bytes
+    assert tables_sh >= tables_one and tables_sh <= 1.4 * tables_one
+    # too few prefix pairs for the key: rejected
+    assert L.lcsb_required_bytes(2, 2, ell, "f32", symmetry=2, block_log4=ell - 1,
+                                 shards=shards) == 0
+
+
+@pytest.mark.gpu
+@pytest.mark.skipif(not has_cuda(), reason="needs a CUDA device")
+@pytest.mark.parametrize("ell,K,shards,dtype", [(8, 4, 2, "f32"), (9, 4, 4, "f64"),
+                                                (10, 5, 8, "f32"), (12, 6, 2, "f32"),
+                                                (12, 5, 4, "f64"), (13, 7, 8, "f32")])
+def test_quarter_virtual_shards_bitwise_equal_unsharded(ell, K, shards, dtype):
+    """The sharded quarter table (§9c) on P virtual shards of one GPU -- one virtual address
+    range per table over P physical allocations, per-shard item lists, reads of other shards'
+    windows and stores of their outputs -- equals the unsharded quarter table bit for bit: both
+    generations and the one-pass bound after 1, 2, 3 and 12 sweeps; the oracle at l <= 9."""
+    import torch
+    from paper_2407_10925_b200 import Lcsb
+    from oracle import ft_oracle as fo
+    a = Lcsb(2, 2, ell, dtype=dtype, symmetry=2, block_log4=K)
+    b = Lcsb(2, 2, ell, dtype=dtype, symmetry=2, block_log4=K, shards=shards,
+             virtual_shards=True)
+    assert b.kernel_in_use == "bin2q" and b.num_shards == shards
+    a.ready(wait=True)
+    for k in (1, 1, 1, 9):
+        a.sweep(k)
+        b.sweep(k)
+        assert np.array_equal(a.table(0), b.table(0))
+        assert np.array_equal(a.table(1), b.table(1))
+        ba, bb = a.bound(), b.bound()
+        assert (ba.R_max, ba.R_min, ba.E_at_Rmax, ba.E_at_Rmin) == \
+               (bb.R_max, bb.R_min, bb.E_at_Rmax, bb.E_at_Rmin)
+    if ell <= 9:
+        ref = fo.feasible_triplet(2, 2, ell, 12, form="two_array", dtype=dtype)
+        tab = b.table(0)
+        if dtype == "f32":
+            assert np.array_equal(tab, ref["table"])
+        else:
+            np.testing.assert_allclose(tab, ref["table"], rtol=1e-12)
+    a.destroy()
+    b.destroy()
+    torch.cuda.empty_cache()
+
+
+def _pm_quarter_worker(rank, world, port, out_dir, ell, K, dtype):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+    from paper_2407_10925_b200 import Lcsb
+    from paper_2407_10925_b200.dist import create_sharded
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    h = create_sharded(ell, dtype=dtype, transport="host", symmetry=2, block_log4=K)
+    assert h.kernel_in_use == "bin2q"
+    out = {}
+    for n in (1, 2, 15):
+        h.sweep(n)
+        b = h.bound()
+        if rank == 0:
+            out[n] = (h.table(0), h.table(1), b)
+    h.reset()
+    h.sweep(2)
+    if rank == 0:
+        out["reset"] = h.table(0)
+    dist.barrier()
+    h.destroy()
+    if rank == 0:
+        ok = []
+        ref = Lcsb(2, 2, ell, dtype=dtype, symmetry=2, block_log4=K)
+        for n in (1, 2, 15):
+            ref.sweep(n)
+            rb = ref.bound()
+            t0, t1, b = out[n]
+            ok += [np.array_equal(t0, ref.table(0)), np.array_equal(t1, ref.table(1)),
+                   (b.R_max, b.R_min, b.E_at_Rmax, b.E_at_Rmin, b.best_bound) ==
+                   (rb.R_max, rb.R_min, rb.E_at_Rmax, rb.E_at_Rmin, rb.best_bound)]
+        ref.reset()
+        ref.sweep(2)
+        ok.append(np.array_equal(out["reset"], ref.table(0)))
+        ref.destroy()
+        np.save(os.path.join(out_dir, "pmq.npy"), np.array(ok))
+    dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+@pytest.mark.skipif(not has_cuda(), reason="needs a CUDA device")
+@pytest.mark.parametrize("world,ell,K,dtype", [(2, 10, 5, "f32"), (4, 12, 6, "f64")])
+def test_quarter_process_mode_multi_rank_on_one_gpu(tmp_path, world, ell, K, dtype):
+    """The sharded quarter table over 2 and 4 PROCESSES on cuda:0: each process maps the peers'
+    shard allocations into its table's address range (POSIX fds over Unix sockets), reads the
+    peers' windows and stores into their memory; tables and bounds equal the unsharded run."""
+    import torch.multiprocessing as mp
+    mp.spawn(_pm_quarter_worker, args=(world, _free_port(), str(tmp_path), ell, K, dtype),
+             nprocs=world, join=True)
+    assert np.load(tmp_path / "pmq.npy").all()
