@@ -647,6 +647,13 @@ static int exchange_ipc(lcsb_t* h) {
 
 static int install_schedule(lcsb_t* h, bool wait);
 
+// passes of the shard-assignment refinement of the sharded quarter table (§9c); LCSB_QSHARD_PASSES
+// (A/B): 0 = the xor key alone
+static int shard_refine_passes() {
+  static const int n = getenv("LCSB_QSHARD_PASSES") ? atoi(getenv("LCSB_QSHARD_PASSES")) : 24;
+  return n;
+}
+
 // LCSB_DEBUG: a SIGSEGV handler that prints the native backtrace (diagnosis only)
 #include <execinfo.h>
 #include <signal.h>
@@ -892,7 +899,8 @@ extern "C" int lcsb_create_ex(const lcsb_config* cfg, lcsb_t** out) {
     uint32_t* hm = (uint32_t*)malloc(h->qmap_bytes);
     h->qmap = (uint32_t*)dev_alloc(h, h->qmap_bytes);
     const bool ok = hm && h->qmap &&
-                    (h->vmm ? build_quarter_map_sharded(cfg->ell, h->qK, h->p, hm, &h->qmaxslots)
+                    (h->vmm ? build_quarter_map_sharded(cfg->ell, h->qK, h->qM, h->p,
+                                                        shard_refine_passes(), hm, &h->qmaxslots)
                             : build_quarter_map(cfg->ell, h->qK, hm));
     e = ok ? cudaMemcpyAsync(h->qmap, hm, h->qmap_bytes, cudaMemcpyHostToDevice, s) : cudaSuccess;
     if (e == cudaSuccess && ok) e = cudaStreamSynchronize(s);

@@ -202,7 +202,9 @@ bool build_quarter_map(int ell, int K, uint32_t* map);
 bool quarter_schedule(int ell, int K, int M, const uint32_t* map, std::vector<uint32_t>& out);
 bool quarter_schedule_cached(int ell, int K, int M, std::vector<uint32_t>& out);  // no build
 // sharded quarter table: shard-major slots with a stride of the largest shard
-bool build_quarter_map_sharded(int ell, int K, int p, uint32_t* map, uint64_t* maxslots);
+// passes > 0: local-search refinement of the assignment (fewer NVLink bytes), deterministic
+bool build_quarter_map_sharded(int ell, int K, int M, int p, int passes, uint32_t* map,
+                               uint64_t* stride_slots);
 uint64_t quarter_shard_maxslots(int ell, int K, int p);
 void quarter_shard_items(int ell, int K, int M, const uint32_t* map, uint64_t maxslots, int shard,
                          const std::vector<uint32_t>& sched, std::vector<uint32_t>& out);

@@ -66,32 +66,159 @@ static uint32_t qblock_key(uint64_t beta, int PL, int p) {
   return k;
 }
 
-bool build_quarter_map_sharded(int ell, int K, int p, uint32_t* map, uint64_t* maxslots) {
+// Shard sizes: every shard gets the same stride of slots -- the largest shard of the xor key, or
+// 2 % above the mean if that is larger (the room the refinement below may use).
+static uint64_t shard_stride(const std::vector<uint64_t>& cnt, uint64_t total) {
+  uint64_t mx = 0;
+  for (uint64_t c : cnt) mx = c > mx ? c : mx;
+  const uint64_t room = total / cnt.size() + total / cnt.size() / 50 + 1;
+  return mx > room ? mx : room;
+}
+
+// Refinement of the block -> shard assignment (round 2): the key places each block by its own
+// prefix, but an item's two windows and its output runs sit in blocks whose prefixes are
+// shifted against each other, so most of them land on other shards.  Any assignment is correct
+// (a slot is a global address), so a local search moves each block to the shard that minimises
+// the NVLink entries of the items touching it -- the psi window read when not on the item's
+// owner (the shard of its first window) and every output run stored elsewhere -- within the
+// stride.  The de Bruijn dependency graph has small-cut partitions: at l = 14-16 this halves
+// the cross-shard bytes at 8 shards and cuts them to a third at 2.  Sequential
+// and deterministic: every rank derives the same assignment.
+static void refine_shards(int ell, int K, int M, const uint32_t* map, uint32_t P, uint64_t stride,
+                          int passes, std::vector<uint32_t>& shard_of_slot) {
+  const int L = 2 * ell;
+  const uint64_t lmask = (1ull << L) - 1, q1 = 1ull << (L - 2);
+  const uint64_t amask = 0xAAAAAAAAAAAAAAAAull & lmask, bmask = 0x5555555555555555ull & lmask;
+  const uint64_t T = 1ull << (2 * M);
+  const int sh = 2 * K;
+  const uint64_t ns = shard_of_slot.size();
+  auto win = [&](uint64_t x) { return (x & amask) | ((x & bmask & ~q1) << 2); };
+  // items: [w1, w2, nr, (run slot, run length)...] flattened
+  std::vector<uint32_t> it;
+  std::vector<uint64_t> ioff;
+  const uint64_t ntiles = 1ull << (2 * (ell - 1 - M));
+  for (uint64_t tau = 0; tau < ntiles; ++tau) {
+    const uint64_t x0 = q1 + tau * T, p0 = pairswap_hd(~x0 & lmask) & ~(T - 1);
+    const uint64_t taup = (p0 - q1) >> (2 * M);
+    if (taup < tau) continue;
+    const bool self = taup == tau;
+    const uint64_t wb = win(x0), wp = win(p0), yf = wb >> 2, ypf = wp >> 2;
+    ioff.push_back(it.size());
+    it.push_back(map[wb >> sh] >> 2);
+    it.push_back(map[wp >> sh] >> 2);
+    const size_t nrpos = it.size();
+    it.push_back(0);
+    const uint64_t runs[6] = {x0, p0, yf, q1 - yf - T / 2, ypf, q1 - ypf - T / 2};
+    for (int r = 0; r < 6; ++r) {
+      if (self && (r == 1 || r >= 4)) continue;
+      if ((map[runs[r] >> sh] & 3u) != 0) continue;
+      it.push_back(map[runs[r] >> sh] >> 2);
+      it.push_back(r < 2 ? (uint32_t)T : (uint32_t)(T / 2));
+      ++it[nrpos];
+    }
+  }
+  const uint64_t E = ioff.size();
+  ioff.push_back(it.size());
+  // slot -> items (CSR, each item once per slot)
+  std::vector<uint64_t> aoff(ns + 1, 0);
+  std::vector<uint32_t> last(ns, ~0u);
+  auto each_slot = [&](uint64_t e, auto&& fn) {
+    const uint32_t* r = it.data() + ioff[e];
+    fn(r[0]);
+    fn(r[1]);
+    for (uint32_t k = 0; k < r[2]; ++k) fn(r[3 + 2 * k]);
+  };
+  for (uint64_t e = 0; e < E; ++e)
+    each_slot(e, [&](uint32_t s) {
+      if (last[s] != (uint32_t)e) {
+        last[s] = (uint32_t)e;
+        ++aoff[s + 1];
+      }
+    });
+  for (uint64_t s = 0; s < ns; ++s) aoff[s + 1] += aoff[s];
+  std::vector<uint32_t> adj(aoff[ns]);
+  std::vector<uint64_t> fillp(aoff.begin(), aoff.end() - 1);
+  std::fill(last.begin(), last.end(), ~0u);
+  for (uint64_t e = 0; e < E; ++e)
+    each_slot(e, [&](uint32_t s) {
+      if (last[s] != (uint32_t)e) {
+        last[s] = (uint32_t)e;
+        adj[fillp[s]++] = (uint32_t)e;
+      }
+    });
+  auto cost = [&](uint64_t e) -> uint64_t {
+    const uint32_t* r = it.data() + ioff[e];
+    const uint32_t o = shard_of_slot[r[0]];
+    uint64_t c = shard_of_slot[r[1]] != o ? 2 * T : 0;
+    for (uint32_t k = 0; k < r[2]; ++k) c += shard_of_slot[r[3 + 2 * k]] != o ? r[4 + 2 * k] : 0;
+    return c;
+  };
+  std::vector<uint64_t> size(P, 0);
+  for (uint32_t k : shard_of_slot) ++size[k];
+  for (int pass = 0; pass < passes; ++pass) {
+    uint64_t moves = 0;
+    for (uint64_t b = 0; b < ns; ++b) {
+      const uint32_t from = shard_of_slot[b];
+      uint64_t before = 0;
+      for (uint64_t a = aoff[b]; a < aoff[b + 1]; ++a) before += cost(adj[a]);
+      uint32_t best = from;
+      uint64_t best_c = before;
+      for (uint32_t to = 0; to < P; ++to) {
+        if (to == from || size[to] >= stride) continue;
+        shard_of_slot[b] = to;
+        uint64_t after = 0;
+        for (uint64_t a = aoff[b]; a < aoff[b + 1] && after < best_c; ++a) after += cost(adj[a]);
+        if (after < best_c) {
+          best_c = after;
+          best = to;
+        }
+      }
+      shard_of_slot[b] = best;
+      if (best != from) {
+        --size[from];
+        ++size[best];
+        ++moves;
+      }
+    }
+    if (!moves) break;
+  }
+}
+
+bool build_quarter_map_sharded(int ell, int K, int M, int p, int passes, uint32_t* map,
+                               uint64_t* stride_slots) {
   if (!build_quarter_map(ell, K, map)) return false;
   const int PL = 2 * (ell - K);
   if (p < 0 || ell - K - 1 < p) return false;
   const uint64_t nb = quarter_map_entries(ell, K), ns = quarter_slots(ell, K);
   const uint32_t P = 1u << p;
-  std::vector<uint32_t> newslot(ns);
+  std::vector<uint32_t> shard(ns);
   std::vector<uint64_t> cnt(P, 0);
-  for (uint64_t b = 0; b < nb; ++b)  // canonical blocks in slot order
-    if ((map[b] & 3u) == 0) newslot[map[b] >> 2] = (uint32_t)(cnt[qblock_key(b, PL, p)]++);
-  uint64_t mx = 0;
-  for (uint32_t k = 0; k < P; ++k) mx = cnt[k] > mx ? cnt[k] : mx;
-  if (mx * P >= (1ull << 30)) return false;  // map entries hold slot << 2 in 32 bits
-  for (uint64_t b = 0; b < nb; ++b)
-    if ((map[b] & 3u) == 0)
-      newslot[map[b] >> 2] += (uint32_t)(qblock_key(b, PL, p) * mx);
-  for (uint64_t b = 0; b < nb; ++b)
-    map[b] = (newslot[map[b] >> 2] << 2) | (map[b] & 3u);
-  *maxslots = mx;
+  for (uint64_t b = 0; b < nb; ++b)  // canonical blocks: the xor key of their prefix
+    if ((map[b] & 3u) == 0) {
+      shard[map[b] >> 2] = qblock_key(b, PL, p);
+      ++cnt[shard[map[b] >> 2]];
+    }
+  const uint64_t stride = shard_stride(cnt, ns);
+  if (stride * P >= (1ull << 30)) return false;  // map entries hold slot << 2 in 32 bits
+  if (P > 1 && passes > 0) refine_shards(ell, K, M, map, P, stride, passes, shard);
+  std::vector<uint32_t> newslot(ns);
+  std::fill(cnt.begin(), cnt.end(), 0);
+  for (uint64_t s = 0; s < ns; ++s) newslot[s] = (uint32_t)(shard[s] * stride + cnt[shard[s]]++);
+  for (uint64_t b = 0; b < nb; ++b) map[b] = (newslot[map[b] >> 2] << 2) | (map[b] & 3u);
+  *stride_slots = stride;
   return true;
 }
 
 uint64_t quarter_shard_maxslots(int ell, int K, int p) {
+  // the stride depends on the key's counts only (the refinement stays within it)
   std::vector<uint32_t> map(quarter_map_entries(ell, K));
-  uint64_t mx = 0;
-  return build_quarter_map_sharded(ell, K, p, map.data(), &mx) ? mx : 0;
+  if (!build_quarter_map(ell, K, map.data()) || p < 0 || ell - K - 1 < p) return 0;
+  const int PL = 2 * (ell - K);
+  std::vector<uint64_t> cnt(1u << p, 0);
+  for (uint64_t b = 0; b < map.size(); ++b)
+    if ((map[b] & 3u) == 0) ++cnt[qblock_key(b, PL, p)];
+  const uint64_t stride = shard_stride(cnt, quarter_slots(ell, K));
+  return stride * (1u << p) >= (1ull << 30) ? 0 : stride;
 }
 
 // The items (tile pairs) of one shard -- those whose first window (tile t's adv_b window) lies in
