@@ -81,9 +81,9 @@ static uint64_t shard_stride(const std::vector<uint64_t>& cnt, uint64_t total) {
 // (a slot is a global address), so a local search moves each block to the shard that minimises
 // the NVLink entries of the items touching it -- the psi window read when not on the item's
 // owner (the shard of its first window) and every output run stored elsewhere -- within the
-// stride.  The de Bruijn dependency graph has small-cut partitions: at l = 14-16 this halves
-// the cross-shard bytes at 8 shards and cuts them to a third at 2.  Sequential
-// and deterministic: every rank derives the same assignment.
+// stride.  The de Bruijn dependency graph has small-cut partitions: at l = 18 this cuts the
+// cross-shard bytes 2.7x at 8 shards and to a third at 2.  Sequential and
+// deterministic: every rank derives the same assignment.
 static void refine_shards(int ell, int K, int M, const uint32_t* map, uint32_t P, uint64_t stride,
                           int passes, std::vector<uint32_t>& shard_of_slot) {
   const int L = 2 * ell;
@@ -200,7 +200,20 @@ bool build_quarter_map_sharded(int ell, int K, int M, int p, int passes, uint32_
     }
   const uint64_t stride = shard_stride(cnt, ns);
   if (stride * P >= (1ull << 30)) return false;  // map entries hold slot << 2 in 32 bits
-  if (P > 1 && passes > 0) refine_shards(ell, K, M, map, P, stride, passes, shard);
+  if (P > 1 && passes > 0) {
+    // hierarchical: refine 2 shards (the key's first bit), split each by the next bit and refine
+    // again, ... -- at 8 shards 20 % fewer NVLink bytes (27 % on the busiest GPU) than refining
+    // the 3-bit key at once
+    const std::vector<uint32_t> key(shard);
+    for (int q = 1; q <= p; ++q) {
+      const uint32_t Pq = 1u << q;
+      for (uint64_t s = 0; s < ns; ++s)
+        shard[s] = (q == 1 ? 0u : 2 * shard[s]) + ((key[s] >> (p - q)) & 1u);
+      std::vector<uint64_t> cq(Pq, 0);
+      for (uint64_t s = 0; s < ns; ++s) ++cq[shard[s]];
+      refine_shards(ell, K, M, map, Pq, q == p ? stride : shard_stride(cq, ns), passes, shard);
+    }
+  }
   std::vector<uint32_t> newslot(ns);
   std::fill(cnt.begin(), cnt.end(), 0);
   for (uint64_t s = 0; s < ns; ++s) newslot[s] = (uint32_t)(shard[s] * stride + cnt[shard[s]]++);
