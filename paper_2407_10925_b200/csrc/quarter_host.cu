@@ -184,8 +184,38 @@ static void refine_shards(int ell, int K, int M, const uint32_t* map, uint32_t P
   }
 }
 
+static bool build_quarter_map_sharded_nocache(int ell, int K, int M, int p, int passes,
+                                              uint32_t* map, uint64_t* stride_slots);
+
 bool build_quarter_map_sharded(int ell, int K, int M, int p, int passes, uint32_t* map,
                                uint64_t* stride_slots) {
+  // the last map of this process is kept: repeated creates of one config skip the search
+  static std::mutex cmu;
+  static int ck[5] = {0, 0, 0, -1, -1};
+  static std::vector<uint32_t> cmap;
+  static uint64_t cstride = 0;
+  const uint64_t nb0 = quarter_map_entries(ell, K);
+  {
+    std::lock_guard<std::mutex> lock(cmu);
+    if (ck[0] == ell && ck[1] == K && ck[2] == M && ck[3] == p && ck[4] == passes &&
+        cmap.size() == nb0) {
+      std::copy(cmap.begin(), cmap.end(), map);
+      *stride_slots = cstride;
+      return true;
+    }
+  }
+  bool ok = build_quarter_map_sharded_nocache(ell, K, M, p, passes, map, stride_slots);
+  if (ok) {
+    std::lock_guard<std::mutex> lock(cmu);
+    cmap.assign(map, map + nb0);
+    cstride = *stride_slots;
+    ck[0] = ell, ck[1] = K, ck[2] = M, ck[3] = p, ck[4] = passes;
+  }
+  return ok;
+}
+
+static bool build_quarter_map_sharded_nocache(int ell, int K, int M, int p, int passes,
+                                              uint32_t* map, uint64_t* stride_slots) {
   if (!build_quarter_map(ell, K, map)) return false;
   const int PL = 2 * (ell - K);
   if (p < 0 || ell - K - 1 < p) return false;
