@@ -6,8 +6,10 @@ There is no fallback: if liblcsb.so is missing or no CUDA device is present, eve
 """
 from __future__ import annotations
 
+import atexit
 import ctypes
 import os
+import weakref
 from dataclasses import dataclass
 
 import numpy as np
@@ -179,7 +181,10 @@ class _TorchAllocator:
             return None
 
     def _free(self, ptr, nbytes, stream, ctx):
-        self.torch.cuda.caching_allocator_delete(int(ptr))
+        try:
+            self.torch.cuda.caching_allocator_delete(int(ptr))
+        except Exception:  # noqa: BLE001 -- interpreter shutdown: torch is gone, so is the memory
+            pass
 
 
 def make_config(sigma, d, ell, dtype="f32", form="auto", rmode="max", symmetry=-1,
@@ -223,6 +228,24 @@ class BoundResult:
     best_sweep: int
 
 
+_LIVE: "weakref.WeakSet[Lcsb]" = weakref.WeakSet()
+
+
+@atexit.register
+def _destroy_live_handles():
+    """Handles still alive at exit are released before torch is torn down (their device
+    memory came from torch's allocator).  Process-mode handles are only dropped: destroying
+    them is collective, and the peers may be gone."""
+    for h in list(_LIVE):
+        try:
+            if h._process_mode:
+                h._h = ctypes.c_void_p()
+            else:
+                h.destroy()
+        except Exception:  # noqa: BLE001
+            pass
+
+
 class Lcsb:
     """One handle: the device tables of one (sigma, d, l) run."""
 
@@ -258,6 +281,8 @@ class Lcsb:
         _check(lib.lcsb_create_ex(ctypes.byref(cfg), ctypes.byref(h)))
         self._h = h
         self.sigma, self.d, self.ell = sigma, d, ell
+        self._process_mode = int(shards) > 1 and not virtual_shards
+        _LIVE.add(self)
 
     # --- the C-ABI calls -------------------------------------------------------------------
     def reset(self):
