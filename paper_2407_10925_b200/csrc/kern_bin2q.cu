@@ -9,7 +9,10 @@ template <bool WMODE>
 cudaError_t dispatch_q(const Bin2QArgs& a, int dtype, int M, cudaStream_t s, int sms) {
   if (dtype == LCSB_F32) {
     switch (M) {
-      case 6: return launch_q<float, 6, 1, WMODE, 3>(a, s, sms);  // A/B: variant 10
+      case 6:  // A/B: variant 10; with a work counter the producer pipelined three deep
+        if (!WMODE && q_dynamic(a, 6))
+          return launch_q<float, 6, 1, WMODE, 3, kThreads, 1, false, false, 3>(a, s, sms);
+        return launch_q<float, 6, 1, WMODE, 3>(a, s, sms);
       case 5: return launch_q<float, 5, 2, WMODE>(a, s, sms);
       case 4: return launch_q<float, 4, 2, WMODE>(a, s, sms);
       case 3: return launch_q<float, 3, 2, WMODE>(a, s, sms);
@@ -18,7 +21,10 @@ cudaError_t dispatch_q(const Bin2QArgs& a, int dtype, int M, cudaStream_t s, int
     }
   } else {
     switch (M) {
-      case 5: return launch_q<double, 5, 2, WMODE, 2>(a, s, sms);  // A/B: variant 9
+      case 5:  // A/B: variant 9
+        if (!WMODE && q_dynamic(a, 5))
+          return launch_q<double, 5, 2, WMODE, 2, kThreads, 1, false, false, 3>(a, s, sms);
+        return launch_q<double, 5, 2, WMODE, 2>(a, s, sms);
       case 4: return launch_q<double, 4, 2, WMODE>(a, s, sms);
       case 3: return launch_q<double, 3, 2, WMODE>(a, s, sms);
       case 2: return launch_q<double, 2, 2, WMODE>(a, s, sms);

@@ -573,7 +573,7 @@ __device__ __forceinline__ void qissue(const QGeo& g, const QItem& it, uint64_t 
 }
 
 template <typename T, int M, int S, bool WMODE, int MINB = 1, int NT = kThreads, int UNR = 1,
-          bool OFS = false, bool RES = false>
+          bool OFS = false, bool RES = false, int DEPTH = 1>
 __global__ void __launch_bounds__(NT, MINB) bin2q_kernel(Bin2QArgs a) {
   using C = QCfg<T, M, S, WMODE, MINB, RES>;
   constexpr uint32_t TT = C::TT, WIN = C::WIN;
@@ -615,13 +615,26 @@ __global__ void __launch_bounds__(NT, MINB) bin2q_kernel(Bin2QArgs a) {
     return first(prev == ~0ull ? (uint64_t)blockIdx.x : prev + G);
   };
   auto entry = [&](uint64_t c) -> uint32_t { return sched ? __ldg(sched + c) : (uint32_t)c; };
-  auto tile_of = [&](uint64_t c) -> uint64_t {
-    return sched ? (uint64_t)(__ldg(sched + c) & kQTileMask) : c;
-  };
   // hint bits only come with a schedule; without one every piece keeps the default policy
   const uint64_t keep = (a.l2keep != 0) ? kL2EvictLast : kL2EvictNormal;
-  uint64_t pc = 0;  // producer cursor (thread 0 only)
-  QItem pit;        // its map entries, fetched one item ahead
+  // producer (thread 0); at depth 3 software-pipelined over three items so none of its dependent
+  // memory latencies (claim -> schedule entry -> map entries) stalls the CTA: at each fill it
+  // issues item pc (map entries in pit), starts pit's loads for p1 (entry e1 loaded a fill
+  // earlier), loads the entry of p2 (claimed a fill earlier) and claims the next item
+  uint64_t pc = 0, p1 = 0, p2 = 0;
+  uint32_t e0 = 0, e1 = 0;
+  // DEPTH 3 (sweeps with dynamic claiming) or 1: the claim, the entry and the map lookups of the
+  // next item back to back.  Depth 3 pays only where the claim is an atomic (A/B at l = 17: fp32
+  // sweep 5.12 -> 5.07-5.10 ms, fp64 12.99 -> 12.56); with static claims (the residual sweep
+  // 19.9 -> 21.2) and in the bound pass, which runs at its 80-register cap (10.86 -> 11.95: the
+  // extra producer state spills), it costs
+  constexpr int depth = DEPTH;
+  static_assert(DEPTH == 1 || DEPTH == 3, "producer depth 1 or 3");
+  QItem pit;
+  auto ent_of = [&](uint64_t c) -> uint32_t { return c < nitems ? entry(c) : 0u; };
+  auto tile_e = [&](uint32_t e) -> uint64_t {
+    return sched ? (uint64_t)(e & kQTileMask) : (uint64_t)e;
+  };
   if (tid == 0) {
     for (int s = 0; s < S; ++s) mbar_init(&bars[s], 1);
     fence_mbar_init();
@@ -634,12 +647,19 @@ __global__ void __launch_bounds__(NT, MINB) bin2q_kernel(Bin2QArgs a) {
     uint64_t* meta = metas + 8 * s;
     if (pc < nitems) {
       meta[7] = 0;
-      const uint32_t ent = entry(pc);
-      qissue<T, M, WMODE, RES>(g, pit, sched ? (uint64_t)(ent & kQTileMask) : (uint64_t)ent,
-                               sbuf, &bars[s], meta, src, sched ? (ent >> kQHintShift) : 0xFu,
-                               keep, prev, base);
-      pc = claim(pc);
-      if (pc < nitems) qlookup<M>(g, map, tile_of(pc), pit);
+      qissue<T, M, WMODE, RES>(g, pit, tile_e(e0), sbuf, &bars[s], meta, src,
+                               sched ? (e0 >> kQHintShift) : 0xFu, keep, prev, base);
+      if constexpr (depth == 1) {  // claim, entry and map lookups back to back
+        pc = claim(pc);
+        e0 = ent_of(pc);
+      } else {  // claim two fills ahead, the entry one
+        pc = p1;
+        e0 = e1;
+        p1 = p2;
+        e1 = ent_of(p1);
+        p2 = claim(p2);
+      }
+      if (pc < nitems) qlookup<M>(g, map, tile_e(e0), pit);
     } else {
       meta[7] = 1;
       mbar_arrive(&bars[s]);
@@ -647,7 +667,13 @@ __global__ void __launch_bounds__(NT, MINB) bin2q_kernel(Bin2QArgs a) {
   };
   if (tid == 0) {
     pc = claim(~0ull);
-    if (pc < nitems) qlookup<M>(g, map, tile_of(pc), pit);
+    if constexpr (depth == 3) {
+      p1 = claim(pc);
+      p2 = claim(p1);
+      e1 = ent_of(p1);
+    }
+    e0 = ent_of(pc);
+    if (pc < nitems) qlookup<M>(g, map, tile_e(e0), pit);
     for (int s = 0; s < S; ++s) fill(s, in + (size_t)s * C::STAGE);
   }
 
@@ -696,18 +722,23 @@ __global__ void __launch_bounds__(NT, MINB) bin2q_kernel(Bin2QArgs a) {
   if (OFS && !WMODE) block_min_to(ba.rmin, a.omin);
 }
 
+// the launch claims items dynamically (a schedule for these tiles and a work counter)
+inline bool q_dynamic(const Bin2QArgs& a, int M) {
+  return a.counter && a.sched && a.sched_m == M;
+}
+
 template <typename T, int M, int S, bool WMODE, int MINB = 1, int NT = kThreads, int UNR = 1,
-          bool OFS = false, bool RES = false>
+          bool OFS = false, bool RES = false, int DEPTH = 1>
 cudaError_t launch_q(const Bin2QArgs& a, cudaStream_t s, int sms) {
   using C = QCfg<T, M, S, WMODE, MINB, RES>;
   static uint64_t cap = 0;
   if (cap == 0) {
-    cudaError_t e = cudaFuncSetAttribute(bin2q_kernel<T, M, S, WMODE, MINB, NT, UNR, OFS, RES>,
+    cudaError_t e = cudaFuncSetAttribute(bin2q_kernel<T, M, S, WMODE, MINB, NT, UNR, OFS, RES, DEPTH>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
     if (e != cudaSuccess) return e;
     int per_sm = 0;
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm,
-                                                      bin2q_kernel<T, M, S, WMODE, MINB, NT, UNR, OFS, RES>,
+                                                      bin2q_kernel<T, M, S, WMODE, MINB, NT, UNR, OFS, RES, DEPTH>,
                                                       NT, C::SMEM) != cudaSuccess ||
         per_sm < 1) {
       cudaGetLastError();
@@ -720,7 +751,7 @@ cudaError_t launch_q(const Bin2QArgs& a, cudaStream_t s, int sms) {
       (a.sched && a.sched_m == M) ? a.nitems : (1ull << (2 * (a.ell - 1 - M)));
   uint64_t blocks = cap < ntiles ? cap : ntiles;
   if (blocks < 1) blocks = 1;
-  bin2q_kernel<T, M, S, WMODE, MINB, NT, UNR, OFS, RES><<<(unsigned)blocks, NT, C::SMEM, s>>>(a);
+  bin2q_kernel<T, M, S, WMODE, MINB, NT, UNR, OFS, RES, DEPTH><<<(unsigned)blocks, NT, C::SMEM, s>>>(a);
   return cudaGetLastError();
 }
 

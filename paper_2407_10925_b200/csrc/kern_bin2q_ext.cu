@@ -22,7 +22,9 @@ cudaError_t launch_bin2q_sweep_ext(const Bin2QArgs& a, int dtype, int M, cudaStr
     constexpr int NT = kThreads;
     if (dtype == LCSB_F32) {
       switch (M) {
-        case 6: return launch_q<float, 6, 1, false, 3, NT, 1, true>(a, s, sms);
+        case 6:
+          if (q_dynamic(a, 6)) return launch_q<float, 6, 1, false, 3, NT, 1, true, false, 3>(a, s, sms);
+          return launch_q<float, 6, 1, false, 3, NT, 1, true>(a, s, sms);
         case 5: return launch_q<float, 5, 2, false, 1, NT, 1, true>(a, s, sms);
         case 4: return launch_q<float, 4, 2, false, 1, NT, 1, true>(a, s, sms);
         case 3: return launch_q<float, 3, 2, false, 1, NT, 1, true>(a, s, sms);
@@ -31,7 +33,9 @@ cudaError_t launch_bin2q_sweep_ext(const Bin2QArgs& a, int dtype, int M, cudaStr
       }
     } else {
       switch (M) {
-        case 5: return launch_q<double, 5, 2, false, 2, NT, 1, true>(a, s, sms);
+        case 5:
+          if (q_dynamic(a, 5)) return launch_q<double, 5, 2, false, 2, NT, 1, true, false, 3>(a, s, sms);
+          return launch_q<double, 5, 2, false, 2, NT, 1, true>(a, s, sms);
         case 4: return launch_q<double, 4, 2, false, 1, NT, 1, true>(a, s, sms);
         case 3: return launch_q<double, 3, 2, false, 1, NT, 1, true>(a, s, sms);
         case 2: return launch_q<double, 2, 2, false, 1, NT, 1, true>(a, s, sms);

@@ -1102,10 +1102,11 @@ static int install_schedule(lcsb_t* h, bool wait) {
     if (!d) return set_err(h, LCSB_ECAPACITY, "schedule allocation failed");
     // pageable source: the call returns once the bytes are staged, so `sched` may be freed
     CU(h, cudaMemcpyAsync(d, sched.data(), bytes, cudaMemcpyHostToDevice, s));
-    // dynamic claiming pays for the 4^6 tiles of fp32 (20.7 vs 26.6 GB read at l = 17); with
-    // the 4x more, smaller items of fp64 (4^5 tiles) the single counter costs more than it
-    // saves (l = 16: 3.99 vs 3.28 ms static)
-    if (h->qM >= 6 && !getenv("LCSB_QSTATIC")) {
+    // dynamic claiming (one work counter): 20.7 vs 26.6 GB read at l = 17 fp32.  For the 4x
+    // more, smaller items of fp64 (4^5 tiles) it paid only once the producer was pipelined
+    // (kern_bin2q.cuh DEPTH 3; l = 17 fp64: 12.56 vs 13.05 ms static, before 3.99 vs 3.28 at
+    // l = 16).  LCSB_QSTATIC (A/B): static round-robin claims
+    if (!getenv("LCSB_QSTATIC")) {
       h->qcounter = (unsigned long long*)dev_alloc(h, 256);
       if (!h->qcounter) return set_err(h, LCSB_ECAPACITY, "counter allocation failed");
     }
