@@ -20,7 +20,9 @@ static __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {  // arrive w
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 // Plain try_wait probe loop.  LCSB_MBAR_HINT (compile-time, A/B only) adds a suspend-time hint;
-// measured on B200: no change for the fp32 sweeps and W passes, 2 % slower for the fp64 sweep.
+// measured on B200: no change for the fp32 sweeps and W passes, 2 % slower for the fp64 sweep;
+// in the power-capped bench loop (round 2: the probe loop is ~17 % of the sweep's issued
+// instructions) neither it nor a __nanosleep backoff of 64 / 256 ns changed the step (2.955-2.967e12).
 static __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   uint32_t done = 0;
   do {
