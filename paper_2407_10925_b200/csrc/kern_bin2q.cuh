@@ -74,6 +74,13 @@ __device__ __forceinline__ double q0_val(double v0, double v1, double v2, double
 
 constexpr int kThreads = 256;
 constexpr uint64_t kNone = ~0ull;
+// fp32 bound pass: the register-lean quad order (pair_quads_w32); LCSB_BOUND_WIDE (compile-time,
+// A/B only) restores the generic order
+#ifndef LCSB_BOUND_WIDE
+constexpr bool WLEAN = true;
+#else
+constexpr bool WLEAN = false;
+#endif
 
 // output stores: nothing in a sweep re-reads them, so they are streaming stores (st.global.cs,
 // evict-first) that leave L2 to the input windows (A/B at l = 17 fp32: 5.161 -> 5.132 ms;
@@ -95,8 +102,9 @@ struct QCfg {
   // pass reads u and v_prev at the outputs straight from global memory (streaming loads, issued
   // before the window reads)
   static constexpr uint32_t STAGE = 2 * WIN * (RES ? 2 : 1);
-  static constexpr size_t SMEM =
-      (size_t)S * STAGE * sizeof(T) + (size_t)S * sizeof(uint64_t) + (size_t)S * 8 * sizeof(uint64_t);
+  // + the bound pass's next-item map entries (QItem, 32 bytes, fetched by cp.async)
+  static constexpr size_t SMEM = (size_t)S * STAGE * sizeof(T) + (size_t)S * sizeof(uint64_t) +
+                                 (size_t)S * 8 * sizeof(uint64_t) + (WMODE ? 32 : 0);
 };
 
 struct QGeo {
@@ -324,6 +332,85 @@ __device__ __forceinline__ void pair_quads_f32(const T* bw, const T* bp, const T
   }
 }
 
+// fp32 storage, bound pass: the arithmetic of pair_quads<float, ..., WMODE> (every value and
+// every accumulated u, v_prev, F(u,u) identical; max / min are order-free) in an order that keeps
+// fewer values live -- the x window's pair sums and Q0 rows are finished before the psi window's
+// groups are loaded (the kernel runs at its 80-register cap; the fp64 group arrays of both
+// windows held at once spilled to local memory)
+template <uint32_t TT, int MW, int MP>
+__device__ __forceinline__ void pair_quads_w32(const float* bw, const float* bp, const float* src,
+                                               const uint64_t* meta, bool self, const float* prev,
+                                               BAcc& ba) {
+  constexpr uint32_t SX = (MW == 0 || MW == 3) ? 2 : 0, SP = (MP == 0 || MP == 3) ? 2 : 1;
+  const uint64_t oQ1 = meta[1], oQ1p = meta[2];
+  const uint64_t of = meta[3], om = meta[4], opf = meta[5], opm = meta[6];
+  const bool rows_x = of != kNone || om != kNone;
+  const bool rows_p = !self && (opf != kNone || opm != kNone);
+  for (uint32_t qd = threadIdx.x; qd < TT / 4; qd += kThreads) {
+    const uint32_t o0 = 4 * qd;
+    const uint32_t g = 2 * pairswap32(o0), u = 2 * (TT - 4 - o0);
+    const uint32_t qb = pairswap32(~o0 & (TT - 1) & ~3u);
+    // u and v_prev at the quad's stored Q1 outputs first (latency overlaps the rest)
+    float uu[4] = {0, 0, 0, 0}, pp[4] = {0, 0, 0, 0};
+    const uint64_t q = oQ1 != kNone ? oQ1 + o0 : (oQ1p != kNone ? oQ1p + qb : kNone);
+    if (q != kNone) {
+      ld4s(src + q, uu);
+      ld4s(prev + q, pp);
+    }
+    const bool sx = (qd >> SX) & 1u, sp = (qd >> SP) & 1u;
+    constexpr uint32_t c0 = comp<MW>(0), c1 = comp<MW>(1), c2 = comp<MW>(2), c3 = comp<MW>(3);
+    constexpr uint32_t d0 = comp<MP>(0), d1 = comp<MP>(1), d2 = comp<MP>(2), d3 = comp<MP>(3);
+    double tx[4];
+    {
+      float X1[4], X2[4], a[4], b[4];
+      ld4r(bw + gbase<TT, MW>(sx ? g + 4 : g), X1);
+      ld4r(bw + gbase<TT, MW>(sx ? g : g + 4), X2);
+      sel4f(sx, X1, X2, a, b);
+      tx[0] = (double)a[c0] + (double)a[c1];
+      tx[1] = (double)b[c0] + (double)b[c1];
+      tx[2] = (double)a[c2] + (double)a[c3];
+      tx[3] = (double)b[c2] + (double)b[c3];
+      if (rows_x) {
+        double G[4];
+        widen4(a, G);
+        q0_group<float, MW, true>(G, g >> 2, TT / 2, src, nullptr, of, om, prev, ba);
+        widen4(b, G);
+        q0_group<float, MW, true>(G, (g >> 2) + 1, TT / 2, src, nullptr, of, om, prev, ba);
+      }
+    }
+    double tq[4];
+    {
+      float P1[4], P2[4], ap[4], bq[4];
+      ld4r(bp + gbase<TT, MP>(sp ? u + 4 : u), P1);
+      ld4r(bp + gbase<TT, MP>(sp ? u : u + 4), P2);
+      sel4f(sp, P1, P2, ap, bq);
+      tq[0] = (double)bq[d2] + (double)bq[d3];
+      tq[1] = (double)bq[d0] + (double)bq[d1];
+      tq[2] = (double)ap[d2] + (double)ap[d3];
+      tq[3] = (double)ap[d0] + (double)ap[d1];
+      if (rows_p) {
+        double G[4];
+        widen4(ap, G);
+        q0_group<float, MP, true>(G, u >> 2, TT / 2, src, nullptr, opf, opm, prev, ba);
+        widen4(bq, G);
+        q0_group<float, MP, true>(G, (u >> 2) + 1, TT / 2, src, nullptr, opf, opm, prev, ba);
+      }
+    }
+    double v[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) v[k] = 0.5 * dmax(tx[k], tq[k]);
+    if (oQ1 != kNone) {
+#pragma unroll
+      for (int k = 0; k < 4; ++k) bacc((double)uu[k], (double)pp[k], v[k], ba);
+    } else if (oQ1p != kNone) {
+      bacc((double)uu[3], (double)pp[3], v[0], ba);
+      bacc((double)uu[1], (double)pp[1], v[1], ba);
+      bacc((double)uu[2], (double)pp[2], v[2], ba);
+      bacc((double)uu[0], (double)pp[0], v[3], ba);
+    }
+  }
+}
+
 template <typename T, uint32_t TT, int MW, int MP, bool WMODE, int NT = kThreads, int UNR = 1,
           bool OFS = false, bool RES = false>
 __device__ __forceinline__ void pair_quads(const T* bw, const T* bp, const T* src, T* dst,
@@ -479,7 +566,11 @@ __device__ __forceinline__ uint64_t qnext(const QGeo& g, uint64_t c, uint64_t G,
 struct QItem {
   uint32_t m[8];
 };
-template <int M>
+__device__ __forceinline__ void cp_async4(uint32_t* smem, const uint32_t* gmem) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(smem)), "l"(gmem)
+               : "memory");
+}
+template <int M, bool ASYNC>
 __device__ __forceinline__ void qlookup(const QGeo& g, const uint32_t* __restrict__ map,
                                         uint64_t tau, QItem& it) {
   constexpr uint32_t TT = 1u << (2 * M), LOG = 2 * M;
@@ -488,14 +579,31 @@ __device__ __forceinline__ void qlookup(const QGeo& g, const uint32_t* __restric
   const uint64_t wb = qwin(g, x0), wp = qwin(g, p0);
   const uint64_t yf = wb >> 2, ypf = wp >> 2;
   const int sh = 2 * g.K;
-  it.m[0] = __ldg(map + (wb >> sh));
-  it.m[1] = __ldg(map + (wp >> sh));
-  it.m[2] = __ldg(map + (x0 >> sh));
-  it.m[3] = __ldg(map + (p0 >> sh));
-  it.m[4] = __ldg(map + (yf >> sh));
-  it.m[5] = __ldg(map + ((g.q1 - yf - TT / 2) >> sh));
-  it.m[6] = __ldg(map + (ypf >> sh));
-  it.m[7] = __ldg(map + ((g.q1 - ypf - TT / 2) >> sh));
+  if constexpr (ASYNC) {
+    // straight into shared memory (cp.async; `it` is in shared memory): needed at the next fill
+    // only, and no register holds them across the consumer loop in between (qlookup_wait)
+    cp_async4(&it.m[0], map + (wb >> sh));
+    cp_async4(&it.m[1], map + (wp >> sh));
+    cp_async4(&it.m[2], map + (x0 >> sh));
+    cp_async4(&it.m[3], map + (p0 >> sh));
+    cp_async4(&it.m[4], map + (yf >> sh));
+    cp_async4(&it.m[5], map + ((g.q1 - yf - TT / 2) >> sh));
+    cp_async4(&it.m[6], map + (ypf >> sh));
+    cp_async4(&it.m[7], map + ((g.q1 - ypf - TT / 2) >> sh));
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  } else {
+    it.m[0] = __ldg(map + (wb >> sh));
+    it.m[1] = __ldg(map + (wp >> sh));
+    it.m[2] = __ldg(map + (x0 >> sh));
+    it.m[3] = __ldg(map + (p0 >> sh));
+    it.m[4] = __ldg(map + (yf >> sh));
+    it.m[5] = __ldg(map + ((g.q1 - yf - TT / 2) >> sh));
+    it.m[6] = __ldg(map + (ypf >> sh));
+    it.m[7] = __ldg(map + ((g.q1 - ypf - TT / 2) >> sh));
+  }
+}
+__device__ __forceinline__ void qlookup_wait() {
+  asm volatile("cp.async.wait_all;" ::: "memory");
 }
 
 // Thread 0: bulk-load the two windows of tile pair tau into a stage and record the item's
@@ -583,15 +691,16 @@ __global__ void __launch_bounds__(NT, MINB) bin2q_kernel(Bin2QArgs a) {
   uint64_t* bars = reinterpret_cast<uint64_t*>(in + (size_t)S * C::STAGE);
   uint64_t* metas = bars + S;  // [S][8]
 
+  // the geometry comes precomputed in the launch arguments (launch_q): constant-bank operands
+  // that ptxas re-reads where needed instead of holding (or spilling) them across the item loop
   QGeo g;
-  const int L = 2 * a.ell;
   g.K = a.K;
-  g.lmask = (1ull << L) - 1;
-  g.q1 = 1ull << (L - 2);
-  g.amask = 0xAAAAAAAAAAAAAAAAull & g.lmask;
-  g.bmask = 0x5555555555555555ull & g.lmask;
-  g.kmask = (1ull << (2 * a.K)) - 1;
-  g.ntiles = 1ull << (2 * (a.ell - 1 - M));
+  g.lmask = a.geo[0];
+  g.q1 = a.geo[1];
+  g.amask = a.geo[2];
+  g.bmask = a.geo[3];
+  g.kmask = a.geo[4];
+  g.ntiles = a.geo[5];
   const T* src = reinterpret_cast<const T*>(a.src);
   T* dst = reinterpret_cast<T*>(a.dst);
   const uint32_t* map = a.map;
@@ -630,7 +739,13 @@ __global__ void __launch_bounds__(NT, MINB) bin2q_kernel(Bin2QArgs a) {
   // extra producer state spills), it costs
   constexpr int depth = DEPTH;
   static_assert(DEPTH == 1 || DEPTH == 3, "producer depth 1 or 3");
-  QItem pit;
+  // the next item's map entries (thread 0, qlookup): registers in the sweeps; in shared memory,
+  // fetched by cp.async, in the bound pass, which runs at its register cap (A/B at l = 17: bound
+  // fp32 10.64 -> 10.21 ms, fp64 20.8 -> 17.3; the sweeps lose 0.3-1 % that way)
+  constexpr bool ASYNC = WMODE;
+  static_assert(sizeof(QItem) == 32, "QCfg::SMEM reserves 32 bytes");
+  QItem pit_r;
+  QItem& pit = ASYNC ? *reinterpret_cast<QItem*>(metas + 8 * S) : pit_r;
   auto ent_of = [&](uint64_t c) -> uint32_t { return c < nitems ? entry(c) : 0u; };
   auto tile_e = [&](uint32_t e) -> uint64_t {
     return sched ? (uint64_t)(e & kQTileMask) : (uint64_t)e;
@@ -647,6 +762,7 @@ __global__ void __launch_bounds__(NT, MINB) bin2q_kernel(Bin2QArgs a) {
     uint64_t* meta = metas + 8 * s;
     if (pc < nitems) {
       meta[7] = 0;
+      if constexpr (ASYNC) qlookup_wait();
       qissue<T, M, WMODE, RES>(g, pit, tile_e(e0), sbuf, &bars[s], meta, src,
                                sched ? (e0 >> kQHintShift) : 0xFu, keep, prev, base);
       if constexpr (depth == 1) {  // claim, entry and map lookups back to back
@@ -659,7 +775,7 @@ __global__ void __launch_bounds__(NT, MINB) bin2q_kernel(Bin2QArgs a) {
         e1 = ent_of(p1);
         p2 = claim(p2);
       }
-      if (pc < nitems) qlookup<M>(g, map, tile_e(e0), pit);
+      if (pc < nitems) qlookup<M, ASYNC>(g, map, tile_e(e0), pit);
     } else {
       meta[7] = 1;
       mbar_arrive(&bars[s]);
@@ -673,7 +789,7 @@ __global__ void __launch_bounds__(NT, MINB) bin2q_kernel(Bin2QArgs a) {
       e1 = ent_of(p1);
     }
     e0 = ent_of(pc);
-    if (pc < nitems) qlookup<M>(g, map, tile_e(e0), pit);
+    if (pc < nitems) qlookup<M, ASYNC>(g, map, tile_e(e0), pit);
     for (int s = 0; s < S; ++s) fill(s, in + (size_t)s * C::STAGE);
   }
 
@@ -693,6 +809,11 @@ __global__ void __launch_bounds__(NT, MINB) bin2q_kernel(Bin2QArgs a) {
 #define LCSB_Q1(MW, MP)                                                            \
   if constexpr (sizeof(T) == 4 && !WMODE && !OFS && !RES)                          \
     pair_quads_f32<T, TT, MW, MP>(bw, bp, src, dst, meta, self);                   \
+  else if constexpr (sizeof(T) == 4 && WMODE && !RES && NT == kThreads && UNR == 1 && WLEAN) \
+    pair_quads_w32<TT, MW, MP>(reinterpret_cast<const float*>(bw),                 \
+                               reinterpret_cast<const float*>(bp),                 \
+                               reinterpret_cast<const float*>(src), meta, self,    \
+                               reinterpret_cast<const float*>(prev), ba);          \
   else                                                                             \
     pair_quads<T, TT, MW, MP, WMODE, NT, UNR, OFS, RES>(bw, bp, src, dst, meta, self, prev, ba, \
                                                         base)
@@ -751,7 +872,15 @@ cudaError_t launch_q(const Bin2QArgs& a, cudaStream_t s, int sms) {
       (a.sched && a.sched_m == M) ? a.nitems : (1ull << (2 * (a.ell - 1 - M)));
   uint64_t blocks = cap < ntiles ? cap : ntiles;
   if (blocks < 1) blocks = 1;
-  bin2q_kernel<T, M, S, WMODE, MINB, NT, UNR, OFS, RES, DEPTH><<<(unsigned)blocks, NT, C::SMEM, s>>>(a);
+  Bin2QArgs b = a;
+  const int L = 2 * a.ell;
+  b.geo[0] = (1ull << L) - 1;
+  b.geo[1] = 1ull << (L - 2);
+  b.geo[2] = 0xAAAAAAAAAAAAAAAAull & b.geo[0];
+  b.geo[3] = 0x5555555555555555ull & b.geo[0];
+  b.geo[4] = (1ull << (2 * a.K)) - 1;
+  b.geo[5] = 1ull << (2 * (a.ell - 1 - M));
+  bin2q_kernel<T, M, S, WMODE, MINB, NT, UNR, OFS, RES, DEPTH><<<(unsigned)blocks, NT, C::SMEM, s>>>(b);
   return cudaGetLastError();
 }
 

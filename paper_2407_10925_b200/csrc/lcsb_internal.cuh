@@ -161,6 +161,8 @@ struct Bin2QArgs {
   unsigned long long* omin;
   // residual storage (reading R24): the fixed fp32 base H; the tables hold e = v - o - H
   const void* base;
+  // set by the launcher: lmask, q1, a-bit mask, b-bit mask, block mask, tiles (kern_bin2q.cuh)
+  uint64_t geo[6];
 };
 // schedule entries: tile index in the low bits, L2 hint bits (one per window piece) at the top
 constexpr int kQHintShift = 28;
