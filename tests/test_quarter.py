@@ -190,17 +190,19 @@ def test_quarter_equals_half_table_l13(dtype):
 
 @pytest.mark.gpu
 @pytest.mark.skipif(not has_cuda(), reason="needs a CUDA device")
-def test_quarter_dynamic_claiming_under_graph_replay(monkeypatch):
-    """l = 12 fp32: the scheduled sweep with dynamic item claiming (its counter zeroed by a memset
-    node before every launch) replayed from captured CUDA graphs equals plain launches, static
-    claiming and the half table, bitwise."""
+@pytest.mark.parametrize("dtype", ["f32", "f64"])
+def test_quarter_dynamic_claiming_under_graph_replay(monkeypatch, dtype):
+    """l = 12: the scheduled sweep with dynamic item claiming (its counter zeroed by a memset
+    node before every launch; the producer pipelined three items deep) replayed from captured
+    CUDA graphs equals plain launches and static claiming bitwise, and the half table (fp32:
+    bitwise; fp64: 1e-12)."""
     from seeded_inputs import splitmix64_indices
     idx = splitmix64_indices(0x240710925, 1 << 18, 1 << 24)
     vals = []
     for env in ({}, {"LCSB_NO_GRAPHS": "1"}, {"LCSB_QSTATIC": "1"}):
         for k, v in env.items():
             monkeypatch.setenv(k, v)
-        h = L.Lcsb(2, 2, 12, dtype="f32")
+        h = L.Lcsb(2, 2, 12, dtype=dtype)
         assert h.kernel_in_use == "bin2q"
         h.ready(wait=True)  # the schedule (built on a host thread) is used from the first sweep
         h.sweep(70)
@@ -209,12 +211,16 @@ def test_quarter_dynamic_claiming_under_graph_replay(monkeypatch):
         h.destroy()
         for k in env:
             monkeypatch.delenv(k)
-    ref = L.Lcsb(2, 2, 12, dtype="f32", symmetry=1)
+    ref = L.Lcsb(2, 2, 12, dtype=dtype, symmetry=1)
     ref.sweep(103)
     rv = (ref.table_gather(idx), ref.table_gather(idx, which=1), ref.bound().bound)
     ref.destroy()
+    for v in vals[1:]:  # every claiming / launch mode: bit for bit
+        assert np.array_equal(v[0], vals[0][0]) and np.array_equal(v[1], vals[0][1])
+        assert v[2] == vals[0][2]
     for v in vals:  # the bound: quarter one-pass vs half-table two-pass (reading R21)
-        assert np.array_equal(v[0], rv[0]) and np.array_equal(v[1], rv[1])
+        _cmp(v[0], rv[0], dtype)
+        _cmp(v[1], rv[1], dtype)
         assert abs(v[2] - rv[2]) <= 1e-12, (v[2], rv[2])
 
 
