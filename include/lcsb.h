@@ -225,6 +225,16 @@ int lcsb_shard_locate_sigma4(int32_t ell, int32_t shards, uint64_t logical, int3
 int lcsb_quarter_locate(int32_t ell, int32_t block_log4, uint64_t logical, uint64_t* stored,
                         uint64_t* n_stored);
 
+/* Host-only plan query (no GPU needed) of the sharded quarter table of the
+ * binary two-array form, length-ell strings, storage `dtype`, `shards` = 2, 4 or 8 GPUs and
+ * `passes` passes of the placement search (as lcsb_create would build it): per shard k, the
+ * items (tile pairs) it runs, and the table ENTRIES one sweep of those items reads from other
+ * shards' memory (windows) and stores into them (output runs).  The arrays hold `shards`
+ * values.  Deterministic; takes seconds at ell = 18.  Errors: EINVAL (no sharded quarter table
+ * for the configuration: ell too small for the key, other shard counts). */
+int lcsb_quarter_shard_plan(int32_t ell, int32_t dtype, int32_t shards, int32_t passes,
+                            uint64_t* items, uint64_t* peer_read, uint64_t* peer_written);
+
 /* Host preparations that affect only speed -- the quarter table's L2 item schedule, which
  * lcsb_create builds on a host thread so that it returns without waiting (about 0.4-1.5 s at
  * l = 17) -- are installed by the first lcsb_sweep / lcsb_bound after they are ready; sweeps

@@ -462,6 +462,36 @@ extern "C" int lcsb_quarter_locate(int32_t ell, int32_t block_log4, uint64_t log
   return LCSB_OK;
 }
 
+extern "C" int lcsb_quarter_shard_plan(int32_t ell, int32_t dtype, int32_t shards,
+                                       int32_t passes, uint64_t* items, uint64_t* peer_read,
+                                       uint64_t* peer_written) {
+  if (!items || !peer_read || !peer_written || passes < 0)
+    return set_err(nullptr, LCSB_EINVAL, "bad arguments to lcsb_quarter_shard_plan");
+  lcsb_config c;
+  lcsb_config_init(&c);
+  c.sigma = 2, c.d = 2, c.ell = ell, c.dtype = dtype, c.symmetry = 2, c.shards = shards;
+  c.virtual_shards = 1;
+  Plan p;
+  char why[256];
+  if (plan_config(&c, &p, why, sizeof why) != LCSB_OK || p.symmetric != 2 || p.P < 2)
+    return set_err(nullptr, LCSB_EINVAL, "no sharded quarter table for this configuration");
+  std::vector<uint32_t> map(quarter_map_entries(ell, p.qK));
+  uint64_t maxslots = 0;
+  if (!build_quarter_map_sharded(ell, p.qK, p.qM, p.p, passes, map.data(), &maxslots))
+    return set_err(nullptr, LCSB_EINVAL, "sharded quarter map construction failed");
+  const std::vector<uint32_t> none;
+  std::vector<uint32_t> mine;
+  for (int k = 0; k < p.P; ++k) {
+    quarter_shard_items(ell, p.qK, p.qM, map.data(), maxslots, k, none, mine);
+    uint64_t tr[3];
+    quarter_shard_traffic(ell, p.qK, p.qM, map.data(), maxslots, k, mine, tr);
+    items[k] = mine.size();
+    peer_read[k] = tr[0];
+    peer_written[k] = tr[1];
+  }
+  return LCSB_OK;
+}
+
 extern "C" int lcsb_nccl_unique_id(void* out, size_t len) {
   if (!out || len < sizeof(ncclUniqueId))
     return set_err(nullptr, LCSB_EINVAL, "need a %zu-byte buffer", sizeof(ncclUniqueId));

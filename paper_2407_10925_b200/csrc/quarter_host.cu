@@ -75,6 +75,46 @@ static uint64_t shard_stride(const std::vector<uint64_t>& cnt, uint64_t total) {
   return mx > room ? mx : room;
 }
 
+// Owner of an item (the shard whose launch runs it) in the sharded quarter table: the kernel
+// addresses every window and output run through the one virtual range, so any shard may run any
+// item.  Default: the shard holding most of the item's entries (both windows, 2 T each, and its
+// stored output runs), ties to the first window's shard; LCSB_QOWNER_FIRST=1 (A/B): always the
+// first window's shard (round 2's first rule).  `sh` holds the shard of each part.
+static bool owner_first() {
+  static const bool f = getenv("LCSB_QOWNER_FIRST") != nullptr;
+  return f;
+}
+static uint32_t item_owner(int n, const uint32_t* sh, const uint32_t* len) {
+  if (owner_first()) return sh[0];
+  uint64_t loc[kMaxShards] = {0};
+  for (int k = 0; k < n; ++k) loc[sh[k]] += len[k];
+  uint32_t best = sh[0];
+  for (uint32_t s = 0; s < (uint32_t)kMaxShards; ++s)
+    if (loc[s] > loc[best]) best = s;
+  return best;
+}
+// the parts of item tau: both windows (2 T entries each) and its stored output runs, as block
+// indices of the half table (`blk`) and lengths; returns the count
+static int item_parts(uint64_t tau, uint64_t q1, uint64_t lmask, uint64_t amask, uint64_t bmask,
+                      int M, int K, const uint32_t* map, uint64_t* blk, uint32_t* len) {
+  const uint64_t T = 1ull << (2 * M);
+  const int sh = 2 * K;
+  const uint64_t x0 = q1 + tau * T, p0 = pairswap_hd(~x0 & lmask) & ~(T - 1);
+  const bool self = ((p0 - q1) >> (2 * M)) == tau;
+  auto win = [&](uint64_t x) { return (x & amask) | ((x & bmask & ~q1) << 2); };
+  const uint64_t wb = win(x0), wp = win(p0), yf = wb >> 2, ypf = wp >> 2;
+  int n = 0;
+  blk[n] = wb >> sh, len[n++] = (uint32_t)(2 * T);
+  blk[n] = wp >> sh, len[n++] = (uint32_t)(2 * T);
+  const uint64_t runs[6] = {x0, p0, yf, q1 - yf - T / 2, ypf, q1 - ypf - T / 2};
+  for (int r = 0; r < 6; ++r) {
+    if (self && (r == 1 || r >= 4)) continue;
+    if ((map[runs[r] >> sh] & 3u) != 0) continue;
+    blk[n] = runs[r] >> sh, len[n++] = (uint32_t)(r < 2 ? T : T / 2);
+  }
+  return n;
+}
+
 // Refinement of the block -> shard assignment (round 2): the key places each block by its own
 // prefix, but an item's two windows and its output runs sit in blocks whose prefixes are
 // shifted against each other, so most of them land on other shards.  Any assignment is correct
@@ -146,11 +186,17 @@ static void refine_shards(int ell, int K, int M, const uint32_t* map, uint32_t P
         adj[fillp[s]++] = (uint32_t)e;
       }
     });
+  // NVLink entries of item e: every part not on the item's owner (item_owner's rule)
   auto cost = [&](uint64_t e) -> uint64_t {
     const uint32_t* r = it.data() + ioff[e];
-    const uint32_t o = shard_of_slot[r[0]];
-    uint64_t c = shard_of_slot[r[1]] != o ? 2 * T : 0;
-    for (uint32_t k = 0; k < r[2]; ++k) c += shard_of_slot[r[3 + 2 * k]] != o ? r[4 + 2 * k] : 0;
+    uint32_t shv[8], lenv[8];
+    int n = 0;
+    shv[n] = shard_of_slot[r[0]], lenv[n++] = (uint32_t)(2 * T);
+    shv[n] = shard_of_slot[r[1]], lenv[n++] = (uint32_t)(2 * T);
+    for (uint32_t k = 0; k < r[2]; ++k) shv[n] = shard_of_slot[r[3 + 2 * k]], lenv[n++] = r[4 + 2 * k];
+    const uint32_t o = item_owner(n, shv, lenv);
+    uint64_t c = 0;
+    for (int k = 0; k < n; ++k) c += shv[k] != o ? lenv[k] : 0;
     return c;
   };
   std::vector<uint64_t> size(P, 0);
@@ -273,9 +319,11 @@ void quarter_shard_items(int ell, int K, int M, const uint32_t* map, uint64_t ma
   const uint64_t amask = 0xAAAAAAAAAAAAAAAAull & lmask, bmask = 0x5555555555555555ull & lmask;
   const uint64_t T = 1ull << (2 * M);
   auto owner = [&](uint64_t tau) {
-    const uint64_t x0 = q1 + tau * T;
-    const uint64_t w = (x0 & amask) | ((x0 & bmask & ~q1) << 2);
-    return (int)((map[w >> (2 * K)] >> 2) / maxslots);
+    uint64_t blk[8];
+    uint32_t len[8], shv[8];
+    const int n = item_parts(tau, q1, lmask, amask, bmask, M, K, map, blk, len);
+    for (int k = 0; k < n; ++k) shv[k] = (uint32_t)((map[blk[k]] >> 2) / maxslots);
+    return (int)item_owner(n, shv, len);
   };
   out.clear();
   if (!sched.empty()) {
@@ -301,28 +349,14 @@ void quarter_shard_traffic(int ell, int K, int M, const uint32_t* map, uint64_t 
   const int L = 2 * ell;
   const uint64_t lmask = (1ull << L) - 1, q1 = 1ull << (L - 2);
   const uint64_t amask = 0xAAAAAAAAAAAAAAAAull & lmask, bmask = 0x5555555555555555ull & lmask;
-  const uint64_t T = 1ull << (2 * M);
-  const int sh = 2 * K;
-  auto win = [&](uint64_t x) { return (x & amask) | ((x & bmask & ~q1) << 2); };
-  auto shard_of = [&](uint64_t s) { return (int)((map[s >> sh] >> 2) / maxslots); };
-  auto stored = [&](uint64_t s) { return (map[s >> sh] & 3u) == 0; };
   out[0] = out[1] = out[2] = 0;
-  for (uint32_t ent : items) {
-    const uint64_t tau = ent & kQTileMask;
-    const uint64_t x0 = q1 + tau * T;
-    const uint64_t p0 = pairswap_hd(~x0 & lmask) & ~(T - 1);
-    const bool self = ((p0 - q1) >> (2 * M)) == tau;
-    const uint64_t wb = win(x0), wp = win(p0);
-    out[2] += 4 * T;  // both windows read
-    if (shard_of(wp) != shard) out[0] += 2 * T;
-    const uint64_t yf = wb >> 2, ypf = wp >> 2;
-    const uint64_t runs[6] = {x0, p0, yf, q1 - yf - T / 2, ypf, q1 - ypf - T / 2};
-    const uint64_t len[6] = {T, T, T / 2, T / 2, T / 2, T / 2};
-    for (int r = 0; r < 6; ++r) {
-      if (self && (r == 1 || r >= 4)) continue;
-      if (!stored(runs[r])) continue;
-      out[2] += len[r];
-      if (shard_of(runs[r]) != shard) out[1] += len[r];
+  for (uint32_t ent : items) {  // the items this shard runs: every part elsewhere crosses NVLink
+    uint64_t blk[8];
+    uint32_t len[8];
+    const int n = item_parts(ent & kQTileMask, q1, lmask, amask, bmask, M, K, map, blk, len);
+    for (int k = 0; k < n; ++k) {
+      out[2] += len[k];
+      if ((int)((map[blk[k]] >> 2) / maxslots) != shard) out[k < 2 ? 0 : 1] += len[k];
     }
   }
 }

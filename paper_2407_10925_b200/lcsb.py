@@ -64,7 +64,7 @@ class LcsbBound(ctypes.Structure):
 EXPORTS = ["lcsb_config_init", "lcsb_required_bytes", "lcsb_create", "lcsb_create_ex",
            "lcsb_reset", "lcsb_sweep", "lcsb_bound", "lcsb_table", "lcsb_table_gather",
            "lcsb_nccl_unique_id", "lcsb_shard_locate", "lcsb_shard_locate_sigma4",
-           "lcsb_quarter_locate", "lcsb_ready", "lcsb_rebase", "lcsb_save", "lcsb_load",
+           "lcsb_quarter_locate", "lcsb_quarter_shard_plan", "lcsb_ready", "lcsb_rebase", "lcsb_save", "lcsb_load",
            "lcsb_sweeps_done",
            "lcsb_num_shards",
            "lcsb_num_states", "lcsb_stored_states", "lcsb_device_bytes", "lcsb_kernel_in_use",
@@ -123,6 +123,8 @@ def load_library():
                                         ctypes.POINTER(ctypes.c_uint64),
                                         ctypes.POINTER(ctypes.c_uint64)]
     lib.lcsb_quarter_locate.restype = ctypes.c_int
+    lib.lcsb_quarter_shard_plan.argtypes = [ctypes.c_int32] * 4 + [ctypes.POINTER(ctypes.c_uint64)] * 3
+    lib.lcsb_quarter_shard_plan.restype = ctypes.c_int
     for name, rt in [("lcsb_sweeps_done", ctypes.c_int64), ("lcsb_num_states", ctypes.c_uint64),
                      ("lcsb_num_shards", ctypes.c_int32),
                      ("lcsb_stored_states", ctypes.c_uint64),
@@ -440,6 +442,18 @@ def lcsb_table_gather(h: Lcsb, idx, which=0) -> np.ndarray:
 
 def lcsb_destroy(h: Lcsb):
     h.destroy()
+
+
+def lcsb_quarter_shard_plan(ell: int, dtype: str = "f32", shards: int = 2, passes: int = 24):
+    """Host-only plan of the sharded quarter table: per shard, the items it runs
+    and the table entries one sweep reads from / stores into other shards (numpy uint64 arrays)."""
+    n = int(shards)
+    items, rd, wr = (np.zeros(n, dtype=np.uint64) for _ in range(3))
+    P = ctypes.POINTER(ctypes.c_uint64)
+    _check(load_library().lcsb_quarter_shard_plan(int(ell), _dtype_code(dtype), n, int(passes),
+                                                  items.ctypes.data_as(P), rd.ctypes.data_as(P),
+                                                  wr.ctypes.data_as(P)))
+    return items, rd, wr
 
 
 def lcsb_quarter_locate(ell: int, block_log4: int, logical: int):

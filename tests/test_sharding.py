@@ -639,3 +639,40 @@ def test_quarter_process_mode_multi_rank_on_one_gpu(tmp_path, world, ell, K, dty
     mp.spawn(_pm_quarter_worker, args=(world, _free_port(), str(tmp_path), ell, K, dtype),
              nprocs=world, join=True)
     assert np.load(tmp_path / "pmq.npy").all()
+
+
+@pytest.mark.parametrize("ell,shards", [(12, 2), (12, 4), (13, 8)])
+def test_quarter_shard_plan_partitions_items_and_search_cuts_nvlink(ell, shards):
+    """Host-only plan of the sharded quarter table (§9c, `lcsb_quarter_shard_plan`): the shards'
+    item lists partition the tile pairs (each pair {t, psi t} run once), stay balanced, and the
+    placement search moves fewer entries over NVLink than the plain xor key -- both at most the
+    entries the items touch."""
+    L.load_library()
+    items, rd, wr = L.lcsb_quarter_shard_plan(ell, "f32", shards, 24)
+    items0, rd0, wr0 = L.lcsb_quarter_shard_plan(ell, "f32", shards, 0)
+    # tile pairs: the tiles of 4^M Q1 outputs (M = K - 1, K = min(7, l - 5)), paired by psi
+    K = min(7, ell - 5)
+    M = min(K - 1, 6)
+    ntiles = 4 ** (ell - 1 - M)
+    npairs = sum(1 for t in range(ntiles) if _psi_tile(ell, M, t) >= t)
+    assert int(items.sum()) == npairs == int(items0.sum())
+    # balance: few blocks per shard at these sizes (1.2-1.35 under either owner rule; ell = 18:
+    # 1.03 / 1.09 / 1.05 at 2 / 4 / 8 shards)
+    assert items.max() <= 1.4 * items.mean()
+    assert (rd + wr).sum() < 0.8 * (rd0 + wr0).sum()
+    T = 4 ** M
+    assert (rd + wr).sum() <= npairs * (4 * T + 2 * T + 4 * (T // 2))
+    with pytest.raises(L.LcsbError):
+        L.lcsb_quarter_shard_plan(ell, "f32", 3, 24)
+
+
+def _psi_tile(ell, M, t):
+    """Tile index of psi(t) (complement o swap of the first output of Q1 tile t)."""
+    L2 = 2 * ell
+    lmask = (1 << L2) - 1
+    q1 = 1 << (L2 - 2)
+    x0 = q1 + (t << (2 * M))
+    v = ~x0 & lmask
+    ps = ((v & 0xAAAAAAAAAAAAAAAA) >> 1) | ((v & 0x5555555555555555) << 1)
+    p0 = ps & ~((1 << (2 * M)) - 1)
+    return (p0 - q1) >> (2 * M)
