@@ -365,6 +365,12 @@ def run_ours(args, w, ws, rank, local):
                      # stores of its items (lcsb_shard_traffic, §9c); otherwise the outputs (and,
                      # q4, the row means) whose owner is another shard, (1 - 1/P) of the shard's
                      "nvlink_bytes_per_launch": nvlink_bytes,
+                     # SURVEY 8(d) number (1): the DRAM bytes the kernel really moves (ncu,
+                     # `traffic`) per launch time, against the same peak -- how close the kernel
+                     # runs to the copy bandwidth for the bytes it moves (frac: for the
+                     # compulsory bytes)
+                     "dram_achieved": (traffic / (launch_ms / 1e3) / 1e9) if traffic else None,
+                     "dram_frac": (traffic / (launch_ms / 1e3) / 1e9 / peak) if traffic else None,
                      "kernel": kernel_name + " sweep kernel"},
         "e2e": {"value": e2e_value, "unit": "state-updates/s",
                 "h2d_bytes_per_step": int(idx.nbytes),
