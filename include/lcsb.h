@@ -172,6 +172,22 @@ int lcsb_reset(lcsb_t* h);
  * failure), ENCCL. */
 int lcsb_sweep(lcsb_t* h, int64_t n);
 
+/* lcsb_sweep_ex flags (round 2, reading R25).  A TRACKING sweep v_k = F(v_{k-1}) also reads
+ * v_{k-1} at every stored output and reduces R_max, R_min of v_k - v_{k-1} (Alg. 5 line 7,
+ * PAPER.md:738, the R of the iterate it writes) and D = min(F(v_{k-1}) - v_{k-1}) (F in fp64
+ * before the storage rounding; max W = R - D, reading R21, for the iterate it reads) into device
+ * slots kept with the handle.  TRACK: the last sweep of the call tracks; TRACK2: the last two.
+ * Only the binary quarter table with plain storage has tracking sweeps; elsewhere the flags are
+ * accepted and ignored (the sweeps are plain). */
+#define LCSB_SWEEP_TRACK 1u
+#define LCSB_SWEEP_TRACK2 3u
+
+/* lcsb_sweep with flags (above).  A tracked last sweep lets the next lcsb_bound skip the read of
+ * v_{n-1} (it evaluates only D at the current iterate, with R from the tracking sweep); values,
+ * R and the bound are identical to the untracked path.  Errors: as lcsb_sweep; EINVAL (unknown
+ * flag bits). */
+int lcsb_sweep_ex(lcsb_t* h, int64_t n, uint32_t flags);
+
 typedef struct {
   double R_max, R_min;         /* max / min over states of v_new - v_prev */
   double E_at_Rmax, E_at_Rmin; /* E = max(0, max W) for each R (Alg. 2 lines 6-7) */
@@ -179,7 +195,8 @@ typedef struct {
   double bound;                /* bound_at_R<rmode> */
   double best_bound;           /* best over every lcsb_bound call so far for rmode, starting
                                   from the triplet (v_0, 0, 0) (Alg. 2 lines 2, 8-10) */
-  int64_t sweeps_done;         /* sweeps performed by this handle */
+  int64_t sweeps_done;         /* sweeps of the iterate u the bound certifies (lcsb_bound: the
+                                  handle's sweep count; lcsb_sweep_bound: that count - 1) */
   int64_t best_sweep;          /* sweeps_done at the best evaluation (0 = initial triplet) */
 } lcsb_bound_t;
 
@@ -187,6 +204,16 @@ typedef struct {
  * Synchronises the handle's stream; the only host round-trip of the path.
  * Errors: ESTATE (no sweep yet), ECUDA. */
 int lcsb_bound(lcsb_t* h, lcsb_bound_t* out);
+
+/* Enqueue n >= 1 sweeps and evaluate the bound (Alg. 2 lines 5-10, both R readings, best-so-far
+ * update) of the iterate BEFORE the last of them, u = v_{N-1} with N = sweeps after the call
+ * (reading R25): in the two-array form Alg. 2's W needs F(u,u) = v_N, i.e. exactly the last
+ * sweep, so on the quarter table the last two sweeps are tracking sweeps and no pass over the
+ * table is added (R of u from sweep N-1, D of u from sweep N).  Other layouts give the same values
+ * by lcsb_sweep(n-1), lcsb_bound, lcsb_sweep(1).  out->sweeps_done = N - 1.  Synchronises the
+ * stream.  Errors: EINVAL (n < 1), ESTATE (N - 1 < 1, or no sweep after lcsb_rebase), ECUDA,
+ * ENCCL. */
+int lcsb_sweep_bound(lcsb_t* h, int64_t n, lcsb_bound_t* out);
 
 /* Copy count table entries, logical indices [first, first+count), of generation `which`
  * (0 = newest, 1 = one sweep back, ... up to d-1 for KS / 1 for two-array) into host_dst,

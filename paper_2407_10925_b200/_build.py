@@ -8,7 +8,7 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 SO = os.path.join(PKG, "liblcsb.so")
 SOURCES = ["lcsb_api.cu", "quarter_host.cu", "kern_generic.cu", "kern_bin2.cu", "kern_bin2_tma.cu",
-           "kern_bin2q.cu", "kern_bin2q_bound.cu", "kern_bin2q_ext.cu", "kern_q4.cu",
+           "kern_bin2q.cu", "kern_bin2q_bound.cu", "kern_bin2q_ext.cu", "kern_bin2q_diff.cu", "kern_q4.cu",
            "kern_small.cu", "kern_reduce.cu", "vmm.cu"]
 NVCC_FLAGS = [
     "-O3", "-std=c++17",

@@ -210,6 +210,15 @@ __device__ __forceinline__ void bacc(double u, double p, double f, BAcc& b) {
   b.rmin = dmin(b.rmin, dd);
   b.dmin = dmin(b.dmin, f - u);
 }
+// tracking sweep (DIFF): at one stored output, u = the table read (v_{n-1}) there, f = F(u,u) in
+// fp64 and st = the stored value (v_n): R of v_n (max / min of v_n - v_{n-1}, the one-pass bound's
+// expression) and D of v_{n-1} (min of F(u,u) - u, reading R21)
+__device__ __forceinline__ void dacc(double u, double f, double st, BAcc& b) {
+  const double dd = st - u;
+  b.rmax = dmax(b.rmax, dd);
+  b.rmin = dmin(b.rmin, dd);
+  b.dmin = dmin(b.dmin, f - u);
+}
 // streaming 4-entry load in the storage type (widened at use)
 __device__ __forceinline__ void ld4s(const float* p, float (&v)[4]) {
   const float4 f = __ldcs(reinterpret_cast<const float4*>(p));
@@ -230,7 +239,7 @@ __device__ __forceinline__ void ld4s(const double* p, double (&v)[4]) {
 // widened to fp64 once.  The A/B load order alternates across threads so each 128-bit smem load
 // is conflict-free (2-way for permuted x windows).
 // bound pass (WMODE): src = u = v_n, prev = v_{n-1}; nothing is stored
-template <typename T, int MODE, bool WMODE, bool OFS = false, bool RES = false>
+template <typename T, int MODE, bool WMODE, bool OFS = false, bool RES = false, bool DIFF = false>
 __device__ __forceinline__ void q0_group(const double (&G)[4], uint32_t r, uint32_t half_rows,
                                          const T* src, T* dst, uint64_t of, uint64_t om,
                                          const T* prev, BAcc& ba, const T* base = nullptr) {
@@ -243,13 +252,29 @@ __device__ __forceinline__ void q0_group(const double (&G)[4], uint32_t r, uint3
     // RES: u = H + e and v_prev = H + e_prev (both exact in fp64)
     if (of != kNone) {
       const double h = RES ? (double)__ldcs(base + of + r) : 0.0;
-      bacc(h + (double)__ldcs(src + of + r), h + (double)__ldcs(prev + of + r),
+      bacc(h + (double)__ldcs(src + of + r), prev ? h + (double)__ldcs(prev + of + r) : 0.0,
            q0_val(v0, v1, v2, v3), ba);
     }
     if (om != kNone) {
       const double h = RES ? (double)__ldcs(base + om + rm) : 0.0;
-      bacc(h + (double)__ldcs(src + om + rm), h + (double)__ldcs(prev + om + rm),
+      bacc(h + (double)__ldcs(src + om + rm), prev ? h + (double)__ldcs(prev + om + rm) : 0.0,
            q0_val(v3, v2, v1, v0), ba);
+    }
+  } else if (DIFF) {  // store round(F), reduce against the table read at the same position
+    if (of != kNone) {
+      const double f = q0_val(v0, v1, v2, v3);
+      const T st = (T)f;
+      const double u = (double)__ldcs(src + of + r);
+      st_out(dst + of + r, st);
+      dacc(u, f, (double)st, ba);
+    }
+    if (om != kNone) {
+      const uint32_t rm = half_rows - 1 - r;
+      const double f = q0_val(v3, v2, v1, v0);
+      const T st = (T)f;
+      const double u = (double)__ldcs(src + om + rm);
+      st_out(dst + om + rm, st);
+      dacc(u, f, (double)st, ba);
     }
   } else if (OFS) {  // store round(F(s) - c) (RES: - H[x]); track the min of s (= H + e)
     if (of != kNone) {
@@ -337,10 +362,12 @@ __device__ __forceinline__ void pair_quads_f32(const T* bw, const T* bp, const T
 // fewer values live -- the x window's pair sums and Q0 rows are finished before the psi window's
 // groups are loaded (the kernel runs at its 80-register cap; the fp64 group arrays of both
 // windows held at once spilled to local memory)
-template <uint32_t TT, int MW, int MP>
+// DIFF (the tracking sweep, kern_bin2q_diff.cu): the same walk storing round32(F) at every stored
+// output and reducing against u = the table read there (dacc); v_prev is not read
+template <uint32_t TT, int MW, int MP, bool DIFF = false>
 __device__ __forceinline__ void pair_quads_w32(const float* bw, const float* bp, const float* src,
                                                const uint64_t* meta, bool self, const float* prev,
-                                               BAcc& ba) {
+                                               BAcc& ba, float* dst = nullptr) {
   constexpr uint32_t SX = (MW == 0 || MW == 3) ? 2 : 0, SP = (MP == 0 || MP == 3) ? 2 : 1;
   const uint64_t oQ1 = meta[1], oQ1p = meta[2];
   const uint64_t of = meta[3], om = meta[4], opf = meta[5], opm = meta[6];
@@ -355,7 +382,7 @@ __device__ __forceinline__ void pair_quads_w32(const float* bw, const float* bp,
     const uint64_t q = oQ1 != kNone ? oQ1 + o0 : (oQ1p != kNone ? oQ1p + qb : kNone);
     if (q != kNone) {
       ld4s(src + q, uu);
-      ld4s(prev + q, pp);
+      if (!DIFF && prev) ld4s(prev + q, pp);  // null: the D-only pass (R tracked by the last sweep)
     }
     const bool sx = (qd >> SX) & 1u, sp = (qd >> SP) & 1u;
     constexpr uint32_t c0 = comp<MW>(0), c1 = comp<MW>(1), c2 = comp<MW>(2), c3 = comp<MW>(3);
@@ -373,9 +400,10 @@ __device__ __forceinline__ void pair_quads_w32(const float* bw, const float* bp,
       if (rows_x) {
         double G[4];
         widen4(a, G);
-        q0_group<float, MW, true>(G, g >> 2, TT / 2, src, nullptr, of, om, prev, ba);
+        q0_group<float, MW, !DIFF, false, false, DIFF>(G, g >> 2, TT / 2, src, dst, of, om, prev, ba);
         widen4(b, G);
-        q0_group<float, MW, true>(G, (g >> 2) + 1, TT / 2, src, nullptr, of, om, prev, ba);
+        q0_group<float, MW, !DIFF, false, false, DIFF>(G, (g >> 2) + 1, TT / 2, src, dst, of, om, prev,
+                                                     ba);
       }
     }
     double tq[4];
@@ -391,15 +419,33 @@ __device__ __forceinline__ void pair_quads_w32(const float* bw, const float* bp,
       if (rows_p) {
         double G[4];
         widen4(ap, G);
-        q0_group<float, MP, true>(G, u >> 2, TT / 2, src, nullptr, opf, opm, prev, ba);
+        q0_group<float, MP, !DIFF, false, false, DIFF>(G, u >> 2, TT / 2, src, dst, opf, opm, prev, ba);
         widen4(bq, G);
-        q0_group<float, MP, true>(G, (u >> 2) + 1, TT / 2, src, nullptr, opf, opm, prev, ba);
+        q0_group<float, MP, !DIFF, false, false, DIFF>(G, (u >> 2) + 1, TT / 2, src, dst, opf, opm, prev,
+                                                     ba);
       }
     }
     double v[4];
 #pragma unroll
     for (int k = 0; k < 4; ++k) v[k] = 0.5 * dmax(tx[k], tq[k]);
-    if (oQ1 != kNone) {
+    if constexpr (DIFF) {
+      float st[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) st[k] = (float)v[k];
+      if (oQ1 != kNone)
+        st_out(reinterpret_cast<float4*>(dst + oQ1 + o0), make_float4(st[0], st[1], st[2], st[3]));
+      if (oQ1p != kNone)
+        st_out(reinterpret_cast<float4*>(dst + oQ1p + qb), make_float4(st[3], st[1], st[2], st[0]));
+      if (oQ1 != kNone) {
+#pragma unroll
+        for (int k = 0; k < 4; ++k) dacc((double)uu[k], v[k], (double)st[k], ba);
+      } else if (oQ1p != kNone) {
+        dacc((double)uu[3], v[0], (double)st[0], ba);
+        dacc((double)uu[1], v[1], (double)st[1], ba);
+        dacc((double)uu[2], v[2], (double)st[2], ba);
+        dacc((double)uu[0], v[3], (double)st[3], ba);
+      }
+    } else if (oQ1 != kNone) {
 #pragma unroll
       for (int k = 0; k < 4; ++k) bacc((double)uu[k], (double)pp[k], v[k], ba);
     } else if (oQ1p != kNone) {
@@ -412,7 +458,7 @@ __device__ __forceinline__ void pair_quads_w32(const float* bw, const float* bp,
 }
 
 template <typename T, uint32_t TT, int MW, int MP, bool WMODE, int NT = kThreads, int UNR = 1,
-          bool OFS = false, bool RES = false>
+          bool OFS = false, bool RES = false, bool DIFF = false>
 __device__ __forceinline__ void pair_quads(const T* bw, const T* bp, const T* src, T* dst,
                                            const uint64_t* meta, bool self, const T* prev,
                                            BAcc& ba, const T* base = nullptr) {
@@ -435,11 +481,11 @@ __device__ __forceinline__ void pair_quads(const T* bw, const T* bp, const T* sr
     // overlaps the window reads and the arithmetic); W(psi x) = W(x), so either copy serves
     T uu[4] = {0, 0, 0, 0}, pp[4] = {0, 0, 0, 0};  // initialised: keeps them out of local memory
     T hq[4] = {0, 0, 0, 0}, hp[4] = {0, 0, 0, 0};  // RES: the base at the Q1 outputs
-    if (WMODE) {
+    if (WMODE || DIFF) {
       const uint64_t q = oQ1 != kNone ? oQ1 + o0 : (oQ1p != kNone ? oQ1p + qb : kNone);
       if (q != kNone) {
         ld4s(src + q, uu);
-        ld4s(prev + q, pp);
+        if (WMODE && prev) ld4s(prev + q, pp);
         if (RES) ld4s(base + q, hq);
       }
     } else if (RES) {
@@ -506,6 +552,21 @@ __device__ __forceinline__ void pair_quads(const T* bw, const T* bp, const T* sr
         bacc((double)hq[2] + (double)uu[2], (double)hq[2] + (double)pp[2], v[2], ba);
         bacc((double)hq[0] + (double)uu[0], (double)hq[0] + (double)pp[0], v[3], ba);
       }
+    } else if (DIFF) {  // the sweep's stores + R of v_n and D of v_{n-1} against the table read
+      const T s0 = (T)v[0], s1 = (T)v[1], s2 = (T)v[2], s3 = (T)v[3];
+      if (oQ1 != kNone) st4(dst + oQ1 + o0, (double)s0, (double)s1, (double)s2, (double)s3);
+      if (oQ1p != kNone) st4(dst + oQ1p + qb, (double)s3, (double)s1, (double)s2, (double)s0);
+      if (oQ1 != kNone) {
+        dacc((double)uu[0], v[0], (double)s0, ba);
+        dacc((double)uu[1], v[1], (double)s1, ba);
+        dacc((double)uu[2], v[2], (double)s2, ba);
+        dacc((double)uu[3], v[3], (double)s3, ba);
+      } else if (oQ1p != kNone) {  // position j of the psi run holds output (3, 1, 2, 0)[j]
+        dacc((double)uu[3], v[0], (double)s0, ba);
+        dacc((double)uu[1], v[1], (double)s1, ba);
+        dacc((double)uu[2], v[2], (double)s2, ba);
+        dacc((double)uu[0], v[3], (double)s3, ba);
+      }
     } else if (OFS && RES) {  // round((F(s) - c) - H[x]) at each stored copy; min of H + e
       if (oQ1 != kNone) {
         T st[4];
@@ -539,14 +600,15 @@ __device__ __forceinline__ void pair_quads(const T* bw, const T* bp, const T* sr
     }
     // Q0 rows of the four groups
     if (rows_x) {
-      q0_group<T, MW, WMODE, OFS, RES>(A, g >> 2, TT / 2, src, dst, of, om, prev, ba, base);
-      q0_group<T, MW, WMODE, OFS, RES>(B, (g >> 2) + 1, TT / 2, src, dst, of, om, prev, ba,
-                                        base);
+      q0_group<T, MW, WMODE, OFS, RES, DIFF>(A, g >> 2, TT / 2, src, dst, of, om, prev, ba, base);
+      q0_group<T, MW, WMODE, OFS, RES, DIFF>(B, (g >> 2) + 1, TT / 2, src, dst, of, om, prev, ba,
+                                              base);
     }
     if (rows_p) {
-      q0_group<T, MP, WMODE, OFS, RES>(Ap, u >> 2, TT / 2, src, dst, opf, opm, prev, ba, base);
-      q0_group<T, MP, WMODE, OFS, RES>(Bp, (u >> 2) + 1, TT / 2, src, dst, opf, opm, prev,
-                                        ba, base);
+      q0_group<T, MP, WMODE, OFS, RES, DIFF>(Ap, u >> 2, TT / 2, src, dst, opf, opm, prev, ba,
+                                              base);
+      q0_group<T, MP, WMODE, OFS, RES, DIFF>(Bp, (u >> 2) + 1, TT / 2, src, dst, opf, opm, prev,
+                                              ba, base);
     }
   }
 }
@@ -610,7 +672,7 @@ __device__ __forceinline__ void qlookup_wait() {
 // metadata: meta[0] = window modes (bits 0-1: window t, 2-3: window psi t, bit 4: self pair),
 // meta[1..6] = stored run starts (Q1 t, Q1 psi t, rows t, mirrors t, rows psi t, mirrors psi t;
 // kNone = not stored).
-template <typename T, int M, bool WMODE = false, bool RES = false>
+template <typename T, int M, bool WMODE = false, bool RES = false, bool DIFF = false>
 __device__ __forceinline__ void qissue(const QGeo& g, const QItem& it, uint64_t tau, T* buf,
                                        uint64_t* bar, uint64_t* meta, const T* src,
                                        uint32_t hints, uint64_t keep, const T* prev = nullptr,
@@ -634,13 +696,12 @@ __device__ __forceinline__ void qissue(const QGeo& g, const QItem& it, uint64_t 
   // bound pass: u and v_prev at the item's stored output runs go to L2 now (bulk prefetch), so
   // the consumers' direct loads of them, one item later, hit L2 (RES: the base there too, in
   // the sweep as well)
-  if ((WMODE || RES) && ((TT / 2) * sizeof(T)) % 16 == 0) {
+  // (tracking sweep, DIFF: the table read at the output runs, likewise)
+  if ((WMODE || RES || DIFF) && ((TT / 2) * sizeof(T)) % 16 == 0) {
     const uint64_t q = meta[1] != kNone ? meta[1] : meta[2];
     if (q != kNone) {
-      if (WMODE) {
-        bulk_prefetch_l2(src + q, TT * (uint32_t)sizeof(T));
-        bulk_prefetch_l2(prev + q, TT * (uint32_t)sizeof(T));
-      }
+      if (WMODE || DIFF) bulk_prefetch_l2(src + q, TT * (uint32_t)sizeof(T));
+      if (WMODE && prev) bulk_prefetch_l2(prev + q, TT * (uint32_t)sizeof(T));
       if (RES) bulk_prefetch_l2(base + q, TT * (uint32_t)sizeof(T));
     }
     if (RES && !WMODE && meta[1] != kNone && meta[2] != kNone)
@@ -648,10 +709,8 @@ __device__ __forceinline__ void qissue(const QGeo& g, const QItem& it, uint64_t 
 #pragma unroll
     for (int k = 3; k < 7; ++k)
       if (meta[k] != kNone) {
-        if (WMODE) {
-          bulk_prefetch_l2(src + meta[k], TT / 2 * (uint32_t)sizeof(T));
-          bulk_prefetch_l2(prev + meta[k], TT / 2 * (uint32_t)sizeof(T));
-        }
+        if (WMODE || DIFF) bulk_prefetch_l2(src + meta[k], TT / 2 * (uint32_t)sizeof(T));
+        if (WMODE && prev) bulk_prefetch_l2(prev + meta[k], TT / 2 * (uint32_t)sizeof(T));
         if (RES) bulk_prefetch_l2(base + meta[k], TT / 2 * (uint32_t)sizeof(T));
       }
   }
@@ -681,7 +740,7 @@ __device__ __forceinline__ void qissue(const QGeo& g, const QItem& it, uint64_t 
 }
 
 template <typename T, int M, int S, bool WMODE, int MINB = 1, int NT = kThreads, int UNR = 1,
-          bool OFS = false, bool RES = false, int DEPTH = 1>
+          bool OFS = false, bool RES = false, int DEPTH = 1, bool DIFF = false>
 __global__ void __launch_bounds__(NT, MINB) bin2q_kernel(Bin2QArgs a) {
   using C = QCfg<T, M, S, WMODE, MINB, RES>;
   constexpr uint32_t TT = C::TT, WIN = C::WIN;
@@ -763,7 +822,7 @@ __global__ void __launch_bounds__(NT, MINB) bin2q_kernel(Bin2QArgs a) {
     if (pc < nitems) {
       meta[7] = 0;
       if constexpr (ASYNC) qlookup_wait();
-      qissue<T, M, WMODE, RES>(g, pit, tile_e(e0), sbuf, &bars[s], meta, src,
+      qissue<T, M, WMODE, RES, DIFF>(g, pit, tile_e(e0), sbuf, &bars[s], meta, src,
                                sched ? (e0 >> kQHintShift) : 0xFu, keep, prev, base);
       if constexpr (depth == 1) {  // claim, entry and map lookups back to back
         pc = claim(pc);
@@ -807,16 +866,17 @@ __global__ void __launch_bounds__(NT, MINB) bin2q_kernel(Bin2QArgs a) {
     const T* bw = buf;
     const T* bp = buf + WIN;
 #define LCSB_Q1(MW, MP)                                                            \
-  if constexpr (sizeof(T) == 4 && !WMODE && !OFS && !RES)                          \
+  if constexpr (sizeof(T) == 4 && !WMODE && !OFS && !RES && !DIFF)                 \
     pair_quads_f32<T, TT, MW, MP>(bw, bp, src, dst, meta, self);                   \
-  else if constexpr (sizeof(T) == 4 && WMODE && !RES && NT == kThreads && UNR == 1 && WLEAN) \
-    pair_quads_w32<TT, MW, MP>(reinterpret_cast<const float*>(bw),                 \
-                               reinterpret_cast<const float*>(bp),                 \
-                               reinterpret_cast<const float*>(src), meta, self,    \
-                               reinterpret_cast<const float*>(prev), ba);          \
+  else if constexpr (sizeof(T) == 4 && (WMODE || DIFF) && !RES && NT == kThreads && UNR == 1 && WLEAN) \
+    pair_quads_w32<TT, MW, MP, DIFF>(reinterpret_cast<const float*>(bw),           \
+                                     reinterpret_cast<const float*>(bp),           \
+                                     reinterpret_cast<const float*>(src), meta, self, \
+                                     reinterpret_cast<const float*>(prev), ba,     \
+                                     reinterpret_cast<float*>(dst));               \
   else                                                                             \
-    pair_quads<T, TT, MW, MP, WMODE, NT, UNR, OFS, RES>(bw, bp, src, dst, meta, self, prev, ba, \
-                                                        base)
+    pair_quads<T, TT, MW, MP, WMODE, NT, UNR, OFS, RES, DIFF>(bw, bp, src, dst, meta, self, prev, \
+                                                              ba, base)
     switch (mw * 4 + mp) {
       case 0: LCSB_Q1(0, 0); break;
       case 1: LCSB_Q1(0, 1); break;
@@ -839,7 +899,7 @@ __global__ void __launch_bounds__(NT, MINB) bin2q_kernel(Bin2QArgs a) {
     __syncthreads();  // stage s (data and metadata) is free again
     if (tid == 0) fill((int)s, buf);
   }
-  if (WMODE) block_red3_to(ba.rmax, ba.rmin, ba.dmin, a.red_out);
+  if (WMODE || DIFF) block_red3_to(ba.rmax, ba.rmin, ba.dmin, a.red_out);
   if (OFS && !WMODE) block_min_to(ba.rmin, a.omin);
 }
 
@@ -849,17 +909,17 @@ inline bool q_dynamic(const Bin2QArgs& a, int M) {
 }
 
 template <typename T, int M, int S, bool WMODE, int MINB = 1, int NT = kThreads, int UNR = 1,
-          bool OFS = false, bool RES = false, int DEPTH = 1>
+          bool OFS = false, bool RES = false, int DEPTH = 1, bool DIFF = false>
 cudaError_t launch_q(const Bin2QArgs& a, cudaStream_t s, int sms) {
   using C = QCfg<T, M, S, WMODE, MINB, RES>;
   static uint64_t cap = 0;
   if (cap == 0) {
-    cudaError_t e = cudaFuncSetAttribute(bin2q_kernel<T, M, S, WMODE, MINB, NT, UNR, OFS, RES, DEPTH>,
+    cudaError_t e = cudaFuncSetAttribute(bin2q_kernel<T, M, S, WMODE, MINB, NT, UNR, OFS, RES, DEPTH, DIFF>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
     if (e != cudaSuccess) return e;
     int per_sm = 0;
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm,
-                                                      bin2q_kernel<T, M, S, WMODE, MINB, NT, UNR, OFS, RES, DEPTH>,
+                                                      bin2q_kernel<T, M, S, WMODE, MINB, NT, UNR, OFS, RES, DEPTH, DIFF>,
                                                       NT, C::SMEM) != cudaSuccess ||
         per_sm < 1) {
       cudaGetLastError();
@@ -880,7 +940,7 @@ cudaError_t launch_q(const Bin2QArgs& a, cudaStream_t s, int sms) {
   b.geo[3] = 0x5555555555555555ull & b.geo[0];
   b.geo[4] = (1ull << (2 * a.K)) - 1;
   b.geo[5] = 1ull << (2 * (a.ell - 1 - M));
-  bin2q_kernel<T, M, S, WMODE, MINB, NT, UNR, OFS, RES, DEPTH><<<(unsigned)blocks, NT, C::SMEM, s>>>(b);
+  bin2q_kernel<T, M, S, WMODE, MINB, NT, UNR, OFS, RES, DEPTH, DIFF><<<(unsigned)blocks, NT, C::SMEM, s>>>(b);
   return cudaGetLastError();
 }
 

@@ -93,6 +93,10 @@ struct lcsb {
   cudaGraphExec_t graph[kMaxGen];
   int graph_sweeps;
   int64_t sweeps_done;
+  // tracking sweeps (quarter table, kern_bin2q_diff.cu): set j = k & 1 of the reduction slots
+  // (red + kTrkSlot + 4 j: R_max, R_min of v_k - v_{k-1}, D = min(F(v_{k-1}) - v_{k-1})) holds
+  // the values of sweep k = trk_at[j]; -1 = none
+  int64_t trk_at[2];
   int64_t launches;
   double best_rho[2];
   int64_t best_sweep[2];
@@ -1082,6 +1086,7 @@ extern "C" int lcsb_reset(lcsb_t* h) {
   h->cur = 0;
   h->pcur = 0;
   h->sweeps_done = 0;
+  h->trk_at[0] = h->trk_at[1] = -1;
   h->best_rho[0] = h->best_rho[1] = 0.0;
   h->best_sweep[0] = h->best_sweep[1] = 0;
   return LCSB_OK;
@@ -1176,7 +1181,7 @@ static void fill_bin2q(const lcsb_t* h, Bin2QArgs* a, int in_slot, int out_slot)
   a->base = h->base;
 }
 
-static int enqueue_sweeps(lcsb_t* h, int64_t n, cudaStream_t s);
+static int enqueue_sweeps(lcsb_t* h, int64_t n, cudaStream_t s, int64_t track = 0);
 
 // Small tables are launch-latency bound: replay a captured graph of G sweeps (G a multiple of
 // the ring length, so the ring slots are the same before and after) instead of G launches.
@@ -1217,17 +1222,41 @@ static int sweep_graph(lcsb_t* h, cudaStream_t s) {
   return LCSB_OK;
 }
 
+// the tracking sweep applies (quarter table, plain storage)
+static bool can_track(const lcsb_t* h) { return h->kernel == 5 && !h->ost && !h->base; }
+constexpr int kTrkSlot = 8;  // red[8..15]: the two tracking sets (h->red holds 32 slots)
+static unsigned long long* trk_slots(lcsb_t* h, int64_t k) { return h->red + kTrkSlot + 4 * (k & 1); }
+
+static int sweep_impl(lcsb_t* h, int64_t n, int64_t track);
+
 extern "C" int lcsb_sweep(lcsb_t* h, int64_t n) {
   if (!h) return set_err(nullptr, LCSB_EINVAL, "handle is NULL");
   NvtxRange r("lcsb_sweep");
+  return sweep_impl(h, n, 0);
+}
+
+extern "C" int lcsb_sweep_ex(lcsb_t* h, int64_t n, uint32_t flags) {
+  if (!h) return set_err(nullptr, LCSB_EINVAL, "handle is NULL");
+  NvtxRange r("lcsb_sweep_ex");
+  if (flags & ~(uint32_t)LCSB_SWEEP_TRACK2) return set_err(h, LCSB_EINVAL, "unknown flags %u", flags);
+  const int64_t t = (flags & LCSB_SWEEP_TRACK2) == LCSB_SWEEP_TRACK2 ? 2 : (flags & 1u) ? 1 : 0;
+  return sweep_impl(h, n, t);
+}
+
+// n sweeps; the last min(track, n) of them are tracking sweeps where the layout has them
+static int sweep_impl(lcsb_t* h, int64_t n, int64_t track) {
   if (n < 0) return set_err(h, LCSB_EINVAL, "n must be >= 0");
+  if (track > n) track = n;
+  if (!can_track(h)) track = 0;
+  const int64_t total = n;
+  n -= track;  // the plain sweeps (graphs, ...) first, the tracked ones at the end
   CU(h, cudaSetDevice(h->device));
   {
     int rc = install_schedule(h, false);
     if (rc != LCSB_OK) return rc;
   }
   cudaStream_t s = (cudaStream_t)h->cfg.stream;
-  if (n > 0 && h->mode == MODE_PROCESS) {
+  if (total > 0 && h->mode == MODE_PROCESS) {
     // every rank is done with the tables (e.g. a rank-local lcsb_table read since the last
     // collective call) before anyone overwrites the oldest generation in the peers' memory
     int rc = barrier(h);
@@ -1250,11 +1279,12 @@ extern "C" int lcsb_sweep(lcsb_t* h, int64_t n) {
       n -= h->graph_sweeps;
     }
   }
-  return enqueue_sweeps(h, n, s);
+  return enqueue_sweeps(h, n + track, s, track);
 }
 
-static int enqueue_sweeps(lcsb_t* h, int64_t n, cudaStream_t s) {
+static int enqueue_sweeps(lcsb_t* h, int64_t n, cudaStream_t s, int64_t track) {
   for (int64_t it = 0; it < n; ++it) {
+    const bool trk = it >= n - track;  // a tracking sweep (can_track checked by the caller)
     NvtxRange r("sweep");
     if (h->qthread && !h->cap_capturing) {  // the schedule finished during a long call
       int rc = install_schedule(h, false);
@@ -1291,6 +1321,12 @@ static int enqueue_sweeps(lcsb_t* h, int64_t n, cudaStream_t s) {
         a.ost = h->ost;
         a.omin = &h->ost->mn[out];
       }
+      if (trk) {  // the tracking set of this sweep: R_max, R_min at -inf / +inf, D at +inf
+        a.red_out = trk_slots(h, h->sweeps_done + 1);
+        h->trk_at[(h->sweeps_done + 1) & 1] = -1;
+        e = launch_red_init(a.red_out, s, 6u);
+        h->launches += 1;
+      }
       // sharded (§9c): one launch per owned shard over its item list; the table pointers span
       // every shard (reads of other shards' windows and stores of their outputs go to peers)
       for (int k = h->first; k < h->first + h->nown && e == cudaSuccess; ++k) {
@@ -1300,7 +1336,8 @@ static int enqueue_sweeps(lcsb_t* h, int64_t n, cudaStream_t s) {
         }
         if (a.counter) e = cudaMemsetAsync(a.counter, 0, sizeof(unsigned long long), s);
         if (e == cudaSuccess)
-          e = launch_bin2q_sweep(a, h->cfg.dtype, h->qM, h->bin2q_variant, s, h->sms);
+          e = trk ? launch_bin2q_diff(a, h->cfg.dtype, h->qM, s, h->sms)
+                  : launch_bin2q_sweep(a, h->cfg.dtype, h->qM, h->bin2q_variant, s, h->sms);
         h->launches += 1;
         if (!h->vmm) break;
       }
@@ -1359,6 +1396,7 @@ static int enqueue_sweeps(lcsb_t* h, int64_t n, cudaStream_t s) {
     if (rc != LCSB_OK) return rc;
     h->cur = out;
     h->sweeps_done += 1;
+    if (trk) h->trk_at[h->sweeps_done & 1] = h->sweeps_done;
   }
   return LCSB_OK;
 }
@@ -1367,6 +1405,46 @@ static double bound_from(const lcsb_t* h, double rho) {
   if (h->form == LCSB_FORM_KS) return (double)h->cfg.d * rho;  // Eq. (lwrbound)
   return rho > 0.0 ? 2.0 * rho / (1.0 + rho) : 0.0;           // reading R10
 }
+
+// the tracking set of sweep k (process mode: reduced over the ranks first) -> v[0..2]
+static int read_trk(lcsb_t* h, int64_t k, unsigned long long* v) {
+  const int first = kTrkSlot + 4 * (int)(k & 1);
+  int rc = allreduce_slots(h, first, 3, (6u << first));
+  if (rc != LCSB_OK) return rc;
+  cudaStream_t s = (cudaStream_t)h->cfg.stream;
+  CU(h, cudaMemcpyAsync(v, h->red + first, 3 * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+                        s));
+  CU(h, cudaStreamSynchronize(s));
+  return LCSB_OK;
+}
+
+// E, the bound for both R and the best-so-far update (Alg. 2 lines 7-10) of the iterate after
+// `u_sweeps` sweeps, from R and max W
+static int finish_bound(lcsb_t* h, const double (&R)[2], const double (&Wm)[2], int64_t u_sweeps,
+                        lcsb_bound_t* out) {
+  double E[2], B[2];
+  for (int i = 0; i < 2; ++i) {
+    E[i] = Wm[i] > 0.0 ? Wm[i] : 0.0;  // E = max(0, max W)
+    B[i] = bound_from(h, R[i] - E[i]);
+    if (R[i] - E[i] >= h->best_rho[i]) {  // Alg. 2 line 8
+      h->best_rho[i] = R[i] - E[i];
+      h->best_sweep[i] = u_sweeps;
+    }
+  }
+  const int m = h->cfg.rmode;
+  out->R_max = R[0];
+  out->R_min = R[1];
+  out->E_at_Rmax = E[0];
+  out->E_at_Rmin = E[1];
+  out->bound_at_Rmax = B[0];
+  out->bound_at_Rmin = B[1];
+  out->bound = B[m];
+  out->best_bound = bound_from(h, h->best_rho[m]);
+  out->sweeps_done = u_sweeps;
+  out->best_sweep = h->best_sweep[m];
+  return LCSB_OK;
+}
+
 
 extern "C" int lcsb_bound(lcsb_t* h, lcsb_bound_t* out) {
   if (!h || !out) return set_err(h, LCSB_EINVAL, "NULL argument");
@@ -1385,6 +1463,9 @@ extern "C" int lcsb_bound(lcsb_t* h, lcsb_bound_t* out) {
   // E = max(0, max W) = max(0, R - D) for both R (reading R21).  Other kernels: the R
   // reduction, then the W pass at the known R.
   const bool one_pass = h->kernel == 5;
+  // the last sweep tracked R of this iterate (lcsb_sweep_ex): the pass needs only D, so it does
+  // not read v_{n-1} at all (reading R25)
+  const bool dpass = can_track(h) && h->trk_at[h->sweeps_done & 1] == h->sweeps_done;
   // integer offsets: v_n - v_{n-1} = s_n - s_{n-1} + (o_n - o_{n-1})  (reading R23)
   double cofs = 0.0;
   if (h->ost) {
@@ -1427,7 +1508,7 @@ extern "C" int lcsb_bound(lcsb_t* h, lcsb_bound_t* out) {
   } else if (h->kernel == 5) {
     Bin2QArgs a;
     fill_bin2q(h, &a, h->cur, -1);
-    a.prev = h->tabs[0][prev];
+    a.prev = dpass ? nullptr : h->tabs[0][prev];
     a.red_out = h->red;
     for (int k = h->first; k < h->first + h->nown; ++k) {  // sharded: each owned shard's items
       if (h->vmm) {
@@ -1472,9 +1553,18 @@ extern "C" int lcsb_bound(lcsb_t* h, lcsb_bound_t* out) {
     int rc = one_pass ? allreduce_slots(h, 0, 3, 6u) : allreduce_slots(h, 2, 2, 0u);
     if (rc != LCSB_OK) return rc;
   }
+  unsigned long long trk[4] = {0, 0, 0, 0};
+  if (dpass) {
+    int rc = read_trk(h, h->sweeps_done, trk);
+    if (rc != LCSB_OK) return rc;
+  }
   CU(h, cudaMemcpyAsync(h->red_host, h->red, kRedSlots * sizeof(unsigned long long),
                         cudaMemcpyDeviceToHost, s));
   CU(h, cudaStreamSynchronize(s));
+  if (dpass) {  // R of this iterate from its tracking sweep
+    h->red_host[0] = trk[0];
+    h->red_host[1] = trk[1];
+  }
   // (generic two-pass with offsets: red[0..1] already hold the shifted R)
   const double radd = (one_pass && h->ost) ? cofs : 0.0;
   const double R[2] = {ord_dec(h->red_host[0]) + radd, ord_dec(h->red_host[1]) + radd};
@@ -1484,27 +1574,41 @@ extern "C" int lcsb_bound(lcsb_t* h, lcsb_bound_t* out) {
     Wm[0] = R[0] - D;
     Wm[1] = R[1] - D;
   }
-  double E[2], B[2];
-  for (int i = 0; i < 2; ++i) {
-    E[i] = Wm[i] > 0.0 ? Wm[i] : 0.0;  // E = max(0, max W)
-    B[i] = bound_from(h, R[i] - E[i]);
-    if (R[i] - E[i] >= h->best_rho[i]) {  // Alg. 2 line 8
-      h->best_rho[i] = R[i] - E[i];
-      h->best_sweep[i] = h->sweeps_done;
-    }
+  return finish_bound(h, R, Wm, h->sweeps_done, out);
+}
+
+// n sweeps and the bound of the iterate BEFORE the last of them (reading R25): Alg. 2's W of
+// iterate u = v_{N-1} needs F(u,u), which the two-array form computes as sweep N anyway, so the
+// last two sweeps track (R of v_{N-1} against v_{N-2}; D = min(F(u,u) - u)) and no pass over the
+// table is added.  Layouts without tracking sweeps (and n = 1 after an untracked sweep): the
+// same result from sweeps, lcsb_bound and one more sweep.
+extern "C" int lcsb_sweep_bound(lcsb_t* h, int64_t n, lcsb_bound_t* out) {
+  if (!h || !out) return set_err(h, LCSB_EINVAL, "NULL argument");
+  NvtxRange r("lcsb_sweep_bound");
+  if (n < 1) return set_err(h, LCSB_EINVAL, "n must be >= 1");
+  const int64_t N = h->sweeps_done + n;
+  if (N - 1 < 1) return set_err(h, LCSB_ESTATE, "the bounded iterate needs at least one sweep");
+  if (h->base && N - 1 <= h->rebase_sweep)
+    return set_err(h, LCSB_ESTATE, "lcsb_bound needs a sweep after lcsb_rebase");
+  const bool fused = can_track(h) && (n >= 2 || h->trk_at[h->sweeps_done & 1] == h->sweeps_done);
+  if (!fused) {
+    int rc = sweep_impl(h, n - 1, 0);
+    if (rc == LCSB_OK) rc = lcsb_bound(h, out);
+    if (rc == LCSB_OK) rc = sweep_impl(h, 1, 0);
+    return rc;
   }
-  const int m = h->cfg.rmode;
-  out->R_max = R[0];
-  out->R_min = R[1];
-  out->E_at_Rmax = E[0];
-  out->E_at_Rmin = E[1];
-  out->bound_at_Rmax = B[0];
-  out->bound_at_Rmin = B[1];
-  out->bound = B[m];
-  out->best_bound = bound_from(h, h->best_rho[m]);
-  out->sweeps_done = h->sweeps_done;
-  out->best_sweep = h->best_sweep[m];
-  return LCSB_OK;
+  int rc = sweep_impl(h, n, 2);
+  if (rc != LCSB_OK) return rc;
+  if (h->trk_at[(N - 1) & 1] != N - 1 || h->trk_at[N & 1] != N)
+    return set_err(h, LCSB_ESTATE, "tracking sets missing");
+  unsigned long long tr[4], td[4];
+  rc = read_trk(h, N - 1, tr);
+  if (rc == LCSB_OK) rc = read_trk(h, N, td);
+  if (rc != LCSB_OK) return rc;
+  const double R[2] = {ord_dec(tr[0]), ord_dec(tr[1])};
+  const double D = ord_dec(td[2]);  // min(F(v_{N-1}) - v_{N-1})
+  const double Wm[2] = {R[0] - D, R[1] - D};  // max W = R - D (reading R21)
+  return finish_bound(h, R, Wm, N - 1, out);
 }
 
 static int readout(lcsb_t* h, int which, uint64_t first, uint64_t count, const uint64_t* host_idx,
@@ -1610,6 +1714,7 @@ extern "C" int lcsb_rebase(lcsb_t* h) {
       h->graph[i] = nullptr;
     }
   h->rebase_sweep = h->sweeps_done;
+  h->trk_at[0] = h->trk_at[1] = -1;
   return LCSB_OK;
 }
 
@@ -1757,6 +1862,7 @@ extern "C" int lcsb_load(lcsb_t* h, const char* path) {
   h->best_sweep[0] = c.best_sweep[0];
   h->best_sweep[1] = c.best_sweep[1];
   h->rebase_sweep = c.rebase_sweep;
+  h->trk_at[0] = h->trk_at[1] = -1;
   return LCSB_OK;
 }
 

@@ -404,6 +404,9 @@ cudaError_t launch_bin2q_sweep(const Bin2QArgs& a, int dtype, int M, int variant
                                int sms);
 int bin2q_variant_m(int dtype, int variant);
 cudaError_t launch_bin2q_wpass(const Bin2QArgs& a, int dtype, int M, cudaStream_t s, int sms);
+// the tracking sweep (kern_bin2q_diff.cu): the plain sweep that also reduces, against the table it
+// reads at every stored output, R of the iterate it writes and D of the one it reads (red_out[0..2])
+cudaError_t launch_bin2q_diff(const Bin2QArgs& a, int dtype, int M, cudaStream_t s, int sms);
 // the sweep with integer offsets (a.ost) or residual storage (a.base): kern_bin2q_ext.cu
 cudaError_t launch_bin2q_sweep_ext(const Bin2QArgs& a, int dtype, int M, cudaStream_t s, int sms);
 cudaError_t launch_q4_sweep(const Q4Args& a, int dtype, cudaStream_t s, int sms);

@@ -52,6 +52,10 @@ class LcsbConfig(ctypes.Structure):
                 ("comm", ctypes.POINTER(LcsbCommHooks)), ("offset_policy", ctypes.c_int32)]
 
 
+# lcsb_sweep_ex flags (include/lcsb.h)
+SWEEP_TRACK, SWEEP_TRACK2 = 1, 3
+
+
 class LcsbBound(ctypes.Structure):
     _fields_ = [("R_max", ctypes.c_double), ("R_min", ctypes.c_double),
                 ("E_at_Rmax", ctypes.c_double), ("E_at_Rmin", ctypes.c_double),
@@ -62,7 +66,7 @@ class LcsbBound(ctypes.Structure):
 
 # every symbol include/lcsb.h declares (checked by tests/test_abi.py)
 EXPORTS = ["lcsb_config_init", "lcsb_required_bytes", "lcsb_create", "lcsb_create_ex",
-           "lcsb_reset", "lcsb_sweep", "lcsb_bound", "lcsb_table", "lcsb_table_gather",
+           "lcsb_reset", "lcsb_sweep", "lcsb_sweep_ex", "lcsb_bound", "lcsb_sweep_bound", "lcsb_table", "lcsb_table_gather",
            "lcsb_nccl_unique_id", "lcsb_shard_locate", "lcsb_shard_locate_sigma4",
            "lcsb_quarter_locate", "lcsb_quarter_shard_plan", "lcsb_ready", "lcsb_rebase", "lcsb_save", "lcsb_load",
            "lcsb_sweeps_done",
@@ -105,6 +109,10 @@ def load_library():
     lib.lcsb_sweep.restype = ctypes.c_int
     lib.lcsb_bound.argtypes = [P, ctypes.POINTER(LcsbBound)]
     lib.lcsb_bound.restype = ctypes.c_int
+    lib.lcsb_sweep_ex.argtypes = [P, ctypes.c_int64, ctypes.c_uint32]
+    lib.lcsb_sweep_ex.restype = ctypes.c_int
+    lib.lcsb_sweep_bound.argtypes = [P, ctypes.c_int64, ctypes.POINTER(LcsbBound)]
+    lib.lcsb_sweep_bound.restype = ctypes.c_int
     lib.lcsb_table.argtypes = [P, ctypes.c_int32, ctypes.c_uint64, ctypes.c_uint64, P]
     lib.lcsb_table.restype = ctypes.c_int
     lib.lcsb_table_gather.argtypes = [P, ctypes.c_int32, P, ctypes.c_uint64, P]
@@ -298,6 +306,16 @@ class Lcsb:
         _check(self._lib.lcsb_bound(self._h, ctypes.byref(out)), self._h)
         return BoundResult(**{f: getattr(out, f) for f, _ in LcsbBound._fields_})
 
+    def sweep_ex(self, n: int = 1, flags: int = SWEEP_TRACK):
+        """lcsb_sweep_ex: n sweeps, the last one (SWEEP_TRACK) or two (SWEEP_TRACK2) tracking"""
+        _check(self._lib.lcsb_sweep_ex(self._h, int(n), int(flags)), self._h)
+
+    def sweep_bound(self, n: int) -> BoundResult:
+        """lcsb_sweep_bound: n sweeps and the bound of the iterate before the last of them"""
+        out = LcsbBound()
+        _check(self._lib.lcsb_sweep_bound(self._h, int(n), ctypes.byref(out)), self._h)
+        return BoundResult(**{f: getattr(out, f) for f, _ in LcsbBound._fields_})
+
     def table(self, which: int = 0, first: int = 0, count: int | None = None) -> np.ndarray:
         if count is None:
             count = self.num_states - first
@@ -430,6 +448,14 @@ def lcsb_sweep(h: Lcsb, n: int = 1):
 
 def lcsb_bound(h: Lcsb) -> BoundResult:
     return h.bound()
+
+
+def lcsb_sweep_ex(h: Lcsb, n: int = 1, flags: int = 1):
+    h.sweep_ex(n, flags)
+
+
+def lcsb_sweep_bound(h: Lcsb, n: int) -> BoundResult:
+    return h.sweep_bound(n)
 
 
 def lcsb_table(h: Lcsb, which=0, first=0, count=None) -> np.ndarray:
