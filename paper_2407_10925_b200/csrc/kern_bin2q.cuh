@@ -357,6 +357,44 @@ __device__ __forceinline__ void pair_quads_f32(const T* bw, const T* bp, const T
   }
 }
 
+// one Q0 row of the fp32 bound pass / tracking sweep (pair_quads_w32), with u (and v_prev) at
+// its output loaded up front by the caller: (fu, fpv) at the row run's entry when `of` is stored,
+// else (mu, mpv) at the mirror run's (the mirror of row r sits at half - 1 - r).  When both runs
+// are stored (tail-complement-fixed blocks) the mirror's entries are read here directly.
+template <uint32_t TT, int MODE, bool DIFF>
+__device__ __forceinline__ void q0_rows_w(const double (&G)[4], uint32_t r, uint64_t of,
+                                          uint64_t om, float fu, float fpv, float mu, float mpv,
+                                          const float* src, const float* prev, float* dst,
+                                          BAcc& ba) {
+  const double v0 = G[comp<MODE>(0)], v1 = G[comp<MODE>(1)], v2 = G[comp<MODE>(2)],
+               v3 = G[comp<MODE>(3)];
+  if (of != kNone) {
+    const double f = q0_val(v0, v1, v2, v3);
+    if constexpr (DIFF) {
+      const float st = (float)f;
+      st_out(dst + of + r, st);
+      dacc((double)fu, f, (double)st, ba);
+    } else {
+      bacc((double)fu, prev ? (double)fpv : 0.0, f, ba);
+    }
+  }
+  if (om != kNone) {
+    const uint32_t rm = TT / 2 - 1 - r;
+    if (of != kNone) {  // both runs stored: the caller loaded the row run's entries
+      mu = __ldcs(src + om + rm);
+      if (!DIFF && prev) mpv = __ldcs(prev + om + rm);
+    }
+    const double f = q0_val(v3, v2, v1, v0);
+    if constexpr (DIFF) {
+      const float st = (float)f;
+      st_out(dst + om + rm, st);
+      dacc((double)mu, f, (double)st, ba);
+    } else {
+      bacc((double)mu, prev ? (double)mpv : 0.0, f, ba);
+    }
+  }
+}
+
 // fp32 storage, bound pass: the arithmetic of pair_quads<float, ..., WMODE> (every value and
 // every accumulated u, v_prev, F(u,u) identical; max / min are order-free) in an order that keeps
 // fewer values live -- the x window's pair sums and Q0 rows are finished before the psi window's
@@ -373,16 +411,33 @@ __device__ __forceinline__ void pair_quads_w32(const float* bw, const float* bp,
   const uint64_t of = meta[3], om = meta[4], opf = meta[5], opm = meta[6];
   const bool rows_x = of != kNone || om != kNone;
   const bool rows_p = !self && (opf != kNone || opm != kNone);
+  const bool rdp = !DIFF && prev;  // v_prev is read (the one-pass bound; not the D-only pass)
   for (uint32_t qd = threadIdx.x; qd < TT / 4; qd += kThreads) {
     const uint32_t o0 = 4 * qd;
     const uint32_t g = 2 * pairswap32(o0), u = 2 * (TT - 4 - o0);
     const uint32_t qb = pairswap32(~o0 & (TT - 1) & ~3u);
-    // u and v_prev at the quad's stored Q1 outputs first (latency overlaps the rest)
+    const uint32_t rx = g >> 2, rp = u >> 2;  // the first of the two rows of each window (even)
+    // every global load of the quad first, so their latencies overlap each other and the window
+    // arithmetic: u and v_prev at the stored Q1 outputs (4 consecutive entries) and at the two
+    // rows of each window (2 consecutive entries of the row run, or of the mirror run reversed:
+    // mirror of row r at half - 1 - r)
     float uu[4] = {0, 0, 0, 0}, pp[4] = {0, 0, 0, 0};
     const uint64_t q = oQ1 != kNone ? oQ1 + o0 : (oQ1p != kNone ? oQ1p + qb : kNone);
     if (q != kNone) {
       ld4s(src + q, uu);
-      if (!DIFF && prev) ld4s(prev + q, pp);  // null: the D-only pass (R tracked by the last sweep)
+      if (rdp) ld4s(prev + q, pp);
+    }
+    const uint64_t xo = of != kNone ? of + rx : (om != kNone ? om + (TT / 2 - 2 - rx) : kNone);
+    const uint64_t po = !rows_p ? kNone
+                                : (opf != kNone ? opf + rp : opm + (TT / 2 - 2 - rp));
+    float2 ux = make_float2(0.f, 0.f), px = ux, up = ux, pq = ux;
+    if (xo != kNone) {
+      ux = __ldcs(reinterpret_cast<const float2*>(src + xo));
+      if (rdp) px = __ldcs(reinterpret_cast<const float2*>(prev + xo));
+    }
+    if (po != kNone) {
+      up = __ldcs(reinterpret_cast<const float2*>(src + po));
+      if (rdp) pq = __ldcs(reinterpret_cast<const float2*>(prev + po));
     }
     const bool sx = (qd >> SX) & 1u, sp = (qd >> SP) & 1u;
     constexpr uint32_t c0 = comp<MW>(0), c1 = comp<MW>(1), c2 = comp<MW>(2), c3 = comp<MW>(3);
@@ -400,10 +455,9 @@ __device__ __forceinline__ void pair_quads_w32(const float* bw, const float* bp,
       if (rows_x) {
         double G[4];
         widen4(a, G);
-        q0_group<float, MW, !DIFF, false, false, DIFF>(G, g >> 2, TT / 2, src, dst, of, om, prev, ba);
+        q0_rows_w<TT, MW, DIFF>(G, rx, of, om, ux.x, px.x, ux.y, px.y, src, prev, dst, ba);
         widen4(b, G);
-        q0_group<float, MW, !DIFF, false, false, DIFF>(G, (g >> 2) + 1, TT / 2, src, dst, of, om, prev,
-                                                     ba);
+        q0_rows_w<TT, MW, DIFF>(G, rx + 1, of, om, ux.y, px.y, ux.x, px.x, src, prev, dst, ba);
       }
     }
     double tq[4];
@@ -419,10 +473,10 @@ __device__ __forceinline__ void pair_quads_w32(const float* bw, const float* bp,
       if (rows_p) {
         double G[4];
         widen4(ap, G);
-        q0_group<float, MP, !DIFF, false, false, DIFF>(G, u >> 2, TT / 2, src, dst, opf, opm, prev, ba);
+        q0_rows_w<TT, MP, DIFF>(G, rp, opf, opm, up.x, pq.x, up.y, pq.y, src, prev, dst, ba);
         widen4(bq, G);
-        q0_group<float, MP, !DIFF, false, false, DIFF>(G, (u >> 2) + 1, TT / 2, src, dst, opf, opm, prev,
-                                                     ba);
+        q0_rows_w<TT, MP, DIFF>(G, rp + 1, opf, opm, up.y, pq.y, up.x, pq.x, src, prev, dst,
+                                ba);
       }
     }
     double v[4];
