@@ -807,6 +807,10 @@ extern "C" int lcsb_create_ex(const lcsb_config* cfg, lcsb_t** out) {
   h->cfg = *cfg;
   h->device = dev;
   cudaDeviceGetAttribute(&h->sms, cudaDevAttrMultiProcessorCount, dev);
+  if (const char* e = getenv("LCSB_SMS")) {  // A/B only: persistent grids on fewer SMs
+    const int k = atoi(e);
+    if (k > 0 && k < h->sms) h->sms = k;
+  }
   h->form = p.form;
   h->symmetric = p.symmetric;
   h->kernel = p.kernel;
