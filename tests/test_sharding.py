@@ -166,6 +166,25 @@ def test_virtual_shards_bitwise_equal_unsharded(ell, shards, dtype):
         ba, bb = a.bound(), b.bound()
         assert (ba.R_max, ba.R_min, ba.E_at_Rmax, ba.E_at_Rmin) == \
                (bb.R_max, bb.R_min, bb.E_at_Rmax, bb.E_at_Rmin)
+    # tracking sweeps (reading R25) on the shards: the fused bound and the D-only pass
+    a.reset()
+    b.reset()
+    for h in (a, b):
+        h.sweep(5)
+        h.bound()
+        h.sweep(1)
+    fa, fb = a.sweep_bound(4), b.sweep_bound(4)
+    a.sweep_ex(3, 1)
+    b.sweep_ex(3, 1)
+    da, db = a.bound(), b.bound()
+    for x, y in ((fa, fb), (da, db)):
+        assert (x.R_max, x.R_min, x.E_at_Rmax, x.E_at_Rmin, x.best_bound, x.sweeps_done) == \
+               (y.R_max, y.R_min, y.E_at_Rmax, y.E_at_Rmin, y.best_bound, y.sweeps_done)
+    assert np.array_equal(a.table(0), b.table(0))
+    a.reset()
+    b.reset()
+    a.sweep(12)
+    b.sweep(12)
     if ell <= 9:
         ref = fo.feasible_triplet(2, 2, ell, 12, form="two_array", dtype=dtype)
         tab = b.table(0)
@@ -608,6 +627,13 @@ def _pm_quarter_worker(rank, world, port, out_dir, ell, K, dtype):
     h.sweep(2)
     if rank == 0:
         out["reset"] = h.table(0)
+    # tracking sweeps across processes (reading R25): the tracking sets are reduced over ranks
+    h.reset()
+    fb = h.sweep_bound(5)
+    h.sweep_ex(3, 1)
+    db = h.bound()
+    if rank == 0:
+        out["trk"] = (fb, db, h.table(0))
     dist.barrier()
     h.destroy()
     if rank == 0:
@@ -623,6 +649,16 @@ def _pm_quarter_worker(rank, world, port, out_dir, ell, K, dtype):
         ref.reset()
         ref.sweep(2)
         ok.append(np.array_equal(out["reset"], ref.table(0)))
+        ref.reset()
+        ref.sweep(4)
+        r4 = ref.bound()
+        ref.sweep(4)
+        r8 = ref.bound()
+        fb, db, t8 = out["trk"]
+        for x, y in ((fb, r4), (db, r8)):
+            ok.append((x.R_max, x.R_min, x.E_at_Rmax, x.E_at_Rmin, x.best_bound, x.sweeps_done) ==
+                      (y.R_max, y.R_min, y.E_at_Rmax, y.E_at_Rmin, y.best_bound, y.sweeps_done))
+        ok.append(np.array_equal(t8, ref.table(0)))
         ref.destroy()
         np.save(os.path.join(out_dir, "pmq.npy"), np.array(ok))
     dist.destroy_process_group()
