@@ -4,12 +4,25 @@
 namespace lcsbk {
 namespace {
 
+static bool qp_on() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("LCSB_QP");
+    v = e ? atoi(e) : 1;
+  }
+  return v != 0;
+}
+
 // the plain sweep (fp32 Q1 path) for the handle's tile 4^M
 template <bool WMODE>
 cudaError_t dispatch_q(const Bin2QArgs& a, int dtype, int M, cudaStream_t s, int sms) {
   if (dtype == LCSB_F32) {
     switch (M) {
       case 6:  // A/B: variant 10; with a work counter the producer pipelined three deep
+        if (!WMODE && qp_on()) {  // the quarter-pipelined sweep (LCSB_QP=0: bin2q_kernel)
+          if (a.K < 7) break;
+          return q_dynamic(a, 6) ? launch_qp<3>(a, s, sms) : launch_qp<1>(a, s, sms);
+        }
         if (!WMODE && q_dynamic(a, 6))
           return launch_q<float, 6, 1, WMODE, 3, kThreads, 1, false, false, 3>(a, s, sms);
         return launch_q<float, 6, 1, WMODE, 3>(a, s, sms);

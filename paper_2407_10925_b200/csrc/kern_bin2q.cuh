@@ -296,65 +296,113 @@ __device__ __forceinline__ void q0_group(const double (&G)[4], uint32_t r, uint3
   }
 }
 
-// fp32 storage, sweep: the Q1 values in fp32 (see the comment inside), the rest as pair_quads
-template <typename T, uint32_t TT, int MW, int MP>
-__device__ __forceinline__ void pair_quads_f32(const T* bw, const T* bp, const T* src, T* dst,
-                                               const uint64_t* meta, bool self) {
+// smem offset of window entry P (the window's smem layout, gbase) inside the quarter buffer of
+// the quarter-pipelined sweep (bin2q_qp_kernel): modes 0 / 3 keep contiguous quarters (P's top
+// two bits fixed), the pairswapped modes fix bits 12 and 10 of P (two runs of 1024; bit 11 -> 10)
+template <uint32_t TT, int MODE>
+__device__ __forceinline__ uint32_t qloc(uint32_t P) {
+  static_assert(TT == 4096, "quarter buffers for tiles of 4^6");
+  if (MODE == 0 || MODE == 3) return P & 2047u;
+  return ((P >> 1) & 1024u) | (P & 1023u);
+}
+
+// fp32 storage, sweep: one quad of Q1 outputs o0..o0+3 (o0 = 4 qd) of the tile pair, its Q0 rows;
+// the Q1 values in fp32 (see the comment inside).  QP: bw / bp are the quarter buffers of the
+// quad's quarter (bin2q_qp_kernel) instead of the whole windows.
+// an item's stored output runs (meta[1..6]), read once per item into registers (the stores to
+// global memory between the quads would otherwise make the compiler re-read them from shared
+// memory, as it cannot rule out aliasing)
+struct QRuns {
+  float *pQ1, *pQ1p, *pf, *pm, *ppf, *ppm;  // run starts in the output table (nullptr: not stored)
+};
+__device__ __forceinline__ QRuns qruns(const uint64_t* meta, bool self, float* dst) {
+  QRuns r;
+  auto ptr = [&](uint64_t o) { return o != kNone ? dst + o : nullptr; };
+  r.pQ1 = ptr(meta[1]);
+  r.pQ1p = ptr(meta[2]);
+  r.pf = ptr(meta[3]);
+  r.pm = ptr(meta[4]);
+  r.ppf = self ? nullptr : ptr(meta[5]);
+  r.ppm = self ? nullptr : ptr(meta[6]);
+  return r;
+}
+// the stored Q0 outputs of one row (row run at pf, mirror run at pm), as q0_group's sweep branch
+template <uint32_t TT, int MODE>
+__device__ __forceinline__ void q0_store_f32(const double (&G)[4], uint32_t r, float* pf,
+                                             float* pm) {
+  const double v0 = G[comp<MODE>(0)], v1 = G[comp<MODE>(1)], v2 = G[comp<MODE>(2)],
+               v3 = G[comp<MODE>(3)];
+  if (pf) st_out(pf + r, (float)q0_val(v0, v1, v2, v3));
+  if (pm) st_out(pm + (TT / 2 - 1 - r), (float)q0_val(v3, v2, v1, v0));
+}
+
+template <typename T, uint32_t TT, int MW, int MP, bool QP = false>
+__device__ __forceinline__ void quad_f32(const T* bw, const T* bp, const QRuns& R, uint32_t qd) {
+  static_assert(sizeof(T) == 4, "fp32 storage");
   constexpr uint32_t SX = (MW == 0 || MW == 3) ? 2 : 0, SP = (MP == 0 || MP == 3) ? 2 : 1;
-  const uint64_t oQ1 = meta[1], oQ1p = meta[2];
-  const uint64_t of = meta[3], om = meta[4], opf = meta[5], opm = meta[6];
-  const bool rows_x = of != kNone || om != kNone;
-  const bool rows_p = !self && (opf != kNone || opm != kNone);
-  BAcc ba;  // unused by the sweep
   // fp32 storage, sweep: the Q1 value round32(max(0.5 (x0 + x1), 0.5 (y0 + y1))) of fp64
   // arithmetic equals the same expression evaluated in fp32 (a two-term fp32 sum is exact in
   // fp64 or off by less than half an fp32 ulp, so no double rounding; halving and max commute
   // with rounding), so Q1 stays in fp32; only the Q0 rows that are stored widen to fp64 (their
   // four-term sums are not exact in fp32).
-  for (uint32_t qd = threadIdx.x; qd < TT / 4; qd += blockDim.x) {
-    const uint32_t o0 = 4 * qd;
-    const uint32_t g = 2 * pairswap32(o0), u = 2 * (TT - 4 - o0);
-    // X1 / X2 hold the groups A (row g/4) and B (row g/4 + 1) in a per-thread order (sx: B
-    // first) that keeps the 128-bit smem loads conflict-free; the pair sums are formed per loaded
-    // group and only they are put back in A/B order (4 selects instead of 8 per window)
-    float X1[4], X2[4], P1[4], P2[4];
-    const bool sx = (qd >> SX) & 1u, sp = (qd >> SP) & 1u;
-    ld4r(reinterpret_cast<const float*>(bw) + gbase<TT, MW>(sx ? g + 4 : g), X1);
-    ld4r(reinterpret_cast<const float*>(bw) + gbase<TT, MW>(sx ? g : g + 4), X2);
-    ld4r(reinterpret_cast<const float*>(bp) + gbase<TT, MP>(sp ? u + 4 : u), P1);
-    ld4r(reinterpret_cast<const float*>(bp) + gbase<TT, MP>(sp ? u : u + 4), P2);
-    constexpr uint32_t c0 = comp<MW>(0), c1 = comp<MW>(1), c2 = comp<MW>(2), c3 = comp<MW>(3);
-    constexpr uint32_t d0 = comp<MP>(0), d1 = comp<MP>(1), d2 = comp<MP>(2), d3 = comp<MP>(3);
-    const float x1l = 0.5f * (X1[c0] + X1[c1]), x1h = 0.5f * (X1[c2] + X1[c3]);
-    const float x2l = 0.5f * (X2[c0] + X2[c1]), x2h = 0.5f * (X2[c2] + X2[c3]);
-    const float p1l = 0.5f * (P1[d0] + P1[d1]), p1h = 0.5f * (P1[d2] + P1[d3]);
-    const float p2l = 0.5f * (P2[d0] + P2[d1]), p2h = 0.5f * (P2[d2] + P2[d3]);
-    // bx = {A lo, B lo, A hi, B hi}; bq = {Bp hi, Bp lo, Ap hi, Ap lo}
-    const float bx[4] = {sx ? x2l : x1l, sx ? x1l : x2l, sx ? x2h : x1h, sx ? x1h : x2h};
-    const float bq[4] = {sp ? p1h : p2h, sp ? p1l : p2l, sp ? p2h : p1h, sp ? p2l : p1l};
-    float v[4];
+  const uint32_t o0 = 4 * qd;
+  const uint32_t g = 2 * pairswap32(o0), u = 2 * (TT - 4 - o0);
+  auto ax = [&](uint32_t gg) -> uint32_t {
+    if constexpr (QP) return qloc<TT, MW>(gbase<TT, MW>(gg));
+    else return gbase<TT, MW>(gg);
+  };
+  auto ap = [&](uint32_t gg) -> uint32_t {
+    if constexpr (QP) return qloc<TT, MP>(gbase<TT, MP>(gg));
+    else return gbase<TT, MP>(gg);
+  };
+  // X1 / X2 hold the groups A (row g/4) and B (row g/4 + 1) in a per-thread order (sx: B
+  // first) that keeps the 128-bit smem loads conflict-free; the pair sums are formed per loaded
+  // group and only they are put back in A/B order (4 selects instead of 8 per window)
+  float X1[4], X2[4], P1[4], P2[4];
+  const bool sx = (qd >> SX) & 1u, sp = (qd >> SP) & 1u;
+  ld4r(reinterpret_cast<const float*>(bw) + ax(sx ? g + 4 : g), X1);
+  ld4r(reinterpret_cast<const float*>(bw) + ax(sx ? g : g + 4), X2);
+  ld4r(reinterpret_cast<const float*>(bp) + ap(sp ? u + 4 : u), P1);
+  ld4r(reinterpret_cast<const float*>(bp) + ap(sp ? u : u + 4), P2);
+  constexpr uint32_t c0 = comp<MW>(0), c1 = comp<MW>(1), c2 = comp<MW>(2), c3 = comp<MW>(3);
+  constexpr uint32_t d0 = comp<MP>(0), d1 = comp<MP>(1), d2 = comp<MP>(2), d3 = comp<MP>(3);
+  const float x1l = 0.5f * (X1[c0] + X1[c1]), x1h = 0.5f * (X1[c2] + X1[c3]);
+  const float x2l = 0.5f * (X2[c0] + X2[c1]), x2h = 0.5f * (X2[c2] + X2[c3]);
+  const float p1l = 0.5f * (P1[d0] + P1[d1]), p1h = 0.5f * (P1[d2] + P1[d3]);
+  const float p2l = 0.5f * (P2[d0] + P2[d1]), p2h = 0.5f * (P2[d2] + P2[d3]);
+  // bx = {A lo, B lo, A hi, B hi}; bq = {Bp hi, Bp lo, Ap hi, Ap lo}
+  const float bx[4] = {sx ? x2l : x1l, sx ? x1l : x2l, sx ? x2h : x1h, sx ? x1h : x2h};
+  const float bq[4] = {sp ? p1h : p2h, sp ? p1l : p2l, sp ? p2h : p1h, sp ? p2l : p1l};
+  float v[4];
 #pragma unroll
-    for (int k = 0; k < 4; ++k) v[k] = fmaxf(bx[k], bq[k]);  // one FMNMX (no NaN, no -0)
-    const uint32_t qb = pairswap32(~o0 & (TT - 1) & ~3u);
-    float* df = reinterpret_cast<float*>(dst);
-    if (oQ1 != kNone)
-      st_out(reinterpret_cast<float4*>(df + oQ1 + o0), make_float4(v[0], v[1], v[2], v[3]));
-    if (oQ1p != kNone)
-      st_out(reinterpret_cast<float4*>(df + oQ1p + qb), make_float4(v[3], v[1], v[2], v[0]));
-    double G[4];
-    if (rows_x) {  // X1 is row g/4 + sx, X2 row g/4 + 1 - sx
-      widen4(X1, G);
-      q0_group<T, MW, false>(G, (g >> 2) + sx, TT / 2, src, dst, of, om, nullptr, ba);
-      widen4(X2, G);
-      q0_group<T, MW, false>(G, (g >> 2) + 1 - sx, TT / 2, src, dst, of, om, nullptr, ba);
-    }
-    if (rows_p) {
-      widen4(P1, G);
-      q0_group<T, MP, false>(G, (u >> 2) + sp, TT / 2, src, dst, opf, opm, nullptr, ba);
-      widen4(P2, G);
-      q0_group<T, MP, false>(G, (u >> 2) + 1 - sp, TT / 2, src, dst, opf, opm, nullptr, ba);
-    }
+  for (int k = 0; k < 4; ++k) v[k] = fmaxf(bx[k], bq[k]);  // one FMNMX (no NaN, no -0)
+  const uint32_t qb = pairswap32(~o0 & (TT - 1) & ~3u);
+  if (R.pQ1) st_out(reinterpret_cast<float4*>(R.pQ1 + o0), make_float4(v[0], v[1], v[2], v[3]));
+  if (R.pQ1p)
+    st_out(reinterpret_cast<float4*>(R.pQ1p + qb), make_float4(v[3], v[1], v[2], v[0]));
+  double G[4];
+  if (R.pf || R.pm) {  // X1 is row g/4 + sx, X2 row g/4 + 1 - sx
+    widen4(X1, G);
+    q0_store_f32<TT, MW>(G, (g >> 2) + sx, R.pf, R.pm);
+    widen4(X2, G);
+    q0_store_f32<TT, MW>(G, (g >> 2) + 1 - sx, R.pf, R.pm);
   }
+  if (R.ppf || R.ppm) {
+    widen4(P1, G);
+    q0_store_f32<TT, MP>(G, (u >> 2) + sp, R.ppf, R.ppm);
+    widen4(P2, G);
+    q0_store_f32<TT, MP>(G, (u >> 2) + 1 - sp, R.ppf, R.ppm);
+  }
+}
+
+// fp32 storage, sweep: every quad of the tile pair (the whole windows in the stage)
+template <typename T, uint32_t TT, int MW, int MP>
+__device__ __forceinline__ void pair_quads_f32(const T* bw, const T* bp, const T* src, T* dst,
+                                               const uint64_t* meta, bool self) {
+  (void)src;
+  const QRuns R = qruns(meta, self, reinterpret_cast<float*>(dst));
+  for (uint32_t qd = threadIdx.x; qd < TT / 4; qd += blockDim.x)
+    quad_f32<T, TT, MW, MP>(bw, bp, R, qd);
 }
 
 // one Q0 row of the fp32 bound pass / tracking sweep (pair_quads_w32), with u (and v_prev) at
@@ -955,6 +1003,271 @@ __global__ void __launch_bounds__(NT, MINB) bin2q_kernel(Bin2QArgs a) {
   }
   if (WMODE || DIFF) block_red3_to(ba.rmax, ba.rmin, ba.dmin, a.red_out);
   if (OFS && !WMODE) block_min_to(ba.rmin, a.omin);
+}
+
+// ---- quarter-pipelined fp32 sweep (tiles of 4^6, round 2).  In bin2q_kernel a CTA's single
+// 64 KB stage is refilled only after all four of its quads per thread are done, so each CTA
+// alternates between waiting for its windows and computing; when the SM clock drops (the board's
+// power cap) the computing share grows and fewer bytes are in flight.  Here the
+// stage is four 16 KB quarter buffers: quad qd = tid + 256 q of every thread reads only logical
+// quarter swap2(q) of the x window and quarter 3 - q of the psi window (g = 2 pairswap(4 qd),
+// u = 2 (TT - 4 - 4 qd)), so quarter q of the NEXT item is loaded as soon as all threads are past
+// quad q of the current one -- loads stay in flight while the CTA computes.  Values, stores and
+// item order are those of bin2q_kernel (bit-identical tables).
+struct QPGeo {
+  static constexpr uint32_t TT = 4096, Q = 2048;  // Q1 outputs per tile; entries per window quarter
+};
+// thread 0: the global start of a window's loaded layout (qissue's TMA sources)
+__device__ __forceinline__ const float* qp_wstart(const QGeo& g, const float* src, uint32_t m,
+                                                  uint64_t w) {
+  constexpr uint64_t TT = QPGeo::TT;
+  const float* blk = src + ((uint64_t)(m >> 2) << (2 * g.K));
+  const uint64_t e = w & g.kmask;
+  if ((m & 3u) == 0) return blk + e;
+  if ((m & 3u) == 3u) return blk + ((~e & g.kmask) & ~(2 * TT - 1));
+  const uint64_t f = ((m & 3u) == 1u) ? pairswap(e) : pairswap(~e & g.kmask);
+  return blk + ((f & ~(4 * TT - 1)) | (f & TT));
+}
+// thread 0: logical quarter L of one window (mode m, loaded layout starting at gs) into its
+// quarter buffer (qloc's layout): modes 0 / 3 one contiguous 8 KB run (mode 3 reversed: physical
+// quarter 3 - L); pairswapped modes two 4 KB runs (physical bits 12 and 10 fixed)
+__device__ __forceinline__ void qp_issue_win(float* dst, const float* gs, uint32_t m, uint32_t L,
+                                             uint64_t* bar) {
+  constexpr uint32_t TT = QPGeo::TT, Q = QPGeo::Q;
+  if (m == 0u) {
+    tma_load_1d(dst, gs + (size_t)Q * L, Q * 4u, bar);
+  } else if (m == 3u) {
+    tma_load_1d(dst, gs + (size_t)Q * (3u - L), Q * 4u, bar);
+  } else {
+    const uint32_t Lw = (m == 1u) ? L : 3u - L;  // psi reads w = ~(g + 3): quarter 3 - L
+    const float* b = gs + (size_t)(Lw >> 1) * 2 * TT + (Lw & 1u) * 1024u;
+    tma_load_1d(dst, b, 1024u * 4u, bar);
+    tma_load_1d(dst + 1024, b + 2048, 1024u * 4u, bar);
+  }
+}
+constexpr int kQPMeta = 10;  // per item: [0] modes, [1..6] runs, [7] end, [8] / [9] window starts
+
+// LCSB_QP_SPIN (A/B): plain probe loops instead of the suspend-hint waits
+#ifdef LCSB_QP_SPIN
+#define QP_WAIT mbar_wait
+#else
+#define QP_WAIT mbar_wait_sleep
+#endif
+// the consumer side of one item of bin2q_qp_kernel: its four quarters in order, each after its
+// buffer has landed (full[q]); each warp then releases the buffer (empty[q])
+template <int MW, int MP>
+__device__ __forceinline__ void qp_item(const float* qbuf, uint64_t* full, uint64_t* empty,
+                                        uint32_t parity, const float* src, float* dst,
+                                        const uint64_t* meta, bool self, uint32_t tid, int lane) {
+  constexpr uint32_t TT = QPGeo::TT, Q = QPGeo::Q;
+  (void)src;
+  const QRuns R = qruns(meta, self, dst);
+#pragma unroll 1
+  for (int q = 0; q < 4; ++q) {
+    if (q) QP_WAIT(&full[q], parity);
+    const float* bw = qbuf + (size_t)(2 * q) * Q;
+    quad_f32<float, TT, MW, MP, true>(bw, bw + Q, R, tid + kThreads * (uint32_t)q);
+    __syncwarp();  // the warp's reads of buffer q are done
+    if (lane == 0) mbar_arrive(&empty[q]);
+  }
+}
+
+// warp-specialised: warps 0-7 consume (one quad per thread per quarter), warp 8 (one lane)
+// produces -- it waits on empty[q] (all 8 consumer warps past quarter q of the previous item)
+// and refills buffer q with the next item's quarter, so no CTA-wide barrier stalls the loop
+constexpr int kQPThreads = kThreads + 32;
+template <int DEPTH>
+__global__ void __launch_bounds__(kQPThreads, 3) bin2q_qp_kernel(Bin2QArgs a) {
+  constexpr int M = 6;
+  constexpr uint32_t TT = QPGeo::TT, Q = QPGeo::Q, LOG = 2 * M;
+  static_assert(TT == (1u << (2 * M)) && TT / 4 == 4 * kThreads, "one quad per thread per quarter");
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  float* qbuf = reinterpret_cast<float*>(smem_raw);  // [quarter][x / psi][Q]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(qbuf + 8 * Q);  // full[4]
+  uint64_t* empty = bars + 4;                                  // empty[4]
+  uint64_t* metas = empty + 4;                                 // [2][kQPMeta]
+  QGeo g;
+  g.K = a.K;
+  g.lmask = a.geo[0];
+  g.q1 = a.geo[1];
+  g.amask = a.geo[2];
+  g.bmask = a.geo[3];
+  g.kmask = a.geo[4];
+  g.ntiles = a.geo[5];
+  const float* src = reinterpret_cast<const float*>(a.src);
+  float* dst = reinterpret_cast<float*>(a.dst);
+  const uint32_t* map = a.map;
+  const int tid = threadIdx.x;
+  const uint64_t G = gridDim.x;
+  // item claims exactly as bin2q_kernel (schedule + dynamic counter, else static round robin)
+  const uint32_t* sched = (a.sched && a.sched_m == M) ? a.sched : nullptr;
+  const uint64_t nitems = sched ? a.nitems : g.ntiles;
+  unsigned long long* counter = sched ? a.counter : nullptr;
+  auto first = [&](uint64_t c) { return sched ? c : qnext(g, c, G, LOG); };
+  auto claim = [&](uint64_t prev) -> uint64_t {
+    if (counter) return (uint64_t)atomicAdd(counter, 1ull);
+    return first(prev == ~0ull ? (uint64_t)blockIdx.x : prev + G);
+  };
+  auto entry = [&](uint64_t c) -> uint32_t { return sched ? __ldg(sched + c) : (uint32_t)c; };
+  auto ent_of = [&](uint64_t c) -> uint32_t { return c < nitems ? entry(c) : 0u; };
+  auto tile_e = [&](uint32_t e) -> uint64_t {
+    return sched ? (uint64_t)(e & kQTileMask) : (uint64_t)e;
+  };
+  uint64_t pc = 0, p1 = 0, p2 = 0;
+  uint32_t e0 = 0, e1 = 0;
+  QItem pit;
+  // thread 0: the metadata of item pc (or the end marker) into slot `slot`, then the claim
+  // pipeline moves on (depth 3: claim two items ahead, the schedule entry one) and the map
+  // entries of the new pc are requested (used one item later)
+  auto prep = [&](int slot) {
+    uint64_t* meta = metas + kQPMeta * slot;
+    if (pc >= nitems) {
+      meta[7] = 1;
+      return;
+    }
+    const uint64_t tau = tile_e(e0);
+    uint64_t x0, p0, taup;
+    qtile(g, tau, LOG, x0, p0, taup);
+    const bool self = taup == tau;
+    const uint64_t wb = qwin(g, x0), wp = qwin(g, p0);
+    const uint64_t yf = wb >> 2, ym = g.q1 - yf - TT / 2, ypf = wp >> 2, ypm = g.q1 - ypf - TT / 2;
+    meta[0] = (pit.m[0] & 3u) | ((pit.m[1] & 3u) << 2) | (self ? 16u : 0u);
+    meta[1] = qrun(g, pit.m[2], x0);
+    meta[2] = self ? kNone : qrun(g, pit.m[3], p0);
+    meta[3] = qrun(g, pit.m[4], yf);
+    meta[4] = qrun(g, pit.m[5], ym);
+    meta[5] = self ? kNone : qrun(g, pit.m[6], ypf);
+    meta[6] = self ? kNone : qrun(g, pit.m[7], ypm);
+    meta[7] = 0;
+    meta[8] = reinterpret_cast<uint64_t>(qp_wstart(g, src, pit.m[0], wb));
+    meta[9] = reinterpret_cast<uint64_t>(qp_wstart(g, src, pit.m[1], wp));
+    if constexpr (DEPTH == 1) {
+      pc = claim(pc);
+      e0 = ent_of(pc);
+    } else {
+      pc = p1;
+      e0 = e1;
+      p1 = p2;
+      e1 = ent_of(p1);
+      p2 = claim(p2);
+    }
+    if (pc < nitems) qlookup<M, false>(g, map, tile_e(e0), pit);
+  };
+  // thread 0: quarter q of the item in `slot` (or a plain arrive after the last item)
+  auto issue = [&](int q, int slot) {
+    const uint64_t* meta = metas + kQPMeta * slot;
+    if (meta[7]) {
+      mbar_arrive(&bars[q]);
+      return;
+    }
+    const uint32_t modes = (uint32_t)meta[0];
+    mbar_expect_tx(&bars[q], 2u * Q * 4u);
+    const uint32_t sq = ((q & 1) << 1) | (q >> 1);  // x window: logical quarter swap2(q)
+    qp_issue_win(qbuf + (size_t)(2 * q) * Q, reinterpret_cast<const float*>(meta[8]), modes & 3u,
+                 sq, &bars[q]);
+    qp_issue_win(qbuf + (size_t)(2 * q + 1) * Q, reinterpret_cast<const float*>(meta[9]),
+                 (modes >> 2) & 3u, 3u - (uint32_t)q, &bars[q]);
+  };
+  if (tid == 0) {
+    for (int q = 0; q < 4; ++q) {
+      mbar_init(&bars[q], 1);
+      mbar_init(&empty[q], kThreads / 32);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+  if (tid >= kThreads) {  // the producer warp
+    if (tid != kThreads) return;
+    pc = claim(~0ull);
+    if constexpr (DEPTH == 3) {
+      p1 = claim(pc);
+      p2 = claim(p1);
+      e1 = ent_of(p1);
+    }
+    e0 = ent_of(pc);
+    if (pc < nitems) qlookup<M, false>(g, map, tile_e(e0), pit);
+    for (uint32_t i = 0;; ++i) {
+      const int slot = (int)(i & 1u);
+      // buffer q and meta slot `slot` are free once every consumer warp is past quarter q of
+      // item i - 1 (for q = 0 that also means past item i - 2, the slot's previous item)
+      if (i) QP_WAIT(&empty[0], (i - 1) & 1u);
+      prep(slot);
+      const bool end = metas[kQPMeta * slot + 7] != 0;
+      issue(0, slot);
+      if (end) return;  // the consumers stop at this item's quarter 0
+      for (int q = 1; q < 4; ++q) {
+        if (i) QP_WAIT(&empty[q], (i - 1) & 1u);
+        issue(q, slot);
+      }
+    }
+  }
+  const int lane = tid & 31;
+  for (uint32_t i = 0;; ++i) {
+    const int slot = (int)(i & 1u);
+    const uint64_t* meta = metas + kQPMeta * slot;
+    QP_WAIT(&bars[0], i & 1u);
+    if (meta[7]) break;  // end marker: no more items for this CTA
+    const uint32_t modes = (uint32_t)meta[0];
+    const uint32_t mw = modes & 3u, mp = (modes >> 2) & 3u;
+    const bool self = (modes & 16u) != 0;
+    // one (mode x mode) code path per item: the quarter loop runs inside it (dispatching per
+    // quarter through the jump table stalled the warps on instruction fetch)
+#define LCSB_QP(MW, MP) \
+  qp_item<MW, MP>(qbuf, bars, empty, i & 1u, src, dst, meta, self, (uint32_t)tid, lane)
+    switch (mw * 4 + mp) {
+      case 0: LCSB_QP(0, 0); break;
+      case 1: LCSB_QP(0, 1); break;
+      case 2: LCSB_QP(0, 2); break;
+      case 3: LCSB_QP(0, 3); break;
+      case 4: LCSB_QP(1, 0); break;
+      case 5: LCSB_QP(1, 1); break;
+      case 6: LCSB_QP(1, 2); break;
+      case 7: LCSB_QP(1, 3); break;
+      case 8: LCSB_QP(2, 0); break;
+      case 9: LCSB_QP(2, 1); break;
+      case 10: LCSB_QP(2, 2); break;
+      case 11: LCSB_QP(2, 3); break;
+      case 12: LCSB_QP(3, 0); break;
+      case 13: LCSB_QP(3, 1); break;
+      case 14: LCSB_QP(3, 2); break;
+      default: LCSB_QP(3, 3); break;
+    }
+#undef LCSB_QP
+  }
+}
+
+template <int DEPTH>
+cudaError_t launch_qp(const Bin2QArgs& a, cudaStream_t s, int sms) {
+  constexpr size_t SMEM = 8 * QPGeo::Q * sizeof(float) + 8 * sizeof(uint64_t) +
+                          2 * kQPMeta * sizeof(uint64_t);
+  static uint64_t cap = 0;
+  if (cap == 0) {
+    cudaError_t e = cudaFuncSetAttribute(bin2q_qp_kernel<DEPTH>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM);
+    if (e != cudaSuccess) return e;
+    int per_sm = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, bin2q_qp_kernel<DEPTH>, kQPThreads,
+                                                      SMEM) != cudaSuccess ||
+        per_sm < 1) {
+      cudaGetLastError();
+      per_sm = 1;
+    }
+    cap = (uint64_t)per_sm * sms;
+  }
+  if (a.K < 7 || a.ell < a.K + 1) return cudaErrorInvalidValue;
+  const uint64_t ntiles = (a.sched && a.sched_m == 6) ? a.nitems : (1ull << (2 * (a.ell - 7)));
+  uint64_t blocks = cap < ntiles ? cap : ntiles;
+  if (blocks < 1) blocks = 1;
+  Bin2QArgs b = a;
+  const int L = 2 * a.ell;
+  b.geo[0] = (1ull << L) - 1;
+  b.geo[1] = 1ull << (L - 2);
+  b.geo[2] = 0xAAAAAAAAAAAAAAAAull & b.geo[0];
+  b.geo[3] = 0x5555555555555555ull & b.geo[0];
+  b.geo[4] = (1ull << (2 * a.K)) - 1;
+  b.geo[5] = 1ull << (2 * (a.ell - 7));
+  bin2q_qp_kernel<DEPTH><<<(unsigned)blocks, kQPThreads, SMEM, s>>>(b);
+  return cudaGetLastError();
 }
 
 // the launch claims items dynamically (a schedule for these tiles and a work counter)

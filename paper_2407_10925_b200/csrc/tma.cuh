@@ -19,6 +19,23 @@ static __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t by
 static __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {  // arrive without transactions
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
+// try_wait with a suspend-time hint: the waiting warp is parked by the hardware until the phase
+// completes (or the hint expires) instead of re-issuing the probe (the quarter-pipelined sweep
+// waits four times per item)
+static __device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
+  uint32_t done = 0;
+  do {
+    asm volatile(
+        "{\n"
+        " .reg .pred p;\n"
+        " mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n"
+        " selp.u32 %0, 1, 0, p;\n"
+        "}\n"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(parity), "r"(0x989680u)
+        : "memory");
+  } while (!done);
+}
 // Plain try_wait probe loop.  LCSB_MBAR_HINT (compile-time, A/B only) adds a suspend-time hint;
 // measured on B200: no change for the fp32 sweeps and W passes, 2 % slower for the fp64 sweep;
 // in the power-capped bench loop (round 2: the probe loop is ~17 % of the sweep's issued

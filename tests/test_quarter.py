@@ -516,3 +516,36 @@ def test_l18_table2_sixth_digit_on_one_gpu():
     b = h.bound()
     h.destroy()
     assert math.floor(b.best_bound * 1e6 + 1e-6) / 1e6 == 0.790668, b.best_bound
+
+
+_QP_SNIPPET = r"""
+import sys, numpy as np
+sys.path.insert(0, sys.argv[1])
+from paper_2407_10925_b200 import lcsb as L
+from seeded_inputs import splitmix64_indices
+h = L.Lcsb(2, 2, 14, dtype="f32", symmetry=2)
+h.ready(wait=True)
+h.sweep(9)
+idx = splitmix64_indices(5, 1 << 16, h.num_states)
+np.save(sys.argv[2], np.stack([h.table_gather(idx), h.table_gather(idx, which=1)]))
+"""
+
+
+@pytest.mark.gpu
+@pytest.mark.skipif(not has_cuda(), reason="needs a CUDA device")
+def test_quarter_pipelined_sweep_equals_whole_stage_sweep(tmp_path):
+    """The quarter-pipelined fp32 sweep (bin2q_qp_kernel, default for tiles of 4^6) and the
+    whole-stage sweep (LCSB_QP=0) store identical tables (l = 14, 9 sweeps, 2^16 sampled states
+    of both generations); each process reads the knob once."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    outs = []
+    for qp in ("1", "0"):
+        out = tmp_path / f"qp{qp}.npy"
+        env = dict(os.environ, LCSB_QP=qp)
+        subprocess.run([sys.executable, "-c", _QP_SNIPPET, root, str(out)], env=env, check=True,
+                       timeout=600)
+        outs.append(np.load(out))
+    assert np.array_equal(outs[0], outs[1])
