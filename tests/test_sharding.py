@@ -666,7 +666,8 @@ def _pm_quarter_worker(rank, world, port, out_dir, ell, K, dtype):
 
 @pytest.mark.gpu
 @pytest.mark.skipif(not has_cuda(), reason="needs a CUDA device")
-@pytest.mark.parametrize("world,ell,K,dtype", [(2, 10, 5, "f32"), (4, 12, 6, "f64")])
+@pytest.mark.parametrize("world,ell,K,dtype", [(2, 10, 5, "f32"), (4, 12, 6, "f64"),
+                                                (2, 12, 7, "f32")])
 def test_quarter_process_mode_multi_rank_on_one_gpu(tmp_path, world, ell, K, dtype):
     """The sharded quarter table over 2 and 4 PROCESSES on cuda:0: each process maps the peers'
     shard allocations into its table's address range (POSIX fds over Unix sockets), reads the
