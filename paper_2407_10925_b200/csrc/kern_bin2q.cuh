@@ -1236,6 +1236,335 @@ __global__ void __launch_bounds__(kQPThreads, 3) bin2q_qp_kernel(Bin2QArgs a) {
   }
 }
 
+// ---- staged, quarter-pipelined fp32 bound pass (tiles of 4^6, round 2).  The one-pass bound
+// (reading R21) of bin2q_kernel<..., WMODE> reads u and v_prev at every stored output with direct
+// loads; they make it long-scoreboard bound.  Here every quarter-step of an item (the quarter
+// buffers of bin2q_qp_kernel) also carries, staged by TMA, u and v_prev at the quarter's outputs:
+// the Q1 outputs of quads tid + 256 q are one contiguous 1024-entry range of the stored Q1 run
+// (quarter q of t's run, or quarter swap2(3 - q) of psi(t)'s), the x window's rows one
+// 512-entry range of the row run (quarter swap2(q); mirror run: quarter 3 - swap2(q)) and the
+// psi window's likewise (quarter 3 - q).  A quarter-step buffer is 32 KB (windows 16 KB, u and
+// v_prev 8 KB each), two per CTA; a producer warp refills them.  Same arithmetic and reductions
+// as the direct-load pass (bit-identical R, D).
+constexpr uint32_t kQWBuf = 8192;  // floats per quarter-step buffer
+// one quad of the staged bound pass: sx_ / sp_ = the staged u and v_prev of the quarter
+// ([Q1 1024 | x rows 512 | psi rows 512]); the arithmetic of quad_w32 (pair_quads_w32)
+template <int MW, int MP>
+__device__ __forceinline__ void quad_wq(const float* bw, const float* bp, const float* su,
+                                        const float* spv, const uint64_t* meta, bool self,
+                                        const float* src, const float* prev, BAcc& ba,
+                                        uint32_t qd) {
+  constexpr uint32_t TT = QPGeo::TT;
+  constexpr uint32_t SX = (MW == 0 || MW == 3) ? 2 : 0, SP = (MP == 0 || MP == 3) ? 2 : 1;
+  const uint64_t oQ1 = meta[1], oQ1p = meta[2];
+  const uint64_t of = meta[3], om = meta[4], opf = meta[5], opm = meta[6];
+  const bool rows_x = of != kNone || om != kNone;
+  const bool rows_p = !self && (opf != kNone || opm != kNone);
+  const bool rdp = prev != nullptr;
+  const uint32_t o0 = 4 * qd;
+  const uint32_t g = 2 * pairswap32(o0), u = 2 * (TT - 4 - o0);
+  const uint32_t qb = pairswap32(~o0 & (TT - 1) & ~3u);
+  const uint32_t rx = g >> 2, rp = u >> 2;
+  const bool sx = (qd >> SX) & 1u, sp = (qd >> SP) & 1u;
+  constexpr uint32_t c0 = comp<MW>(0), c1 = comp<MW>(1), c2 = comp<MW>(2), c3 = comp<MW>(3);
+  constexpr uint32_t d0 = comp<MP>(0), d1 = comp<MP>(1), d2 = comp<MP>(2), d3 = comp<MP>(3);
+  double tx[4];
+  {
+    float X1[4], X2[4], a[4], b[4];
+    ld4r(bw + qloc<TT, MW>(gbase<TT, MW>(sx ? g + 4 : g)), X1);
+    ld4r(bw + qloc<TT, MW>(gbase<TT, MW>(sx ? g : g + 4)), X2);
+    sel4f(sx, X1, X2, a, b);
+    tx[0] = (double)a[c0] + (double)a[c1];
+    tx[1] = (double)b[c0] + (double)b[c1];
+    tx[2] = (double)a[c2] + (double)a[c3];
+    tx[3] = (double)b[c2] + (double)b[c3];
+    if (rows_x) {  // staged pair: the row run's (rows rx, rx + 1) or the mirror run's (rx + 1, rx)
+      const uint32_t xi = of != kNone ? (rx & 511u) : (510u - (rx & 511u));
+      const float2 ux = *reinterpret_cast<const float2*>(su + 1024 + xi);
+      const float2 px = rdp ? *reinterpret_cast<const float2*>(spv + 1024 + xi) : make_float2(0.f, 0.f);
+      double G[4];
+      widen4(a, G);
+      q0_rows_w<TT, MW, false>(G, rx, of, om, ux.x, px.x, ux.y, px.y, src, prev, nullptr, ba);
+      widen4(b, G);
+      q0_rows_w<TT, MW, false>(G, rx + 1, of, om, ux.y, px.y, ux.x, px.x, src, prev, nullptr, ba);
+    }
+  }
+  double tq[4];
+  {
+    float P1[4], P2[4], ap[4], bq[4];
+    ld4r(bp + qloc<TT, MP>(gbase<TT, MP>(sp ? u + 4 : u)), P1);
+    ld4r(bp + qloc<TT, MP>(gbase<TT, MP>(sp ? u : u + 4)), P2);
+    sel4f(sp, P1, P2, ap, bq);
+    tq[0] = (double)bq[d2] + (double)bq[d3];
+    tq[1] = (double)bq[d0] + (double)bq[d1];
+    tq[2] = (double)ap[d2] + (double)ap[d3];
+    tq[3] = (double)ap[d0] + (double)ap[d1];
+    if (rows_p) {
+      const uint32_t pi = opf != kNone ? (rp & 511u) : (510u - (rp & 511u));
+      const float2 up = *reinterpret_cast<const float2*>(su + 1536 + pi);
+      const float2 pq = rdp ? *reinterpret_cast<const float2*>(spv + 1536 + pi) : make_float2(0.f, 0.f);
+      double G[4];
+      widen4(ap, G);
+      q0_rows_w<TT, MP, false>(G, rp, opf, opm, up.x, pq.x, up.y, pq.y, src, prev, nullptr, ba);
+      widen4(bq, G);
+      q0_rows_w<TT, MP, false>(G, rp + 1, opf, opm, up.y, pq.y, up.x, pq.x, src, prev, nullptr,
+                               ba);
+    }
+  }
+  double v[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) v[k] = 0.5 * dmax(tx[k], tq[k]);
+  if (oQ1 != kNone || oQ1p != kNone) {
+    const uint32_t qi = oQ1 != kNone ? (o0 & 1023u) : (qb & 1023u);
+    float uu[4], pp[4] = {0, 0, 0, 0};
+    ld4r(su + qi, uu);
+    if (rdp) ld4r(spv + qi, pp);
+    if (oQ1 != kNone) {
+#pragma unroll
+      for (int k = 0; k < 4; ++k) bacc((double)uu[k], (double)pp[k], v[k], ba);
+    } else {  // position j of the psi run holds output (3, 1, 2, 0)[j]
+      bacc((double)uu[3], (double)pp[3], v[0], ba);
+      bacc((double)uu[1], (double)pp[1], v[1], ba);
+      bacc((double)uu[2], (double)pp[2], v[2], ba);
+      bacc((double)uu[0], (double)pp[0], v[3], ba);
+    }
+  }
+}
+
+template <int MW, int MP>
+__device__ __forceinline__ void qpw_item(const float* qbuf, uint64_t* full, uint64_t* empty,
+                                         const uint64_t* meta, bool self, const float* src,
+                                         const float* prev, BAcc& ba, uint32_t tid, int lane) {
+#pragma unroll 1
+  for (int q = 0; q < 4; ++q) {
+    const int b = q & 1;
+    if (q) QP_WAIT(&full[b], (uint32_t)(q >> 1));
+    const float* buf = qbuf + (size_t)b * kQWBuf;
+    quad_wq<MW, MP>(buf, buf + 2048, buf + 4096, buf + 6144, meta, self, src, prev, ba,
+                    tid + kThreads * (uint32_t)q);
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[b]);
+  }
+}
+
+template <int DEPTH>
+__global__ void __launch_bounds__(kQPThreads, 3) bin2q_qpw_kernel(Bin2QArgs a) {
+  constexpr int M = 6;
+  constexpr uint32_t TT = QPGeo::TT, Q = QPGeo::Q, LOG = 2 * M;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  float* qbuf = reinterpret_cast<float*>(smem_raw);  // [2][kQWBuf]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(qbuf + 2 * kQWBuf);  // full[2]
+  uint64_t* empty = bars + 2;                                        // empty[2]
+  uint64_t* metas = empty + 2;                                       // [2][kQPMeta]
+  __shared__ double r0[8], r1[8], r2[8];
+  QGeo g;
+  g.K = a.K;
+  g.lmask = a.geo[0];
+  g.q1 = a.geo[1];
+  g.amask = a.geo[2];
+  g.bmask = a.geo[3];
+  g.kmask = a.geo[4];
+  g.ntiles = a.geo[5];
+  const float* src = reinterpret_cast<const float*>(a.src);
+  const float* prev = reinterpret_cast<const float*>(a.prev);
+  const uint32_t* map = a.map;
+  const int tid = threadIdx.x;
+  const uint64_t G = gridDim.x;
+  const uint32_t* sched = (a.sched && a.sched_m == M) ? a.sched : nullptr;
+  const uint64_t nitems = sched ? a.nitems : g.ntiles;
+  unsigned long long* counter = sched ? a.counter : nullptr;
+  auto first = [&](uint64_t c) { return sched ? c : qnext(g, c, G, LOG); };
+  auto claim = [&](uint64_t prv) -> uint64_t {
+    if (counter) return (uint64_t)atomicAdd(counter, 1ull);
+    return first(prv == ~0ull ? (uint64_t)blockIdx.x : prv + G);
+  };
+  auto entry = [&](uint64_t c) -> uint32_t { return sched ? __ldg(sched + c) : (uint32_t)c; };
+  auto ent_of = [&](uint64_t c) -> uint32_t { return c < nitems ? entry(c) : 0u; };
+  auto tile_e = [&](uint32_t e) -> uint64_t {
+    return sched ? (uint64_t)(e & kQTileMask) : (uint64_t)e;
+  };
+  if (tid == 0) {
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&bars[b], 1);
+      mbar_init(&empty[b], kThreads / 32);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+  if (tid >= kThreads) {  // the producer warp (one lane)
+    if (tid != kThreads) return;
+    uint64_t pc = 0, p1 = 0, p2 = 0;
+    uint32_t e0 = 0, e1 = 0;
+    QItem pit;
+    pc = claim(~0ull);
+    if constexpr (DEPTH == 3) {
+      p1 = claim(pc);
+      p2 = claim(p1);
+      e1 = ent_of(p1);
+    }
+    e0 = ent_of(pc);
+    if (pc < nitems) qlookup<M, false>(g, map, tile_e(e0), pit);
+    for (uint64_t k = 0;; ++k) {
+      const int q = (int)(k & 3u), b = (int)(k & 1u), slot = (int)((k >> 2) & 1u);
+      if (k >= 2) QP_WAIT(&empty[b], (uint32_t)(((k >> 1) - 1) & 1u));
+      uint64_t* meta = metas + kQPMeta * slot;
+      if (q == 0) {  // the item's metadata (or the end marker), then the claim pipeline moves on
+        if (pc >= nitems) {
+          meta[7] = 1;
+          mbar_arrive(&bars[b]);
+          return;
+        }
+        const uint64_t tau = tile_e(e0);
+        uint64_t x0, p0, taup;
+        qtile(g, tau, LOG, x0, p0, taup);
+        const bool self = taup == tau;
+        const uint64_t wb = qwin(g, x0), wp = qwin(g, p0);
+        const uint64_t yf = wb >> 2, ym = g.q1 - yf - TT / 2, ypf = wp >> 2,
+                       ypm = g.q1 - ypf - TT / 2;
+        meta[0] = (pit.m[0] & 3u) | ((pit.m[1] & 3u) << 2) | (self ? 16u : 0u);
+        meta[1] = qrun(g, pit.m[2], x0);
+        meta[2] = self ? kNone : qrun(g, pit.m[3], p0);
+        meta[3] = qrun(g, pit.m[4], yf);
+        meta[4] = qrun(g, pit.m[5], ym);
+        meta[5] = self ? kNone : qrun(g, pit.m[6], ypf);
+        meta[6] = self ? kNone : qrun(g, pit.m[7], ypm);
+        meta[7] = 0;
+        meta[8] = reinterpret_cast<uint64_t>(qp_wstart(g, src, pit.m[0], wb));
+        meta[9] = reinterpret_cast<uint64_t>(qp_wstart(g, src, pit.m[1], wp));
+        if constexpr (DEPTH == 1) {
+          pc = claim(pc);
+          e0 = ent_of(pc);
+        } else {
+          pc = p1;
+          e0 = e1;
+          p1 = p2;
+          e1 = ent_of(p1);
+          p2 = claim(p2);
+        }
+        if (pc < nitems) qlookup<M, false>(g, map, tile_e(e0), pit);
+      }
+      // quarter q: both windows' quarters, u and v_prev at its outputs
+      const uint32_t modes = (uint32_t)meta[0];
+      const bool self = (modes & 16u) != 0;
+      const uint32_t sq = (((uint32_t)q & 1u) << 1) | ((uint32_t)q >> 1);  // swap2(q)
+      const uint64_t oQ1 = meta[1], oQ1p = meta[2], of = meta[3], om = meta[4], opf = meta[5],
+                     opm = meta[6];
+      const uint64_t q1s = oQ1 != kNone ? oQ1 + 1024u * (uint32_t)q
+                                        : (oQ1p != kNone ? oQ1p + 1024u * (((3u - q) & 1u) << 1 | ((3u - q) >> 1)) : kNone);
+      const uint64_t xs = of != kNone ? of + 512u * sq : (om != kNone ? om + 512u * (3u - sq) : kNone);
+      const uint64_t ps = self ? kNone
+                               : (opf != kNone ? opf + 512u * (3u - q)
+                                               : (opm != kNone ? opm + 512u * (uint32_t)q : kNone));
+      const int na = prev ? 2 : 1;
+      uint32_t bytes = 2u * Q * 4u;
+      bytes += (uint32_t)na * ((q1s != kNone ? 4096u : 0u) + (xs != kNone ? 2048u : 0u) +
+                               (ps != kNone ? 2048u : 0u));
+      mbar_expect_tx(&bars[b], bytes);
+      float* buf = qbuf + (size_t)b * kQWBuf;
+      qp_issue_win(buf, reinterpret_cast<const float*>(meta[8]), modes & 3u, sq, &bars[b]);
+      qp_issue_win(buf + Q, reinterpret_cast<const float*>(meta[9]), (modes >> 2) & 3u,
+                   3u - (uint32_t)q, &bars[b]);
+      for (int ar = 0; ar < na; ++ar) {
+        const float* base = ar ? prev : src;
+        float* st = buf + 4096 + 2048 * ar;
+        if (q1s != kNone) tma_load_1d(st, base + q1s, 4096u, &bars[b]);
+        if (xs != kNone) tma_load_1d(st + 1024, base + xs, 2048u, &bars[b]);
+        if (ps != kNone) tma_load_1d(st + 1536, base + ps, 2048u, &bars[b]);
+      }
+      (void)self;
+    }
+  }
+  const int lane = tid & 31;
+  BAcc ba{-INFINITY, INFINITY, INFINITY, 0.0};
+  for (uint32_t i = 0;; ++i) {
+    const uint64_t* meta = metas + kQPMeta * (i & 1u);
+    QP_WAIT(&bars[0], 0u);
+    if (meta[7]) break;
+    const uint32_t modes = (uint32_t)meta[0];
+    const uint32_t mw = modes & 3u, mp = (modes >> 2) & 3u;
+    const bool self = (modes & 16u) != 0;
+#define LCSB_QPW(MW, MP) \
+  qpw_item<MW, MP>(qbuf, bars, empty, meta, self, src, prev, ba, (uint32_t)tid, lane)
+    switch (mw * 4 + mp) {
+      case 0: LCSB_QPW(0, 0); break;
+      case 1: LCSB_QPW(0, 1); break;
+      case 2: LCSB_QPW(0, 2); break;
+      case 3: LCSB_QPW(0, 3); break;
+      case 4: LCSB_QPW(1, 0); break;
+      case 5: LCSB_QPW(1, 1); break;
+      case 6: LCSB_QPW(1, 2); break;
+      case 7: LCSB_QPW(1, 3); break;
+      case 8: LCSB_QPW(2, 0); break;
+      case 9: LCSB_QPW(2, 1); break;
+      case 10: LCSB_QPW(2, 2); break;
+      case 11: LCSB_QPW(2, 3); break;
+      case 12: LCSB_QPW(3, 0); break;
+      case 13: LCSB_QPW(3, 1); break;
+      case 14: LCSB_QPW(3, 2); break;
+      default: LCSB_QPW(3, 3); break;
+    }
+#undef LCSB_QPW
+  }
+  // block reduction over the 8 consumer warps (named barrier 1: the producer has left)
+  double x = ba.rmax, y = ba.rmin, z = ba.dmin;
+  for (int o = 16; o > 0; o >>= 1) {
+    x = dmax(x, __shfl_xor_sync(0xffffffffu, x, o));
+    y = dmin(y, __shfl_xor_sync(0xffffffffu, y, o));
+    z = dmin(z, __shfl_xor_sync(0xffffffffu, z, o));
+  }
+  const int wid = tid >> 5;
+  if (lane == 0) {
+    r0[wid] = x;
+    r1[wid] = y;
+    r2[wid] = z;
+  }
+  asm volatile("bar.sync 1, %0;" ::"n"(kThreads) : "memory");
+  if (tid == 0) {
+    for (int w = 1; w < kThreads / 32; ++w) {
+      x = dmax(x, r0[w]);
+      y = dmin(y, r1[w]);
+      z = dmin(z, r2[w]);
+    }
+    atomicMax(a.red_out + 0, ord_enc(x));
+    atomicMin(a.red_out + 1, ord_enc(y));
+    atomicMin(a.red_out + 2, ord_enc(z));
+  }
+}
+
+template <int DEPTH>
+cudaError_t launch_qpw(const Bin2QArgs& a, cudaStream_t s, int sms) {
+  constexpr size_t SMEM = 2 * kQWBuf * sizeof(float) + 4 * sizeof(uint64_t) +
+                          2 * kQPMeta * sizeof(uint64_t);
+  static uint64_t cap = 0;
+  if (cap == 0) {
+    cudaError_t e = cudaFuncSetAttribute(bin2q_qpw_kernel<DEPTH>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM);
+    if (e != cudaSuccess) return e;
+    int per_sm = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, bin2q_qpw_kernel<DEPTH>,
+                                                      kQPThreads, SMEM) != cudaSuccess ||
+        per_sm < 1) {
+      cudaGetLastError();
+      per_sm = 1;
+    }
+    cap = (uint64_t)per_sm * sms;
+  }
+  if (a.K < 7 || a.ell < a.K + 1) return cudaErrorInvalidValue;
+  const uint64_t ntiles = (a.sched && a.sched_m == 6) ? a.nitems : (1ull << (2 * (a.ell - 7)));
+  uint64_t blocks = cap < ntiles ? cap : ntiles;
+  if (blocks < 1) blocks = 1;
+  Bin2QArgs b = a;
+  const int L = 2 * a.ell;
+  b.geo[0] = (1ull << L) - 1;
+  b.geo[1] = 1ull << (L - 2);
+  b.geo[2] = 0xAAAAAAAAAAAAAAAAull & b.geo[0];
+  b.geo[3] = 0x5555555555555555ull & b.geo[0];
+  b.geo[4] = (1ull << (2 * a.K)) - 1;
+  b.geo[5] = 1ull << (2 * (a.ell - 7));
+  bin2q_qpw_kernel<DEPTH><<<(unsigned)blocks, kQPThreads, SMEM, s>>>(b);
+  return cudaGetLastError();
+}
+
 template <int DEPTH>
 cudaError_t launch_qp(const Bin2QArgs& a, cudaStream_t s, int sms) {
   constexpr size_t SMEM = 8 * QPGeo::Q * sizeof(float) + 8 * sizeof(uint64_t) +

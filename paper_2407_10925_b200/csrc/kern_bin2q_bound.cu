@@ -24,6 +24,13 @@ cudaError_t launch_bin2q_wpass(const Bin2QArgs& a, int dtype, int M, cudaStream_
       const char* e = getenv("LCSB_BIN2Q_WDIRECT");
       wv = e ? atoi(e) : 0;
     }
+    static int qpw = -1;  // the staged quarter-pipelined pass (default; LCSB_QPW=0: direct loads)
+    if (qpw < 0) {
+      const char* e = getenv("LCSB_QPW");
+      qpw = e ? atoi(e) : 1;
+    }
+    if (qpw && wv == 0 && a.K >= 7)
+      return q_dynamic(a, 6) ? launch_qpw<3>(a, s, sms) : launch_qpw<1>(a, s, sms);
     if (wv == 1) return launch_q<float, 6, 1, true, 2>(a, s, sms);
     // LCSB_BIN2Q_WDIRECT=2 (A/B): one 512-thread CTA per SM with two stages (prefetch overlap)
     if (wv == 2) return launch_q<float, 6, 2, true, 1, 512>(a, s, sms);

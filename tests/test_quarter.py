@@ -549,3 +549,42 @@ def test_quarter_pipelined_sweep_equals_whole_stage_sweep(tmp_path):
                        timeout=600)
         outs.append(np.load(out))
     assert np.array_equal(outs[0], outs[1])
+
+
+_QPW_SNIPPET = r"""
+import sys, json
+sys.path.insert(0, sys.argv[1])
+from paper_2407_10925_b200 import lcsb as L
+h = L.Lcsb(2, 2, 14, dtype="f32", symmetry=2)
+h.ready(wait=True)
+out = []
+for n in (1, 8):
+    h.sweep(n)
+    b = h.bound()
+    out.append([b.R_max, b.R_min, b.E_at_Rmax, b.E_at_Rmin, b.bound_at_Rmax, b.bound_at_Rmin])
+h.sweep_ex(2, 1)
+b = h.bound()  # the D-only pass
+out.append([b.R_max, b.R_min, b.E_at_Rmax, b.E_at_Rmin, b.bound_at_Rmax, b.bound_at_Rmin])
+json.dump(out, open(sys.argv[2], "w"))
+"""
+
+
+@pytest.mark.gpu
+@pytest.mark.skipif(not has_cuda(), reason="needs a CUDA device")
+def test_quarter_staged_bound_equals_direct_load_bound(tmp_path):
+    """The staged quarter-pipelined bound pass (bin2q_qpw_kernel, default for tiles of 4^6: u
+    and v_prev at the outputs staged by TMA) and the direct-load pass (LCSB_QPW=0) give the same
+    R, E and bounds bit for bit (l = 14 fp32, after 1 and 9 sweeps, and the D-only pass)."""
+    import json
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    outs = []
+    for qpw in ("1", "0"):
+        out = tmp_path / f"qpw{qpw}.json"
+        env = dict(os.environ, LCSB_QPW=qpw)
+        subprocess.run([sys.executable, "-c", _QPW_SNIPPET, root, str(out)], env=env, check=True,
+                       timeout=600)
+        outs.append(json.load(open(out)))
+    assert outs[0] == outs[1]
