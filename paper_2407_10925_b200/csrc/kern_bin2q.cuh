@@ -1053,6 +1053,13 @@ constexpr int kQPMeta = 10;  // per item: [0] modes, [1..6] runs, [7] end, [8] /
 #else
 #define QP_WAIT mbar_wait_sleep
 #endif
+// consumer threads of bin2q_qp_kernel (LCSB_QP_CONSUMERS, compile-time A/B: 128 = four warps
+// with two quads per thread per quarter)
+#ifndef LCSB_QP_CONSUMERS
+#define LCSB_QP_CONSUMERS 256
+#endif
+constexpr int kQPC = LCSB_QP_CONSUMERS;
+static_assert(kThreads % kQPC == 0 && kQPC % 32 == 0, "consumer threads");
 // the consumer side of one item of bin2q_qp_kernel: its four quarters in order, each after its
 // buffer has landed (full[q]); each warp then releases the buffer (empty[q])
 template <int MW, int MP>
@@ -1066,7 +1073,9 @@ __device__ __forceinline__ void qp_item(const float* qbuf, uint64_t* full, uint6
   for (int q = 0; q < 4; ++q) {
     if (q) QP_WAIT(&full[q], parity);
     const float* bw = qbuf + (size_t)(2 * q) * Q;
-    quad_f32<float, TT, MW, MP, true>(bw, bw + Q, R, tid + kThreads * (uint32_t)q);
+#pragma unroll 1
+    for (uint32_t j = 0; j < (uint32_t)(kThreads / kQPC); ++j)
+      quad_f32<float, TT, MW, MP, true>(bw, bw + Q, R, tid + kQPC * j + kThreads * (uint32_t)q);
     __syncwarp();  // the warp's reads of buffer q are done
     if (lane == 0) mbar_arrive(&empty[q]);
   }
@@ -1075,12 +1084,12 @@ __device__ __forceinline__ void qp_item(const float* qbuf, uint64_t* full, uint6
 // warp-specialised: warps 0-7 consume (one quad per thread per quarter), warp 8 (one lane)
 // produces -- it waits on empty[q] (all 8 consumer warps past quarter q of the previous item)
 // and refills buffer q with the next item's quarter, so no CTA-wide barrier stalls the loop
-constexpr int kQPThreads = kThreads + 32;
+constexpr int kQPThreads = kQPC + 32;
 template <int DEPTH>
 __global__ void __launch_bounds__(kQPThreads, 3) bin2q_qp_kernel(Bin2QArgs a) {
   constexpr int M = 6;
   constexpr uint32_t TT = QPGeo::TT, Q = QPGeo::Q, LOG = 2 * M;
-  static_assert(TT == (1u << (2 * M)) && TT / 4 == 4 * kThreads, "one quad per thread per quarter");
+  static_assert(TT == (1u << (2 * M)) && TT / 4 == 4 * kThreads, "256 quads per quarter");
   extern __shared__ __align__(128) unsigned char smem_raw[];
   float* qbuf = reinterpret_cast<float*>(smem_raw);  // [quarter][x / psi][Q]
   uint64_t* bars = reinterpret_cast<uint64_t*>(qbuf + 8 * Q);  // full[4]
@@ -1171,13 +1180,13 @@ __global__ void __launch_bounds__(kQPThreads, 3) bin2q_qp_kernel(Bin2QArgs a) {
   if (tid == 0) {
     for (int q = 0; q < 4; ++q) {
       mbar_init(&bars[q], 1);
-      mbar_init(&empty[q], kThreads / 32);
+      mbar_init(&empty[q], kQPC / 32);
     }
     fence_mbar_init();
   }
   __syncthreads();
-  if (tid >= kThreads) {  // the producer warp
-    if (tid != kThreads) return;
+  if (tid >= kQPC) {  // the producer warp
+    if (tid != kQPC) return;
     pc = claim(~0ull);
     if constexpr (DEPTH == 3) {
       p1 = claim(pc);
@@ -1347,8 +1356,9 @@ __device__ __forceinline__ void qpw_item(const float* qbuf, uint64_t* full, uint
   }
 }
 
+constexpr int kQPWThreads = kThreads + 32;  // the bound pass: 8 consumer warps + the producer
 template <int DEPTH>
-__global__ void __launch_bounds__(kQPThreads, 3) bin2q_qpw_kernel(Bin2QArgs a) {
+__global__ void __launch_bounds__(kQPWThreads, 3) bin2q_qpw_kernel(Bin2QArgs a) {
   constexpr int M = 6;
   constexpr uint32_t TT = QPGeo::TT, Q = QPGeo::Q, LOG = 2 * M;
   extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -1542,7 +1552,7 @@ cudaError_t launch_qpw(const Bin2QArgs& a, cudaStream_t s, int sms) {
     if (e != cudaSuccess) return e;
     int per_sm = 0;
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, bin2q_qpw_kernel<DEPTH>,
-                                                      kQPThreads, SMEM) != cudaSuccess ||
+                                                      kQPWThreads, SMEM) != cudaSuccess ||
         per_sm < 1) {
       cudaGetLastError();
       per_sm = 1;
@@ -1561,7 +1571,7 @@ cudaError_t launch_qpw(const Bin2QArgs& a, cudaStream_t s, int sms) {
   b.geo[3] = 0x5555555555555555ull & b.geo[0];
   b.geo[4] = (1ull << (2 * a.K)) - 1;
   b.geo[5] = 1ull << (2 * (a.ell - 7));
-  bin2q_qpw_kernel<DEPTH><<<(unsigned)blocks, kQPThreads, SMEM, s>>>(b);
+  bin2q_qpw_kernel<DEPTH><<<(unsigned)blocks, kQPWThreads, SMEM, s>>>(b);
   return cudaGetLastError();
 }
 
