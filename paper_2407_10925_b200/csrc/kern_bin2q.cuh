@@ -1258,11 +1258,13 @@ __global__ void __launch_bounds__(kQPThreads, 3) bin2q_qp_kernel(Bin2QArgs a) {
 constexpr uint32_t kQWBuf = 8192;  // floats per quarter-step buffer
 // one quad of the staged bound pass: sx_ / sp_ = the staged u and v_prev of the quarter
 // ([Q1 1024 | x rows 512 | psi rows 512]); the arithmetic of quad_w32 (pair_quads_w32)
-template <int MW, int MP>
+// DF (the tracking sweep of reading R25): store round32(F) at every stored output and reduce
+// against the staged u (dacc), as quad_w32<..., DIFF>; v_prev is not read
+template <int MW, int MP, bool DF = false>
 __device__ __forceinline__ void quad_wq(const float* bw, const float* bp, const float* su,
                                         const float* spv, const uint64_t* meta, bool self,
                                         const float* src, const float* prev, BAcc& ba,
-                                        uint32_t qd) {
+                                        uint32_t qd, float* dst = nullptr) {
   constexpr uint32_t TT = QPGeo::TT;
   constexpr uint32_t SX = (MW == 0 || MW == 3) ? 2 : 0, SP = (MP == 0 || MP == 3) ? 2 : 1;
   const uint64_t oQ1 = meta[1], oQ1p = meta[2];
@@ -1293,9 +1295,9 @@ __device__ __forceinline__ void quad_wq(const float* bw, const float* bp, const 
       const float2 px = rdp ? *reinterpret_cast<const float2*>(spv + 1024 + xi) : make_float2(0.f, 0.f);
       double G[4];
       widen4(a, G);
-      q0_rows_w<TT, MW, false>(G, rx, of, om, ux.x, px.x, ux.y, px.y, src, prev, nullptr, ba);
+      q0_rows_w<TT, MW, DF>(G, rx, of, om, ux.x, px.x, ux.y, px.y, src, prev, dst, ba);
       widen4(b, G);
-      q0_rows_w<TT, MW, false>(G, rx + 1, of, om, ux.y, px.y, ux.x, px.x, src, prev, nullptr, ba);
+      q0_rows_w<TT, MW, DF>(G, rx + 1, of, om, ux.y, px.y, ux.x, px.x, src, prev, dst, ba);
     }
   }
   double tq[4];
@@ -1314,10 +1316,9 @@ __device__ __forceinline__ void quad_wq(const float* bw, const float* bp, const 
       const float2 pq = rdp ? *reinterpret_cast<const float2*>(spv + 1536 + pi) : make_float2(0.f, 0.f);
       double G[4];
       widen4(ap, G);
-      q0_rows_w<TT, MP, false>(G, rp, opf, opm, up.x, pq.x, up.y, pq.y, src, prev, nullptr, ba);
+      q0_rows_w<TT, MP, DF>(G, rp, opf, opm, up.x, pq.x, up.y, pq.y, src, prev, dst, ba);
       widen4(bq, G);
-      q0_rows_w<TT, MP, false>(G, rp + 1, opf, opm, up.y, pq.y, up.x, pq.x, src, prev, nullptr,
-                               ba);
+      q0_rows_w<TT, MP, DF>(G, rp + 1, opf, opm, up.y, pq.y, up.x, pq.x, src, prev, dst, ba);
     }
   }
   double v[4];
@@ -1328,6 +1329,25 @@ __device__ __forceinline__ void quad_wq(const float* bw, const float* bp, const 
     float uu[4], pp[4] = {0, 0, 0, 0};
     ld4r(su + qi, uu);
     if (rdp) ld4r(spv + qi, pp);
+    if constexpr (DF) {
+      float st[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) st[k] = (float)v[k];
+      if (oQ1 != kNone)
+        st_out(reinterpret_cast<float4*>(dst + oQ1 + o0), make_float4(st[0], st[1], st[2], st[3]));
+      if (oQ1p != kNone)
+        st_out(reinterpret_cast<float4*>(dst + oQ1p + qb), make_float4(st[3], st[1], st[2], st[0]));
+      if (oQ1 != kNone) {
+#pragma unroll
+        for (int k = 0; k < 4; ++k) dacc((double)uu[k], v[k], (double)st[k], ba);
+      } else {
+        dacc((double)uu[3], v[0], (double)st[0], ba);
+        dacc((double)uu[1], v[1], (double)st[1], ba);
+        dacc((double)uu[2], v[2], (double)st[2], ba);
+        dacc((double)uu[0], v[3], (double)st[3], ba);
+      }
+      return;
+    }
     if (oQ1 != kNone) {
 #pragma unroll
       for (int k = 0; k < 4; ++k) bacc((double)uu[k], (double)pp[k], v[k], ba);
@@ -1340,24 +1360,25 @@ __device__ __forceinline__ void quad_wq(const float* bw, const float* bp, const 
   }
 }
 
-template <int MW, int MP>
+template <int MW, int MP, bool DF>
 __device__ __forceinline__ void qpw_item(const float* qbuf, uint64_t* full, uint64_t* empty,
                                          const uint64_t* meta, bool self, const float* src,
-                                         const float* prev, BAcc& ba, uint32_t tid, int lane) {
+                                         const float* prev, BAcc& ba, uint32_t tid, int lane,
+                                         float* dst) {
 #pragma unroll 1
   for (int q = 0; q < 4; ++q) {
     const int b = q & 1;
     if (q) QP_WAIT(&full[b], (uint32_t)(q >> 1));
     const float* buf = qbuf + (size_t)b * kQWBuf;
-    quad_wq<MW, MP>(buf, buf + 2048, buf + 4096, buf + 6144, meta, self, src, prev, ba,
-                    tid + kThreads * (uint32_t)q);
+    quad_wq<MW, MP, DF>(buf, buf + 2048, buf + 4096, buf + 6144, meta, self, src, prev, ba,
+                        tid + kThreads * (uint32_t)q, dst);
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[b]);
   }
 }
 
 constexpr int kQPWThreads = kThreads + 32;  // the bound pass: 8 consumer warps + the producer
-template <int DEPTH>
+template <int DEPTH, bool DF>
 __global__ void __launch_bounds__(kQPWThreads, 3) bin2q_qpw_kernel(Bin2QArgs a) {
   constexpr int M = 6;
   constexpr uint32_t TT = QPGeo::TT, Q = QPGeo::Q, LOG = 2 * M;
@@ -1376,7 +1397,10 @@ __global__ void __launch_bounds__(kQPWThreads, 3) bin2q_qpw_kernel(Bin2QArgs a) 
   g.kmask = a.geo[4];
   g.ntiles = a.geo[5];
   const float* src = reinterpret_cast<const float*>(a.src);
-  const float* prev = reinterpret_cast<const float*>(a.prev);
+  // DF (tracking sweep): the table read is staged at the outputs, v_prev is not read, the new
+  // values go to dst
+  const float* prev = DF ? nullptr : reinterpret_cast<const float*>(a.prev);
+  float* dst = DF ? reinterpret_cast<float*>(a.dst) : nullptr;
   const uint32_t* map = a.map;
   const int tid = threadIdx.x;
   const uint64_t G = gridDim.x;
@@ -1494,7 +1518,7 @@ __global__ void __launch_bounds__(kQPWThreads, 3) bin2q_qpw_kernel(Bin2QArgs a) 
     const uint32_t mw = modes & 3u, mp = (modes >> 2) & 3u;
     const bool self = (modes & 16u) != 0;
 #define LCSB_QPW(MW, MP) \
-  qpw_item<MW, MP>(qbuf, bars, empty, meta, self, src, prev, ba, (uint32_t)tid, lane)
+  qpw_item<MW, MP, DF>(qbuf, bars, empty, meta, self, src, prev, ba, (uint32_t)tid, lane, dst)
     switch (mw * 4 + mp) {
       case 0: LCSB_QPW(0, 0); break;
       case 1: LCSB_QPW(0, 1); break;
@@ -1541,17 +1565,17 @@ __global__ void __launch_bounds__(kQPWThreads, 3) bin2q_qpw_kernel(Bin2QArgs a) 
   }
 }
 
-template <int DEPTH>
+template <int DEPTH, bool DF = false>
 cudaError_t launch_qpw(const Bin2QArgs& a, cudaStream_t s, int sms) {
   constexpr size_t SMEM = 2 * kQWBuf * sizeof(float) + 4 * sizeof(uint64_t) +
                           2 * kQPMeta * sizeof(uint64_t);
   static uint64_t cap = 0;
   if (cap == 0) {
-    cudaError_t e = cudaFuncSetAttribute(bin2q_qpw_kernel<DEPTH>,
+    cudaError_t e = cudaFuncSetAttribute(bin2q_qpw_kernel<DEPTH, DF>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM);
     if (e != cudaSuccess) return e;
     int per_sm = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, bin2q_qpw_kernel<DEPTH>,
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, bin2q_qpw_kernel<DEPTH, DF>,
                                                       kQPWThreads, SMEM) != cudaSuccess ||
         per_sm < 1) {
       cudaGetLastError();
@@ -1571,7 +1595,7 @@ cudaError_t launch_qpw(const Bin2QArgs& a, cudaStream_t s, int sms) {
   b.geo[3] = 0x5555555555555555ull & b.geo[0];
   b.geo[4] = (1ull << (2 * a.K)) - 1;
   b.geo[5] = 1ull << (2 * (a.ell - 7));
-  bin2q_qpw_kernel<DEPTH><<<(unsigned)blocks, kQPWThreads, SMEM, s>>>(b);
+  bin2q_qpw_kernel<DEPTH, DF><<<(unsigned)blocks, kQPWThreads, SMEM, s>>>(b);
   return cudaGetLastError();
 }
 

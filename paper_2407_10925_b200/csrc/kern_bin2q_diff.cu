@@ -9,6 +9,15 @@
 
 namespace lcsbk {
 
+static bool qpw_on() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("LCSB_QPW");
+    v = e ? atoi(e) : 1;
+  }
+  return v != 0;
+}
+
 cudaError_t launch_bin2q_diff(const Bin2QArgs& a, int dtype, int M, cudaStream_t s, int sms) {
   if (a.ost || a.base) return cudaErrorInvalidValue;  // plain storage only
   constexpr bool W = false, DF = true;
@@ -17,6 +26,10 @@ cudaError_t launch_bin2q_diff(const Bin2QArgs& a, int dtype, int M, cudaStream_t
   if (dtype == LCSB_F32) {
     switch (M) {
       case 6:
+        // the staged quarter-pipelined pass of the bound in its tracking-sweep form (default;
+        // LCSB_QPW=0: the direct-load walks below)
+        if (qpw_on() && a.K >= 7)
+          return dyn ? launch_qpw<3, true>(a, s, sms) : launch_qpw<1, true>(a, s, sms);
         // the register-lean fp32 walk (pair_quads_w32) at 3 CTAs/SM, like the bound pass
         // (LCSB_DIFF_MINB=2, A/B: 2 CTAs/SM, no register cap spills)
         if (getenv("LCSB_DIFF_MINB") && atoi(getenv("LCSB_DIFF_MINB")) == 2)
