@@ -44,12 +44,18 @@
 //  * Residual storage (RES, reading R24): the table holds a residual e against a fixed fp32 base
 //    H (v = H + e + o); every window is loaded from both and added in fp64 (exact), outputs
 //    store round((F + shift) - H[x]) and the bound reads H at the outputs too.
+//  * fp32 tiles of 4^6 (the config-4/5 default, round 2): bin2q_qp_kernel pipelines the sweep by
+//    window quarters (quad tid + 256 q of every thread reads one quarter of each window) with a
+//    producer warp, and bin2q_qpw_kernel does the same for the bound pass and the tracking sweep
+//    (DIFF, reading R25) with u (and v_prev) at each quarter's outputs staged by TMA; the
+//    whole-stage bin2q_kernel remains for the other tiles, fp64 and the A/B knobs.
 #include <math.h>
 #include <stdlib.h>
 
-// The kernel templates live here; the instantiations are split over three translation units
+// The kernel templates live here; the instantiations are split over four translation units
 // (compiled in parallel): kern_bin2q.cu (the sweep), kern_bin2q_bound.cu (the one-pass bound),
-// kern_bin2q_ext.cu (the integer-offset and residual-storage sweeps).
+// kern_bin2q_ext.cu (the integer-offset and residual-storage sweeps), kern_bin2q_diff.cu (the
+// tracking sweep).
 #include "lcsb_internal.cuh"
 #include "tma.cuh"
 
