@@ -7,9 +7,9 @@ lcsb_sweep(S) + lcsb_bound.  metric = logical state-updates per second (sigma^(d
   python bench.py [--gpus N] [--steps K] [--warmup W] [--workload config4] [--impl ours|reference]
 
 Prints ONE JSON line on rank 0.  N = 1 runs config 4 (l = 17, the largest single-GPU config);
-under torchrun (N > 1) the ranks run config 5 (l = 18) with the half table sharded over the N
-GPUs (NCCL communicator + CUDA-IPC peer stores inside the library), timed as the
-max over ranks, or `--workload config3` (sigma = 4, the q4 table sharded, §9b; strong scaling of
+under torchrun (N > 1) the ranks run config 5 (l = 18) with the symmetry-folded table sharded
+over the N GPUs (one virtual address range per table over the shards' memory,
+peer reads and stores over NVLink, NCCL or host collectives), timed as the max over ranks, or `--workload config3` (sigma = 4, the q4 table sharded, §9b; strong scaling of
 the same workload as its N = 1 line).  For config 5 rank 0 also times the same sharded-path
 kernel on one GPU at l = 17 (`config.u1_same_kernel`), so U_P / (P U_1) is
 computable from the line.  `--impl reference` times the CPU oracle (oracle/, the reference arm
