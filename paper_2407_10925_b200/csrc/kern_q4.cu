@@ -378,17 +378,36 @@ __global__ void __launch_bounds__(kThreads, GR ? 4 : (WMODE ? 1 : 3)) q4_kernel(
         bS[1] = 0.25 * sum4<T, false, WMODE>(ubS + 1 * C::WB + offS, sh);
         bS[2] = 0.25 * sum4<T, true, WMODE>(ubCS + 1 * C::WB + offCS, sh);
         bS[3] = 0.25 * sum4<T, true, WMODE>(ubCS + 0 * C::WB + offCS, sh);
+        // fp32 storage, sweep: round32(max(a, b, c)) = max(round32(a), round32(b), round32(c))
+        // (rounding is monotone), so the candidates are rounded once each (7 conversions instead
+        // of 8 fp64 max chains + 8 conversions) and the maxima taken in fp32 (one FMNMX each; no
+        // NaN, no -0); the stored values are unchanged bit for bit
+        [[maybe_unused]] float fU[2], fS[4], fpu = 0.f, fsame = 0.f;
+        if constexpr (sizeof(T) == 4 && !WMODE) {
+          fU[0] = (float)bU[0];
+          fU[1] = (float)bU[1];
+#pragma unroll
+          for (int hb = 0; hb < 4; ++hb) fS[hb] = (float)bS[hb];
+          fpu = (float)pu;
+          fsame = (float)(1.0 + pu);
+        }
 #pragma unroll
         for (int ha = 0; ha < 2; ++ha) {
 #pragma unroll
           for (int hb = 0; hb < 4; ++hb) {
             double v;
-            if (ha == hb)  // 1 + max(0, P): P is a mean of non-negative iterates, so P >= 0
+            if constexpr (sizeof(T) == 4 && !WMODE) {
+              const float v32 = (ha == hb) ? fsame
+                                           : (ta ? fmaxf(fU[ha], fS[hb])
+                                                 : fmaxf(fmaxf(fU[ha], fS[hb]), fpu));
+              v = (double)v32;  // exact; (T)v below gives v32 back
+            } else if (ha == hb) {  // 1 + max(0, P): P is a mean of non-negative iterates, P >= 0
               v = 1.0 + pu;
-            else if (ta)
+            } else if (ta) {
               v = dmax(bU[ha], bS[hb]);  // two-array: no drop-both option (reading R20)
-            else
+            } else {
               v = dmax(dmax(bU[ha], bS[hb]), pu);  // adv_b, adv_a, P
+            }
             const int hh = ha * 4 + hb;
             if (!WMODE) {
               // the head bits sit above the tail bits: | == +, so the row pointer is per unit
