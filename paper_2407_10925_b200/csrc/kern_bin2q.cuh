@@ -1366,6 +1366,120 @@ __device__ __forceinline__ void quad_wq(const float* bw, const float* bp, const 
   }
 }
 
+// The staged bound pass splits quad_wq in two (round 2): the (mode x mode)-specific window loads,
+// the groups put into logical order (register renaming), and one mode-independent part for the
+// fp64 arithmetic, the staged u / v_prev and the reductions, shared by the sixteen combinations
+// (sixteen full copies kept ~30 % of the warps waiting on instruction fetch)
+template <int MW, int MP>
+__device__ __forceinline__ void wq_load(const float* bw, const float* bp, uint32_t qd,
+                                        float (&a)[4], float (&b)[4], float (&ap)[4],
+                                        float (&bq)[4]) {
+  constexpr uint32_t TT = QPGeo::TT;
+  constexpr uint32_t SX = (MW == 0 || MW == 3) ? 2 : 0, SP = (MP == 0 || MP == 3) ? 2 : 1;
+  const uint32_t o0 = 4 * qd;
+  const uint32_t g = 2 * pairswap32(o0), u = 2 * (TT - 4 - o0);
+  const bool sx = (qd >> SX) & 1u, sp = (qd >> SP) & 1u;
+  float X1[4], X2[4], P1[4], P2[4], A[4], B[4], Ap[4], Bp[4];
+  ld4r(bw + qloc<TT, MW>(gbase<TT, MW>(sx ? g + 4 : g)), X1);
+  ld4r(bw + qloc<TT, MW>(gbase<TT, MW>(sx ? g : g + 4)), X2);
+  ld4r(bp + qloc<TT, MP>(gbase<TT, MP>(sp ? u + 4 : u)), P1);
+  ld4r(bp + qloc<TT, MP>(gbase<TT, MP>(sp ? u : u + 4)), P2);
+  sel4f(sx, X1, X2, A, B);
+  sel4f(sp, P1, P2, Ap, Bp);
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    a[k] = A[comp<MW>(k)];
+    b[k] = B[comp<MW>(k)];
+    ap[k] = Ap[comp<MP>(k)];
+    bq[k] = Bp[comp<MP>(k)];
+  }
+}
+// the rest of quad_wq on logical-order groups (identical values and reductions)
+template <bool DF>
+__device__ __forceinline__ void wq_common(const float (&a)[4], const float (&b)[4],
+                                          const float (&ap)[4], const float (&bq)[4],
+                                          const float* su, const float* spv,
+                                          const uint64_t* meta, bool self, const float* src,
+                                          const float* prev, BAcc& ba, uint32_t qd, float* dst) {
+  constexpr uint32_t TT = QPGeo::TT;
+  const uint64_t oQ1 = meta[1], oQ1p = meta[2];
+  const uint64_t of = meta[3], om = meta[4], opf = meta[5], opm = meta[6];
+  const bool rows_x = of != kNone || om != kNone;
+  const bool rows_p = !self && (opf != kNone || opm != kNone);
+  const bool rdp = prev != nullptr;
+  const uint32_t o0 = 4 * qd;
+  const uint32_t g = 2 * pairswap32(o0), u = 2 * (TT - 4 - o0);
+  const uint32_t qb = pairswap32(~o0 & (TT - 1) & ~3u);
+  const uint32_t rx = g >> 2, rp = u >> 2;
+  double tx[4];
+  tx[0] = (double)a[0] + (double)a[1];
+  tx[1] = (double)b[0] + (double)b[1];
+  tx[2] = (double)a[2] + (double)a[3];
+  tx[3] = (double)b[2] + (double)b[3];
+  if (rows_x) {
+    const uint32_t xi = of != kNone ? (rx & 511u) : (510u - (rx & 511u));
+    const float2 ux = *reinterpret_cast<const float2*>(su + 1024 + xi);
+    const float2 px = rdp ? *reinterpret_cast<const float2*>(spv + 1024 + xi) : make_float2(0.f, 0.f);
+    double G[4];
+    widen4(a, G);
+    q0_rows_w<TT, 0, DF>(G, rx, of, om, ux.x, px.x, ux.y, px.y, src, prev, dst, ba);
+    widen4(b, G);
+    q0_rows_w<TT, 0, DF>(G, rx + 1, of, om, ux.y, px.y, ux.x, px.x, src, prev, dst, ba);
+  }
+  double tq[4];
+  tq[0] = (double)bq[2] + (double)bq[3];
+  tq[1] = (double)bq[0] + (double)bq[1];
+  tq[2] = (double)ap[2] + (double)ap[3];
+  tq[3] = (double)ap[0] + (double)ap[1];
+  if (rows_p) {
+    const uint32_t pi = opf != kNone ? (rp & 511u) : (510u - (rp & 511u));
+    const float2 up = *reinterpret_cast<const float2*>(su + 1536 + pi);
+    const float2 pq = rdp ? *reinterpret_cast<const float2*>(spv + 1536 + pi) : make_float2(0.f, 0.f);
+    double G[4];
+    widen4(ap, G);
+    q0_rows_w<TT, 0, DF>(G, rp, opf, opm, up.x, pq.x, up.y, pq.y, src, prev, dst, ba);
+    widen4(bq, G);
+    q0_rows_w<TT, 0, DF>(G, rp + 1, opf, opm, up.y, pq.y, up.x, pq.x, src, prev, dst, ba);
+  }
+  double v[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) v[k] = 0.5 * dmax(tx[k], tq[k]);
+  if (oQ1 != kNone || oQ1p != kNone) {
+    const uint32_t qi = oQ1 != kNone ? (o0 & 1023u) : (qb & 1023u);
+    float uu[4], pp[4] = {0, 0, 0, 0};
+    ld4r(su + qi, uu);
+    if (rdp) ld4r(spv + qi, pp);
+    if constexpr (DF) {
+      float st[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) st[k] = (float)v[k];
+      if (oQ1 != kNone)
+        st_out(reinterpret_cast<float4*>(dst + oQ1 + o0), make_float4(st[0], st[1], st[2], st[3]));
+      if (oQ1p != kNone)
+        st_out(reinterpret_cast<float4*>(dst + oQ1p + qb), make_float4(st[3], st[1], st[2], st[0]));
+      if (oQ1 != kNone) {
+#pragma unroll
+        for (int k = 0; k < 4; ++k) dacc((double)uu[k], v[k], (double)st[k], ba);
+      } else {
+        dacc((double)uu[3], v[0], (double)st[0], ba);
+        dacc((double)uu[1], v[1], (double)st[1], ba);
+        dacc((double)uu[2], v[2], (double)st[2], ba);
+        dacc((double)uu[0], v[3], (double)st[3], ba);
+      }
+      return;
+    }
+    if (oQ1 != kNone) {
+#pragma unroll
+      for (int k = 0; k < 4; ++k) bacc((double)uu[k], (double)pp[k], v[k], ba);
+    } else {
+      bacc((double)uu[3], (double)pp[3], v[0], ba);
+      bacc((double)uu[1], (double)pp[1], v[1], ba);
+      bacc((double)uu[2], (double)pp[2], v[2], ba);
+      bacc((double)uu[0], (double)pp[0], v[3], ba);
+    }
+  }
+}
+
 template <int MW, int MP, bool DF>
 __device__ __forceinline__ void qpw_item(const float* qbuf, uint64_t* full, uint64_t* empty,
                                          const uint64_t* meta, bool self, const float* src,
@@ -1523,27 +1637,38 @@ __global__ void __launch_bounds__(kQPWThreads, 3) bin2q_qpw_kernel(Bin2QArgs a) 
     const uint32_t modes = (uint32_t)meta[0];
     const uint32_t mw = modes & 3u, mp = (modes >> 2) & 3u;
     const bool self = (modes & 16u) != 0;
-#define LCSB_QPW(MW, MP) \
-  qpw_item<MW, MP, DF>(qbuf, bars, empty, meta, self, src, prev, ba, (uint32_t)tid, lane, dst)
-    switch (mw * 4 + mp) {
-      case 0: LCSB_QPW(0, 0); break;
-      case 1: LCSB_QPW(0, 1); break;
-      case 2: LCSB_QPW(0, 2); break;
-      case 3: LCSB_QPW(0, 3); break;
-      case 4: LCSB_QPW(1, 0); break;
-      case 5: LCSB_QPW(1, 1); break;
-      case 6: LCSB_QPW(1, 2); break;
-      case 7: LCSB_QPW(1, 3); break;
-      case 8: LCSB_QPW(2, 0); break;
-      case 9: LCSB_QPW(2, 1); break;
-      case 10: LCSB_QPW(2, 2); break;
-      case 11: LCSB_QPW(2, 3); break;
-      case 12: LCSB_QPW(3, 0); break;
-      case 13: LCSB_QPW(3, 1); break;
-      case 14: LCSB_QPW(3, 2); break;
-      default: LCSB_QPW(3, 3); break;
-    }
+    const uint32_t combo = mw * 4 + mp;
+#pragma unroll 1
+    for (int q = 0; q < 4; ++q) {
+      const int bb = q & 1;
+      if (q) QP_WAIT(&bars[bb], (uint32_t)(q >> 1));
+      const float* buf = qbuf + (size_t)bb * kQWBuf;
+      const uint32_t qd = (uint32_t)tid + kThreads * (uint32_t)q;
+      float xa[4], xb[4], pa[4], pb[4];
+#define LCSB_QPW(MW, MP) wq_load<MW, MP>(buf, buf + 2048, qd, xa, xb, pa, pb)
+      switch (combo) {
+        case 0: LCSB_QPW(0, 0); break;
+        case 1: LCSB_QPW(0, 1); break;
+        case 2: LCSB_QPW(0, 2); break;
+        case 3: LCSB_QPW(0, 3); break;
+        case 4: LCSB_QPW(1, 0); break;
+        case 5: LCSB_QPW(1, 1); break;
+        case 6: LCSB_QPW(1, 2); break;
+        case 7: LCSB_QPW(1, 3); break;
+        case 8: LCSB_QPW(2, 0); break;
+        case 9: LCSB_QPW(2, 1); break;
+        case 10: LCSB_QPW(2, 2); break;
+        case 11: LCSB_QPW(2, 3); break;
+        case 12: LCSB_QPW(3, 0); break;
+        case 13: LCSB_QPW(3, 1); break;
+        case 14: LCSB_QPW(3, 2); break;
+        default: LCSB_QPW(3, 3); break;
+      }
 #undef LCSB_QPW
+      wq_common<DF>(xa, xb, pa, pb, buf + 4096, buf + 6144, meta, self, src, prev, ba, qd, dst);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[bb]);
+    }
   }
   // block reduction over the 8 consumer warps (named barrier 1: the producer has left)
   double x = ba.rmax, y = ba.rmin, z = ba.dmin;
