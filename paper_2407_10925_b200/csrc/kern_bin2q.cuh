@@ -1262,114 +1262,13 @@ __global__ void __launch_bounds__(kQPThreads, 3) bin2q_qp_kernel(Bin2QArgs a) {
 // v_prev 8 KB each), two per CTA; a producer warp refills them.  Same arithmetic and reductions
 // as the direct-load pass (bit-identical R, D).
 constexpr uint32_t kQWBuf = 8192;  // floats per quarter-step buffer
-// one quad of the staged bound pass: sx_ / sp_ = the staged u and v_prev of the quarter
-// ([Q1 1024 | x rows 512 | psi rows 512]); the arithmetic of quad_w32 (pair_quads_w32)
+// One quad of the staged bound pass (round 2), in two parts: the (mode x mode)-specific window
+// loads, the groups put into logical order (register renaming), and one mode-independent part
+// for the fp64 arithmetic of quad_w32 (pair_quads_w32), the staged u / v_prev (the quarter's
+// [Q1 1024 | x rows 512 | psi rows 512]) and the reductions, shared by the sixteen combinations
+// (sixteen full copies of the whole quad kept ~30 % of the warps waiting on instruction fetch).
 // DF (the tracking sweep of reading R25): store round32(F) at every stored output and reduce
-// against the staged u (dacc), as quad_w32<..., DIFF>; v_prev is not read
-template <int MW, int MP, bool DF = false>
-__device__ __forceinline__ void quad_wq(const float* bw, const float* bp, const float* su,
-                                        const float* spv, const uint64_t* meta, bool self,
-                                        const float* src, const float* prev, BAcc& ba,
-                                        uint32_t qd, float* dst = nullptr) {
-  constexpr uint32_t TT = QPGeo::TT;
-  constexpr uint32_t SX = (MW == 0 || MW == 3) ? 2 : 0, SP = (MP == 0 || MP == 3) ? 2 : 1;
-  const uint64_t oQ1 = meta[1], oQ1p = meta[2];
-  const uint64_t of = meta[3], om = meta[4], opf = meta[5], opm = meta[6];
-  const bool rows_x = of != kNone || om != kNone;
-  const bool rows_p = !self && (opf != kNone || opm != kNone);
-  const bool rdp = prev != nullptr;
-  const uint32_t o0 = 4 * qd;
-  const uint32_t g = 2 * pairswap32(o0), u = 2 * (TT - 4 - o0);
-  const uint32_t qb = pairswap32(~o0 & (TT - 1) & ~3u);
-  const uint32_t rx = g >> 2, rp = u >> 2;
-  const bool sx = (qd >> SX) & 1u, sp = (qd >> SP) & 1u;
-  constexpr uint32_t c0 = comp<MW>(0), c1 = comp<MW>(1), c2 = comp<MW>(2), c3 = comp<MW>(3);
-  constexpr uint32_t d0 = comp<MP>(0), d1 = comp<MP>(1), d2 = comp<MP>(2), d3 = comp<MP>(3);
-  double tx[4];
-  {
-    float X1[4], X2[4], a[4], b[4];
-    ld4r(bw + qloc<TT, MW>(gbase<TT, MW>(sx ? g + 4 : g)), X1);
-    ld4r(bw + qloc<TT, MW>(gbase<TT, MW>(sx ? g : g + 4)), X2);
-    sel4f(sx, X1, X2, a, b);
-    tx[0] = (double)a[c0] + (double)a[c1];
-    tx[1] = (double)b[c0] + (double)b[c1];
-    tx[2] = (double)a[c2] + (double)a[c3];
-    tx[3] = (double)b[c2] + (double)b[c3];
-    if (rows_x) {  // staged pair: the row run's (rows rx, rx + 1) or the mirror run's (rx + 1, rx)
-      const uint32_t xi = of != kNone ? (rx & 511u) : (510u - (rx & 511u));
-      const float2 ux = *reinterpret_cast<const float2*>(su + 1024 + xi);
-      const float2 px = rdp ? *reinterpret_cast<const float2*>(spv + 1024 + xi) : make_float2(0.f, 0.f);
-      double G[4];
-      widen4(a, G);
-      q0_rows_w<TT, MW, DF>(G, rx, of, om, ux.x, px.x, ux.y, px.y, src, prev, dst, ba);
-      widen4(b, G);
-      q0_rows_w<TT, MW, DF>(G, rx + 1, of, om, ux.y, px.y, ux.x, px.x, src, prev, dst, ba);
-    }
-  }
-  double tq[4];
-  {
-    float P1[4], P2[4], ap[4], bq[4];
-    ld4r(bp + qloc<TT, MP>(gbase<TT, MP>(sp ? u + 4 : u)), P1);
-    ld4r(bp + qloc<TT, MP>(gbase<TT, MP>(sp ? u : u + 4)), P2);
-    sel4f(sp, P1, P2, ap, bq);
-    tq[0] = (double)bq[d2] + (double)bq[d3];
-    tq[1] = (double)bq[d0] + (double)bq[d1];
-    tq[2] = (double)ap[d2] + (double)ap[d3];
-    tq[3] = (double)ap[d0] + (double)ap[d1];
-    if (rows_p) {
-      const uint32_t pi = opf != kNone ? (rp & 511u) : (510u - (rp & 511u));
-      const float2 up = *reinterpret_cast<const float2*>(su + 1536 + pi);
-      const float2 pq = rdp ? *reinterpret_cast<const float2*>(spv + 1536 + pi) : make_float2(0.f, 0.f);
-      double G[4];
-      widen4(ap, G);
-      q0_rows_w<TT, MP, DF>(G, rp, opf, opm, up.x, pq.x, up.y, pq.y, src, prev, dst, ba);
-      widen4(bq, G);
-      q0_rows_w<TT, MP, DF>(G, rp + 1, opf, opm, up.y, pq.y, up.x, pq.x, src, prev, dst, ba);
-    }
-  }
-  double v[4];
-#pragma unroll
-  for (int k = 0; k < 4; ++k) v[k] = 0.5 * dmax(tx[k], tq[k]);
-  if (oQ1 != kNone || oQ1p != kNone) {
-    const uint32_t qi = oQ1 != kNone ? (o0 & 1023u) : (qb & 1023u);
-    float uu[4], pp[4] = {0, 0, 0, 0};
-    ld4r(su + qi, uu);
-    if (rdp) ld4r(spv + qi, pp);
-    if constexpr (DF) {
-      float st[4];
-#pragma unroll
-      for (int k = 0; k < 4; ++k) st[k] = (float)v[k];
-      if (oQ1 != kNone)
-        st_out(reinterpret_cast<float4*>(dst + oQ1 + o0), make_float4(st[0], st[1], st[2], st[3]));
-      if (oQ1p != kNone)
-        st_out(reinterpret_cast<float4*>(dst + oQ1p + qb), make_float4(st[3], st[1], st[2], st[0]));
-      if (oQ1 != kNone) {
-#pragma unroll
-        for (int k = 0; k < 4; ++k) dacc((double)uu[k], v[k], (double)st[k], ba);
-      } else {
-        dacc((double)uu[3], v[0], (double)st[0], ba);
-        dacc((double)uu[1], v[1], (double)st[1], ba);
-        dacc((double)uu[2], v[2], (double)st[2], ba);
-        dacc((double)uu[0], v[3], (double)st[3], ba);
-      }
-      return;
-    }
-    if (oQ1 != kNone) {
-#pragma unroll
-      for (int k = 0; k < 4; ++k) bacc((double)uu[k], (double)pp[k], v[k], ba);
-    } else {  // position j of the psi run holds output (3, 1, 2, 0)[j]
-      bacc((double)uu[3], (double)pp[3], v[0], ba);
-      bacc((double)uu[1], (double)pp[1], v[1], ba);
-      bacc((double)uu[2], (double)pp[2], v[2], ba);
-      bacc((double)uu[0], (double)pp[0], v[3], ba);
-    }
-  }
-}
-
-// The staged bound pass splits quad_wq in two (round 2): the (mode x mode)-specific window loads,
-// the groups put into logical order (register renaming), and one mode-independent part for the
-// fp64 arithmetic, the staged u / v_prev and the reductions, shared by the sixteen combinations
-// (sixteen full copies kept ~30 % of the warps waiting on instruction fetch)
+// against the staged u (dacc), as quad_w32<..., DIFF>; v_prev is not read.
 template <int MW, int MP>
 __device__ __forceinline__ void wq_load(const float* bw, const float* bp, uint32_t qd,
                                         float (&a)[4], float (&b)[4], float (&ap)[4],
@@ -1394,7 +1293,7 @@ __device__ __forceinline__ void wq_load(const float* bw, const float* bp, uint32
     bq[k] = Bp[comp<MP>(k)];
   }
 }
-// the rest of quad_wq on logical-order groups (identical values and reductions)
+// the mode-independent part on logical-order groups
 template <bool DF>
 __device__ __forceinline__ void wq_common(const float (&a)[4], const float (&b)[4],
                                           const float (&ap)[4], const float (&bq)[4],
@@ -1477,23 +1376,6 @@ __device__ __forceinline__ void wq_common(const float (&a)[4], const float (&b)[
       bacc((double)uu[2], (double)pp[2], v[2], ba);
       bacc((double)uu[0], (double)pp[0], v[3], ba);
     }
-  }
-}
-
-template <int MW, int MP, bool DF>
-__device__ __forceinline__ void qpw_item(const float* qbuf, uint64_t* full, uint64_t* empty,
-                                         const uint64_t* meta, bool self, const float* src,
-                                         const float* prev, BAcc& ba, uint32_t tid, int lane,
-                                         float* dst) {
-#pragma unroll 1
-  for (int q = 0; q < 4; ++q) {
-    const int b = q & 1;
-    if (q) QP_WAIT(&full[b], (uint32_t)(q >> 1));
-    const float* buf = qbuf + (size_t)b * kQWBuf;
-    quad_wq<MW, MP, DF>(buf, buf + 2048, buf + 4096, buf + 6144, meta, self, src, prev, ba,
-                        tid + kThreads * (uint32_t)q, dst);
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&empty[b]);
   }
 }
 
