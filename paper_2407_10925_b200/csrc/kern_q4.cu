@@ -279,7 +279,7 @@ __device__ __forceinline__ double row16_sum(const T* p) {
 }
 
 template <typename T, int M, int S, bool WMODE, bool GR = false, bool SH = false>
-__global__ void __launch_bounds__(kThreads, GR ? 4 : (WMODE ? 1 : 3)) q4_kernel(Q4Args a) {
+__global__ void __launch_bounds__(kThreads, GR ? 4 : ((WMODE && sizeof(T) == 8) ? 1 : 3)) q4_kernel(Q4Args a) {
   using C = Q4Cfg<T, M, S, WMODE, GR>;
   constexpr uint32_t TT = C::TT;
   extern __shared__ __align__(128) unsigned char smem_raw[];
