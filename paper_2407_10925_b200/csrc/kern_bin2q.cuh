@@ -420,6 +420,8 @@ __device__ __forceinline__ void q0_rows_w(const double (&G)[4], uint32_t r, uint
                                           uint64_t om, float fu, float fpv, float mu, float mpv,
                                           const float* src, const float* prev, float* dst,
                                           BAcc& ba) {
+  (void)fpv;
+  (void)mpv;  // v_prev: unused by the tracking sweep (DIFF)
   const double v0 = G[comp<MODE>(0)], v1 = G[comp<MODE>(1)], v2 = G[comp<MODE>(2)],
                v3 = G[comp<MODE>(3)];
   if (of != kNone) {
@@ -436,7 +438,9 @@ __device__ __forceinline__ void q0_rows_w(const double (&G)[4], uint32_t r, uint
     const uint32_t rm = TT / 2 - 1 - r;
     if (of != kNone) {  // both runs stored: the caller loaded the row run's entries
       mu = __ldcs(src + om + rm);
-      if (!DIFF && prev) mpv = __ldcs(prev + om + rm);
+      if constexpr (!DIFF) {
+        if (prev) mpv = __ldcs(prev + om + rm);
+      }
     }
     const double f = q0_val(v3, v2, v1, v0);
     if constexpr (DIFF) {
@@ -1053,6 +1057,98 @@ __device__ __forceinline__ void qp_issue_win(float* dst, const float* gs, uint32
 }
 constexpr int kQPMeta = 10;  // per item: [0] modes, [1..6] runs, [7] end, [8] / [9] window starts
 
+// The producer side shared by bin2q_qp_kernel and bin2q_qpw_kernel (one lane of the producer
+// warp): item claims as bin2q_kernel (the L2 schedule with the dynamic work counter, else static
+// round robin), pipelined DEPTH deep (3: claim two items ahead, load the schedule entry one
+// ahead), and each item's metadata -- modes, stored output runs, window starts -- from the map
+// entries requested one item earlier.
+template <int DEPTH>
+struct QPItems {
+  static constexpr int M = 6;
+  static constexpr uint32_t TT = QPGeo::TT, LOG = 2 * M;
+  QGeo g;
+  const float* src;
+  const uint32_t* map;
+  const uint32_t* sched;
+  unsigned long long* counter;
+  uint64_t nitems, G;
+  uint64_t pc = 0, p1 = 0, p2 = 0;
+  uint32_t e0 = 0, e1 = 0;
+  QItem pit;
+  __device__ explicit QPItems(const Bin2QArgs& a) {
+    g.K = a.K;
+    g.lmask = a.geo[0];
+    g.q1 = a.geo[1];
+    g.amask = a.geo[2];
+    g.bmask = a.geo[3];
+    g.kmask = a.geo[4];
+    g.ntiles = a.geo[5];
+    src = reinterpret_cast<const float*>(a.src);
+    map = a.map;
+    sched = (a.sched && a.sched_m == M) ? a.sched : nullptr;
+    nitems = sched ? a.nitems : g.ntiles;
+    counter = sched ? a.counter : nullptr;
+    G = gridDim.x;
+  }
+  __device__ uint64_t claim(uint64_t prev) {
+    if (counter) return (uint64_t)atomicAdd(counter, 1ull);
+    const uint64_t c = prev == ~0ull ? (uint64_t)blockIdx.x : prev + G;
+    return sched ? c : qnext(g, c, G, LOG);
+  }
+  __device__ uint32_t ent_of(uint64_t c) const {
+    return c < nitems ? (sched ? __ldg(sched + c) : (uint32_t)c) : 0u;
+  }
+  __device__ uint64_t tile_e(uint32_t e) const {
+    return sched ? (uint64_t)(e & kQTileMask) : (uint64_t)e;
+  }
+  __device__ void start() {
+    pc = claim(~0ull);
+    if constexpr (DEPTH == 3) {
+      p1 = claim(pc);
+      p2 = claim(p1);
+      e1 = ent_of(p1);
+    }
+    e0 = ent_of(pc);
+    if (pc < nitems) qlookup<M, false>(g, map, tile_e(e0), pit);
+  }
+  // the metadata of item pc into meta (false and the end marker when no item is left), then
+  // the pipeline moves on and the map entries of the new pc are requested
+  __device__ bool prep(uint64_t* meta) {
+    if (pc >= nitems) {
+      meta[7] = 1;
+      return false;
+    }
+    const uint64_t tau = tile_e(e0);
+    uint64_t x0, p0, taup;
+    qtile(g, tau, LOG, x0, p0, taup);
+    const bool self = taup == tau;
+    const uint64_t wb = qwin(g, x0), wp = qwin(g, p0);
+    const uint64_t yf = wb >> 2, ym = g.q1 - yf - TT / 2, ypf = wp >> 2, ypm = g.q1 - ypf - TT / 2;
+    meta[0] = (pit.m[0] & 3u) | ((pit.m[1] & 3u) << 2) | (self ? 16u : 0u);
+    meta[1] = qrun(g, pit.m[2], x0);
+    meta[2] = self ? kNone : qrun(g, pit.m[3], p0);
+    meta[3] = qrun(g, pit.m[4], yf);
+    meta[4] = qrun(g, pit.m[5], ym);
+    meta[5] = self ? kNone : qrun(g, pit.m[6], ypf);
+    meta[6] = self ? kNone : qrun(g, pit.m[7], ypm);
+    meta[7] = 0;
+    meta[8] = reinterpret_cast<uint64_t>(qp_wstart(g, src, pit.m[0], wb));
+    meta[9] = reinterpret_cast<uint64_t>(qp_wstart(g, src, pit.m[1], wp));
+    if constexpr (DEPTH == 1) {
+      pc = claim(pc);
+      e0 = ent_of(pc);
+    } else {
+      pc = p1;
+      e0 = e1;
+      p1 = p2;
+      e1 = ent_of(p1);
+      p2 = claim(p2);
+    }
+    if (pc < nitems) qlookup<M, false>(g, map, tile_e(e0), pit);
+    return true;
+  }
+};
+
 // LCSB_QP_SPIN (A/B): plain probe loops instead of the suspend-hint waits
 #ifdef LCSB_QP_SPIN
 #define QP_WAIT mbar_wait
@@ -1094,80 +1190,16 @@ constexpr int kQPThreads = kQPC + 32;
 template <int DEPTH>
 __global__ void __launch_bounds__(kQPThreads, 3) bin2q_qp_kernel(Bin2QArgs a) {
   constexpr int M = 6;
-  constexpr uint32_t TT = QPGeo::TT, Q = QPGeo::Q, LOG = 2 * M;
+  constexpr uint32_t TT = QPGeo::TT, Q = QPGeo::Q;
   static_assert(TT == (1u << (2 * M)) && TT / 4 == 4 * kThreads, "256 quads per quarter");
   extern __shared__ __align__(128) unsigned char smem_raw[];
   float* qbuf = reinterpret_cast<float*>(smem_raw);  // [quarter][x / psi][Q]
   uint64_t* bars = reinterpret_cast<uint64_t*>(qbuf + 8 * Q);  // full[4]
   uint64_t* empty = bars + 4;                                  // empty[4]
   uint64_t* metas = empty + 4;                                 // [2][kQPMeta]
-  QGeo g;
-  g.K = a.K;
-  g.lmask = a.geo[0];
-  g.q1 = a.geo[1];
-  g.amask = a.geo[2];
-  g.bmask = a.geo[3];
-  g.kmask = a.geo[4];
-  g.ntiles = a.geo[5];
-  const float* src = reinterpret_cast<const float*>(a.src);
   float* dst = reinterpret_cast<float*>(a.dst);
-  const uint32_t* map = a.map;
+  const float* src = reinterpret_cast<const float*>(a.src);
   const int tid = threadIdx.x;
-  const uint64_t G = gridDim.x;
-  // item claims exactly as bin2q_kernel (schedule + dynamic counter, else static round robin)
-  const uint32_t* sched = (a.sched && a.sched_m == M) ? a.sched : nullptr;
-  const uint64_t nitems = sched ? a.nitems : g.ntiles;
-  unsigned long long* counter = sched ? a.counter : nullptr;
-  auto first = [&](uint64_t c) { return sched ? c : qnext(g, c, G, LOG); };
-  auto claim = [&](uint64_t prev) -> uint64_t {
-    if (counter) return (uint64_t)atomicAdd(counter, 1ull);
-    return first(prev == ~0ull ? (uint64_t)blockIdx.x : prev + G);
-  };
-  auto entry = [&](uint64_t c) -> uint32_t { return sched ? __ldg(sched + c) : (uint32_t)c; };
-  auto ent_of = [&](uint64_t c) -> uint32_t { return c < nitems ? entry(c) : 0u; };
-  auto tile_e = [&](uint32_t e) -> uint64_t {
-    return sched ? (uint64_t)(e & kQTileMask) : (uint64_t)e;
-  };
-  uint64_t pc = 0, p1 = 0, p2 = 0;
-  uint32_t e0 = 0, e1 = 0;
-  QItem pit;
-  // thread 0: the metadata of item pc (or the end marker) into slot `slot`, then the claim
-  // pipeline moves on (depth 3: claim two items ahead, the schedule entry one) and the map
-  // entries of the new pc are requested (used one item later)
-  auto prep = [&](int slot) {
-    uint64_t* meta = metas + kQPMeta * slot;
-    if (pc >= nitems) {
-      meta[7] = 1;
-      return;
-    }
-    const uint64_t tau = tile_e(e0);
-    uint64_t x0, p0, taup;
-    qtile(g, tau, LOG, x0, p0, taup);
-    const bool self = taup == tau;
-    const uint64_t wb = qwin(g, x0), wp = qwin(g, p0);
-    const uint64_t yf = wb >> 2, ym = g.q1 - yf - TT / 2, ypf = wp >> 2, ypm = g.q1 - ypf - TT / 2;
-    meta[0] = (pit.m[0] & 3u) | ((pit.m[1] & 3u) << 2) | (self ? 16u : 0u);
-    meta[1] = qrun(g, pit.m[2], x0);
-    meta[2] = self ? kNone : qrun(g, pit.m[3], p0);
-    meta[3] = qrun(g, pit.m[4], yf);
-    meta[4] = qrun(g, pit.m[5], ym);
-    meta[5] = self ? kNone : qrun(g, pit.m[6], ypf);
-    meta[6] = self ? kNone : qrun(g, pit.m[7], ypm);
-    meta[7] = 0;
-    meta[8] = reinterpret_cast<uint64_t>(qp_wstart(g, src, pit.m[0], wb));
-    meta[9] = reinterpret_cast<uint64_t>(qp_wstart(g, src, pit.m[1], wp));
-    if constexpr (DEPTH == 1) {
-      pc = claim(pc);
-      e0 = ent_of(pc);
-    } else {
-      pc = p1;
-      e0 = e1;
-      p1 = p2;
-      e1 = ent_of(p1);
-      p2 = claim(p2);
-    }
-    if (pc < nitems) qlookup<M, false>(g, map, tile_e(e0), pit);
-  };
   // thread 0: quarter q of the item in `slot` (or a plain arrive after the last item)
   auto issue = [&](int q, int slot) {
     const uint64_t* meta = metas + kQPMeta * slot;
@@ -1193,21 +1225,14 @@ __global__ void __launch_bounds__(kQPThreads, 3) bin2q_qp_kernel(Bin2QArgs a) {
   __syncthreads();
   if (tid >= kQPC) {  // the producer warp
     if (tid != kQPC) return;
-    pc = claim(~0ull);
-    if constexpr (DEPTH == 3) {
-      p1 = claim(pc);
-      p2 = claim(p1);
-      e1 = ent_of(p1);
-    }
-    e0 = ent_of(pc);
-    if (pc < nitems) qlookup<M, false>(g, map, tile_e(e0), pit);
+    QPItems<DEPTH> P(a);
+    P.start();
     for (uint32_t i = 0;; ++i) {
       const int slot = (int)(i & 1u);
       // buffer q and meta slot `slot` are free once every consumer warp is past quarter q of
       // item i - 1 (for q = 0 that also means past item i - 2, the slot's previous item)
       if (i) QP_WAIT(&empty[0], (i - 1) & 1u);
-      prep(slot);
-      const bool end = metas[kQPMeta * slot + 7] != 0;
+      const bool end = !P.prep(metas + kQPMeta * slot);
       issue(0, slot);
       if (end) return;  // the consumers stop at this item's quarter 0
       for (int q = 1; q < 4; ++q) {
@@ -1382,43 +1407,19 @@ __device__ __forceinline__ void wq_common(const float (&a)[4], const float (&b)[
 constexpr int kQPWThreads = kThreads + 32;  // the bound pass: 8 consumer warps + the producer
 template <int DEPTH, bool DF>
 __global__ void __launch_bounds__(kQPWThreads, 3) bin2q_qpw_kernel(Bin2QArgs a) {
-  constexpr int M = 6;
-  constexpr uint32_t TT = QPGeo::TT, Q = QPGeo::Q, LOG = 2 * M;
+  constexpr uint32_t Q = QPGeo::Q;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   float* qbuf = reinterpret_cast<float*>(smem_raw);  // [2][kQWBuf]
   uint64_t* bars = reinterpret_cast<uint64_t*>(qbuf + 2 * kQWBuf);  // full[2]
   uint64_t* empty = bars + 2;                                        // empty[2]
   uint64_t* metas = empty + 2;                                       // [2][kQPMeta]
   __shared__ double r0[8], r1[8], r2[8];
-  QGeo g;
-  g.K = a.K;
-  g.lmask = a.geo[0];
-  g.q1 = a.geo[1];
-  g.amask = a.geo[2];
-  g.bmask = a.geo[3];
-  g.kmask = a.geo[4];
-  g.ntiles = a.geo[5];
   const float* src = reinterpret_cast<const float*>(a.src);
   // DF (tracking sweep): the table read is staged at the outputs, v_prev is not read, the new
   // values go to dst
   const float* prev = DF ? nullptr : reinterpret_cast<const float*>(a.prev);
   float* dst = DF ? reinterpret_cast<float*>(a.dst) : nullptr;
-  const uint32_t* map = a.map;
   const int tid = threadIdx.x;
-  const uint64_t G = gridDim.x;
-  const uint32_t* sched = (a.sched && a.sched_m == M) ? a.sched : nullptr;
-  const uint64_t nitems = sched ? a.nitems : g.ntiles;
-  unsigned long long* counter = sched ? a.counter : nullptr;
-  auto first = [&](uint64_t c) { return sched ? c : qnext(g, c, G, LOG); };
-  auto claim = [&](uint64_t prv) -> uint64_t {
-    if (counter) return (uint64_t)atomicAdd(counter, 1ull);
-    return first(prv == ~0ull ? (uint64_t)blockIdx.x : prv + G);
-  };
-  auto entry = [&](uint64_t c) -> uint32_t { return sched ? __ldg(sched + c) : (uint32_t)c; };
-  auto ent_of = [&](uint64_t c) -> uint32_t { return c < nitems ? entry(c) : 0u; };
-  auto tile_e = [&](uint32_t e) -> uint64_t {
-    return sched ? (uint64_t)(e & kQTileMask) : (uint64_t)e;
-  };
   if (tid == 0) {
     for (int b = 0; b < 2; ++b) {
       mbar_init(&bars[b], 1);
@@ -1429,55 +1430,15 @@ __global__ void __launch_bounds__(kQPWThreads, 3) bin2q_qpw_kernel(Bin2QArgs a) 
   __syncthreads();
   if (tid >= kThreads) {  // the producer warp (one lane)
     if (tid != kThreads) return;
-    uint64_t pc = 0, p1 = 0, p2 = 0;
-    uint32_t e0 = 0, e1 = 0;
-    QItem pit;
-    pc = claim(~0ull);
-    if constexpr (DEPTH == 3) {
-      p1 = claim(pc);
-      p2 = claim(p1);
-      e1 = ent_of(p1);
-    }
-    e0 = ent_of(pc);
-    if (pc < nitems) qlookup<M, false>(g, map, tile_e(e0), pit);
+    QPItems<DEPTH> P(a);
+    P.start();
     for (uint64_t k = 0;; ++k) {
       const int q = (int)(k & 3u), b = (int)(k & 1u), slot = (int)((k >> 2) & 1u);
       if (k >= 2) QP_WAIT(&empty[b], (uint32_t)(((k >> 1) - 1) & 1u));
       uint64_t* meta = metas + kQPMeta * slot;
-      if (q == 0) {  // the item's metadata (or the end marker), then the claim pipeline moves on
-        if (pc >= nitems) {
-          meta[7] = 1;
-          mbar_arrive(&bars[b]);
-          return;
-        }
-        const uint64_t tau = tile_e(e0);
-        uint64_t x0, p0, taup;
-        qtile(g, tau, LOG, x0, p0, taup);
-        const bool self = taup == tau;
-        const uint64_t wb = qwin(g, x0), wp = qwin(g, p0);
-        const uint64_t yf = wb >> 2, ym = g.q1 - yf - TT / 2, ypf = wp >> 2,
-                       ypm = g.q1 - ypf - TT / 2;
-        meta[0] = (pit.m[0] & 3u) | ((pit.m[1] & 3u) << 2) | (self ? 16u : 0u);
-        meta[1] = qrun(g, pit.m[2], x0);
-        meta[2] = self ? kNone : qrun(g, pit.m[3], p0);
-        meta[3] = qrun(g, pit.m[4], yf);
-        meta[4] = qrun(g, pit.m[5], ym);
-        meta[5] = self ? kNone : qrun(g, pit.m[6], ypf);
-        meta[6] = self ? kNone : qrun(g, pit.m[7], ypm);
-        meta[7] = 0;
-        meta[8] = reinterpret_cast<uint64_t>(qp_wstart(g, src, pit.m[0], wb));
-        meta[9] = reinterpret_cast<uint64_t>(qp_wstart(g, src, pit.m[1], wp));
-        if constexpr (DEPTH == 1) {
-          pc = claim(pc);
-          e0 = ent_of(pc);
-        } else {
-          pc = p1;
-          e0 = e1;
-          p1 = p2;
-          e1 = ent_of(p1);
-          p2 = claim(p2);
-        }
-        if (pc < nitems) qlookup<M, false>(g, map, tile_e(e0), pit);
+      if (q == 0 && !P.prep(meta)) {  // no item left: the end marker completes buffer 0
+        mbar_arrive(&bars[b]);
+        return;
       }
       // quarter q: both windows' quarters, u and v_prev at its outputs
       const uint32_t modes = (uint32_t)meta[0];
