@@ -27,12 +27,16 @@ Bound bookkeeping (both R readings are computed, reading R5 in DESIGN.md):
   best: the largest R - E over the evaluations so far, starting from the triplet (v_0, 0, 0)
         (Alg. 2 lines 2, 8-10), reported as a bound.
 
-Integer offsets (``offsets=True``, two-array form only, DESIGN.md reading
-R23): by translation invariance, F(v + c 1) = F(v) + c 1 (Lemma 1 (2)), so the
+Integer offsets (``offsets=True``, readings R23, R26): by
+translation invariance, F(v + c 1) = F(v) + c 1 (Lemma 1 (2)), so the
 table may hold s_n = v_n - o_n with an integer o_n: each sweep subtracts c_n = floor(min s_n),
   s_{n+1} = round_storage(F(s_n, s_n) - c_n),   o_{n+1} = o_n + c_n,   o_0 = 0,
 which keeps the stored magnitudes (and so the fp32 rounding) small.  The bound in stored terms:
 R = max(s_n - s_{n-1}) + c_{n-1} (min likewise), W = (s_n + R) - F(s_n, s_n).
+KS form (R26): every generation keeps its own o; F reads the table k sweeps back relative to the
+newest one's offset, F(v_n, ..., v_{n-d+1}) - o_n = F(s_n, s_{n-1} + (o_{n-1} - o_n), ...), so
+  s_{n+1} = round_storage(F(s_n + 0, ..., s_{n-d+1} + (o_{n-d+1} - o_n)) - c_n),  o_{n+1} = o_n + c_n,
+and W (Alg. 2 line 6) reads only the newest table: W = (s_n + dR) - F(s_n + (d-1)R, ..., s_n).
 
 Residual storage (``Run.rebase()``, offsets on; reading R24): the table is split into
 a fixed base H (the stored table at the rebase, fp32) and a stored residual e, v = H + e + o.
@@ -245,11 +249,10 @@ class Run:
         self.sweeps_done = 0
         self.best = {"max": 0.0, "min": 0.0}     # best r - eps per R reading (Alg. 2 line 3)
         self.best_sweep = {"max": 0, "min": 0}
-        if offsets and self.form != FORM_TWO_ARRAY:
-            raise ValueError("integer offsets are defined for the two-array form (reading R23)")
         self.offsets = bool(offsets)
         self.off = 0.0        # o_n of the newest table (an integer, exact in fp64)
         self.off_prev = 0.0   # o_{n-1}
+        self.goff = [0.0] * depth  # KS (R26): o of gens[k-1], the table k sweeps back
         self.base = None      # residual storage: the fixed base H (rebase), else None
         self.quantum = 1.0    # offset granularity: 1 (integer offsets), 1/64 after a rebase
         self.rebase_sweep = -1
@@ -278,10 +281,20 @@ class Run:
     def sweep(self, count: int = 1):
         for _ in range(count):
             if self.form == FORM_KS:
-                new = apply_F(self.sigma, self.d, self.ell, self.gens, threads=self.threads)
+                shift = None
+                c = 0.0
+                if self.offsets:  # read every generation relative to o_n (R26)
+                    shift = [o - self.goff[0] for o in self.goff]
+                    c = float(math.floor(float(self.gens[0].min())))
+                new = apply_F(self.sigma, self.d, self.ell, self.gens, shift=shift,
+                              threads=self.threads)
+                if self.offsets:
+                    new = new - c
                 new = round_storage(new, self.dtype)
                 self.prev = self.gens[0]
                 self.gens = [new] + self.gens[:-1]          # shift the rows (line 11)
+                self.goff = [self.goff[0] + c] + self.goff[:-1]
+                self.off_prev, self.off = self.off, self.goff[0]
             else:
                 g = self.gens[0]
                 full = self._full(g)

@@ -566,9 +566,57 @@ def test_offsets_cut_fp32_drift():
     assert abs(off - ref) / ref < 2e-6
 
 
-def test_offsets_rejected_for_ks():
-    with pytest.raises(ValueError):
-        fo.Run(2, 2, 3, "ks", offsets=True)
+# KS form (reading R26): every generation keeps its own integer offset
+
+def test_offsets_ks_ell1_exact_rationals():
+    """l = 1 binary KS with offsets, fp64: the values s_n + o_n are the exact rationals of the
+    hand recurrence (x = 1, 1, 3/2, 7/4, ...; y = 0, 1/2, 3/4, 9/8, ...) for 12 sweeps, every
+    o is an integer, and each generation's o is the one it was stored with."""
+    xs, ys = _ell1_binary_ks(12)
+    run = fo.Run(2, 2, 1, "ks", "f64", offsets=True)
+    for n in range(12):
+        run.sweep()
+        v = run.values(0)
+        assert v[0] == float(xs[n]) and v[3] == float(xs[n])
+        assert v[1] == float(ys[n]) and v[2] == float(ys[n])
+        if n >= 1:
+            p = run.values(1)
+            assert p[0] == float(xs[n - 1]) and p[1] == float(ys[n - 1])
+        assert all(o == int(o) for o in run.goff)
+        assert run.goff[0] == run.off and run.goff[1] == run.off_prev
+    assert run.off > 0
+
+
+@pytest.mark.parametrize("sigma,d,ell", [(2, 2, 3), (2, 2, 5), (3, 2, 2), (2, 3, 2), (4, 2, 2)])
+def test_offsets_ks_fp64_equal_plain_run(sigma, d, ell):
+    """Translation invariance (Lemma 1 (2)) for the KS form: with per-generation
+    offsets the values equal the plain KS iterate (fp64, 1e-12) at every generation, and so do
+    R and the bound (Alg. 2 lines 5-7)."""
+    a = fo.Run(sigma, d, ell, "ks", "f64")
+    b = fo.Run(sigma, d, ell, "ks", "f64", offsets=True)
+    for k in range(1, 61):
+        a.sweep()
+        b.sweep()
+        if k in (1, 2, 3, 17, 60):
+            np.testing.assert_allclose(b.values(0), a.newest, rtol=1e-12, atol=1e-12)
+            np.testing.assert_allclose(b.values(1), a.prev, rtol=1e-12, atol=1e-12)
+            for g, o, ga in zip(b.gens, b.goff, a.gens):
+                np.testing.assert_allclose(g + o, ga, rtol=1e-12, atol=1e-12)
+    ra, rb = a.bound(), b.bound()
+    for key in ("R_max", "R_min", "bound_at_Rmax", "bound_at_Rmin"):
+        assert rb[key] == pytest.approx(ra[key], abs=1e-12), key
+    assert b.off > 0 and b.off == int(b.off)
+
+
+@pytest.mark.parametrize("sigma,d,ell", [(2, 2, 4), (4, 2, 2), (2, 3, 2), (3, 3, 1)])
+def test_offsets_ks_fp32_reaches_appendix3(sigma, d, ell):
+    """fp32 storage with KS offsets converges to Appendix 3's printed cell."""
+    cells = {(int(r[0]), int(r[1]), int(r[2])): (float(r[3]), int(r[4]))
+             for r in _load("appendix3.txt") if len(r) == 5}
+    printed, line = cells[(sigma, d, ell)]
+    run = fo.Run(sigma, d, ell, "ks", "f32", offsets=True)
+    value = _converge(run, printed)
+    assert _in_band(value, printed), (value, printed, f"PAPER.md:{line}")
 
 
 # ---------------------------------------------------------------- residual storage (R24)
