@@ -136,14 +136,16 @@ typedef struct {
   /* process-sharded mode: host communication hooks instead of NCCL (see lcsb_comm_hooks); the
    * struct must stay valid until lcsb_destroy returns.  NULL = NCCL (nccl_id). */
   const lcsb_comm_hooks* comm;
-  /* integer-offset storage (reading R23), two-array form only:
+  /* integer-offset storage (readings R23, R26):
    *   0 = none (default);
    *   1 = each table holds s = v - o with an integer o: before every sweep c = floor(min s) of
    *       the table it reads, and the sweep stores round(F(s) - c) (F(v + c) = F(v) + c,
    *       translation invariance, Lemma 1 (2)), so stored magnitudes stay small and
    *       fp32 storage drifts less.  Values read out (lcsb_table) and the bound are those of v.
-   *       Binary: the quarter table (l >= 3) or, below that, the generic kernel; other sigma
-   *       (d = 2): the generic kernel.  KS form, the half table and sharding: LCSB_EINVAL. */
+   *       Two-array form: binary on the quarter table (l >= 3) or, below that, the generic
+   *       kernel; other sigma (d = 2): the generic kernel.  KS form (any sigma, d; R26): the
+   *       generic kernel, every generation keeps its own o and the table k sweeps back is read
+   *       relative to the newest one's.  The half table and sharding: LCSB_EINVAL. */
   int32_t offset_policy;
 } lcsb_config;
 

@@ -155,11 +155,13 @@ __global__ void __launch_bounds__(256) generic_sweep_kernel(GenericArgs a) {
   for (int i = 0; i < kMaxD; ++i) zero[i] = 0.0;
   T* dst = reinterpret_cast<T*>(a.dst);
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-  // integer offsets (reading R23): store round(F(s) + shift), reduce the min of the stored values
+  // integer offsets (reading R23): store round(F(s) + shift), reduce the min of the stored values;
+  // KS (R26): the table k back is read with gshift[k-1] added (0 in the two-array form)
   const double sh = a.ost ? a.ost->shift : 0.0;
+  const double* gsh = a.ost ? a.ost->gshift : zero;
   double mn = INFINITY;
   for (uint64_t x = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; x < a.n; x += stride) {
-    double v = g.F_at(a, x, zero);
+    double v = g.F_at(a, x, gsh);
     if (a.ost) {
       const T st = (T)(v + sh);  // F(s) + (-c): exact in fp64 (c an integer), then the rounding
       dst[x] = st;

@@ -31,13 +31,16 @@ __global__ void offset_init_kernel(OffState* o) {
     o->off[i] = 0.0;
     o->mn[i] = ord_enc(0.0);
   }
+  if (i < kMaxD) o->gshift[i] = 0.0;
   if (i == 0) {
     o->shift = 0.0;
     o->quantum = 1.0;
   }
 }
 
-__global__ void offset_prep_kernel(OffState* o, int cur, int out) {
+__global__ void offset_prep_kernel(OffState* o, int cur, int out, GenSlots g) {
+  // KS (reading R26): generation k is read relative to o_n = off[cur] (integers: exact)
+  for (int k = 0; k < kMaxD; ++k) o->gshift[k] = k < g.n ? o->off[g.slot[k]] - o->off[cur] : 0.0;
   const double m = dec_ord(o->mn[cur]);
   // a multiple of the quantum (1, or 1/64 after a rebase): exact, and so is every shift by it
   const double q = o->quantum;
@@ -180,8 +183,11 @@ cudaError_t launch_offset_init(OffState* o, cudaStream_t s) {
   offset_init_kernel<<<1, 32, 0, s>>>(o);
   return cudaGetLastError();
 }
-cudaError_t launch_offset_prep(OffState* o, int cur, int out, cudaStream_t s) {
-  offset_prep_kernel<<<1, 1, 0, s>>>(o, cur, out);
+cudaError_t launch_offset_prep(OffState* o, int cur, int out, cudaStream_t s,
+                               const GenSlots* gens) {
+  GenSlots g{};
+  if (gens) g = *gens;
+  offset_prep_kernel<<<1, 1, 0, s>>>(o, cur, out, g);
   return cudaGetLastError();
 }
 

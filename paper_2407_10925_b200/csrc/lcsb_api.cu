@@ -263,16 +263,17 @@ static int plan_config(const lcsb_config* c, Plan* p, char* why, size_t whylen) 
   const bool quarter_ok = sym_ok && qK >= 2 && qK <= c->ell - 1 && c->ell - qK <= 16 &&
                           2 * (c->ell - 1 - qM) <= kQHintShift &&
                           (!sharded || (lp0 >= 0 && c->ell - qK - 1 >= lp0));
-  // integer offsets (reading R23): two-array form, unsharded; the quarter table or the generic
-  // kernel carry the per-sweep shift and min
+  // integer offsets (readings R23, R26): unsharded; the quarter table (two-array binary) or the
+  // generic kernel (either form; KS with per-generation offsets) carry the shift and min
   const int ofs = c->offset_policy;
   if (ofs != 0 && ofs != 1) {
     snprintf(why, whylen, "offset_policy must be 0 or 1");
     return LCSB_EINVAL;
   }
-  if (ofs && (form != LCSB_FORM_TWO_ARRAY || sharded || c->symmetry == 1)) {
+  if (ofs && (sharded || c->symmetry == 1 ||
+              (form != LCSB_FORM_TWO_ARRAY && c->symmetry == 2))) {
     snprintf(why, whylen,
-             "integer offsets need the two-array form, no sharding and symmetry -1, 0 or 2");
+             "integer offsets need no sharding, symmetry -1, 0 or 2 (2: the two-array form)");
     return LCSB_EINVAL;
   }
   int sym = c->symmetry;
@@ -1382,8 +1383,13 @@ static int enqueue_sweeps(lcsb_t* h, int64_t n, cudaStream_t s, int64_t track) {
         }
         e = launch_small_pooled(a, h->cfg.dtype, s, h->sms);
       } else {
-        if (h->ost) {  // integer offsets (generic kernel, two-array form)
-          e = launch_offset_prep(h->ost, h->cur, out, s);
+        if (h->ost) {  // integer offsets (generic kernel; KS: per-generation shifts, R26)
+          GenSlots gs{};
+          if (h->form == LCSB_FORM_KS) {
+            gs.n = h->cfg.d;
+            for (int k = 1; k <= h->cfg.d; ++k) gs.slot[k - 1] = slot_back(h, k - 1);
+          }
+          e = launch_offset_prep(h->ost, h->cur, out, s, &gs);
           h->launches += 1;
           a.ost = h->ost;
           a.omin = &h->ost->mn[out];

@@ -46,15 +46,23 @@ inline uint64_t resident_blocks(K kernel, int tpb, int sms) {
   return (uint64_t)per_sm * (uint64_t)sms;
 }
 
-// Integer-offset storage (lcsb_config.offset_policy, reading R23; two-array form):
+// Integer-offset storage (lcsb_config.offset_policy, readings R23, R26):
 // ring slot i holds s = v - off[i]; before each sweep (cur -> out) the prep kernel sets
 // c = floor(min s[cur]) (mn[cur], ordered encoding), off[out] = off[cur] + c and shift = -c; the
 // sweep stores round(F(s) + shift) and reduces the min of what it stores into mn[out].
+// KS form (R26): the table k sweeps back is read with gshift[k-1] = off[its slot] - off[cur]
+// added (an integer, exact), so F sees every generation relative to o_n; two-array: all 0.
 struct OffState {
   double off[kMaxGen];
   unsigned long long mn[kMaxGen];
   double shift;
   double quantum;  // granularity of c: 1 (integer offsets), 1/64 with residual storage (R24)
+  double gshift[kMaxD];
+};
+// the ring slots of the tables 1..d sweeps back (KS form; the two-array form passes cur)
+struct GenSlots {
+  int n;
+  int slot[kMaxD];
 };
 
 // Reduction slots (device, unsigned long long each):
@@ -422,8 +430,10 @@ cudaError_t launch_red_init(unsigned long long* red, cudaStream_t s, unsigned mi
 // integer offsets: zero every slot's offset, min(s) = 0 (the zero tables of W_0), shift 0
 cudaError_t launch_offset_init(OffState* o, cudaStream_t s);
 // before a sweep cur -> out: c = floor(min s[cur]), off[out] = off[cur] + c, shift = -c,
-// mn[out] = +inf (the sweep reduces into it)
-cudaError_t launch_offset_prep(OffState* o, int cur, int out, cudaStream_t s);
+// mn[out] = +inf (the sweep reduces into it); gshift[k] = off[gens.slot[k]] - off[cur] for
+// k < gens.n, 0 beyond (gens = NULL: all 0)
+cudaError_t launch_offset_prep(OffState* o, int cur, int out, cudaStream_t s,
+                               const GenSlots* gens = nullptr);
 // residual storage: H = round32(H + e), e = (H + e) - H (both fp32 arrays of n entries)
 cudaError_t launch_rebase_fold(void* H, void* e, uint64_t n, cudaStream_t s, int sms);
 cudaError_t launch_rdiff(const void* newest, const void* prev, uint64_t n, int dtype,

@@ -395,6 +395,32 @@ def test_offsets_generic_two_array_matches_oracle_twin(sigma, ell, dtype):
 
 @pytest.mark.gpu
 @pytest.mark.skipif(not has_cuda(), reason="needs a CUDA device")
+@pytest.mark.parametrize("sigma,d,ell,dtype", [(2, 2, 3, "f32"), (2, 2, 6, "f64"),
+                                               (4, 2, 2, "f32"), (3, 2, 3, "f32"),
+                                               (2, 3, 2, "f32"), (2, 3, 3, "f64")])
+def test_offsets_generic_ks_matches_oracle_twin(sigma, d, ell, dtype):
+    """offset_policy = 1 in the KS form (reading R26: per-generation offsets, the table k back
+    read relative to the newest one's) on the generic kernel: every generation's values and the
+    two-pass bound bit-exact against the oracle's KS offset twin in fp32 (1e-12 in fp64)."""
+    from oracle import ft_oracle as fo
+    h = L.Lcsb(sigma, d, ell, dtype=dtype, form="ks", offset_policy=1)
+    assert h.kernel_in_use == "generic"
+    run = fo.Run(sigma, d, ell, "ks", dtype, offsets=True)
+    for n in (1, 2, 30):
+        h.sweep(n)
+        run.sweep(n)
+        _cmp(h.table(0), run.values(0), dtype)
+        _cmp(h.table(1), run.values(1), dtype)
+        gb, rb = h.bound(), run.bound()
+        for key in ("R_max", "R_min", "E_at_Rmax", "E_at_Rmin", "bound_at_Rmax", "bound_at_Rmin"):
+            g, r = getattr(gb, key), rb[key]
+            assert (g == r) if dtype == "f32" else abs(g - r) <= 1e-12 * max(1, abs(r)), key
+    assert run.off > 0
+    h.destroy()
+
+
+@pytest.mark.gpu
+@pytest.mark.skipif(not has_cuda(), reason="needs a CUDA device")
 def test_offsets_graph_replay_and_reset():
     """Offsets under CUDA-graph replay (l = 8, 77 + 5 sweeps per call) equal plain launches,
     and a reset restarts from offset 0 (the second run repeats the first bit for bit)."""
