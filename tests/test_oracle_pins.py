@@ -608,6 +608,17 @@ def test_offsets_ks_fp64_equal_plain_run(sigma, d, ell):
     assert b.off > 0 and b.off == int(b.off)
 
 
+def test_offsets_ks_cut_fp32_drift():
+    """KS form, fp32 storage: per-generation offsets bring the bound closer to the fp64 bound
+    (sigma = 4, d = 2, l = 4, 150 sweeps: 2.0e-5 -> 1.0e-6 relative)."""
+    ref = fo.feasible_triplet(4, 2, 4, 150, form="ks", dtype="f64")["bound_at_Rmax"]
+    plain = fo.feasible_triplet(4, 2, 4, 150, form="ks", dtype="f32")["bound_at_Rmax"]
+    off = fo.feasible_triplet(4, 2, 4, 150, form="ks", dtype="f32",
+                              offsets=True)["bound_at_Rmax"]
+    assert abs(off - ref) < 0.2 * abs(plain - ref)
+    assert abs(off - ref) / ref < 2e-6
+
+
 @pytest.mark.parametrize("sigma,d,ell", [(2, 2, 4), (4, 2, 2), (2, 3, 2), (3, 3, 1)])
 def test_offsets_ks_fp32_reaches_appendix3(sigma, d, ell):
     """fp32 storage with KS offsets converges to Appendix 3's printed cell."""
