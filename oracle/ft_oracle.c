@@ -79,7 +79,7 @@ uint64_t fo_encode(int sigma, int d, int ell, const int* A) {
  *                sigma = 2 that option never exists, so the binary form is unaffected.
  */
 static double fo_F_at(int sigma, int d, int ell, const double* const* src, const double* shift,
-                      int two_array, uint64_t x) {
+                      const double* post, int two_array, uint64_t x) {
     int A[FO_MAXD * FO_MAXL];
     int S[FO_MAXD * FO_MAXL];
     int N[FO_MAXD];
@@ -100,7 +100,7 @@ static double fo_F_at(int sigma, int d, int ell, const double* const* src, const
         if (two_array && nN == d && !b) continue; /* R20: drop-both not offered */
         double cand;
         if (nN == 0) {
-            cand = 0.0; /* R3 */
+            cand = post ? post[0] : 0.0; /* R3 (offsets, R26: the 0 in stored terms, -o_n) */
         } else {
             double r = 0.0;
             uint64_t combos = fo_ipow((uint64_t)sigma, nN);
@@ -123,6 +123,9 @@ static double fo_F_at(int sigma, int d, int ell, const double* const* src, const
             }
             double inv = 1.0 / (double)combos; /* sigma^{-|N|} (R16) */
             cand = inv * r;
+            /* integer offsets, KS form (R26): the table |N| sweeps back is read relative to the
+             * newest one's offset, F_z(s + p) = F_z(s) + p (Lemma 1 (2)); p is added to the mean */
+            if (post) cand = cand + post[nN];
         }
         if (cand > best) best = cand;
     }
@@ -145,7 +148,25 @@ int fo_apply_F(int sigma, int d, int ell, const double* const* src, const double
     if (threads > 0) omp_set_num_threads(threads);
 #pragma omp parallel for schedule(static)
 #endif
-    for (int64_t x = 0; x < (int64_t)n; ++x) out[x] = fo_F_at(sigma, d, ell, src, sh, two_array, (uint64_t)x);
+    for (int64_t x = 0; x < (int64_t)n; ++x) out[x] = fo_F_at(sigma, d, ell, src, sh, NULL, two_array, (uint64_t)x);
+    (void)threads;
+    return 0;
+}
+
+/* fo_apply_F with post[k] added to every F_z whose |N| = k >= 1, after its mean, and post[0]
+ * as the value of the |N| = 0 option instead of R3's 0 (reading R26; d + 1 entries). */
+int fo_apply_F_post(int sigma, int d, int ell, const double* const* src, const double* post,
+                    double* out, int threads, int two_array) {
+    if (sigma < 2 || d < 2 || ell < 1 || d > FO_MAXD || ell > FO_MAXL || !post) return 1;
+    if (two_array && d != 2) return 1;
+    uint64_t n = fo_ipow((uint64_t)sigma, d * ell);
+    double zero[FO_MAXD] = {0};
+#ifdef _OPENMP
+    if (threads > 0) omp_set_num_threads(threads);
+#pragma omp parallel for schedule(static)
+#endif
+    for (int64_t x = 0; x < (int64_t)n; ++x)
+        out[x] = fo_F_at(sigma, d, ell, src, zero, post, two_array, (uint64_t)x);
     (void)threads;
     return 0;
 }
@@ -157,7 +178,7 @@ int fo_apply_F_at(int sigma, int d, int ell, const double* const* src, const dou
     if (two_array && d != 2) return 1;
     double zero[FO_MAXD] = {0};
     const double* sh = shift ? shift : zero;
-    for (int64_t i = 0; i < count; ++i) out[i] = fo_F_at(sigma, d, ell, src, sh, two_array, idx[i]);
+    for (int64_t i = 0; i < count; ++i) out[i] = fo_F_at(sigma, d, ell, src, sh, NULL, two_array, idx[i]);
     return 0;
 }
 

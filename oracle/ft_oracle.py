@@ -34,8 +34,12 @@ table may hold s_n = v_n - o_n with an integer o_n: each sweep subtracts c_n = f
 which keeps the stored magnitudes (and so the fp32 rounding) small.  The bound in stored terms:
 R = max(s_n - s_{n-1}) + c_{n-1} (min likewise), W = (s_n + R) - F(s_n, s_n).
 KS form (R26): every generation keeps its own o; F reads the table k sweeps back relative to the
-newest one's offset, F(v_n, ..., v_{n-d+1}) - o_n = F(s_n, s_{n-1} + (o_{n-1} - o_n), ...), so
-  s_{n+1} = round_storage(F(s_n + 0, ..., s_{n-d+1} + (o_{n-d+1} - o_n)) - c_n),  o_{n+1} = o_n + c_n,
+newest one's offset, F(v_n, ..., v_{n-d+1}) - o_n = F(s_n, s_{n-1} + (o_{n-1} - o_n), ...), with
+p_k = o_{n+1-k} - o_n added to each option's mean over the table k back (the mean of s + p is
+the mean of s plus p; added after the mean, as kernels that keep pooled row means can), and the
+|N| = 0 option's 0 (R3) written in stored terms, -o_n (the 0 is a constant, not an iterate
+value, so translating the tables translates it too; it never wins: every iterate is >= 0), so
+  s_{n+1} = round_storage(F_p(s_n, ..., s_{n-d+1}) - c_n),  o_{n+1} = o_n + c_n,
 and W (Alg. 2 line 6) reads only the newest table: W = (s_n + dR) - F(s_n + (d-1)R, ..., s_n).
 
 Residual storage (``Run.rebase()``, offsets on; reading R24): the table is split into
@@ -87,6 +91,8 @@ def _lib():
                                        ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int,
                                        ctypes.c_int]
             lib.fo_apply_F.restype = ctypes.c_int
+            lib.fo_apply_F_post.argtypes = lib.fo_apply_F.argtypes
+            lib.fo_apply_F_post.restype = ctypes.c_int
             lib.fo_apply_F_at.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, dpp,
                                           ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64,
                                           ctypes.c_void_p]
@@ -168,10 +174,12 @@ def _as_f64(v) -> np.ndarray:
 
 
 def apply_F(sigma: int, d: int, ell: int, src, shift=None, threads: int = 0,
-            two_array: bool = False) -> np.ndarray:
+            two_array: bool = False, post=None) -> np.ndarray:
     """F(src[0], ..., src[d-1]): src[k-1] is read when |N| = k (reading R1).  ``shift[k-1]`` is
     added to every value read from src[k-1] (used for Alg. 2 line 6).  ``two_array`` (d = 2):
-    the drop-both option (both heads differ, |N| = 2) is not offered (reading R20)."""
+    the drop-both option (both heads differ, |N| = 2) is not offered (reading R20).  ``post[k-1]``
+    (instead of ``shift``; d + 1 entries) is added to each option's mean with |N| = k >= 1, and
+    ``post[0]`` replaces the |N| = 0 option's 0 (KS offsets, reading R26)."""
     n = n_states(sigma, d, ell)
     if len(src) != d:
         raise ValueError("need d source vectors")
@@ -180,8 +188,20 @@ def apply_F(sigma: int, d: int, ell: int, src, shift=None, threads: int = 0,
         if a.shape != (n,):
             raise ValueError("bad vector length")
     ptrs = (ctypes.c_void_p * d)(*[a.ctypes.data for a in arrs])
-    sh = np.zeros(d, dtype=np.float64) if shift is None else np.ascontiguousarray(shift, np.float64)
     out = np.empty(n, dtype=np.float64)
+    if post is not None:
+        if shift is not None:
+            raise ValueError("shift and post are exclusive")
+        po = np.ascontiguousarray(post, np.float64)
+        if po.shape != (d + 1,):
+            raise ValueError("post needs d + 1 entries")
+        rc = _lib().fo_apply_F_post(sigma, d, ell, ctypes.cast(ptrs, ctypes.POINTER(ctypes.c_void_p)),
+                                    po.ctypes.data, out.ctypes.data, int(threads),
+                                    int(bool(two_array)))
+        if rc:
+            raise ValueError("fo_apply_F_post rejected the parameters")
+        return out
+    sh = np.zeros(d, dtype=np.float64) if shift is None else np.ascontiguousarray(shift, np.float64)
     rc = _lib().fo_apply_F(sigma, d, ell, ctypes.cast(ptrs, ctypes.POINTER(ctypes.c_void_p)),
                            sh.ctypes.data, out.ctypes.data, int(threads), int(bool(two_array)))
     if rc:
@@ -281,13 +301,14 @@ class Run:
     def sweep(self, count: int = 1):
         for _ in range(count):
             if self.form == FORM_KS:
-                shift = None
+                post = None
                 c = 0.0
                 if self.offsets:  # read every generation relative to o_n (R26)
-                    shift = [o - self.goff[0] for o in self.goff]
+                    # the |N| = 0 option's 0 (R3) in stored terms is -o_n; |N| = k: o_{n+1-k} - o_n
+                    post = [-self.goff[0]] + [o - self.goff[0] for o in self.goff]
                     c = float(math.floor(float(self.gens[0].min())))
-                new = apply_F(self.sigma, self.d, self.ell, self.gens, shift=shift,
-                              threads=self.threads)
+                new = apply_F(self.sigma, self.d, self.ell, self.gens, threads=self.threads,
+                              post=post)
                 if self.offsets:
                     new = new - c
                 new = round_storage(new, self.dtype)

@@ -587,11 +587,14 @@ def test_offsets_ks_ell1_exact_rationals():
     assert run.off > 0
 
 
-@pytest.mark.parametrize("sigma,d,ell", [(2, 2, 3), (2, 2, 5), (3, 2, 2), (2, 3, 2), (4, 2, 2)])
+@pytest.mark.parametrize("sigma,d,ell", [(2, 2, 3), (2, 2, 5), (3, 2, 2), (2, 3, 2), (4, 2, 2),
+                                         (2, 3, 1), (2, 4, 1), (2, 5, 1)])
 def test_offsets_ks_fp64_equal_plain_run(sigma, d, ell):
     """Translation invariance (Lemma 1 (2)) for the KS form: with per-generation
     offsets the values equal the plain KS iterate (fp64, 1e-12) at every generation, and so do
-    R and the bound (Alg. 2 lines 5-7)."""
+    R and the bound (Alg. 2 lines 5-7).  (2,3,1), (2,4,1), (2,5,1): the |N| = 0 option must be
+    the translated 0 (-o_n, reading R26); R3's literal 0 in stored terms wins there for d >= 3
+    and moves the values by up to 0.42."""
     a = fo.Run(sigma, d, ell, "ks", "f64")
     b = fo.Run(sigma, d, ell, "ks", "f64", offsets=True)
     for k in range(1, 61):
