@@ -60,9 +60,11 @@ struct Gen {
   }
 
   // mean over the appended characters for mask `mask` (bit j = string j advances), reading
-  // table src[popcount-1] with `shift[popcount-1]` added to each value (W pass).
+  // table src[popcount-1] with `shift[popcount-1]` added to each value (W pass); `post`
+  // (KS integer offsets, reading R26; NULL = none): post[popcount] added to the mean.
   __device__ double option_mean(const GenericArgs& a, const uint64_t* contrib, const int* head,
-                                unsigned mask, const double* shift) const {
+                                unsigned mask, const double* shift,
+                                const double* post = nullptr) const {
     int k = __popc(mask);
     uint64_t base = 0;
     uint64_t w[kMaxD];
@@ -101,11 +103,12 @@ struct Gen {
       }
     }
     double inv = 1.0 / (double)combos;  // sigma^{-|N|}, correctly rounded
-    return inv * r;
+    return post ? inv * r + post[k] : inv * r;
   }
 
   // F(src...)[x] with per-|N| shifts; also returns the decoded structure for reuse
-  __device__ double F_at(const GenericArgs& a, uint64_t x, const double* shift) const {
+  __device__ double F_at(const GenericArgs& a, uint64_t x, const double* shift,
+                         const double* post = nullptr) const {
     uint64_t contrib[kMaxD];
     int head[kMaxD];
     for (int j = 0; j < d; ++j) contrib[j] = 0;
@@ -134,13 +137,14 @@ struct Gen {
       unsigned mask = 0;
       for (int i = 0; i < d; ++i)
         if (head[i] != hz) mask |= 1u << i;
-      double cand = mask ? option_mean(a, contrib, head, mask, shift) : 0.0;
+      // |N| = 0: R3's 0 (offsets: in stored terms, post[0] = -o_n, reading R26)
+      double cand = mask ? option_mean(a, contrib, head, mask, shift, post) : (post ? post[0] : 0.0);
       if (cand > best) best = cand;
     }
     // some z is no string's head: N = all strings; not offered by the two-array form (d = 2)
     // when the heads differ (drop-both, reading R20)
     if (nseen < sigma && !(a.form == LCSB_FORM_TWO_ARRAY && !b)) {
-      double cand = option_mean(a, contrib, head, full, shift);
+      double cand = option_mean(a, contrib, head, full, shift, post);
       if (cand > best) best = cand;
     }
     return (double)b + best;
@@ -156,12 +160,12 @@ __global__ void __launch_bounds__(256) generic_sweep_kernel(GenericArgs a) {
   T* dst = reinterpret_cast<T*>(a.dst);
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   // integer offsets (reading R23): store round(F(s) + shift), reduce the min of the stored values;
-  // KS (R26): the table k back is read with gshift[k-1] added (0 in the two-array form)
+  // KS (R26): gpost[k] added to the means over the table k back (0 in the two-array form)
   const double sh = a.ost ? a.ost->shift : 0.0;
-  const double* gsh = a.ost ? a.ost->gshift : zero;
+  const double* gsh = a.ost ? a.ost->gpost : nullptr;
   double mn = INFINITY;
   for (uint64_t x = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; x < a.n; x += stride) {
-    double v = g.F_at(a, x, gsh);
+    double v = g.F_at(a, x, zero, gsh);
     if (a.ost) {
       const T st = (T)(v + sh);  // F(s) + (-c): exact in fp64 (c an integer), then the rounding
       dst[x] = st;

@@ -278,7 +278,7 @@ __device__ __forceinline__ double row16_sum(const T* p) {
   return sum;
 }
 
-template <typename T, int M, int S, bool WMODE, bool GR = false, bool SH = false>
+template <typename T, int M, int S, bool WMODE, bool GR = false, bool SH = false, bool OFS = false>
 __global__ void __launch_bounds__(kThreads, GR ? 4 : ((WMODE && sizeof(T) == 8) ? 1 : 3)) q4_kernel(Q4Args a) {
   using C = Q4Cfg<T, M, S, WMODE, GR>;
   constexpr uint32_t TT = C::TT;
@@ -326,6 +326,17 @@ __global__ void __launch_bounds__(kThreads, GR ? 4 : ((WMODE && sizeof(T) == 8) 
   }
 
   const bool ta = (a.flags & kQ4TwoArray) != 0;
+  // integer offsets (OFS, sweep only; readings R23, R26): the row means read are of the table two
+  // back (KS; one back in the two-array form, shift 0) and get gpost added after the mean; every
+  // output gets shift = -c before the storage rounding; omn = min of the stored values.  The
+  // |N| = 0 option (-o_n in stored terms, R26) never wins against P + gpost[2] >= -o_n, so
+  // h_a == h_b stays 1 + P
+  static_assert(!(OFS && (WMODE || SH)), "offsets: unsharded sweeps only");
+  [[maybe_unused]] double psh = 0.0, osh = 0.0, omn = INFINITY;
+  if constexpr (OFS) {
+    psh = a.ost->gpost[ta ? 1 : 2];
+    osh = a.ost->shift;
+  }
   static_assert(TT == kThreads, "one tail per thread and unit");
   const uint32_t i = tail_of((uint32_t)tid, (a.flags & kQ4TailPerm) != 0);
   const uint32_t i2 = (uint32_t)digit_swap(i);  // this tail's offset in the swapped unit
@@ -366,6 +377,7 @@ __global__ void __launch_bounds__(kThreads, GR ? 4 : ((WMODE && sizeof(T) == 8) 
         const T* ubC = buf + (size_t)((sl >> 4) & 3u) * C::UNIT;
         pu = reinterpret_cast<const double*>(ubC + C::WIN)[TT - 1 - i];
       }
+      if constexpr (OFS) pu = pu + psh;
 #pragma unroll
       for (int m = 0; m < (WMODE ? 2 : 1); ++m) {
         const double sh = (WMODE && !ta) ? R[m] : 0.0;  // KS |N| = 1: shift (d-1) R = R
@@ -383,7 +395,7 @@ __global__ void __launch_bounds__(kThreads, GR ? 4 : ((WMODE && sizeof(T) == 8) 
         // of 8 fp64 max chains + 8 conversions) and the maxima taken in fp32 (one FMNMX each; no
         // NaN, no -0); the stored values are unchanged bit for bit
         [[maybe_unused]] float fU[2], fS[4], fpu = 0.f, fsame = 0.f;
-        if constexpr (sizeof(T) == 4 && !WMODE) {
+        if constexpr (sizeof(T) == 4 && !WMODE && !OFS) {
           fU[0] = (float)bU[0];
           fU[1] = (float)bU[1];
 #pragma unroll
@@ -396,7 +408,7 @@ __global__ void __launch_bounds__(kThreads, GR ? 4 : ((WMODE && sizeof(T) == 8) 
 #pragma unroll
           for (int hb = 0; hb < 4; ++hb) {
             double v;
-            if constexpr (sizeof(T) == 4 && !WMODE) {
+            if constexpr (sizeof(T) == 4 && !WMODE && !OFS) {
               const float v32 = (ha == hb) ? fsame
                                            : (ta ? fmaxf(fU[ha], fS[hb])
                                                  : fmaxf(fmaxf(fU[ha], fS[hb]), fpu));
@@ -407,6 +419,10 @@ __global__ void __launch_bounds__(kThreads, GR ? 4 : ((WMODE && sizeof(T) == 8) 
               v = dmax(bU[ha], bS[hb]);  // two-array: no drop-both option (reading R20)
             } else {
               v = dmax(dmax(bU[ha], bS[hb]), pu);  // adv_b, adv_a, P
+            }
+            if constexpr (OFS) {  // F - c (exact in fp64: c a small integer), then the rounding
+              v = v + osh;
+              omn = dmin(omn, (double)(T)v);
             }
             const int hh = ha * 4 + hb;
             if (!WMODE) {
@@ -473,18 +489,19 @@ __global__ void __launch_bounds__(kThreads, GR ? 4 : ((WMODE && sizeof(T) == 8) 
     }
   }
   if (WMODE) block_max2_to(wmax[0], wmax[1], a.red_out);
+  if constexpr (OFS) block_min_to(omn, a.omin);
 }
 
-template <typename T, int M, int S, bool WMODE, bool GR = false, bool SH = false>
+template <typename T, int M, int S, bool WMODE, bool GR = false, bool SH = false, bool OFS = false>
 cudaError_t launch_q4_one(const Q4Args& a, cudaStream_t s, int sms) {
   using C = Q4Cfg<T, M, S, WMODE, GR>;
   static uint64_t cap = 0;
   if (cap == 0) {
-    cudaError_t e = cudaFuncSetAttribute(q4_kernel<T, M, S, WMODE, GR, SH>,
+    cudaError_t e = cudaFuncSetAttribute(q4_kernel<T, M, S, WMODE, GR, SH, OFS>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
     if (e != cudaSuccess) return e;
     int per_sm = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, q4_kernel<T, M, S, WMODE, GR, SH>,
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, q4_kernel<T, M, S, WMODE, GR, SH, OFS>,
                                                       kThreads, C::SMEM) != cudaSuccess ||
         per_sm < 1) {
       cudaGetLastError();
@@ -494,7 +511,7 @@ cudaError_t launch_q4_one(const Q4Args& a, cudaStream_t s, int sms) {
   }
   const uint64_t nunits = 1ull << (4 * (a.ell - 1) - 4 * M);
   uint64_t blocks = cap < nunits ? cap : nunits;
-  q4_kernel<T, M, S, WMODE, GR, SH><<<(unsigned)blocks, kThreads, C::SMEM, s>>>(a);
+  q4_kernel<T, M, S, WMODE, GR, SH, OFS><<<(unsigned)blocks, kThreads, C::SMEM, s>>>(a);
   return cudaGetLastError();
 }
 // sharded launches (a.p > 0) take the instantiation with the shard indexing compiled in
@@ -531,6 +548,11 @@ cudaError_t launch_q4_sweep(const Q4Args& a0, int dtype, cudaStream_t s, int sms
   if (grows < 0) {
     const char* e = getenv("LCSB_Q4_GROWS");
     grows = e ? atoi(e) : 0;
+  }
+  if (a.ost) {  // integer offsets: the default pipeline, unsharded (plan_config)
+    if (a.p > 0) return cudaErrorInvalidValue;
+    return dtype == LCSB_F32 ? launch_q4_one<float, 2, 1, false, false, false, true>(a, s, sms)
+                             : launch_q4_one<double, 2, 1, false, false, false, true>(a, s, sms);
   }
   if (dtype == LCSB_F32) {
     if (variant == 2) return launch_q4_t<float, 2, 2, false>(a, s, sms);

@@ -31,7 +31,7 @@ __global__ void offset_init_kernel(OffState* o) {
     o->off[i] = 0.0;
     o->mn[i] = ord_enc(0.0);
   }
-  if (i < kMaxD) o->gshift[i] = 0.0;
+  if (i <= kMaxD) o->gpost[i] = 0.0;
   if (i == 0) {
     o->shift = 0.0;
     o->quantum = 1.0;
@@ -40,7 +40,9 @@ __global__ void offset_init_kernel(OffState* o) {
 
 __global__ void offset_prep_kernel(OffState* o, int cur, int out, GenSlots g) {
   // KS (reading R26): generation k is read relative to o_n = off[cur] (integers: exact)
-  for (int k = 0; k < kMaxD; ++k) o->gshift[k] = k < g.n ? o->off[g.slot[k]] - o->off[cur] : 0.0;
+  o->gpost[0] = g.n > 0 ? -o->off[cur] : 0.0;
+  for (int k = 1; k <= kMaxD; ++k)
+    o->gpost[k] = k <= g.n ? o->off[g.slot[k - 1]] - o->off[cur] : 0.0;
   const double m = dec_ord(o->mn[cur]);
   // a multiple of the quantum (1, or 1/64 after a rebase): exact, and so is every shift by it
   const double q = o->quantum;
@@ -147,7 +149,8 @@ __global__ void expand_kernel(ExpandTabs tabs, int p, int symmetric, int q4,
       continue;
     }
     if (q4) {  // sigma = 4 digit-key shards
-      out[i] = (double)reinterpret_cast<const T*>(tabs.t[q4_key(y, ell, p)])[q4_local(y, ell, p)];
+      out[i] = (double)reinterpret_cast<const T*>(tabs.t[q4_key(y, ell, p)])[q4_local(y, ell, p)] +
+               off;
       continue;
     }
     const uint32_t sh = shard_of_stored(y, 2 * ell, p);

@@ -354,12 +354,12 @@ static int plan_config(const lcsb_config* c, Plan* p, char* why, size_t whylen) 
   p->qM = (sym == 2) ? qM : 0;
   p->kernel = sym == 2 ? 5 : (sym ? 2 : 1);
   p->offsets = ofs;
-  if (ofs) {
-    // the quarter table (binary) or the generic full-table kernel: nothing else below
-  } else if (!sym && c->sigma == 4 && c->d == 2 && c->ell >= q4_min_ell() &&
+  if (!sym && c->sigma == 4 && c->d == 2 && c->ell >= q4_min_ell() &&
       c->kernel == LCSB_KERNEL_AUTO)
-    p->kernel = 3;  // sigma = 4, d = 2 swap-paired TMA kernel (kern_q4.cu)
-  else if (p->kernel == 1 && c->kernel == LCSB_KERNEL_AUTO && small_supported(c->sigma, c->d, n))
+    p->kernel = 3;  // sigma = 4, d = 2 swap-paired TMA kernel (kern_q4.cu; offsets too)
+  else if (ofs) {
+    // the quarter table (binary) or the generic full-table kernel: no small kernel
+  } else if (p->kernel == 1 && c->kernel == LCSB_KERNEL_AUTO && small_supported(c->sigma, c->d, n))
     p->kernel = 4;  // register-resident compile-time (sigma, d) kernel (kern_small.cu)
   p->ntab = (form == LCSB_FORM_KS) ? c->d + 1 : 2;  // Alg. 2: d+1 rows; two-array: 2
   // q4: v_{n-2} is only read through its row means (kern_q4.cu): 2 full tables + 3 mean arrays
@@ -893,6 +893,7 @@ extern "C" int lcsb_create_ex(const lcsb_config* cfg, lcsb_t** out) {
     lcsb_destroy(h);
     return set_err(nullptr, LCSB_ECAPACITY, "scratch allocation failed");
   }
+  static_assert(sizeof(OffState) <= 512, "plan_config reserves 512 bytes for the offset state");
   if (p.offsets) {  // W_0 = 0 with offset 0; min of the zero table = 0
     h->ost = (OffState*)dev_alloc(h, 512);
     if (!h->ost || launch_offset_init(h->ost, s) != cudaSuccess) {
@@ -1365,7 +1366,19 @@ static int enqueue_sweeps(lcsb_t* h, int64_t n, cudaStream_t s, int64_t track) {
           a.dst_sh[j] = h->tabs[j][out];
           a.pout_sh[j] = h->pools[j][pout];
         }
-        e = launch_q4_sweep(a, h->cfg.dtype, s, h->sms);
+        if (h->ost) {  // integer offsets (R23; KS: the row means read are of the table two back)
+          GenSlots gs{};
+          if (h->form == LCSB_FORM_KS) {
+            gs.n = 2;
+            gs.slot[0] = slot_back(h, 0);
+            gs.slot[1] = slot_back(h, 1);  // = out (ring of 2): read before prep overwrites it
+          }
+          e = launch_offset_prep(h->ost, h->cur, out, s, &gs);
+          h->launches += 1;
+          a.ost = h->ost;
+          a.omin = &h->ost->mn[out];
+        }
+        if (e == cudaSuccess) e = launch_q4_sweep(a, h->cfg.dtype, s, h->sms);
         h->launches += 1;
       }
       h->pcur = (h->pcur + 1) % 3;

@@ -50,14 +50,15 @@ inline uint64_t resident_blocks(K kernel, int tpb, int sms) {
 // ring slot i holds s = v - off[i]; before each sweep (cur -> out) the prep kernel sets
 // c = floor(min s[cur]) (mn[cur], ordered encoding), off[out] = off[cur] + c and shift = -c; the
 // sweep stores round(F(s) + shift) and reduces the min of what it stores into mn[out].
-// KS form (R26): the table k sweeps back is read with gshift[k-1] = off[its slot] - off[cur]
-// added (an integer, exact), so F sees every generation relative to o_n; two-array: all 0.
+// KS form (R26): gpost[k] = off[slot of the table k sweeps back] - off[cur] (an integer) is
+// added to every option mean over that table, so F sees every generation relative to o_n, and
+// gpost[0] = -off[cur] is the |N| = 0 option's 0 (R3) in stored terms; two-array: all 0.
 struct OffState {
   double off[kMaxGen];
   unsigned long long mn[kMaxGen];
   double shift;
   double quantum;  // granularity of c: 1 (integer offsets), 1/64 with residual storage (R24)
-  double gshift[kMaxD];
+  double gpost[kMaxD + 1];
 };
 // the ring slots of the tables 1..d sweeps back (KS form; the two-array form passes cur)
 struct GenSlots {
@@ -304,6 +305,11 @@ struct Q4Args {
   void* dst_sh[kMaxShards];
   double* pout_sh[kMaxShards];
   const void* g1_sh[kMaxShards];
+  // integer offsets (sweep, unsharded; readings R23, R26): P gets gpost[2] (KS: of the table two
+  // back), outputs get shift before the storage rounding, the min of the stored values goes to
+  // omin.  NULL = off
+  const OffState* ost;
+  unsigned long long* omin;
 };
 constexpr int kQ4TwoArray = 4;  // Q4Args::flags: two-array form (reading R20)
 
@@ -430,8 +436,8 @@ cudaError_t launch_red_init(unsigned long long* red, cudaStream_t s, unsigned mi
 // integer offsets: zero every slot's offset, min(s) = 0 (the zero tables of W_0), shift 0
 cudaError_t launch_offset_init(OffState* o, cudaStream_t s);
 // before a sweep cur -> out: c = floor(min s[cur]), off[out] = off[cur] + c, shift = -c,
-// mn[out] = +inf (the sweep reduces into it); gshift[k] = off[gens.slot[k]] - off[cur] for
-// k < gens.n, 0 beyond (gens = NULL: all 0)
+// mn[out] = +inf (the sweep reduces into it); gens->n > 0 (KS): gpost[0] = -off[cur] and
+// gpost[k] = off[gens.slot[k-1]] - off[cur] for 1 <= k <= gens.n; otherwise all 0
 cudaError_t launch_offset_prep(OffState* o, int cur, int out, cudaStream_t s,
                                const GenSlots* gens = nullptr);
 // residual storage: H = round32(H + e), e = (H + e) - H (both fp32 arrays of n entries)

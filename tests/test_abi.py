@@ -72,13 +72,16 @@ def test_required_bytes_and_validation():
     assert L.lcsb_required_bytes(2, 2, 17, "f32", symmetry=2, block_log4=7) > 0
     assert L.lcsb_required_bytes(2, 2, 18, "f32", symmetry=2, block_log4=3) == 0
     # integer offsets (readings R23, R26): not the half table, not sharded; + 512 B.  KS form:
-    # the generic kernel over d + 1 full tables (never the quarter table, q4 or small kernels)
+    # sigma = 4, d = 2 keeps the q4 layout; otherwise the generic kernel over d + 1 full tables
+    # (never the quarter table or the small kernels)
     q8 = L.lcsb_required_bytes(2, 2, 8, "f32", symmetry=2)
     assert L.lcsb_required_bytes(2, 2, 8, "f32", offset_policy=1) == q8 + 512
     assert L.lcsb_required_bytes(2, 2, 8, "f32", form="ks", offset_policy=1) == \
         3 * 4 ** 8 * 4 + 256 + 512
     assert L.lcsb_required_bytes(4, 2, 4, "f32", form="ks", offset_policy=1) == \
-        3 * 4 ** 8 * 4 + 256 + 512
+        L.lcsb_required_bytes(4, 2, 4, "f32", form="ks") + 512
+    assert L.lcsb_required_bytes(4, 2, 5, "f32", form="two_array", offset_policy=1) == \
+        L.lcsb_required_bytes(4, 2, 5, "f32", form="two_array") + 512
     assert L.lcsb_required_bytes(2, 3, 3, "f64", offset_policy=1) == 4 * 2 ** 9 * 8 + 256 + 512
     assert L.lcsb_required_bytes(2, 2, 8, "f32", form="ks", symmetry=2, offset_policy=1) == 0
     assert L.lcsb_required_bytes(2, 2, 8, "f32", symmetry=1, offset_policy=1) == 0

@@ -421,6 +421,34 @@ def test_offsets_generic_ks_matches_oracle_twin(sigma, d, ell, dtype):
 
 @pytest.mark.gpu
 @pytest.mark.skipif(not has_cuda(), reason="needs a CUDA device")
+@pytest.mark.parametrize("ell,form,dtype,sweeps", [(4, "ks", "f32", (1, 2, 40)),
+                                                   (4, "ks", "f64", (1, 2, 40)),
+                                                   (5, "ks", "f32", (1, 2, 12)),
+                                                   (4, "two_array", "f32", (1, 2, 40))])
+def test_offsets_q4_matches_oracle_twin(ell, form, dtype, sweeps):
+    """offset_policy = 1 on the sigma = 4, d = 2 q4 kernel (complement-folded table, pooled row
+    means of the table two back): KS with per-generation offsets added to the row means
+    (reading R26), two-array with R23's shift; both generations' values and the bound bit-exact
+    against the oracle's twin in fp32 (1e-12 in fp64)."""
+    from oracle import ft_oracle as fo
+    h = L.Lcsb(4, 2, ell, dtype=dtype, form=form, offset_policy=1)
+    assert h.kernel_in_use == "q4"
+    run = fo.Run(4, 2, ell, form, dtype, offsets=True)
+    for n in sweeps:
+        h.sweep(n)
+        run.sweep(n)
+        _cmp(h.table(0), run.values(0), dtype)
+        _cmp(h.table(1), run.values(1), dtype)
+        gb, rb = h.bound(), run.bound()
+        for key in ("R_max", "R_min", "E_at_Rmax", "E_at_Rmin", "bound_at_Rmax", "bound_at_Rmin"):
+            g, r = getattr(gb, key), rb[key]
+            assert (g == r) if dtype == "f32" else abs(g - r) <= 1e-12 * max(1, abs(r)), key
+    assert run.off > 0
+    h.destroy()
+
+
+@pytest.mark.gpu
+@pytest.mark.skipif(not has_cuda(), reason="needs a CUDA device")
 def test_offsets_graph_replay_and_reset():
     """Offsets under CUDA-graph replay (l = 8, 77 + 5 sweeps per call) equal plain launches,
     and a reset restarts from offset 0 (the second run repeats the first bit for bit)."""
