@@ -333,6 +333,7 @@ __global__ void __launch_bounds__(kThreads, GR ? 4 : ((WMODE && sizeof(T) == 8) 
   // h_a == h_b stays 1 + P
   static_assert(!(OFS && (WMODE || SH)), "offsets: unsharded sweeps only");
   [[maybe_unused]] double psh = 0.0, osh = 0.0, omn = INFINITY;
+  [[maybe_unused]] float omn32 = INFINITY;  // fp32 storage: the min of the stored values
   if constexpr (OFS) {
     psh = a.ost->gpost[ta ? 1 : 2];
     osh = a.ost->shift;
@@ -394,25 +395,31 @@ __global__ void __launch_bounds__(kThreads, GR ? 4 : ((WMODE && sizeof(T) == 8) 
         // (rounding is monotone), so the candidates are rounded once each (7 conversions instead
         // of 8 fp64 max chains + 8 conversions) and the maxima taken in fp32 (one FMNMX each; no
         // NaN, no -0); the stored values are unchanged bit for bit
+        // (OFS: x -> round32(x - c) is monotone too, so each candidate gets -c in fp64 first)
         [[maybe_unused]] float fU[2], fS[4], fpu = 0.f, fsame = 0.f;
-        if constexpr (sizeof(T) == 4 && !WMODE && !OFS) {
-          fU[0] = (float)bU[0];
-          fU[1] = (float)bU[1];
+        if constexpr (sizeof(T) == 4 && !WMODE) {
+          auto shc = [osh](double x) {  // OFS: x - c; otherwise x itself (no instruction)
+            if constexpr (OFS) return x + osh;
+            else return x;
+          };
+          fU[0] = (float)shc(bU[0]);
+          fU[1] = (float)shc(bU[1]);
 #pragma unroll
-          for (int hb = 0; hb < 4; ++hb) fS[hb] = (float)bS[hb];
-          fpu = (float)pu;
-          fsame = (float)(1.0 + pu);
+          for (int hb = 0; hb < 4; ++hb) fS[hb] = (float)shc(bS[hb]);
+          fpu = (float)shc(pu);
+          fsame = (float)shc(1.0 + pu);
         }
 #pragma unroll
         for (int ha = 0; ha < 2; ++ha) {
 #pragma unroll
           for (int hb = 0; hb < 4; ++hb) {
             double v;
-            if constexpr (sizeof(T) == 4 && !WMODE && !OFS) {
+            if constexpr (sizeof(T) == 4 && !WMODE) {
               const float v32 = (ha == hb) ? fsame
                                            : (ta ? fmaxf(fU[ha], fS[hb])
                                                  : fmaxf(fmaxf(fU[ha], fS[hb]), fpu));
               v = (double)v32;  // exact; (T)v below gives v32 back
+              if constexpr (OFS) omn32 = fminf(omn32, v32);
             } else if (ha == hb) {  // 1 + max(0, P): P is a mean of non-negative iterates, P >= 0
               v = 1.0 + pu;
             } else if (ta) {
@@ -420,9 +427,9 @@ __global__ void __launch_bounds__(kThreads, GR ? 4 : ((WMODE && sizeof(T) == 8) 
             } else {
               v = dmax(dmax(bU[ha], bS[hb]), pu);  // adv_b, adv_a, P
             }
-            if constexpr (OFS) {  // F - c (exact in fp64: c a small integer), then the rounding
+            if constexpr (OFS && sizeof(T) == 8) {  // F - c (as the oracle: fp64), then the store
               v = v + osh;
-              omn = dmin(omn, (double)(T)v);
+              omn = dmin(omn, v);
             }
             const int hh = ha * 4 + hb;
             if (!WMODE) {
@@ -489,7 +496,7 @@ __global__ void __launch_bounds__(kThreads, GR ? 4 : ((WMODE && sizeof(T) == 8) 
     }
   }
   if (WMODE) block_max2_to(wmax[0], wmax[1], a.red_out);
-  if constexpr (OFS) block_min_to(omn, a.omin);
+  if constexpr (OFS) block_min_to(sizeof(T) == 4 ? (double)omn32 : omn, a.omin);
 }
 
 template <typename T, int M, int S, bool WMODE, bool GR = false, bool SH = false, bool OFS = false>

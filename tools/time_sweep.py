@@ -24,6 +24,7 @@ def main():
     ap.add_argument("--warm", type=int, default=3)
     ap.add_argument("--reps", type=int, default=3)
     ap.add_argument("--tag", default="")
+    ap.add_argument("--offsets", action="store_true", help="offset_policy = 1 (R23 / R26)")
     ap.add_argument("--residual", action="store_true",
                     help="offsets + lcsb_rebase after the warm-up: time the residual sweep (R24)")
     args = ap.parse_args()
@@ -31,7 +32,7 @@ def main():
     from paper_2407_10925_b200 import Lcsb
     from seeded_inputs import splitmix64_indices
     h = Lcsb(args.sigma, args.d, args.ell, dtype=args.dtype, form=args.form,
-             offset_policy=1 if args.residual else 0)
+             offset_policy=1 if (args.residual or args.offsets) else 0)
     h.ready(wait=True)
     h.sweep(args.warm)
     if args.residual:
