@@ -143,9 +143,10 @@ typedef struct {
    *       translation invariance, Lemma 1 (2)), so stored magnitudes stay small and
    *       fp32 storage drifts less.  Values read out (lcsb_table) and the bound are those of v.
    *       Two-array form: binary on the quarter table (l >= 3) or, below that, the generic
-   *       kernel; other sigma (d = 2): the generic kernel.  KS form (any sigma, d; R26): the
-   *       generic kernel, every generation keeps its own o and the table k sweeps back is read
-   *       relative to the newest one's.  The half table and sharding: LCSB_EINVAL. */
+   *       kernel; other sigma (d = 2): the generic kernel (q4 for sigma = 4, l >= 4).  KS form
+   *       (any sigma, d; R26): the generic kernel or q4 (sigma = 4, d = 2); every generation
+   *       keeps its own o and the means over the table k sweeps back get o_{n+1-k} - o_n added.
+   *       The half table and sharding: LCSB_EINVAL. */
   int32_t offset_policy;
 } lcsb_config;
 
