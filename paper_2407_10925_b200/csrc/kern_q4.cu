@@ -331,7 +331,7 @@ __global__ void __launch_bounds__(kThreads, GR ? 4 : ((WMODE && sizeof(T) == 8) 
   // output gets shift = -c before the storage rounding; omn = min of the stored values.  The
   // |N| = 0 option (-o_n in stored terms, R26) never wins against P + gpost[2] >= -o_n, so
   // h_a == h_b stays 1 + P
-  static_assert(!(OFS && (WMODE || SH)), "offsets: unsharded sweeps only");
+  static_assert(!(OFS && WMODE), "offsets: sweeps only");
   [[maybe_unused]] double psh = 0.0, osh = 0.0, omn = INFINITY;
   [[maybe_unused]] float omn32 = INFINITY;  // fp32 storage: the min of the stored values
   if constexpr (OFS) {
@@ -556,8 +556,10 @@ cudaError_t launch_q4_sweep(const Q4Args& a0, int dtype, cudaStream_t s, int sms
     const char* e = getenv("LCSB_Q4_GROWS");
     grows = e ? atoi(e) : 0;
   }
-  if (a.ost) {  // integer offsets: the default pipeline, unsharded (plan_config)
-    if (a.p > 0) return cudaErrorInvalidValue;
+  if (a.ost) {  // integer offsets: the default pipeline (sharded: the shard indexing too)
+    if (a.p > 0)
+      return dtype == LCSB_F32 ? launch_q4_one<float, 2, 1, false, false, true, true>(a, s, sms)
+                               : launch_q4_one<double, 2, 1, false, false, true, true>(a, s, sms);
     return dtype == LCSB_F32 ? launch_q4_one<float, 2, 1, false, false, false, true>(a, s, sms)
                              : launch_q4_one<double, 2, 1, false, false, false, true>(a, s, sms);
   }

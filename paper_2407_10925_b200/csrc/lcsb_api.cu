@@ -270,10 +270,16 @@ static int plan_config(const lcsb_config* c, Plan* p, char* why, size_t whylen) 
     snprintf(why, whylen, "offset_policy must be 0 or 1");
     return LCSB_EINVAL;
   }
-  if (ofs && (sharded || c->symmetry == 1 ||
+  // sharded: the quarter table and sigma = 4, d = 2 (their kernels carry the offsets; the min
+  // crosses the ranks before each sweep's prep), not the half table
+  const bool ofs_shard_ok = (c->sigma == 4 && c->d == 2) ||
+                            (c->sigma == 2 && c->d == 2 && form == LCSB_FORM_TWO_ARRAY &&
+                             (c->symmetry == 2 || c->symmetry == -1));
+  if (ofs && ((sharded && !ofs_shard_ok) || c->symmetry == 1 ||
               (form != LCSB_FORM_TWO_ARRAY && c->symmetry == 2))) {
     snprintf(why, whylen,
-             "integer offsets need no sharding, symmetry -1, 0 or 2 (2: the two-array form)");
+             "integer offsets need symmetry -1, 0 or 2 (2: the two-array form) and, sharded, the "
+             "quarter table or sigma = 4, d = 2");
     return LCSB_EINVAL;
   }
   int sym = c->symmetry;
@@ -563,29 +569,41 @@ static int barrier(lcsb_t* h) {  // process mode: every rank's preceding work is
 // process mode: element-wise max over the ranks of device reduction slots [first, first + n)
 // (slot 1 = R_min is a minimum: the NCCL path reduces it with ncclMin, the hook path by a max of
 // the complemented encoding)
-static int allreduce_slots(lcsb_t* h, int first, int n, unsigned min_mask) {
+// process mode: element-wise max (bit i of min_mask: min) over the ranks of n ordered-encoded
+// device values at d, in place, stream-ordered
+static int allreduce_dev(lcsb_t* h, unsigned long long* d, int n, unsigned min_mask) {
   if (h->mode != MODE_PROCESS) return LCSB_OK;
   cudaStream_t s = (cudaStream_t)h->cfg.stream;
   if (const lcsb_comm_hooks* c = hooks(h)) {
     unsigned long long v[kRedSlots];
-    CU(h, cudaMemcpyAsync(v, h->red + first, n * sizeof(unsigned long long),
-                          cudaMemcpyDeviceToHost, s));
+    if (n > kRedSlots) return set_err(h, LCSB_EINVAL, "allreduce of %d values", n);
+    CU(h, cudaMemcpyAsync(v, d, n * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
     CU(h, cudaStreamSynchronize(s));
     for (int i = 0; i < n; ++i)
-      if ((min_mask >> (first + i)) & 1u) v[i] = ~v[i];
+      if ((min_mask >> i) & 1u) v[i] = ~v[i];
     if (c->allreduce_max_u64(reinterpret_cast<uint64_t*>(v), n, c->ctx) != 0)
       return set_err(h, LCSB_ENCCL, "comm hook allreduce_max_u64 failed");
     for (int i = 0; i < n; ++i)
-      if ((min_mask >> (first + i)) & 1u) v[i] = ~v[i];
-    CU(h, cudaMemcpyAsync(h->red + first, v, n * sizeof(unsigned long long),
-                          cudaMemcpyHostToDevice, s));
+      if ((min_mask >> i) & 1u) v[i] = ~v[i];
+    CU(h, cudaMemcpyAsync(d, v, n * sizeof(unsigned long long), cudaMemcpyHostToDevice, s));
     CU(h, cudaStreamSynchronize(s));
     return LCSB_OK;
   }
   for (int i = 0; i < n; ++i)
-    NC(h, ncclAllReduce(h->red + first + i, h->red + first + i, 1, ncclUint64,
-                        ((min_mask >> (first + i)) & 1u) ? ncclMin : ncclMax, h->comm, s));
+    NC(h, ncclAllReduce(d + i, d + i, 1, ncclUint64, ((min_mask >> i) & 1u) ? ncclMin : ncclMax,
+                        h->comm, s));
   return LCSB_OK;
+}
+
+static int allreduce_slots(lcsb_t* h, int first, int n, unsigned min_mask) {
+  return allreduce_dev(h, h->red + first, n, min_mask >> first);
+}
+
+// integer offsets, sharded process mode: every rank's sweep reduced the min of the outputs it
+// computed into its own mn[cur]; the global min before the prep kernel derives c from it
+static int offsets_global_min(lcsb_t* h) {
+  if (!h->ost || h->mode != MODE_PROCESS) return LCSB_OK;
+  return allreduce_dev(h, &h->ost->mn[h->cur], 1, 1u);
 }
 
 extern "C" void lcsb_destroy(lcsb_t* h) {
@@ -1322,6 +1340,8 @@ static int enqueue_sweeps(lcsb_t* h, int64_t n, cudaStream_t s, int64_t track) {
       Bin2QArgs a;
       fill_bin2q(h, &a, h->cur, out);
       if (h->ost) {  // integer offsets: c = floor(min s) of the table read, then the sweep
+        int rc = offsets_global_min(h);
+        if (rc != LCSB_OK) return rc;
         e = launch_offset_prep(h->ost, h->cur, out, s);
         h->launches += 1;
         a.ost = h->ost;
@@ -1351,6 +1371,18 @@ static int enqueue_sweeps(lcsb_t* h, int64_t n, cudaStream_t s, int64_t track) {
       // row means of v_{n-2} (KS) / of v_{n-1}, the table this sweep reads (two-array)
       const int pin = (h->form == LCSB_FORM_KS) ? (h->pcur + 2) % 3 : h->pcur;
       const int pout = (h->pcur + 1) % 3;  // row means of the table written now
+      if (h->ost) {  // integer offsets (R23; KS: the row means read are of the table two back)
+        int rc = offsets_global_min(h);
+        if (rc != LCSB_OK) return rc;
+        GenSlots gs{};
+        if (h->form == LCSB_FORM_KS) {
+          gs.n = 2;
+          gs.slot[0] = slot_back(h, 0);
+          gs.slot[1] = slot_back(h, 1);  // = out (ring of 2): read before prep overwrites it
+        }
+        e = launch_offset_prep(h->ost, h->cur, out, s, &gs);
+        h->launches += 1;
+      }
       for (int k = h->first; k < h->first + h->nown && e == cudaSuccess; ++k) {
         Q4Args a;
         memset(&a, 0, sizeof a);
@@ -1366,19 +1398,11 @@ static int enqueue_sweeps(lcsb_t* h, int64_t n, cudaStream_t s, int64_t track) {
           a.dst_sh[j] = h->tabs[j][out];
           a.pout_sh[j] = h->pools[j][pout];
         }
-        if (h->ost) {  // integer offsets (R23; KS: the row means read are of the table two back)
-          GenSlots gs{};
-          if (h->form == LCSB_FORM_KS) {
-            gs.n = 2;
-            gs.slot[0] = slot_back(h, 0);
-            gs.slot[1] = slot_back(h, 1);  // = out (ring of 2): read before prep overwrites it
-          }
-          e = launch_offset_prep(h->ost, h->cur, out, s, &gs);
-          h->launches += 1;
+        if (h->ost) {  // every shard's launch reduces into the same min (virtual shards)
           a.ost = h->ost;
           a.omin = &h->ost->mn[out];
         }
-        if (e == cudaSuccess) e = launch_q4_sweep(a, h->cfg.dtype, s, h->sms);
+        e = launch_q4_sweep(a, h->cfg.dtype, s, h->sms);
         h->launches += 1;
       }
       h->pcur = (h->pcur + 1) % 3;

@@ -93,12 +93,14 @@ def comm_hooks(group=None) -> LcsbCommHooks:
 
 def create_sharded(ell: int, dtype: str = "f32", rmode: str = "max", group=None,
                    stream=None, transport: str = "nccl", sigma: int = 2,
-                   form: str = "auto", symmetry: int = -1, block_log4: int = 0) -> Lcsb:
+                   form: str = "auto", symmetry: int = -1, block_log4: int = 0,
+                   offset_policy: int = 0) -> Lcsb:
     """Collective: every rank of the (torch) process group gets one shard of the d = 2 table of
     length-ell strings: sigma = 2 -- the symmetry-folded quarter table for l >= 12 (DESIGN.md
     §9c; the same kernels as one GPU) or the complement-folded half table (§9; symmetry = 1,
     and below l = 12); sigma = 4 -- the complement-folded q4 table, KS or two-array form
-    (§9b)."""
+    (§9b).  offset_policy = 1: integer offsets (readings R23, R26; quarter table and sigma = 4;
+    the min crosses the ranks before every sweep)."""
     import torch.distributed as dist
     if sigma not in (2, 4):
         raise ValueError("sharded tables exist for sigma = 2 and sigma = 4 (d = 2)")
@@ -109,10 +111,11 @@ def create_sharded(ell: int, dtype: str = "f32", rmode: str = "max", group=None,
     if transport == "host":
         return Lcsb(sigma, 2, ell, dtype=dtype, form=form, rmode=rmode, shards=ws,
                     shard=rank, comm_hooks=comm_hooks(group), stream=stream,
-                    torch_allocator=False, symmetry=symmetry, block_log4=block_log4)
+                    torch_allocator=False, symmetry=symmetry, block_log4=block_log4,
+                    offset_policy=offset_policy)
     if transport != "nccl":
         raise ValueError("transport must be 'nccl' or 'host'")
     nid = broadcast_id(lcsb_nccl_unique_id() if rank == 0 else None, group)
     return Lcsb(sigma, 2, ell, dtype=dtype, form=form, rmode=rmode, shards=ws, shard=rank,
                 nccl_id=nid, stream=stream, torch_allocator=False, symmetry=symmetry,
-                block_log4=block_log4)
+                block_log4=block_log4, offset_policy=offset_policy)

@@ -85,7 +85,13 @@ def test_required_bytes_and_validation():
     assert L.lcsb_required_bytes(2, 3, 3, "f64", offset_policy=1) == 4 * 2 ** 9 * 8 + 256 + 512
     assert L.lcsb_required_bytes(2, 2, 8, "f32", form="ks", symmetry=2, offset_policy=1) == 0
     assert L.lcsb_required_bytes(2, 2, 8, "f32", symmetry=1, offset_policy=1) == 0
-    assert L.lcsb_required_bytes(2, 2, 12, "f32", shards=2, offset_policy=1) == 0
+    # sharded: the quarter table and sigma = 4 carry offsets (the min crosses the ranks), the
+    # half table does not
+    assert L.lcsb_required_bytes(2, 2, 12, "f32", shards=2, symmetry=1, offset_policy=1) == 0
+    assert L.lcsb_required_bytes(2, 2, 12, "f32", shards=2, symmetry=2, offset_policy=1) == \
+        L.lcsb_required_bytes(2, 2, 12, "f32", shards=2, symmetry=2) + 512
+    assert L.lcsb_required_bytes(4, 2, 5, "f32", form="ks", shards=2, offset_policy=1) == \
+        L.lcsb_required_bytes(4, 2, 5, "f32", form="ks", shards=2) + 512
     assert L.lcsb_required_bytes(2, 2, 8, "f32", offset_policy=2) == 0
     assert L.lcsb_required_bytes(3, 2, 3, "f32", form="two_array", offset_policy=1) == \
         2 * 3 ** 6 * 4 + 256 + 512

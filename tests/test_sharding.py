@@ -713,3 +713,96 @@ def _psi_tile(ell, M, t):
     ps = ((v & 0xAAAAAAAAAAAAAAAA) >> 1) | ((v & 0x5555555555555555) << 1)
     p0 = ps & ~((1 << (2 * M)) - 1)
     return (p0 - q1) >> (2 * M)
+
+
+# ------------------------------------------------- integer offsets on the sharded layouts (R23/R26)
+
+@pytest.mark.gpu
+@pytest.mark.skipif(not has_cuda(), reason="needs a CUDA device")
+@pytest.mark.parametrize("sigma,ell,shards,dtype,form,K", [
+    (2, 10, 2, "f32", "two_array", 5), (2, 12, 4, "f64", "two_array", 6),
+    (2, 13, 8, "f32", "two_array", 7), (4, 5, 2, "f32", "ks", 0), (4, 5, 8, "f64", "ks", 0),
+    (4, 6, 4, "f32", "two_array", 0)])
+def test_offsets_virtual_shards_bitwise_equal_unsharded(sigma, ell, shards, dtype, form, K):
+    """offset_policy = 1 on P virtual shards (the quarter table, sigma = 4): every shard's launch
+    reduces its outputs' min into the one offset state, so the offsets, both generations' values
+    and the bound equal the unsharded offset run bit for bit (and the oracle's twin at small l)."""
+    import torch
+    from paper_2407_10925_b200 import Lcsb
+    from oracle import ft_oracle as fo
+    kw = dict(symmetry=2, block_log4=K) if sigma == 2 else {}
+    a = Lcsb(sigma, 2, ell, dtype=dtype, form=form, offset_policy=1, **kw)
+    b = Lcsb(sigma, 2, ell, dtype=dtype, form=form, offset_policy=1, shards=shards,
+             virtual_shards=True, **kw)
+    assert b.num_shards == shards and a.kernel_in_use == b.kernel_in_use
+    a.ready(wait=True)
+    for k in (1, 1, 1, 27):
+        a.sweep(k)
+        b.sweep(k)
+        assert np.array_equal(a.table(0), b.table(0))
+        assert np.array_equal(a.table(1), b.table(1))
+        ba, bb = a.bound(), b.bound()
+        assert (ba.R_max, ba.R_min, ba.E_at_Rmax, ba.E_at_Rmin) == \
+               (bb.R_max, bb.R_min, bb.E_at_Rmax, bb.E_at_Rmin)
+    if sigma ** (2 * ell) <= 1 << 20:
+        run = fo.Run(sigma, 2, ell, form, dtype, offsets=True)
+        run.sweep(30)
+        assert run.off > 0
+        tab = b.table(0)
+        if dtype == "f32":
+            assert np.array_equal(tab, run.values(0))
+        else:
+            np.testing.assert_allclose(tab, run.values(0), rtol=1e-12)
+    a.destroy()
+    b.destroy()
+    torch.cuda.empty_cache()
+
+
+def _pm_offsets_worker(rank, world, port, out_dir, sigma, ell, dtype, form, K):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+    from paper_2407_10925_b200 import Lcsb
+    from paper_2407_10925_b200.dist import create_sharded
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    kw = dict(symmetry=2, block_log4=K) if sigma == 2 else {}
+    h = create_sharded(ell, dtype=dtype, transport="host", sigma=sigma, form=form,
+                       offset_policy=1, **kw)
+    out = {}
+    for n in (1, 2, 27):
+        h.sweep(n)
+        b = h.bound()
+        if rank == 0:
+            out[n] = (h.table(0), h.table(1), b)
+    dist.barrier()
+    h.destroy()
+    if rank == 0:
+        ok = []
+        ref = Lcsb(sigma, 2, ell, dtype=dtype, form=form, offset_policy=1, **kw)
+        for n in (1, 2, 27):
+            ref.sweep(n)
+            rb = ref.bound()
+            t0, t1, b = out[n]
+            ok += [np.array_equal(t0, ref.table(0)), np.array_equal(t1, ref.table(1)),
+                   (b.R_max, b.R_min, b.E_at_Rmax, b.E_at_Rmin) ==
+                   (rb.R_max, rb.R_min, rb.E_at_Rmax, rb.E_at_Rmin)]
+        ref.destroy()
+        np.save(os.path.join(out_dir, "pmo.npy"), np.array(ok))
+    dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+@pytest.mark.skipif(not has_cuda(), reason="needs a CUDA device")
+@pytest.mark.parametrize("world,sigma,ell,dtype,form,K", [(2, 2, 10, "f32", "two_array", 5),
+                                                          (4, 4, 5, "f32", "ks", 0)])
+def test_offsets_process_mode_multi_rank_on_one_gpu(tmp_path, world, sigma, ell, dtype, form, K):
+    """Integer offsets over 2 and 4 PROCESSES sharing cuda:0 (host comm hooks): each rank reduces
+    the min of the outputs it computed, the ranks all-reduce it before every sweep's prep, and
+    tables and bounds equal the unsharded offset run bit for bit."""
+    import torch.multiprocessing as mp
+    mp.spawn(_pm_offsets_worker, args=(world, _free_port(), str(tmp_path), sigma, ell, dtype,
+                                       form, K), nprocs=world, join=True)
+    assert np.load(tmp_path / "pmo.npy").all()
