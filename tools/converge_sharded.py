@@ -38,6 +38,8 @@ def main():
     ap.add_argument("--every", type=int, default=20)
     ap.add_argument("--max-sweeps", type=int, default=600)
     ap.add_argument("--transport", default="nccl", choices=["nccl", "host"])
+    ap.add_argument("--offsets", type=int, default=0,
+                    help="offset_policy (1: integer offsets, readings R23 / R26; fp32 drift 4-30x lower)")
     args = ap.parse_args()
     import torch
     import torch.distributed as dist
@@ -49,7 +51,8 @@ def main():
         dist.init_process_group("gloo")
     else:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    h = create_sharded(args.ell, dtype=args.dtype, transport=args.transport)
+    h = create_sharded(args.ell, dtype=args.dtype, transport=args.transport,
+                       offset_policy=args.offsets)
     t0 = time.perf_counter()
     last = -1.0
     while h.sweeps_done < args.max_sweeps:
