@@ -18,6 +18,8 @@ pytestmark = [pytest.mark.gpu,
     (3, 3, 3, "f64", {}),                                   # small, pooled KS means
     (3, 2, 3, "f32", {"form": "two_array", "offset_policy": 1}),  # generic + offsets
     (2, 2, 9, "f32", {"offset_policy": 1}),                 # quarter table + offsets
+    (4, 2, 5, "f32", {"form": "ks", "offset_policy": 1}),   # q4 + KS per-generation offsets
+    (2, 3, 3, "f64", {"offset_policy": 1}),                 # generic KS (d = 3) + offsets
 ])
 def test_resume_equals_uninterrupted(tmp_path, sigma, d, ell, dtype, kw):
     from paper_2407_10925_b200 import Lcsb
