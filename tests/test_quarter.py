@@ -397,11 +397,14 @@ def test_offsets_generic_two_array_matches_oracle_twin(sigma, ell, dtype):
 @pytest.mark.skipif(not has_cuda(), reason="needs a CUDA device")
 @pytest.mark.parametrize("sigma,d,ell,dtype", [(2, 2, 3, "f32"), (2, 2, 6, "f64"),
                                                (4, 2, 2, "f32"), (3, 2, 3, "f32"),
-                                               (2, 3, 2, "f32"), (2, 3, 3, "f64")])
+                                               (2, 3, 2, "f32"), (2, 3, 3, "f64"),
+                                               (2, 3, 1, "f32"), (2, 4, 1, "f64"),
+                                               (2, 5, 1, "f32"), (2, 4, 3, "f32")])
 def test_offsets_generic_ks_matches_oracle_twin(sigma, d, ell, dtype):
     """offset_policy = 1 in the KS form (reading R26: per-generation offsets, the table k back
     read relative to the newest one's) on the generic kernel: every generation's values and the
-    two-pass bound bit-exact against the oracle's KS offset twin in fp32 (1e-12 in fp64)."""
+    two-pass bound bit-exact against the oracle's KS offset twin in fp32 (1e-12 in fp64).
+    (2,3,1), (2,4,1), (2,5,1): the |N| = 0 option is -o_n on the device too (R26)."""
     from oracle import ft_oracle as fo
     h = L.Lcsb(sigma, d, ell, dtype=dtype, form="ks", offset_policy=1)
     assert h.kernel_in_use == "generic"
