@@ -75,7 +75,11 @@ __device__ __forceinline__ uint32_t pairswap32(uint32_t v) {
 // cand itself: the compare is dropped, the value is unchanged.
 __device__ __forceinline__ double q0_val(double v0, double v1, double v2, double v3) {
   const double r = ((v0 + v1) + v2) + v3;
+#ifdef LCSB_Q0_FMA  // A/B: 0.25 r is exact, so one fused op rounds exactly as DMUL + DADD do
+  return __fma_rn(0.25, r, 1.0);
+#else
   return 1.0 + 0.25 * r;
+#endif
 }
 
 constexpr int kThreads = 256;
