@@ -305,9 +305,9 @@ struct Q4Args {
   void* dst_sh[kMaxShards];
   double* pout_sh[kMaxShards];
   const void* g1_sh[kMaxShards];
-  // integer offsets (sweep, unsharded; readings R23, R26): P gets gpost[2] (KS: of the table two
-  // back), outputs get shift before the storage rounding, the min of the stored values goes to
-  // omin.  NULL = off
+  // integer offsets (sweep; readings R23, R26): P gets gpost[2] (KS: of the table two back),
+  // outputs get shift before the storage rounding, the min of the stored values this launch
+  // computes goes to omin (sharded: every shard's launch into the same min).  NULL = off
   const OffState* ost;
   unsigned long long* omin;
 };
